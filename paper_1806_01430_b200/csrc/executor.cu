@@ -1,0 +1,731 @@
+// executor.cu -- contexts, device slots, plan execution, timing, and the C ABI of include/mmx.h.
+//
+// One measurement (mmx_measure) is the in-process replacement of ToolchainBackend::measure
+// (/root/reference/proj/src/evaluator.cpp:61-142): plan the genome, run the plan `repetitions`
+// times, take the median (evaluator.cpp:133-136), map failures to outcomes:
+//     infeasible genome       -> CompileError, time 0          (evaluator.cpp:87-91)
+//     run over timeout_s      -> Timeout, time = budget        (evaluator.cpp:103-108)
+//     CUDA failure / t <= 0   -> RuntimeError                  (evaluator.cpp:109-113,125-129)
+// The timed region of a run starts with every array invalid on both sides (a fresh process, as
+// in the reference) and ends when the checksum is on the host; allocation happens before it
+// (the program's arrays are static storage, matmul.c:5).
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "host_loops.hpp"
+#include "kernels.cuh"
+#include "mmx.h"
+#include "plan.hpp"
+
+namespace mmx {
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Train {  // a captured train of K inner-loop launches + the counter bump
+  cudaGraphExec_t exec = nullptr;
+  int k = 0;
+};
+
+struct Slot {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
+  void* d_arr[MMX_NUM_ARRAYS] = {};
+  void* h_arr[MMX_NUM_ARRAYS] = {};  // pinned, allocated on first need
+  void* d_sum = nullptr;
+  void* h_sum = nullptr;  // pinned, 16 bytes
+  int* d_iter = nullptr;
+  void* d_scrub = nullptr;
+  std::size_t scrub_bytes = 0;
+  bool host_valid[MMX_NUM_ARRAYS] = {};
+  bool dev_valid[MMX_NUM_ARRAYS] = {};
+  bool host_diag_only = false;  // host c holds only its diagonal
+  std::map<int, Train> trains;  // by gene
+  mmx_run_stats stats{};
+  std::mutex mu;
+};
+
+}  // namespace
+}  // namespace mmx
+
+struct mmx_ctx {
+  mmx_config cfg{};
+  std::vector<int> devices;
+  std::vector<std::unique_ptr<mmx::Slot>> slots;
+  mutable std::mutex err_mu;
+  std::string error;
+  mutable std::string error_snapshot;
+
+  void set_error(const std::string& e) {
+    std::lock_guard<std::mutex> g(err_mu);
+    error = e;
+  }
+};
+
+namespace mmx {
+namespace {
+
+using Seconds = std::chrono::duration<double>;
+
+inline double since(Clock::time_point t0) { return Seconds(Clock::now() - t0).count(); }
+
+#define MMX_CUDA(ctx, call)                                                                      \
+  do {                                                                                           \
+    cudaError_t e__ = (call);                                                                    \
+    if (e__ != cudaSuccess) {                                                                    \
+      (ctx)->set_error(std::string(#call) + ": " + cudaGetErrorString(e__));                     \
+      return e__ == cudaErrorMemoryAllocation ? MMX_E_NOMEM : MMX_E_CUDA;                        \
+    }                                                                                            \
+  } while (0)
+
+std::size_t matrix_bytes(const mmx_ctx* ctx) {
+  return static_cast<std::size_t>(ctx->cfg.n) * ctx->cfg.n * elem_size(ctx->cfg.dtype);
+}
+
+int ensure_host(mmx_ctx* ctx, Slot& s, int array) {
+  if (s.h_arr[array] != nullptr) return MMX_OK;
+  MMX_CUDA(ctx, cudaHostAlloc(&s.h_arr[array], matrix_bytes(ctx), cudaHostAllocDefault));
+  return MMX_OK;
+}
+
+// ---- kernel dispatch by gene --------------------------------------------------------------------
+
+template <typename T>
+cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter) {
+  const int n = ctx->cfg.n;
+  const bool strict = ctx->cfg.numerics == MMX_NUMERICS_STRICT;
+  T* a = static_cast<T*>(s.d_arr[MMX_ARRAY_A]);
+  T* b = static_cast<T*>(s.d_arr[MMX_ARRAY_B]);
+  T* c = static_cast<T*>(s.d_arr[MMX_ARRAY_C]);
+  T* bt = static_cast<T*>(s.d_arr[MMX_ARRAY_BT]);
+  switch (gene) {
+    case 0: return launch_fill2d<T>(FILL_INIT_A, a, n, s.stream);
+    case 1: return launch_fill_row<T>(FILL_INIT_A, a, n, iter, s.stream);
+    case 2: return launch_fill2d<T>(FILL_INIT_B, b, n, s.stream);
+    case 3: return launch_fill_row<T>(FILL_INIT_B, b, n, iter, s.stream);
+    case 4: return launch_fill2d<T>(FILL_ZERO, c, n, s.stream);
+    case 5: return launch_fill_row<T>(FILL_ZERO, c, n, iter, s.stream);
+    case 6: return launch_transpose<T>(bt, b, n, s.stream);
+    case 7: return launch_transpose_row<T>(bt, b, n, iter, s.stream);
+    case 8: {
+      int variant = ctx->cfg.matmul_variant;
+      if (variant == 0) variant = 2;  // auto: tensor (DMMA) where it applies
+      return launch_matmul<T>(c, a, bt, n, 0, n, strict, variant, s.stream);
+    }
+    case 9: return launch_gemv_row<T>(c, a, bt, n, iter, strict, s.stream);
+    case 10: return launch_dot<T>(c, a, bt, n, iter, strict, s.stream);
+    case 11: return launch_trace<T>(static_cast<T*>(s.d_sum), c, n, strict, s.stream);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+cudaError_t launch_gene_any(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter) {
+  return ctx->cfg.dtype == MMX_F64 ? launch_gene<double>(ctx, s, gene, iter) : launch_gene<float>(ctx, s, gene, iter);
+}
+
+// gene that serves `nest` in `mode`
+int gene_of(int nest, int mode) { return kNests[nest].first_gene + (mode - MMX_MODE_GPU_NEST); }
+
+constexpr int kTrainLength = 512;
+
+// Capture (once per slot and gene) a graph of k launches of an inner-loop gene whose iteration
+// index is `*d_iter + node`, followed by `*d_iter += k`.  This is the genome's "compile step":
+// it runs before the timed region.
+cudaError_t prepare_train(mmx_ctx* ctx, Slot& s, int gene, long long total) {
+  if (!ctx->cfg.launch_batching || total < 64) return cudaSuccess;
+  const int k = static_cast<int>(std::min<long long>(total, kTrainLength));
+  Train& tr = s.trains[gene];
+  if (tr.exec != nullptr && tr.k == k) return cudaSuccess;
+  if (tr.exec) cudaGraphExecDestroy(tr.exec);
+  tr.exec = nullptr;
+  tr.k = 0;
+  cudaGraph_t graph = nullptr;
+  cudaError_t e = cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) return e;
+  for (int q = 0; q < k && e == cudaSuccess; ++q) e = launch_gene_any(ctx, s, gene, IterRef{s.d_iter, q});
+  if (e == cudaSuccess) e = launch_advance(s.d_iter, k, s.stream);
+  const cudaError_t e2 = cudaStreamEndCapture(s.stream, &graph);
+  if (e == cudaSuccess) e = e2;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&tr.exec, graph, 0);
+  if (graph) cudaGraphDestroy(graph);
+  if (e == cudaSuccess) tr.k = k;
+  return e;
+}
+
+// Submit `total` launches of an inner-loop gene (iterations 0..total-1): whole trains as graph
+// launches when one was prepared, the remainder (or everything) as plain stream launches.
+// Returns cudaSuccess, an error, or sets *timed_out.
+cudaError_t run_train(mmx_ctx* ctx, Slot& s, int gene, long long total, const Deadline& dl, bool* timed_out,
+                      std::uint64_t* graph_launches) {
+  cudaError_t e = cudaSuccess;
+  long long done = 0;
+  auto it_train = s.trains.find(gene);
+  if (ctx->cfg.launch_batching && it_train != s.trains.end() && it_train->second.exec != nullptr &&
+      it_train->second.k <= total) {
+    const Train& tr = it_train->second;
+    if ((e = cudaMemsetAsync(s.d_iter, 0, sizeof(int), s.stream)) != cudaSuccess) return e;
+    const long long trains = total / tr.k;
+    for (long long t = 0; t < trains; ++t) {
+      if ((e = cudaGraphLaunch(tr.exec, s.stream)) != cudaSuccess) return e;
+      ++*graph_launches;
+      done += tr.k;
+      // keep the queue shallow enough that a timeout is noticed within a few trains
+      if ((t & 7) == 7) {
+        if ((e = cudaStreamSynchronize(s.stream)) != cudaSuccess) return e;
+        if (dl.expired()) {
+          *timed_out = true;
+          return cudaSuccess;
+        }
+      }
+    }
+  }
+  for (long long it = done; it < total; ++it) {
+    if ((e = launch_gene_any(ctx, s, gene, IterRef{nullptr, static_cast<int>(it)})) != cudaSuccess) return e;
+    if (((it - done) & 1023) == 1023) {
+      if ((e = cudaStreamSynchronize(s.stream)) != cudaSuccess) return e;
+      if (dl.expired()) {
+        *timed_out = true;
+        return cudaSuccess;
+      }
+    }
+  }
+  return cudaSuccess;
+}
+
+template <typename T>
+bool run_host_nest(const mmx_ctx* ctx, Slot& s, int nest, const Deadline& dl, double* checksum) {
+  const int n = ctx->cfg.n, th = ctx->cfg.host_threads;
+  T* a = static_cast<T*>(s.h_arr[MMX_ARRAY_A]);
+  T* b = static_cast<T*>(s.h_arr[MMX_ARRAY_B]);
+  T* c = static_cast<T*>(s.h_arr[MMX_ARRAY_C]);
+  T* bt = static_cast<T*>(s.h_arr[MMX_ARRAY_BT]);
+  switch (nest) {
+    case MMX_NEST_INIT_A: return host_init_a<T>(a, n, th, dl);
+    case MMX_NEST_INIT_B: return host_init_b<T>(b, n, th, dl);
+    case MMX_NEST_ZERO_C: return host_zero_c<T>(c, n, th, dl);
+    case MMX_NEST_TRANSPOSE: return host_transpose<T>(bt, b, n, th, dl);
+    case MMX_NEST_MATMUL: return host_matmul<T>(c, a, bt, n, th, dl);
+    case MMX_NEST_TRACE: *checksum = host_trace<T>(c, n); return true;
+    default: return false;
+  }
+}
+
+struct RunResult {
+  int status = MMX_RUNTIME_ERROR;
+  double time_s = 0.0;
+};
+
+// arrays a nest writes (whole array) -- for the validity bookkeeping mmx_fetch_array relies on
+int written_array(int nest) {
+  switch (nest) {
+    case MMX_NEST_INIT_A: return MMX_ARRAY_A;
+    case MMX_NEST_INIT_B: return MMX_ARRAY_B;
+    case MMX_NEST_ZERO_C: return MMX_ARRAY_C;
+    case MMX_NEST_TRANSPOSE: return MMX_ARRAY_BT;
+    case MMX_NEST_MATMUL: return MMX_ARRAY_C;
+    default: return -1;
+  }
+}
+
+// bit q set: the nest reads or writes array q
+unsigned nest_arrays(int nest) {
+  switch (nest) {
+    case MMX_NEST_INIT_A: return 1u << MMX_ARRAY_A;
+    case MMX_NEST_INIT_B: return 1u << MMX_ARRAY_B;
+    case MMX_NEST_ZERO_C: return 1u << MMX_ARRAY_C;
+    case MMX_NEST_TRANSPOSE: return 1u << MMX_ARRAY_B | 1u << MMX_ARRAY_BT;
+    case MMX_NEST_MATMUL: return 1u << MMX_ARRAY_A | 1u << MMX_ARRAY_BT | 1u << MMX_ARRAY_C;
+    case MMX_NEST_TRACE: return 1u << MMX_ARRAY_C;
+    default: return 0;
+  }
+}
+
+// One benchmark run of a feasible plan on a prepared slot.
+RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan) {
+  RunResult rr;
+  const std::size_t mbytes = matrix_bytes(ctx);
+  const std::size_t esz = elem_size(ctx->cfg.dtype);
+  const std::size_t n = static_cast<std::size_t>(ctx->cfg.n);
+  const double budget = ctx->cfg.timeout_s;
+  for (int q = 0; q < MMX_NUM_ARRAYS; ++q) s.host_valid[q] = s.dev_valid[q] = false;
+  s.host_diag_only = false;
+  s.stats.host_s = 0.0;
+  s.stats.graph_launches = 0;
+  for (double& x : s.stats.nest_s) x = 0.0;
+  double checksum = 0.0;
+  bool any_gpu = false, timed_out = false, sum_on_device = false;
+  cudaError_t e = cudaSuccess;
+
+  const Clock::time_point t0 = Clock::now();
+  const Deadline dl{t0 + std::chrono::duration_cast<Clock::duration>(Seconds(budget))};
+  e = cudaEventRecord(s.ev_begin, s.stream);
+
+  for (int si = 0; si < plan.num_steps && e == cudaSuccess && !timed_out; ++si) {
+    const mmx_plan_step& st = plan.steps[si];
+    const Clock::time_point ts = Clock::now();
+    switch (st.kind) {
+      case MMX_STEP_H2D:
+        e = cudaMemcpyAsync(s.d_arr[st.array], s.h_arr[st.array], mbytes, cudaMemcpyHostToDevice, s.stream);
+        s.dev_valid[st.array] = true;
+        any_gpu = true;
+        break;
+      case MMX_STEP_D2H:
+        e = cudaMemcpyAsync(s.h_arr[st.array], s.d_arr[st.array], mbytes, cudaMemcpyDeviceToHost, s.stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s.stream);  // the host consumes it next
+        s.host_valid[st.array] = true;
+        any_gpu = true;
+        break;
+      case MMX_STEP_D2H_DIAG:
+        e = cudaMemcpy2DAsync(s.h_arr[st.array], (n + 1) * esz, s.d_arr[st.array], (n + 1) * esz, esz, n,
+                              cudaMemcpyDeviceToHost, s.stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s.stream);
+        s.host_diag_only = true;
+        any_gpu = true;
+        break;
+      case MMX_STEP_H2D_DIAG:
+        e = cudaMemcpy2DAsync(s.d_arr[st.array], (n + 1) * esz, s.h_arr[st.array], (n + 1) * esz, esz, n,
+                              cudaMemcpyHostToDevice, s.stream);
+        any_gpu = true;
+        break;
+      case MMX_STEP_CPU: {
+        const bool ok = ctx->cfg.dtype == MMX_F64 ? run_host_nest<double>(ctx, s, st.nest, dl, &checksum)
+                                                  : run_host_nest<float>(ctx, s, st.nest, dl, &checksum);
+        if (!ok) timed_out = true;
+        const int w = written_array(st.nest);
+        if (w >= 0) {
+          s.host_valid[w] = true;
+          s.dev_valid[w] = false;
+          if (w == MMX_ARRAY_C) s.host_diag_only = false;
+        }
+        s.stats.host_s += since(ts);
+        break;
+      }
+      case MMX_STEP_GPU: {
+        any_gpu = true;
+        const int gene = gene_of(st.nest, st.mode);
+        if (st.mode == MMX_MODE_GPU_NEST) {
+          e = launch_gene_any(ctx, s, gene, IterRef{nullptr, 0});
+        } else {
+          e = run_train(ctx, s, gene, static_cast<long long>(st.launches), dl, &timed_out, &s.stats.graph_launches);
+        }
+        const int w = written_array(st.nest);
+        if (w >= 0) {
+          s.dev_valid[w] = true;
+          s.host_valid[w] = false;
+        }
+        if (st.nest == MMX_NEST_TRACE) sum_on_device = true;
+        break;
+      }
+      case MMX_STEP_D2H_SUM:
+        e = cudaMemcpyAsync(s.h_sum, s.d_sum, esz, cudaMemcpyDeviceToHost, s.stream);
+        break;
+      default: e = cudaErrorInvalidValue; break;
+    }
+    if (st.nest >= 0) s.stats.nest_s[st.nest] += since(ts);
+    if (!timed_out && dl.expired()) timed_out = true;
+  }
+
+  if (e == cudaSuccess) e = cudaEventRecord(s.ev_end, s.stream);
+  cudaError_t esync = cudaStreamSynchronize(s.stream);  // always drain, also after a timeout
+  if (e == cudaSuccess) e = esync;
+  const double wall = since(t0);
+  if (e != cudaSuccess) {
+    ctx->set_error(std::string("run failed: ") + cudaGetErrorString(e));
+    cudaGetLastError();
+    rr.status = MMX_RUNTIME_ERROR;
+    return rr;
+  }
+  if (timed_out || wall > budget) {
+    rr.status = MMX_TIMEOUT;
+    rr.time_s = budget;
+    return rr;
+  }
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, s.ev_begin, s.ev_end);
+  s.stats.gpu_ms = ms;
+  if (sum_on_device)
+    checksum = ctx->cfg.dtype == MMX_F64 ? *static_cast<double*>(s.h_sum) : static_cast<double>(*static_cast<float*>(s.h_sum));
+  s.stats.checksum = checksum;
+  // An individual with device work is timed by its CUDA events (begin recorded on an idle stream
+  // before the first step, end after the last: host-side nests in between are inside the bracket);
+  // an all-CPU individual has no device timeline and is timed by the host clock.
+  rr.time_s = any_gpu ? static_cast<double>(ms) * 1e-3 : wall;
+  rr.status = rr.time_s > 0.0 ? MMX_MEASURED : MMX_RUNTIME_ERROR;
+  return rr;
+}
+
+int measure_on_slot(mmx_ctx* ctx, int slot, const std::uint8_t* bits, std::size_t gene_len, mmx_outcome* out) {
+  if (ctx == nullptr || bits == nullptr || out == nullptr) return MMX_E_INVALID;
+  if (slot < 0 || slot >= static_cast<int>(ctx->slots.size())) {
+    ctx->set_error("slot out of range");
+    return MMX_E_INVALID;
+  }
+  if (gene_len != MMX_GENE_LENGTH) {
+    ctx->set_error("genome length " + std::to_string(gene_len) + " does not match candidate count 12");
+    return MMX_E_LENGTH;
+  }
+  const Clock::time_point t0 = Clock::now();
+  mmx_plan_info plan;
+  int rc = build_plan(bits, gene_len, ctx->cfg.n, ctx->cfg.dtype, &plan);
+  if (rc != MMX_OK) return rc;
+  out->status = MMX_RUNTIME_ERROR;
+  out->time_s = 0.0;
+  out->wall_cost_s = 0.0;
+  if (!plan.feasible) {
+    out->status = MMX_COMPILE_ERROR;
+    out->wall_cost_s = since(t0);
+    return MMX_OK;
+  }
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> guard(s.mu);
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  // allocation is outside the timed region: host mirrors for every array a step touches on the host
+  for (int si = 0; si < plan.num_steps; ++si) {
+    const mmx_plan_step& st = plan.steps[si];
+    if (st.kind == MMX_STEP_CPU) {
+      for (int q = 0; q < MMX_NUM_ARRAYS; ++q)
+        if ((nest_arrays(st.nest) >> q & 1) && (rc = ensure_host(ctx, s, q)) != MMX_OK) return rc;
+    } else if (st.array >= 0) {
+      if ((rc = ensure_host(ctx, s, st.array)) != MMX_OK) return rc;
+    } else if (st.kind == MMX_STEP_GPU && st.mode != MMX_MODE_GPU_NEST) {
+      MMX_CUDA(ctx, prepare_train(ctx, s, gene_of(st.nest, st.mode), static_cast<long long>(st.launches)));
+    }
+  }
+  s.stats.h2d_bytes = plan.h2d_bytes;
+  s.stats.d2h_bytes = plan.d2h_bytes;
+  s.stats.kernel_launches = plan.kernel_launches;
+
+  for (int w = 0; w < ctx->cfg.warmup; ++w) {
+    const RunResult r = run_plan_once(ctx, s, plan);
+    if (r.status != MMX_MEASURED) break;  // the timed loop below reports it
+  }
+  const int reps = std::max(1, ctx->cfg.repetitions);
+  std::vector<double> times;
+  for (int r = 0; r < reps; ++r) {
+    const RunResult rr = run_plan_once(ctx, s, plan);
+    if (rr.status != MMX_MEASURED) {
+      out->status = rr.status;
+      out->time_s = rr.status == MMX_TIMEOUT ? rr.time_s : 0.0;
+      out->wall_cost_s = since(t0);
+      return MMX_OK;
+    }
+    times.push_back(rr.time_s);
+  }
+  std::sort(times.begin(), times.end());
+  const std::size_t m = times.size();
+  out->time_s = m % 2 == 1 ? times[m / 2] : 0.5 * (times[m / 2 - 1] + times[m / 2]);
+  out->status = MMX_MEASURED;
+  out->wall_cost_s = since(t0);
+  return MMX_OK;
+}
+
+void destroy_slot(Slot& s) {
+  cudaSetDevice(s.device);
+  for (auto& kv : s.trains)
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
+  for (int q = 0; q < MMX_NUM_ARRAYS; ++q) {
+    if (s.d_arr[q]) cudaFree(s.d_arr[q]);
+    if (s.h_arr[q]) cudaFreeHost(s.h_arr[q]);
+  }
+  if (s.d_sum) cudaFree(s.d_sum);
+  if (s.h_sum) cudaFreeHost(s.h_sum);
+  if (s.d_iter) cudaFree(s.d_iter);
+  if (s.d_scrub) cudaFree(s.d_scrub);
+  if (s.ev_begin) cudaEventDestroy(s.ev_begin);
+  if (s.ev_end) cudaEventDestroy(s.ev_end);
+  if (s.stream) cudaStreamDestroy(s.stream);
+}
+
+}  // namespace
+}  // namespace mmx
+
+// ================================================================================================
+// C ABI
+// ================================================================================================
+using namespace mmx;
+
+extern "C" {
+
+MMX_API int mmx_loop_catalogue(mmx_loop_info* rows, size_t cap) {
+  for (size_t k = 0; k < cap && k < MMX_GENE_LENGTH; ++k) {
+    const LoopRow& r = kCatalogue[k];
+    rows[k].gene = r.gene;
+    rows[k].line = r.line;
+    rows[k].depth = r.depth;
+    rows[k].nest = r.nest;
+    rows[k].induction = r.induction;
+    rows[k].kernel = r.kernel;
+  }
+  return MMX_GENE_LENGTH;
+}
+
+MMX_API int mmx_plan(const uint8_t* bits, size_t gene_len, int32_t n, int32_t dtype, mmx_plan_info* out) {
+  return build_plan(bits, gene_len, n, dtype, out);
+}
+
+MMX_API void mmx_default_config(mmx_config* cfg) {
+  if (cfg == nullptr) return;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->struct_size = sizeof(mmx_config);
+  cfg->n = 256;                 // fixtures/matmul.c:3
+  cfg->dtype = MMX_F64;         // fixtures/matmul.c:5
+  cfg->numerics = MMX_NUMERICS_FAST;
+  cfg->timeout_s = 120.0;       // ToolchainConfig::timeout_s (evaluator.hpp:43)
+  cfg->repetitions = 1;         // ToolchainConfig::repetitions (evaluator.hpp:44)
+  cfg->num_slots = 1;
+  cfg->devices = nullptr;
+  cfg->host_threads = 1;
+  cfg->launch_batching = 1;
+  cfg->matmul_variant = 0;
+  cfg->warmup = 0;
+}
+
+MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
+  if (cfg == nullptr || out == nullptr) {
+    g_create_error = "null argument";
+    return MMX_E_INVALID;
+  }
+  *out = nullptr;
+  if (cfg->struct_size != sizeof(mmx_config)) {
+    g_create_error = "mmx_config.struct_size mismatch";
+    return MMX_E_INVALID;
+  }
+  if (cfg->n < 1 || cfg->n > 65536 || (cfg->dtype != MMX_F64 && cfg->dtype != MMX_F32) ||
+      (cfg->numerics != MMX_NUMERICS_FAST && cfg->numerics != MMX_NUMERICS_STRICT) || !(cfg->timeout_s > 0.0) ||
+      cfg->repetitions < 1 || cfg->num_slots < 1 || cfg->num_slots > 64 || cfg->host_threads < 1 || cfg->warmup < 0 ||
+      cfg->matmul_variant < 0 || cfg->matmul_variant > 2) {
+    g_create_error = "invalid configuration value";
+    return MMX_E_INVALID;
+  }
+  int count = 0;
+  const cudaError_t ce = cudaGetDeviceCount(&count);
+  if (ce != cudaSuccess || count < 1) {
+    // the reference throws ToolchainMissing when the tool itself is absent (evaluator.cpp:102);
+    // there is deliberately no CPU path to fall back to.
+    g_create_error = std::string("no usable CUDA device: ") + (ce != cudaSuccess ? cudaGetErrorString(ce) : "device count is 0");
+    cudaGetLastError();
+    return MMX_E_NODEVICE;
+  }
+  std::unique_ptr<mmx_ctx> ctx(new mmx_ctx);
+  ctx->cfg = *cfg;
+  ctx->cfg.devices = nullptr;
+  for (int s = 0; s < cfg->num_slots; ++s) {
+    const int dev = cfg->devices ? cfg->devices[s] : s % count;
+    if (dev < 0 || dev >= count) {
+      g_create_error = "device ordinal out of range";
+      return MMX_E_INVALID;
+    }
+    ctx->devices.push_back(dev);
+  }
+  const std::size_t mbytes = matrix_bytes(ctx.get());
+  auto fail = [&](cudaError_t e, const char* what) {
+    g_create_error = std::string(what) + ": " + cudaGetErrorString(e);
+    for (auto& sl : ctx->slots) destroy_slot(*sl);
+    cudaGetLastError();
+    return e == cudaErrorMemoryAllocation ? MMX_E_NOMEM : MMX_E_CUDA;
+  };
+  for (int s = 0; s < cfg->num_slots; ++s) {
+    ctx->slots.emplace_back(new Slot);
+    Slot& sl = *ctx->slots.back();
+    sl.device = ctx->devices[s];
+    cudaError_t e;
+    if ((e = cudaSetDevice(sl.device)) != cudaSuccess) return fail(e, "cudaSetDevice");
+    if ((e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "cudaStreamCreate");
+    if ((e = cudaEventCreate(&sl.ev_begin)) != cudaSuccess) return fail(e, "cudaEventCreate");
+    if ((e = cudaEventCreate(&sl.ev_end)) != cudaSuccess) return fail(e, "cudaEventCreate");
+    for (int q = 0; q < MMX_NUM_ARRAYS; ++q)
+      if ((e = cudaMalloc(&sl.d_arr[q], mbytes)) != cudaSuccess) return fail(e, "cudaMalloc(array)");
+    if ((e = cudaMalloc(&sl.d_sum, 16)) != cudaSuccess) return fail(e, "cudaMalloc(sum)");
+    if ((e = cudaMalloc(reinterpret_cast<void**>(&sl.d_iter), sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(iter)");
+    if ((e = cudaHostAlloc(&sl.h_sum, 16, cudaHostAllocDefault)) != cudaSuccess) return fail(e, "cudaHostAlloc(sum)");
+    std::memset(sl.h_sum, 0, 16);
+  }
+  *out = ctx.release();
+  return MMX_OK;
+}
+
+MMX_API void mmx_destroy(mmx_ctx* ctx) {
+  if (ctx == nullptr) return;
+  for (auto& sl : ctx->slots) destroy_slot(*sl);
+  delete ctx;
+}
+
+MMX_API size_t mmx_gene_length(const mmx_ctx*) { return MMX_GENE_LENGTH; }
+
+MMX_API int mmx_num_slots(const mmx_ctx* ctx) { return ctx ? static_cast<int>(ctx->slots.size()) : 0; }
+
+MMX_API const char* mmx_last_error(const mmx_ctx* ctx) {
+  if (ctx == nullptr) return g_create_error.c_str();
+  std::lock_guard<std::mutex> g(ctx->err_mu);
+  ctx->error_snapshot = ctx->error;
+  return ctx->error_snapshot.c_str();
+}
+
+MMX_API int mmx_measure(mmx_ctx* ctx, int slot, const uint8_t* bits, size_t gene_len, mmx_outcome* out) {
+  return measure_on_slot(ctx, slot, bits, gene_len, out);
+}
+
+MMX_API int mmx_measure_batch(mmx_ctx* ctx, const uint8_t* bits, size_t n_genomes, size_t gene_len, mmx_outcome* outs) {
+  if (ctx == nullptr || (n_genomes > 0 && (bits == nullptr || outs == nullptr))) return MMX_E_INVALID;
+  if (gene_len != MMX_GENE_LENGTH) {
+    ctx->set_error("genome length " + std::to_string(gene_len) + " does not match candidate count 12");
+    return MMX_E_LENGTH;
+  }
+  if (n_genomes == 0) return MMX_OK;
+  // dynamic pull, one worker per slot -- the scheme of Evaluator::evaluate_all (evaluator.cpp:254-273):
+  // per-individual cost varies by orders of magnitude, so static blocks would idle most slots.
+  std::atomic<size_t> next{0};
+  std::atomic<int> first_error{MMX_OK};
+  auto worker = [&](int slot) {
+    for (;;) {
+      const size_t i = next.fetch_add(1);
+      if (i >= n_genomes) return;
+      const int rc = measure_on_slot(ctx, slot, bits + i * gene_len, gene_len, &outs[i]);
+      if (rc != MMX_OK) {
+        int expected = MMX_OK;
+        first_error.compare_exchange_strong(expected, rc);
+        return;
+      }
+    }
+  };
+  const int workers = static_cast<int>(std::min<size_t>(ctx->slots.size(), n_genomes));
+  if (workers == 1) {
+    worker(0);
+  } else {
+    std::vector<std::thread> pool;
+    for (int s = 0; s < workers; ++s) pool.emplace_back(worker, s);
+    for (auto& t : pool) t.join();
+  }
+  return first_error.load();
+}
+
+MMX_API int mmx_last_stats(mmx_ctx* ctx, int slot, mmx_run_stats* out) {
+  if (ctx == nullptr || out == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size())) return MMX_E_INVALID;
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  *out = s.stats;
+  return MMX_OK;
+}
+
+MMX_API int mmx_fetch_array(mmx_ctx* ctx, int slot, int array, void* host, size_t bytes) {
+  if (ctx == nullptr || host == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size()) || array < 0 ||
+      array >= MMX_NUM_ARRAYS)
+    return MMX_E_INVALID;
+  if (bytes != matrix_bytes(ctx)) {
+    ctx->set_error("mmx_fetch_array: size mismatch");
+    return MMX_E_INVALID;
+  }
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  if (s.dev_valid[array]) {
+    MMX_CUDA(ctx, cudaMemcpyAsync(host, s.d_arr[array], bytes, cudaMemcpyDeviceToHost, s.stream));
+    MMX_CUDA(ctx, cudaStreamSynchronize(s.stream));
+    return MMX_OK;
+  }
+  if (s.host_valid[array] && s.h_arr[array] != nullptr && !(array == MMX_ARRAY_C && s.host_diag_only)) {
+    std::memcpy(host, s.h_arr[array], bytes);
+    return MMX_OK;
+  }
+  ctx->set_error("mmx_fetch_array: array is not valid on either side");
+  return MMX_E_STATE;
+}
+
+MMX_API int mmx_upload_array(mmx_ctx* ctx, int slot, int array, const void* host, size_t bytes) {
+  if (ctx == nullptr || host == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size()) || array < 0 ||
+      array >= MMX_NUM_ARRAYS)
+    return MMX_E_INVALID;
+  if (bytes != matrix_bytes(ctx)) {
+    ctx->set_error("mmx_upload_array: size mismatch");
+    return MMX_E_INVALID;
+  }
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  MMX_CUDA(ctx, cudaMemcpyAsync(s.d_arr[array], host, bytes, cudaMemcpyHostToDevice, s.stream));
+  MMX_CUDA(ctx, cudaStreamSynchronize(s.stream));
+  s.dev_valid[array] = true;
+  s.host_valid[array] = false;
+  return MMX_OK;
+}
+
+MMX_API int mmx_run_loop(mmx_ctx* ctx, int slot, int gene, int i, int j, double* sum_out) {
+  if (ctx == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size()) || gene < 0 || gene >= MMX_GENE_LENGTH)
+    return MMX_E_INVALID;
+  const int n = ctx->cfg.n;
+  if (i < 0 || i >= n || j < 0 || j >= n) return MMX_E_INVALID;
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  const int it = gene == 10 ? i * n + j : i;
+  MMX_CUDA(ctx, launch_gene_any(ctx, s, gene, IterRef{nullptr, it}));
+  const int w = written_array(kCatalogue[gene].nest);
+  if (w >= 0) {
+    s.dev_valid[w] = true;
+    s.host_valid[w] = false;
+  }
+  if (gene == 11) {
+    const std::size_t esz = elem_size(ctx->cfg.dtype);
+    MMX_CUDA(ctx, cudaMemcpyAsync(s.h_sum, s.d_sum, esz, cudaMemcpyDeviceToHost, s.stream));
+  }
+  MMX_CUDA(ctx, cudaStreamSynchronize(s.stream));
+  if (gene == 11 && sum_out != nullptr)
+    *sum_out = ctx->cfg.dtype == MMX_F64 ? *static_cast<double*>(s.h_sum) : static_cast<double>(*static_cast<float*>(s.h_sum));
+  return MMX_OK;
+}
+
+MMX_API int mmx_time_loop(mmx_ctx* ctx, int slot, int gene, int iters, int flush_l2, double* ms_out) {
+  if (ctx == nullptr || ms_out == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size()) || gene < 0 ||
+      gene >= MMX_GENE_LENGTH || iters < 1)
+    return MMX_E_INVALID;
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  if (flush_l2 && s.d_scrub == nullptr) {
+    s.scrub_bytes = std::size_t{256} << 20;  // 256 MiB > 126 MB L2
+    MMX_CUDA(ctx, cudaMalloc(&s.d_scrub, s.scrub_bytes));
+  }
+  double total = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    if (flush_l2) MMX_CUDA(ctx, launch_scrub(s.d_scrub, s.scrub_bytes, s.stream));
+    MMX_CUDA(ctx, cudaEventRecord(s.ev_begin, s.stream));
+    MMX_CUDA(ctx, launch_gene_any(ctx, s, gene, IterRef{nullptr, 0}));
+    MMX_CUDA(ctx, cudaEventRecord(s.ev_end, s.stream));
+    MMX_CUDA(ctx, cudaEventSynchronize(s.ev_end));
+    float ms = 0.f;
+    MMX_CUDA(ctx, cudaEventElapsedTime(&ms, s.ev_begin, s.ev_end));
+    total += ms;
+  }
+  *ms_out = total / iters;
+  return MMX_OK;
+}
+
+MMX_API int mmx_peak_probe(int device, int kind, double* value_out) {
+  if (value_out == nullptr) return MMX_E_INVALID;
+  int count = 0;
+  if (cudaGetDeviceCount(&count) != cudaSuccess || count < 1) {
+    cudaGetLastError();
+    return MMX_E_NODEVICE;
+  }
+  if (device < 0 || device >= count) return MMX_E_INVALID;
+  if (cudaSetDevice(device) != cudaSuccess) return MMX_E_CUDA;
+  const cudaError_t e = probe_peak(kind, value_out);
+  if (e != cudaSuccess) {
+    g_create_error = std::string("peak probe: ") + cudaGetErrorString(e);
+    cudaGetLastError();
+    return e == cudaErrorInvalidValue ? MMX_E_INVALID : MMX_E_CUDA;
+  }
+  return MMX_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,161 @@
+// fill.cu -- genes 0-5: the three initialisation nests of fixtures/matmul.c
+//   a[i][j] = (T)(i + j) / N   (:8-10)    b[i][j] = (T)(i - j) / N   (:12-14)    c[i][j] = 0   (:16-18)
+// Pure HBM writes: E*N^2 bytes per nest, 128-bit stores, no reads.
+//
+// Bit-exactness: the integer add and the int->float conversion are exact; the division is
+// IEEE round-to-nearest (`/` without -use_fast_math is div.rn for both float and double).
+// When N is a power of two, x / N == x * (1/N) exactly, so the divide is replaced by one
+// multiply (POW2 path) -- same bits, and it keeps the nest write-bound instead of
+// FP64-divide-bound.
+#include "kernels.cuh"
+
+namespace mmx {
+namespace {
+
+template <typename T, int V> struct Vec;
+template <> struct Vec<double, 2> { using type = double2; };
+template <> struct Vec<float, 4> { using type = float4; };
+template <> struct Vec<double, 1> { using type = double; };
+template <> struct Vec<float, 1> { using type = float; };
+
+template <typename T, int OP, bool POW2>
+__device__ __forceinline__ T fill_value(int i, int j, T nn, T inv) {
+  if (OP == FILL_ZERO) return static_cast<T>(0.0);
+  const int x = OP == FILL_INIT_A ? i + j : i - j;
+  return POW2 ? static_cast<T>(x) * inv : static_cast<T>(x) / nn;
+}
+
+template <typename T, int OP, bool POW2, int V>
+__device__ __forceinline__ void store_vec(T* dst, int i, int j0, T nn, T inv) {
+  if constexpr (V == 1) {
+    *dst = fill_value<T, OP, POW2>(i, j0, nn, inv);
+  } else if constexpr (V == 2) {
+    double2 v;
+    v.x = fill_value<T, OP, POW2>(i, j0, nn, inv);
+    v.y = fill_value<T, OP, POW2>(i, j0 + 1, nn, inv);
+    *reinterpret_cast<double2*>(dst) = v;
+  } else {
+    float4 v;
+    v.x = fill_value<T, OP, POW2>(i, j0, nn, inv);
+    v.y = fill_value<T, OP, POW2>(i, j0 + 1, nn, inv);
+    v.z = fill_value<T, OP, POW2>(i, j0 + 2, nn, inv);
+    v.w = fill_value<T, OP, POW2>(i, j0 + 3, nn, inv);
+    *reinterpret_cast<float4*>(dst) = v;
+  }
+}
+
+constexpr int kRowsPerThread = 8;
+
+// blockDim = (bx, by), bx*by = 256.  A block covers bx*V columns x by*kRowsPerThread rows.
+template <typename T, int OP, bool POW2, int V>
+__global__ void __launch_bounds__(256) fill2d_kernel(T* __restrict__ dst, int n, T nn, T inv) {
+  const int jv = blockIdx.x * blockDim.x + threadIdx.x;  // vector column
+  const int j0 = jv * V;
+  if (j0 >= n) return;
+  const int row0 = (blockIdx.y * blockDim.y + threadIdx.y) * kRowsPerThread;
+#pragma unroll
+  for (int r = 0; r < kRowsPerThread; ++r) {
+    const int i = row0 + r;
+    if (i < n) store_vec<T, OP, POW2, V>(dst + static_cast<size_t>(i) * n + j0, i, j0, nn, inv);
+  }
+}
+
+template <typename T, int OP, bool POW2, int V>
+__global__ void __launch_bounds__(256) fill_row_kernel(T* __restrict__ dst, int n, T nn, T inv, IterRef iter) {
+  const int i = iter.off + (iter.base ? *iter.base : 0);
+  const int j0 = (blockIdx.x * blockDim.x + threadIdx.x) * V;
+  if (j0 < n) store_vec<T, OP, POW2, V>(dst + static_cast<size_t>(i) * n + j0, i, j0, nn, inv);
+}
+
+inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+template <typename T, int OP, bool POW2, int V>
+cudaError_t fill2d_go(T* dst, int n, cudaStream_t stream) {
+  const int nvec = (n + V - 1) / V;
+  int bx = 32;
+  while (bx < 256 && bx < nvec) bx <<= 1;
+  const int by = 256 / bx;
+  dim3 block(bx, by);
+  dim3 grid((nvec + bx - 1) / bx, (n + by * kRowsPerThread - 1) / (by * kRowsPerThread));
+  fill2d_kernel<T, OP, POW2, V><<<grid, block, 0, stream>>>(dst, n, static_cast<T>(n), static_cast<T>(1.0) / static_cast<T>(n));
+  return cudaGetLastError();
+}
+
+template <typename T, int OP, bool POW2, int V>
+cudaError_t fill_row_go(T* dst, int n, IterRef iter, cudaStream_t stream) {
+  const int nvec = (n + V - 1) / V;
+  const int threads = nvec < 256 ? ((nvec + 31) / 32) * 32 : 256;
+  fill_row_kernel<T, OP, POW2, V><<<(nvec + threads - 1) / threads, threads, 0, stream>>>(
+      dst, n, static_cast<T>(n), static_cast<T>(1.0) / static_cast<T>(n), iter);
+  return cudaGetLastError();
+}
+
+template <typename T> constexpr int vec_width() { return 16 / sizeof(T); }
+
+}  // namespace
+
+#define MMX_FILL_CASE(OPV, P2, VV, CALL) \
+  if (op == OPV && pow2 == P2 && vec == (VV != 1)) return CALL<T, OPV, P2, VV>
+
+template <typename T>
+cudaError_t launch_fill2d(int op, T* dst, int n, cudaStream_t stream) {
+  constexpr int W = vec_width<T>();
+  const bool pow2 = is_pow2(n);
+  const bool vec = n % W == 0;
+  MMX_FILL_CASE(FILL_INIT_A, true, W, fill2d_go)(dst, n, stream);
+  MMX_FILL_CASE(FILL_INIT_A, false, W, fill2d_go)(dst, n, stream);
+  MMX_FILL_CASE(FILL_INIT_A, true, 1, fill2d_go)(dst, n, stream);
+  MMX_FILL_CASE(FILL_INIT_A, false, 1, fill2d_go)(dst, n, stream);
+  MMX_FILL_CASE(FILL_INIT_B, true, W, fill2d_go)(dst, n, stream);
+  MMX_FILL_CASE(FILL_INIT_B, false, W, fill2d_go)(dst, n, stream);
+  MMX_FILL_CASE(FILL_INIT_B, true, 1, fill2d_go)(dst, n, stream);
+  MMX_FILL_CASE(FILL_INIT_B, false, 1, fill2d_go)(dst, n, stream);
+  if (op == FILL_ZERO) return vec ? fill2d_go<T, FILL_ZERO, true, W>(dst, n, stream) : fill2d_go<T, FILL_ZERO, true, 1>(dst, n, stream);
+  return cudaErrorInvalidValue;
+}
+
+template <typename T>
+cudaError_t launch_fill_row(int op, T* dst, int n, IterRef iter, cudaStream_t stream) {
+  constexpr int W = vec_width<T>();
+  const bool pow2 = is_pow2(n);
+  const bool vec = n % W == 0;
+  MMX_FILL_CASE(FILL_INIT_A, true, W, fill_row_go)(dst, n, iter, stream);
+  MMX_FILL_CASE(FILL_INIT_A, false, W, fill_row_go)(dst, n, iter, stream);
+  MMX_FILL_CASE(FILL_INIT_A, true, 1, fill_row_go)(dst, n, iter, stream);
+  MMX_FILL_CASE(FILL_INIT_A, false, 1, fill_row_go)(dst, n, iter, stream);
+  MMX_FILL_CASE(FILL_INIT_B, true, W, fill_row_go)(dst, n, iter, stream);
+  MMX_FILL_CASE(FILL_INIT_B, false, W, fill_row_go)(dst, n, iter, stream);
+  MMX_FILL_CASE(FILL_INIT_B, true, 1, fill_row_go)(dst, n, iter, stream);
+  MMX_FILL_CASE(FILL_INIT_B, false, 1, fill_row_go)(dst, n, iter, stream);
+  if (op == FILL_ZERO) return vec ? fill_row_go<T, FILL_ZERO, true, W>(dst, n, iter, stream) : fill_row_go<T, FILL_ZERO, true, 1>(dst, n, iter, stream);
+  return cudaErrorInvalidValue;
+}
+
+template cudaError_t launch_fill2d<double>(int, double*, int, cudaStream_t);
+template cudaError_t launch_fill2d<float>(int, float*, int, cudaStream_t);
+template cudaError_t launch_fill_row<double>(int, double*, int, IterRef, cudaStream_t);
+template cudaError_t launch_fill_row<float>(int, float*, int, IterRef, cudaStream_t);
+
+// ---- small helpers shared by the executor -------------------------------------------------
+
+namespace {
+__global__ void advance_kernel(int* counter, int delta) { *counter += delta; }
+
+__global__ void __launch_bounds__(256) scrub_kernel(uint4* p, size_t nvec) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  for (size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec; v += stride)
+    p[v] = make_uint4(0x9e3779b9u, 0x7f4a7c15u, 0xf39cc060u, 0x5cedc834u);
+}
+}  // namespace
+
+cudaError_t launch_advance(int* counter, int delta, cudaStream_t stream) {
+  advance_kernel<<<1, 1, 0, stream>>>(counter, delta);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_scrub(void* p, std::size_t bytes, cudaStream_t stream) {
+  scrub_kernel<<<kNumSMs * 8, 256, 0, stream>>>(static_cast<uint4*>(p), bytes / 16);
+  return cudaGetLastError();
+}
+
+}  // namespace mmx

@@ -1,0 +1,34 @@
+// host_loops.hpp -- the CPU side of a genome: loops whose gene bit is 0 run here, on the
+// slot's pinned host arrays, exactly as the program writes them
+// (/root/reference/proj/fixtures/matmul.c:8-32; same loop order, k ascending, separate
+// multiply and add -- this translation unit is built with -ffp-contract=off).
+#pragma once
+
+#include <chrono>
+#include <cstddef>
+
+namespace mmx {
+
+using Clock = std::chrono::steady_clock;
+
+// Budget shared by every step of one benchmark run (ToolchainConfig::timeout_s).
+struct Deadline {
+  Clock::time_point at;
+  bool expired() const { return Clock::now() >= at; }
+};
+
+// Each returns false when the deadline passed before the nest finished (rows are the unit
+// of the check).  `threads` > 1 splits the outer loop into contiguous row blocks; per-element
+// arithmetic is unchanged, so results do not depend on it.
+template <typename T> bool host_init_a(T* a, int n, int threads, const Deadline& dl);
+template <typename T> bool host_init_b(T* b, int n, int threads, const Deadline& dl);
+template <typename T> bool host_zero_c(T* c, int n, int threads, const Deadline& dl);
+template <typename T> bool host_transpose(T* bt, const T* b, int n, int threads, const Deadline& dl);
+template <typename T> bool host_matmul(T* c, const T* a, const T* bt, int n, int threads, const Deadline& dl);
+// matmul.c:30-32; the accumulator has the array's type, the result is widened for printf.
+template <typename T> double host_trace(const T* c, int n);
+
+// Pieces used when the host only drives an outer loop and the device runs the inner one
+// are not needed here: in those modes the host loop body is just a kernel launch.
+
+}  // namespace mmx

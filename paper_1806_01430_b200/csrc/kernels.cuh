@@ -1,0 +1,61 @@
+// kernels.cuh -- launchers of the sm_100a kernel library: one kernel family per offloadable
+// loop of /root/reference/proj/fixtures/matmul.c (catalogue in plan.cpp).
+//
+// Every launcher enqueues on `stream` and returns the launch status; none synchronises.
+// Iterations of host-driven outer loops are passed as IterRef so that one captured CUDA
+// graph can replay a train of launches: the kernel adds a device-resident base counter to a
+// per-node constant.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace mmx {
+
+// Which iteration of the enclosing host loop(s) a launch serves: value = off + (base ? *base : 0).
+struct IterRef {
+  const int* base;  // device pointer or nullptr
+  int off;
+};
+
+enum FillOp { FILL_INIT_A = 0, FILL_INIT_B = 1, FILL_ZERO = 2 };
+
+// genes 0,2,4: dst[i][j] = op(i,j) over the whole n x n array (matmul.c:8-18)
+template <typename T> cudaError_t launch_fill2d(int op, T* dst, int n, cudaStream_t stream);
+// genes 1,3,5: one row i = iter of the same
+template <typename T> cudaError_t launch_fill_row(int op, T* dst, int n, IterRef iter, cudaStream_t stream);
+
+// gene 6: bt[i][j] = b[j][i] (matmul.c:21-23)
+template <typename T> cudaError_t launch_transpose(T* bt, const T* b, int n, cudaStream_t stream);
+// gene 7: row i of bt = column i of b
+template <typename T> cudaError_t launch_transpose_row(T* bt, const T* b, int n, IterRef iter, cudaStream_t stream);
+
+// gene 8: c[i][j] += sum_k a[i][k] * bt[j][k] (matmul.c:25-28).  variant: 1 SIMT, 2 DMMA (FP64 only).
+// Rows [row0, row0+rows) of a and c only (row0 = 0, rows = n for the whole nest; the
+// row-sharded multi-GPU path passes its block).
+template <typename T>
+cudaError_t launch_matmul(T* c, const T* a, const T* bt, int n, int row0, int rows, bool strict, int variant,
+                          cudaStream_t stream);
+// gene 9: row i of the same (GEMV against bt)
+template <typename T>
+cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, bool strict, cudaStream_t stream);
+// gene 10: one element (i, j): flat iteration f = i*n + j
+template <typename T>
+cudaError_t launch_dot(T* c, const T* a, const T* bt, int n, IterRef flat_iter, bool strict, cudaStream_t stream);
+
+// gene 11: *sum = sum_i c[i][i] (matmul.c:30-32)
+template <typename T> cudaError_t launch_trace(T* sum, const T* c, int n, bool strict, cudaStream_t stream);
+
+// graph plumbing: *counter += delta
+cudaError_t launch_advance(int* counter, int delta, cudaStream_t stream);
+
+// L2 flush helper for benchmarking: overwrite `bytes` at p
+cudaError_t launch_scrub(void* p, std::size_t bytes, cudaStream_t stream);
+
+// peak probes (peaks.cu); each returns the achieved rate through *value
+cudaError_t probe_peak(int kind, double* value);
+
+constexpr int kNumSMs = 148;  // B200
+
+}  // namespace mmx

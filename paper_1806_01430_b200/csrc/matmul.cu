@@ -1,0 +1,347 @@
+// matmul.cu -- gene 8: c[i][j] += sum_k a[i][k] * bt[j][k]   (fixtures/matmul.c:25-28)
+//
+// "NT" GEMM: both operands are K-contiguous (that is why the program transposes b first).
+// Compute-bound: 2*N^3 flop against 4*E*N^2 bytes of compulsory traffic.
+//
+// tcgen05/UMMA has no FP64 and no FP32-input kind, so at the reference's precision the dense
+// contraction runs on the FP64 pipe (DFMA, or DMMA.8x8x4 through mma.sync -- the only shape
+// sm_100a implements natively; m16n8k{4,8,16}.f64 lower to chains of it) or the FP32 FFMA pipe.
+//
+// Summation order.  Each c[i][j] is owned by one thread, initialised with the incoming c value
+// and accumulated k ascending, so:
+//   STRICT  (mul.rn then add.rn)  == the CPU loop bit for bit, any N, both dtypes;
+//   FAST    (fma.rn, k ascending) == the CPU loop bit for bit whenever all partial sums are
+//           exactly representable (FP64, N a power of two: SURVEY appendix A); otherwise it
+//           differs only by the single rounding FMA saves per term.
+// The DMMA variant keeps the same k-ascending FMA chain per element (the MMA accumulates its
+// four products in order into the running sum), so it produces the same bits as FAST SIMT.
+#include "kernels.cuh"
+
+namespace mmx {
+namespace {
+
+// ---------------------------------------------------------------------------------------------
+// SIMT kernel: 128x128 CTA tile, BK = 16, 256 threads, 8x8 outputs per thread (2x2 groups of 4x4).
+// Shared tiles are stored k-major ([k][m]) so the inner loop reads its 8 a's and 8 b's with
+// 128-bit LDS that broadcast across the warp.
+// ---------------------------------------------------------------------------------------------
+constexpr int BM = 128, BN = 128, BK = 16;
+
+template <typename T> struct V16;
+template <> struct V16<double> { using type = double2; static constexpr int W = 2; };
+template <> struct V16<float> { using type = float4; static constexpr int W = 4; };
+
+template <typename T, bool STRICT>
+__device__ __forceinline__ T mac(T acc, T x, T y) {
+  if constexpr (STRICT) {
+    if constexpr (sizeof(T) == 8) return __dadd_rn(acc, __dmul_rn(x, y));
+    else return __fadd_rn(acc, __fmul_rn(x, y));
+  } else {
+    if constexpr (sizeof(T) == 8) return __fma_rn(x, y, acc);
+    else return __fmaf_rn(x, y, acc);
+  }
+}
+
+// Load 8 consecutive k of one row (row-major, K contiguous) into regs; zero outside [0,n).
+template <typename T>
+__device__ __forceinline__ void load_row8(T (&dst)[8], const T* __restrict__ base, int row, int row_limit, int k0,
+                                          int n, bool vec_ok) {
+  using VT = typename V16<T>::type;
+  constexpr int W = V16<T>::W;
+  if (row < row_limit && vec_ok && k0 + 8 <= n) {
+    const VT* p = reinterpret_cast<const VT*>(base + static_cast<size_t>(row) * n + k0);
+#pragma unroll
+    for (int v = 0; v < 8 / W; ++v) {
+      const VT x = p[v];
+      if constexpr (W == 2) {
+        dst[2 * v] = x.x;
+        dst[2 * v + 1] = x.y;
+      } else {
+        dst[4 * v] = x.x;
+        dst[4 * v + 1] = x.y;
+        dst[4 * v + 2] = x.z;
+        dst[4 * v + 3] = x.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      dst[q] = (row < row_limit && k0 + q < n) ? base[static_cast<size_t>(row) * n + k0 + q] : static_cast<T>(0.0);
+  }
+}
+
+template <typename T, bool STRICT>
+__global__ void __launch_bounds__(256, 1)
+matmul_simt_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ bt, int n, int row0, int rows,
+                   bool vec_ok) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* As = reinterpret_cast<T*>(smem_raw);  // [2][BK][BM]
+  T* Bs = As + 2 * BK * BM;                // [2][BK][BN]
+
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int m_base = row0 + blockIdx.y * BM;  // first row of a / c of this CTA
+  const int n_base = blockIdx.x * BN;         // first row of bt == first column of c
+  const int m_limit = row0 + rows;
+
+  // global -> smem staging role: one row, 8 consecutive k
+  const int ld_row = tid % 128;
+  const int ld_k = (tid / 128) * 8;
+
+  T acc[8][8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int m = m_base + (r / 4) * 64 + ty * 4 + (r % 4);
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const int j = n_base + (q / 4) * 64 + tx * 4 + (q % 4);
+      acc[r][q] = (m < m_limit && j < n) ? c[static_cast<size_t>(m) * n + j] : static_cast<T>(0.0);
+    }
+  }
+
+  T ra[8], rb[8];
+  load_row8(ra, a, m_base + ld_row, m_limit, ld_k, n, vec_ok);
+  load_row8(rb, bt, n_base + ld_row, n, ld_k, n, vec_ok);
+#pragma unroll
+  for (int q = 0; q < 8; ++q) {
+    As[(ld_k + q) * BM + ld_row] = ra[q];
+    Bs[(ld_k + q) * BN + ld_row] = rb[q];
+  }
+  __syncthreads();
+
+  const int k_tiles = (n + BK - 1) / BK;
+  for (int t = 0; t < k_tiles; ++t) {
+    const int cur = t & 1;
+    const bool more = t + 1 < k_tiles;
+    if (more) {
+      load_row8(ra, a, m_base + ld_row, m_limit, (t + 1) * BK + ld_k, n, vec_ok);
+      load_row8(rb, bt, n_base + ld_row, n, (t + 1) * BK + ld_k, n, vec_ok);
+    }
+    const T* Ac = As + cur * BK * BM;
+    const T* Bc = Bs + cur * BK * BN;
+    // STRICT must not add the zero-padded tail terms (x + 0*0 can flip a -0 accumulator)
+    const int k_valid = STRICT ? min(BK, n - t * BK) : BK;
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      if (STRICT && k >= k_valid) break;
+      T fa[8], fb[8];
+      using VT = typename V16<T>::type;
+      constexpr int W = V16<T>::W;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+#pragma unroll
+        for (int v = 0; v < 4 / W; ++v) {
+          const VT xa = *reinterpret_cast<const VT*>(Ac + k * BM + h * 64 + ty * 4 + v * W);
+          const VT xb = *reinterpret_cast<const VT*>(Bc + k * BN + h * 64 + tx * 4 + v * W);
+          if constexpr (W == 2) {
+            fa[h * 4 + v * 2] = xa.x; fa[h * 4 + v * 2 + 1] = xa.y;
+            fb[h * 4 + v * 2] = xb.x; fb[h * 4 + v * 2 + 1] = xb.y;
+          } else {
+            fa[h * 4] = xa.x; fa[h * 4 + 1] = xa.y; fa[h * 4 + 2] = xa.z; fa[h * 4 + 3] = xa.w;
+            fb[h * 4] = xb.x; fb[h * 4 + 1] = xb.y; fb[h * 4 + 2] = xb.z; fb[h * 4 + 3] = xb.w;
+          }
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int q = 0; q < 8; ++q) acc[r][q] = mac<T, STRICT>(acc[r][q], fa[r], fb[q]);
+    }
+    if (more) {
+      T* An = As + (cur ^ 1) * BK * BM;
+      T* Bn = Bs + (cur ^ 1) * BK * BN;
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        An[(ld_k + q) * BM + ld_row] = ra[q];
+        Bn[(ld_k + q) * BN + ld_row] = rb[q];
+      }
+    }
+    __syncthreads();
+  }
+
+#pragma unroll
+  for (int r = 0; r < 8; ++r) {
+    const int m = m_base + (r / 4) * 64 + ty * 4 + (r % 4);
+    if (m >= m_limit) continue;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int j = n_base + h * 64 + tx * 4;
+      T* dst = c + static_cast<size_t>(m) * n + j;
+      if (vec_ok && j + 4 <= n) {
+        using VT = typename V16<T>::type;
+        if constexpr (sizeof(T) == 8) {
+          reinterpret_cast<VT*>(dst)[0] = make_double2(acc[r][h * 4], acc[r][h * 4 + 1]);
+          reinterpret_cast<VT*>(dst)[1] = make_double2(acc[r][h * 4 + 2], acc[r][h * 4 + 3]);
+        } else {
+          reinterpret_cast<VT*>(dst)[0] = make_float4(acc[r][h * 4], acc[r][h * 4 + 1], acc[r][h * 4 + 2], acc[r][h * 4 + 3]);
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (j + q < n) dst[q] = acc[r][h * 4 + q];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// DMMA kernel (FP64, FAST only): mma.sync.m8n8k4.f64.  CTA tile 128x128, BK = 16, 8 warps as
+// 2 (m) x 4 (n); warp tile 64x32 = 8x4 MMA tiles.  Operands go global -> smem with 16-byte
+// cp.async in their native K-contiguous layout (no transposition: both fragments of
+// DMMA.8x8x4 want "row r = lane/4, k = lane%4", which is exactly a K-contiguous read).  Rows are
+// padded to BK+4 doubles (160 B) so the 8-row x 4-k fragment reads of a half-warp hit 32 distinct
+// banks.  3-stage pipeline.
+// ---------------------------------------------------------------------------------------------
+constexpr int DK = 16;            // k per stage
+constexpr int DLD = DK + 4;       // padded row length in doubles (160 B)
+constexpr int DSTAGES = 3;
+constexpr int DTILE = 128;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned s = static_cast<unsigned>(__cvta_generic_to_shared(smem));
+  const int bytes = valid ? 16 : 0;  // src-size 0 => zero fill
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(s), "l"(gmem), "r"(bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N> __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// Requires n % 2 == 0 (16-byte aligned rows); rows/cols outside the matrix are zero-filled on
+// load and masked on store.  k tail (n % 16) is zero-filled: adding +0 products is harmless in
+// FAST mode except for the sign of an all-zero sum, which compares equal.
+__global__ void __launch_bounds__(256, 1)
+matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const double* __restrict__ bt, int n,
+                   int row0, int rows) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* As = reinterpret_cast<double*>(smem_raw);   // [DSTAGES][DTILE][DLD]
+  double* Bs = As + DSTAGES * DTILE * DLD;            // [DSTAGES][DTILE][DLD]
+
+  const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  const int wm = warp / 4, wn = warp % 4;  // 2 x 4 warps
+  const int m_base = row0 + blockIdx.y * DTILE, n_base = blockIdx.x * DTILE;
+  const int m_limit = row0 + rows;
+  const int g = lane / 4, t4 = lane % 4;   // fragment row, fragment k
+
+  // cp.async role: 128 rows x 16 k = 128 x 8 chunks of 16 B per operand; 256 threads x 4 chunks
+  auto issue_stage = [&](int stage, int k0) {
+#pragma unroll
+    for (int it = 0; it < 4; ++it) {
+      const int chunk = tid + it * 256;     // 0..1023
+      const int row = chunk / 8, kc = (chunk % 8) * 2;
+      const bool kin = k0 + kc < n;
+      const int ar = m_base + row, br = n_base + row;
+      const bool av = kin && ar < m_limit, bv = kin && br < n;
+      cp_async16(As + (stage * DTILE + row) * DLD + kc, av ? a + static_cast<size_t>(ar) * n + k0 + kc : a, av);
+      cp_async16(Bs + (stage * DTILE + row) * DLD + kc, bv ? bt + static_cast<size_t>(br) * n + k0 + kc : bt, bv);
+    }
+  };
+
+  // accumulators: 8 (m tiles) x 4 (n tiles) x 2
+  double acc[8][4][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m_base + wm * 64 + i * 8 + g;
+      const int col = n_base + wn * 32 + j * 8 + t4 * 2;
+      const bool ok = m < m_limit && col < n;  // n even => col+1 < n too
+      const double2 v = ok ? *reinterpret_cast<const double2*>(c + static_cast<size_t>(m) * n + col) : make_double2(0.0, 0.0);
+      acc[i][j][0] = v.x;
+      acc[i][j][1] = v.y;
+    }
+
+  const int k_tiles = (n + DK - 1) / DK;
+#pragma unroll
+  for (int s = 0; s < DSTAGES - 1; ++s) {
+    if (s < k_tiles) issue_stage(s, s * DK);
+    cp_async_commit();
+  }
+
+  for (int t = 0; t < k_tiles; ++t) {
+    cp_async_wait<DSTAGES - 2>();
+    __syncthreads();
+    {
+      const int nt = t + DSTAGES - 1;
+      if (nt < k_tiles) issue_stage(nt % DSTAGES, nt * DK);
+      cp_async_commit();
+    }
+    const double* Ac = As + ((t % DSTAGES) * DTILE + wm * 64) * DLD;
+    const double* Bc = Bs + ((t % DSTAGES) * DTILE + wn * 32) * DLD;
+#pragma unroll
+    for (int kk = 0; kk < DK; kk += 4) {
+      double fa[8], fb[4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) fa[i] = Ac[(i * 8 + g) * DLD + kk + t4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) fb[j] = Bc[(j * 8 + g) * DLD + kk + t4];
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], fa[i], fb[j]);
+    }
+  }
+  cp_async_wait<0>();
+
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m_base + wm * 64 + i * 8 + g;
+      const int col = n_base + wn * 32 + j * 8 + t4 * 2;
+      if (m < m_limit && col < n)
+        *reinterpret_cast<double2*>(c + static_cast<size_t>(m) * n + col) = make_double2(acc[i][j][0], acc[i][j][1]);
+    }
+}
+
+template <typename T, bool STRICT>
+cudaError_t simt_go(T* c, const T* a, const T* bt, int n, int row0, int rows, cudaStream_t stream) {
+  const size_t smem = 2 * BK * (BM + BN) * sizeof(T);
+  static bool configured = false;  // per instantiation; benign race (idempotent)
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(matmul_simt_kernel<T, STRICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((n + BN - 1) / BN, (rows + BM - 1) / BM);
+  const bool vec_ok = n % V16<T>::W == 0;
+  matmul_simt_kernel<T, STRICT><<<grid, 256, smem, stream>>>(c, a, bt, n, row0, rows, vec_ok);
+  return cudaGetLastError();
+}
+
+cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row0, int rows, cudaStream_t stream) {
+  const size_t smem = 2 * DSTAGES * DTILE * DLD * sizeof(double);
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(matmul_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((n + DTILE - 1) / DTILE, (rows + DTILE - 1) / DTILE);
+  matmul_dmma_kernel<<<grid, 256, smem, stream>>>(c, a, bt, n, row0, rows);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+template <>
+cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, int n, int row0, int rows, bool strict,
+                                  int variant, cudaStream_t stream) {
+  if (strict) return simt_go<double, true>(c, a, bt, n, row0, rows, stream);
+  if (variant == 2 && n % 2 == 0) return dmma_go(c, a, bt, n, row0, rows, stream);
+  return simt_go<double, false>(c, a, bt, n, row0, rows, stream);
+}
+
+template <>
+cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int n, int row0, int rows, bool strict,
+                                 int variant, cudaStream_t stream) {
+  (void)variant;
+  if (strict) return simt_go<float, true>(c, a, bt, n, row0, rows, stream);
+  return simt_go<float, false>(c, a, bt, n, row0, rows, stream);
+}
+
+}  // namespace mmx

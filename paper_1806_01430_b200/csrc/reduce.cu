@@ -1,0 +1,240 @@
+// reduce.cu -- the reduction-style loops of fixtures/matmul.c:
+//   gene 9  (:26)  for j: c[i][j] += dot(a[i][:], bt[j][:])   -- one GEMV against bt per launch
+//   gene 10 (:27)  for k: c[i][j] += a[i][k] * bt[j][k]       -- one dot product per launch
+//   gene 11 (:31)  for i: sum += c[i][i]                      -- the trace
+//
+// FAST: lanes stride over k with 128-bit loads, warp-shuffle tree, then c += partial.  Exact
+// (hence bit-identical to the CPU loop) whenever the partial sums are exactly representable
+// (FP64, N = 2^p); otherwise within the stated tolerance.
+// STRICT: the data is staged through shared memory with coalesced loads, then ONE thread per
+// output walks k ascending with a separate multiply and add, starting from the incoming c
+// value -- the CPU loop's exact operation sequence.
+#include "kernels.cuh"
+
+namespace mmx {
+namespace {
+
+template <typename T> struct V16;
+template <> struct V16<double> { using type = double2; static constexpr int W = 2; };
+template <> struct V16<float> { using type = float4; static constexpr int W = 4; };
+
+__device__ __forceinline__ double vdot(double2 x, double2 y, double acc) {
+  acc = __fma_rn(x.x, y.x, acc);
+  return __fma_rn(x.y, y.y, acc);
+}
+__device__ __forceinline__ float vdot(float4 x, float4 y, float acc) {
+  acc = __fmaf_rn(x.x, y.x, acc);
+  acc = __fmaf_rn(x.y, y.y, acc);
+  acc = __fmaf_rn(x.z, y.z, acc);
+  return __fmaf_rn(x.w, y.w, acc);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T strict_mac(T acc, T x, T y) {
+  if constexpr (sizeof(T) == 8) return __dadd_rn(acc, __dmul_rn(x, y));
+  else return __fadd_rn(acc, __fmul_rn(x, y));
+}
+
+// Partial dot of two K-contiguous rows over the lanes of one warp (FAST).
+template <typename T>
+__device__ __forceinline__ T warp_dot(const T* __restrict__ x, const T* __restrict__ y, int n, int lane, bool vec_ok) {
+  using VT = typename V16<T>::type;
+  constexpr int W = V16<T>::W;
+  T acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+  if (vec_ok) {
+    const VT* xv = reinterpret_cast<const VT*>(x);
+    const VT* yv = reinterpret_cast<const VT*>(y);
+    const int nv = n / W;
+    int v = lane;
+    for (; v + 96 < nv; v += 128) {  // 4 independent 16-byte loads per operand in flight
+      const VT x0 = xv[v], x1 = xv[v + 32], x2 = xv[v + 64], x3 = xv[v + 96];
+      const VT y0 = yv[v], y1 = yv[v + 32], y2 = yv[v + 64], y3 = yv[v + 96];
+      acc0 = vdot(x0, y0, acc0);
+      acc1 = vdot(x1, y1, acc1);
+      acc2 = vdot(x2, y2, acc2);
+      acc3 = vdot(x3, y3, acc3);
+    }
+    for (; v < nv; v += 32) acc0 = vdot(xv[v], yv[v], acc0);
+  } else {
+    for (int k = lane; k < n; k += 32) acc0 += x[k] * y[k];
+  }
+  return warp_sum((acc0 + acc1) + (acc2 + acc3));
+}
+
+// ---- gene 9 ------------------------------------------------------------------------------------
+
+// FAST: one warp per output column j; block = 256 threads = 8 columns.
+template <typename T>
+__global__ void __launch_bounds__(256) gemv_row_fast_kernel(T* __restrict__ c, const T* __restrict__ a,
+                                                            const T* __restrict__ bt, int n, IterRef iter, bool vec_ok) {
+  const int i = iter.off + (iter.base ? *iter.base : 0);
+  const int lane = threadIdx.x % 32;
+  const int j = blockIdx.x * 8 + threadIdx.x / 32;
+  if (j >= n) return;
+  const T s = warp_dot(a + static_cast<size_t>(i) * n, bt + static_cast<size_t>(j) * n, n, lane, vec_ok);
+  if (lane == 0) c[static_cast<size_t>(i) * n + j] += s;
+}
+
+// STRICT: block = 64 threads owns 64 columns j; k is walked in tiles of 64 staged in smem.
+template <typename T>
+__global__ void __launch_bounds__(64) gemv_row_strict_kernel(T* __restrict__ c, const T* __restrict__ a,
+                                                             const T* __restrict__ bt, int n, IterRef iter) {
+  __shared__ T sb[64][65];
+  __shared__ T sa[64];
+  const int i = iter.off + (iter.base ? *iter.base : 0);
+  const int t = threadIdx.x;
+  const int j0 = blockIdx.x * 64;
+  const int j = j0 + t;
+  T acc = j < n ? c[static_cast<size_t>(i) * n + j] : static_cast<T>(0.0);
+  for (int k0 = 0; k0 < n; k0 += 64) {
+    const int kw = min(64, n - k0);
+    if (t < kw) sa[t] = a[static_cast<size_t>(i) * n + k0 + t];
+    for (int r = 0; r < 64; ++r)  // coalesced: thread t reads bt[j0+r][k0+t]
+      if (j0 + r < n && t < kw) sb[r][t] = bt[static_cast<size_t>(j0 + r) * n + k0 + t];
+    __syncthreads();
+    if (j < n)
+      for (int k = 0; k < kw; ++k) acc = strict_mac(acc, sa[k], sb[t][k]);
+    __syncthreads();
+  }
+  if (j < n) c[static_cast<size_t>(i) * n + j] = acc;
+}
+
+// ---- gene 10 -----------------------------------------------------------------------------------
+
+// FAST: one block of 256 threads per (i, j).
+template <typename T>
+__global__ void __launch_bounds__(256) dot_fast_kernel(T* __restrict__ c, const T* __restrict__ a,
+                                                       const T* __restrict__ bt, int n, IterRef iter, bool vec_ok) {
+  using VT = typename V16<T>::type;
+  constexpr int W = V16<T>::W;
+  __shared__ T partial[8];
+  const int f = iter.off + (iter.base ? *iter.base : 0);
+  const int i = f / n, j = f % n;
+  const T* x = a + static_cast<size_t>(i) * n;
+  const T* y = bt + static_cast<size_t>(j) * n;
+  T acc = 0;
+  if (vec_ok) {
+    const VT* xv = reinterpret_cast<const VT*>(x);
+    const VT* yv = reinterpret_cast<const VT*>(y);
+    for (int v = threadIdx.x; v < n / W; v += 256) acc = vdot(xv[v], yv[v], acc);
+  } else {
+    for (int k = threadIdx.x; k < n; k += 256) acc += x[k] * y[k];
+  }
+  acc = warp_sum(acc);
+  if (threadIdx.x % 32 == 0) partial[threadIdx.x / 32] = acc;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    T v = threadIdx.x < 8 ? partial[threadIdx.x] : static_cast<T>(0.0);
+    v = warp_sum(v);
+    if (threadIdx.x == 0) c[static_cast<size_t>(i) * n + j] += v;
+  }
+}
+
+// STRICT: stage both rows in smem chunk by chunk, thread 0 walks k ascending.
+template <typename T>
+__global__ void __launch_bounds__(256) dot_strict_kernel(T* __restrict__ c, const T* __restrict__ a,
+                                                         const T* __restrict__ bt, int n, IterRef iter) {
+  constexpr int CH = 2048;
+  __shared__ T sx[CH], sy[CH];
+  const int f = iter.off + (iter.base ? *iter.base : 0);
+  const int i = f / n, j = f % n;
+  const T* x = a + static_cast<size_t>(i) * n;
+  const T* y = bt + static_cast<size_t>(j) * n;
+  T acc = c[static_cast<size_t>(i) * n + j];
+  for (int k0 = 0; k0 < n; k0 += CH) {
+    const int kw = min(CH, n - k0);
+    for (int k = threadIdx.x; k < kw; k += 256) {
+      sx[k] = x[k0 + k];
+      sy[k] = y[k0 + k];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int k = 0; k < kw; ++k) acc = strict_mac(acc, sx[k], sy[k]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) c[static_cast<size_t>(i) * n + j] = acc;
+}
+
+// ---- gene 11 -----------------------------------------------------------------------------------
+
+// One block of 1024 threads: strided gather of the diagonal, shuffle + smem tree (FAST), or
+// staged chunks summed in index order by thread 0 (STRICT).  N elements, latency-bound.
+template <typename T, bool STRICT>
+__global__ void __launch_bounds__(1024) trace_kernel(T* __restrict__ sum, const T* __restrict__ c, int n) {
+  __shared__ T buf[1024];
+  const int t = threadIdx.x;
+  const size_t pitch = static_cast<size_t>(n) + 1;
+  if constexpr (STRICT) {
+    T acc = static_cast<T>(0.0);
+    for (int i0 = 0; i0 < n; i0 += 1024) {
+      const int w = min(1024, n - i0);
+      if (t < w) buf[t] = c[(i0 + t) * pitch];
+      __syncthreads();
+      if (t == 0)
+        for (int i = 0; i < w; ++i) {
+          if constexpr (sizeof(T) == 8) acc = __dadd_rn(acc, buf[i]);
+          else acc = __fadd_rn(acc, buf[i]);
+        }
+      __syncthreads();
+    }
+    if (t == 0) *sum = acc;
+  } else {
+    T acc = static_cast<T>(0.0);
+    for (int i = t; i < n; i += 1024) acc += c[i * pitch];
+    acc = warp_sum(acc);
+    if (t % 32 == 0) buf[t / 32] = acc;
+    __syncthreads();
+    if (t < 32) {
+      T v = buf[t];  // 32 warps
+      v = warp_sum(v);
+      if (t == 0) *sum = v;
+    }
+  }
+}
+
+}  // namespace
+
+template <typename T>
+cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, bool strict, cudaStream_t stream) {
+  if (strict) {
+    gemv_row_strict_kernel<T><<<(n + 63) / 64, 64, 0, stream>>>(c, a, bt, n, iter);
+  } else {
+    const bool vec_ok = n % V16<T>::W == 0;
+    gemv_row_fast_kernel<T><<<(n + 7) / 8, 256, 0, stream>>>(c, a, bt, n, iter, vec_ok);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_dot(T* c, const T* a, const T* bt, int n, IterRef flat_iter, bool strict, cudaStream_t stream) {
+  if (strict) {
+    dot_strict_kernel<T><<<1, 256, 0, stream>>>(c, a, bt, n, flat_iter);
+  } else {
+    const bool vec_ok = n % V16<T>::W == 0;
+    dot_fast_kernel<T><<<1, 256, 0, stream>>>(c, a, bt, n, flat_iter, vec_ok);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_trace(T* sum, const T* c, int n, bool strict, cudaStream_t stream) {
+  if (strict) trace_kernel<T, true><<<1, 1024, 0, stream>>>(sum, c, n);
+  else trace_kernel<T, false><<<1, 1024, 0, stream>>>(sum, c, n);
+  return cudaGetLastError();
+}
+
+#define MMX_INST(T)                                                                                        \
+  template cudaError_t launch_gemv_row<T>(T*, const T*, const T*, int, IterRef, bool, cudaStream_t);      \
+  template cudaError_t launch_dot<T>(T*, const T*, const T*, int, IterRef, bool, cudaStream_t);           \
+  template cudaError_t launch_trace<T>(T*, const T*, int, bool, cudaStream_t);
+MMX_INST(double)
+MMX_INST(float)
+
+}  // namespace mmx

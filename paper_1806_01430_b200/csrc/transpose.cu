@@ -1,0 +1,131 @@
+// transpose.cu -- genes 6 and 7: bt[i][j] = b[j][i]  (fixtures/matmul.c:21-23)
+//
+// Pure data movement, bit-exact by construction.  HBM-bound: 2*E*N^2 bytes (read b, write bt).
+//
+// gene 6 (whole nest), fast path for N % 64 == 0: a CTA moves one 64x64 tile.  Global loads
+// and stores are both 128-bit and fully coalesced (a warp covers whole 512 B / 256 B row
+// segments).  The exchange goes through shared memory in units of VxV micro-blocks
+// (V = 16 B / E): a thread loads V vectors from V consecutive rows, transposes the VxV block in
+// registers and stores V vectors into the *output-ordered* tile.  The tile is XOR-swizzled at
+// 16-byte granularity (chunk ^= (row / V) & 7) so that both the micro-block stores (lanes walk
+// down the rows) and the row reads (lanes walk along a row) are bank-conflict free.
+//
+// gene 7 (one row of bt per launch): row i of bt is column i of b -- a strided gather; each
+// 8-byte element costs a 32-byte sector, which is the sector amplification the catalogue notes.
+#include "kernels.cuh"
+
+namespace mmx {
+namespace {
+
+constexpr int kTile = 64;
+
+template <typename T> struct VecOf;
+template <> struct VecOf<double> { using type = double2; static constexpr int V = 2; };
+template <> struct VecOf<float> { using type = float4; static constexpr int V = 4; };
+
+__device__ __forceinline__ void transpose_micro(const double2 (&in)[2], double2 (&out)[2]) {
+  out[0] = make_double2(in[0].x, in[1].x);
+  out[1] = make_double2(in[0].y, in[1].y);
+}
+__device__ __forceinline__ void transpose_micro(const float4 (&in)[4], float4 (&out)[4]) {
+  out[0] = make_float4(in[0].x, in[1].x, in[2].x, in[3].x);
+  out[1] = make_float4(in[0].y, in[1].y, in[2].y, in[3].y);
+  out[2] = make_float4(in[0].z, in[1].z, in[2].z, in[3].z);
+  out[3] = make_float4(in[0].w, in[1].w, in[2].w, in[3].w);
+}
+
+// grid = (n/64, n/64); block = 256 threads.
+template <typename T>
+__global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt, const T* __restrict__ b, int n) {
+  using VT = typename VecOf<T>::type;
+  constexpr int V = VecOf<T>::V;
+  constexpr int MB = kTile / V;         // micro-blocks per tile side == 16-byte chunks per tile row
+  __shared__ VT tile[kTile * MB];        // output-ordered: tile[out_row][chunk], swizzled
+
+  const int in_row0 = blockIdx.y * kTile;   // rows of b  == columns of bt
+  const int in_col0 = blockIdx.x * kTile;   // cols of b  == rows of bt
+  const int tid = threadIdx.x;
+
+  // phase 1: micro-blocks, lanes along the input row (coalesced 128-bit loads)
+#pragma unroll
+  for (int mb = tid; mb < MB * MB; mb += 256) {
+    const int C = mb % MB;  // micro column (input cols C*V ..)
+    const int R = mb / MB;  // micro row    (input rows R*V ..)
+    VT in[V], out[V];
+#pragma unroll
+    for (int r = 0; r < V; ++r)
+      in[r] = *reinterpret_cast<const VT*>(b + static_cast<size_t>(in_row0 + R * V + r) * n + in_col0 + C * V);
+    transpose_micro(in, out);
+#pragma unroll
+    for (int r = 0; r < V; ++r) {
+      const int out_row = C * V + r;                 // row of the output tile
+      const int chunk = R ^ ((out_row / V) & 7);     // == R ^ (C & 7)
+      tile[out_row * MB + chunk] = out[r];
+    }
+  }
+  __syncthreads();
+
+  // phase 2: lanes along the output row (coalesced 128-bit stores)
+#pragma unroll
+  for (int v = tid; v < kTile * MB; v += 256) {
+    const int out_row = v / MB;
+    const int chunk = v % MB;
+    const VT val = tile[out_row * MB + (chunk ^ ((out_row / V) & 7))];
+    *reinterpret_cast<VT*>(bt + static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V) = val;
+  }
+}
+
+// Any n: 32x32 tile, scalar accesses, +1 padding.  block = (32, 8).
+template <typename T>
+__global__ void __launch_bounds__(256) transpose_generic_kernel(T* __restrict__ bt, const T* __restrict__ b, int n) {
+  __shared__ T tile[32][33];
+  const int x = blockIdx.x * 32 + threadIdx.x;
+#pragma unroll
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int y = blockIdx.y * 32 + r;
+    if (x < n && y < n) tile[r][threadIdx.x] = b[static_cast<size_t>(y) * n + x];
+  }
+  __syncthreads();
+  const int ox = blockIdx.y * 32 + threadIdx.x;  // column of bt = row of b
+#pragma unroll
+  for (int r = threadIdx.y; r < 32; r += 8) {
+    const int oy = blockIdx.x * 32 + r;          // row of bt = column of b
+    if (ox < n && oy < n) bt[static_cast<size_t>(oy) * n + ox] = tile[threadIdx.x][r];
+  }
+}
+
+// gene 7: bt[i][j] = b[j][i] for all j; i = iteration of the host loop.
+template <typename T>
+__global__ void __launch_bounds__(256) transpose_row_kernel(T* __restrict__ bt, const T* __restrict__ b, int n, IterRef iter) {
+  const int i = iter.off + (iter.base ? *iter.base : 0);
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) bt[static_cast<size_t>(i) * n + j] = b[static_cast<size_t>(j) * n + i];
+}
+
+}  // namespace
+
+template <typename T>
+cudaError_t launch_transpose(T* bt, const T* b, int n, cudaStream_t stream) {
+  if (n % kTile == 0) {
+    dim3 grid(n / kTile, n / kTile);
+    transpose_tile_kernel<T><<<grid, 256, 0, stream>>>(bt, b, n);
+  } else {
+    dim3 grid((n + 31) / 32, (n + 31) / 32);
+    transpose_generic_kernel<T><<<grid, dim3(32, 8), 0, stream>>>(bt, b, n);
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_transpose_row(T* bt, const T* b, int n, IterRef iter, cudaStream_t stream) {
+  const int threads = n < 256 ? ((n + 31) / 32) * 32 : 256;
+  transpose_row_kernel<T><<<(n + threads - 1) / threads, threads, 0, stream>>>(bt, b, n, iter);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_transpose<double>(double*, const double*, int, cudaStream_t);
+template cudaError_t launch_transpose<float>(float*, const float*, int, cudaStream_t);
+template cudaError_t launch_transpose_row<double>(double*, const double*, int, IterRef, cudaStream_t);
+template cudaError_t launch_transpose_row<float>(float*, const float*, int, IterRef, cudaStream_t);
+
+}  // namespace mmx

@@ -1,0 +1,350 @@
+"""Parity of the CUDA path (through the C ABI) against the oracle.  Run with -m gpu on a B200.
+
+Bars (BASELINE.json north_star):
+  * integer / index / data-movement work (fills, transpose, feasibility, plan): bit-exact;
+  * STRICT numerics: c and the checksum bit-exact for every N and both dtypes;
+  * FAST numerics: bit-exact for FP64 at N = 2^p (every partial sum is exact);
+    otherwise |delta_ij| <= tol * sum_k |a_ik| |bt_jk| with tol = 1e-12 (FP64) / 1e-6 (FP32),
+    measured against the float64-exact product of the same inputs (option i).
+"""
+import numpy as np
+import pytest
+
+from oracle import cpu
+from paper_1806_01430_b200 import capi
+
+pytestmark = pytest.mark.gpu
+
+TOL = {capi.F64: 1e-12, capi.F32: 1e-6}
+SIZES = [64, 256, 300, 257, 33]   # tile multiple, fixture size, even non-multiple, odd, tiny odd
+
+
+def bits_equal(x, y):
+    u = np.uint64 if x.dtype == np.float64 else np.uint32
+    return np.array_equal(np.ascontiguousarray(x).view(u), np.ascontiguousarray(y).view(u))
+
+
+def rand(n, dtype, seed):
+    rs = np.random.RandomState(seed)
+    return rs.uniform(-1.0, 1.0, (n, n)).astype(np.float64 if dtype == capi.F64 else np.float32)
+
+
+def oracle_matmul(a, bt, c, dtype, i0=0, i1=None):
+    """The CPU loop (k ascending, mul then add) on explicit operands."""
+    n = a.shape[0]
+    app = cpu.App(n, dtype, threads=8)
+    app.a[:], app.bt[:], app.c[:] = a, bt, c
+    app.run_nest(4, i0, n if i1 is None else i1)
+    return app.c
+
+
+def normwise_ok(got, a, bt, c0, dtype):
+    exact = c0.astype(np.float64) + a.astype(np.float64) @ bt.astype(np.float64).T
+    bound = TOL[dtype] * (np.abs(c0).astype(np.float64) + np.abs(a).astype(np.float64) @ np.abs(bt).astype(np.float64).T)
+    err = np.abs(got.astype(np.float64) - exact)
+    if dtype == capi.F32:  # the result itself is rounded to float: allow half an ulp of it
+        bound = bound + np.abs(exact) * 2.0 ** -24
+    return bool((err <= bound).all()), float((err / np.maximum(bound, 1e-300)).max())
+
+
+# ---- fills, transpose: bit-exact -------------------------------------------------------------
+
+@pytest.mark.parametrize("dtype", [capi.F64, capi.F32])
+@pytest.mark.parametrize("n", SIZES + [1000, 1023])
+def test_fill_nests_bit_exact(n, dtype):
+    ref = cpu.App(n, dtype)
+    for nest in range(3):
+        ref.run_nest(nest)
+    with capi.Context(n=n, dtype=dtype) as ctx:
+        for gene, arr, want in ((0, capi.ARRAY_A, ref.a), (2, capi.ARRAY_B, ref.b), (4, capi.ARRAY_C, ref.c)):
+            ctx.upload(arr, np.full((n, n), np.nan))
+            ctx.run_loop(gene)
+            assert bits_equal(ctx.fetch(arr), want), (gene, n)
+
+
+@pytest.mark.parametrize("dtype", [capi.F64, capi.F32])
+@pytest.mark.parametrize("n", [64, 300, 33])
+def test_fill_rows_touch_only_their_row(n, dtype):
+    ref = cpu.App(n, dtype)
+    for nest in range(3):
+        ref.run_nest(nest)
+    with capi.Context(n=n, dtype=dtype) as ctx:
+        for gene, arr, want in ((1, capi.ARRAY_A, ref.a), (3, capi.ARRAY_B, ref.b), (5, capi.ARRAY_C, ref.c)):
+            ctx.upload(arr, np.full((n, n), np.nan))
+            rows = [0, n // 2, n - 1]
+            for i in rows:
+                ctx.run_loop(gene, i)
+            got = ctx.fetch(arr)
+            for i in range(n):
+                if i in rows:
+                    assert bits_equal(got[i], want[i]), (gene, i)
+                else:
+                    assert np.isnan(got[i]).all(), (gene, i)
+
+
+@pytest.mark.parametrize("dtype", [capi.F64, capi.F32])
+@pytest.mark.parametrize("n", SIZES + [128, 1024])
+def test_transpose_bit_exact(n, dtype):
+    b = rand(n, dtype, 1)
+    b[0, 0] = -0.0
+    b[n - 1, 0] = np.inf
+    with capi.Context(n=n, dtype=dtype) as ctx:
+        ctx.upload(capi.ARRAY_B, b)
+        ctx.upload(capi.ARRAY_BT, np.full((n, n), np.nan))
+        ctx.run_loop(6)
+        assert bits_equal(ctx.fetch(capi.ARRAY_BT), b.T)
+        ctx.upload(capi.ARRAY_BT, np.full((n, n), np.nan))
+        for i in (0, 1, n - 1):
+            ctx.run_loop(7, i)
+        got = ctx.fetch(capi.ARRAY_BT)
+        for i in (0, 1, n - 1):
+            assert bits_equal(got[i], b.T[i])
+        assert np.isnan(got[2:n - 1]).all() if n > 3 else True
+
+
+# ---- the contraction: gene 8 --------------------------------------------------------------
+
+@pytest.mark.parametrize("dtype", [capi.F64, capi.F32])
+@pytest.mark.parametrize("n", SIZES)
+def test_matmul_strict_is_bit_exact_on_random_inputs(n, dtype):
+    a, bt, c0 = rand(n, dtype, 2), rand(n, dtype, 3), rand(n, dtype, 4)
+    c0[0, 0] = -0.0
+    want = oracle_matmul(a, bt, c0, dtype)
+    with capi.Context(n=n, dtype=dtype, numerics=capi.STRICT) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        ctx.run_loop(8)
+        assert bits_equal(ctx.fetch(capi.ARRAY_C), want)
+
+
+@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("dtype", [capi.F64, capi.F32])
+@pytest.mark.parametrize("n", SIZES)
+def test_matmul_fast_within_tolerance_on_random_inputs(n, dtype, variant):
+    a, bt, c0 = rand(n, dtype, 5), rand(n, dtype, 6), rand(n, dtype, 7)
+    with capi.Context(n=n, dtype=dtype, matmul_variant=variant) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        ctx.run_loop(8)
+        ok, worst = normwise_ok(ctx.fetch(capi.ARRAY_C), a, bt, c0, dtype)
+        assert ok, f"worst error / bound = {worst}"
+
+
+@pytest.mark.parametrize("n", [64, 256, 300])
+def test_dmma_and_simt_fast_agree_bitwise(n):
+    # both keep one k-ascending FMA chain per element
+    a, bt, c0 = rand(n, capi.F64, 8), rand(n, capi.F64, 9), rand(n, capi.F64, 10)
+    outs = []
+    for variant in (1, 2):
+        with capi.Context(n=n, matmul_variant=variant) as ctx:
+            ctx.upload(capi.ARRAY_A, a)
+            ctx.upload(capi.ARRAY_BT, bt)
+            ctx.upload(capi.ARRAY_C, c0)
+            ctx.run_loop(8)
+            outs.append(ctx.fetch(capi.ARRAY_C))
+    assert bits_equal(outs[0], outs[1])
+
+
+# ---- reduction-style loops: genes 9, 10, 11 -------------------------------------------------
+
+@pytest.mark.parametrize("numerics", [capi.FAST, capi.STRICT])
+@pytest.mark.parametrize("dtype", [capi.F64, capi.F32])
+@pytest.mark.parametrize("n", [64, 300, 33])
+def test_gemv_row_and_dot(n, dtype, numerics):
+    a, bt, c0 = rand(n, dtype, 11), rand(n, dtype, 12), rand(n, dtype, 13)
+    want = oracle_matmul(a, bt, c0, dtype)
+    with capi.Context(n=n, dtype=dtype, numerics=numerics) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        rows = [0, n - 1]
+        for i in rows:
+            ctx.run_loop(9, i)                       # whole row i
+        cells = [(1, 0), (1, n - 1), (n // 2, n // 3)]
+        for i, j in cells:
+            ctx.run_loop(10, i, j)                   # single element
+        got = ctx.fetch(capi.ARRAY_C)
+    touched = np.zeros((n, n), bool)
+    touched[rows] = True
+    for i, j in cells:
+        touched[i, j] = True
+    assert bits_equal(got[~touched], c0[~touched])   # nothing else moved
+    if numerics == capi.STRICT:
+        assert bits_equal(got[touched], want[touched])
+    else:
+        exact = c0.astype(np.float64) + a.astype(np.float64) @ bt.astype(np.float64).T
+        bound = TOL[dtype] * (np.abs(c0) + np.abs(a).astype(np.float64) @ np.abs(bt).astype(np.float64).T)
+        if dtype == capi.F32:
+            bound = bound + np.abs(exact) * 2.0 ** -24
+        assert (np.abs(got.astype(np.float64) - exact)[touched] <= bound[touched]).all()
+
+
+@pytest.mark.parametrize("numerics", [capi.FAST, capi.STRICT])
+@pytest.mark.parametrize("dtype", [capi.F64, capi.F32])
+@pytest.mark.parametrize("n", [64, 300, 1025, 2500])
+def test_trace(n, dtype, numerics):
+    c = rand(n, dtype, 14)
+    app = cpu.App(n, dtype)
+    app.c[:] = c
+    want = app.run_nest(5)
+    with capi.Context(n=n, dtype=dtype, numerics=numerics) as ctx:
+        ctx.upload(capi.ARRAY_C, c)
+        got = ctx.run_loop(11)
+    if numerics == capi.STRICT:
+        assert got == want
+    else:
+        assert abs(got - float(np.trace(c.astype(np.float64)))) <= TOL[dtype] * float(np.abs(np.diag(c)).sum()) + abs(want) * 2.0 ** -24
+
+
+# ---- whole individuals through mmx_measure --------------------------------------------------
+
+MIXED = [
+    "101010101001",  # six nests on the GPU: 0 B up, 8 B down
+    "001010101001",  # init-a on the CPU
+    "101010001001",  # transpose on the CPU
+    "101010101000",  # trace on the CPU (diagonal only comes back)
+    "000000001001",  # only matmul + trace on the GPU
+    "101010100001",  # matmul on the CPU, trace on the GPU
+    "000000000000",  # baseline: all CPU
+    "100000000000",  # the replay fixture's optimum shape
+]
+INNER = ["010000000000", "000100000000", "000001000000", "000000010000", "000000000100", "000000000010",
+         "010101010101", "010101010011"]
+
+
+@pytest.mark.parametrize("dtype", [capi.F64, capi.F32])
+@pytest.mark.parametrize("genome", MIXED + INNER)
+def test_individuals_match_the_cpu_program_bit_for_bit(genome, dtype):
+    n = 64  # power of two: FAST is exact in FP64; FP32 at this size is exact too (appendix A)
+    ref = cpu.App(n, dtype).run()
+    for batching in (1, 0):
+        with capi.Context(n=n, dtype=dtype, launch_batching=batching, timeout_s=60) as ctx:
+            out = ctx.measure(genome)
+            assert out.status == capi.MEASURED and out.time_s > 0 and out.wall_cost_s >= out.time_s * 0.5
+            st = ctx.stats()
+            assert st.checksum == ref.checksum == 0.0
+            p = capi.plan(genome, n, dtype)
+            assert (st.h2d_bytes, st.d2h_bytes, st.kernel_launches) == (p.h2d_bytes, p.d2h_bytes, p.kernel_launches)
+            assert bits_equal(ctx.fetch(capi.ARRAY_C), ref.c), genome
+
+
+@pytest.mark.parametrize("numerics", [capi.FAST, capi.STRICT])
+@pytest.mark.parametrize("genome", ["101010101001", "101010100101", "010101010011", "000000001000"])
+def test_individuals_at_awkward_sizes(genome, numerics):
+    for n, dtype in ((100, capi.F64), (100, capi.F32), (33, capi.F64)):
+        ref = cpu.App(n, dtype).run()
+        with capi.Context(n=n, dtype=dtype, numerics=numerics, timeout_s=60) as ctx:
+            out = ctx.measure(genome)
+            assert out.status == capi.MEASURED
+            got = ctx.fetch(capi.ARRAY_C)
+            if numerics == capi.STRICT:
+                assert bits_equal(got, ref.c)
+                assert ctx.stats().checksum == ref.checksum
+            else:
+                ok, worst = normwise_ok(got, ref.a, ref.bt, np.zeros_like(ref.c), dtype)
+                assert ok, worst
+
+
+def test_fixture_size_matches_golden_hash(golden):
+    g = golden("fixture_n256.json")
+    with capi.Context(n=256) as ctx:
+        assert ctx.measure("101010101001").status == capi.MEASURED
+        for name, arr in (("a", capi.ARRAY_A), ("b", capi.ARRAY_B), ("c", capi.ARRAY_C), ("bt", capi.ARRAY_BT)):
+            assert f"{cpu.fnv1a64(ctx.fetch(arr)):016x}" == g["arrays"][name]["fnv1a64"], name
+        assert ctx.stats().checksum == 0.0
+
+
+def test_infeasible_genomes_are_compile_errors_with_zero_gpu_work(golden):
+    verdict = golden("feasibility_mockacc.txt").strip()
+    with capi.Context(n=64) as ctx:
+        for g in ("110000000000", "000000001100", "000000001010", "111111111111", "110110101101"):
+            mask = sum(1 << k for k, ch in enumerate(g) if ch == "1")
+            assert verdict[mask] == "0"
+            out = ctx.measure(g)
+            assert (out.status, out.time_s) == (capi.COMPILE_ERROR, 0.0)
+
+
+def test_wrong_length_is_an_error_not_an_outcome():
+    with capi.Context(n=64) as ctx:
+        with pytest.raises(capi.MmxError) as e:
+            ctx.measure("1010")
+        assert e.value.code == capi.E_LENGTH
+        assert "length" in str(e.value)
+
+
+def test_timeout_scores_the_budget():
+    # CPU matmul at N=1024 takes ~1 s single-threaded; the budget is 50 ms
+    with capi.Context(n=1024, timeout_s=0.05) as ctx:
+        out = ctx.measure("101010100001")
+        assert (out.status, out.time_s) == (capi.TIMEOUT, 0.05)
+        assert out.wall_cost_s < 2.0
+        # the k-loop genome needs N^2 = 1M launches: also over budget, and it must stop early
+        out = ctx.measure("101010000011")
+        assert (out.status, out.time_s) == (capi.TIMEOUT, 0.05)
+        assert out.wall_cost_s < 2.0
+        # and the slot is still usable afterwards
+        assert ctx.measure("101010101001").status == capi.MEASURED
+
+
+def test_repetitions_take_the_median_and_warmup_is_untimed():
+    with capi.Context(n=256, repetitions=5, warmup=2) as ctx:
+        out = ctx.measure("101010101001")
+        assert out.status == capi.MEASURED and 0 < out.time_s < 0.01
+        assert out.wall_cost_s >= 5 * out.time_s
+
+
+def test_batch_is_aligned_with_its_input_and_uses_every_slot():
+    genomes = ["101010101001", "110000000000", "000000000000", "101010101000", "001010101001", "101010101001"]
+    with capi.Context(n=128, num_slots=2, devices=[0, 0]) as ctx:
+        assert ctx.num_slots == 2 and ctx.gene_length == 12
+        outs = ctx.measure_batch(genomes)
+        assert [o.status for o in outs] == [0, 1, 0, 0, 0, 0]
+        assert outs[1].time_s == 0.0
+        assert outs[2].time_s > outs[0].time_s  # CPU matmul is slower than the GPU one
+        assert ctx.measure_batch([]) == []
+
+
+def test_host_threads_do_not_change_results():
+    ref = cpu.App(96).run()
+    with capi.Context(n=96, host_threads=4) as ctx:
+        assert ctx.measure("000000000000").status == capi.MEASURED
+        assert bits_equal(ctx.fetch(capi.ARRAY_C), ref.c)
+
+
+# ---- BASELINE.json sizes: size-independent properties ----------------------------------------
+
+@pytest.mark.parametrize("variant", [1, 2])
+def test_n4096_fp64_equals_closed_form(variant):
+    n = 4096
+    with capi.Context(n=n, matmul_variant=variant) as ctx:
+        out = ctx.measure("101010101001")
+        assert out.status == capi.MEASURED
+        assert ctx.stats().checksum == 0.0   # the trace is exactly 0 for every N = 2^p (H7) ...
+        got = ctx.fetch(capi.ARRAY_C)
+        # ... so compare c itself: exact closed form, bit for bit
+        for r0 in range(0, n, 1024):
+            assert bits_equal(got[r0:r0 + 1024], cpu.closed_form_c(n, r0, r0 + 1024))
+        bt = ctx.fetch(capi.ARRAY_BT)
+        b = ctx.fetch(capi.ARRAY_B)
+        assert bits_equal(bt, b.T)            # transpose round trip
+        assert b[5, 3] == 2.0 / n and ctx.fetch(capi.ARRAY_A)[5, 3] == 8.0 / n
+
+
+def test_n4096_fp32_within_tolerance_and_linear():
+    n = 4096
+    with capi.Context(n=n, dtype=capi.F32) as ctx:
+        assert ctx.measure("101010101001").status == capi.MEASURED
+        got = ctx.fetch(capi.ARRAY_C).astype(np.float64)
+        exact = cpu.closed_form_c(n)  # the float inputs (i+j)/N, (i-j)/N are exact for N = 2^p
+        # sum_k |a_ik| |bt_jk| = sum_k (i+k)|k-j| / N^2 = (i * A_j + B_j) / N^2, computed exactly
+        k = np.arange(n, dtype=np.float64)
+        dist = np.abs(k[None, :] - k[:, None])            # |k - j|, indexed [j, k]
+        A, B = dist.sum(axis=1), (dist * k[None, :]).sum(axis=1)
+        bound = 1e-6 * (k[:, None] * A[None, :] + B[None, :]) / n ** 2
+        assert (np.abs(got - exact) <= bound + np.abs(exact) * 2.0 ** -24).all()
+        # linearity: running the matmul nest twice on the same c doubles it (c += a bt^T)
+        ctx.run_loop(8)
+        twice = ctx.fetch(capi.ARRAY_C).astype(np.float64)
+        assert (np.abs(twice - 2 * exact) <= 2 * bound + np.abs(exact) * 2.0 ** -22).all()
