@@ -387,7 +387,7 @@ REF_API int ref_run_ga_cb(std::size_t a, measure_cb cb, void* user, int m, int t
 
 // ---- Evaluator over a callback backend (evaluator.cpp:144-292) -------------------------
 
-REF_API void* ref_evaluator_create(std::size_t genes, measure_cb cb, void* user, int jobs,
+REF_API void* ref_evaluator_create_cb(std::size_t genes, measure_cb cb, void* user, int jobs,
                                    const char* cache_file) {
   try {
     auto* h = new RefEvaluator;

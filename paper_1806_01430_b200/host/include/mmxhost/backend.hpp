@@ -1,0 +1,104 @@
+// backend.hpp -- EvalBackend and its implementations.
+//
+// EvalBackend is THE drop-in boundary (/root/reference/proj/include/acctune/evaluator.hpp:19-24):
+// one call = one real measurement of one genome; backends carry no cache; measure() is called
+// concurrently from up to `jobs` threads on distinct genomes (evaluator.cpp:196-205).
+//
+//   SimBackend      times from a CostModel (evaluator.cpp:23-35) -- deterministic test double
+//   CallbackBackend scripted by a std::function (the reference tests' ScriptBackend, test_util.hpp:55-81)
+//   CudaBackend     the product: forwards to the C ABI (include/mmx.h); concurrent callers are
+//                   spread over the context's device slots
+#pragma once
+
+#include <atomic>
+#include <condition_variable>
+#include <cstddef>
+#include <functional>
+#include <mutex>
+#include <vector>
+
+#include "mmx.h"
+#include "mmxhost/evaluation.hpp"
+#include "mmxhost/sim_model.hpp"
+
+namespace mmxhost {
+
+class EvalBackend {
+ public:
+  virtual ~EvalBackend() = default;
+  virtual EvaluationOutcome measure(const Genome& genome) = 0;
+  virtual std::size_t gene_length() const = 0;
+};
+
+class SimBackend : public EvalBackend {
+ public:
+  explicit SimBackend(CostModel model) : model_(std::move(model)) {}
+  EvaluationOutcome measure(const Genome& genome) override;
+  std::size_t gene_length() const override { return model_.gene_length(); }
+  const CostModel& model() const { return model_; }
+
+ private:
+  CostModel model_;
+};
+
+class CallbackBackend : public EvalBackend {
+ public:
+  using Fn = std::function<EvaluationOutcome(const Genome&)>;
+  CallbackBackend(std::size_t gene_length, Fn fn) : gene_length_(gene_length), fn_(std::move(fn)) {}
+  EvaluationOutcome measure(const Genome& genome) override;
+  std::size_t gene_length() const override { return gene_length_; }
+
+  std::atomic<int> calls{0};
+  std::atomic<int> in_flight{0};
+  std::atomic<int> max_in_flight{0};
+
+ private:
+  std::size_t gene_length_;
+  Fn fn_;
+};
+
+struct CudaBackendConfig {
+  int n = 256;                 // fixtures/matmul.c:3
+  int dtype = MMX_F64;
+  int numerics = MMX_NUMERICS_FAST;
+  double timeout_s = 120.0;    // ToolchainConfig::timeout_s
+  int repetitions = 1;         // ToolchainConfig::repetitions
+  int warmup = 0;
+  std::vector<int> devices = {0};  // one slot per entry (repeat an ordinal for several slots on one GPU)
+  int host_threads = 1;
+  bool launch_batching = true;
+  int matmul_variant = 0;
+};
+
+// Throws ToolchainMissing when there is no CUDA device (there is no CPU fallback), ConfigError
+// on bad settings, WorkdirUnwritable-class Error on allocation failure.
+class CudaBackend : public EvalBackend {
+ public:
+  explicit CudaBackend(const CudaBackendConfig& config);
+  ~CudaBackend() override;
+  CudaBackend(const CudaBackend&) = delete;
+  CudaBackend& operator=(const CudaBackend&) = delete;
+
+  EvaluationOutcome measure(const Genome& genome) override;
+  std::size_t gene_length() const override;
+
+  // measure on a caller-chosen slot (MultiGpuEvaluator pins worker s to slot s)
+  EvaluationOutcome measure_on(int slot, const Genome& genome);
+  int num_slots() const;
+  mmx_ctx* handle() const { return ctx_; }
+  mmx_run_stats last_stats(int slot) const;
+
+ private:
+  int acquire_slot();
+  void release_slot(int slot);
+
+  mmx_ctx* ctx_ = nullptr;
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::vector<char> busy_;
+};
+
+// Turns a C ABI return code into the exception type the reference would throw.
+[[noreturn]] void throw_for_code(int code, const std::string& message);
+
+}  // namespace mmxhost

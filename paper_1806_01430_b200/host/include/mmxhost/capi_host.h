@@ -1,0 +1,97 @@
+/*
+ * capi_host.h -- C window onto the C++ host layer (namespace mmxhost), for Python tests and
+ * bench.py.  The C++ classes are the product API (they mirror the reference's acctune classes);
+ * this header only lets a ctypes caller drive them.  Return: >= 0 success, negative = error class
+ * (same numbering as oracle/ref_shim.cpp so both sides can be driven by one test).
+ */
+#ifndef MMXHOST_CAPI_H_
+#define MMXHOST_CAPI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MMXH_API __attribute__((visibility("default")))
+
+enum {
+  MMXH_E_ERROR = -1,
+  MMXH_E_LENGTH = -2,        /* GenomeLengthMismatch */
+  MMXH_E_TOOLCHAIN = -3,     /* ToolchainMissing */
+  MMXH_E_WORKDIR = -4,       /* WorkdirUnwritable */
+  MMXH_E_ZERO_FITNESS = -5,  /* ZeroTotalFitness */
+  MMXH_E_UNAVAILABLE = -6,   /* EvaluatorUnavailable */
+  MMXH_E_NONPOSITIVE = -7,   /* NonPositiveTime */
+  MMXH_E_CONFIG = -8,        /* ConfigError */
+  MMXH_E_NOCANDIDATES = -9,  /* NoCandidates */
+  MMXH_E_MODEL = -10         /* ModelError */
+};
+
+typedef struct mmxh_outcome {
+  int32_t status;
+  double time_s;
+  double wall_cost_s;
+} mmxh_outcome;
+
+/* callback backend: return 0 ok, -3 => ToolchainMissing is thrown, other negative => Error */
+typedef int (*mmxh_measure_cb)(const uint8_t* bits, size_t n, mmxh_outcome* out, void* user);
+
+typedef struct mmxh_ga_params {
+  int32_t population, generations;
+  double crossover_rate, mutation_rate;
+  uint64_t seed;
+  int32_t elite_count;
+} mmxh_ga_params;
+
+typedef struct mmxh_cuda_config {
+  int32_t n, dtype, numerics;
+  double timeout_s;
+  int32_t repetitions, warmup, host_threads, launch_batching, matmul_variant;
+  int32_t num_devices;
+  const int32_t* devices;
+} mmxh_cuda_config;
+
+MMXH_API const char* mmxh_last_error(void);
+
+/* sim model */
+MMXH_API int mmxh_model_time_all(const char* model_path, double* times, size_t count);
+MMXH_API int mmxh_exhaustive_best(const char* model_path, uint8_t* bits, size_t n, double* t);
+
+/* GA pieces */
+MMXH_API int mmxh_fitness_from_time(double t, double* f);
+MMXH_API int mmxh_assign_fitness(const int32_t* status, const double* time_s, size_t m, double* fitness);
+MMXH_API int mmxh_init_population(size_t a, int m, uint64_t seed, uint8_t* bits);
+MMXH_API int mmxh_breed(const uint8_t* bits, const double* fitness, size_t m, size_t a, double pc, double pm, int elite,
+                        uint64_t seed, uint64_t skip, uint8_t* next_bits);
+MMXH_API int mmxh_roulette(const double* fitness, size_t m, size_t count, uint64_t seed, int32_t* picks);
+MMXH_API int mmxh_mutate(const uint8_t* bits, size_t a, double pm, uint64_t seed, uint8_t* out);
+MMXH_API int mmxh_one_point_crossover(const uint8_t* p1, const uint8_t* p2, size_t a, uint64_t seed, uint8_t* c1, uint8_t* c2);
+MMXH_API int mmxh_rng_draws(uint64_t seed, int kind, uint64_t n_arg, size_t count, double* out, uint64_t* raw_out);
+
+/* evaluators: kind of backend chosen by the constructor used */
+MMXH_API void* mmxh_evaluator_create_sim(const char* model_path, int jobs, const char* cache_file);
+MMXH_API void* mmxh_evaluator_create_cb(size_t genes, mmxh_measure_cb cb, void* user, int jobs, const char* cache_file);
+/* MultiGpuEvaluator over a CudaBackend (jobs = number of device slots) */
+MMXH_API void* mmxh_evaluator_create_cuda(const mmxh_cuda_config* cfg, const char* cache_file);
+MMXH_API void mmxh_evaluator_destroy(void* h);
+MMXH_API int mmxh_evaluator_gene_length(void* h);
+MMXH_API int mmxh_evaluator_evaluate(void* h, const uint8_t* bits, size_t n, mmxh_outcome* out);
+MMXH_API int mmxh_evaluator_evaluate_all(void* h, const uint8_t* bits, size_t count, size_t n, mmxh_outcome* outs);
+MMXH_API int mmxh_evaluator_counters(void* h, uint64_t c4[4], double* elapsed_s);
+/* call counters of a callback backend: calls, max_in_flight */
+MMXH_API int mmxh_evaluator_cb_stats(void* h, int32_t out2[2]);
+
+/* run_ga over an evaluator handle; csv receives generations.csv text; returns its length */
+MMXH_API int mmxh_run_ga(void* evaluator, const mmxh_ga_params* params, char* csv, size_t csv_cap, uint8_t* best_bits,
+                         double* best_s, double* baseline_s);
+
+MMXH_API const char* mmxh_status_name(int status);
+/* nlohmann-compatible number formatting used by the cache writer */
+MMXH_API int mmxh_dump_number(double v, char* out, size_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,332 @@
+#include "mmxhost/capi_host.h"
+
+#include <cstring>
+#include <memory>
+#include <sstream>
+#include <string>
+
+#include "mmxhost/backend.hpp"
+#include "mmxhost/errors.hpp"
+#include "mmxhost/evaluator.hpp"
+#include "mmxhost/ga.hpp"
+#include "mmxhost/json_lite.hpp"
+#include "mmxhost/sim_model.hpp"
+
+using namespace mmxhost;
+
+namespace {
+
+thread_local std::string g_error;
+
+int classify(const std::exception& e) {
+  if (dynamic_cast<const GenomeLengthMismatch*>(&e)) return MMXH_E_LENGTH;
+  if (dynamic_cast<const ToolchainMissing*>(&e)) return MMXH_E_TOOLCHAIN;
+  if (dynamic_cast<const WorkdirUnwritable*>(&e)) return MMXH_E_WORKDIR;
+  if (dynamic_cast<const ZeroTotalFitness*>(&e)) return MMXH_E_ZERO_FITNESS;
+  if (dynamic_cast<const EvaluatorUnavailable*>(&e)) return MMXH_E_UNAVAILABLE;
+  if (dynamic_cast<const NonPositiveTime*>(&e)) return MMXH_E_NONPOSITIVE;
+  if (dynamic_cast<const ConfigError*>(&e)) return MMXH_E_CONFIG;
+  if (dynamic_cast<const NoCandidates*>(&e)) return MMXH_E_NOCANDIDATES;
+  if (dynamic_cast<const ModelError*>(&e)) return MMXH_E_MODEL;
+  return MMXH_E_ERROR;
+}
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    return f();
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return classify(e);
+  }
+}
+
+Genome genome_of(const std::uint8_t* bits, std::size_t n) { return Genome(Genome::Bits(bits, bits + n)); }
+
+int copy_out(const std::string& s, char* out, std::size_t cap) {
+  if (out != nullptr && cap > 0) {
+    const std::size_t n = s.size() < cap - 1 ? s.size() : cap - 1;
+    std::memcpy(out, s.data(), n);
+    out[n] = '\0';
+  }
+  return static_cast<int>(s.size());
+}
+
+struct Handle {
+  std::unique_ptr<Evaluator> ev;
+  CallbackBackend* cb = nullptr;  // owned by ev
+};
+
+mmxh_outcome pack(const EvaluationOutcome& o) { return {static_cast<std::int32_t>(o.status), o.time_s, o.wall_cost_s}; }
+
+std::filesystem::path path_or_empty(const char* p) { return p ? std::filesystem::path(p) : std::filesystem::path(); }
+
+}  // namespace
+
+extern "C" {
+
+MMXH_API const char* mmxh_last_error(void) { return g_error.c_str(); }
+
+MMXH_API int mmxh_model_time_all(const char* model_path, double* times, size_t count) {
+  return guarded([&] {
+    const CostModel m = load_model(model_path);
+    const std::size_t a = m.gene_length();
+    if (count != (std::size_t{1} << a)) return -1;
+    for (std::size_t mask = 0; mask < count; ++mask) {
+      Genome g = Genome::zeros(a);
+      for (std::size_t k = 0; k < a; ++k) g.set(k, (mask >> k) & 1u);
+      try {
+        times[mask] = model_time(m, g);
+      } catch (const SimulatedCompileError&) {
+        times[mask] = -1.0;
+      }
+    }
+    return static_cast<int>(a);
+  });
+}
+
+MMXH_API int mmxh_exhaustive_best(const char* model_path, uint8_t* bits, size_t n, double* t) {
+  return guarded([&] {
+    const OracleResult r = exhaustive_best(load_model(model_path));
+    if (r.genome.size() != n) return -1;
+    std::memcpy(bits, r.genome.bits().data(), n);
+    *t = r.time_s;
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_fitness_from_time(double t, double* f) {
+  return guarded([&] {
+    *f = fitness_from_time(t);
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_assign_fitness(const int32_t* status, const double* time_s, size_t m, double* fitness) {
+  return guarded([&] {
+    std::vector<Individual> pop(m);
+    for (std::size_t i = 0; i < m; ++i) {
+      pop[i].status = static_cast<IndividualStatus>(status[i]);
+      pop[i].time_s = time_s[i];
+    }
+    assign_fitness(pop);
+    for (std::size_t i = 0; i < m; ++i) fitness[i] = pop[i].fitness;
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_init_population(size_t a, int m, uint64_t seed, uint8_t* bits) {
+  return guarded([&] {
+    GAParams p;
+    p.population = m;
+    Rng rng(seed);
+    const auto pop = init_population(a, p, rng);
+    for (std::size_t i = 0; i < pop.size(); ++i) std::memcpy(bits + i * a, pop[i].bits().data(), a);
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_breed(const uint8_t* bits, const double* fitness, size_t m, size_t a, double pc, double pm, int elite,
+                        uint64_t seed, uint64_t skip, uint8_t* next_bits) {
+  return guarded([&] {
+    GAParams p;
+    p.population = static_cast<int>(m);
+    p.crossover_rate = pc;
+    p.mutation_rate = pm;
+    p.elite_count = elite;
+    std::vector<Individual> pop(m);
+    for (std::size_t i = 0; i < m; ++i) {
+      pop[i].genome = genome_of(bits + i * a, a);
+      pop[i].status = IndividualStatus::Measured;
+      pop[i].fitness = fitness[i];
+    }
+    Rng rng(seed);
+    for (std::uint64_t s = 0; s < skip; ++s) rng.raw();
+    const auto next = breed(pop, p, rng);
+    for (std::size_t i = 0; i < next.size(); ++i) std::memcpy(next_bits + i * a, next[i].genome.bits().data(), a);
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_roulette(const double* fitness, size_t m, size_t count, uint64_t seed, int32_t* picks) {
+  return guarded([&] {
+    std::vector<Individual> pop(m);
+    for (std::size_t i = 0; i < m; ++i) {
+      Genome::Bits b(32);
+      for (int k = 0; k < 32; ++k) b[static_cast<std::size_t>(k)] = (i >> k) & 1u;
+      pop[i].genome = Genome(std::move(b));
+      pop[i].fitness = fitness[i];
+    }
+    Rng rng(seed);
+    const auto sel = roulette_select(pop, count, rng);
+    for (std::size_t n = 0; n < sel.size(); ++n) {
+      std::int32_t v = 0;
+      for (int k = 0; k < 31; ++k) v |= static_cast<std::int32_t>(sel[n].bits()[static_cast<std::size_t>(k)]) << k;
+      picks[n] = v;
+    }
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_mutate(const uint8_t* bits, size_t a, double pm, uint64_t seed, uint8_t* out) {
+  return guarded([&] {
+    Rng rng(seed);
+    const Genome g = mutate(genome_of(bits, a), pm, rng);
+    std::memcpy(out, g.bits().data(), a);
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_one_point_crossover(const uint8_t* p1, const uint8_t* p2, size_t a, uint64_t seed, uint8_t* c1, uint8_t* c2) {
+  return guarded([&] {
+    Rng rng(seed);
+    const auto kids = one_point_crossover(genome_of(p1, a), genome_of(p2, a), rng);
+    std::memcpy(c1, kids.first.bits().data(), a);
+    std::memcpy(c2, kids.second.bits().data(), a);
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_rng_draws(uint64_t seed, int kind, uint64_t n_arg, size_t count, double* out, uint64_t* raw_out) {
+  return guarded([&] {
+    Rng rng(seed);
+    for (std::size_t i = 0; i < count; ++i) {
+      if (kind == 0) out[i] = rng.bit() ? 1.0 : 0.0;
+      else if (kind == 1) out[i] = rng.real01();
+      else if (kind == 2) out[i] = static_cast<double>(rng.index(n_arg));
+      else raw_out[i] = rng.raw();
+    }
+    return 0;
+  });
+}
+
+MMXH_API void* mmxh_evaluator_create_sim(const char* model_path, int jobs, const char* cache_file) {
+  try {
+    auto h = std::make_unique<Handle>();
+    h->ev = std::make_unique<Evaluator>(std::make_unique<SimBackend>(load_model(model_path)), jobs, path_or_empty(cache_file));
+    return h.release();
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return nullptr;
+  }
+}
+
+MMXH_API void* mmxh_evaluator_create_cb(size_t genes, mmxh_measure_cb cb, void* user, int jobs, const char* cache_file) {
+  try {
+    auto h = std::make_unique<Handle>();
+    auto backend = std::make_unique<CallbackBackend>(genes, [cb, user](const Genome& g) {
+      mmxh_outcome o{static_cast<std::int32_t>(EvalStatus::RuntimeError), 0.0, 0.0};
+      const int rc = cb(g.bits().data(), g.size(), &o, user);
+      if (rc == -3) throw ToolchainMissing("callback: toolchain missing");
+      if (rc < 0) throw Error("callback failed");
+      EvaluationOutcome out;
+      out.status = static_cast<EvalStatus>(o.status);
+      out.time_s = o.time_s;
+      out.wall_cost_s = o.wall_cost_s;
+      return out;
+    });
+    h->cb = backend.get();
+    h->ev = std::make_unique<Evaluator>(std::move(backend), jobs, path_or_empty(cache_file));
+    return h.release();
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return nullptr;
+  }
+}
+
+MMXH_API void* mmxh_evaluator_create_cuda(const mmxh_cuda_config* cfg, const char* cache_file) {
+  try {
+    CudaBackendConfig c;
+    c.n = cfg->n;
+    c.dtype = cfg->dtype;
+    c.numerics = cfg->numerics;
+    c.timeout_s = cfg->timeout_s;
+    c.repetitions = cfg->repetitions;
+    c.warmup = cfg->warmup;
+    c.host_threads = cfg->host_threads;
+    c.launch_batching = cfg->launch_batching != 0;
+    c.matmul_variant = cfg->matmul_variant;
+    c.devices.assign(cfg->devices, cfg->devices + cfg->num_devices);
+    auto h = std::make_unique<Handle>();
+    h->ev = std::make_unique<MultiGpuEvaluator>(std::make_unique<CudaBackend>(c), path_or_empty(cache_file));
+    return h.release();
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    // encode the class in the message prefix so a ctypes caller can tell "no device" apart
+    g_error = std::to_string(classify(e)) + ":" + g_error;
+    return nullptr;
+  }
+}
+
+MMXH_API void mmxh_evaluator_destroy(void* h) { delete static_cast<Handle*>(h); }
+
+MMXH_API int mmxh_evaluator_gene_length(void* h) { return static_cast<int>(static_cast<Handle*>(h)->ev->gene_length()); }
+
+MMXH_API int mmxh_evaluator_evaluate(void* h, const uint8_t* bits, size_t n, mmxh_outcome* out) {
+  return guarded([&] {
+    *out = pack(static_cast<Handle*>(h)->ev->evaluate(genome_of(bits, n)));
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_evaluator_evaluate_all(void* h, const uint8_t* bits, size_t count, size_t n, mmxh_outcome* outs) {
+  return guarded([&] {
+    std::vector<Genome> gs;
+    gs.reserve(count);
+    for (std::size_t i = 0; i < count; ++i) gs.push_back(genome_of(bits + i * n, n));
+    const auto os = static_cast<Handle*>(h)->ev->evaluate_all(gs);
+    for (std::size_t i = 0; i < count; ++i) outs[i] = pack(os[i]);
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_evaluator_counters(void* h, uint64_t c4[4], double* elapsed_s) {
+  return guarded([&] {
+    const EvalCounters c = static_cast<Handle*>(h)->ev->counters();
+    c4[0] = c.requests;
+    c4[1] = c.distinct;
+    c4[2] = c.cache_hits;
+    c4[3] = c.backend_calls;
+    *elapsed_s = c.elapsed_s;
+    return 0;
+  });
+}
+
+MMXH_API int mmxh_evaluator_cb_stats(void* h, int32_t out2[2]) {
+  auto* hd = static_cast<Handle*>(h);
+  if (hd->cb == nullptr) return -1;
+  out2[0] = hd->cb->calls.load();
+  out2[1] = hd->cb->max_in_flight.load();
+  return 0;
+}
+
+MMXH_API int mmxh_run_ga(void* evaluator, const mmxh_ga_params* params, char* csv, size_t csv_cap, uint8_t* best_bits,
+                         double* best_s, double* baseline_s) {
+  return guarded([&] {
+    auto* hd = static_cast<Handle*>(evaluator);
+    GAParams p;
+    p.population = params->population;
+    p.generations = params->generations;
+    p.crossover_rate = params->crossover_rate;
+    p.mutation_rate = params->mutation_rate;
+    p.seed = params->seed;
+    p.elite_count = params->elite_count;
+    const TuningResult r = run_ga(hd->ev->gene_length(), p, *hd->ev);
+    std::ostringstream s;
+    write_generation_csv(s, r);
+    std::memcpy(best_bits, r.best_genome.bits().data(), r.best_genome.size());
+    *best_s = r.best_time_s;
+    *baseline_s = r.baseline_s;
+    return copy_out(s.str(), csv, csv_cap);
+  });
+}
+
+MMXH_API const char* mmxh_status_name(int status) {
+  static thread_local std::string s;
+  s = std::string(to_string(static_cast<EvalStatus>(status)));
+  return s.c_str();
+}
+
+MMXH_API int mmxh_dump_number(double v, char* out, size_t cap) { return copy_out(json::dump_number(v), out, cap); }
+
+}  // extern "C"

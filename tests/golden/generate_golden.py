@@ -12,6 +12,7 @@ mockacc).  Everything written here is an output of the reference's own code:
                           fitness_from_time, assign_fitness vectors
   eval_cache_sample.jsonl the first lines Evaluator appends to its cache file
   rendered_best.c         render_variant(matmul.c, "100000000000")
+  models/*.json           copies of fixtures/models/*.json (input data of the runs above)
 """
 from __future__ import annotations
 
@@ -268,12 +269,21 @@ def gen_rendered(lib):
     (HERE / "rendered_all_nests.c").write_bytes(buf.value)
 
 
+def gen_models():
+    """The three cost-model fixtures are input DATA of the golden runs: keep a copy beside them."""
+    dst = HERE / "models"
+    dst.mkdir(exist_ok=True)
+    for name in ("matrix12", "separable", "coupled"):
+        (dst / f"{name}.json").write_bytes((REF / "fixtures" / "models" / f"{name}.json").read_bytes())
+
+
 def main():
     if not REF.is_dir():
         sys.exit("needs /root/reference (build container only)")
     subprocess.run(["make", "-C", str(ROOT / "oracle"), "-j8", "oracle", "ref"], check=True, capture_output=True)
     lib = load_ref()
     gen_fixture()
+    gen_models()
     gen_catalogue(lib)
     gen_model_times(lib)
     gen_ga_runs(lib)
