@@ -1,0 +1,324 @@
+#!/usr/bin/env python
+"""bench.py -- the matrix application under the all-nests-offloaded genome, N=4096 FP64 (BASELINE.json
+configs[1]), one process per GPU.
+
+A *step* is one individual: one full pass of the application (init a, init b, zero c, transpose,
+matmul, trace) under genome 101010101001 through the C ABI (`mmx_measure`, what the reference's
+EvalBackend::measure would call).  Metric: matrix-app GFLOP/s = 2 N^3 / time.
+
+  value   device-resident throughput: 2N^3 * steps / sum of the per-step CUDA-event times of the
+          whole individual (events recorded on the library's own stream), max over ranks
+  e2e     the same steps timed by the host clock around the C-ABI calls, barrier +
+          torch.cuda.synchronize() on both sides: includes planning, launches, the D2H of the checksum.
+          The program generates its own inputs (matmul.c:8-18), so for this genome the planner moves
+          0 bytes up and 8 bytes down per step; `e2e_mixed` adds a genome with host-produced operands.
+  roofline  dominant kernel (the FP64 contraction, gene 8) timed live with CUDA events
+  cpu_baseline  the oracle port (oracle/matmul_oracle.c) on this box's host cores, bounded sample
+
+`--impl reference` times the reference's CPU implementation of the same path (the oracle port of
+fixtures/matmul.c with runtime N; the fixture itself is hard-wired to N=256) on the host cores.
+With N > 1 GPUs every rank runs its own individuals (population sharding, no collective on the
+data path); value is the job total; scaling is weak.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+GENOME_ALL_NESTS = "101010101001"   # depth-0 loop of each of the six nests
+GENOME_MIXED = "001010101001"       # init-a on the CPU => a crosses the bus once per step
+
+
+def parse_args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ga", action="store_true", help="also run the GA search (M=12, T=12) with real timings")
+    return ap.parse_args()
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("LOCAL_RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region (B200_PROFILING.md recipe)."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.proc, self.lines = index, None, []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits", "-lms", "20"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._pump, daemon=True).start()
+        except OSError:
+            self.proc = None
+
+    def _pump(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        sm, smax, reasons = [], None, set()
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"), parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(n: int, dtype: int, cores: int) -> dict:
+    """The oracle port on the host cores: whole application, matmul nest sampled on its first rows."""
+    from oracle import cpu
+    flops = 2.0 * n ** 3
+    per_row_s = 2.0 * n * n / 2.0e9            # ~2 GFLOP/s per core, only to size the sample
+    rows = int(min(n, max(cores, (12.0 / per_row_s) * cores)))   # ~12 s of matmul work
+    r = cpu.time_app(n, dtype, cores, rows)
+    other = sum(v for k, v in r["seconds"].items() if k != "matmul")
+    total = other + r["seconds"]["matmul"] * n / r["matmul_rows"]
+    out = {"value": flops / total / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+           "sample": f"all six nests at N={n}; matmul nest timed on rows [0,{r['matmul_rows']}) of {n} and scaled "
+                     f"(every row costs the same 2N^2 flop); {cores} host threads, gcc -O2 -ffp-contract=off",
+           "app_seconds_scaled": total, "nest_seconds": r["seconds"]}
+    if cores > 1:   # the faithful single-thread figure (the reference program has no threading)
+        rows1 = int(min(n, max(1, 4.0 / per_row_s)))
+        r1 = cpu.time_app(n, dtype, 1, rows1)
+        t1 = sum(v for k, v in r1["seconds"].items() if k != "matmul") + r1["seconds"]["matmul"] * n / r1["matmul_rows"]
+        out["single_thread_value"] = flops / t1 / 1e9
+        out["single_thread_app_seconds_scaled"] = t1
+    return out
+
+
+def run_reference(args):
+    rank, _, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_1806_01430_b200 import build
+    build.build_oracle()
+    n, dtype = args.n, 0 if args.dtype == "f64" else 1
+    cores = os.cpu_count() or 1
+    from oracle import cpu
+    flops = 2.0 * n ** 3
+    per_row_s = 2.0 * n * n / 2.0e9
+    # each step: a bounded sample of one application pass (~4 s of matmul work over all threads)
+    rows = int(min(n, max(cores, (4.0 / per_row_s) * cores)))
+    times = []
+    for it in range(args.warmup + args.steps):
+        r = cpu.time_app(n, dtype, cores, rows)
+        t = sum(v for k, v in r["seconds"].items() if k != "matmul") + r["seconds"]["matmul"] * n / r["matmul_rows"]
+        if it >= args.warmup:
+            times.append(t)
+    ms = 1e3 * sum(times) / len(times)
+    value = flops / (ms * 1e-3) / 1e9
+    sample = (f"per step: all six nests at N={n}, matmul nest on rows [0,{rows}) of {n} scaled to the full nest; "
+              f"{cores} host threads; oracle port of fixtures/matmul.c (the fixture is fixed at N=256)")
+    line = {
+        "impl": "reference", "metric": "matrix_app_gflops", "value": value, "unit": "GFLOP/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (the program generates its own inputs)",
+        "config": {"workload": f"matrix app N={n} {args.dtype}, all six nests (reference CPU path)", "n": n},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def load_measured_peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        try:
+            return json.loads(p.read_text()), "measured"
+        except ValueError:
+            pass
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1806_01430_b200 import capi
+
+    rank, local_rank, world = dist_env()
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py needs a CUDA device: the product has no CPU fallback")
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    n, dtype = args.n, capi.F64 if args.dtype == "f64" else capi.F32
+    esz = 8 if dtype == capi.F64 else 4
+    flops = 2.0 * n ** 3
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    ctx = capi.Context(n=n, dtype=dtype, devices=[local_rank], timeout_s=600.0)
+    plan = capi.plan(GENOME_ALL_NESTS, n, dtype)
+
+    def step(genome):
+        out = ctx.measure(genome)
+        if out.status != capi.MEASURED:
+            raise SystemExit(f"step failed: status {capi.STATUS_NAMES[out.status]}: {ctx._lib.mmx_last_error(ctx._h).decode()}")
+        return out
+
+    for _ in range(max(3, args.warmup)):
+        step(GENOME_ALL_NESTS)
+    # every step rewrites a, b, c, bt: 4 x N^2 x E = 512 MiB at N=4096 FP64, larger than the 126 MB L2,
+    # so no explicit flush is needed between steps
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    barrier()
+    t0 = time.perf_counter()
+    device_s = 0.0
+    for _ in range(args.steps):
+        out = step(GENOME_ALL_NESTS)
+        device_s += out.time_s                      # CUDA-event time of the whole individual
+    barrier()
+    wall_s = time.perf_counter() - t0
+    checksum = ctx.stats().checksum
+    wall_s = max_over_ranks(wall_s)
+    device_s = max_over_ranks(device_s)
+
+    # a genome whose operand is produced on the host: the planner moves `a` up once per step
+    mixed = None
+    if rank == 0:
+        pm = capi.plan(GENOME_MIXED, n, dtype)
+        for _ in range(2):
+            step(GENOME_MIXED)
+        torch.cuda.synchronize()
+        t1 = time.perf_counter()
+        reps = max(3, args.steps // 4)
+        for _ in range(reps):
+            step(GENOME_MIXED)
+        torch.cuda.synchronize()
+        mixed = {"genome": GENOME_MIXED, "value": flops * reps / (time.perf_counter() - t1) / 1e9, "unit": "GFLOP/s",
+                 "h2d_bytes_per_step": int(pm.h2d_bytes), "d2h_bytes_per_step": int(pm.d2h_bytes),
+                 "note": "init-a runs on one host core inside the timed region, then a (N^2 E bytes) is copied from pinned memory"}
+
+    # roofline of the dominant kernel, measured live (CUDA events on the library's stream, L2 flushed)
+    roof = hbm_roof = None
+    if rank == 0:
+        peaks, peaks_kind = load_measured_peaks()
+        ms8 = ctx.time_loop(8, 5, True)
+        pipe_peak = capi.peak_probe(capi.PEAK_FP64_FMA if dtype == capi.F64 else capi.PEAK_FP32_FMA, local_rank)
+        ach = flops / (ms8 * 1e-3) / 1e12
+        share = ms8 * 1e-3 / (device_s / args.steps)
+        roof = {"bound": "tensor", "pipe": "fp64 (DMMA.8x8x4 via mma.sync)" if dtype == capi.F64 else "fp32 (FFMA)",
+                "kernel": "matmul_nt (gene 8)", "achieved": ach, "peak": pipe_peak, "unit": "TFLOP/s", "frac": ach / pipe_peak,
+                "traffic": None, "ms_per_launch": ms8, "share_of_step": share,
+                "peak_source": "FMA-issue peak of the same pipe measured in this run by csrc/peaks.cu "
+                               "(MEASURED_PEAKS.json carries only HBM and bf16 figures)"}
+        ms6 = ctx.time_loop(6, 10, True)
+        gb = 2.0 * esz * n * n / (ms6 * 1e-3) / 1e9
+        hbm_roof = {"bound": "hbm", "kernel": "transpose_tiled (gene 6)", "achieved": gb, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": gb / peaks["hbm_gbs"], "traffic": None, "peak_source": f"MEASURED_PEAKS.json ({peaks_kind})"}
+
+    # the sampler covers the timed region plus the (equally loaded) mixed-genome and roofline phases
+    clocks = sampler.stop()
+
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline(n, 0 if dtype == capi.F64 else 1, os.cpu_count() or 1)
+
+    ga = None
+    if rank == 0 and args.ga:
+        ga = run_ga_search(n, dtype, [local_rank])
+
+    if rank == 0:
+        ms_per_step = 1e3 * wall_s / args.steps
+        line = {
+            "metric": "matrix_app_gflops", "value": flops * args.steps * world / device_s / 1e9, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "data": "synthetic (the program generates its own inputs: a=(i+j)/N, b=(i-j)/N)",
+            "config": {"workload": f"matrix app N={n} {args.dtype}, genome {GENOME_ALL_NESTS} (all six loop nests offloaded)",
+                       "n": n, "genome": GENOME_ALL_NESTS, "individuals_per_step_per_gpu": 1,
+                       "l2": "working set 4*N^2*E per step exceeds L2; no flush needed"},
+            "e2e": {"value": flops * args.steps * world / wall_s / 1e9, "unit": "GFLOP/s",
+                    "h2d_bytes_per_step": int(plan.h2d_bytes), "d2h_bytes_per_step": int(plan.d2h_bytes),
+                    "note": "host clock around mmx_measure (plan + 6 launches + checksum D2H + sync); this genome has no host-side inputs"},
+            "e2e_mixed": mixed,
+            "gpu_launches": int(plan.kernel_launches) * args.steps,
+            "clocks": clocks, "roofline": roof, "roofline_hbm": hbm_roof, "cpu_baseline": base,
+            "checksum": checksum,
+        }
+        if ga is not None:
+            line["ga_search"] = ga
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def run_ga_search(n, dtype, devices, population=12, generations=12, seed=1, timeout_s=0.5):
+    """GA wall-time to best pattern with real CUDA-event timings (MultiGpuEvaluator over the C ABI)."""
+    from paper_1806_01430_b200 import hostapi as H
+    api = H.mine()
+    t0 = time.perf_counter()
+    with H.Evaluator.from_cuda(api, n=n, dtype=dtype, timeout_s=timeout_s, devices=tuple(devices)) as ev:
+        res = ev.run_ga(population=population, generations=generations, seed=seed)
+        c = ev.counters()
+    wall = time.perf_counter() - t0
+    rows = res["csv"].splitlines()[1:]
+    first_best = next(int(r.split(",")[0]) for r in rows if r.split(",")[3] == res["best_genome"])
+    return {"population": population, "generations": generations, "seed": seed, "timeout_s": timeout_s,
+            "wall_s": wall, "best_genome": res["best_genome"], "best_s": res["best_s"], "baseline_s": res["baseline_s"],
+            "speedup_vs_all_cpu_genome": res["baseline_s"] / res["best_s"], "generation_of_best": first_best,
+            "distinct": c["distinct"], "requests": c["requests"],
+            "note": "all-CPU baseline genome hits the timeout budget when N is large; then baseline_s = budget"}
+
+
+def main():
+    args = parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()
