@@ -132,9 +132,13 @@ def run_reference(args):
     cores = os.cpu_count() or 1
     from oracle import cpu
     flops = 2.0 * n ** 3
-    per_row_s = 2.0 * n * n / 2.0e9
-    # each step: a bounded sample of one application pass (~4 s of matmul work over all threads)
-    rows = int(min(n, max(cores, (4.0 / per_row_s) * cores)))
+    # calibrate the cost of one matmul row on this box, then size each step's sample so that the whole
+    # --steps/--warmup run stays within ~150 s (at most ~4 s of matmul per step)
+    cal_rows = min(n, 4 * cores)
+    cal = cpu.time_app(n, dtype, cores, cal_rows)
+    per_row_wall = max(cal["seconds"]["matmul"] / cal_rows, 1e-9)      # wall seconds per row with all threads busy
+    step_budget_s = min(4.0, 150.0 / max(1, args.steps + args.warmup))
+    rows = int(min(n, max(cores, step_budget_s / per_row_wall)))
     times = []
     for it in range(args.warmup + args.steps):
         r = cpu.time_app(n, dtype, cores, rows)

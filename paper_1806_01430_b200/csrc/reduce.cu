@@ -82,6 +82,63 @@ __global__ void __launch_bounds__(256) gemv_row_fast_kernel(T* __restrict__ c, c
   if (lane == 0) c[static_cast<size_t>(i) * n + j] += s;
 }
 
+// FAST, row fits in shared memory and is 16-byte aligned: persistent CTAs (2 per SM), each owning a
+// contiguous block of output columns j.  a[i][:] is staged once per CTA in shared memory (it would
+// otherwise be re-read from L1/L2 by every warp); all 8 warps then stream each bt row together --
+// a thread issues up to 8 independent 128-bit loads per row, two rows per iteration -- so the work
+// is balanced to within one row per CTA and the only global traffic is bt itself (E*N^2 bytes).
+template <typename T>
+__global__ void __launch_bounds__(256, 2) gemv_row_staged_kernel(T* __restrict__ c, const T* __restrict__ a,
+                                                                 const T* __restrict__ bt, int n, IterRef iter) {
+  using VT = typename V16<T>::type;
+  constexpr int W = V16<T>::W;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  VT* sa = reinterpret_cast<VT*>(smem_raw);                   // n / W vectors
+  __shared__ T partial[2][2][8];                              // [buffer][row of the pair][warp]
+  const int i = iter.off + (iter.base ? *iter.base : 0);
+  const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  const int nv = n / W;
+  const VT* av = reinterpret_cast<const VT*>(a + static_cast<size_t>(i) * n);
+  for (int v = tid; v < nv; v += 256) sa[v] = av[v];
+  __syncthreads();
+
+  const int j0 = static_cast<int>(static_cast<long long>(n) * blockIdx.x / gridDim.x);
+  const int j1 = static_cast<int>(static_cast<long long>(n) * (blockIdx.x + 1) / gridDim.x);
+  int buf = 0;
+  for (int j = j0; j < j1; j += 2, buf ^= 1) {
+    const bool two = j + 1 < j1;
+    const VT* r0 = reinterpret_cast<const VT*>(bt + static_cast<size_t>(j) * n);
+    const VT* r1 = reinterpret_cast<const VT*>(bt + static_cast<size_t>(two ? j + 1 : j) * n);
+    T s0 = 0, s1 = 0, t0 = 0, t1 = 0;
+    int v = tid;
+    for (; v + 768 < nv; v += 1024) {  // 4 vectors per row per thread in flight, two rows
+      const VT x0 = r0[v], x1 = r0[v + 256], x2 = r0[v + 512], x3 = r0[v + 768];
+      const VT y0 = r1[v], y1 = r1[v + 256], y2 = r1[v + 512], y3 = r1[v + 768];
+      const VT a0 = sa[v], a1 = sa[v + 256], a2 = sa[v + 512], a3 = sa[v + 768];
+      s0 = vdot(a0, x0, s0); t0 = vdot(a1, x1, t0); s0 = vdot(a2, x2, s0); t0 = vdot(a3, x3, t0);
+      s1 = vdot(a0, y0, s1); t1 = vdot(a1, y1, t1); s1 = vdot(a2, y2, s1); t1 = vdot(a3, y3, t1);
+    }
+    for (; v < nv; v += 256) {
+      const VT a0 = sa[v];
+      s0 = vdot(a0, r0[v], s0);
+      s1 = vdot(a0, r1[v], s1);
+    }
+    s0 = warp_sum(s0 + t0);
+    s1 = warp_sum(s1 + t1);
+    if (lane == 0) {
+      partial[buf][0][warp] = s0;
+      partial[buf][1][warp] = s1;
+    }
+    __syncthreads();  // one barrier per row pair; the partial buffers alternate
+    if (warp == 0 && lane < 2 && (lane == 0 || two)) {
+      T tot = 0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) tot += partial[buf][lane][w];
+      c[static_cast<size_t>(i) * n + j + lane] += tot;
+    }
+  }
+}
+
 // STRICT: block = 64 threads owns 64 columns j; k is walked in tiles of 64 staged in smem.
 template <typename T>
 __global__ void __launch_bounds__(64) gemv_row_strict_kernel(T* __restrict__ c, const T* __restrict__ a,
@@ -207,7 +264,19 @@ cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, 
     gemv_row_strict_kernel<T><<<(n + 63) / 64, 64, 0, stream>>>(c, a, bt, n, iter);
   } else {
     const bool vec_ok = n % V16<T>::W == 0;
-    gemv_row_fast_kernel<T><<<(n + 7) / 8, 256, 0, stream>>>(c, a, bt, n, iter, vec_ok);
+    const size_t row_bytes = static_cast<size_t>(n) * sizeof(T);
+    if (vec_ok && row_bytes <= 64 * 1024 && n >= 512) {
+      static bool configured = false;
+      if (!configured) {
+        cudaError_t e = cudaFuncSetAttribute(gemv_row_staged_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        if (e != cudaSuccess) return e;
+        configured = true;
+      }
+      const int grid = n / 2 < 2 * kNumSMs ? n / 2 : 2 * kNumSMs;
+      gemv_row_staged_kernel<T><<<grid, 256, row_bytes, stream>>>(c, a, bt, n, iter);
+    } else {
+      gemv_row_fast_kernel<T><<<(n + 7) / 8, 256, 0, stream>>>(c, a, bt, n, iter, vec_ok);
+    }
   }
   return cudaGetLastError();
 }
