@@ -227,8 +227,8 @@ MMX_API int mmx_upload_array(mmx_ctx* ctx, int slot, int array, const void* host
 MMX_API int mmx_run_loop(mmx_ctx* ctx, int slot, int gene, int i, int j, double* sum_out);
 
 /* Time `iters` launches of loop `gene` (iteration 0 for inner loops) with CUDA events on
- * the slot's stream; when flush_l2 != 0 a buffer larger than L2 is overwritten before every
- * timed launch (outside the event bracket).  ms_out receives the mean per launch. */
+ * the slot's stream; when flush_l2 != 0 a 256 MiB buffer (larger than the 126 MB L2) is read before
+ * every timed launch, outside the event bracket, so the cache holds only clean foreign lines.  ms_out receives the mean per launch. */
 MMX_API int mmx_time_loop(mmx_ctx* ctx, int slot, int gene, int iters, int flush_l2, double* ms_out);
 
 /* On-device peak probes (roofline denominators the driver file does not carry).

@@ -561,7 +561,7 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
   if (cfg->n < 1 || cfg->n > 65536 || (cfg->dtype != MMX_F64 && cfg->dtype != MMX_F32) ||
       (cfg->numerics != MMX_NUMERICS_FAST && cfg->numerics != MMX_NUMERICS_STRICT) || !(cfg->timeout_s > 0.0) ||
       cfg->repetitions < 1 || cfg->num_slots < 1 || cfg->num_slots > 64 || cfg->host_threads < 1 || cfg->warmup < 0 ||
-      cfg->matmul_variant < 0 || cfg->matmul_variant > 9) {
+      cfg->matmul_variant < 0 || cfg->matmul_variant > 31) {
     g_create_error = "invalid configuration value";
     return MMX_E_INVALID;
   }
@@ -752,10 +752,11 @@ MMX_API int mmx_time_loop(mmx_ctx* ctx, int slot, int gene, int iters, int flush
   if (flush_l2 && s.d_scrub == nullptr) {
     s.scrub_bytes = std::size_t{256} << 20;  // 256 MiB > 126 MB L2
     MMX_CUDA(ctx, cudaMalloc(&s.d_scrub, s.scrub_bytes));
+    MMX_CUDA(ctx, launch_scrub(s.d_scrub, s.scrub_bytes, s.stream));
   }
   double total = 0.0;
   for (int it = 0; it < iters; ++it) {
-    if (flush_l2) MMX_CUDA(ctx, launch_scrub(s.d_scrub, s.scrub_bytes, s.stream));
+    if (flush_l2) MMX_CUDA(ctx, launch_evict(s.d_scrub, s.scrub_bytes, s.stream));
     MMX_CUDA(ctx, cudaEventRecord(s.ev_begin, s.stream));
     MMX_CUDA(ctx, launch_gene_any(ctx, s, gene, IterRef{nullptr, 0}));
     MMX_CUDA(ctx, cudaEventRecord(s.ev_end, s.stream));

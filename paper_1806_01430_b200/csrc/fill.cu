@@ -146,6 +146,19 @@ __global__ void __launch_bounds__(256) scrub_kernel(uint4* p, size_t nvec) {
   for (size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec; v += stride)
     p[v] = make_uint4(0x9e3779b9u, 0x7f4a7c15u, 0xf39cc060u, 0x5cedc834u);
 }
+
+// Evict by READING a buffer larger than L2: the cache ends up full of clean lines, so the kernel
+// timed next pays for its own traffic only.  (Evicting by writing leaves up to 126 MB of dirty lines
+// whose write-back is then billed to the next kernel: a read-only GEMV measured 3.7 TB/s that way.)
+__global__ void __launch_bounds__(256) evict_kernel(const uint4* __restrict__ p, size_t nvec, uint4* sink) {
+  const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
+  unsigned acc = 0;
+  for (size_t v = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; v < nvec; v += stride) {
+    const uint4 x = p[v];
+    acc ^= x.x ^ x.y ^ x.z ^ x.w;
+  }
+  if (acc == 0x1234567u) sink[0] = make_uint4(acc, 0, 0, 0);  // practically never
+}
 }  // namespace
 
 cudaError_t launch_advance(int* counter, int delta, cudaStream_t stream) {
@@ -155,6 +168,11 @@ cudaError_t launch_advance(int* counter, int delta, cudaStream_t stream) {
 
 cudaError_t launch_scrub(void* p, std::size_t bytes, cudaStream_t stream) {
   scrub_kernel<<<kNumSMs * 8, 256, 0, stream>>>(static_cast<uint4*>(p), bytes / 16);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_evict(void* p, std::size_t bytes, cudaStream_t stream) {
+  evict_kernel<<<kNumSMs * 8, 256, 0, stream>>>(static_cast<const uint4*>(p), bytes / 16, static_cast<uint4*>(p));
   return cudaGetLastError();
 }
 

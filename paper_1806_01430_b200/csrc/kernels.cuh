@@ -50,8 +50,9 @@ template <typename T> cudaError_t launch_trace(T* sum, const T* c, int n, bool s
 // graph plumbing: *counter += delta
 cudaError_t launch_advance(int* counter, int delta, cudaStream_t stream);
 
-// L2 flush helper for benchmarking: overwrite `bytes` at p
+// L2 helpers for benchmarking: overwrite `bytes` at p / read them (evicts, leaves only clean lines)
 cudaError_t launch_scrub(void* p, std::size_t bytes, cudaStream_t stream);
+cudaError_t launch_evict(void* p, std::size_t bytes, cudaStream_t stream);
 
 // peak probes (peaks.cu); each returns the achieved rate through *value
 cudaError_t probe_peak(int kind, double* value);

@@ -321,49 +321,53 @@ matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const d
 //   * FULL tiles take a path with no bounds checks at all.
 // Each accumulator still sees k strictly ascending.
 // ---------------------------------------------------------------------------------------------
-constexpr int S2_STAGES = 4;
-
-template <typename T, bool STRICT, bool FULL>
-__global__ void __launch_bounds__(256, sizeof(T) == 4 ? 2 : 1)
+// TM x TN CTA tile, (TM/8)*(TN/8) threads; a warp always spans 8 tx x 4 ty so that each HALF-warp (the
+// unit a 128-bit LDS is split into) sees 2 distinct A rows and 8 distinct B rows.  Small CTAs (64x64 =
+// two warps) are the default: 6-7 of them share an SM, so one CTA's barrier or cp.async wait never
+// idles the FMA pipe -- the same effect that took the DMMA kernel from 29.5 to 33.6 TFLOP/s.
+// min-blocks hint: cap FP32 at 128 registers (16 warps per SM whatever the CTA size); FP64 needs ~250
+template <typename T, bool STRICT, bool FULL, int TM, int TN, int STAGES>
+__global__ void __launch_bounds__((TM / 8) * (TN / 8), (sizeof(T) == 4 ? 512 : 256) / ((TM / 8) * (TN / 8)))
 matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ bt, int n, int row0, int rows) {
   using VT = typename V16<T>::type;
   constexpr int W = V16<T>::W;           // elements per 16-byte chunk
   constexpr int LD = BK + W;             // padded row length (elements): +16 bytes
   constexpr int CPR = BK / W;            // chunks per row
-  constexpr int ITERS = BM * CPR / 256;  // chunks per thread per operand
+  constexpr int TX = TN / 8, TY = TM / 8, THREADS = TX * TY;
+  static_assert(TX % 8 == 0 && TY % 4 == 0, "a warp spans 8 tx x 4 ty");
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  T* As = reinterpret_cast<T*>(smem_raw);   // [S2_STAGES][BM][LD]
-  T* Bs = As + S2_STAGES * BM * LD;         // [S2_STAGES][BN][LD]
+  T* As = reinterpret_cast<T*>(smem_raw);   // [STAGES][TM][LD]
+  T* Bs = As + STAGES * TM * LD;            // [STAGES][TN][LD]
 
   const int tid = threadIdx.x;
-  // A warp covers 8 tx x 4 ty: each HALF-warp (the unit a 128-bit LDS is split into) then sees only
-  // 2 distinct A rows (32 B) and 8 distinct B rows (128 B).
   const int lane = tid % 32, warp = tid / 32;
-  const int tx = (warp % 2) * 8 + lane % 8, ty = (warp / 2) * 4 + lane / 8;
-  const int m_base = row0 + blockIdx.y * BM, n_base = blockIdx.x * BN;
+  constexpr int WX = TX / 8;                // warps along n
+  const int tx = (warp % WX) * 8 + lane % 8, ty = (warp / WX) * 4 + lane / 8;
+  const int m_base = row0 + blockIdx.y * TM, n_base = blockIdx.x * TN;
   const int m_limit = row0 + rows;
 
   auto issue_stage = [&](int stage, int k0) {
 #pragma unroll
-    for (int it = 0; it < ITERS; ++it) {
-      const int chunk = tid + it * 256;
+    for (int it = 0; it < TM * CPR / THREADS; ++it) {
+      const int chunk = tid + it * THREADS;
       const int row = chunk / CPR, kc = (chunk % CPR) * W;
-      const int ar = m_base + row, br = n_base + row;
-      if constexpr (FULL) {
-        cp_async16(As + (stage * BM + row) * LD + kc, a + static_cast<size_t>(ar) * n + k0 + kc, true);
-        cp_async16(Bs + (stage * BN + row) * LD + kc, bt + static_cast<size_t>(br) * n + k0 + kc, true);
-      } else {
-        const bool kin = k0 + kc < n;  // n % W == 0, so a chunk is all in or all out
-        const bool av = kin && ar < m_limit, bv = kin && br < n;
-        cp_async16(As + (stage * BM + row) * LD + kc, av ? a + static_cast<size_t>(ar) * n + k0 + kc : a, av);
-        cp_async16(Bs + (stage * BN + row) * LD + kc, bv ? bt + static_cast<size_t>(br) * n + k0 + kc : bt, bv);
-      }
+      const int ar = m_base + row;
+      const bool av = FULL || (k0 + kc < n && ar < m_limit);  // n % W == 0: a chunk is all in or all out
+      cp_async16(As + (stage * TM + row) * LD + kc, av ? a + static_cast<size_t>(ar) * n + k0 + kc : a, av);
+    }
+#pragma unroll
+    for (int it = 0; it < TN * CPR / THREADS; ++it) {
+      const int chunk = tid + it * THREADS;
+      const int row = chunk / CPR, kc = (chunk % CPR) * W;
+      const int br = n_base + row;
+      const bool bv = FULL || (k0 + kc < n && br < n);
+      cp_async16(Bs + (stage * TN + row) * LD + kc, bv ? bt + static_cast<size_t>(br) * n + k0 + kc : bt, bv);
     }
   };
 
   const int k_tiles = (n + BK - 1) / BK;
 #pragma unroll
-  for (int s = 0; s < S2_STAGES - 1; ++s) {
+  for (int s = 0; s < STAGES - 1; ++s) {
     if (s < k_tiles) issue_stage(s, s * BK);
     cp_async_commit();
   }
@@ -373,31 +377,31 @@ matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restr
   for (int r = 0; r < 8; ++r)
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int m = m_base + ty + 16 * r, j = n_base + tx + 16 * q;
+      const int m = m_base + ty + TY * r, j = n_base + tx + TX * q;
       acc[r][q] = (FULL || (m < m_limit && j < n)) ? c[static_cast<size_t>(m) * n + j] : static_cast<T>(0.0);
     }
 
   for (int t = 0; t < k_tiles; ++t) {
-    cp_async_wait<S2_STAGES - 2>();
+    cp_async_wait<STAGES - 2>();
     __syncthreads();
     {
-      const int nt = t + S2_STAGES - 1;
-      if (nt < k_tiles) issue_stage(nt % S2_STAGES, nt * BK);
+      const int nt = t + STAGES - 1;
+      if (nt < k_tiles) issue_stage(nt % STAGES, nt * BK);
       cp_async_commit();
     }
-    const T* Ac = As + ((t % S2_STAGES) * BM + ty) * LD;
-    const T* Bc = Bs + ((t % S2_STAGES) * BN + tx) * LD;
+    const T* Ac = As + ((t % STAGES) * TM + ty) * LD;
+    const T* Bc = Bs + ((t % STAGES) * TN + tx) * LD;
     // STRICT must not add zero-padded tail terms (x + 0*0 can flip the sign of a -0 accumulator)
     const int k_valid = (STRICT && !FULL) ? min(BK, n - t * BK) : BK;
 #pragma unroll
     for (int ks = 0; ks < BK; ks += W) {
       VT fa[8];
 #pragma unroll
-      for (int r = 0; r < 8; ++r) fa[r] = *reinterpret_cast<const VT*>(Ac + 16 * r * LD + ks);
+      for (int r = 0; r < 8; ++r) fa[r] = *reinterpret_cast<const VT*>(Ac + TY * r * LD + ks);
 #pragma unroll
       for (int q = 0; q < 8; q += 2) {
-        const VT fb0 = *reinterpret_cast<const VT*>(Bc + 16 * q * LD + ks);
-        const VT fb1 = *reinterpret_cast<const VT*>(Bc + 16 * (q + 1) * LD + ks);
+        const VT fb0 = *reinterpret_cast<const VT*>(Bc + TX * q * LD + ks);
+        const VT fb1 = *reinterpret_cast<const VT*>(Bc + TX * (q + 1) * LD + ks);
         const T* pa = reinterpret_cast<const T*>(fa);
         const T* pb0 = reinterpret_cast<const T*>(&fb0);
         const T* pb1 = reinterpret_cast<const T*>(&fb1);
@@ -419,27 +423,30 @@ matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restr
   for (int r = 0; r < 8; ++r)
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
-      const int m = m_base + ty + 16 * r, j = n_base + tx + 16 * q;
+      const int m = m_base + ty + TY * r, j = n_base + tx + TX * q;
       if (FULL || (m < m_limit && j < n)) c[static_cast<size_t>(m) * n + j] = acc[r][q];
     }
 }
 
-template <typename T, bool STRICT>
+template <typename T, bool STRICT, int TM, int TN, int STAGES>
 cudaError_t simt2_go(T* c, const T* a, const T* bt, int n, int row0, int rows, cudaStream_t stream) {
   constexpr int W = V16<T>::W;
-  const size_t smem = 2 * S2_STAGES * BM * (BK + W) * sizeof(T);
+  constexpr int THREADS = (TM / 8) * (TN / 8);
+  const size_t smem = static_cast<size_t>(STAGES) * (TM + TN) * (BK + W) * sizeof(T);
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(matmul_simt2_kernel<T, STRICT, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    cudaError_t e = cudaFuncSetAttribute(matmul_simt2_kernel<T, STRICT, true, TM, TN, STAGES>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e == cudaSuccess)
-      e = cudaFuncSetAttribute(matmul_simt2_kernel<T, STRICT, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      e = cudaFuncSetAttribute(matmul_simt2_kernel<T, STRICT, false, TM, TN, STAGES>,
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((n + BN - 1) / BN, (rows + BM - 1) / BM);
-  const bool full = n % BN == 0 && rows % BM == 0 && n % BK == 0;
-  if (full) matmul_simt2_kernel<T, STRICT, true><<<grid, 256, smem, stream>>>(c, a, bt, n, row0, rows);
-  else matmul_simt2_kernel<T, STRICT, false><<<grid, 256, smem, stream>>>(c, a, bt, n, row0, rows);
+  dim3 grid((n + TN - 1) / TN, (rows + TM - 1) / TM);
+  const bool full = n % TN == 0 && rows % TM == 0 && n % BK == 0;
+  if (full) matmul_simt2_kernel<T, STRICT, true, TM, TN, STAGES><<<grid, THREADS, smem, stream>>>(c, a, bt, n, row0, rows);
+  else matmul_simt2_kernel<T, STRICT, false, TM, TN, STAGES><<<grid, THREADS, smem, stream>>>(c, a, bt, n, row0, rows);
   return cudaGetLastError();
 }
 
@@ -480,7 +487,8 @@ template <>
 cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, int n, int row0, int rows, bool strict,
                                   int variant, cudaStream_t stream) {
   if (strict) {
-    if (n % 2 == 0 && variant != 1) return simt2_go<double, true>(c, a, bt, n, row0, rows, stream);
+    if (n % 2 == 0 && variant == 20) return simt2_go<double, true, 128, 128, 4>(c, a, bt, n, row0, rows, stream);
+    if (n % 2 == 0 && variant != 1) return simt2_go<double, true, 64, 64, 3>(c, a, bt, n, row0, rows, stream);
     return simt_go<double, true>(c, a, bt, n, row0, rows, stream);
   }
   if (n % 2 == 0) {
@@ -489,10 +497,15 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
       case 5: return dmma_go<32, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);   // 64x64
       case 6: return dmma_go<32, 3, 2, 2, 2, 2>(c, a, bt, n, row0, rows, stream);   // 32x32
       case 7: return dmma_go<32, 3, 2, 4, 8, 4>(c, a, bt, n, row0, rows, stream);   // 128x128, BK=32
+      case 8: return dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);   // 64x64, BK=16
+      case 9: return dmma_go<16, 4, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);   // 64x64, BK=16, 4 stages
+      case 10: return dmma_go<32, 2, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);  // 64x64, BK=32, 2 stages
+      case 11: return dmma_go<32, 3, 2, 2, 8, 4>(c, a, bt, n, row0, rows, stream);  // 128x64, 4 warps
+      case 12: return dmma_go<32, 3, 1, 4, 8, 2>(c, a, bt, n, row0, rows, stream);  // 64x64 as 1x4 warps of 64x16
+      case 13: return dmma_go<32, 3, 2, 2, 4, 8>(c, a, bt, n, row0, rows, stream);  // 64x128, 4 warps
       case 4:  // auto: the largest tile that still gives every SM work (N=256 would be a 2x2 grid of 128-tiles)
-        if (n <= 512) return dmma_go<32, 3, 2, 2, 2, 2>(c, a, bt, n, row0, rows, stream);
-        if (n <= 1536) return dmma_go<32, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);
-        return dmma_go<32, 3, 2, 4, 8, 4>(c, a, bt, n, row0, rows, stream);
+        if (n <= 1024) return dmma_go<32, 3, 2, 2, 2, 2>(c, a, bt, n, row0, rows, stream);
+        return dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);
       default: break;
     }
   }
@@ -505,8 +518,15 @@ cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int 
   // variant 1 keeps the first-generation kernel (k-major smem, register-staged) for A/B runs and
   // for n % 4 != 0, where rows are not 16-byte aligned
   if (variant != 1 && n % 4 == 0) {
-    if (strict) return simt2_go<float, true>(c, a, bt, n, row0, rows, stream);
-    return simt2_go<float, false>(c, a, bt, n, row0, rows, stream);
+    // FP32 is not barrier-bound (small CTAs measured 39.5-43.8 TFLOP/s against 45.6 for 128x128x4
+    // stages): it is limited by register-bank dispatch stalls and LDS issue, so the big tile stays.
+    // Small matrices still get the 64x64 tile so that N=256 is 16 CTAs, not 4.
+    if (strict) {
+      if (n <= 1024) return simt2_go<float, true, 64, 64, 4>(c, a, bt, n, row0, rows, stream);
+      return simt2_go<float, true, 128, 128, 4>(c, a, bt, n, row0, rows, stream);
+    }
+    if (variant == 22 || (variant != 20 && n <= 1024)) return simt2_go<float, false, 64, 64, 4>(c, a, bt, n, row0, rows, stream);
+    return simt2_go<float, false, 128, 128, 4>(c, a, bt, n, row0, rows, stream);
   }
   if (strict) return simt_go<float, true>(c, a, bt, n, row0, rows, stream);
   return simt_go<float, false>(c, a, bt, n, row0, rows, stream);

@@ -83,58 +83,68 @@ __global__ void __launch_bounds__(256) gemv_row_fast_kernel(T* __restrict__ c, c
 }
 
 // FAST, row fits in shared memory and is 16-byte aligned: persistent CTAs (2 per SM), each owning a
-// contiguous block of output columns j.  a[i][:] is staged once per CTA in shared memory (it would
-// otherwise be re-read from L1/L2 by every warp); all 8 warps then stream each bt row together --
-// a thread issues up to 8 independent 128-bit loads per row, two rows per iteration -- so the work
-// is balanced to within one row per CTA and the only global traffic is bt itself (E*N^2 bytes).
+// contiguous block of output columns j, so the work is balanced to within one row per CTA.
+// a[i][:] is staged once per CTA in shared memory (it would otherwise be re-read from L1/L2 by
+// every warp); all 8 warps stream each bt row together.  The first 8 vectors per thread of row j+1
+// are already in flight while row j is reduced, so the per-row barrier never drains the memory
+// pipeline; the only global traffic is bt itself (E*N^2 bytes).
+constexpr int GEMV_VPT = 8;
+
 template <typename T>
 __global__ void __launch_bounds__(256, 2) gemv_row_staged_kernel(T* __restrict__ c, const T* __restrict__ a,
                                                                  const T* __restrict__ bt, int n, IterRef iter) {
   using VT = typename V16<T>::type;
   constexpr int W = V16<T>::W;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  VT* sa = reinterpret_cast<VT*>(smem_raw);                   // n / W vectors
-  __shared__ T partial[2][2][8];                              // [buffer][row of the pair][warp]
+  VT* sa = reinterpret_cast<VT*>(smem_raw);  // n / W vectors
+  __shared__ T partial[2][8];                // [buffer][warp]
   const int i = iter.off + (iter.base ? *iter.base : 0);
   const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
   const int nv = n / W;
   const VT* av = reinterpret_cast<const VT*>(a + static_cast<size_t>(i) * n);
   for (int v = tid; v < nv; v += 256) sa[v] = av[v];
-  __syncthreads();
 
   const int j0 = static_cast<int>(static_cast<long long>(n) * blockIdx.x / gridDim.x);
   const int j1 = static_cast<int>(static_cast<long long>(n) * (blockIdx.x + 1) / gridDim.x);
-  int buf = 0;
-  for (int j = j0; j < j1; j += 2, buf ^= 1) {
-    const bool two = j + 1 < j1;
-    const VT* r0 = reinterpret_cast<const VT*>(bt + static_cast<size_t>(j) * n);
-    const VT* r1 = reinterpret_cast<const VT*>(bt + static_cast<size_t>(two ? j + 1 : j) * n);
-    T s0 = 0, s1 = 0, t0 = 0, t1 = 0;
-    int v = tid;
-    for (; v + 768 < nv; v += 1024) {  // 4 vectors per row per thread in flight, two rows
-      const VT x0 = r0[v], x1 = r0[v + 256], x2 = r0[v + 512], x3 = r0[v + 768];
-      const VT y0 = r1[v], y1 = r1[v + 256], y2 = r1[v + 512], y3 = r1[v + 768];
-      const VT a0 = sa[v], a1 = sa[v + 256], a2 = sa[v + 512], a3 = sa[v + 768];
-      s0 = vdot(a0, x0, s0); t0 = vdot(a1, x1, t0); s0 = vdot(a2, x2, s0); t0 = vdot(a3, x3, t0);
-      s1 = vdot(a0, y0, s1); t1 = vdot(a1, y1, t1); s1 = vdot(a2, y2, s1); t1 = vdot(a3, y3, t1);
+
+  auto prefetch = [&](VT (&dst)[GEMV_VPT], int j) {
+    const VT* r = reinterpret_cast<const VT*>(bt + static_cast<size_t>(j) * n);
+#pragma unroll
+    for (int q = 0; q < GEMV_VPT; ++q) {
+      const int v = tid + q * 256;
+      if (v < nv) dst[q] = r[v];
     }
-    for (; v < nv; v += 256) {
-      const VT a0 = sa[v];
-      s0 = vdot(a0, r0[v], s0);
-      s1 = vdot(a0, r1[v], s1);
+  };
+  auto reduce_row = [&](const VT (&row)[GEMV_VPT], int j, int buf) {
+    T s0 = 0, s1 = 0;
+#pragma unroll
+    for (int q = 0; q < GEMV_VPT; q += 2) {
+      const int v = tid + q * 256;
+      if (v < nv) s0 = vdot(sa[v], row[q], s0);
+      if (v + 256 < nv) s1 = vdot(sa[v + 256], row[q + 1], s1);
     }
-    s0 = warp_sum(s0 + t0);
-    s1 = warp_sum(s1 + t1);
-    if (lane == 0) {
-      partial[buf][0][warp] = s0;
-      partial[buf][1][warp] = s1;
-    }
-    __syncthreads();  // one barrier per row pair; the partial buffers alternate
-    if (warp == 0 && lane < 2 && (lane == 0 || two)) {
+    const VT* r = reinterpret_cast<const VT*>(bt + static_cast<size_t>(j) * n);
+    for (int v = tid + GEMV_VPT * 256; v < nv; v += 256) s0 = vdot(sa[v], r[v], s0);  // rows longer than 2048 vectors
+    s0 = warp_sum(s0 + s1);
+    if (lane == 0) partial[buf][warp] = s0;
+    __syncthreads();  // one barrier per row; the partial buffers alternate
+    if (tid == 0) {
       T tot = 0;
 #pragma unroll
-      for (int w = 0; w < 8; ++w) tot += partial[buf][lane][w];
-      c[static_cast<size_t>(i) * n + j + lane] += tot;
+      for (int w = 0; w < 8; ++w) tot += partial[buf][w];
+      c[static_cast<size_t>(i) * n + j] += tot;
+    }
+  };
+
+  VT even[GEMV_VPT], odd[GEMV_VPT];
+  if (j0 < j1) prefetch(even, j0);
+  __syncthreads();  // sa is complete
+  for (int j = j0; j < j1; j += 2) {
+    if (j + 1 < j1) prefetch(odd, j + 1);
+    reduce_row(even, j, 0);
+    if (j + 1 < j1) {
+      if (j + 2 < j1) prefetch(even, j + 2);
+      reduce_row(odd, j + 1, 1);
     }
   }
 }
