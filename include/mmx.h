@@ -226,6 +226,16 @@ MMX_API int mmx_upload_array(mmx_ctx* ctx, int slot, int array, const void* host
  * iteration (i, j).  For gene 11 the sum is returned in *sum_out (may be NULL otherwise). */
 MMX_API int mmx_run_loop(mmx_ctx* ctx, int slot, int gene, int i, int j, double* sum_out);
 
+/* Row-block form of a depth-0 loop (genes 0, 2, 4, 6, 8, 11): only iterations i in [row0, row0+rows)
+ * of the loop's outer index.  This is the building block of the row-sharded multi-GPU run (each GPU
+ * owns a block of rows of a, c and bt; bt is then all-gathered): SURVEY 8e.  For gene 11 *sum_out
+ * receives the partial trace of the block. */
+MMX_API int mmx_run_loop_rows(mmx_ctx* ctx, int slot, int gene, int row0, int rows, double* sum_out);
+
+/* Device address of a slot's array (n*n elements of the context dtype), so that a collective library
+ * can exchange it in place (the all-gather of bt); valid until mmx_destroy. */
+MMX_API int mmx_device_ptr(mmx_ctx* ctx, int slot, int array, void** ptr_out);
+
 /* Time `iters` launches of loop `gene` (iteration 0 for inner loops) with CUDA events on
  * the slot's stream; when flush_l2 != 0 a 256 MiB buffer (larger than the 126 MB L2) is read before
  * every timed launch, outside the event bracket, so the cache holds only clean foreign lines.  ms_out receives the mean per launch. */

@@ -97,6 +97,8 @@ _SIGNATURES = {
     "mmx_fetch_array": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t]),
     "mmx_upload_array": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t]),
     "mmx_run_loop": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
+    "mmx_run_loop_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
+    "mmx_device_ptr": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "mmx_time_loop": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "mmx_peak_probe": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double)]),
 }
@@ -255,6 +257,16 @@ class Context:
         s = C.c_double(0.0)
         self._check(self._lib.mmx_run_loop(self._h, slot, gene, i, j, C.byref(s)))
         return s.value
+
+    def run_loop_rows(self, gene: int, row0: int, rows: int, slot: int = 0) -> float:
+        s = C.c_double(0.0)
+        self._check(self._lib.mmx_run_loop_rows(self._h, slot, gene, row0, rows, C.byref(s)))
+        return s.value
+
+    def device_ptr(self, array: int, slot: int = 0) -> int:
+        p = C.c_void_p()
+        self._check(self._lib.mmx_device_ptr(self._h, slot, array, C.byref(p)))
+        return p.value
 
     def time_loop(self, gene: int, iters: int = 10, flush_l2: bool = True, slot: int = 0) -> float:
         ms = C.c_double()

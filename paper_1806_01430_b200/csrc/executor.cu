@@ -101,8 +101,9 @@ int ensure_host(mmx_ctx* ctx, Slot& s, int array) {
 
 // ---- kernel dispatch by gene --------------------------------------------------------------------
 
+// rows [row0, row0+rows) of the loop's outer index for depth-0 genes (the whole nest: 0, n)
 template <typename T>
-cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter) {
+cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int row0, int rows) {
   const int n = ctx->cfg.n;
   const bool strict = ctx->cfg.numerics == MMX_NUMERICS_STRICT;
   T* a = static_cast<T*>(s.d_arr[MMX_ARRAY_A]);
@@ -110,28 +111,33 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter) {
   T* c = static_cast<T*>(s.d_arr[MMX_ARRAY_C]);
   T* bt = static_cast<T*>(s.d_arr[MMX_ARRAY_BT]);
   switch (gene) {
-    case 0: return launch_fill2d<T>(FILL_INIT_A, a, n, s.stream);
+    case 0: return launch_fill2d<T>(FILL_INIT_A, a, n, row0, rows, s.stream);
     case 1: return launch_fill_row<T>(FILL_INIT_A, a, n, iter, s.stream);
-    case 2: return launch_fill2d<T>(FILL_INIT_B, b, n, s.stream);
+    case 2: return launch_fill2d<T>(FILL_INIT_B, b, n, row0, rows, s.stream);
     case 3: return launch_fill_row<T>(FILL_INIT_B, b, n, iter, s.stream);
-    case 4: return launch_fill2d<T>(FILL_ZERO, c, n, s.stream);
+    case 4: return launch_fill2d<T>(FILL_ZERO, c, n, row0, rows, s.stream);
     case 5: return launch_fill_row<T>(FILL_ZERO, c, n, iter, s.stream);
-    case 6: return launch_transpose<T>(bt, b, n, s.stream);
+    case 6: return launch_transpose<T>(bt, b, n, row0, rows, s.stream);
     case 7: return launch_transpose_row<T>(bt, b, n, iter, s.stream);
     case 8: {
       int variant = ctx->cfg.matmul_variant;
       if (variant == 0) variant = 4;  // auto: DMMA, BK=32, 3 stages (best of the tuning points, profiles/)
-      return launch_matmul<T>(c, a, bt, n, 0, n, strict, variant, s.stream);
+      return launch_matmul<T>(c, a, bt, n, row0, rows, strict, variant, s.stream);
     }
     case 9: return launch_gemv_row<T>(c, a, bt, n, iter, strict, s.stream);
     case 10: return launch_dot<T>(c, a, bt, n, iter, strict, s.stream);
-    case 11: return launch_trace<T>(static_cast<T*>(s.d_sum), c, n, strict, s.stream);
+    case 11: return launch_trace<T>(static_cast<T*>(s.d_sum), c, n, row0, rows, strict, s.stream);
     default: return cudaErrorInvalidValue;
   }
 }
 
+cudaError_t launch_gene_rows(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int row0, int rows) {
+  return ctx->cfg.dtype == MMX_F64 ? launch_gene<double>(ctx, s, gene, iter, row0, rows)
+                                   : launch_gene<float>(ctx, s, gene, iter, row0, rows);
+}
+
 cudaError_t launch_gene_any(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter) {
-  return ctx->cfg.dtype == MMX_F64 ? launch_gene<double>(ctx, s, gene, iter) : launch_gene<float>(ctx, s, gene, iter);
+  return launch_gene_rows(ctx, s, gene, iter, 0, ctx->cfg.n);
 }
 
 // gene that serves `nest` in `mode`
@@ -739,6 +745,38 @@ MMX_API int mmx_run_loop(mmx_ctx* ctx, int slot, int gene, int i, int j, double*
   MMX_CUDA(ctx, cudaStreamSynchronize(s.stream));
   if (gene == 11 && sum_out != nullptr)
     *sum_out = ctx->cfg.dtype == MMX_F64 ? *static_cast<double*>(s.h_sum) : static_cast<double>(*static_cast<float*>(s.h_sum));
+  return MMX_OK;
+}
+
+MMX_API int mmx_run_loop_rows(mmx_ctx* ctx, int slot, int gene, int row0, int rows, double* sum_out) {
+  if (ctx == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size())) return MMX_E_INVALID;
+  const int n = ctx->cfg.n;
+  const bool depth0 = gene == 0 || gene == 2 || gene == 4 || gene == 6 || gene == 8 || gene == 11;
+  if (!depth0 || row0 < 0 || rows < 0 || row0 + rows > n) {
+    ctx->set_error("mmx_run_loop_rows: needs a depth-0 gene and a row block inside the matrix");
+    return MMX_E_INVALID;
+  }
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  MMX_CUDA(ctx, launch_gene_rows(ctx, s, gene, IterRef{nullptr, 0}, row0, rows));
+  const int w = written_array(kCatalogue[gene].nest);
+  if (w >= 0) {
+    s.dev_valid[w] = true;
+    s.host_valid[w] = false;
+  }
+  if (gene == 11) MMX_CUDA(ctx, cudaMemcpyAsync(s.h_sum, s.d_sum, elem_size(ctx->cfg.dtype), cudaMemcpyDeviceToHost, s.stream));
+  MMX_CUDA(ctx, cudaStreamSynchronize(s.stream));
+  if (gene == 11 && sum_out != nullptr)
+    *sum_out = ctx->cfg.dtype == MMX_F64 ? *static_cast<double*>(s.h_sum) : static_cast<double>(*static_cast<float*>(s.h_sum));
+  return MMX_OK;
+}
+
+MMX_API int mmx_device_ptr(mmx_ctx* ctx, int slot, int array, void** ptr_out) {
+  if (ctx == nullptr || ptr_out == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size()) || array < 0 ||
+      array >= MMX_NUM_ARRAYS)
+    return MMX_E_INVALID;
+  *ptr_out = ctx->slots[slot]->d_arr[array];
   return MMX_OK;
 }
 

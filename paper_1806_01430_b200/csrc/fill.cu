@@ -48,15 +48,15 @@ constexpr int kRowsPerThread = 8;
 
 // blockDim = (bx, by), bx*by = 256.  A block covers bx*V columns x by*kRowsPerThread rows.
 template <typename T, int OP, bool POW2, int V>
-__global__ void __launch_bounds__(256) fill2d_kernel(T* __restrict__ dst, int n, T nn, T inv) {
+__global__ void __launch_bounds__(256) fill2d_kernel(T* __restrict__ dst, int n, int first_row, int row_limit, T nn, T inv) {
   const int jv = blockIdx.x * blockDim.x + threadIdx.x;  // vector column
   const int j0 = jv * V;
   if (j0 >= n) return;
-  const int row0 = (blockIdx.y * blockDim.y + threadIdx.y) * kRowsPerThread;
+  const int row0 = first_row + (blockIdx.y * blockDim.y + threadIdx.y) * kRowsPerThread;
 #pragma unroll
   for (int r = 0; r < kRowsPerThread; ++r) {
     const int i = row0 + r;
-    if (i < n) store_vec<T, OP, POW2, V>(dst + static_cast<size_t>(i) * n + j0, i, j0, nn, inv);
+    if (i < row_limit) store_vec<T, OP, POW2, V>(dst + static_cast<size_t>(i) * n + j0, i, j0, nn, inv);
   }
 }
 
@@ -70,14 +70,16 @@ __global__ void __launch_bounds__(256) fill_row_kernel(T* __restrict__ dst, int 
 inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
 template <typename T, int OP, bool POW2, int V>
-cudaError_t fill2d_go(T* dst, int n, cudaStream_t stream) {
+cudaError_t fill2d_go(T* dst, int n, int row0, int rows, cudaStream_t stream) {
   const int nvec = (n + V - 1) / V;
   int bx = 32;
   while (bx < 256 && bx < nvec) bx <<= 1;
   const int by = 256 / bx;
   dim3 block(bx, by);
-  dim3 grid((nvec + bx - 1) / bx, (n + by * kRowsPerThread - 1) / (by * kRowsPerThread));
-  fill2d_kernel<T, OP, POW2, V><<<grid, block, 0, stream>>>(dst, n, static_cast<T>(n), static_cast<T>(1.0) / static_cast<T>(n));
+  if (rows <= 0) return cudaSuccess;
+  dim3 grid((nvec + bx - 1) / bx, (rows + by * kRowsPerThread - 1) / (by * kRowsPerThread));
+  fill2d_kernel<T, OP, POW2, V><<<grid, block, 0, stream>>>(dst, n, row0, row0 + rows, static_cast<T>(n),
+                                                            static_cast<T>(1.0) / static_cast<T>(n));
   return cudaGetLastError();
 }
 
@@ -98,19 +100,19 @@ template <typename T> constexpr int vec_width() { return 16 / sizeof(T); }
   if (op == OPV && pow2 == P2 && vec == (VV != 1)) return CALL<T, OPV, P2, VV>
 
 template <typename T>
-cudaError_t launch_fill2d(int op, T* dst, int n, cudaStream_t stream) {
+cudaError_t launch_fill2d(int op, T* dst, int n, int row0, int rows, cudaStream_t stream) {
   constexpr int W = vec_width<T>();
   const bool pow2 = is_pow2(n);
   const bool vec = n % W == 0;
-  MMX_FILL_CASE(FILL_INIT_A, true, W, fill2d_go)(dst, n, stream);
-  MMX_FILL_CASE(FILL_INIT_A, false, W, fill2d_go)(dst, n, stream);
-  MMX_FILL_CASE(FILL_INIT_A, true, 1, fill2d_go)(dst, n, stream);
-  MMX_FILL_CASE(FILL_INIT_A, false, 1, fill2d_go)(dst, n, stream);
-  MMX_FILL_CASE(FILL_INIT_B, true, W, fill2d_go)(dst, n, stream);
-  MMX_FILL_CASE(FILL_INIT_B, false, W, fill2d_go)(dst, n, stream);
-  MMX_FILL_CASE(FILL_INIT_B, true, 1, fill2d_go)(dst, n, stream);
-  MMX_FILL_CASE(FILL_INIT_B, false, 1, fill2d_go)(dst, n, stream);
-  if (op == FILL_ZERO) return vec ? fill2d_go<T, FILL_ZERO, true, W>(dst, n, stream) : fill2d_go<T, FILL_ZERO, true, 1>(dst, n, stream);
+  MMX_FILL_CASE(FILL_INIT_A, true, W, fill2d_go)(dst, n, row0, rows, stream);
+  MMX_FILL_CASE(FILL_INIT_A, false, W, fill2d_go)(dst, n, row0, rows, stream);
+  MMX_FILL_CASE(FILL_INIT_A, true, 1, fill2d_go)(dst, n, row0, rows, stream);
+  MMX_FILL_CASE(FILL_INIT_A, false, 1, fill2d_go)(dst, n, row0, rows, stream);
+  MMX_FILL_CASE(FILL_INIT_B, true, W, fill2d_go)(dst, n, row0, rows, stream);
+  MMX_FILL_CASE(FILL_INIT_B, false, W, fill2d_go)(dst, n, row0, rows, stream);
+  MMX_FILL_CASE(FILL_INIT_B, true, 1, fill2d_go)(dst, n, row0, rows, stream);
+  MMX_FILL_CASE(FILL_INIT_B, false, 1, fill2d_go)(dst, n, row0, rows, stream);
+  if (op == FILL_ZERO) return vec ? fill2d_go<T, FILL_ZERO, true, W>(dst, n, row0, rows, stream) : fill2d_go<T, FILL_ZERO, true, 1>(dst, n, row0, rows, stream);
   return cudaErrorInvalidValue;
 }
 
@@ -131,8 +133,8 @@ cudaError_t launch_fill_row(int op, T* dst, int n, IterRef iter, cudaStream_t st
   return cudaErrorInvalidValue;
 }
 
-template cudaError_t launch_fill2d<double>(int, double*, int, cudaStream_t);
-template cudaError_t launch_fill2d<float>(int, float*, int, cudaStream_t);
+template cudaError_t launch_fill2d<double>(int, double*, int, int, int, cudaStream_t);
+template cudaError_t launch_fill2d<float>(int, float*, int, int, int, cudaStream_t);
 template cudaError_t launch_fill_row<double>(int, double*, int, IterRef, cudaStream_t);
 template cudaError_t launch_fill_row<float>(int, float*, int, IterRef, cudaStream_t);
 

@@ -22,12 +22,14 @@ struct IterRef {
 enum FillOp { FILL_INIT_A = 0, FILL_INIT_B = 1, FILL_ZERO = 2 };
 
 // genes 0,2,4: dst[i][j] = op(i,j) over the whole n x n array (matmul.c:8-18)
-template <typename T> cudaError_t launch_fill2d(int op, T* dst, int n, cudaStream_t stream);
+// rows [row0, row0+rows) only (row0 = 0, rows = n for the whole nest; the row-sharded multi-GPU path passes its block)
+template <typename T> cudaError_t launch_fill2d(int op, T* dst, int n, int row0, int rows, cudaStream_t stream);
 // genes 1,3,5: one row i = iter of the same
 template <typename T> cudaError_t launch_fill_row(int op, T* dst, int n, IterRef iter, cudaStream_t stream);
 
 // gene 6: bt[i][j] = b[j][i] (matmul.c:21-23)
-template <typename T> cudaError_t launch_transpose(T* bt, const T* b, int n, cudaStream_t stream);
+// rows [row0, row0+rows) of bt only (= columns of b)
+template <typename T> cudaError_t launch_transpose(T* bt, const T* b, int n, int row0, int rows, cudaStream_t stream);
 // gene 7: row i of bt = column i of b
 template <typename T> cudaError_t launch_transpose_row(T* bt, const T* b, int n, IterRef iter, cudaStream_t stream);
 
@@ -45,7 +47,8 @@ template <typename T>
 cudaError_t launch_dot(T* c, const T* a, const T* bt, int n, IterRef flat_iter, bool strict, cudaStream_t stream);
 
 // gene 11: *sum = sum_i c[i][i] (matmul.c:30-32)
-template <typename T> cudaError_t launch_trace(T* sum, const T* c, int n, bool strict, cudaStream_t stream);
+// diagonal entries i in [row0, row0+rows)
+template <typename T> cudaError_t launch_trace(T* sum, const T* c, int n, int row0, int rows, bool strict, cudaStream_t stream);
 
 // graph plumbing: *counter += delta
 cudaError_t launch_advance(int* counter, int delta, cudaStream_t stream);

@@ -234,10 +234,13 @@ __global__ void __launch_bounds__(256) dot_strict_kernel(T* __restrict__ c, cons
 // One block of 1024 threads: strided gather of the diagonal, shuffle + smem tree (FAST), or
 // staged chunks summed in index order by thread 0 (STRICT).  N elements, latency-bound.
 template <typename T, bool STRICT>
-__global__ void __launch_bounds__(1024) trace_kernel(T* __restrict__ sum, const T* __restrict__ c, int n) {
+__global__ void __launch_bounds__(1024) trace_kernel(T* __restrict__ sum, const T* __restrict__ c_full, int n_full,
+                                                     int first, int count) {
   __shared__ T buf[1024];
   const int t = threadIdx.x;
-  const size_t pitch = static_cast<size_t>(n) + 1;
+  const size_t pitch = static_cast<size_t>(n_full) + 1;
+  const T* c = c_full + first * pitch;  // diagonal entry `first`
+  const int n = count;
   if constexpr (STRICT) {
     T acc = static_cast<T>(0.0);
     for (int i0 = 0; i0 < n; i0 += 1024) {
@@ -303,16 +306,16 @@ cudaError_t launch_dot(T* c, const T* a, const T* bt, int n, IterRef flat_iter, 
 }
 
 template <typename T>
-cudaError_t launch_trace(T* sum, const T* c, int n, bool strict, cudaStream_t stream) {
-  if (strict) trace_kernel<T, true><<<1, 1024, 0, stream>>>(sum, c, n);
-  else trace_kernel<T, false><<<1, 1024, 0, stream>>>(sum, c, n);
+cudaError_t launch_trace(T* sum, const T* c, int n, int row0, int rows, bool strict, cudaStream_t stream) {
+  if (strict) trace_kernel<T, true><<<1, 1024, 0, stream>>>(sum, c, n, row0, rows);
+  else trace_kernel<T, false><<<1, 1024, 0, stream>>>(sum, c, n, row0, rows);
   return cudaGetLastError();
 }
 
 #define MMX_INST(T)                                                                                        \
   template cudaError_t launch_gemv_row<T>(T*, const T*, const T*, int, IterRef, bool, cudaStream_t);      \
   template cudaError_t launch_dot<T>(T*, const T*, const T*, int, IterRef, bool, cudaStream_t);           \
-  template cudaError_t launch_trace<T>(T*, const T*, int, bool, cudaStream_t);
+  template cudaError_t launch_trace<T>(T*, const T*, int, int, int, bool, cudaStream_t);
 MMX_INST(double)
 MMX_INST(float)
 

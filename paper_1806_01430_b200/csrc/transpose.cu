@@ -36,14 +36,14 @@ __device__ __forceinline__ void transpose_micro(const float4 (&in)[4], float4 (&
 
 // grid = (n/64, n/64); block = 256 threads.
 template <typename T>
-__global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt, const T* __restrict__ b, int n) {
+__global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt, const T* __restrict__ b, int n, int first_row) {
   using VT = typename VecOf<T>::type;
   constexpr int V = VecOf<T>::V;
   constexpr int MB = kTile / V;         // micro-blocks per tile side == 16-byte chunks per tile row
   __shared__ VT tile[kTile * MB];        // output-ordered: tile[out_row][chunk], swizzled
 
   const int in_row0 = blockIdx.y * kTile;   // rows of b  == columns of bt
-  const int in_col0 = blockIdx.x * kTile;   // cols of b  == rows of bt
+  const int in_col0 = first_row + blockIdx.x * kTile;   // cols of b  == rows of bt
   const int tid = threadIdx.x;
 
   // phase 1: micro-blocks, lanes along the input row (coalesced 128-bit loads)
@@ -77,20 +77,21 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
 
 // Any n: 32x32 tile, scalar accesses, +1 padding.  block = (32, 8).
 template <typename T>
-__global__ void __launch_bounds__(256) transpose_generic_kernel(T* __restrict__ bt, const T* __restrict__ b, int n) {
+__global__ void __launch_bounds__(256) transpose_generic_kernel(T* __restrict__ bt, const T* __restrict__ b, int n,
+                                                                int first_row, int row_limit) {
   __shared__ T tile[32][33];
-  const int x = blockIdx.x * 32 + threadIdx.x;
+  const int x = first_row + blockIdx.x * 32 + threadIdx.x;  // column of b = row of bt
 #pragma unroll
   for (int r = threadIdx.y; r < 32; r += 8) {
     const int y = blockIdx.y * 32 + r;
-    if (x < n && y < n) tile[r][threadIdx.x] = b[static_cast<size_t>(y) * n + x];
+    if (x < row_limit && y < n) tile[r][threadIdx.x] = b[static_cast<size_t>(y) * n + x];
   }
   __syncthreads();
   const int ox = blockIdx.y * 32 + threadIdx.x;  // column of bt = row of b
 #pragma unroll
   for (int r = threadIdx.y; r < 32; r += 8) {
-    const int oy = blockIdx.x * 32 + r;          // row of bt = column of b
-    if (ox < n && oy < n) bt[static_cast<size_t>(oy) * n + ox] = tile[threadIdx.x][r];
+    const int oy = first_row + blockIdx.x * 32 + r;  // row of bt = column of b
+    if (ox < n && oy < row_limit) bt[static_cast<size_t>(oy) * n + ox] = tile[threadIdx.x][r];
   }
 }
 
@@ -105,13 +106,14 @@ __global__ void __launch_bounds__(256) transpose_row_kernel(T* __restrict__ bt, 
 }  // namespace
 
 template <typename T>
-cudaError_t launch_transpose(T* bt, const T* b, int n, cudaStream_t stream) {
-  if (n % kTile == 0) {
-    dim3 grid(n / kTile, n / kTile);
-    transpose_tile_kernel<T><<<grid, 256, 0, stream>>>(bt, b, n);
+cudaError_t launch_transpose(T* bt, const T* b, int n, int row0, int rows, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (n % kTile == 0 && row0 % kTile == 0 && rows % kTile == 0) {
+    dim3 grid(rows / kTile, n / kTile);
+    transpose_tile_kernel<T><<<grid, 256, 0, stream>>>(bt, b, n, row0);
   } else {
-    dim3 grid((n + 31) / 32, (n + 31) / 32);
-    transpose_generic_kernel<T><<<grid, dim3(32, 8), 0, stream>>>(bt, b, n);
+    dim3 grid((rows + 31) / 32, (n + 31) / 32);
+    transpose_generic_kernel<T><<<grid, dim3(32, 8), 0, stream>>>(bt, b, n, row0, row0 + rows);
   }
   return cudaGetLastError();
 }
@@ -123,8 +125,8 @@ cudaError_t launch_transpose_row(T* bt, const T* b, int n, IterRef iter, cudaStr
   return cudaGetLastError();
 }
 
-template cudaError_t launch_transpose<double>(double*, const double*, int, cudaStream_t);
-template cudaError_t launch_transpose<float>(float*, const float*, int, cudaStream_t);
+template cudaError_t launch_transpose<double>(double*, const double*, int, int, int, cudaStream_t);
+template cudaError_t launch_transpose<float>(float*, const float*, int, int, int, cudaStream_t);
 template cudaError_t launch_transpose_row<double>(double*, const double*, int, IterRef, cudaStream_t);
 template cudaError_t launch_transpose_row<float>(float*, const float*, int, IterRef, cudaStream_t);
 

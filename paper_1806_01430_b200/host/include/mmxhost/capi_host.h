@@ -83,6 +83,17 @@ MMXH_API int mmxh_evaluator_counters(void* h, uint64_t c4[4], double* elapsed_s)
 /* call counters of a callback backend: calls, max_in_flight */
 MMXH_API int mmxh_evaluator_cb_stats(void* h, int32_t out2[2]);
 
+/* A GenomeEvaluator implemented by the caller (evaluation.hpp:42-56): `batch` receives the whole
+ * evaluate_all() input (count genomes of n bits each) and fills outs[count]; `counters` fills
+ * {requests, distinct, cache_hits, backend_calls} and *elapsed_s.  This is the seam a rank-sharded
+ * evaluator (paper_1806_01430_b200/sharded.py, torch.distributed) plugs into run_ga through.
+ * Return 0, or a negative MMXH_E_* code to make run_ga fail with that error class. */
+typedef int (*mmxh_batch_cb)(const uint8_t* bits, size_t count, size_t n, mmxh_outcome* outs, void* user);
+typedef int (*mmxh_counters_cb)(uint64_t c4[4], double* elapsed_s, void* user);
+MMXH_API int mmxh_run_ga_external(size_t gene_length, mmxh_batch_cb batch, mmxh_counters_cb counters, void* user,
+                                  const mmxh_ga_params* params, char* csv, size_t csv_cap, uint8_t* best_bits,
+                                  double* best_s, double* baseline_s);
+
 /* run_ga over an evaluator handle; csv receives generations.csv text; returns its length */
 MMXH_API int mmxh_run_ga(void* evaluator, const mmxh_ga_params* params, char* csv, size_t csv_cap, uint8_t* best_bits,
                          double* best_s, double* baseline_s);

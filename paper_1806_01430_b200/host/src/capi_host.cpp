@@ -321,6 +321,86 @@ MMXH_API int mmxh_run_ga(void* evaluator, const mmxh_ga_params* params, char* cs
   });
 }
 
+namespace {
+
+[[noreturn]] void rethrow_code(int rc) {
+  switch (rc) {
+    case MMXH_E_LENGTH: throw GenomeLengthMismatch("external evaluator: genome length mismatch");
+    case MMXH_E_TOOLCHAIN: throw ToolchainMissing("external evaluator: measuring tool missing");
+    case MMXH_E_WORKDIR: throw WorkdirUnwritable("external evaluator: workspace unwritable");
+    case MMXH_E_CONFIG: throw ConfigError("external evaluator: bad configuration");
+    default: throw Error("external evaluator failed");
+  }
+}
+
+class ExternalEvaluator : public GenomeEvaluator {
+ public:
+  ExternalEvaluator(mmxh_batch_cb batch, mmxh_counters_cb counters, void* user) : batch_(batch), counters_(counters), user_(user) {}
+
+  EvaluationOutcome evaluate(const Genome& genome) override { return evaluate_all({genome}).front(); }
+
+  std::vector<EvaluationOutcome> evaluate_all(const std::vector<Genome>& genomes) override {
+    std::vector<EvaluationOutcome> out(genomes.size());
+    if (genomes.empty()) return out;
+    const std::size_t n = genomes.front().size();
+    std::vector<std::uint8_t> flat;
+    flat.reserve(genomes.size() * n);
+    for (const Genome& g : genomes) flat.insert(flat.end(), g.bits().begin(), g.bits().end());
+    std::vector<mmxh_outcome> raw(genomes.size());
+    const int rc = batch_(flat.data(), genomes.size(), n, raw.data(), user_);
+    if (rc < 0) rethrow_code(rc);
+    for (std::size_t i = 0; i < genomes.size(); ++i) {
+      out[i].status = static_cast<EvalStatus>(raw[i].status);
+      out[i].time_s = raw[i].time_s;
+      out[i].wall_cost_s = raw[i].wall_cost_s;
+    }
+    return out;
+  }
+
+  EvalCounters counters() const override {
+    std::uint64_t c4[4] = {0, 0, 0, 0};
+    double elapsed = 0.0;
+    const int rc = counters_(c4, &elapsed, user_);
+    if (rc < 0) rethrow_code(rc);
+    EvalCounters c;
+    c.requests = c4[0];
+    c.distinct = c4[1];
+    c.cache_hits = c4[2];
+    c.backend_calls = c4[3];
+    c.elapsed_s = elapsed;
+    return c;
+  }
+
+ private:
+  mmxh_batch_cb batch_;
+  mmxh_counters_cb counters_;
+  void* user_;
+};
+
+}  // namespace
+
+MMXH_API int mmxh_run_ga_external(size_t gene_length, mmxh_batch_cb batch, mmxh_counters_cb counters, void* user,
+                                  const mmxh_ga_params* params, char* csv, size_t csv_cap, uint8_t* best_bits,
+                                  double* best_s, double* baseline_s) {
+  return guarded([&] {
+    ExternalEvaluator ev(batch, counters, user);
+    GAParams p;
+    p.population = params->population;
+    p.generations = params->generations;
+    p.crossover_rate = params->crossover_rate;
+    p.mutation_rate = params->mutation_rate;
+    p.seed = params->seed;
+    p.elite_count = params->elite_count;
+    const TuningResult r = run_ga(gene_length, p, ev);
+    std::ostringstream s;
+    write_generation_csv(s, r);
+    std::memcpy(best_bits, r.best_genome.bits().data(), r.best_genome.size());
+    *best_s = r.best_time_s;
+    *baseline_s = r.baseline_s;
+    return copy_out(s.str(), csv, csv_cap);
+  });
+}
+
 MMXH_API const char* mmxh_status_name(int status) {
   static thread_local std::string s;
   s = std::string(to_string(static_cast<EvalStatus>(status)));
