@@ -236,6 +236,44 @@ MMX_API int mmx_run_loop_rows(mmx_ctx* ctx, int slot, int gene, int row0, int ro
  * can exchange it in place (the all-gather of bt); valid until mmx_destroy. */
 MMX_API int mmx_device_ptr(mmx_ctx* ctx, int slot, int array, void** ptr_out);
 
+/* ---- row-sharded run across a group of GPUs (BASELINE.json config 5) -----------------
+ * One individual (every nest offloaded) spread over `world` <= 8 members, one device slot each.  Member r
+ * owns a contiguous block of rows of a, c and bt (64-row aligned when N allows).  The single exchange of
+ * the path -- every member needs all of bt for the contraction -- is fused into the transpose kernel, which
+ * stores its rows of bt into every member's bt through peer-mapped pointers; the contraction then walks the
+ * column blocks in ring order, waiting per block on the owner's event.  No collective library is involved.
+ * The reference has no multi-device mode; the nearest interface is its `jobs` worker pool
+ * (evaluator.cpp:246-276), which this does not replace -- it is the large-N extension north_star names. */
+typedef struct mmx_shard_handle {
+  unsigned char mem[64];   /* cudaIpcMemHandle_t of the member's bt   */
+  unsigned char event[64]; /* cudaIpcEventHandle_t of its ready event */
+} mmx_shard_handle;
+
+typedef struct mmx_shard_stats {
+  int32_t rank, world;
+  int32_t row0, rows;     /* the member's block                                             */
+  double gpu_ms;          /* CUDA-event time of the member's whole share of the individual   */
+  double exchange_ms;     /* the fused transpose + all-gather kernel                         */
+  double matmul_ms;       /* the `world` column-block launches of the contraction            */
+  uint64_t peer_bytes;    /* bytes this member stored into other members' bt                 */
+  double partial_trace;   /* sum of the member's diagonal entries                            */
+} mmx_shard_stats;
+
+/* Members in ONE process (a context with one slot per GPU, or several slots on one GPU for tests): binds
+ * the slots as ranks 0..world-1 on first use, runs the individual, waits; outs[world] and *checksum (sum of
+ * the partial traces in rank order) may be NULL. */
+MMX_API int mmx_shard_run_local(mmx_ctx* ctx, const int32_t* slots, int world, mmx_shard_stats* outs, double* checksum);
+
+/* Members in DIFFERENT processes (one process per GPU): each exports its handle, the handles are exchanged by
+ * the caller (any transport), then every process binds its slot with the full table.  Per run the caller
+ * does: phase1 on every member; a host barrier (each member's ready event must have been recorded before a
+ * peer waits on it); phase2 on every member; a host barrier before the next run. */
+MMX_API int mmx_shard_export(mmx_ctx* ctx, int slot, mmx_shard_handle* out);
+MMX_API int mmx_shard_bind(mmx_ctx* ctx, int slot, int rank, int world, const mmx_shard_handle* handles,
+                           const int32_t* local_slots);
+MMX_API int mmx_shard_phase1(mmx_ctx* ctx, int slot);
+MMX_API int mmx_shard_phase2(mmx_ctx* ctx, int slot, mmx_shard_stats* out);
+
 /* Time `iters` launches of loop `gene` (iteration 0 for inner loops) with CUDA events on
  * the slot's stream; when flush_l2 != 0 a 256 MiB buffer (larger than the 126 MB L2) is read before
  * every timed launch, outside the event bracket, so the cache holds only clean foreign lines.  ms_out receives the mean per launch. */

@@ -75,6 +75,19 @@ class LoopInfo(C.Structure):
                 ("induction", C.c_char_p), ("kernel", C.c_char_p)]
 
 
+class ShardHandle(C.Structure):
+    _fields_ = [("mem", C.c_ubyte * 64), ("event", C.c_ubyte * 64)]
+
+
+class ShardStats(C.Structure):
+    _fields_ = [("rank", C.c_int32), ("world", C.c_int32), ("row0", C.c_int32), ("rows", C.c_int32),
+                ("gpu_ms", C.c_double), ("exchange_ms", C.c_double), ("matmul_ms", C.c_double),
+                ("peer_bytes", C.c_uint64), ("partial_trace", C.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class MmxError(RuntimeError):
     def __init__(self, code: int, message: str):
         super().__init__(f"mmx error {code}: {message}")
@@ -99,6 +112,11 @@ _SIGNATURES = {
     "mmx_run_loop": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "mmx_run_loop_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "mmx_device_ptr": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "mmx_shard_run_local": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int, C.POINTER(ShardStats), C.POINTER(C.c_double)]),
+    "mmx_shard_export": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(ShardHandle)]),
+    "mmx_shard_bind": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(ShardHandle), C.POINTER(C.c_int32)]),
+    "mmx_shard_phase1": (C.c_int, [C.c_void_p, C.c_int]),
+    "mmx_shard_phase2": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(ShardStats)]),
     "mmx_time_loop": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "mmx_peak_probe": (C.c_int, [C.c_int, C.c_int, C.POINTER(C.c_double)]),
 }
@@ -267,6 +285,35 @@ class Context:
         p = C.c_void_p()
         self._check(self._lib.mmx_device_ptr(self._h, slot, array, C.byref(p)))
         return p.value
+
+    # -- row-sharded run (include/mmx.h: mmx_shard_*) ---------------------------------------------
+    def shard_run_local(self, slots=None) -> tuple[float, list[dict]]:
+        """One individual sharded over the given slots of this context (all of them by default)."""
+        slots = list(range(self.num_slots)) if slots is None else list(slots)
+        arr = (C.c_int32 * len(slots))(*slots)
+        stats = (ShardStats * len(slots))()
+        checksum = C.c_double()
+        self._check(self._lib.mmx_shard_run_local(self._h, arr, len(slots), stats, C.byref(checksum)))
+        return checksum.value, [st.as_dict() for st in stats]
+
+    def shard_export(self, slot: int = 0) -> bytes:
+        h = ShardHandle()
+        self._check(self._lib.mmx_shard_export(self._h, slot, C.byref(h)))
+        return bytes(h)
+
+    def shard_bind(self, rank: int, world: int, handles: list[bytes], slot: int = 0) -> None:
+        table = (ShardHandle * world)()
+        for r, raw in enumerate(handles):
+            C.memmove(C.byref(table[r]), raw, C.sizeof(ShardHandle))
+        self._check(self._lib.mmx_shard_bind(self._h, slot, rank, world, table, None))
+
+    def shard_phase1(self, slot: int = 0) -> None:
+        self._check(self._lib.mmx_shard_phase1(self._h, slot))
+
+    def shard_phase2(self, slot: int = 0) -> dict:
+        st = ShardStats()
+        self._check(self._lib.mmx_shard_phase2(self._h, slot, C.byref(st)))
+        return st.as_dict()
 
     def time_loop(self, gene: int, iters: int = 10, flush_l2: bool = True, slot: int = 0) -> float:
         ms = C.c_double()

@@ -54,6 +54,13 @@ struct Slot {
   std::map<unsigned, cudaGraphExec_t> plan_graphs;  // by genome mask: whole device-only individuals
   mmx_run_stats stats{};
   std::mutex mu;
+  // row-sharded group membership (mmx_shard_*): this slot is member `shard_rank` of `shard_world`
+  int shard_rank = -1, shard_world = 0;
+  void* peer_bt[kMaxPeers] = {};          // bt of every member as seen from this device (own array at [shard_rank])
+  cudaEvent_t peer_ready[kMaxPeers] = {}; // member r's "my rows of bt are stored everywhere" event
+  bool peer_ipc[kMaxPeers] = {};          // opened from another process's handle: must be closed / destroyed here
+  cudaEvent_t ev_ready = nullptr;         // interprocess-capable, no timing
+  cudaEvent_t ev_x0 = nullptr, ev_x1 = nullptr, ev_m0 = nullptr, ev_m1 = nullptr;
 };
 
 }  // namespace
@@ -122,7 +129,7 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
     case 8: {
       int variant = ctx->cfg.matmul_variant;
       if (variant == 0) variant = 4;  // auto: DMMA, BK=32, 3 stages (best of the tuning points, profiles/)
-      return launch_matmul<T>(c, a, bt, n, row0, rows, strict, variant, s.stream);
+      return launch_matmul<T>(c, a, bt, n, row0, rows, 0, n, strict, variant, s.stream);
     }
     case 9: return launch_gemv_row<T>(c, a, bt, n, iter, strict, s.stream);
     case 10: return launch_dot<T>(c, a, bt, n, iter, strict, s.stream);
@@ -507,6 +514,13 @@ void destroy_slot(Slot& s) {
   if (s.d_scrub) cudaFree(s.d_scrub);
   if (s.ev_begin) cudaEventDestroy(s.ev_begin);
   if (s.ev_end) cudaEventDestroy(s.ev_end);
+  for (int r = 0; r < kMaxPeers; ++r)
+    if (s.peer_ipc[r]) {
+      if (s.peer_bt[r]) cudaIpcCloseMemHandle(s.peer_bt[r]);
+      if (s.peer_ready[r]) cudaEventDestroy(s.peer_ready[r]);
+    }
+  for (cudaEvent_t e : {s.ev_ready, s.ev_x0, s.ev_x1, s.ev_m0, s.ev_m1})
+    if (e) cudaEventDestroy(e);
   if (s.stream) cudaStreamDestroy(s.stream);
 }
 
@@ -826,3 +840,252 @@ MMX_API int mmx_peak_probe(int device, int kind, double* value_out) {
 }
 
 }  // extern "C"
+
+// ================================================================================================
+// Row-sharded run over a group of GPUs (BASELINE config 5)
+// ================================================================================================
+// Member r of a group of G owns rows R_r of a, c and bt.  Everything index-generated shards without
+// communication (init-a, zero-c on R_r; init-b is regenerated locally because the transpose needs
+// columns R_r of every row of b).  The one exchange of the path -- every member needs all of bt for
+// the contraction -- is fused into the kernel that produces bt: the transpose stores each finished
+// tile of bt[R_r][:] into the bt of every member through peer-mapped pointers (NVLink stores), so
+// there is no separate all-gather and no staging buffer.  The contraction is then walked column
+// block by column block in ring order starting with the member's own rows of bt; block s waits only
+// for member s's "stored everywhere" event, so transfers from the slower members overlap the math
+// on the blocks that have already arrived.
+namespace mmx {
+namespace {
+
+void shard_block(int n, int world, int rank, int* row0, int* rows) {
+  // contiguous, nearly equal blocks; boundaries are multiples of 64 when n allows it, so that the tiled
+  // transpose and the GEMM tiles never straddle a block edge (same rule as rowshard.py: row_block)
+  const int unit = (n % 64 == 0 && n / 64 >= world) ? 64 : 1;
+  const long long units = n / unit;
+  const int lo = static_cast<int>(units * rank / world) * unit;
+  const int hi = static_cast<int>(units * (rank + 1) / world) * unit;
+  *row0 = lo;
+  *rows = hi - lo;
+}
+
+int shard_events(mmx_ctx* ctx, Slot& s) {
+  if (s.ev_ready != nullptr) return MMX_OK;
+  MMX_CUDA(ctx, cudaEventCreateWithFlags(&s.ev_ready, cudaEventDisableTiming | cudaEventInterprocess));
+  MMX_CUDA(ctx, cudaEventCreate(&s.ev_x0));
+  MMX_CUDA(ctx, cudaEventCreate(&s.ev_x1));
+  MMX_CUDA(ctx, cudaEventCreate(&s.ev_m0));
+  MMX_CUDA(ctx, cudaEventCreate(&s.ev_m1));
+  return MMX_OK;
+}
+
+template <typename T>
+int shard_phase1(mmx_ctx* ctx, Slot& s) {
+  const int n = ctx->cfg.n;
+  int r0 = 0, rows = 0;
+  shard_block(n, s.shard_world, s.shard_rank, &r0, &rows);
+  MMX_CUDA(ctx, cudaEventRecord(s.ev_begin, s.stream));
+  MMX_CUDA(ctx, launch_fill2d<T>(FILL_INIT_A, static_cast<T*>(s.d_arr[MMX_ARRAY_A]), n, r0, rows, s.stream));
+  MMX_CUDA(ctx, launch_fill2d<T>(FILL_INIT_B, static_cast<T*>(s.d_arr[MMX_ARRAY_B]), n, 0, n, s.stream));
+  MMX_CUDA(ctx, launch_fill2d<T>(FILL_ZERO, static_cast<T*>(s.d_arr[MMX_ARRAY_C]), n, r0, rows, s.stream));
+  BtPeers peers;
+  peers.count = s.shard_world;
+  // own copy first, then the ring: member r+1, r+2, ... so that at any instant the members store into
+  // different destinations
+  for (int d = 0; d < s.shard_world; ++d) peers.p[d] = s.peer_bt[(s.shard_rank + d) % s.shard_world];
+  MMX_CUDA(ctx, cudaEventRecord(s.ev_x0, s.stream));
+  MMX_CUDA(ctx, launch_transpose_push<T>(peers, static_cast<const T*>(s.d_arr[MMX_ARRAY_B]), n, r0, rows, s.stream));
+  MMX_CUDA(ctx, cudaEventRecord(s.ev_x1, s.stream));
+  MMX_CUDA(ctx, cudaEventRecord(s.ev_ready, s.stream));
+  return MMX_OK;
+}
+
+template <typename T>
+int shard_phase2(mmx_ctx* ctx, Slot& s) {
+  const int n = ctx->cfg.n;
+  const bool strict = ctx->cfg.numerics == MMX_NUMERICS_STRICT;
+  int variant = ctx->cfg.matmul_variant;
+  if (variant == 0) variant = 4;
+  int r0 = 0, rows = 0;
+  shard_block(n, s.shard_world, s.shard_rank, &r0, &rows);
+  T* a = static_cast<T*>(s.d_arr[MMX_ARRAY_A]);
+  T* c = static_cast<T*>(s.d_arr[MMX_ARRAY_C]);
+  T* bt = static_cast<T*>(s.d_arr[MMX_ARRAY_BT]);
+  MMX_CUDA(ctx, cudaEventRecord(s.ev_m0, s.stream));
+  for (int d = 0; d < s.shard_world; ++d) {
+    const int src = (s.shard_rank + d) % s.shard_world;
+    int c0 = 0, cols = 0;
+    shard_block(n, s.shard_world, src, &c0, &cols);
+    if (src != s.shard_rank) MMX_CUDA(ctx, cudaStreamWaitEvent(s.stream, s.peer_ready[src], 0));
+    if (rows > 0 && cols > 0) MMX_CUDA(ctx, launch_matmul<T>(c, a, bt, n, r0, rows, c0, cols, strict, variant, s.stream));
+  }
+  MMX_CUDA(ctx, cudaEventRecord(s.ev_m1, s.stream));
+  MMX_CUDA(ctx, launch_trace<T>(static_cast<T*>(s.d_sum), c, n, r0, rows, strict, s.stream));
+  MMX_CUDA(ctx, cudaMemcpyAsync(s.h_sum, s.d_sum, sizeof(T), cudaMemcpyDeviceToHost, s.stream));
+  MMX_CUDA(ctx, cudaEventRecord(s.ev_end, s.stream));
+  return MMX_OK;
+}
+
+int shard_collect(mmx_ctx* ctx, Slot& s, mmx_shard_stats* out) {
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  MMX_CUDA(ctx, cudaStreamSynchronize(s.stream));
+  const int n = ctx->cfg.n;
+  for (int q : {MMX_ARRAY_A, MMX_ARRAY_B, MMX_ARRAY_C, MMX_ARRAY_BT}) {
+    s.dev_valid[q] = true;   // a and c: this member's rows only
+    s.host_valid[q] = false;
+  }
+  if (out == nullptr) return MMX_OK;
+  std::memset(out, 0, sizeof(*out));
+  out->rank = s.shard_rank;
+  out->world = s.shard_world;
+  shard_block(n, s.shard_world, s.shard_rank, &out->row0, &out->rows);
+  float ms = 0.f;
+  MMX_CUDA(ctx, cudaEventElapsedTime(&ms, s.ev_begin, s.ev_end));
+  out->gpu_ms = ms;
+  MMX_CUDA(ctx, cudaEventElapsedTime(&ms, s.ev_x0, s.ev_x1));
+  out->exchange_ms = ms;
+  MMX_CUDA(ctx, cudaEventElapsedTime(&ms, s.ev_m0, s.ev_m1));
+  out->matmul_ms = ms;
+  out->peer_bytes = static_cast<uint64_t>(out->rows) * n * elem_size(ctx->cfg.dtype) * (s.shard_world - 1);
+  out->partial_trace = ctx->cfg.dtype == MMX_F64 ? *static_cast<double*>(s.h_sum) : static_cast<double>(*static_cast<float*>(s.h_sum));
+  return MMX_OK;
+}
+
+bool shard_slot_ok(mmx_ctx* ctx, int slot) { return ctx != nullptr && slot >= 0 && slot < static_cast<int>(ctx->slots.size()); }
+
+}  // namespace
+}  // namespace mmx
+
+MMX_API int mmx_shard_export(mmx_ctx* ctx, int slot, mmx_shard_handle* out) {
+  if (!shard_slot_ok(ctx, slot) || out == nullptr) return MMX_E_INVALID;
+  static_assert(sizeof(cudaIpcMemHandle_t) == 64 && sizeof(cudaIpcEventHandle_t) == 64, "handle layout of mmx_shard_handle");
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  if (int rc = shard_events(ctx, s)) return rc;
+  cudaIpcMemHandle_t mh;
+  cudaIpcEventHandle_t eh;
+  MMX_CUDA(ctx, cudaIpcGetMemHandle(&mh, s.d_arr[MMX_ARRAY_BT]));
+  MMX_CUDA(ctx, cudaIpcGetEventHandle(&eh, s.ev_ready));
+  std::memcpy(out->mem, &mh, 64);
+  std::memcpy(out->event, &eh, 64);
+  return MMX_OK;
+}
+
+MMX_API int mmx_shard_bind(mmx_ctx* ctx, int slot, int rank, int world, const mmx_shard_handle* handles, const int32_t* local_slots) {
+  if (!shard_slot_ok(ctx, slot) || world < 1 || world > kMaxPeers || rank < 0 || rank >= world ||
+      ((handles == nullptr) == (local_slots == nullptr) && world > 1)) {
+    if (ctx) ctx->set_error("mmx_shard_bind: need 1 <= world <= 8, 0 <= rank < world and exactly one of handles / local_slots");
+    return MMX_E_INVALID;
+  }
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  if (int rc = shard_events(ctx, s)) return rc;
+  for (int r = 0; r < kMaxPeers; ++r) {  // drop an earlier binding
+    if (s.peer_ipc[r]) {
+      if (s.peer_bt[r]) cudaIpcCloseMemHandle(s.peer_bt[r]);
+      if (s.peer_ready[r]) cudaEventDestroy(s.peer_ready[r]);
+    }
+    s.peer_bt[r] = nullptr;
+    s.peer_ready[r] = nullptr;
+    s.peer_ipc[r] = false;
+  }
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) {
+      s.peer_bt[r] = s.d_arr[MMX_ARRAY_BT];
+      s.peer_ready[r] = s.ev_ready;
+    } else if (local_slots != nullptr) {
+      if (!shard_slot_ok(ctx, local_slots[r]) || local_slots[r] == slot) return MMX_E_INVALID;
+      Slot& o = *ctx->slots[local_slots[r]];
+      if (o.device != s.device) {
+        int can = 0;
+        MMX_CUDA(ctx, cudaDeviceCanAccessPeer(&can, s.device, o.device));
+        if (!can) {
+          ctx->set_error("mmx_shard_bind: devices " + std::to_string(s.device) + " and " + std::to_string(o.device) + " have no peer access");
+          return MMX_E_CUDA;
+        }
+        const cudaError_t e = cudaDeviceEnablePeerAccess(o.device, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) MMX_CUDA(ctx, e);
+        cudaGetLastError();
+      }
+      if (o.ev_ready == nullptr) {  // created on the owner's device
+        MMX_CUDA(ctx, cudaSetDevice(o.device));
+        if (int rc = shard_events(ctx, o)) return rc;
+        MMX_CUDA(ctx, cudaSetDevice(s.device));
+      }
+      s.peer_bt[r] = o.d_arr[MMX_ARRAY_BT];
+      s.peer_ready[r] = o.ev_ready;
+    } else {
+      cudaIpcMemHandle_t mh;
+      cudaIpcEventHandle_t eh;
+      std::memcpy(&mh, handles[r].mem, 64);
+      std::memcpy(&eh, handles[r].event, 64);
+      MMX_CUDA(ctx, cudaIpcOpenMemHandle(&s.peer_bt[r], mh, cudaIpcMemLazyEnablePeerAccess));
+      s.peer_ipc[r] = true;
+      MMX_CUDA(ctx, cudaIpcOpenEventHandle(&s.peer_ready[r], eh));
+    }
+  }
+  s.shard_rank = rank;
+  s.shard_world = world;
+  return MMX_OK;
+}
+
+MMX_API int mmx_shard_phase1(mmx_ctx* ctx, int slot) {
+  if (!shard_slot_ok(ctx, slot)) return MMX_E_INVALID;
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  if (s.shard_world < 1) {
+    ctx->set_error("mmx_shard_phase1: slot is not bound to a group (mmx_shard_bind)");
+    return MMX_E_STATE;
+  }
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  return ctx->cfg.dtype == MMX_F64 ? shard_phase1<double>(ctx, s) : shard_phase1<float>(ctx, s);
+}
+
+MMX_API int mmx_shard_phase2(mmx_ctx* ctx, int slot, mmx_shard_stats* out) {
+  if (!shard_slot_ok(ctx, slot)) return MMX_E_INVALID;
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  if (s.shard_world < 1) {
+    ctx->set_error("mmx_shard_phase2: slot is not bound to a group (mmx_shard_bind)");
+    return MMX_E_STATE;
+  }
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  if (int rc = ctx->cfg.dtype == MMX_F64 ? shard_phase2<double>(ctx, s) : shard_phase2<float>(ctx, s)) return rc;
+  return shard_collect(ctx, s, out);
+}
+
+MMX_API int mmx_shard_run_local(mmx_ctx* ctx, const int32_t* slots, int world, mmx_shard_stats* outs, double* checksum) {
+  if (ctx == nullptr || slots == nullptr || world < 1 || world > kMaxPeers) return MMX_E_INVALID;
+  for (int r = 0; r < world; ++r) {
+    if (!shard_slot_ok(ctx, slots[r])) return MMX_E_INVALID;
+    Slot& s = *ctx->slots[slots[r]];
+    bool bound = s.shard_rank == r && s.shard_world == world;
+    for (int q = 0; bound && q < world; ++q) bound = s.peer_bt[q] == ctx->slots[slots[q]]->d_arr[MMX_ARRAY_BT];
+    if (!bound)
+      if (int rc = mmx_shard_bind(ctx, slots[r], r, world, nullptr, world > 1 ? slots : nullptr)) return rc;
+  }
+  // every member's production phase is enqueued before any consumption phase: a member's contraction only
+  // waits on events that are already recorded
+  for (int r = 0; r < world; ++r)
+    if (int rc = mmx_shard_phase1(ctx, slots[r])) return rc;
+  std::vector<mmx_shard_stats> local(world);
+  for (int r = 0; r < world; ++r) {
+    Slot& s = *ctx->slots[slots[r]];
+    std::lock_guard<std::mutex> g(s.mu);
+    MMX_CUDA(ctx, cudaSetDevice(s.device));
+    if (int rc = ctx->cfg.dtype == MMX_F64 ? shard_phase2<double>(ctx, s) : shard_phase2<float>(ctx, s)) return rc;
+  }
+  double sum = 0.0;
+  float fsum = 0.f;
+  for (int r = 0; r < world; ++r) {
+    Slot& s = *ctx->slots[slots[r]];
+    std::lock_guard<std::mutex> g(s.mu);
+    if (int rc = shard_collect(ctx, s, &local[r])) return rc;
+    // rank order, in the context dtype: the association the program's own loop would use across the blocks
+    if (ctx->cfg.dtype == MMX_F64) sum += local[r].partial_trace;
+    else fsum += static_cast<float>(local[r].partial_trace);
+    if (outs != nullptr) outs[r] = local[r];
+  }
+  if (checksum != nullptr) *checksum = ctx->cfg.dtype == MMX_F64 ? sum : static_cast<double>(fsum);
+  return MMX_OK;
+}

@@ -30,15 +30,24 @@ template <typename T> cudaError_t launch_fill_row(int op, T* dst, int n, IterRef
 // gene 6: bt[i][j] = b[j][i] (matmul.c:21-23)
 // rows [row0, row0+rows) of bt only (= columns of b)
 template <typename T> cudaError_t launch_transpose(T* bt, const T* b, int n, int row0, int rows, cudaStream_t stream);
+// Row-sharded run: rows [row0, row0+rows) of bt are produced once and stored into the bt of
+// every GPU of the group (peer-mapped pointers; p[0..count) includes this GPU's own array).
+constexpr int kMaxPeers = 8;
+struct BtPeers {
+  void* p[kMaxPeers] = {};
+  int count = 0;
+};
+template <typename T> cudaError_t launch_transpose_push(const BtPeers& peers, const T* b, int n, int row0, int rows, cudaStream_t stream);
 // gene 7: row i of bt = column i of b
 template <typename T> cudaError_t launch_transpose_row(T* bt, const T* b, int n, IterRef iter, cudaStream_t stream);
 
 // gene 8: c[i][j] += sum_k a[i][k] * bt[j][k] (matmul.c:25-28).  variant: 1 SIMT, 2 DMMA (FP64 only).
-// Rows [row0, row0+rows) of a and c only (row0 = 0, rows = n for the whole nest; the
-// row-sharded multi-GPU path passes its block).
+// Rows [row0, row0+rows) of a and c, columns [col0, col0+cols) of c (= rows of bt) only: the whole nest is
+// (0, n, 0, n); the row-sharded multi-GPU path passes its row block and walks the column blocks in the
+// order the owners' rows of bt arrive.
 template <typename T>
-cudaError_t launch_matmul(T* c, const T* a, const T* bt, int n, int row0, int rows, bool strict, int variant,
-                          cudaStream_t stream);
+cudaError_t launch_matmul(T* c, const T* a, const T* bt, int n, int row0, int rows, int col0, int cols, bool strict,
+                          int variant, cudaStream_t stream);
 // gene 9: row i of the same (GEMV against bt)
 template <typename T>
 cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, bool strict, cudaStream_t stream);

@@ -81,7 +81,7 @@ __device__ __forceinline__ void load_row8(T (&dst)[8], const T* __restrict__ bas
 template <typename T, bool STRICT>
 __global__ void __launch_bounds__(256, 1)
 matmul_simt_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ bt, int n, int row0, int rows,
-                   bool vec_ok) {
+                   int col0, int cols, bool vec_ok) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* As = reinterpret_cast<T*>(smem_raw);  // [2][BK][BM]
   T* Bs = As + 2 * BK * BM;                // [2][BK][BN]
@@ -89,8 +89,8 @@ matmul_simt_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restri
   const int tid = threadIdx.x;
   const int tx = tid % 16, ty = tid / 16;
   const int m_base = row0 + blockIdx.y * BM;  // first row of a / c of this CTA
-  const int n_base = blockIdx.x * BN;         // first row of bt == first column of c
-  const int m_limit = row0 + rows;
+  const int n_base = col0 + blockIdx.x * BN;  // first row of bt == first column of c
+  const int m_limit = row0 + rows, n_limit = col0 + cols;
 
   // global -> smem staging role: one row, 8 consecutive k
   const int ld_row = tid % 128;
@@ -103,13 +103,13 @@ matmul_simt_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restri
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int j = n_base + (q / 4) * 64 + tx * 4 + (q % 4);
-      acc[r][q] = (m < m_limit && j < n) ? c[static_cast<size_t>(m) * n + j] : static_cast<T>(0.0);
+      acc[r][q] = (m < m_limit && j < n_limit) ? c[static_cast<size_t>(m) * n + j] : static_cast<T>(0.0);
     }
   }
 
   T ra[8], rb[8];
   load_row8(ra, a, m_base + ld_row, m_limit, ld_k, n, vec_ok);
-  load_row8(rb, bt, n_base + ld_row, n, ld_k, n, vec_ok);
+  load_row8(rb, bt, n_base + ld_row, n_limit, ld_k, n, vec_ok);
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
     As[(ld_k + q) * BM + ld_row] = ra[q];
@@ -123,7 +123,7 @@ matmul_simt_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restri
     const bool more = t + 1 < k_tiles;
     if (more) {
       load_row8(ra, a, m_base + ld_row, m_limit, (t + 1) * BK + ld_k, n, vec_ok);
-      load_row8(rb, bt, n_base + ld_row, n, (t + 1) * BK + ld_k, n, vec_ok);
+      load_row8(rb, bt, n_base + ld_row, n_limit, (t + 1) * BK + ld_k, n, vec_ok);
     }
     const T* Ac = As + cur * BK * BM;
     const T* Bc = Bs + cur * BK * BN;
@@ -175,7 +175,7 @@ matmul_simt_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restri
     for (int h = 0; h < 2; ++h) {
       const int j = n_base + h * 64 + tx * 4;
       T* dst = c + static_cast<size_t>(m) * n + j;
-      if (vec_ok && j + 4 <= n) {
+      if (vec_ok && j + 4 <= n_limit) {
         using VT = typename V16<T>::type;
         if constexpr (sizeof(T) == 8) {
           reinterpret_cast<VT*>(dst)[0] = make_double2(acc[r][h * 4], acc[r][h * 4 + 1]);
@@ -186,7 +186,7 @@ matmul_simt_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restri
       } else {
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-          if (j + q < n) dst[q] = acc[r][h * 4 + q];
+          if (j + q < n_limit) dst[q] = acc[r][h * 4 + q];
       }
     }
   }
@@ -218,7 +218,7 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 template <int DK, int DSTAGES, int WM, int WN, int MT, int NT>
 __global__ void __launch_bounds__(32 * WM * WN)
 matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const double* __restrict__ bt, int n,
-                   int row0, int rows) {
+                   int row0, int rows, int col0, int cols) {
   constexpr int THREADS = 32 * WM * WN;
   constexpr int TM = WM * MT * 8, TN = WN * NT * 8;
   constexpr int DLD = DK + 4;  // padded row: (DK+4)*8 B = 32 mod 128 for DK in {16, 32} => conflict-free fragments
@@ -228,8 +228,8 @@ matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const d
 
   const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
   const int wm = warp / WN, wn = warp % WN;
-  const int m_base = row0 + blockIdx.y * TM, n_base = blockIdx.x * TN;
-  const int m_limit = row0 + rows;
+  const int m_base = row0 + blockIdx.y * TM, n_base = col0 + blockIdx.x * TN;
+  const int m_limit = row0 + rows, n_limit = col0 + cols;  // col0, cols even
   const int g = lane / 4, t4 = lane % 4;   // fragment row, fragment k
 
   // cp.async role: rows x DK/2 chunks of 16 B per operand
@@ -248,7 +248,7 @@ matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const d
       const int chunk = tid + it * THREADS;
       const int row = chunk / CPR, kc = (chunk % CPR) * 2;
       const int br = n_base + row;
-      const bool bv = k0 + kc < n && br < n;
+      const bool bv = k0 + kc < n && br < n_limit;
       cp_async16(Bs + (stage * TN + row) * DLD + kc, bv ? bt + static_cast<size_t>(br) * n + k0 + kc : bt, bv);
     }
   };
@@ -268,7 +268,7 @@ matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const d
     for (int j = 0; j < NT; ++j) {
       const int m = m_base + (wm * MT + i) * 8 + g;
       const int col = n_base + (wn * NT + j) * 8 + t4 * 2;
-      const bool ok = m < m_limit && col < n;  // n even => col+1 < n too
+      const bool ok = m < m_limit && col < n_limit;  // n_limit even => col+1 < n_limit too
       const double2 v = ok ? *reinterpret_cast<const double2*>(c + static_cast<size_t>(m) * n + col) : make_double2(0.0, 0.0);
       acc[i][j][0] = v.x;
       acc[i][j][1] = v.y;
@@ -305,7 +305,7 @@ matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const d
     for (int j = 0; j < NT; ++j) {
       const int m = m_base + (wm * MT + i) * 8 + g;
       const int col = n_base + (wn * NT + j) * 8 + t4 * 2;
-      if (m < m_limit && col < n)
+      if (m < m_limit && col < n_limit)
         *reinterpret_cast<double2*>(c + static_cast<size_t>(m) * n + col) = make_double2(acc[i][j][0], acc[i][j][1]);
     }
 }
@@ -328,7 +328,8 @@ matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const d
 // min-blocks hint: cap FP32 at 128 registers (16 warps per SM whatever the CTA size); FP64 needs ~250
 template <typename T, bool STRICT, bool FULL, int TM, int TN, int STAGES>
 __global__ void __launch_bounds__((TM / 8) * (TN / 8), (sizeof(T) == 4 ? 512 : 256) / ((TM / 8) * (TN / 8)))
-matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ bt, int n, int row0, int rows) {
+matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ bt, int n, int row0, int rows,
+                    int col0, int cols) {
   using VT = typename V16<T>::type;
   constexpr int W = V16<T>::W;           // elements per 16-byte chunk
   constexpr int LD = BK + W;             // padded row length (elements): +16 bytes
@@ -343,8 +344,8 @@ matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restr
   const int lane = tid % 32, warp = tid / 32;
   constexpr int WX = TX / 8;                // warps along n
   const int tx = (warp % WX) * 8 + lane % 8, ty = (warp / WX) * 4 + lane / 8;
-  const int m_base = row0 + blockIdx.y * TM, n_base = blockIdx.x * TN;
-  const int m_limit = row0 + rows;
+  const int m_base = row0 + blockIdx.y * TM, n_base = col0 + blockIdx.x * TN;
+  const int m_limit = row0 + rows, n_limit = col0 + cols;
 
   auto issue_stage = [&](int stage, int k0) {
 #pragma unroll
@@ -360,7 +361,7 @@ matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restr
       const int chunk = tid + it * THREADS;
       const int row = chunk / CPR, kc = (chunk % CPR) * W;
       const int br = n_base + row;
-      const bool bv = FULL || (k0 + kc < n && br < n);
+      const bool bv = FULL || (k0 + kc < n && br < n_limit);
       cp_async16(Bs + (stage * TN + row) * LD + kc, bv ? bt + static_cast<size_t>(br) * n + k0 + kc : bt, bv);
     }
   };
@@ -378,7 +379,7 @@ matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restr
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int m = m_base + ty + TY * r, j = n_base + tx + TX * q;
-      acc[r][q] = (FULL || (m < m_limit && j < n)) ? c[static_cast<size_t>(m) * n + j] : static_cast<T>(0.0);
+      acc[r][q] = (FULL || (m < m_limit && j < n_limit)) ? c[static_cast<size_t>(m) * n + j] : static_cast<T>(0.0);
     }
 
   for (int t = 0; t < k_tiles; ++t) {
@@ -424,12 +425,12 @@ matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restr
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
       const int m = m_base + ty + TY * r, j = n_base + tx + TX * q;
-      if (FULL || (m < m_limit && j < n)) c[static_cast<size_t>(m) * n + j] = acc[r][q];
+      if (FULL || (m < m_limit && j < n_limit)) c[static_cast<size_t>(m) * n + j] = acc[r][q];
     }
 }
 
 template <typename T, bool STRICT, int TM, int TN, int STAGES>
-cudaError_t simt2_go(T* c, const T* a, const T* bt, int n, int row0, int rows, cudaStream_t stream) {
+cudaError_t simt2_go(T* c, const T* a, const T* bt, int n, int row0, int rows, int col0, int cols, cudaStream_t stream) {
   constexpr int W = V16<T>::W;
   constexpr int THREADS = (TM / 8) * (TN / 8);
   const size_t smem = static_cast<size_t>(STAGES) * (TM + TN) * (BK + W) * sizeof(T);
@@ -443,15 +444,15 @@ cudaError_t simt2_go(T* c, const T* a, const T* bt, int n, int row0, int rows, c
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((n + TN - 1) / TN, (rows + TM - 1) / TM);
-  const bool full = n % TN == 0 && rows % TM == 0 && n % BK == 0;
-  if (full) matmul_simt2_kernel<T, STRICT, true, TM, TN, STAGES><<<grid, THREADS, smem, stream>>>(c, a, bt, n, row0, rows);
-  else matmul_simt2_kernel<T, STRICT, false, TM, TN, STAGES><<<grid, THREADS, smem, stream>>>(c, a, bt, n, row0, rows);
+  dim3 grid((cols + TN - 1) / TN, (rows + TM - 1) / TM);
+  const bool full = cols % TN == 0 && rows % TM == 0 && n % BK == 0;
+  if (full) matmul_simt2_kernel<T, STRICT, true, TM, TN, STAGES><<<grid, THREADS, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols);
+  else matmul_simt2_kernel<T, STRICT, false, TM, TN, STAGES><<<grid, THREADS, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols);
   return cudaGetLastError();
 }
 
 template <typename T, bool STRICT>
-cudaError_t simt_go(T* c, const T* a, const T* bt, int n, int row0, int rows, cudaStream_t stream) {
+cudaError_t simt_go(T* c, const T* a, const T* bt, int n, int row0, int rows, int col0, int cols, cudaStream_t stream) {
   const size_t smem = 2 * BK * (BM + BN) * sizeof(T);
   static bool configured = false;  // per instantiation; benign race (idempotent)
   if (!configured) {
@@ -459,14 +460,14 @@ cudaError_t simt_go(T* c, const T* a, const T* bt, int n, int row0, int rows, cu
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((n + BN - 1) / BN, (rows + BM - 1) / BM);
-  const bool vec_ok = n % V16<T>::W == 0;
-  matmul_simt_kernel<T, STRICT><<<grid, 256, smem, stream>>>(c, a, bt, n, row0, rows, vec_ok);
+  dim3 grid((cols + BN - 1) / BN, (rows + BM - 1) / BM);
+  const bool vec_ok = n % V16<T>::W == 0 && col0 % V16<T>::W == 0;
+  matmul_simt_kernel<T, STRICT><<<grid, 256, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols, vec_ok);
   return cudaGetLastError();
 }
 
 template <int DK, int DSTAGES, int WM, int WN, int MT, int NT>
-cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row0, int rows, cudaStream_t stream) {
+cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row0, int rows, int col0, int cols, cudaStream_t stream) {
   constexpr int TM = WM * MT * 8, TN = WN * NT * 8;
   const size_t smem = static_cast<size_t>(DSTAGES) * (TM + TN) * (DK + 4) * sizeof(double);
   static bool configured = false;
@@ -476,45 +477,45 @@ cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((n + TN - 1) / TN, (rows + TM - 1) / TM);
-  matmul_dmma_kernel<DK, DSTAGES, WM, WN, MT, NT><<<grid, 32 * WM * WN, smem, stream>>>(c, a, bt, n, row0, rows);
+  dim3 grid((cols + TN - 1) / TN, (rows + TM - 1) / TM);
+  matmul_dmma_kernel<DK, DSTAGES, WM, WN, MT, NT><<<grid, 32 * WM * WN, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 template <>
-cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, int n, int row0, int rows, bool strict,
-                                  int variant, cudaStream_t stream) {
+cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, int n, int row0, int rows, int col0, int cols,
+                                  bool strict, int variant, cudaStream_t stream) {
   if (strict) {
-    if (n % 2 == 0 && variant == 20) return simt2_go<double, true, 128, 128, 4>(c, a, bt, n, row0, rows, stream);
-    if (n % 2 == 0 && variant != 1) return simt2_go<double, true, 64, 64, 3>(c, a, bt, n, row0, rows, stream);
-    return simt_go<double, true>(c, a, bt, n, row0, rows, stream);
+    if (n % 2 == 0 && variant == 20) return simt2_go<double, true, 128, 128, 4>(c, a, bt, n, row0, rows, col0, cols, stream);
+    if (n % 2 == 0 && variant != 1) return simt2_go<double, true, 64, 64, 3>(c, a, bt, n, row0, rows, col0, cols, stream);
+    return simt_go<double, true>(c, a, bt, n, row0, rows, col0, cols, stream);
   }
-  if (n % 2 == 0) {
+  if (n % 2 == 0 && col0 % 2 == 0 && cols % 2 == 0) {  // 16-byte aligned double2 accesses of c
     switch (variant) {
-      case 2: return dmma_go<16, 3, 2, 4, 8, 4>(c, a, bt, n, row0, rows, stream);   // 128x128, BK=16 (first tuning point)
-      case 5: return dmma_go<32, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);   // 64x64
-      case 6: return dmma_go<32, 3, 2, 2, 2, 2>(c, a, bt, n, row0, rows, stream);   // 32x32
-      case 7: return dmma_go<32, 3, 2, 4, 8, 4>(c, a, bt, n, row0, rows, stream);   // 128x128, BK=32
-      case 8: return dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);   // 64x64, BK=16
-      case 9: return dmma_go<16, 4, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);   // 64x64, BK=16, 4 stages
-      case 10: return dmma_go<32, 2, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);  // 64x64, BK=32, 2 stages
-      case 11: return dmma_go<32, 3, 2, 2, 8, 4>(c, a, bt, n, row0, rows, stream);  // 128x64, 4 warps
-      case 12: return dmma_go<32, 3, 1, 4, 8, 2>(c, a, bt, n, row0, rows, stream);  // 64x64 as 1x4 warps of 64x16
-      case 13: return dmma_go<32, 3, 2, 2, 4, 8>(c, a, bt, n, row0, rows, stream);  // 64x128, 4 warps
+      case 2: return dmma_go<16, 3, 2, 4, 8, 4>(c, a, bt, n, row0, rows, col0, cols, stream);   // 128x128, BK=16 (first tuning point)
+      case 5: return dmma_go<32, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, stream);   // 64x64
+      case 6: return dmma_go<32, 3, 2, 2, 2, 2>(c, a, bt, n, row0, rows, col0, cols, stream);   // 32x32
+      case 7: return dmma_go<32, 3, 2, 4, 8, 4>(c, a, bt, n, row0, rows, col0, cols, stream);   // 128x128, BK=32
+      case 8: return dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, stream);   // 64x64, BK=16
+      case 9: return dmma_go<16, 4, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, stream);   // 64x64, BK=16, 4 stages
+      case 10: return dmma_go<32, 2, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, stream);  // 64x64, BK=32, 2 stages
+      case 11: return dmma_go<32, 3, 2, 2, 8, 4>(c, a, bt, n, row0, rows, col0, cols, stream);  // 128x64, 4 warps
+      case 12: return dmma_go<32, 3, 1, 4, 8, 2>(c, a, bt, n, row0, rows, col0, cols, stream);  // 64x64 as 1x4 warps of 64x16
+      case 13: return dmma_go<32, 3, 2, 2, 4, 8>(c, a, bt, n, row0, rows, col0, cols, stream);  // 64x128, 4 warps
       case 4:  // auto: the largest tile that still gives every SM work (N=256 would be a 2x2 grid of 128-tiles)
-        if (n <= 1024) return dmma_go<32, 3, 2, 2, 2, 2>(c, a, bt, n, row0, rows, stream);
-        return dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, stream);
+        if (n <= 1024) return dmma_go<32, 3, 2, 2, 2, 2>(c, a, bt, n, row0, rows, col0, cols, stream);
+        return dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, stream);
       default: break;
     }
   }
-  return simt_go<double, false>(c, a, bt, n, row0, rows, stream);
+  return simt_go<double, false>(c, a, bt, n, row0, rows, col0, cols, stream);
 }
 
 template <>
-cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int n, int row0, int rows, bool strict,
-                                 int variant, cudaStream_t stream) {
+cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int n, int row0, int rows, int col0, int cols,
+                                 bool strict, int variant, cudaStream_t stream) {
   // variant 1 keeps the first-generation kernel (k-major smem, register-staged) for A/B runs and
   // for n % 4 != 0, where rows are not 16-byte aligned
   if (variant != 1 && n % 4 == 0) {
@@ -522,14 +523,14 @@ cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int 
     // stages): it is limited by register-bank dispatch stalls and LDS issue, so the big tile stays.
     // Small matrices still get the 64x64 tile so that N=256 is 16 CTAs, not 4.
     if (strict) {
-      if (n <= 1024) return simt2_go<float, true, 64, 64, 4>(c, a, bt, n, row0, rows, stream);
-      return simt2_go<float, true, 128, 128, 4>(c, a, bt, n, row0, rows, stream);
+      if (n <= 1024) return simt2_go<float, true, 64, 64, 4>(c, a, bt, n, row0, rows, col0, cols, stream);
+      return simt2_go<float, true, 128, 128, 4>(c, a, bt, n, row0, rows, col0, cols, stream);
     }
-    if (variant == 22 || (variant != 20 && n <= 1024)) return simt2_go<float, false, 64, 64, 4>(c, a, bt, n, row0, rows, stream);
-    return simt2_go<float, false, 128, 128, 4>(c, a, bt, n, row0, rows, stream);
+    if (variant == 22 || (variant != 20 && n <= 1024)) return simt2_go<float, false, 64, 64, 4>(c, a, bt, n, row0, rows, col0, cols, stream);
+    return simt2_go<float, false, 128, 128, 4>(c, a, bt, n, row0, rows, col0, cols, stream);
   }
-  if (strict) return simt_go<float, true>(c, a, bt, n, row0, rows, stream);
-  return simt_go<float, false>(c, a, bt, n, row0, rows, stream);
+  if (strict) return simt_go<float, true>(c, a, bt, n, row0, rows, col0, cols, stream);
+  return simt_go<float, false>(c, a, bt, n, row0, rows, col0, cols, stream);
 }
 
 }  // namespace mmx

@@ -34,9 +34,12 @@ __device__ __forceinline__ void transpose_micro(const float4 (&in)[4], float4 (&
   out[3] = make_float4(in[0].w, in[1].w, in[2].w, in[3].w);
 }
 
-// grid = (n/64, n/64); block = 256 threads.
-template <typename T>
-__global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt, const T* __restrict__ b, int n, int first_row) {
+// grid = (rows/64, n/64); block = 256 threads.  PUSH: the finished tile is stored into every destination
+// of `peers` (this GPU's bt and, through peer-mapped pointers, the bt of every other GPU of a row-sharded
+// run): the all-gather of bt happens inside the kernel that produces it, as NVLink stores.
+template <typename T, bool PUSH>
+__global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt, const T* __restrict__ b, int n, int first_row,
+                                                             BtPeers peers) {
   using VT = typename VecOf<T>::type;
   constexpr int V = VecOf<T>::V;
   constexpr int MB = kTile / V;         // micro-blocks per tile side == 16-byte chunks per tile row
@@ -71,14 +74,19 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
     const int out_row = v / MB;
     const int chunk = v % MB;
     const VT val = tile[out_row * MB + (chunk ^ ((out_row / V) & 7))];
-    *reinterpret_cast<VT*>(bt + static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V) = val;
+    const size_t at = static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V;
+    if constexpr (PUSH) {
+      for (int d = 0; d < peers.count; ++d) *reinterpret_cast<VT*>(static_cast<T*>(peers.p[d]) + at) = val;
+    } else {
+      *reinterpret_cast<VT*>(bt + at) = val;
+    }
   }
 }
 
 // Any n: 32x32 tile, scalar accesses, +1 padding.  block = (32, 8).
-template <typename T>
+template <typename T, bool PUSH>
 __global__ void __launch_bounds__(256) transpose_generic_kernel(T* __restrict__ bt, const T* __restrict__ b, int n,
-                                                                int first_row, int row_limit) {
+                                                                int first_row, int row_limit, BtPeers peers) {
   __shared__ T tile[32][33];
   const int x = first_row + blockIdx.x * 32 + threadIdx.x;  // column of b = row of bt
 #pragma unroll
@@ -91,7 +99,15 @@ __global__ void __launch_bounds__(256) transpose_generic_kernel(T* __restrict__ 
 #pragma unroll
   for (int r = threadIdx.y; r < 32; r += 8) {
     const int oy = first_row + blockIdx.x * 32 + r;  // row of bt = column of b
-    if (ox < n && oy < row_limit) bt[static_cast<size_t>(oy) * n + ox] = tile[threadIdx.x][r];
+    if (ox < n && oy < row_limit) {
+      const T val = tile[threadIdx.x][r];
+      const size_t at = static_cast<size_t>(oy) * n + ox;
+      if constexpr (PUSH) {
+        for (int d = 0; d < peers.count; ++d) static_cast<T*>(peers.p[d])[at] = val;
+      } else {
+        bt[at] = val;
+      }
+    }
   }
 }
 
@@ -110,10 +126,24 @@ cudaError_t launch_transpose(T* bt, const T* b, int n, int row0, int rows, cudaS
   if (rows <= 0) return cudaSuccess;
   if (n % kTile == 0 && row0 % kTile == 0 && rows % kTile == 0) {
     dim3 grid(rows / kTile, n / kTile);
-    transpose_tile_kernel<T><<<grid, 256, 0, stream>>>(bt, b, n, row0);
+    transpose_tile_kernel<T, false><<<grid, 256, 0, stream>>>(bt, b, n, row0, BtPeers{});
   } else {
     dim3 grid((rows + 31) / 32, (n + 31) / 32);
-    transpose_generic_kernel<T><<<grid, dim3(32, 8), 0, stream>>>(bt, b, n, row0, row0 + rows);
+    transpose_generic_kernel<T, false><<<grid, dim3(32, 8), 0, stream>>>(bt, b, n, row0, row0 + rows, BtPeers{});
+  }
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_transpose_push(const BtPeers& peers, const T* b, int n, int row0, int rows, cudaStream_t stream) {
+  if (rows <= 0) return cudaSuccess;
+  if (peers.count < 1 || peers.count > kMaxPeers) return cudaErrorInvalidValue;
+  if (n % kTile == 0 && row0 % kTile == 0 && rows % kTile == 0) {
+    dim3 grid(rows / kTile, n / kTile);
+    transpose_tile_kernel<T, true><<<grid, 256, 0, stream>>>(nullptr, b, n, row0, peers);
+  } else {
+    dim3 grid((rows + 31) / 32, (n + 31) / 32);
+    transpose_generic_kernel<T, true><<<grid, dim3(32, 8), 0, stream>>>(nullptr, b, n, row0, row0 + rows, peers);
   }
   return cudaGetLastError();
 }
@@ -127,6 +157,8 @@ cudaError_t launch_transpose_row(T* bt, const T* b, int n, IterRef iter, cudaStr
 
 template cudaError_t launch_transpose<double>(double*, const double*, int, int, int, cudaStream_t);
 template cudaError_t launch_transpose<float>(float*, const float*, int, int, int, cudaStream_t);
+template cudaError_t launch_transpose_push<double>(const BtPeers&, const double*, int, int, int, cudaStream_t);
+template cudaError_t launch_transpose_push<float>(const BtPeers&, const float*, int, int, int, cudaStream_t);
 template cudaError_t launch_transpose_row<double>(double*, const double*, int, IterRef, cudaStream_t);
 template cudaError_t launch_transpose_row<float>(float*, const float*, int, IterRef, cudaStream_t);
 
