@@ -106,7 +106,9 @@ typedef struct mmx_config {
   const int32_t* devices;   /* CUDA ordinal per slot; NULL = slot s -> device s % deviceCount  */
   int32_t host_threads;     /* threads for CPU-mapped nests; 1 = the reference program         */
   int32_t launch_batching;  /* 1: inner-loop launch trains are submitted as CUDA graphs        */
-  int32_t matmul_variant;   /* 0 auto, 1 SIMT FMA, 2 tensor (DMMA) -- FP64 gene-8 kernel choice */
+  int32_t matmul_variant;   /* gene-8 kernel: 0 auto (FP64: DMMA, tile by N; FP32: tcgen05 split-TF32 with compensated
+                             * accumulation for N >= 1024, FFMA below); 1 first SIMT kernel; 2, 4-13 DMMA tile shapes (FP64);
+                             * 20, 22 SIMT tile shapes; 30 FP32 tcgen05 at any N % 4 == 0; 31 its wide-tile uncompensated form */
   int32_t warmup;           /* untimed runs per genome before the timed repetitions (default 0) */
 } mmx_config;
 

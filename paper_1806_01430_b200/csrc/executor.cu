@@ -47,6 +47,7 @@ struct Slot {
   int* d_iter = nullptr;
   void* d_scrub = nullptr;
   std::size_t scrub_bytes = 0;
+  void* d_scratch = nullptr;  // FP32 FAST: split operands of the tensor-core contraction (matmul_tc.cu)
   bool host_valid[MMX_NUM_ARRAYS] = {};
   bool dev_valid[MMX_NUM_ARRAYS] = {};
   bool host_diag_only = false;  // host c holds only its diagonal
@@ -128,8 +129,8 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
     case 7: return launch_transpose_row<T>(bt, b, n, iter, s.stream);
     case 8: {
       int variant = ctx->cfg.matmul_variant;
-      if (variant == 0) variant = 4;  // auto: DMMA, BK=32, 3 stages (best of the tuning points, profiles/)
-      return launch_matmul<T>(c, a, bt, n, row0, rows, 0, n, strict, variant, s.stream);
+      if (variant == 0 && sizeof(T) == 8) variant = 4;  // FP64 auto: DMMA, tile by size (best of the tuning points, profiles/)
+      return launch_matmul<T>(c, a, bt, n, row0, rows, 0, n, strict, variant, s.d_scratch, s.stream);
     }
     case 9: return launch_gemv_row<T>(c, a, bt, n, iter, strict, s.stream);
     case 10: return launch_dot<T>(c, a, bt, n, iter, strict, s.stream);
@@ -512,6 +513,7 @@ void destroy_slot(Slot& s) {
   if (s.h_sum) cudaFreeHost(s.h_sum);
   if (s.d_iter) cudaFree(s.d_iter);
   if (s.d_scrub) cudaFree(s.d_scrub);
+  if (s.d_scratch) cudaFree(s.d_scratch);
   if (s.ev_begin) cudaEventDestroy(s.ev_begin);
   if (s.ev_end) cudaEventDestroy(s.ev_end);
   for (int r = 0; r < kMaxPeers; ++r)
@@ -623,6 +625,13 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
     if ((e = cudaEventCreate(&sl.ev_end)) != cudaSuccess) return fail(e, "cudaEventCreate");
     for (int q = 0; q < MMX_NUM_ARRAYS; ++q)
       if ((e = cudaMalloc(&sl.d_arr[q], mbytes)) != cudaSuccess) return fail(e, "cudaMalloc(array)");
+    // allocated up front: whole individuals are captured into CUDA graphs, where cudaMalloc is not allowed
+    if (cfg->dtype == MMX_F32 && cfg->numerics == MMX_NUMERICS_FAST && matmul_3xtf32_usable(cfg->n) &&
+        (cfg->matmul_variant == 30 || cfg->matmul_variant == 31 || (cfg->matmul_variant == 0 && cfg->n >= kTcMinN)))
+    {
+      if ((e = matmul_3xtf32_prepare()) != cudaSuccess) return fail(e, "matmul_3xtf32_prepare");
+      if ((e = cudaMalloc(&sl.d_scratch, matmul_3xtf32_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
+    }
     if ((e = cudaMalloc(&sl.d_sum, 16)) != cudaSuccess) return fail(e, "cudaMalloc(sum)");
     if ((e = cudaMalloc(reinterpret_cast<void**>(&sl.d_iter), sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(iter)");
     if ((e = cudaHostAlloc(&sl.h_sum, 16, cudaHostAllocDefault)) != cudaSuccess) return fail(e, "cudaHostAlloc(sum)");
@@ -903,7 +912,7 @@ int shard_phase2(mmx_ctx* ctx, Slot& s) {
   const int n = ctx->cfg.n;
   const bool strict = ctx->cfg.numerics == MMX_NUMERICS_STRICT;
   int variant = ctx->cfg.matmul_variant;
-  if (variant == 0) variant = 4;
+  if (variant == 0 && sizeof(T) == 8) variant = 4;
   int r0 = 0, rows = 0;
   shard_block(n, s.shard_world, s.shard_rank, &r0, &rows);
   T* a = static_cast<T*>(s.d_arr[MMX_ARRAY_A]);
@@ -915,7 +924,7 @@ int shard_phase2(mmx_ctx* ctx, Slot& s) {
     int c0 = 0, cols = 0;
     shard_block(n, s.shard_world, src, &c0, &cols);
     if (src != s.shard_rank) MMX_CUDA(ctx, cudaStreamWaitEvent(s.stream, s.peer_ready[src], 0));
-    if (rows > 0 && cols > 0) MMX_CUDA(ctx, launch_matmul<T>(c, a, bt, n, r0, rows, c0, cols, strict, variant, s.stream));
+    if (rows > 0 && cols > 0) MMX_CUDA(ctx, launch_matmul<T>(c, a, bt, n, r0, rows, c0, cols, strict, variant, s.d_scratch, s.stream));
   }
   MMX_CUDA(ctx, cudaEventRecord(s.ev_m1, s.stream));
   MMX_CUDA(ctx, launch_trace<T>(static_cast<T*>(s.d_sum), c, n, r0, rows, strict, s.stream));

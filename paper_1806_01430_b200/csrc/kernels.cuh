@@ -14,6 +14,17 @@
 namespace mmx {
 
 // Which iteration of the enclosing host loop(s) a launch serves: value = off + (base ? *base : 0).
+// cudaFuncSetAttribute applies to the current device only: one flag per device ordinal (a context may own
+// slots on all 8 GPUs of a box)
+struct PerDeviceOnce {
+  bool done[64] = {};
+  bool& here() {
+    int d = 0;
+    cudaGetDevice(&d);
+    return done[d & 63];
+  }
+};
+
 struct IterRef {
   const int* base;  // device pointer or nullptr
   int off;
@@ -45,9 +56,20 @@ template <typename T> cudaError_t launch_transpose_row(T* bt, const T* b, int n,
 // Rows [row0, row0+rows) of a and c, columns [col0, col0+cols) of c (= rows of bt) only: the whole nest is
 // (0, n, 0, n); the row-sharded multi-GPU path passes its row block and walks the column blocks in the
 // order the owners' rows of bt arrive.
+// `scratch` (may be NULL): matmul_3xtf32_scratch_bytes(n) bytes of device memory; with it, FP32 FAST
+// launches at n >= kTcMinN (or variants 30 / 31) run on the tcgen05 tensor cores (matmul_tc.cu).
 template <typename T>
 cudaError_t launch_matmul(T* c, const T* a, const T* bt, int n, int row0, int rows, int col0, int cols, bool strict,
-                          int variant, cudaStream_t stream);
+                          int variant, void* scratch, cudaStream_t stream);
+
+// FP32 on the 5th-generation tensor cores as three TF32 products per term with two-level accumulation
+constexpr int kTcMinN = 1024;
+bool matmul_3xtf32_usable(int n);
+size_t matmul_3xtf32_scratch_bytes(int n);
+cudaError_t matmul_3xtf32_prepare();  // per device, before the first launch (not inside a stream capture)
+// wide: 128 x 256 tile with plain FP32 masters (faster, looser); default 128 x 128 with compensated masters
+cudaError_t launch_matmul_3xtf32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0,
+                                 int cols, bool wide, cudaStream_t stream);
 // gene 9: row i of the same (GEMV against bt)
 template <typename T>
 cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, bool strict, cudaStream_t stream);

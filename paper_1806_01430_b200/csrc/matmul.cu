@@ -434,7 +434,8 @@ cudaError_t simt2_go(T* c, const T* a, const T* bt, int n, int row0, int rows, i
   constexpr int W = V16<T>::W;
   constexpr int THREADS = (TM / 8) * (TN / 8);
   const size_t smem = static_cast<size_t>(STAGES) * (TM + TN) * (BK + W) * sizeof(T);
-  static bool configured = false;
+  static PerDeviceOnce once;  // function attributes are per device
+  bool& configured = once.here();
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(matmul_simt2_kernel<T, STRICT, true, TM, TN, STAGES>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -454,7 +455,8 @@ cudaError_t simt2_go(T* c, const T* a, const T* bt, int n, int row0, int rows, i
 template <typename T, bool STRICT>
 cudaError_t simt_go(T* c, const T* a, const T* bt, int n, int row0, int rows, int col0, int cols, cudaStream_t stream) {
   const size_t smem = 2 * BK * (BM + BN) * sizeof(T);
-  static bool configured = false;  // per instantiation; benign race (idempotent)
+  static PerDeviceOnce once;  // function attributes are per device
+  bool& configured = once.here();
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(matmul_simt_kernel<T, STRICT>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     if (e != cudaSuccess) return e;
@@ -470,7 +472,8 @@ template <int DK, int DSTAGES, int WM, int WN, int MT, int NT>
 cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row0, int rows, int col0, int cols, cudaStream_t stream) {
   constexpr int TM = WM * MT * 8, TN = WN * NT * 8;
   const size_t smem = static_cast<size_t>(DSTAGES) * (TM + TN) * (DK + 4) * sizeof(double);
-  static bool configured = false;
+  static PerDeviceOnce once;  // function attributes are per device
+  bool& configured = once.here();
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(matmul_dmma_kernel<DK, DSTAGES, WM, WN, MT, NT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
@@ -486,7 +489,7 @@ cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row
 
 template <>
 cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, int n, int row0, int rows, int col0, int cols,
-                                  bool strict, int variant, cudaStream_t stream) {
+                                  bool strict, int variant, void* /*scratch*/, cudaStream_t stream) {
   if (strict) {
     if (n % 2 == 0 && variant == 20) return simt2_go<double, true, 128, 128, 4>(c, a, bt, n, row0, rows, col0, cols, stream);
     if (n % 2 == 0 && variant != 1) return simt2_go<double, true, 64, 64, 3>(c, a, bt, n, row0, rows, col0, cols, stream);
@@ -515,7 +518,10 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
 
 template <>
 cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int n, int row0, int rows, int col0, int cols,
-                                 bool strict, int variant, cudaStream_t stream) {
+                                 bool strict, int variant, void* scratch, cudaStream_t stream) {
+  // tensor cores (split-precision TF32, matmul_tc.cu): large matrices by default, any n % 4 == 0 on request
+  if (!strict && scratch != nullptr && n % 4 == 0 && (variant == 30 || variant == 31 || (variant == 0 && n >= kTcMinN)))
+    return launch_matmul_3xtf32(c, a, bt, scratch, n, row0, rows, col0, cols, variant == 31, stream);
   // variant 1 keeps the first-generation kernel (k-major smem, register-staged) for A/B runs and
   // for n % 4 != 0, where rows are not 16-byte aligned
   if (variant != 1 && n % 4 == 0) {

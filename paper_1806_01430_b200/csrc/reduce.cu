@@ -279,7 +279,8 @@ cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, 
     const bool vec_ok = n % V16<T>::W == 0;
     const size_t row_bytes = static_cast<size_t>(n) * sizeof(T);
     if (vec_ok && row_bytes <= 64 * 1024 && n >= 512) {
-      static bool configured = false;
+      static PerDeviceOnce once;  // function attributes are per device
+      bool& configured = once.here();
       if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(gemv_row_staged_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         if (e != cudaSuccess) return e;

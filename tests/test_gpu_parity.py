@@ -340,11 +340,10 @@ def _normwise_bound_structured(n, tol):
     return tol * (k[:, None] * A[None, :] + B[None, :]) / n ** 2
 
 
-@pytest.mark.parametrize("n", [256, 1024])
-def test_fp32_fast_is_as_accurate_as_the_cpu_float_program(n):
-    """On the program's own inputs plain float accumulation (GPU FAST and the CPU program alike) drifts
-    outside 1e-6 norm-wise once N reaches ~1000 (1e-3 element-wise at N=1024).  FAST must be no
-    less accurate than the CPU float program, and exact where that program is exact (N=256)."""
+@pytest.mark.parametrize("n", [256, 512])
+def test_fp32_ffma_fast_is_as_accurate_as_the_cpu_float_program(n):
+    """Below N = 1024 FP32 FAST runs on the FFMA pipe with plain float accumulation, like the CPU program:
+    it must be no less accurate than that program, and exact where that program is exact (N=256)."""
     ref = cpu.App(n, 1, threads=8).run()
     with capi.Context(n=n, dtype=capi.F32) as ctx:
         assert ctx.measure("101010101001").status == capi.MEASURED
@@ -356,15 +355,64 @@ def test_fp32_fast_is_as_accurate_as_the_cpu_float_program(n):
     if n == 256:
         assert gpu_ratio == cpu_ratio == 0.0
     else:
-        assert gpu_ratio <= 1.25 * cpu_ratio, (gpu_ratio, cpu_ratio)
-        assert (np.abs(got - exact) <= 10 * bound + np.abs(exact) * 2.0 ** -24).all()
+        assert gpu_ratio <= max(1.0, 1.25 * cpu_ratio), (gpu_ratio, cpu_ratio)
 
 
-def test_n4096_fp32_strict_bit_exact_fast_as_accurate_as_the_cpu_program():
-    """FP32 at full size.  Plain float accumulation over 4096 terms -- on the GPU *and* in the CPU
-    reference program -- rounds at |c| ~ 3000 (ulp 2.4e-4) and ends up to ~8x outside the 1e-6 norm-wise
-    bar against the exact value.  So the full-size FP32 claims are: STRICT reproduces the CPU
-    float program bit for bit, and FAST is no less accurate than that program; linearity holds."""
+def _app_operands(n):
+    i = np.arange(n, dtype=np.float64)
+    a = ((i[:, None] + i[None, :]) / n).astype(np.float32)
+    b = ((i[:, None] - i[None, :]) / n).astype(np.float32)
+    return a, np.ascontiguousarray(b.T)
+
+
+@pytest.mark.parametrize("variant,slack", [(0, 1.0), (30, 1.0), (31, 4.0)])
+@pytest.mark.parametrize("n", [1000, 1024, 1536, 2048])
+def test_fp32_tensor_core_contraction_within_tolerance(n, variant, slack):
+    """FP32 FAST at N >= 1024: tcgen05 split-TF32 (matmul_tc.cu).  The default (compensated accumulation) meets
+    the 1e-6 norm-wise bar against the float64-exact product on random AND on the application's smooth inputs
+    (where plain float accumulation, CPU program included, is ~8x outside it); the wide-tile variant 31 trades
+    that for speed and is held to 4x the bar."""
+    if variant == 0 and n < 1024:
+        pytest.skip("auto selects the FFMA kernel below N = 1024")
+    a_app, bt_app = _app_operands(n)
+    cases = [(rand(n, capi.F32, 21), rand(n, capi.F32, 22), rand(n, capi.F32, 23)),
+             (a_app, bt_app, np.zeros((n, n), np.float32))]
+    with capi.Context(n=n, dtype=capi.F32, matmul_variant=variant) as ctx:
+        for a, bt, c0 in cases:
+            ctx.upload(capi.ARRAY_A, a)
+            ctx.upload(capi.ARRAY_BT, bt)
+            ctx.upload(capi.ARRAY_C, c0)
+            ctx.run_loop(8)
+            ok, worst = normwise_ok(ctx.fetch(capi.ARRAY_C), a, bt, c0, capi.F32)
+            assert worst <= slack, worst
+
+
+@pytest.mark.parametrize("n", [64, 256, 300, 260])
+def test_fp32_tensor_core_contraction_small_and_ragged(n):
+    """Forced onto the tensor cores at sizes below one tile / not a tile multiple: TMA zero-fill and the masked
+    epilogue."""
+    a, bt, c0 = rand(n, capi.F32, 31), rand(n, capi.F32, 32), rand(n, capi.F32, 33)
+    with capi.Context(n=n, dtype=capi.F32, matmul_variant=30) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        ctx.run_loop(8)
+        ok, worst = normwise_ok(ctx.fetch(capi.ARRAY_C), a, bt, c0, capi.F32)
+        assert ok, worst
+        # a ragged row block: only rows [r0, r1) of c may change
+        ctx.upload(capi.ARRAY_C, c0)
+        r0, r1 = n // 3, (2 * n) // 3 + 1
+        ctx.run_loop_rows(8, r0, r1 - r0)
+        got = ctx.fetch(capi.ARRAY_C)
+        assert bits_equal(got[:r0], c0[:r0]) and bits_equal(got[r1:], c0[r1:])
+        assert normwise_ok(got[r0:r1], a[r0:r1], bt, c0[r0:r1], capi.F32)[0]
+
+
+def test_n4096_fp32_strict_bit_exact_fast_within_tolerance():
+    """FP32 at full size on the program's own inputs.  The CPU float program itself ends up to ~8x outside the
+    1e-6 norm-wise bar against the exact value (plain float accumulation over 4096 smooth terms).
+    STRICT reproduces that program bit for bit; FAST (tensor cores, compensated accumulation) is inside the
+    bar against the exact value; linearity holds."""
     n = 4096
     exact = cpu.closed_form_c(n)
     bound = _normwise_bound_structured(n, 1e-6)
@@ -384,14 +432,12 @@ def test_n4096_fp32_strict_bit_exact_fast_as_accurate_as_the_cpu_program():
         fast = ctx.fetch(capi.ARRAY_C).astype(np.float64)
         ctx.run_loop(8)                      # c += a bt^T once more
         twice = ctx.fetch(capi.ARRAY_C).astype(np.float64)
-    for r0, r1 in blocks:
-        cpu_ratio = (np.abs(ref.c[r0:r1].astype(np.float64) - exact[r0:r1]) / bound[r0:r1]).max()
-        gpu_ratio = (np.abs(fast[r0:r1] - exact[r0:r1]) / bound[r0:r1]).max()
-        assert gpu_ratio <= 1.25 * cpu_ratio, (gpu_ratio, cpu_ratio)
-    # and everywhere: within 1e-5 norm-wise of the exact value (10x the bar; documented gap)
-    assert (np.abs(fast - exact) <= 10 * bound + np.abs(exact) * 2.0 ** -24).all()
-    # linearity (c += a bt^T applied twice doubles c); the second pass accumulates at twice the magnitude
-    assert (np.abs(twice - 2 * exact) <= 60 * bound + np.abs(exact) * 2.0 ** -22).all()
+    cpu_ratio = max((np.abs(ref.c[r0:r1].astype(np.float64) - exact[r0:r1]) / bound[r0:r1]).max() for r0, r1 in blocks)
+    gpu_ratio = (np.abs(fast - exact) / (bound + np.abs(exact) * 2.0 ** -24)).max()
+    assert gpu_ratio <= 1.0, gpu_ratio
+    assert cpu_ratio > gpu_ratio             # and it is the more accurate of the two
+    # linearity (c += a bt^T applied twice doubles c): the second pass starts from a rounded c
+    assert (np.abs(twice - 2 * exact) <= 2 * bound + np.abs(exact) * 2.0 ** -22).all()
 
 
 # ---- row-sharded run: row/column-block kernels, fused transpose + all-gather, ring-ordered contraction ----
@@ -441,6 +487,21 @@ def test_row_sharded_individual_matches_the_cpu_program(n, dtype, numerics, worl
         _check_sharded_trace(checksum, ref, dtype)
 
 
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharded_fp32_fast_through_the_tensor_cores(world):
+    """Column-block launches of the tcgen05 contraction (one per owner of bt rows) against the exact product."""
+    n = 1024
+    exact = cpu.closed_form_c(n)
+    bound = _normwise_bound_structured(n, 1e-6)
+    with capi.Context(n=n, dtype=capi.F32, num_slots=world, devices=[0] * world) as ctx:
+        checksum, stats = ctx.shard_run_local()
+        for r, st in enumerate(stats):
+            lo, hi = st["row0"], st["row0"] + st["rows"]
+            got = ctx.fetch(capi.ARRAY_C, slot=r)[lo:hi].astype(np.float64)
+            assert (np.abs(got - exact[lo:hi]) <= bound[lo:hi] + np.abs(exact[lo:hi]) * 2.0 ** -24).all()
+        assert abs(checksum) <= 1e-6 * float(np.abs(np.diag(exact)).sum())
+
+
 def _check_sharded_trace(got, ref, dtype):
     # the partial traces are added block by block: the same bits as the program's running sum whenever the
     # partial sums are exact (N = 2^p), otherwise a different association of the same terms
@@ -448,7 +509,9 @@ def _check_sharded_trace(got, ref, dtype):
     if n & (n - 1) == 0 and (dtype == capi.F64 or n <= 256):   # float partial sums stay exact only for small N
         assert got == ref.checksum
     else:
-        assert abs(got - ref.checksum) <= TOL[dtype] * float(np.abs(np.diag(ref.c)).astype(np.float64).sum())
+        # two orders of one floating-point sum of n terms: each is within (n-1) u sum|x| of the exact sum
+        u = 2.0 ** -53 if dtype == capi.F64 else 2.0 ** -24
+        assert abs(got - ref.checksum) <= 2 * n * u * float(np.abs(np.diag(ref.c)).astype(np.float64).sum())
 
 
 def _shard_member(rank, world, n, dtype, numerics, conns, barrier, out_q):
