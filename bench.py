@@ -48,6 +48,7 @@ def parse_args():
     ap.add_argument("--n", type=int, default=4096)
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 arm of the configuration")
     ap.add_argument("--ga", action="store_true", help="also run the GA search (M=12, T=12) with real timings")
     return ap.parse_args()
 
@@ -253,13 +254,21 @@ def run_ours(args):
         share = ms8 * 1e-3 / (device_s / args.steps)
         roof = {"bound": "tensor", "pipe": "fp64 (DMMA.8x8x4 via mma.sync)" if dtype == capi.F64 else "fp32 (FFMA)",
                 "kernel": "matmul_nt (gene 8)", "achieved": ach, "peak": pipe_peak, "unit": "TFLOP/s", "frac": ach / pipe_peak,
-                "traffic": None, "ms_per_launch": ms8, "share_of_step": share,
+                "traffic": ncu_traffic("matmul_dmma" if dtype == capi.F64 else "matmul_3xtf32", n), "ms_per_launch": ms8,
+                "share_of_step": share,
                 "peak_source": "FMA-issue peak of the same pipe measured in this run by csrc/peaks.cu "
                                "(MEASURED_PEAKS.json carries only HBM and bf16 figures)"}
         ms6 = ctx.time_loop(6, 10, True)
         gb = 2.0 * esz * n * n / (ms6 * 1e-3) / 1e9
         hbm_roof = {"bound": "hbm", "kernel": "transpose_tiled (gene 6)", "achieved": gb, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                    "frac": gb / peaks["hbm_gbs"], "traffic": None, "peak_source": f"MEASURED_PEAKS.json ({peaks_kind})"}
+                    "frac": gb / peaks["hbm_gbs"], "traffic": ncu_traffic("transpose_tile", n),
+                    "peak_source": f"MEASURED_PEAKS.json ({peaks_kind})"}
+
+    # FP32 arm of the same configuration (BASELINE configs[1] names both precisions): whole individuals through
+    # the C ABI, then the gene-8 kernel alone (tcgen05 split-TF32 with compensated accumulation, matmul_tc.cu)
+    fp32 = None
+    if rank == 0 and dtype == capi.F64 and not args.no_fp32:
+        fp32 = fp32_arm(n, local_rank, max(10, args.steps // 4), peaks)
 
     # the sampler covers the timed region plus the (equally loaded) mixed-genome and roofline phases
     clocks = sampler.stop()
@@ -290,12 +299,50 @@ def run_ours(args):
             "clocks": clocks, "roofline": roof, "roofline_hbm": hbm_roof, "cpu_baseline": base,
             "checksum": checksum,
         }
+        if fp32 is not None:
+            line["fp32"] = fp32
         if ga is not None:
             line["ga_search"] = ga
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def ncu_traffic(kernel: str, n: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the committed `ncu --set full`
+    summary (profiles/ncu_traffic.json, written by tools/ncu_summary.py --traffic); None when not captured at this N."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    try:
+        table = json.loads(p.read_text())
+    except (OSError, ValueError):
+        return None
+    hit = table.get(f"{kernel}@{n}")
+    return hit["bytes_per_launch"] if hit else None
+
+
+def fp32_arm(n, device, steps, peaks):
+    from paper_1806_01430_b200 import capi
+    flops = 2.0 * n ** 3
+    with capi.Context(n=n, dtype=capi.F32, devices=[device], timeout_s=600.0) as ctx:
+        for _ in range(3):
+            ctx.measure(GENOME_ALL_NESTS)
+        dev_s = 0.0
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            dev_s += ctx.measure(GENOME_ALL_NESTS).time_s
+        wall = time.perf_counter() - t0
+        ms8 = ctx.time_loop(8, 5, True)
+        ffma_peak = capi.peak_probe(capi.PEAK_FP32_FMA, device)
+    tf32_peak = peaks["bf16_tflops"] / 2.0
+    return {"value": flops * steps / dev_s / 1e9, "unit": "GFLOP/s", "steps": steps, "e2e": flops * steps / wall / 1e9,
+            "kernel": "matmul_3xtf32 (gene 8: tcgen05.mma kind::tf32 x3 per term, compensated accumulation; split passes included)",
+            "ms_per_launch": ms8, "effective_fp32_tflops": flops / ms8 / 1e9,
+            "roofline": {"bound": "tensor", "achieved": 3.0 * flops / ms8 / 1e9, "peak": tf32_peak, "unit": "TFLOP/s",
+                         "frac": 3.0 * flops / ms8 / 1e9 / tf32_peak, "traffic": ncu_traffic("matmul_3xtf32", n),
+                         "peak_source": "half of MEASURED_PEAKS.json bf16_tflops (TF32 runs at half the bf16 rate); "
+                                        "achieved counts the three tensor-core products issued per FP32 term"},
+            "vs_ffma_pipe_peak": flops / ms8 / 1e9 / ffma_peak, "ffma_pipe_peak_tflops": ffma_peak}
 
 
 def run_ga_search(n, dtype, devices, population=12, generations=12, seed=1, timeout_s=0.5):

@@ -26,7 +26,33 @@ KEEP = [
 ]
 
 
+def traffic(rep, n, out_path):
+    """Merge `kernel@N -> dram bytes per launch` of this report into a JSON table (bench.py reads it)."""
+    import json
+    import re
+    from pathlib import Path
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
+    rows = list(csv.reader(raw.splitlines()))
+    hdr, units = rows[0], rows[1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12}
+    ir, iw, ik, it = (hdr.index(k) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "Kernel Name", "gpu__time_duration.sum"))
+    acc = {}
+    for r in rows[2:]:
+        m = re.search(r"(\w+_kernel)", r[ik])
+        name = (m.group(1) if m else r[ik])[: -len("_kernel")] if m else r[ik]
+        b = float(r[ir]) * scale[units[ir]] + float(r[iw]) * scale[units[iw]]
+        acc.setdefault(name, []).append((b, float(r[it])))
+    p = Path(out_path)
+    table = json.loads(p.read_text()) if p.exists() else {}
+    for name, vals in acc.items():
+        table[f"{name}@{n}"] = {"bytes_per_launch": sum(v[0] for v in vals) / len(vals), "launches": len(vals),
+                                "ncu_duration_" + units[it]: sum(v[1] for v in vals) / len(vals), "report": Path(rep).name}
+    p.write_text(json.dumps(table, indent=1, sort_keys=True) + "\n")
+
+
 def main():
+    if sys.argv[1] == "--traffic":   # --traffic <rep> <N> <out.json>
+        return traffic(sys.argv[2], int(sys.argv[3]), sys.argv[4])
     rep = sys.argv[1]
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True, check=True).stdout
     rows = list(csv.reader(raw.splitlines()))
