@@ -16,6 +16,7 @@
 #include <string>
 #include <vector>
 
+#include "acctune/commands.hpp"
 #include "acctune/errors.hpp"
 #include "acctune/evaluation.hpp"
 #include "acctune/evaluator.hpp"
@@ -434,6 +435,49 @@ REF_API int ref_evaluator_counters(void* h, std::uint64_t c4[4], double* elapsed
     *elapsed_s = c.elapsed_s;
     return 0;
   });
+}
+
+// scan_loops on in-memory text: one line per loop "id,line,depth,header_start,body_begin,body_end,indent_len"
+REF_API int ref_scan_text(const char* text, char* out, std::size_t cap) {
+  return guarded([&] {
+    const SourceUnit unit = SourceUnit::from_string("<text>", text);
+    std::ostringstream s;
+    for (const LoopSite& l : scan_loops(unit))
+      s << l.id << "," << unit.lines.line_col_of(l.header_start).line << "," << l.depth << "," << l.header_start << ","
+        << l.body_span.begin << "," << l.body_span.end << "," << l.indent.size() << "\n";
+    return copy_out(s.str(), out, cap);
+  });
+}
+
+// render_variant on in-memory text with every scanned loop a candidate
+REF_API int ref_render_text(const char* text, const std::uint8_t* bits, std::size_t n, char* out, std::size_t cap) {
+  return guarded([&] {
+    CandidateSet cs;
+    cs.unit = SourceUnit::from_string("<text>", text);
+    cs.all_loops = scan_loops(cs.unit);
+    for (const auto& l : cs.all_loops) cs.candidate_ids.push_back(l.id);
+    return copy_out(render_variant(cs, genome_of(bits, n)), out, cap);
+  });
+}
+
+// cmd_tune / cmd_report: return the exit code, copy stdout / stderr text out
+REF_API int ref_cmd_tune(const char* config_path, int has_seed, std::uint64_t seed, char* out, std::size_t out_cap, char* err,
+                         std::size_t err_cap) {
+  std::ostringstream o, e;
+  TuneOptions opt;
+  if (has_seed) opt.seed = seed;
+  const int rc = cmd_tune(config_path, opt, o, e);
+  copy_out(o.str(), out, out_cap);
+  copy_out(e.str(), err, err_cap);
+  return rc;
+}
+
+REF_API int ref_cmd_report(const char* workdir, char* out, std::size_t out_cap, char* err, std::size_t err_cap) {
+  std::ostringstream o, e;
+  const int rc = cmd_report(workdir, o, e);
+  copy_out(o.str(), out, out_cap);
+  copy_out(e.str(), err, err_cap);
+  return rc;
 }
 
 REF_API const char* ref_status_name(int status) {

@@ -2,6 +2,7 @@
 
   lib/libmmx.so       CUDA kernels (sm_100a) + executor + the C ABI of include/mmx.h
   lib/libmmx_host.so  C++ host mirror of the reference tuner API (Genome, Evaluator, GA, ...)
+  bin/mmx_tune        analyze | tune | report command line over the same host layer
 
 nvcc cross-compiles without a GPU.  Objects are rebuilt only when a source or header is newer.
 """
@@ -19,6 +20,7 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 HOST = PKG / "host"
 LIB = PKG / "lib"
+BIN = PKG / "bin"
 OBJ = PKG / "build"
 
 NVCC = os.environ.get("NVCC") or shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc"
@@ -95,6 +97,16 @@ def build_libmmx_host(verbose: bool = False) -> Path | None:
         # libmmx.so is resolved at run time next to this library
         _run([CXX, "-shared", "-o", str(out), *map(str, objs), f"-L{LIB}", "-lmmx", "-Wl,-rpath,$ORIGIN", "-Wl,-Bsymbolic",
               "-Wl,--exclude-libs,ALL", "-lpthread"])
+    # the command-line front end (analyze | tune | report): the same objects, linked into an executable
+    cli_src = HOST / "tools" / "mmx_tune.cpp"
+    if cli_src.exists():
+        BIN.mkdir(exist_ok=True)
+        cli_obj = OBJ / "host_cli_mmx_tune.o"
+        cli_changed = _compile(cli_src, cli_obj, hm, verbose)
+        exe = BIN / "mmx_tune"
+        if any(changed) or cli_changed or not exe.exists():
+            core = [o for o in objs if "capi_host" not in o.name]
+            _run([CXX, "-o", str(exe), str(cli_obj), *map(str, core), f"-L{LIB}", "-lmmx", "-Wl,-rpath,$ORIGIN/../lib", "-lpthread"])
     return out
 
 

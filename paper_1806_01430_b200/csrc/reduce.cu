@@ -9,6 +9,8 @@
 // STRICT: the data is staged through shared memory with coalesced loads, then ONE thread per
 // output walks k ascending with a separate multiply and add, starting from the incoming c
 // value -- the CPU loop's exact operation sequence.
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace mmx {
@@ -149,6 +151,61 @@ __global__ void __launch_bounds__(256, 2) gemv_row_staged_kernel(T* __restrict__
   }
 }
 
+// FAST, streaming form: every WARP owns whole rows of bt (j = warp, warp + #warps, ...) and there is no
+// CTA-wide barrier after the a-row has been staged.  A lane keeps GEMV_Q 16-byte loads of bt in flight
+// (L1 bypassed: the matrix is read once), multiplies them against the staged a-row from shared memory
+// (consecutive lanes, consecutive 16-byte chunks: conflict-free), and a shuffle tree finishes the row.
+// The grid is sized so that every warp gets the same number of rows when N is a power of two.
+constexpr int GEMV_Q = 8;
+
+template <typename VT>
+__device__ __forceinline__ VT ld_stream(const VT* p) {
+  VT v;
+  if constexpr (sizeof(VT) == 16 && alignof(VT) == 16) {
+    unsigned x, y, z, w;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];\n" : "=r"(x), "=r"(y), "=r"(z), "=r"(w) : "l"(p));
+    const uint4 u = make_uint4(x, y, z, w);
+    v = *reinterpret_cast<const VT*>(&u);
+  }
+  return v;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 2) gemv_row_stream_kernel(T* __restrict__ c, const T* __restrict__ a,
+                                                                 const T* __restrict__ bt, int n, IterRef iter) {
+  using VT = typename V16<T>::type;
+  constexpr int W = V16<T>::W;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  VT* sa = reinterpret_cast<VT*>(smem_raw);  // n / W vectors
+  const int i = iter.off + (iter.base ? *iter.base : 0);
+  const int tid = threadIdx.x, lane = tid % 32;
+  const int nv = n / W;
+  const VT* av = reinterpret_cast<const VT*>(a + static_cast<size_t>(i) * n);
+  for (int v = tid; v < nv; v += 256) sa[v] = av[v];
+  __syncthreads();
+
+  const int warps = gridDim.x * 8;
+  T* crow = c + static_cast<size_t>(i) * n;
+  for (int j = blockIdx.x * 8 + tid / 32; j < n; j += warps) {
+    const VT* r = reinterpret_cast<const VT*>(bt + static_cast<size_t>(j) * n);
+    T s0 = 0, s1 = 0;
+    int v = lane;
+    for (; v + 32 * (GEMV_Q - 1) < nv; v += 32 * GEMV_Q) {
+      VT x[GEMV_Q];
+#pragma unroll
+      for (int q = 0; q < GEMV_Q; ++q) x[q] = ld_stream(r + v + 32 * q);
+#pragma unroll
+      for (int q = 0; q < GEMV_Q; q += 2) {
+        s0 = vdot(sa[v + 32 * q], x[q], s0);
+        s1 = vdot(sa[v + 32 * (q + 1)], x[q + 1], s1);
+      }
+    }
+    for (; v < nv; v += 32) s0 = vdot(sa[v], ld_stream(r + v), s0);
+    s0 = warp_sum(s0 + s1);
+    if (lane == 0) crow[j] += s0;
+  }
+}
+
 // STRICT: block = 64 threads owns 64 columns j; k is walked in tiles of 64 staged in smem.
 template <typename T>
 __global__ void __launch_bounds__(64) gemv_row_strict_kernel(T* __restrict__ c, const T* __restrict__ a,
@@ -283,11 +340,23 @@ cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, 
       bool& configured = once.here();
       if (!configured) {
         cudaError_t e = cudaFuncSetAttribute(gemv_row_staged_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
+        if (e == cudaSuccess)
+          e = cudaFuncSetAttribute(gemv_row_stream_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 64 * 1024);
         if (e != cudaSuccess) return e;
         configured = true;
       }
-      const int grid = n / 2 < 2 * kNumSMs ? n / 2 : 2 * kNumSMs;
-      gemv_row_staged_kernel<T><<<grid, 256, row_bytes, stream>>>(c, a, bt, n, iter);
+      static const int form = [] { const char* e = getenv("MMX_GEMV_FORM"); return e ? atoi(e) : 0; }();  // tuning hook
+      if (form == 1) {
+        const int grid = n / 2 < 2 * kNumSMs ? n / 2 : 2 * kNumSMs;
+        gemv_row_staged_kernel<T><<<grid, 256, row_bytes, stream>>>(c, a, bt, n, iter);
+      } else {
+        // largest CTA count <= 2 per SM that gives every warp the same number of rows (when 8 divides n)
+        int grid = 2 * kNumSMs;
+        const int row_groups = (n + 7) / 8;
+        if (row_groups <= grid) grid = row_groups;
+        else if (row_groups % 2 == 0) { const int per = (row_groups + grid - 1) / grid; grid = (row_groups + per - 1) / per; }
+        gemv_row_stream_kernel<T><<<grid, 256, row_bytes, stream>>>(c, a, bt, n, iter);
+      }
     } else {
       gemv_row_fast_kernel<T><<<(n + 7) / 8, 256, 0, stream>>>(c, a, bt, n, iter, vec_ok);
     }

@@ -98,6 +98,18 @@ MMXH_API int mmxh_run_ga_external(size_t gene_length, mmxh_batch_cb batch, mmxh_
 MMXH_API int mmxh_run_ga(void* evaluator, const mmxh_ga_params* params, char* csv, size_t csv_cap, uint8_t* best_bits,
                          double* best_s, double* baseline_s);
 
+/* source model: scan_loops / render_variant (source_model.hpp).  mmxh_scan_loops fills up to cap rows of
+ * {id, line, depth, header_start, body_begin, body_end, indent_len} and returns the loop count. */
+MMXH_API int mmxh_scan_loops(const char* path_label, const char* text, int64_t* rows7, size_t cap);
+MMXH_API int mmxh_render_variant(const char* text, const uint8_t* bits, size_t n, char* out, size_t cap);
+MMXH_API int mmxh_strip_directives(const char* text, char* out, size_t cap);
+
+/* commands (commands.hpp): return the process exit code (0, 1..5); stdout / stderr text is copied out */
+MMXH_API int mmxh_cmd_tune(const char* config_path, int has_seed, uint64_t seed, const char* sim_model_or_null, char* out, size_t out_cap,
+                           char* err, size_t err_cap);
+MMXH_API int mmxh_cmd_report(const char* workdir, char* out, size_t out_cap, char* err, size_t err_cap);
+MMXH_API int mmxh_cmd_analyze(const char* config_path, char* out, size_t out_cap, char* err, size_t err_cap);
+
 MMXH_API const char* mmxh_status_name(int status);
 /* nlohmann-compatible number formatting used by the cache writer */
 MMXH_API int mmxh_dump_number(double v, char* out, size_t cap);

@@ -33,6 +33,9 @@ MMXHOST_ERROR(ModelGenomeMismatch, ModelError);
 MMXHOST_ERROR(GeneLengthTooLarge, ModelError);
 MMXHOST_ERROR(SimulatedCompileError, ModelError);
 
+MMXHOST_ERROR(ScanError, Error);              // the source file cannot be tokenised / parsed
+MMXHOST_ERROR(MissingLog, Error);             // report: an artifact of a run is absent
+
 #undef MMXHOST_ERROR
 
 }  // namespace mmxhost

@@ -1,4 +1,6 @@
 #include "mmxhost/capi_host.h"
+#include "mmxhost/commands.hpp"
+#include "mmxhost/source_model.hpp"
 
 #include <cstring>
 #include <memory>
@@ -399,6 +401,64 @@ MMXH_API int mmxh_run_ga_external(size_t gene_length, mmxh_batch_cb batch, mmxh_
     *baseline_s = r.baseline_s;
     return copy_out(s.str(), csv, csv_cap);
   });
+}
+
+MMXH_API int mmxh_scan_loops(const char* path_label, const char* text, int64_t* rows7, size_t cap) {
+  return guarded([&] {
+    const SourceUnit unit = SourceUnit::from_string(path_label ? path_label : "<text>", text);
+    const std::vector<LoopSite> loops = scan_loops(unit);
+    for (std::size_t k = 0; k < loops.size() && k < cap; ++k) {
+      const LoopSite& l = loops[k];
+      int64_t* r = rows7 + 7 * k;
+      r[0] = l.id;
+      r[1] = static_cast<int64_t>(l.line);
+      r[2] = l.depth;
+      r[3] = static_cast<int64_t>(l.header_start);
+      r[4] = static_cast<int64_t>(l.body_begin);
+      r[5] = static_cast<int64_t>(l.body_end);
+      r[6] = static_cast<int64_t>(l.indent.size());
+    }
+    return static_cast<int>(loops.size());
+  });
+}
+
+MMXH_API int mmxh_render_variant(const char* text, const uint8_t* bits, size_t n, char* out, size_t cap) {
+  return guarded([&] {
+    const CandidateSet cs = all_loops_candidate_set(SourceUnit::from_string("<text>", text));
+    return copy_out(render_variant(cs, Genome(std::vector<std::uint8_t>(bits, bits + n))), out, cap);
+  });
+}
+
+MMXH_API int mmxh_strip_directives(const char* text, char* out, size_t cap) {
+  return guarded([&] { return copy_out(strip_directives(text), out, cap); });
+}
+
+MMXH_API int mmxh_cmd_tune(const char* config_path, int has_seed, uint64_t seed, const char* sim_model_or_null, char* out, size_t out_cap,
+                           char* err, size_t err_cap) {
+  std::ostringstream o, e;
+  TuneOptions opt;
+  if (has_seed) opt.seed = seed;
+  if (sim_model_or_null != nullptr) opt.sim_model = std::string(sim_model_or_null);
+  const int rc = cmd_tune(config_path, opt, o, e);
+  copy_out(o.str(), out, out_cap);
+  copy_out(e.str(), err, err_cap);
+  return rc;
+}
+
+MMXH_API int mmxh_cmd_report(const char* workdir, char* out, size_t out_cap, char* err, size_t err_cap) {
+  std::ostringstream o, e;
+  const int rc = cmd_report(workdir, o, e);
+  copy_out(o.str(), out, out_cap);
+  copy_out(e.str(), err, err_cap);
+  return rc;
+}
+
+MMXH_API int mmxh_cmd_analyze(const char* config_path, char* out, size_t out_cap, char* err, size_t err_cap) {
+  std::ostringstream o, e;
+  const int rc = cmd_analyze(config_path, o, e);
+  copy_out(o.str(), out, out_cap);
+  copy_out(e.str(), err, err_cap);
+  return rc;
 }
 
 MMXH_API const char* mmxh_status_name(int status) {

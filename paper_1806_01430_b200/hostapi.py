@@ -256,3 +256,46 @@ def dump_number(v: float) -> str:
     buf = C.create_string_buffer(64)
     mine().lib.mmxh_dump_number(C.c_double(v), buf, C.c_size_t(64))
     return buf.value.decode()
+
+
+# ---- source model and commands (source_model.hpp, commands.hpp) -------------------------------------
+
+def scan_loops(api: Api, text: str, label: str = "<text>") -> list[dict]:
+    """scan_loops on in-memory text: id, line, depth, header_start, body_begin, body_end, indent_len per loop."""
+    rows = (C.c_int64 * (7 * 256))()
+    n = api.check(api.f("scan_loops")(label.encode(), text.encode(), rows, C.c_size_t(256)))
+    keys = ("id", "line", "depth", "header_start", "body_begin", "body_end", "indent_len")
+    return [dict(zip(keys, (int(rows[7 * k + q]) for q in range(7)))) for k in range(n)]
+
+
+def render_variant(api: Api, text: str, genome) -> str:
+    bits = _bits(genome)
+    buf = C.create_string_buffer(len(text.encode()) + 64 * (bits.size + 1) + 64)
+    api.check(api.f("render_variant")(text.encode(), bits.ctypes.data_as(C.POINTER(C.c_uint8)), C.c_size_t(bits.size), buf, C.c_size_t(len(buf))))
+    return buf.value.decode()
+
+
+def strip_directives(api: Api, text: str) -> str:
+    buf = C.create_string_buffer(len(text.encode()) + 16)
+    api.check(api.f("strip_directives")(text.encode(), buf, C.c_size_t(len(buf))))
+    return buf.value.decode()
+
+
+def _run_command(fn, *args) -> tuple[int, str, str]:
+    out, err = C.create_string_buffer(1 << 16), C.create_string_buffer(1 << 16)
+    rc = fn(*args, out, C.c_size_t(len(out)), err, C.c_size_t(len(err)))
+    return rc, out.value.decode(), err.value.decode()
+
+
+def cmd_tune(api: Api, config_path, seed=None, sim_model=None) -> tuple[int, str, str]:
+    """(exit code, stdout, stderr) of `tune <config> [--seed N] [--sim model]`."""
+    return _run_command(api.f("cmd_tune"), str(config_path).encode(), int(seed is not None), C.c_uint64(seed or 0),
+                        str(sim_model).encode() if sim_model else None)
+
+
+def cmd_report(api: Api, workdir) -> tuple[int, str, str]:
+    return _run_command(api.f("cmd_report"), str(workdir).encode())
+
+
+def cmd_analyze(api: Api, config_path) -> tuple[int, str, str]:
+    return _run_command(api.f("cmd_analyze"), str(config_path).encode())

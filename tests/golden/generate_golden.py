@@ -269,6 +269,69 @@ def gen_rendered(lib):
     (HERE / "rendered_all_nests.c").write_bytes(buf.value)
 
 
+SCAN_CASES = {
+    "braceless_nest": "void f(int n, double a[8][8]) {\n  int i, j;\n  for (i = 0; i < n; i++)\n    for (j = 0; j < n; j++)\n      a[i][j] = 0.0;\n}\n",
+    "comments_and_strings": "/* for (;;) in a comment */\nint g(void) {\n  const char* s = \"for (x) { \\\" }\";  // for (y)\n  char c = '{';\n  int k = 0;\n\tfor (int i = 0; i < 3; ++i) { k += i; }\n  return k + (c == s[0]);\n}\n",
+    "preprocessor": "#define LOOP for (int q = 0; q < 4; ++q) \\\n    do_it(q);\n#include <stdio.h>\nvoid h(void) {\n  LOOP\n  for (int i = 0; i < 2; ++i)\n    ;\n}\n",
+    "if_else_do_while": "void k(int n) {\n  if (n > 0)\n    for (int i = 0; i < n; ++i) n--;\n  else {\n    do {\n      for (int j = 0; j < 3; ++j) { while (n < 0) for (int z = 0; z < 1; ++z) n++; }\n    } while (n < 10);\n  }\n  switch (n) { case 1: for (;;) break; default: break; }\n}\n",
+    "same_line_and_struct": "struct P { int x; } p = { 1 };\nvoid m(int n) { for (int i = 0; i < n; ++i) for (int j = 0; j < n; ++j) p.x += i * j; }\nint arr[] = { 1, 2, 3 };\nvoid w(void) {\n    for (int forty = 0; forty < 2; ++forty) { int format = forty; (void)format; }\n}\n",
+    "no_loops": "int main(void) { return 0; }\n",
+}
+
+
+def gen_scan_cases(lib):
+    """Synthetic sources (written for this repo) scanned and rendered by the reference."""
+    out = {}
+    for name, text in SCAN_CASES.items():
+        buf = C.create_string_buffer(1 << 14)
+        rc = lib.ref_scan_text(text.encode(), buf, C.c_size_t(1 << 14))
+        assert rc >= 0, (name, lib.ref_last_error())
+        rows = [list(map(int, line.split(","))) for line in buf.value.decode().splitlines()]
+        n = len(rows)
+        renders = {}
+        for genome in {"1" * n, ("10" * n)[:n], ("01" * n)[:n]} if n else set():
+            rbuf = C.create_string_buffer(1 << 14)
+            assert lib.ref_render_text(text.encode(), bits_of(genome), C.c_size_t(n), rbuf, C.c_size_t(1 << 14)) > 0
+            renders[genome] = rbuf.value.decode()
+        out[name] = {"text": text, "rows": rows, "renders": renders}
+    (HERE / "scan_cases.json").write_text(json.dumps(out, indent=1) + "\n")
+
+
+def gen_tune_runs(lib):
+    """Artifact sets of the reference's cmd_tune on fixtures/matmul.c + models/matrix12.json (sim backend)."""
+    dst = HERE / "tune_sim"
+    dst.mkdir(exist_ok=True)
+    runs = {"default_seed1": {"seed": 1}, "m8_t6_seed7": {"population": 8, "generations": 6, "seed": 7},
+            "m64_t40_seed1": {"population": 64, "generations": 40, "seed": 1}}
+    index = {}
+    for name, ga in runs.items():
+        with tempfile.TemporaryDirectory() as tmp:
+            tmp = Path(tmp)
+            (tmp / "matmul.c").write_bytes(FIXTURE_SRC.read_bytes())
+            (tmp / "model.json").write_bytes((REF / "fixtures" / "models" / "matrix12.json").read_bytes())
+            cfg = {"source": "matmul.c", "workdir": "work", "jobs": 1, "ga": ga, "sim_model": "model.json"}
+            (tmp / "cfg.json").write_text(json.dumps(cfg))
+            out, err = C.create_string_buffer(1 << 14), C.create_string_buffer(1 << 14)
+            rc = lib.ref_cmd_tune(str(tmp / "cfg.json").encode(), 0, C.c_uint64(0), out, C.c_size_t(1 << 14), err, C.c_size_t(1 << 14))
+            assert rc == 0, err.value
+            rout, rerr = C.create_string_buffer(1 << 14), C.create_string_buffer(1 << 14)
+            assert lib.ref_cmd_report(str(tmp / "work").encode(), rout, C.c_size_t(1 << 14), rerr, C.c_size_t(1 << 14)) == 0
+            files = {}
+            for rel in ("config.resolved.json", "generations.csv", "summary.json", "eval_cache.jsonl"):
+                files[rel] = (tmp / "work" / rel).read_text().replace(str(tmp), "@TMP@")
+            best = (tmp / "work" / "best" / "matmul.c").read_text()
+            index[name] = {"config": cfg, "stdout": out.value.decode().replace(str(tmp), "@TMP@"), "report_stdout": rout.value.decode(),
+                           "files": files, "best_genome_render_sha": fnv(best), "best_is_render_of": json.loads(files["summary.json"])["best_genome"]}
+    (dst / "runs.json").write_text(json.dumps(index, indent=1) + "\n")
+
+
+def fnv(text: str) -> str:
+    h = 0xcbf29ce484222325
+    for b in text.encode():
+        h = ((h ^ b) * 0x100000001b3) & 0xFFFFFFFFFFFFFFFF
+    return f"{h:016x}"
+
+
 def gen_models():
     """The three cost-model fixtures are input DATA of the golden runs: keep a copy beside them."""
     dst = HERE / "models"
@@ -290,6 +353,8 @@ def main():
     gen_operators(lib)
     gen_rendered(lib)
     gen_feasibility(lib)
+    gen_scan_cases(lib)
+    gen_tune_runs(lib)
     print("golden vectors written to", HERE)
 
 
