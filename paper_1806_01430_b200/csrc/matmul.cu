@@ -15,7 +15,10 @@
 //           differs only by the single rounding FMA saves per term.
 // The DMMA variant keeps the same k-ascending FMA chain per element (the MMA accumulates its
 // four products in order into the running sum), so it produces the same bits as FAST SIMT.
+#include <cstdlib>
+
 #include "kernels.cuh"
+#include "raster.cuh"
 
 namespace mmx {
 namespace {
@@ -218,7 +221,7 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 template <int DK, int DSTAGES, int WM, int WN, int MT, int NT>
 __global__ void __launch_bounds__(32 * WM * WN)
 matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const double* __restrict__ bt, int n,
-                   int row0, int rows, int col0, int cols) {
+                   int row0, int rows, int col0, int cols, int group) {
   constexpr int THREADS = 32 * WM * WN;
   constexpr int TM = WM * MT * 8, TN = WN * NT * 8;
   constexpr int DLD = DK + 4;  // padded row: (DK+4)*8 B = 32 mod 128 for DK in {16, 32} => conflict-free fragments
@@ -228,7 +231,9 @@ matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const d
 
   const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
   const int wm = warp / WN, wn = warp % WN;
-  const int m_base = row0 + blockIdx.y * TM, n_base = col0 + blockIdx.x * TN;
+  int bx, by;
+  raster_tile(group, bx, by);
+  const int m_base = row0 + by * TM, n_base = col0 + bx * TN;
   const int m_limit = row0 + rows, n_limit = col0 + cols;  // col0, cols even
   const int g = lane / 4, t4 = lane % 4;   // fragment row, fragment k
 
@@ -329,7 +334,7 @@ matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const d
 template <typename T, bool STRICT, bool FULL, int TM, int TN, int STAGES>
 __global__ void __launch_bounds__((TM / 8) * (TN / 8), (sizeof(T) == 4 ? 512 : 256) / ((TM / 8) * (TN / 8)))
 matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ bt, int n, int row0, int rows,
-                    int col0, int cols) {
+                    int col0, int cols, int group) {
   using VT = typename V16<T>::type;
   constexpr int W = V16<T>::W;           // elements per 16-byte chunk
   constexpr int LD = BK + W;             // padded row length (elements): +16 bytes
@@ -344,7 +349,9 @@ matmul_simt2_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restr
   const int lane = tid % 32, warp = tid / 32;
   constexpr int WX = TX / 8;                // warps along n
   const int tx = (warp % WX) * 8 + lane % 8, ty = (warp / WX) * 4 + lane / 8;
-  const int m_base = row0 + blockIdx.y * TM, n_base = col0 + blockIdx.x * TN;
+  int bx, by;
+  raster_tile(group, bx, by);
+  const int m_base = row0 + by * TM, n_base = col0 + bx * TN;
   const int m_limit = row0 + rows, n_limit = col0 + cols;
 
   auto issue_stage = [&](int stage, int k0) {
@@ -447,8 +454,9 @@ cudaError_t simt2_go(T* c, const T* a, const T* bt, int n, int row0, int rows, i
   }
   dim3 grid((cols + TN - 1) / TN, (rows + TM - 1) / TM);
   const bool full = cols % TN == 0 && rows % TM == 0 && n % BK == 0;
-  if (full) matmul_simt2_kernel<T, STRICT, true, TM, TN, STAGES><<<grid, THREADS, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols);
-  else matmul_simt2_kernel<T, STRICT, false, TM, TN, STAGES><<<grid, THREADS, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols);
+  const int group = raster_group(TM, static_cast<size_t>(n) * sizeof(T));
+  if (full) matmul_simt2_kernel<T, STRICT, true, TM, TN, STAGES><<<grid, THREADS, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols, group);
+  else matmul_simt2_kernel<T, STRICT, false, TM, TN, STAGES><<<grid, THREADS, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols, group);
   return cudaGetLastError();
 }
 
@@ -481,11 +489,19 @@ cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row
     configured = true;
   }
   dim3 grid((cols + TN - 1) / TN, (rows + TM - 1) / TM);
-  matmul_dmma_kernel<DK, DSTAGES, WM, WN, MT, NT><<<grid, 32 * WM * WN, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols);
+  matmul_dmma_kernel<DK, DSTAGES, WM, WN, MT, NT><<<grid, 32 * WM * WN, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols,
+                                                                                         raster_group(TM, static_cast<size_t>(n) * sizeof(double)));
   return cudaGetLastError();
 }
 
 }  // namespace
+
+int raster_group(int /*tile_m*/, size_t /*row_bytes*/) {
+  static const int forced = [] { const char* e = getenv("MMX_RASTER_GROUP"); return e ? atoi(e) : 0; }();  // tuning hook
+  // measured (tools/raster_sweep.sh, profiles/r1d_raster.txt): 16 tile-rows per group minimises DRAM traffic for both
+  // the 64 x 64 DMMA tiles (296 resident CTAs) and the 128 x 128 tcgen05 tiles (148) at N = 4096 and 8192
+  return forced > 0 ? forced : 16;
+}
 
 template <>
 cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, int n, int row0, int rows, int col0, int cols,

@@ -41,6 +41,7 @@
 #include <mutex>
 
 #include "kernels.cuh"
+#include "raster.cuh"
 
 namespace mmx {
 namespace {
@@ -192,7 +193,7 @@ __device__ __forceinline__ float fold_comp(float cin, float hi, float lo) {
 template <int BN, int CHUNK_STAGES, bool COMP>
 __global__ void __launch_bounds__(TC_THREADS, 1)
 matmul_3xtf32_kernel(float* __restrict__ c, const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b, int n,
-                     int row0, int rows, int col0, int cols, int debug_noload) {
+                     int row0, int rows, int col0, int cols, int debug_noload, int group) {
   using S = TcShape<BN>;
   constexpr int STAGES = S::NSTAGES;
   constexpr int COLS = BN / 2;  // columns per drain thread
@@ -209,7 +210,9 @@ matmul_3xtf32_kernel(float* __restrict__ c, const __grid_constant__ CUtensorMap 
   volatile unsigned* tmem_slot_ptr = reinterpret_cast<volatile unsigned*>(smem_raw + (tmem_slot - raw));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m_base = row0 + blockIdx.y * TC_BM, n_base = col0 + blockIdx.x * BN;
+  int bx, by;
+  raster_tile(group, bx, by);
+  const int m_base = row0 + by * TC_BM, n_base = col0 + bx * BN;
   const int k_stages = (n + TC_BK - 1) / TC_BK;
   const int n_chunks = (k_stages + CHUNK_STAGES - 1) / CHUNK_STAGES;
 
@@ -473,7 +476,8 @@ cudaError_t tc_go(cudaStream_t stream, float* c, const float* pa, const float* p
   if (!make_map(&map_a, pa, n, kp, TC_BM) || !make_map(&map_b, pb, n, kp, BN)) return cudaErrorNotSupported;
   static const int noload = env_int("MMX_TC_NOLOAD", 0);
   dim3 grid((cols + BN - 1) / BN, (rows + TC_BM - 1) / TC_BM);
-  matmul_3xtf32_kernel<BN, CS, COMP><<<grid, TC_THREADS, S::SMEM_BYTES, stream>>>(c, map_a, map_b, n, row0, rows, col0, cols, noload);
+  matmul_3xtf32_kernel<BN, CS, COMP><<<grid, TC_THREADS, S::SMEM_BYTES, stream>>>(c, map_a, map_b, n, row0, rows, col0, cols, noload,
+                                                                                  raster_group(TC_BM, static_cast<size_t>(kp) * sizeof(float)));
   return cudaGetLastError();
 }
 
