@@ -10,6 +10,8 @@
 // reference symbol named in its comment.
 #include <cstdint>
 #include <cstring>
+#include <filesystem>
+#include <fstream>
 #include <functional>
 #include <memory>
 #include <sstream>
@@ -21,6 +23,7 @@
 #include "acctune/evaluation.hpp"
 #include "acctune/evaluator.hpp"
 #include "acctune/ga.hpp"
+#include "acctune/probe.hpp"
 #include "acctune/genome.hpp"
 #include "acctune/rng.hpp"
 #include "acctune/sim_model.hpp"
@@ -458,6 +461,35 @@ REF_API int ref_render_text(const char* text, const std::uint8_t* bits, std::siz
     for (const auto& l : cs.all_loops) cs.candidate_ids.push_back(l.id);
     return copy_out(render_variant(cs, genome_of(bits, n)), out, cap);
   });
+}
+
+// build_candidate_set (probe.cpp:187) over in-memory text with `compile_cmd` as the compiler (the reference's mockacc):
+// the probe report (write_probe_report, one JSON object per loop) is copied out; returns the number of accepted
+// loops, or the error class (NoCandidates = -9) with the report still filled in.
+REF_API int ref_probe_text(const char* text, const char* basename, const char* compile_cmd, const char* workdir, char* report,
+                           std::size_t cap) {
+  namespace fs = std::filesystem;
+  const fs::path report_file = fs::path(workdir) / "probe_report.jsonl";
+  auto read_report = [&] {
+    std::ifstream in(report_file, std::ios::binary);
+    std::ostringstream ss;
+    ss << in.rdbuf();
+    copy_out(ss.str(), report, cap);
+  };
+  const int rc = guarded([&] {
+    const SourceUnit unit = SourceUnit::from_string(basename, text);
+    const std::vector<LoopSite> loops = scan_loops(unit);
+    CompilerDriver driver;
+    driver.compile_cmd = compile_cmd;
+    driver.timeout_s = 30.0;
+    ProbeOptions opt;
+    opt.workdir = workdir;
+    opt.report_file = report_file;
+    const CandidateSet cs = build_candidate_set(unit, loops, driver, opt);
+    return static_cast<int>(cs.candidate_ids.size());
+  });
+  read_report();
+  return rc;
 }
 
 // cmd_tune / cmd_report: return the exit code, copy stdout / stderr text out

@@ -104,6 +104,16 @@ MMXH_API int mmxh_scan_loops(const char* path_label, const char* text, int64_t* 
 MMXH_API int mmxh_render_variant(const char* text, const uint8_t* bits, size_t n, char* out, size_t cap);
 MMXH_API int mmxh_strip_directives(const char* text, char* out, size_t cap);
 
+/* static feasibility (feasibility.hpp): probe every loop of `text`; `report` receives the probe report (one JSON object per
+ * loop, the reference's write_probe_report format); returns the number of accepted loops or MMXH_E_NOCANDIDATES (report still filled). */
+MMXH_API int mmxh_probe_source(const char* path_label, const char* text, char* report, size_t cap);
+/* would the variant with directives on the loops whose bit is 1 (every scanned loop is a gene) compile?  1 / 0; `diag` receives
+ * one diagnostic line per rejected annotated loop. */
+MMXH_API int mmxh_variant_feasible(const char* path_label, const char* text, const uint8_t* bits, size_t n, char* diag, size_t cap);
+/* kernel matcher (kernel_match.hpp): JSON {"loops":[{id,line,depth,nest,var,bound,idiom,kernel,writes,reads,why}],"dataflow":[[array,p,q]]};
+ * returns the loop count */
+MMXH_API int mmxh_match_kernels(const char* path_label, const char* text, char* json_out, size_t cap);
+
 /* commands (commands.hpp): return the process exit code (0, 1..5); stdout / stderr text is copied out */
 MMXH_API int mmxh_cmd_tune(const char* config_path, int has_seed, uint64_t seed, const char* sim_model_or_null, char* out, size_t out_cap,
                            char* err, size_t err_cap);

@@ -10,8 +10,10 @@
 #include "mmxhost/backend.hpp"
 #include "mmxhost/errors.hpp"
 #include "mmxhost/evaluator.hpp"
+#include "mmxhost/feasibility.hpp"
 #include "mmxhost/ga.hpp"
 #include "mmxhost/json_lite.hpp"
+#include "mmxhost/kernel_match.hpp"
 #include "mmxhost/sim_model.hpp"
 
 using namespace mmxhost;
@@ -431,6 +433,62 @@ MMXH_API int mmxh_render_variant(const char* text, const uint8_t* bits, size_t n
 
 MMXH_API int mmxh_strip_directives(const char* text, char* out, size_t cap) {
   return guarded([&] { return copy_out(strip_directives(text), out, cap); });
+}
+
+MMXH_API int mmxh_probe_source(const char* path_label, const char* text, char* report, size_t cap) {
+  return guarded([&] {
+    const SourceUnit unit = SourceUnit::from_string(path_label ? path_label : "<text>", text);
+    const std::vector<LoopSite> loops = scan_loops(unit);
+    std::vector<ProbeResult> results;
+    int accepted = 0;
+    try {
+      accepted = static_cast<int>(build_candidate_set(unit, loops, &results).candidate_ids.size());
+    } catch (const NoCandidates&) {
+      copy_out(probe_report_jsonl(unit, loops, results), report, cap);
+      throw;
+    }
+    copy_out(probe_report_jsonl(unit, loops, results), report, cap);
+    return accepted;
+  });
+}
+
+MMXH_API int mmxh_variant_feasible(const char* path_label, const char* text, const uint8_t* bits, size_t n, char* diag, size_t cap) {
+  return guarded([&] {
+    const CandidateSet cs = all_loops_candidate_set(SourceUnit::from_string(path_label ? path_label : "<text>", text));
+    std::vector<ProbeResult> rejected;
+    const bool ok = variant_feasible(cs, Genome(std::vector<std::uint8_t>(bits, bits + n)), &rejected);
+    std::string lines;
+    for (const ProbeResult& r : rejected) lines += r.compiler_message + "\n";
+    copy_out(lines, diag, cap);
+    return ok ? 1 : 0;
+  });
+}
+
+MMXH_API int mmxh_match_kernels(const char* path_label, const char* text, char* json_out, size_t cap) {
+  return guarded([&] {
+    const SourceUnit unit = SourceUnit::from_string(path_label ? path_label : "<text>", text);
+    const std::vector<LoopSite> loops = scan_loops(unit);
+    const std::vector<KernelBinding> bs = match_kernels(unit, loops);
+    std::string j = "{\"loops\":[";
+    for (std::size_t k = 0; k < bs.size(); ++k) {
+      const KernelBinding& b = bs[k];
+      if (k) j += ",";
+      j += "{\"id\":" + std::to_string(b.loop_id) + ",\"line\":" + std::to_string(b.line) + ",\"depth\":" + std::to_string(b.depth) +
+           ",\"nest\":" + std::to_string(b.nest) + ",\"var\":" + json::dump_string(b.header.var) + ",\"bound\":" +
+           json::dump_string(b.header.bound) + ",\"idiom\":" + json::dump_string(to_string(b.idiom)) + ",\"kernel\":" +
+           json::dump_string(b.kernel) + ",\"writes\":" + json::dump_string(b.writes) + ",\"reads\":[";
+      for (std::size_t r = 0; r < b.reads.size(); ++r) j += (r ? "," : "") + json::dump_string(b.reads[r]);
+      j += "],\"why\":" + json::dump_string(b.why_unmatched) + "}";
+    }
+    j += "],\"dataflow\":[";
+    const std::vector<DataflowEdge> edges = derive_dataflow(bs);
+    for (std::size_t k = 0; k < edges.size(); ++k)
+      j += std::string(k ? "," : "") + "[" + json::dump_string(edges[k].array) + "," + std::to_string(edges[k].producer_nest) + "," +
+           std::to_string(edges[k].consumer_nest) + "]";
+    j += "]}";
+    copy_out(j, json_out, cap);
+    return static_cast<int>(bs.size());
+  });
 }
 
 MMXH_API int mmxh_cmd_tune(const char* config_path, int has_seed, uint64_t seed, const char* sim_model_or_null, char* out, size_t out_cap,

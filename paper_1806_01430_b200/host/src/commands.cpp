@@ -1,6 +1,7 @@
 // commands.cpp -- cmd_tune / cmd_report / cmd_analyze.  Contract: /root/reference/proj/src/commands.cpp.
 #include "mmxhost/commands.hpp"
 
+#include <algorithm>
 #include <cstdio>
 #include <filesystem>
 #include <fstream>
@@ -13,8 +14,10 @@
 #include "mmxhost/config.hpp"
 #include "mmxhost/errors.hpp"
 #include "mmxhost/evaluator.hpp"
+#include "mmxhost/feasibility.hpp"
 #include "mmxhost/ga.hpp"
 #include "mmxhost/json_lite.hpp"
+#include "mmxhost/kernel_match.hpp"
 #include "mmxhost/sim_model.hpp"
 #include "mmxhost/source_model.hpp"
 
@@ -52,26 +55,100 @@ void write_text_file(const std::string& path, const std::string& text) {
   if (!out) throw WorkdirUnwritable("short write to " + path);
 }
 
-CandidateSet scan_source(const RunConfig& cfg) {
-  CandidateSet cs;
-  cs.unit = SourceUnit::from_file(cfg.source);
-  cs.all_loops = scan_loops(cs.unit);
-  for (const LoopSite& loop : cs.all_loops)
-    if (cfg.candidates == CandidateFilter::All || loop.depth == 0) cs.candidate_ids.push_back(loop.id);
-  return cs;
-}
+bool keep_candidate(const LoopSite& loop, CandidateFilter filter) { return filter == CandidateFilter::All || loop.depth == 0; }
 
-// The CUDA kernel library serves one catalogue: the 12 loops of the matrix application at their lines and depths.
-void require_kernel_catalogue(const CandidateSet& cs, const RunConfig& cfg) {
+// What `analyze` prints and `tune` searches over: the scanned loops, one probe verdict per loop, the candidate set, and
+// (cuda backend) the kernel each loop is served by.
+struct Inventory {
+  CandidateSet cs;
+  std::vector<ProbeResult> probes;
+  std::vector<KernelBinding> kernels;  // empty for sim runs
+};
+
+// The CUDA kernel library serves the loops whose idiom it has a kernel for (kernel_match.hpp); today that is the catalogue
+// of the matrix application, and the executor is wired to exactly those 12 genes (mmx_loop_catalogue).  The catalogue is
+// DERIVED from the source and must equal the served one row for row.
+void require_kernel_catalogue(const Inventory& inv, const RunConfig& cfg) {
   mmx_loop_info rows[MMX_GENE_LENGTH];
   const int count = mmx_loop_catalogue(rows, MMX_GENE_LENGTH);
-  bool same = cfg.candidates == CandidateFilter::All && static_cast<int>(cs.all_loops.size()) == count;
-  for (int k = 0; same && k < count; ++k)
-    same = static_cast<int>(cs.all_loops[static_cast<std::size_t>(k)].line) == rows[k].line &&
-           cs.all_loops[static_cast<std::size_t>(k)].depth == rows[k].depth;
+  for (const KernelBinding& b : inv.kernels)
+    if (b.kernel.empty())
+      throw ConfigError("the 'cuda' backend has no kernel for loop " + std::to_string(b.loop_id) + " of " + cfg.source + " (line " +
+                        std::to_string(b.line) + "): " + b.why_unmatched);
+  bool same = cfg.candidates == CandidateFilter::All && static_cast<int>(inv.kernels.size()) == count &&
+              inv.cs.candidate_ids.size() == inv.kernels.size();
+  for (int k = 0; same && k < count; ++k) {
+    const KernelBinding& b = inv.kernels[static_cast<std::size_t>(k)];
+    same = b.loop_id == rows[k].gene && static_cast<int>(b.line) == rows[k].line && b.depth == rows[k].depth && b.nest == rows[k].nest &&
+           b.header.var == rows[k].induction && b.kernel == rows[k].kernel;
+  }
   if (!same)
     throw ConfigError("the 'cuda' backend serves the loop catalogue of the matrix application (12 loops, all candidates); " +
-                      cfg.source + " has " + std::to_string(cs.all_loops.size()) + " loops that do not match it");
+                      cfg.source + " has " + std::to_string(inv.cs.all_loops.size()) + " loops that do not match it");
+}
+
+// Sim runs have nothing to probe with: every loop that passes the filter is a candidate and the report says so
+// (/root/reference/proj/src/commands.cpp:78-106).  With the cuda backend the verdicts come from the static rules
+// (feasibility.hpp) -- the compiler probe of commands.cpp:108-127 without a compiler -- and the kernel matcher.
+Inventory take_inventory(const RunConfig& cfg) {
+  Inventory inv;
+  const SourceUnit unit = SourceUnit::from_file(cfg.source);
+  const std::vector<LoopSite> loops = scan_loops(unit);
+  if (cfg.cuda) {
+    try {
+      inv.cs = build_candidate_set(unit, loops, &inv.probes);
+    } catch (const NoCandidates&) {
+      write_text_file(cfg.probe_report_path(), probe_report_jsonl(unit, loops, inv.probes));
+      throw;
+    }
+    write_text_file(cfg.probe_report_path(), probe_report_jsonl(unit, loops, inv.probes));
+    if (cfg.candidates == CandidateFilter::Outermost) {
+      std::erase_if(inv.cs.candidate_ids, [&](int id) { return inv.cs.all_loops[static_cast<std::size_t>(id)].depth != 0; });
+      if (inv.cs.candidate_ids.empty()) throw NoCandidates("no outermost candidate loops in " + cfg.source);
+    }
+    inv.kernels = match_kernels(unit, loops);
+    return inv;
+  }
+  for (const LoopSite& loop : loops) {
+    ProbeResult r;
+    r.loop_id = loop.id;
+    r.verdict = ProbeVerdict::Parallelizable;
+    r.compiler_message = "probe skipped: timings come from a sim model";
+    inv.probes.push_back(std::move(r));
+  }
+  write_text_file(cfg.probe_report_path(), probe_report_jsonl(unit, loops, inv.probes));
+  inv.cs.unit = unit;
+  inv.cs.all_loops = loops;
+  for (const LoopSite& loop : loops)
+    if (keep_candidate(loop, cfg.candidates)) inv.cs.candidate_ids.push_back(loop.id);
+  if (inv.cs.candidate_ids.empty()) throw NoCandidates("no candidate loops in " + cfg.source);
+  return inv;
+}
+
+// commands.cpp:129-155 of the reference, plus the kernel column
+void print_inventory(std::ostream& out, const RunConfig& cfg, const Inventory& inv) {
+  out << "source: " << cfg.source << "\n";
+  out << "loops: " << inv.cs.all_loops.size() << "\n";
+  for (const LoopSite& loop : inv.cs.all_loops) {
+    out << "  loop " << loop.id << ": line " << loop.line << ", depth " << loop.depth;
+    const auto r = std::find_if(inv.probes.begin(), inv.probes.end(), [&](const ProbeResult& x) { return x.loop_id == loop.id; });
+    const bool selected = std::find(inv.cs.candidate_ids.begin(), inv.cs.candidate_ids.end(), loop.id) != inv.cs.candidate_ids.end();
+    if (r == inv.probes.end()) {
+      out << " -> not probed";
+    } else if (r->verdict == ProbeVerdict::Parallelizable) {
+      out << (selected ? " -> candidate" : " -> parallelizable, filtered out");
+    } else {
+      const std::string msg = r->compiler_message.substr(0, r->compiler_message.find('\n'));
+      out << " -> rejected [" << to_string(r->reject_class) << "]";
+      if (!msg.empty()) out << " " << msg;
+    }
+    const auto k = std::find_if(inv.kernels.begin(), inv.kernels.end(), [&](const KernelBinding& x) { return x.loop_id == loop.id; });
+    if (k != inv.kernels.end()) out << (k->kernel.empty() ? " [no kernel: " + k->why_unmatched + "]" : " [kernel: " + k->kernel + "]");
+    out << "\n";
+  }
+  out << "candidates: " << inv.cs.candidate_ids.size() << " (filter: " << to_string(cfg.candidates) << ")\n";
+  out << "gene length: " << inv.cs.candidate_ids.size() << "\n";
+  out << "probe report: " << cfg.probe_report_path() << "\n";
 }
 
 std::string render_summary_json(const TuningResult& result, const EvalCounters& counters) {
@@ -136,22 +213,24 @@ int cmd_analyze(const std::string& config_path, std::ostream& out, std::ostream&
     const RunConfig cfg = load_config(config_path);
     ensure_workdir(cfg.workdir);
     write_text_file(cfg.resolved_config_path(), render_resolved_config(cfg));
-    const CandidateSet cs = scan_source(cfg);
-    if (cfg.cuda) require_kernel_catalogue(cs, cfg);
-    mmx_loop_info rows[MMX_GENE_LENGTH];
-    const int count = cfg.cuda ? mmx_loop_catalogue(rows, MMX_GENE_LENGTH) : 0;
-    out << "source: " << cfg.source << "\n";
-    out << "loops: " << cs.all_loops.size() << "\n";
-    for (const LoopSite& loop : cs.all_loops) {
-      out << "  loop " << loop.id << ": line " << loop.line << ", depth " << loop.depth;
-      const bool selected = cfg.candidates == CandidateFilter::All || loop.depth == 0;
-      out << (selected ? " -> candidate" : " -> parallelizable, filtered out");
-      if (loop.id < count) out << " [kernel: " << rows[loop.id].kernel << "]";
-      out << "\n";
+    Inventory inv;
+    try {
+      inv = take_inventory(cfg);
+    } catch (const NoCandidates&) {
+      // analyze still reports: rerun the scan for the listing (the probe report is already on disk)
+      const SourceUnit unit = SourceUnit::from_file(cfg.source);
+      inv.cs.unit = unit;
+      inv.cs.all_loops = scan_loops(unit);
+      if (cfg.cuda) {
+        const FeasibilityAnalyzer an(unit, inv.cs.all_loops);
+        for (const LoopSite& l : inv.cs.all_loops) inv.probes.push_back(an.probe(l.id));
+        inv.kernels = match_kernels(unit, inv.cs.all_loops);
+      }
+      print_inventory(out, cfg, inv);
+      out << "nothing to tune: every loop was rejected or filtered out\n";
+      return 0;
     }
-    out << "candidates: " << cs.candidate_ids.size() << " (filter: " << to_string(cfg.candidates) << ")\n";
-    out << "gene length: " << cs.candidate_ids.size() << "\n";
-    if (cs.candidate_ids.empty()) out << "nothing to tune: every loop was rejected or filtered out\n";
+    print_inventory(out, cfg, inv);
     return 0;
   } catch (const std::exception& e) {
     err << "analyze: " << e.what() << "\n";
@@ -170,8 +249,8 @@ int cmd_tune(const std::string& config_path, const TuneOptions& options, std::os
     ensure_workdir(cfg.workdir);
     write_text_file(cfg.resolved_config_path(), render_resolved_config(cfg));
 
-    const CandidateSet cs = scan_source(cfg);
-    if (cs.candidate_ids.empty()) throw NoCandidates("no candidate loops in " + cfg.source);
+    const Inventory inv = take_inventory(cfg);
+    const CandidateSet& cs = inv.cs;
     std::unique_ptr<Evaluator> evaluator;
     if (cfg.sim_model) {
       CostModel model = load_model(*cfg.sim_model);
@@ -180,7 +259,7 @@ int cmd_tune(const std::string& config_path, const TuneOptions& options, std::os
                           std::to_string(cs.gene_length()) + " candidates");
       evaluator = std::make_unique<Evaluator>(std::make_unique<SimBackend>(std::move(model)), cfg.jobs, cfg.eval_cache_path());
     } else {
-      require_kernel_catalogue(cs, cfg);
+      require_kernel_catalogue(inv, cfg);
       // worker s of a batch is pinned to device slot s; `jobs` is implied by the device list
       evaluator = std::make_unique<MultiGpuEvaluator>(std::make_unique<CudaBackend>(*cfg.cuda), cfg.eval_cache_path());
     }

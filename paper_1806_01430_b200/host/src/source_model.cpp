@@ -2,6 +2,8 @@
 // Contract: /root/reference/proj/src/source_model.cpp:57-376 (lexer modes, statement walk, render_variant).
 #include "mmxhost/source_model.hpp"
 
+#include "tokens.hpp"
+
 #include <algorithm>
 #include <cctype>
 #include <fstream>
@@ -20,14 +22,12 @@ std::vector<std::size_t> index_lines(std::string_view text) {
 
 bool ident_char(char c) { return std::isalnum(static_cast<unsigned char>(c)) || c == '_'; }
 
-struct Token {
-  enum Kind { Word, Punct } kind;
-  std::size_t at;     // byte offset in the source
-  std::string_view s;  // the word, or one punctuation byte
-};
-
 // Code tokens only.  Dropped: // and /* */ comments, "..." and '...' literals (with escapes), and preprocessor
 // lines (a '#' first on its line, continued by trailing backslashes).
+}  // namespace
+
+namespace detail {
+
 std::vector<Token> tokenize(const SourceUnit& unit) {
   const std::string_view t = unit.text;
   std::vector<Token> out;
@@ -84,6 +84,13 @@ std::vector<Token> tokenize(const SourceUnit& unit) {
   }
   return out;
 }
+
+}  // namespace detail
+
+namespace {
+
+using detail::Token;
+using detail::tokenize;
 
 class Parser {
  public:

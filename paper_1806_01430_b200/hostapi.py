@@ -299,3 +299,40 @@ def cmd_report(api: Api, workdir) -> tuple[int, str, str]:
 
 def cmd_analyze(api: Api, config_path) -> tuple[int, str, str]:
     return _run_command(api.f("cmd_analyze"), str(config_path).encode())
+
+
+# ---- static feasibility and kernel matching (feasibility.hpp, kernel_match.hpp) ----------------------------
+
+def probe_source(text: str, label: str = "<text>") -> tuple[int, list[dict]]:
+    """(accepted loop count or negative error class, probe report rows) of this repo's static probe."""
+    import json
+    api = mine()
+    buf = C.create_string_buffer(1 << 16)
+    rc = api.f("probe_source")(label.encode(), text.encode(), buf, C.c_size_t(len(buf)))
+    return rc, [json.loads(line) for line in buf.value.decode().splitlines() if line]
+
+
+def variant_feasible(text: str, genome, label: str = "<text>") -> tuple[bool, list[str]]:
+    api = mine()
+    bits = _bits(genome)
+    buf = C.create_string_buffer(1 << 14)
+    rc = api.check(api.f("variant_feasible")(label.encode(), text.encode(), bits.ctypes.data_as(C.POINTER(C.c_uint8)), C.c_size_t(bits.size),
+                                             buf, C.c_size_t(len(buf))))
+    return rc == 1, buf.value.decode().splitlines()
+
+
+def match_kernels(text: str, label: str = "<text>") -> dict:
+    import json
+    api = mine()
+    buf = C.create_string_buffer(1 << 16)
+    api.check(api.f("match_kernels")(label.encode(), text.encode(), buf, C.c_size_t(len(buf))))
+    return json.loads(buf.value.decode())
+
+
+def ref_probe_text(text: str, basename: str, compile_cmd: str, workdir) -> tuple[int, list[dict]]:
+    """The reference's build_candidate_set with `compile_cmd` as the compiler (oracle/ref_shim.cpp: ref_probe_text)."""
+    import json
+    api = reference()
+    buf = C.create_string_buffer(1 << 16)
+    rc = api.f("probe_text")(text.encode(), basename.encode(), compile_cmd.encode(), str(workdir).encode(), buf, C.c_size_t(len(buf)))
+    return rc, [json.loads(line) for line in buf.value.decode().splitlines() if line]

@@ -269,6 +269,59 @@ def gen_rendered(lib):
     (HERE / "rendered_all_nests.c").write_bytes(buf.value)
 
 
+# Synthetic sources written for this repo: one per accept/reject rule and its edge cases.  The golden verdicts come from the
+# reference's own probe (build_candidate_set, probe.cpp:187) driving the reference's bundled compiler (tools/mockacc.cpp), and
+# from that compiler run on the reference-rendered variant of every genome.
+PROBE_CASES = {
+    "dependence": "void f(double* a, double* b, double* xa, int n) {\n  for (int i = 1; i < n; i++)\n    a[i] = a[i - 1] + 1.0;\n"
+                  "  for (int i = 0; i < n - 1; i++)\n    a[i] = b[i + 1] * 2.0;\n  for (int i = 1; i < n; i++)\n    b[i] += b[i - 1];\n"
+                  "  for (int i = 2; i < n; i++)\n    xa[i] = a[i-2] * 2;\n  for (int i = 1; i < n; i++) {\n    if (a[i] == a[i - 1]) b[i] = 0.0;\n  }\n"
+                  "  for (int i = 1; i < n; i++) {\n    b[i] = 1.0;\n    a[i] = b[i] + a[i + 10];\n  }\n}\n",
+    "calls": "#include <math.h>\n#define MAX(x, y) ((x) > (y) ? (x) : (y))\nvoid g(double* a, double* b, int n) {\n"
+             "  for (int i = 0; i < n; i++)\n    a[i] = sqrt(b[i]);\n  for (int i = 0; i < n; i++)\n    a[i] = (double)(i) * sizeof(double);\n"
+             "  for (int i = 0; i < n; i++)\n    a[i] = MAX(a[i], b[i]);\n  for (int i = 0; i < n; i++) {\n    /* log(a[i]) would be a call */\n    a[i] = b[i]; // exp(x)\n  }\n"
+             "  for (int i = 0; i < n; i++) {\n    const char* s = \"f(x)\";\n    a[i] = s[0];\n  }\n  for (int i = 0; i < n; i++)\n    a[i] = b [i] + fabs  (b[i]);\n}\n",
+    "exits": "int h(double* a, int n, int mode) {\n  for (int i = 0; i < n; i++) {\n    switch (mode) {\n      case 0: a[i] = 1.0; break;\n      default: a[i] = 2.0;\n    }\n  }\n"
+             "  for (int i = 0; i < n; i++) {\n    if (a[i] < 0.0) return i;\n  }\n  for (int i = 0; i < n; i++) {\n    if (a[i] > 9.0) goto out;\n  }\n"
+             "  for (int i = 0; i < n; i++) {\n    double breakfast = a[i]; /* break */\n    a[i] = breakfast * 2.0; // return\n  }\nout:\n  return -1;\n}\n",
+    "preannotated": "void k(double* a, double* b, int n, int m) {\n  #  pragma   acc   kernels\n  for (int i = 0; i < n; i++) {\n    for (int j = 0; j < m; j++)\n      b[i * m + j] = a[i * m + j];\n  }\n"
+                    "  #pragma acc kernelsx\n  for (int i = 0; i < n; i++) {\n    for (int j = 0; j < m; j++)\n      a[i * m + j] = 0.0;\n  }\n"
+                    "  for (int i = 0; i < n; i++) {\n    #pragma acc kernels loop independent\n    #pragma acc kernels\n    for (int j = 0; j < m; j++)\n      a[i * m + j] += 1.0;\n  }\n}\n",
+    "triple": "void t(double* a, int n) {\n  for (int i = 0; i < n; i++)\n    for (int j = 0; j < n; j++) {\n      for (int k = 0; k < n; k++)\n        a[i] += 1.0;\n      for (int l = 0; l < n; l++)\n        a[j] += 2.0;\n    }\n}\n",
+    "poisoned": "#include <stdio.h>\nvoid p(double* a, int n) {\n#pragma acc kernels\n  for (int i = 0; i < n; i++)\n    printf(\"%f\\n\", a[i]);\n  for (int i = 1; i < n; i++)\n    a[i] = a[i - 1];\n  for (int i = 0; i < n; i++)\n    a[i] = 0.0;\n}\n",
+    "all_rejected": "#include <stdlib.h>\nvoid r(double* a, int n) {\n  for (int i = 0; i < n; i++)\n    a[i] = rand();\n  for (int i = 0; i < n; i++) {\n    if (a[i] > 1.0) break;\n  }\n}\n",
+    "no_loops": "int main(void) { return 0; }\n",
+}
+
+
+def gen_probe_cases(lib):
+    import re
+    out = {}
+    mock = REFLIB / "mockacc"
+    for name, text in PROBE_CASES.items():
+        with tempfile.TemporaryDirectory() as td:
+            buf = C.create_string_buffer(1 << 16)
+            rc = lib.ref_probe_text(text.encode(), f"{name}.c".encode(), f"{mock} -acc {{src}} -o {{out}}".encode(), td.encode(), buf, C.c_size_t(1 << 16))
+            rows = [json.loads(line) for line in buf.value.decode().splitlines() if line]
+            for r in rows:   # keep the diagnostics, drop the temporary directory from their location
+                r["message"] = re.sub(r"\(/[^ ]*/probe/loop_\d+/", "(", r["message"])
+            # every genome over all scanned loops: does the reference's compiler accept the reference-rendered variant?
+            a = len(rows)
+            genomes = {}
+            src, exe = Path(td) / f"{name}.c", Path(td) / "out.bin"
+            rbuf = C.create_string_buffer(1 << 16)
+            for mask in range(1 << a if 0 < a <= 7 else 0):
+                g = "".join("1" if (mask >> k) & 1 else "0" for k in range(a))
+                assert lib.ref_render_text(text.encode(), bits_of(g), C.c_size_t(a), rbuf, C.c_size_t(1 << 16)) > 0
+                src.write_bytes(rbuf.value)
+                proc = subprocess.run([str(mock), "-acc", str(src), "-o", str(exe)], capture_output=True, text=True)
+                genomes[g] = {"ok": proc.returncode == 0,
+                              "diagnostics": [re.sub(r"\(/[^ ]*/", "(", line) for line in proc.stderr.splitlines()]}
+            out[name] = {"text": text, "rc": rc, "report": rows, "genomes": genomes}
+    (HERE / "probe_cases.json").write_text(json.dumps(out, indent=1) + "\n")
+    print("probe cases:", {k: v["rc"] for k, v in out.items()})
+
+
 SCAN_CASES = {
     "braceless_nest": "void f(int n, double a[8][8]) {\n  int i, j;\n  for (i = 0; i < n; i++)\n    for (j = 0; j < n; j++)\n      a[i][j] = 0.0;\n}\n",
     "comments_and_strings": "/* for (;;) in a comment */\nint g(void) {\n  const char* s = \"for (x) { \\\" }\";  // for (y)\n  char c = '{';\n  int k = 0;\n\tfor (int i = 0; i < 3; ++i) { k += i; }\n  return k + (c == s[0]);\n}\n",
@@ -317,7 +370,7 @@ def gen_tune_runs(lib):
             rout, rerr = C.create_string_buffer(1 << 14), C.create_string_buffer(1 << 14)
             assert lib.ref_cmd_report(str(tmp / "work").encode(), rout, C.c_size_t(1 << 14), rerr, C.c_size_t(1 << 14)) == 0
             files = {}
-            for rel in ("config.resolved.json", "generations.csv", "summary.json", "eval_cache.jsonl"):
+            for rel in ("config.resolved.json", "generations.csv", "summary.json", "eval_cache.jsonl", "probe_report.jsonl"):
                 files[rel] = (tmp / "work" / rel).read_text().replace(str(tmp), "@TMP@")
             best = (tmp / "work" / "best" / "matmul.c").read_text()
             index[name] = {"config": cfg, "stdout": out.value.decode().replace(str(tmp), "@TMP@"), "report_stdout": rout.value.decode(),
@@ -354,6 +407,7 @@ def main():
     gen_rendered(lib)
     gen_feasibility(lib)
     gen_scan_cases(lib)
+    gen_probe_cases(lib)
     gen_tune_runs(lib)
     print("golden vectors written to", HERE)
 

@@ -160,7 +160,16 @@ def test_cuda_backend_needs_the_matrix_application_and_a_device(api, matmul_sour
     cfg_path = _workspace(other, "void f(int n, double* a) {\n  for (int i = 0; i < n; ++i) a[i] = 0.0;\n}\n",
                           {"source": "matmul.c", "workdir": "work", "cuda": {"n": 64}})
     rc, _, err = H.cmd_tune(api, cfg_path)
+    assert rc == 2 and "has no kernel for loop 0" in err and "matches no kernel idiom" in err
+    # loops the library does have kernels for, but not the application the executor is wired to
+    third = tmp_path / "third"
+    third.mkdir()
+    cfg_path = _workspace(third, "double c[8][8];\nvoid z(void) {\n  for (int i = 0; i < 8; i++)\n    for (int j = 0; j < 8; j++)\n      c[i][j] = 0.0;\n}\n",
+                          {"source": "matmul.c", "workdir": "work", "cuda": {"n": 64}})
+    rc, _, err = H.cmd_tune(api, cfg_path)
     assert rc == 2 and "loop catalogue of the matrix application" in err
+    rc, out, _ = H.cmd_analyze(api, cfg_path)           # analyze needs no device: static probe + kernel matcher
+    assert rc == 0 and "loop 0: line 3, depth 0 -> candidate [kernel: fill2d<zero>]" in out and "[kernel: fill_row<zero>]" in out
     if not torch.cuda.is_available():
         # no CPU fallback: the measuring tool is absent -> ToolchainMissing -> exit 4 (commands.cpp:172)
         cfg_path = _workspace(tmp_path, matmul_source, {"source": "matmul.c", "workdir": "work", "cuda": {"n": 64}})
@@ -181,6 +190,35 @@ def test_report_rejects_corrupted_logs(api, matmul_source, tmp_path):
     assert rc == 1 and "best time regresses" in err
     (work / "generations.csv").write_text("generation,best\n")
     assert H.cmd_report(api, work)[0] == 1
+
+
+def test_analyze_with_the_cuda_backend_probes_statically(api, matmul_source, tmp_path):
+    """`analyze` on a "cuda" config: verdicts from the static rules, kernels from the matcher, the reference's report file."""
+    cfg_path = _workspace(tmp_path, matmul_source, {"source": "matmul.c", "workdir": "work", "cuda": {"n": 256}})
+    rc, out, err = H.cmd_analyze(api, cfg_path)
+    assert rc == 0, err
+    assert "loops: 12" in out and "gene length: 12" in out and "loop 8: line 25, depth 0 -> candidate [kernel: matmul_nt]" in out
+    report = [json.loads(x) for x in (tmp_path / "work" / "probe_report.jsonl").read_text().splitlines()]
+    assert [r["id"] for r in report] == list(range(12)) and all(r["verdict"] == "parallelizable" and r["message"] == "" for r in report)
+    # a loop the rules reject is listed with its class and drops out of the gene
+    poisoned = matmul_source.replace("sum += c[i][i];", "sum += fabs(c[i][i]);")
+    (tmp_path / "p").mkdir()
+    cfg_path = _workspace(tmp_path / "p", poisoned, {"source": "matmul.c", "workdir": "work", "cuda": {"n": 256}})
+    rc, out, _ = H.cmd_analyze(api, cfg_path)
+    assert rc == 0 and "gene length: 11" in out
+    assert "loop 11: line 31, depth 0 -> rejected [external_call] call to 'fabs' with no acc routine information" in out
+
+
+def test_sim_runs_write_the_skipped_probe_report(api, matmul_source, tmp_path):
+    """commands.cpp:78-97 of the reference: sim runs record one 'probe skipped' row per loop."""
+    golden = json.loads((GOLDEN / "tune_sim" / "runs.json").read_text())["m8_t6_seed7"]
+    cfg_path = _workspace(tmp_path, matmul_source, golden["config"])
+    assert H.cmd_tune(api, cfg_path)[0] == 0
+    rows = [json.loads(x) for x in (tmp_path / "work" / "probe_report.jsonl").read_text().splitlines()]
+    assert len(rows) == 12 and all(r["message"] == "probe skipped: timings come from a sim model" and r["verdict"] == "parallelizable"
+                                   and r["reject_class"] is None and r["timed_out"] is False for r in rows)
+    if "probe_report.jsonl" in golden["files"]:
+        assert (tmp_path / "work" / "probe_report.jsonl").read_text() == golden["files"]["probe_report.jsonl"]
 
 
 @pytest.mark.gpu
