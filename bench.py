@@ -254,7 +254,7 @@ def run_ours(args):
         share = ms8 * 1e-3 / (device_s / args.steps)
         roof = {"bound": "tensor", "pipe": "fp64 (DMMA.8x8x4 via mma.sync)" if dtype == capi.F64 else "fp32 (FFMA)",
                 "kernel": "matmul_nt (gene 8)", "achieved": ach, "peak": pipe_peak, "unit": "TFLOP/s", "frac": ach / pipe_peak,
-                "traffic": ncu_traffic("matmul_dmma" if dtype == capi.F64 else "matmul_3xtf32", n), "ms_per_launch": ms8,
+                "traffic": ncu_traffic("matmul_dmma" if dtype == capi.F64 else "matmul_3xtf32s", n), "ms_per_launch": ms8,
                 "share_of_step": share,
                 "peak_source": "FMA-issue peak of the same pipe measured in this run by csrc/peaks.cu "
                                "(MEASURED_PEAKS.json carries only HBM and bf16 figures)"}
@@ -336,10 +336,10 @@ def fp32_arm(n, device, steps, peaks):
         ffma_peak = capi.peak_probe(capi.PEAK_FP32_FMA, device)
     tf32_peak = peaks["bf16_tflops"] / 2.0
     return {"value": flops * steps / dev_s / 1e9, "unit": "GFLOP/s", "steps": steps, "e2e": flops * steps / wall / 1e9,
-            "kernel": "matmul_3xtf32 (gene 8: tcgen05.mma kind::tf32 x3 per term, compensated accumulation; split passes included)",
+            "kernel": "matmul_3xtf32s (gene 8: three TF32 products per term on tcgen05, b parts stacked along N so two of them share one N=256 MMA; compensated accumulation; split passes included)",
             "ms_per_launch": ms8, "effective_fp32_tflops": flops / ms8 / 1e9,
             "roofline": {"bound": "tensor", "achieved": 3.0 * flops / ms8 / 1e9, "peak": tf32_peak, "unit": "TFLOP/s",
-                         "frac": 3.0 * flops / ms8 / 1e9 / tf32_peak, "traffic": ncu_traffic("matmul_3xtf32", n),
+                         "frac": 3.0 * flops / ms8 / 1e9 / tf32_peak, "traffic": ncu_traffic("matmul_3xtf32s", n),
                          "peak_source": "half of MEASURED_PEAKS.json bf16_tflops (TF32 runs at half the bf16 rate); "
                                         "achieved counts the three tensor-core products issued per FP32 term"},
             "vs_ffma_pipe_peak": flops / ms8 / 1e9 / ffma_peak, "ffma_pipe_peak_tflops": ffma_peak}

@@ -10,6 +10,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 # the FP64 contraction (DMMA), the FP32 contraction (tcgen05) and the HBM-bound kernels of one individual
 ncu --set full --clock-control none --import-source on -k regex:'matmul_dmma|transpose_tile|fill2d|trace' -s 12 -c 6 -f \
     -o $out/${tag}_prof_f64 python tools/one_individual.py f64 4096 > $out/${tag}_ncu_f64.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:'matmul_3xtf32|split_tf32' -s 6 -c 3 -f \
+ncu --set full --clock-control none --import-source on -k regex:'matmul_3xtf32|split_tf32|split_planes' -s 6 -c 3 -f \
     -o $out/${tag}_prof_f32 python tools/one_individual.py f32 4096 > $out/${tag}_ncu_f32.log 2>&1
 ls -la $out | tail -8
