@@ -114,6 +114,15 @@ MMXH_API int mmxh_variant_feasible(const char* path_label, const char* text, con
  * returns the loop count */
 MMXH_API int mmxh_match_kernels(const char* path_label, const char* text, char* json_out, size_t cap);
 
+/* calibration (calibrate.hpp): fit the executor's plan model to `count` measured genomes (bits: count x 12), project it onto the
+ * reference's cost-model form and write that JSON.  plan22 receives the fitted parameters {serial, cpu[6], loop[12], h2d s/B, d2h s/B,
+ * per-transfer s}; report8 = {fit rms rel err, fit max rel err, projection rms, projection max, plan best s, cost best s, #inexact loops,
+ * samples used}; best_bits (2 x 12): exhaustive optimum of the plan model, then of the cost model.  Returns the JSON length. */
+MMXH_API int mmxh_calibrate(const uint8_t* bits, const double* times, size_t count, int n, int dtype, char* model_json, size_t cap,
+                            double* plan22, double* report8, uint8_t* best_bits);
+/* time of every genome (index = sum bit_k << k) under the plan model plan22; infeasible genomes get -1 */
+MMXH_API int mmxh_plan_model_times(const double* plan22, int n, int dtype, double* times4096);
+
 /* commands (commands.hpp): return the process exit code (0, 1..5); stdout / stderr text is copied out */
 MMXH_API int mmxh_cmd_tune(const char* config_path, int has_seed, uint64_t seed, const char* sim_model_or_null, char* out, size_t out_cap,
                            char* err, size_t err_cap);

@@ -8,6 +8,7 @@
 #include <string>
 
 #include "mmxhost/backend.hpp"
+#include "mmxhost/calibrate.hpp"
 #include "mmxhost/errors.hpp"
 #include "mmxhost/evaluator.hpp"
 #include "mmxhost/feasibility.hpp"
@@ -488,6 +489,62 @@ MMXH_API int mmxh_match_kernels(const char* path_label, const char* text, char* 
     j += "]}";
     copy_out(j, json_out, cap);
     return static_cast<int>(bs.size());
+  });
+}
+
+namespace {
+PlanModel plan_of(const double* p, int n, int dtype) {
+  PlanModel m;
+  m.n = n;
+  m.dtype = dtype;
+  m.serial_s = p[0];
+  for (int i = 0; i < MMX_NUM_NESTS; ++i) m.cpu_s[i] = p[1 + i];
+  for (int k = 0; k < MMX_GENE_LENGTH; ++k) m.loop_s[k] = p[7 + k];
+  m.h2d_s_per_byte = p[19];
+  m.d2h_s_per_byte = p[20];
+  m.per_transfer_s = p[21];
+  return m;
+}
+}  // namespace
+
+MMXH_API int mmxh_calibrate(const uint8_t* bits, const double* times, size_t count, int n, int dtype, char* model_json, size_t cap,
+                            double* plan22, double* report8, uint8_t* best_bits) {
+  return guarded([&] {
+    std::vector<GenomeSample> samples;
+    for (std::size_t k = 0; k < count; ++k)
+      samples.push_back({Genome(std::vector<std::uint8_t>(bits + k * MMX_GENE_LENGTH, bits + (k + 1) * MMX_GENE_LENGTH)), times[k]});
+    FitReport fit;
+    const PlanModel m = fit_plan_model(samples, n, dtype, &fit);
+    ProjectionReport proj;
+    const CostModel cm = project_to_cost_model(m, &proj);
+    plan22[0] = m.serial_s;
+    for (int i = 0; i < MMX_NUM_NESTS; ++i) plan22[1 + i] = m.cpu_s[i];
+    for (int k = 0; k < MMX_GENE_LENGTH; ++k) plan22[7 + k] = m.loop_s[k];
+    plan22[19] = m.h2d_s_per_byte;
+    plan22[20] = m.d2h_s_per_byte;
+    plan22[21] = m.per_transfer_s;
+    const double rep[8] = {fit.rms_rel_err, fit.max_rel_err, proj.rms_rel_err, proj.max_rel_err, proj.plan_best_s, proj.cost_best_s,
+                           static_cast<double>(proj.inexact_loops.size()), static_cast<double>(fit.samples)};
+    std::memcpy(report8, rep, sizeof(rep));
+    std::memcpy(best_bits, proj.plan_best.bits().data(), MMX_GENE_LENGTH);
+    std::memcpy(best_bits + MMX_GENE_LENGTH, proj.cost_best.bits().data(), MMX_GENE_LENGTH);
+    return copy_out(dump_cost_model_json(cm), model_json, cap);
+  });
+}
+
+MMXH_API int mmxh_plan_model_times(const double* plan22, int n, int dtype, double* times4096) {
+  return guarded([&] {
+    const PlanModel m = plan_of(plan22, n, dtype);
+    for (unsigned mask = 0; mask < 4096; ++mask) {
+      std::vector<std::uint8_t> b(MMX_GENE_LENGTH);
+      for (int k = 0; k < MMX_GENE_LENGTH; ++k) b[static_cast<std::size_t>(k)] = (mask >> k) & 1u;
+      try {
+        times4096[mask] = predict_time(m, Genome(std::move(b)));
+      } catch (const SimulatedCompileError&) {
+        times4096[mask] = -1.0;
+      }
+    }
+    return 0;
   });
 }
 

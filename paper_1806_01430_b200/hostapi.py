@@ -336,3 +336,30 @@ def ref_probe_text(text: str, basename: str, compile_cmd: str, workdir) -> tuple
     buf = C.create_string_buffer(1 << 16)
     rc = api.f("probe_text")(text.encode(), basename.encode(), compile_cmd.encode(), str(workdir).encode(), buf, C.c_size_t(len(buf)))
     return rc, [json.loads(line) for line in buf.value.decode().splitlines() if line]
+
+
+# ---- calibration (calibrate.hpp) ------------------------------------------------------------------------------
+
+def calibrate(genomes, times, n: int, dtype: int = 0) -> dict:
+    """Fit the plan model to measured (genome, seconds) samples and project it onto the reference's cost-model JSON."""
+    api = mine()
+    flat = np.ascontiguousarray(np.concatenate([_bits(g) for g in genomes]).astype(np.uint8))
+    t = np.ascontiguousarray(np.asarray(times, dtype=np.float64))
+    buf = C.create_string_buffer(1 << 18)
+    plan, rep, best = np.zeros(22), np.zeros(8), np.zeros(24, dtype=np.uint8)
+    api.check(api.f("calibrate")(flat.ctypes.data_as(C.POINTER(C.c_uint8)), t.ctypes.data_as(C.POINTER(C.c_double)), C.c_size_t(len(genomes)),
+                                 n, dtype, buf, C.c_size_t(len(buf)), plan.ctypes.data_as(C.POINTER(C.c_double)),
+                                 rep.ctypes.data_as(C.POINTER(C.c_double)), best.ctypes.data_as(C.POINTER(C.c_uint8))))
+    keys = ("fit_rms_rel_err", "fit_max_rel_err", "projection_rms_rel_err", "projection_max_rel_err", "plan_best_s", "cost_best_s",
+            "inexact_loops", "samples")
+    return {"model_json": buf.value.decode(), "plan": plan, "report": dict(zip(keys, map(float, rep))),
+            "plan_best": _str(best[:12]), "cost_best": _str(best[12:])}
+
+
+def plan_model_times(plan22, n: int, dtype: int = 0) -> np.ndarray:
+    """Seconds of all 4096 genomes under a plan model (index = sum bit_k << k); -1 for infeasible genomes."""
+    api = mine()
+    p = np.ascontiguousarray(np.asarray(plan22, dtype=np.float64))
+    out = np.zeros(4096)
+    api.check(api.f("plan_model_times")(p.ctypes.data_as(C.POINTER(C.c_double)), n, dtype, out.ctypes.data_as(C.POINTER(C.c_double))))
+    return out
