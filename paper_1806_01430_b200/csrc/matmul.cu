@@ -218,8 +218,10 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 // Requires n % 2 == 0 (16-byte aligned rows); rows/cols outside the matrix are zero-filled on
 // load and masked on store.  k tail (n % DK) is zero-filled: adding +0 products is harmless in
 // FAST mode except for the sign of an all-zero sum, which compares equal.
+// min-blocks hint: the 4-warp tiles are built to run 3 CTAs per SM (one CTA's barrier or cp.async wait never idles
+// the DMMA pipe); without the cap ptxas drifts to 170 registers and the third CTA no longer fits (measured: -2.5 %)
 template <int DK, int DSTAGES, int WM, int WN, int MT, int NT>
-__global__ void __launch_bounds__(32 * WM * WN)
+__global__ void __launch_bounds__(32 * WM * WN, (WM * WN <= 4 && MT * NT <= 16) ? 3 : 1)
 matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const double* __restrict__ bt, int n,
                    int row0, int rows, int col0, int cols, int group) {
   constexpr int THREADS = 32 * WM * WN;

@@ -332,6 +332,29 @@ def test_n4096_fp64_equals_closed_form(variant):
         assert b[5, 3] == 2.0 / n and ctx.fetch(capi.ARRAY_A)[5, 3] == 8.0 / n
 
 
+@pytest.mark.parametrize("genome,what", [
+    ("101010101001", "all six nests on the GPU"),
+    ("001010101001", "init-a on the CPU: a goes up"),
+    ("101010101000", "trace on the CPU: only the diagonal of c comes down"),
+    ("000000001001", "only matmul + trace on the GPU: a, bt, c go up"),
+])
+def test_n8192_mixed_genomes_move_the_lower_bound_and_equal_the_closed_form(genome, what):
+    """BASELINE config 3 (N=8192, mixed GPU/CPU genomes): the residency planner moves exactly the lower bound of bytes
+    and c equals the exact closed form bit for bit whichever side produced the operands."""
+    n = 8192
+    plan = capi.plan(genome, n, capi.F64)
+    assert plan.feasible and plan.h2d_bytes == plan.h2d_lower_bound and plan.d2h_bytes == plan.d2h_lower_bound
+    with capi.Context(n=n, timeout_s=120.0, host_threads=8) as ctx:
+        out = ctx.measure(genome)
+        assert out.status == capi.MEASURED, what
+        st = ctx.stats()
+        assert (st.h2d_bytes, st.d2h_bytes) == (plan.h2d_bytes, plan.d2h_bytes)
+        assert st.checksum == 0.0
+        got = ctx.fetch(capi.ARRAY_C)
+        for r0 in range(0, n, 1024):
+            assert bits_equal(got[r0:r0 + 1024], cpu.closed_form_c(n, r0, r0 + 1024)), (what, r0)
+
+
 def _normwise_bound_structured(n, tol):
     """tol * sum_k |a_ik| |bt_jk| for the program's own inputs: sum_k (i+k)|k-j| / N^2 = (i A_j + B_j) / N^2."""
     k = np.arange(n, dtype=np.float64)
