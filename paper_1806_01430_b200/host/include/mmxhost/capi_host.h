@@ -128,6 +128,7 @@ MMXH_API int mmxh_cmd_tune(const char* config_path, int has_seed, uint64_t seed,
                            char* err, size_t err_cap);
 MMXH_API int mmxh_cmd_report(const char* workdir, char* out, size_t out_cap, char* err, size_t err_cap);
 MMXH_API int mmxh_cmd_analyze(const char* config_path, char* out, size_t out_cap, char* err, size_t err_cap);
+MMXH_API int mmxh_cmd_calibrate(const char* config_path, char* out, size_t out_cap, char* err, size_t err_cap);
 
 MMXH_API const char* mmxh_status_name(int status);
 /* nlohmann-compatible number formatting used by the cache writer */

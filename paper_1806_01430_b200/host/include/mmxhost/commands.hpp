@@ -7,9 +7,12 @@
 //   generations.csv       %.9g table (ga.cpp:297-309)
 //   summary.json          baseline_s, best_s, speedup, best_genome, distinct_evals, elapsed_s (commands.cpp:157-166)
 //   best/<source>         the winning variant: the source with `#pragma acc kernels` above each selected loop
-// There is no compiler probe on this path, hence no probe_report / probe_cache: with the sim backend every
-// scanned loop (after the filter) is a candidate, as in the reference; with the cuda backend the scanned
-// catalogue must be the one the kernel library serves (mmx_loop_catalogue) and every loop is a candidate.
+//   probe_report.jsonl    one verdict per loop (probe.cpp:162-185): "probe skipped" rows for sim runs, as in the
+//                         reference; the static rules' verdicts (feasibility.hpp) for the cuda backend
+// With the cuda backend the catalogue derived from the source (kernel_match.hpp) must be the one the kernel library
+// serves (mmx_loop_catalogue).  `calibrate` (cuda backend only) adds
+//   calibrated_model.json the reference's cost-model file fitted to measured times (calibrate.hpp)
+//   calibration.json      fit and projection report, the measured and the modelled optimum
 #pragma once
 
 #include <cstdint>
@@ -32,5 +35,8 @@ struct TuneOptions {
 int cmd_analyze(const std::string& config_path, std::ostream& out, std::ostream& err);
 int cmd_tune(const std::string& config_path, const TuneOptions& options, std::ostream& out, std::ostream& err);
 int cmd_report(const std::string& workdir, std::ostream& out, std::ostream& err);
+// Measures every feasible genome through the evaluator (memoised: a rerun replays eval_cache.jsonl), fits the plan
+// model, projects it onto the reference's cost-model form and writes both files into the workdir.
+int cmd_calibrate(const std::string& config_path, std::ostream& out, std::ostream& err);
 
 }  // namespace mmxhost

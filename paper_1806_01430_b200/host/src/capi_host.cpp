@@ -576,6 +576,14 @@ MMXH_API int mmxh_cmd_analyze(const char* config_path, char* out, size_t out_cap
   return rc;
 }
 
+MMXH_API int mmxh_cmd_calibrate(const char* config_path, char* out, size_t out_cap, char* err, size_t err_cap) {
+  std::ostringstream o, e;
+  const int rc = cmd_calibrate(config_path, o, e);
+  copy_out(o.str(), out, out_cap);
+  copy_out(e.str(), err, err_cap);
+  return rc;
+}
+
 MMXH_API const char* mmxh_status_name(int status) {
   static thread_local std::string s;
   s = std::string(to_string(static_cast<EvalStatus>(status)));

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "mmx.h"
+#include "mmxhost/calibrate.hpp"
 #include "mmxhost/config.hpp"
 #include "mmxhost/errors.hpp"
 #include "mmxhost/evaluator.hpp"
@@ -284,6 +285,80 @@ int cmd_tune(const std::string& config_path, const TuneOptions& options, std::os
     return 0;
   } catch (const std::exception& e) {
     err << "tune: " << e.what() << "\n";
+    return exit_code_for(e);
+  }
+}
+
+int cmd_calibrate(const std::string& config_path, std::ostream& out, std::ostream& err) {
+  try {
+    const RunConfig cfg = load_config(config_path);
+    if (!cfg.cuda) throw ConfigError("calibrate needs a 'cuda' block: there is nothing to measure on the sim backend");
+    ensure_workdir(cfg.workdir);
+    write_text_file(cfg.resolved_config_path(), render_resolved_config(cfg));
+    const Inventory inv = take_inventory(cfg);
+    require_kernel_catalogue(inv, cfg);
+    MultiGpuEvaluator evaluator(std::make_unique<CudaBackend>(*cfg.cuda), cfg.eval_cache_path());
+
+    // every genome the static rules accept (648 of 4096 for the matrix application)
+    const std::size_t a = inv.cs.gene_length();
+    const FeasibilityAnalyzer analyzer(inv.cs.unit, inv.cs.all_loops);
+    std::vector<Genome> genomes;
+    for (std::uint64_t mask = 0; mask < (std::uint64_t{1} << a); ++mask) {
+      std::vector<int> annotated;
+      std::vector<std::uint8_t> bits(a);
+      for (std::size_t k = 0; k < a; ++k)
+        if ((mask >> k) & 1u) {
+          bits[k] = 1;
+          annotated.push_back(inv.cs.candidate_ids[k]);
+        }
+      if (analyzer.check(annotated).empty()) genomes.emplace_back(std::move(bits));
+    }
+    const std::vector<EvaluationOutcome> outcomes = evaluator.evaluate_all(genomes);
+    std::vector<GenomeSample> samples;
+    std::size_t timeouts = 0;
+    const GenomeSample* fastest = nullptr;
+    for (std::size_t k = 0; k < genomes.size(); ++k) {
+      if (outcomes[k].status == EvalStatus::Timeout) ++timeouts;
+      if (outcomes[k].status != EvalStatus::Measured) continue;  // a timed-out run says only "slower than the budget"
+      samples.push_back({genomes[k], outcomes[k].time_s});
+    }
+    for (const GenomeSample& s : samples)
+      if (!fastest || s.time_s < fastest->time_s) fastest = &s;
+    FitReport fit;
+    const PlanModel plan = fit_plan_model(samples, cfg.cuda->n, cfg.cuda->dtype, &fit);
+    ProjectionReport proj;
+    const CostModel model = project_to_cost_model(plan, &proj);
+    const std::string model_path = cfg.workdir + "/calibrated_model.json";
+    write_text_file(model_path, dump_cost_model_json(model));
+
+    std::string r = "{\n";
+    r += "  \"n\": " + std::to_string(cfg.cuda->n) + ",\n";
+    r += "  \"feasible_genomes\": " + std::to_string(genomes.size()) + ",\n";
+    r += "  \"measured\": " + std::to_string(samples.size()) + ",\n";
+    r += "  \"timeouts\": " + std::to_string(timeouts) + ",\n";
+    r += "  \"measured_best_genome\": " + json::dump_string(fastest->genome.to_string()) + ",\n";
+    r += "  \"measured_best_s\": " + json::dump_number(fastest->time_s) + ",\n";
+    r += "  \"plan_best_genome\": " + json::dump_string(proj.plan_best.to_string()) + ",\n";
+    r += "  \"plan_best_s\": " + json::dump_number(proj.plan_best_s) + ",\n";
+    r += "  \"cost_best_genome\": " + json::dump_string(proj.cost_best.to_string()) + ",\n";
+    r += "  \"cost_best_s\": " + json::dump_number(proj.cost_best_s) + ",\n";
+    r += "  \"fit_rms_rel_err\": " + json::dump_number(fit.rms_rel_err) + ",\n";
+    r += "  \"fit_max_rel_err\": " + json::dump_number(fit.max_rel_err) + ",\n";
+    r += "  \"projection_rms_rel_err\": " + json::dump_number(proj.rms_rel_err) + ",\n";
+    r += "  \"projection_max_rel_err\": " + json::dump_number(proj.max_rel_err) + ",\n";
+    r += "  \"inexact_loops\": [";
+    for (std::size_t k = 0; k < proj.inexact_loops.size(); ++k) r += (k ? ", " : "") + std::to_string(proj.inexact_loops[k]);
+    r += "]\n}\n";
+    write_text_file(cfg.workdir + "/calibration.json", r);
+
+    out << "genomes:  " << genomes.size() << " feasible, " << samples.size() << " measured, " << timeouts << " over budget\n";
+    out << "measured: " << fastest->genome.to_string() << " " << fmt_s(fastest->time_s) << " s\n";
+    out << "model:    " << proj.cost_best.to_string() << " " << fmt_s(proj.cost_best_s) << " s (fit rms " << fmt_s(fit.rms_rel_err)
+        << ", max " << fmt_s(fit.max_rel_err) << "; " << proj.inexact_loops.size() << " loops not representable additively)\n";
+    out << "model file: " << model_path << "\n";
+    return 0;
+  } catch (const std::exception& e) {
+    err << "calibrate: " << e.what() << "\n";
     return exit_code_for(e);
   }
 }

@@ -4,6 +4,7 @@
 //   mmx_tune analyze <config.json>
 //   mmx_tune tune    <config.json> [--seed N] [--sim model.json]
 //   mmx_tune report  <workdir>
+//   mmx_tune calibrate <config.json>      (cuda backend: measured times -> calibrated_model.json)
 #include <cstdint>
 #include <cstdlib>
 #include <iostream>
@@ -16,7 +17,8 @@ namespace {
 int usage() {
   std::cerr << "usage: mmx_tune analyze <config.json>\n"
                "       mmx_tune tune <config.json> [--seed N] [--sim model.json]\n"
-               "       mmx_tune report <workdir>\n";
+               "       mmx_tune report <workdir>\n"
+               "       mmx_tune calibrate <config.json>\n";
   return 2;
 }
 
@@ -27,6 +29,7 @@ int main(int argc, char** argv) {
   const std::string cmd = argv[1], target = argv[2];
   if (cmd == "analyze" && argc == 3) return mmxhost::cmd_analyze(target, std::cout, std::cerr);
   if (cmd == "report" && argc == 3) return mmxhost::cmd_report(target, std::cout, std::cerr);
+  if (cmd == "calibrate" && argc == 3) return mmxhost::cmd_calibrate(target, std::cout, std::cerr);
   if (cmd == "tune") {
     mmxhost::TuneOptions opt;
     for (int i = 3; i < argc; ++i) {

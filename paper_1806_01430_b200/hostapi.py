@@ -363,3 +363,7 @@ def plan_model_times(plan22, n: int, dtype: int = 0) -> np.ndarray:
     out = np.zeros(4096)
     api.check(api.f("plan_model_times")(p.ctypes.data_as(C.POINTER(C.c_double)), n, dtype, out.ctypes.data_as(C.POINTER(C.c_double))))
     return out
+
+
+def cmd_calibrate(api: Api, config_path) -> tuple[int, str, str]:
+    return _run_command(api.f("cmd_calibrate"), str(config_path).encode())

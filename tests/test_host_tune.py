@@ -221,6 +221,43 @@ def test_sim_runs_write_the_skipped_probe_report(api, matmul_source, tmp_path):
         assert (tmp_path / "work" / "probe_report.jsonl").read_text() == golden["files"]["probe_report.jsonl"]
 
 
+def test_calibrate_needs_the_cuda_backend_and_a_device(api, matmul_source, tmp_path):
+    import torch
+    cfg_path = _workspace(tmp_path, matmul_source, {"source": "matmul.c", "workdir": "work", "sim_model": "model.json"})
+    rc, _, err = H.cmd_calibrate(api, cfg_path)
+    assert rc == 2 and "needs a 'cuda' block" in err
+    if not torch.cuda.is_available():
+        cfg_path = _workspace(tmp_path, matmul_source, {"source": "matmul.c", "workdir": "work", "cuda": {"n": 64}})
+        assert H.cmd_calibrate(api, cfg_path)[0] == 4        # ToolchainMissing: no CPU fallback
+
+
+@pytest.mark.gpu
+def test_calibrate_end_to_end(api, matmul_source, tmp_path):
+    """`calibrate`: every feasible genome measured through the evaluator, the reference's model file written; the file
+    loads, its optimum is a feasible genome close to the measured one, and `tune --sim` replays it."""
+    cfg = {"source": "matmul.c", "workdir": "work", "cuda": {"n": 64, "timeout_s": 20.0, "repetitions": 3, "warmup": 1, "devices": [0, 0]}}
+    cfg_path = _workspace(tmp_path, matmul_source, cfg)
+    rc, out, err = H.cmd_calibrate(api, cfg_path)
+    assert rc == 0, err
+    work = tmp_path / "work"
+    rep = json.loads((work / "calibration.json").read_text())
+    assert rep["feasible_genomes"] == 648 and rep["measured"] + rep["timeouts"] == 648 and rep["measured"] >= 600
+    assert capi.plan(rep["cost_best_genome"], 64, capi.F64).feasible
+    assert rep["fit_rms_rel_err"] < 0.25
+    times = api.model_time_all(work / "calibrated_model.json", 12)
+    assert (times > 0).sum() == 648
+    lines = (work / "eval_cache.jsonl").read_text().splitlines()
+    assert len(lines) == 648
+    # the modelled optimum is among the fastest measured genomes
+    measured = sorted((json.loads(x)["time_s"], json.loads(x)["genome"]) for x in lines if json.loads(x)["status"] == "measured")
+    rank = [g for _, g in measured].index(rep["cost_best_genome"])
+    assert rank < 32, (rank, measured[:3])
+    rc, out2, _ = H.cmd_calibrate(api, cfg_path)                     # rerun: replayed from the cache, same model
+    assert rc == 0 and json.loads((work / "calibration.json").read_text())["cost_best_genome"] == rep["cost_best_genome"]
+    rc, out3, err3 = H.cmd_tune(api, cfg_path, seed=1, sim_model=work / "calibrated_model.json")
+    assert rc == 0, err3
+
+
 @pytest.mark.gpu
 def test_tune_with_the_cuda_backend_end_to_end(api, matmul_source, tmp_path):
     """The drop-in path: `tune` with a "cuda" block measures real individuals at the fixture size and leaves the
