@@ -108,7 +108,9 @@ typedef struct mmx_config {
   int32_t launch_batching;  /* 1: inner-loop launch trains are submitted as CUDA graphs        */
   int32_t matmul_variant;   /* gene-8 kernel: 0 auto (FP64: DMMA, tile by N; FP32: tcgen05 split-TF32 with compensated
                              * accumulation for N >= 1024, FFMA below); 1 first SIMT kernel; 2, 4-13 DMMA tile shapes (FP64);
-                             * 20, 22 SIMT tile shapes; 30 FP32 tcgen05 at any N % 4 == 0; 31 its wide-tile uncompensated form */
+                             * 20, 22 SIMT tile shapes; 30 FP32 tcgen05 at any N % 4 == 0; 31 its wide-tile uncompensated form;
+                             * 40 FP64 on the tcgen05 INT8 tensor cores (7 exact 7-bit slices per operand, error <= 2e-14 K max|a| max|b|,
+                             * bit-identical on the application's inputs), 41 the same with 6 slices */
   int32_t warmup;           /* untimed runs per genome before the timed repetitions (default 0) */
 } mmx_config;
 

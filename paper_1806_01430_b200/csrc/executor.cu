@@ -47,7 +47,7 @@ struct Slot {
   int* d_iter = nullptr;
   void* d_scrub = nullptr;
   std::size_t scrub_bytes = 0;
-  void* d_scratch = nullptr;  // FP32 FAST: split operands of the tensor-core contraction (matmul_tc.cu)
+  void* d_scratch = nullptr;  // operands re-encoded for the tensor-core contractions (FP32: matmul_tc.cu; FP64: matmul_ozaki.cu)
   bool host_valid[MMX_NUM_ARRAYS] = {};
   bool dev_valid[MMX_NUM_ARRAYS] = {};
   bool host_diag_only = false;  // host c holds only its diagonal
@@ -583,7 +583,7 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
   if (cfg->n < 1 || cfg->n > 65536 || (cfg->dtype != MMX_F64 && cfg->dtype != MMX_F32) ||
       (cfg->numerics != MMX_NUMERICS_FAST && cfg->numerics != MMX_NUMERICS_STRICT) || !(cfg->timeout_s > 0.0) ||
       cfg->repetitions < 1 || cfg->num_slots < 1 || cfg->num_slots > 64 || cfg->host_threads < 1 || cfg->warmup < 0 ||
-      cfg->matmul_variant < 0 || cfg->matmul_variant > 31) {
+      cfg->matmul_variant < 0 || cfg->matmul_variant > 41) {
     g_create_error = "invalid configuration value";
     return MMX_E_INVALID;
   }
@@ -631,6 +631,11 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
     {
       if ((e = matmul_3xtf32_prepare()) != cudaSuccess) return fail(e, "matmul_3xtf32_prepare");
       if ((e = cudaMalloc(&sl.d_scratch, matmul_3xtf32_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
+    }
+    if (cfg->dtype == MMX_F64 && cfg->numerics == MMX_NUMERICS_FAST && matmul_ozaki_usable(cfg->n) &&
+        (cfg->matmul_variant == 40 || cfg->matmul_variant == 41)) {
+      if ((e = matmul_ozaki_prepare()) != cudaSuccess) return fail(e, "matmul_ozaki_prepare");
+      if ((e = cudaMalloc(&sl.d_scratch, matmul_ozaki_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
     }
     if ((e = cudaMalloc(&sl.d_sum, 16)) != cudaSuccess) return fail(e, "cudaMalloc(sum)");
     if ((e = cudaMalloc(reinterpret_cast<void**>(&sl.d_iter), sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(iter)");

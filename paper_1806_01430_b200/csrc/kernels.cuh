@@ -70,6 +70,13 @@ cudaError_t matmul_3xtf32_prepare();  // per device, before the first launch (no
 // wide: 128 x 256 tile with plain FP32 masters (faster, looser); default 128 x 128 with compensated masters
 cudaError_t launch_matmul_3xtf32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0,
                                  int cols, bool wide, cudaStream_t stream);
+// FP64 on the 5th-generation tensor cores as exact INT8 slice products (Ozaki scheme, matmul_ozaki.cu); `slices` = 7 (default,
+// |error| <= 2e-14 K max|a| max|b|, bit-identical on the application's inputs) or 6
+bool matmul_ozaki_usable(int n);
+size_t matmul_ozaki_scratch_bytes(int n);
+cudaError_t matmul_ozaki_prepare();  // per device, before the first launch (not inside a stream capture)
+cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0,
+                                int cols, int slices, cudaStream_t stream);
 // gene 9: row i of the same (GEMV against bt)
 template <typename T>
 cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, bool strict, cudaStream_t stream);

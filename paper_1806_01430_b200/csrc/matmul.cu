@@ -507,7 +507,10 @@ int raster_group(int /*tile_m*/, size_t /*row_bytes*/) {
 
 template <>
 cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, int n, int row0, int rows, int col0, int cols,
-                                  bool strict, int variant, void* /*scratch*/, cudaStream_t stream) {
+                                  bool strict, int variant, void* scratch, cudaStream_t stream) {
+  // tensor cores (INT8 slice products, matmul_ozaki.cu): on request
+  if (!strict && scratch != nullptr && (variant == 40 || variant == 41))
+    return launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, variant == 41 ? 6 : 7, stream);
   if (strict) {
     if (n % 2 == 0 && variant == 20) return simt2_go<double, true, 128, 128, 4>(c, a, bt, n, row0, rows, col0, cols, stream);
     if (n % 2 == 0 && variant != 1) return simt2_go<double, true, 64, 64, 3>(c, a, bt, n, row0, rows, col0, cols, stream);

@@ -1,0 +1,321 @@
+// matmul_ozaki.cu -- gene 8 in FP64 on the 5th-generation tensor cores: c[i][j] += sum_k a[i][k] * bt[j][k]
+// (fixtures/matmul.c:25-28) as an error-free INT8 slice decomposition (Ozaki scheme) on tcgen05.mma.kind::i8.
+//
+// B200 has no FP64 tensor-core kind and its FP64 pipe peaks at 36 TFLOP/s, but INT8 MMAs with INT32 accumulation are
+// EXACT and ~120x faster per operation.  Each operand row is scaled by a power of two and cut into S signed 7-bit digits,
+//     x = 2^e * (d_1 2^-6 + d_2 2^-13 + ... + d_S 2^-(7S-1)) + r,   |d_t| <= 64,  |r| <= 2^(e - 7S)
+// (every step exact in FP64: power-of-two scaling, rint, subtraction of a prefix of x's own bits), so
+//     sum_k a_ik b_jk = 2^(ea_i + eb_j + 2) * sum_g 2^(-7g) L_g,        L_g = sum_{t+u=g} sum_k da_t[i][k] db_u[j][k]
+// where every L_g is an integer dot product the tensor core computes without rounding (|L_g| <= 7 * K * 2^12 < 2^31 for
+// K <= 74k).  Levels g > S + 1 are dropped: |error| <= (S + 3) K 2^(-7S) * max_k|a_ik| max_k|b_jk|, i.e. 2e-14 K max max for
+// S = 7 -- below what FP64 accumulation over K terms itself guarantees -- and ZERO whenever the operands carry <= 7S bits
+// below their row maximum: on the application's inputs ((i +- k) / N, 14 bits) the result is bit-identical to the CPU program.
+//
+// Kernel (one CTA per 128 x 64 tile of c, 1 CTA per SM, the S level accumulators of the tile live in TMEM for the whole
+// K loop -- S * 64 = 448 columns -- so there is no mid-loop drain at all):
+//   slice pass  x -> S int8 planes [t][row][k] + one exponent per row            (HBM-bound, (8 + S) N^2 bytes per operand)
+//   warp 0      TMA producer: per 64-k stage ONE 3-D box per operand brings all S slices ([t][row][64 B], SWIZZLE_64B);
+//               2 stages of 84 KB
+//   warp 1      MMA issuer: per 32 k, for t = 1..S: a_t against the slices b_1..b_(S+1-t) STACKED along N (they are
+//               contiguous in shared memory, and their products belong to consecutive levels = consecutive TMEM column
+//               blocks), split into instructions of N <= 256: 10 MMAs carry the 28 slice products of S = 7
+//   warps 2-5   epilogue: L_g -> FP64 Horner sum -> scale by 2^(ea_i + eb_j - 12) -> c += .
+#include <algorithm>
+#include <cstdlib>
+
+#include "kernels.cuh"
+#include "raster.cuh"
+#include "tc_ptx.cuh"
+
+namespace mmx {
+namespace {
+
+constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 64;  // tile of c; k bytes per stage
+constexpr int OZ_STAGES = 2;
+constexpr int OZ_THREADS = 192;                      // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue (one per TMEM lane quarter)
+
+template <int S> struct OzShape {
+  static constexpr int A_SLICE = OZ_BM * OZ_BK, B_SLICE = OZ_BN * OZ_BK;   // 8 KB, 4 KB
+  static constexpr int A_BYTES = S * A_SLICE, B_BYTES = S * B_SLICE;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;                    // 84 KB for S = 7
+  static constexpr int SMEM_BYTES = OZ_STAGES * STAGE_BYTES + 1024 + 256;
+};
+
+// K-major operand tile in the SWIZZLE_64B layout: rows of 64 bytes, 8-row groups 512 bytes apart
+__device__ __forceinline__ unsigned long long umma_desc_sw64(unsigned smem_addr) {
+  return static_cast<unsigned long long>((smem_addr & 0x3FFFF) >> 4) | (static_cast<unsigned long long>(512 >> 4) << 32) | (1ull << 46) |
+         (4ull << 61);
+}
+// cute::UMMA::InstrDescriptor for kind::i8: D = S32 (2 @4), A = B = signed 8 bit (1 @7, 1 @10), both K-major, N >> 3 @17, M >> 4 @24
+__host__ __device__ constexpr unsigned idesc_i8(int n) {
+  return (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<unsigned>(n >> 3) << 17) | (static_cast<unsigned>(OZ_BM >> 4) << 24);
+}
+__device__ __forceinline__ void tc_mma_i8(unsigned d_tmem, unsigned long long adesc, unsigned long long bdesc, unsigned idesc,
+                                          unsigned accumulate) {
+  asm volatile(
+      "{\n.reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ double pow2(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
+
+template <int S>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                    const int* __restrict__ exp_a, const int* __restrict__ exp_b, int n, int kq, int row0, int rows, int col0, int cols,
+                    int group) {
+  using Sh = OzShape<S>;
+  extern __shared__ unsigned char smem_raw[];
+  const unsigned raw = smem_u32(smem_raw);
+  const unsigned base = (raw + 1023u) & ~1023u;
+  const unsigned bars = base + OZ_STAGES * Sh::STAGE_BYTES;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (OZ_STAGES + s); };
+  const unsigned done_bar = bars + 8u * (2 * OZ_STAGES);
+  const unsigned tmem_slot = bars + 8u * (2 * OZ_STAGES + 1);
+  volatile unsigned* tmem_slot_ptr = reinterpret_cast<volatile unsigned*>(smem_raw + (tmem_slot - raw));
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int bx, by;
+  raster_tile(group, bx, by);
+  // a rows are absolute; bt rows are relative to the launch's first column (the slice pass writes them that way)
+  const int m_base = row0 + by * OZ_BM, n_rel = bx * OZ_BN;
+  const int k_stages = kq / OZ_BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < OZ_STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), 1);
+    }
+    mbar_init(done_bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tmem_slot), "n"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const unsigned tmem_base = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < k_stages; ++kb) {
+        const int s = kb % OZ_STAGES;
+        mbar_wait(empty_bar(s), ((kb / OZ_STAGES) & 1) ^ 1);
+        const unsigned st = base + s * Sh::STAGE_BYTES;
+        mbar_expect_tx(full_bar(s), Sh::STAGE_BYTES);
+        tma_load_3d(st, &map_a, kb * OZ_BK, m_base, 0, full_bar(s));
+        tma_load_3d(st + Sh::A_BYTES, &map_b, kb * OZ_BK, n_rel, 0, full_bar(s));
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      for (int kb = 0; kb < k_stages; ++kb) {
+        const int s = kb % OZ_STAGES;
+        mbar_wait(full_bar(s), (kb / OZ_STAGES) & 1);
+        tc_fence_after();
+        const unsigned st = base + s * Sh::STAGE_BYTES;
+#pragma unroll
+        for (int ks = 0; ks < OZ_BK / 32; ++ks) {
+          const unsigned long long adv = 2ull * ks;  // 32 bytes along K inside the 64-byte swizzle row
+#pragma unroll
+          for (int t = 1; t <= S; ++t) {
+            const unsigned long long a_t = umma_desc_sw64(st + (t - 1) * Sh::A_SLICE) + adv;
+            const unsigned first = (kb | ks | (t - 1)) != 0;  // t = 1 of the very first step initialises every level
+            const int count = S + 1 - t;                      // slices b_1 .. b_count pair with a_t (levels t+1 .. S+1)
+#pragma unroll
+            for (int u0 = 0; u0 < count; u0 += 4) {
+              const int nsl = count - u0 < 4 ? count - u0 : 4;
+              const unsigned long long b_u = umma_desc_sw64(st + Sh::A_BYTES + u0 * Sh::B_SLICE) + adv;
+              // level of (t, u0 + 1) is t + u0 + 1; its TMEM column block is level - 2
+              tc_mma_i8(tmem_base + (t - 1 + u0) * OZ_BN, a_t, b_u, idesc_i8(nsl * OZ_BN), first);
+            }
+          }
+        }
+        tc_commit(empty_bar(s));
+      }
+      tc_commit(done_bar);
+    }
+  } else {
+    // epilogue: thread = one row of the tile (TMEM lane), 8 columns at a time
+    const int q = warp % 4;
+    mbar_wait(done_bar, 0);
+    tc_fence_after();
+    const int m = m_base + q * 32 + lane;
+    const int m_limit = row0 + rows;
+    const bool row_ok = m < m_limit;
+    const double scale_i = row_ok ? pow2(exp_a[m] - 12) : 0.0;
+    double* crow = c + static_cast<size_t>(row_ok ? m : 0) * n;
+    const unsigned t0 = tmem_base + (static_cast<unsigned>(q * 32) << 16);
+    const bool vec_ok = (n % 2 == 0) && (col0 % 2 == 0);
+#pragma unroll 1
+    for (int cb = 0; cb < OZ_BN / 8; ++cb) {
+      unsigned lv[S][8];
+#pragma unroll
+      for (int g = 0; g < S; ++g) tc_ld8_issue(t0 + g * OZ_BN + cb * 8, lv[g]);
+      tc_ld_wait();
+#pragma unroll
+      for (int e = 0; e < 8; e += 2) {
+        const int jr = n_rel + cb * 8 + e;  // relative to col0
+        double v[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          double acc = static_cast<double>(static_cast<int>(lv[S - 1][e + h]));
+#pragma unroll
+          for (int g = S - 2; g >= 0; --g) acc = fma(acc, 0.0078125, static_cast<double>(static_cast<int>(lv[g][e + h])));
+          v[h] = acc;
+        }
+        if (!row_ok) continue;
+        const int j = col0 + jr;
+        if (vec_ok && jr + 2 <= cols) {
+          double2 x = *reinterpret_cast<const double2*>(crow + j);
+          x.x += v[0] * scale_i * pow2(exp_b[jr]);
+          x.y += v[1] * scale_i * pow2(exp_b[jr + 1]);
+          *reinterpret_cast<double2*>(crow + j) = x;
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h)
+            if (jr + h < cols) crow[j + h] += v[h] * scale_i * pow2(exp_b[jr + h]);
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(512) : "memory");
+  }
+}
+
+// One CTA per row: row maximum -> exponent e (|x| < 2^e), then S digits per element.  dst plane t of row r (relative
+// index) is dst + t * plane + r * kq; k >= n is zero.  Rows [src_row0, src_row0 + nrows) of src; rows up to nrows_pad are
+// written as zeros with exponent 0 (tile overhang inside the tensor map).
+template <int S>
+__global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restrict__ src, signed char* __restrict__ dst, int* __restrict__ exps,
+                                                          size_t plane, int n, int kq, int src_row0, int nrows, int dst_row0) {
+  __shared__ double red[8];
+  __shared__ int e_sh;
+  const int r = blockIdx.x;  // relative row
+  const int tid = threadIdx.x;
+  const bool live = r < nrows;
+  const double* x = src + static_cast<size_t>(src_row0 + (live ? r : 0)) * n;
+  double mx = 0.0;
+  if (live)
+    for (int k = tid; k < n; k += 256) mx = fmax(mx, fabs(x[k]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if (tid % 32 == 0) red[tid / 32] = mx;
+  __syncthreads();
+  if (tid == 0) {
+    double m = red[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) m = fmax(m, red[w]);
+    const int e = m > 0.0 ? ilogb(m) + 1 : 0;
+    e_sh = e;
+    exps[dst_row0 + r] = e;
+  }
+  __syncthreads();
+  const double inv = live ? scalbn(1.0, -e_sh) : 0.0;  // exact power of two (rows of normal doubles)
+  signed char* drow = dst + static_cast<size_t>(dst_row0 + r) * kq;
+  // 16 consecutive k per thread and iteration: one 16-byte store per slice
+  for (int k0 = tid * 16; k0 < kq; k0 += 256 * 16) {
+    int dig[S][4] = {};
+#pragma unroll
+    for (int q = 0; q < 16; ++q) {
+      const int k = k0 + q;
+      double rem = (live && k < n) ? x[k] * inv : 0.0;
+#pragma unroll
+      for (int t = 0; t < S; ++t) {
+        const double up = pow2(7 * (t + 1) - 1), down = pow2(-(7 * (t + 1) - 1));
+        const int d = __double2int_rn(rem * up);
+        rem = fma(-static_cast<double>(d), down, rem);  // exact: removes a prefix of rem's bits
+        dig[t][q / 4] |= (d & 0xff) << (8 * (q % 4));
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < S; ++t)
+      *reinterpret_cast<int4*>(drow + t * plane + k0) = make_int4(dig[t][0], dig[t][1], dig[t][2], dig[t][3]);
+  }
+}
+
+// [S][rows][kq] bytes; box = 64 bytes x box_rows rows x S slices; 64-byte swizzle
+bool make_slice_map(CUtensorMap* map, const signed char* ptr, size_t rows, int kq, int box_rows, int slices) {
+  EncodeTiledFn enc = encode_tiled();
+  if (enc == nullptr) return false;
+  const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kq), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(slices)};
+  const cuuint64_t strides[2] = {static_cast<cuuint64_t>(kq), static_cast<cuuint64_t>(kq) * rows};
+  const cuuint32_t box[3] = {OZ_BK, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(slices)};
+  const cuuint32_t elem[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<signed char*>(ptr), dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+inline int oz_kq(int n) { return (n + OZ_BK - 1) / OZ_BK * OZ_BK; }
+inline size_t oz_rows_pad(int rows, int tile) { return static_cast<size_t>((rows + tile - 1) / tile) * tile; }
+
+template <int S>
+cudaError_t oz_configure() {
+  static PerDeviceOnce once;
+  bool& configured = once.here();
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(matmul_ozaki_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, OzShape<S>::SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  return cudaSuccess;
+}
+
+template <int S>
+cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
+                  cudaStream_t stream) {
+  if (cudaError_t e = oz_configure<S>(); e != cudaSuccess) return e;
+  const int kq = oz_kq(n);
+  // scratch: a slices [S][n][kq] (absolute rows), bt slices [S][pad64(n)][kq] (rows relative to col0), exponents
+  const size_t a_plane = static_cast<size_t>(n) * kq, b_rows = oz_rows_pad(n, OZ_BN), b_plane = b_rows * kq;
+  signed char* sa = static_cast<signed char*>(scratch);
+  signed char* sb = sa + S * a_plane;
+  int* ea = reinterpret_cast<int*>(sb + S * b_plane);
+  int* eb = ea + n;
+  const int cols_pad = static_cast<int>(oz_rows_pad(cols, OZ_BN));
+  ozaki_slice_kernel<S><<<rows, 256, 0, stream>>>(a, sa, ea, a_plane, n, kq, row0, rows, row0);
+  ozaki_slice_kernel<S><<<cols_pad, 256, 0, stream>>>(bt, sb, eb, b_plane, n, kq, col0, cols, 0);
+  CUtensorMap map_a, map_b;
+  if (!make_slice_map(&map_a, sa, static_cast<size_t>(n), kq, OZ_BM, S) || !make_slice_map(&map_b, sb, b_rows, kq, OZ_BN, S))
+    return cudaErrorNotSupported;
+  dim3 grid((cols + OZ_BN - 1) / OZ_BN, (rows + OZ_BM - 1) / OZ_BM);
+  matmul_ozaki_kernel<S><<<grid, OZ_THREADS, OzShape<S>::SMEM_BYTES, stream>>>(c, map_a, map_b, ea, eb, n, kq, row0, rows, col0, cols,
+                                                                              raster_group(OZ_BM, static_cast<size_t>(kq)));
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool matmul_ozaki_usable(int n) { return n >= 1 && encode_tiled() != nullptr; }
+
+cudaError_t matmul_ozaki_prepare() {
+  if (encode_tiled() == nullptr) return cudaErrorNotSupported;
+  if (cudaError_t e = oz_configure<7>(); e != cudaSuccess) return e;
+  return oz_configure<6>();
+}
+
+size_t matmul_ozaki_scratch_bytes(int n) {
+  const size_t kq = static_cast<size_t>(oz_kq(n));
+  return 7 * (static_cast<size_t>(n) + oz_rows_pad(n, OZ_BN)) * kq + 2 * (static_cast<size_t>(n) + OZ_BN) * sizeof(int) + 256;
+}
+
+cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
+                                int slices, cudaStream_t stream) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  if (scratch == nullptr) return cudaErrorInvalidValue;
+  if (slices == 6) return oz_go<6>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+  return oz_go<7>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+}
+
+}  // namespace mmx
