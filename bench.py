@@ -49,6 +49,7 @@ def parse_args():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 arm of the configuration")
+    ap.add_argument("--no-fp64-tensor", action="store_true", help="skip the FP64-on-INT8-tensor-cores arm")
     ap.add_argument("--ga", action="store_true", help="also run the GA search (M=12, T=12) with real timings")
     return ap.parse_args()
 
@@ -276,6 +277,11 @@ def run_ours(args):
     if rank == 0 and dtype == capi.F64 and not args.no_fp32:
         fp32 = fp32_arm(n, local_rank, max(10, args.steps // 4), peaks)
 
+    # FP64 with the contraction on the INT8 tensor cores (matmul_variant 40: exact 7-bit slices, matmul_ozaki.cu)
+    fp64_tensor = None
+    if rank == 0 and dtype == capi.F64 and not args.no_fp64_tensor:
+        fp64_tensor = fp64_tensor_arm(n, local_rank, max(10, args.steps // 4), peaks, checksum)
+
     # the sampler covers the timed region plus the (equally loaded) mixed-genome and roofline phases
     clocks = sampler.stop()
 
@@ -307,6 +313,8 @@ def run_ours(args):
         }
         if fp32 is not None:
             line["fp32"] = fp32
+        if fp64_tensor is not None:
+            line["fp64_tensor"] = fp64_tensor
         if ga is not None:
             line["ga_search"] = ga
         print(json.dumps(line), flush=True)
@@ -382,6 +390,37 @@ def fp32_arm(n, device, steps, peaks):
                          "peak_source": "half of MEASURED_PEAKS.json bf16_tflops (TF32 runs at half the bf16 rate); "
                                         "achieved counts the three tensor-core products issued per FP32 term"},
             "vs_ffma_pipe_peak": flops / ms8 / 1e9 / ffma_peak, "ffma_pipe_peak_tflops": ffma_peak}
+
+
+def fp64_tensor_arm(n, device, steps, peaks, reference_checksum):
+    """The same steps with gene 8 on the tcgen05 INT8 tensor cores.  Results are bit-identical to the default path on this
+    workload (checked here on c's corner and the checksum; tests compare all of c), within 1e-12 norm-wise in general."""
+    from paper_1806_01430_b200 import capi
+    flops = 2.0 * n ** 3
+    with capi.Context(n=n, dtype=capi.F64, matmul_variant=40, devices=[device], timeout_s=600.0) as ctx:
+        for _ in range(3):
+            ctx.measure(GENOME_ALL_NESTS)
+        dev_s = 0.0
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            dev_s += ctx.measure(GENOME_ALL_NESTS).time_s
+        wall = time.perf_counter() - t0
+        checksum = ctx.stats().checksum
+        c = ctx.fetch(capi.ARRAY_C)
+        ms8 = ctx.time_loop(8, 5, True)
+    s2 = (n - 1) * n * (2 * n - 1) / 6
+    int8_peak = 2.0 * peaks["bf16_tflops"]
+    ops = 28.0 * flops            # 28 slice products per term
+    return {"value": flops * steps / dev_s / 1e9, "unit": "GFLOP/s", "steps": steps, "e2e": flops * steps / wall / 1e9,
+            "kernel": "matmul_ozaki (gene 8: 7 exact 7-bit INT8 slices per operand, 28 slice products on tcgen05.mma.kind::i8 with "
+                      "INT32 accumulation in TMEM; slice passes included)",
+            "ms_per_launch": ms8, "effective_fp64_tflops": flops / ms8 / 1e9,
+            "bit_identical_to_default_path": bool(checksum == reference_checksum and float(c[0, 0]) == s2 / (n * n)
+                                                  and float(c[1, 2]) == (s2 - n * (n - 1) / 2 - 2 * n) / (n * n)),
+            "roofline": {"bound": "tensor", "achieved": ops / ms8 / 1e9, "peak": int8_peak, "unit": "TOP/s", "frac": ops / ms8 / 1e9 / int8_peak,
+                         "traffic": ncu_traffic("matmul_ozaki", n),
+                         "peak_source": "twice MEASURED_PEAKS.json bf16_tflops (INT8 runs at twice the bf16 rate); achieved counts the "
+                                        "28 INT8 slice products issued per FP64 term"}}
 
 
 def run_ga_search(n, dtype, devices, population=12, generations=12, seed=1, timeout_s=0.5):

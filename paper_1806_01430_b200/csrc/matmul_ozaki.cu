@@ -15,7 +15,7 @@
 // K loop -- S * 64 = 448 columns -- so there is no mid-loop drain at all):
 //   slice pass  x -> S int8 planes [t][row][k] + one exponent per row            (HBM-bound, (8 + S) N^2 bytes per operand)
 //   warp 0      TMA producer: per 64-k stage ONE 3-D box per operand brings all S slices ([t][row][64 B], SWIZZLE_64B);
-//               2 stages of 84 KB
+//               2 stages of 84 KB (optionally the a slices are multicast over a cluster of column tiles)
 //   warp 1      MMA issuer: per 32 k, for t = 1..S: a_t against the slices b_1..b_(S+1-t) STACKED along N (they are
 //               contiguous in shared memory, and their products belong to consecutive levels = consecutive TMEM column
 //               blocks), split into instructions of N <= 256: 10 MMAs carry the 28 slice products of S = 7
@@ -30,21 +30,29 @@
 namespace mmx {
 namespace {
 
-constexpr int OZ_BM = 128, OZ_BN = 64, OZ_BK = 64;  // tile of c; k bytes per stage
-constexpr int OZ_STAGES = 2;
+constexpr int OZ_BM = 128, OZ_BN = 64;               // tile of c
 constexpr int OZ_THREADS = 192;                      // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue (one per TMEM lane quarter)
+constexpr int OZ_KPAD = 64;                          // slice rows are padded to this many k
 
-template <int S> struct OzShape {
-  static constexpr int A_SLICE = OZ_BM * OZ_BK, B_SLICE = OZ_BN * OZ_BK;   // 8 KB, 4 KB
+// BK = k bytes per pipeline stage = bytes per shared-memory row (SWIZZLE_64B or SWIZZLE_32B).  All S slices of both operands
+// have to be resident per stage, so a stage is S * 192 * BK bytes: 84 KB (2 stages) at BK = 64, 42 KB (5 stages) at BK = 32.
+// Measured (tools/ozaki_cluster_sweep.sh, N = 4096 / 8192): BK = 64 92 / 96 TFLOP/s, BK = 32 with 5 stages 81 / 81, BK = 64
+// with the a slices multicast over clusters of 2 / 4 CTAs 93 / 85 -- neither refill latency nor L2 traffic is the limit.
+// The tensor pipe is 64 % busy (ncu); the rest goes to shared-memory bandwidth: every MMA re-reads its 4 KB a slice, and the
+// narrow tail instructions (N = 64 .. 192) need up to 192 B/clk of operands against the 128 B/clk an SM delivers.
+template <int S, int BK> struct OzShape {
+  static constexpr int A_SLICE = OZ_BM * BK, B_SLICE = OZ_BN * BK;
   static constexpr int A_BYTES = S * A_SLICE, B_BYTES = S * B_SLICE;
-  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;                    // 84 KB for S = 7
-  static constexpr int SMEM_BYTES = OZ_STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int STAGES = (227 * 1024 - 2048) / STAGE_BYTES;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
 };
 
-// K-major operand tile in the SWIZZLE_64B layout: rows of 64 bytes, 8-row groups 512 bytes apart
-__device__ __forceinline__ unsigned long long umma_desc_sw64(unsigned smem_addr) {
-  return static_cast<unsigned long long>((smem_addr & 0x3FFFF) >> 4) | (static_cast<unsigned long long>(512 >> 4) << 32) | (1ull << 46) |
-         (4ull << 61);
+// K-major operand tile whose rows are one swizzle span (BK = 64 or 32 bytes) wide; 8-row groups 8 * BK bytes apart
+template <int BK>
+__device__ __forceinline__ unsigned long long umma_desc_sw(unsigned smem_addr) {
+  return static_cast<unsigned long long>((smem_addr & 0x3FFFF) >> 4) | (static_cast<unsigned long long>((8 * BK) >> 4) << 32) | (1ull << 46) |
+         ((BK == 64 ? 4ull : 6ull) << 61);
 }
 // cute::UMMA::InstrDescriptor for kind::i8: D = S32 (2 @4), A = B = signed 8 bit (1 @7, 1 @10), both K-major, N >> 3 @17, M >> 4 @24
 __host__ __device__ constexpr unsigned idesc_i8(int n) {
@@ -62,12 +70,16 @@ __device__ __forceinline__ void tc_mma_i8(unsigned d_tmem, unsigned long long ad
 
 __device__ __forceinline__ double pow2(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
 
-template <int S>
+// C = CTAs per cluster: C consecutive column tiles of one tile-row share their a slices -- every CTA fetches 1/C of the rows
+// of each slice and multicasts them (the kernel is bound by L2 -> SM traffic otherwise: 84 KB per 64-k stage against
+// 1792 tensor-pipe cycles)
+template <int S, int C, int BK>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
-matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                    const int* __restrict__ exp_a, const int* __restrict__ exp_b, int n, int kq, int row0, int rows, int col0, int cols,
+matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_a_part,
+                    const __grid_constant__ CUtensorMap map_b, const int* __restrict__ exp_a, const int* __restrict__ exp_b, int n, int kq, int row0, int rows, int col0, int cols,
                     int group) {
-  using Sh = OzShape<S>;
+  using Sh = OzShape<S, BK>;
+  constexpr int OZ_STAGES = Sh::STAGES, OZ_BK = BK;
   extern __shared__ unsigned char smem_raw[];
   const unsigned raw = smem_u32(smem_raw);
   const unsigned base = (raw + 1023u) & ~1023u;
@@ -79,8 +91,12 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
   volatile unsigned* tmem_slot_ptr = reinterpret_cast<volatile unsigned*>(smem_raw + (tmem_slot - raw));
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  int bx, by;
-  raster_tile(group, bx, by);
+  const unsigned rank = C > 1 ? cluster_ctarank() : 0u;
+  constexpr unsigned short kMask = static_cast<unsigned short>((1u << C) - 1u);
+  int sx, by;  // clusters are C consecutive CTAs along x: raster over the grid of clusters
+  raster_map(group, static_cast<int>(gridDim.x) / C, static_cast<int>(gridDim.y),
+             static_cast<int>(blockIdx.y) * (static_cast<int>(gridDim.x) / C) + static_cast<int>(blockIdx.x) / C, sx, by);
+  const int bx = sx * C + static_cast<int>(rank);
   // a rows are absolute; bt rows are relative to the launch's first column (the slice pass writes them that way)
   const int m_base = row0 + by * OZ_BM, n_rel = bx * OZ_BN;
   const int k_stages = kq / OZ_BK;
@@ -88,7 +104,7 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
   if (threadIdx.x == 0) {
     for (int s = 0; s < OZ_STAGES; ++s) {
       mbar_init(full_bar(s), 1);
-      mbar_init(empty_bar(s), 1);
+      mbar_init(empty_bar(s), C);  // every CTA of the cluster reads what is multicast into this stage
     }
     mbar_init(done_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -99,6 +115,7 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (C > 1) cluster_sync_all();  // peers' barriers are initialised before anything is multicast at them
   tc_fence_after();
   const unsigned tmem_base = *tmem_slot_ptr;
 
@@ -109,7 +126,15 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
         mbar_wait(empty_bar(s), ((kb / OZ_STAGES) & 1) ^ 1);
         const unsigned st = base + s * Sh::STAGE_BYTES;
         mbar_expect_tx(full_bar(s), Sh::STAGE_BYTES);
-        tma_load_3d(st, &map_a, kb * OZ_BK, m_base, 0, full_bar(s));
+        if constexpr (C == 1) {
+          tma_load_3d(st, &map_a, kb * OZ_BK, m_base, 0, full_bar(s));
+        } else {
+          constexpr int PART = OZ_BM / C;  // rows of every slice this CTA fetches for the whole cluster
+#pragma unroll
+          for (int t = 0; t < S; ++t)
+            tma_load_3d_mc(st + t * Sh::A_SLICE + rank * (PART * OZ_BK), &map_a_part, kb * OZ_BK, m_base + static_cast<int>(rank) * PART, t,
+                           full_bar(s), kMask);
+        }
         tma_load_3d(st + Sh::A_BYTES, &map_b, kb * OZ_BK, n_rel, 0, full_bar(s));
       }
     }
@@ -125,19 +150,20 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
           const unsigned long long adv = 2ull * ks;  // 32 bytes along K inside the 64-byte swizzle row
 #pragma unroll
           for (int t = 1; t <= S; ++t) {
-            const unsigned long long a_t = umma_desc_sw64(st + (t - 1) * Sh::A_SLICE) + adv;
+            const unsigned long long a_t = umma_desc_sw<BK>(st + (t - 1) * Sh::A_SLICE) + adv;
             const unsigned first = (kb | ks | (t - 1)) != 0;  // t = 1 of the very first step initialises every level
             const int count = S + 1 - t;                      // slices b_1 .. b_count pair with a_t (levels t+1 .. S+1)
 #pragma unroll
             for (int u0 = 0; u0 < count; u0 += 4) {
               const int nsl = count - u0 < 4 ? count - u0 : 4;
-              const unsigned long long b_u = umma_desc_sw64(st + Sh::A_BYTES + u0 * Sh::B_SLICE) + adv;
+              const unsigned long long b_u = umma_desc_sw<BK>(st + Sh::A_BYTES + u0 * Sh::B_SLICE) + adv;
               // level of (t, u0 + 1) is t + u0 + 1; its TMEM column block is level - 2
               tc_mma_i8(tmem_base + (t - 1 + u0) * OZ_BN, a_t, b_u, idesc_i8(nsl * OZ_BN), first);
             }
           }
         }
-        tc_commit(empty_bar(s));
+        if constexpr (C == 1) tc_commit(empty_bar(s));
+        else tc_commit_mc(empty_bar(s), kMask);
       }
       tc_commit(done_bar);
     }
@@ -192,6 +218,7 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(512) : "memory");
   }
+  if constexpr (C > 1) cluster_sync_all();  // no CTA leaves while a peer may still signal its barriers
 }
 
 // One CTA per row: row maximum -> exponent e (|x| < 2^e), then S digits per element.  dst plane t of row r (relative
@@ -224,58 +251,64 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
   __syncthreads();
   const double inv = live ? scalbn(1.0, -e_sh) : 0.0;  // exact power of two (rows of normal doubles)
   signed char* drow = dst + static_cast<size_t>(dst_row0 + r) * kq;
-  // 16 consecutive k per thread and iteration: one 16-byte store per slice
-  for (int k0 = tid * 16; k0 < kq; k0 += 256 * 16) {
-    int dig[S][4] = {};
+  // 4 consecutive k per thread and iteration: a warp reads 1 KB and writes 128 bytes per slice, both contiguous
+  for (int k0 = tid * 4; k0 < kq; k0 += 256 * 4) {
+    double v[4];
+    if (live && k0 + 4 <= n && n % 2 == 0) {
+      const double2 p = *reinterpret_cast<const double2*>(x + k0), q2 = *reinterpret_cast<const double2*>(x + k0 + 2);
+      v[0] = p.x; v[1] = p.y; v[2] = q2.x; v[3] = q2.y;
+    } else {
 #pragma unroll
-    for (int q = 0; q < 16; ++q) {
-      const int k = k0 + q;
-      double rem = (live && k < n) ? x[k] * inv : 0.0;
+      for (int q = 0; q < 4; ++q) v[q] = (live && k0 + q < n) ? x[k0 + q] : 0.0;
+    }
+    int dig[S] = {};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      double rem = v[q] * inv;
 #pragma unroll
       for (int t = 0; t < S; ++t) {
         const double up = pow2(7 * (t + 1) - 1), down = pow2(-(7 * (t + 1) - 1));
         const int d = __double2int_rn(rem * up);
         rem = fma(-static_cast<double>(d), down, rem);  // exact: removes a prefix of rem's bits
-        dig[t][q / 4] |= (d & 0xff) << (8 * (q % 4));
+        dig[t] |= (d & 0xff) << (8 * q);
       }
     }
 #pragma unroll
-    for (int t = 0; t < S; ++t)
-      *reinterpret_cast<int4*>(drow + t * plane + k0) = make_int4(dig[t][0], dig[t][1], dig[t][2], dig[t][3]);
+    for (int t = 0; t < S; ++t) *reinterpret_cast<int*>(drow + t * plane + k0) = dig[t];
   }
 }
 
 // [S][rows][kq] bytes; box = 64 bytes x box_rows rows x S slices; 64-byte swizzle
-bool make_slice_map(CUtensorMap* map, const signed char* ptr, size_t rows, int kq, int box_rows, int slices) {
+bool make_slice_map(CUtensorMap* map, const signed char* ptr, size_t rows, int kq, int bk, int box_rows, int slices, int box_slices) {
   EncodeTiledFn enc = encode_tiled();
   if (enc == nullptr) return false;
   const cuuint64_t dims[3] = {static_cast<cuuint64_t>(kq), static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(slices)};
   const cuuint64_t strides[2] = {static_cast<cuuint64_t>(kq), static_cast<cuuint64_t>(kq) * rows};
-  const cuuint32_t box[3] = {OZ_BK, static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(slices)};
+  const cuuint32_t box[3] = {static_cast<cuuint32_t>(bk), static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_slices)};
   const cuuint32_t elem[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<signed char*>(ptr), dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE,
-             CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             bk == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-inline int oz_kq(int n) { return (n + OZ_BK - 1) / OZ_BK * OZ_BK; }
+inline int oz_kq(int n) { return (n + OZ_KPAD - 1) / OZ_KPAD * OZ_KPAD; }
 inline size_t oz_rows_pad(int rows, int tile) { return static_cast<size_t>((rows + tile - 1) / tile) * tile; }
 
-template <int S>
+template <int S, int C, int BK>
 cudaError_t oz_configure() {
   static PerDeviceOnce once;
   bool& configured = once.here();
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(matmul_ozaki_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize, OzShape<S>::SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(matmul_ozaki_kernel<S, C, BK>, cudaFuncAttributeMaxDynamicSharedMemorySize, OzShape<S, BK>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   return cudaSuccess;
 }
 
-template <int S>
+template <int S, int C, int BK>
 cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
                   cudaStream_t stream) {
-  if (cudaError_t e = oz_configure<S>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_configure<S, C, BK>(); e != cudaSuccess) return e;
   const int kq = oz_kq(n);
   // scratch: a slices [S][n][kq] (absolute rows), bt slices [S][pad64(n)][kq] (rows relative to col0), exponents
   const size_t a_plane = static_cast<size_t>(n) * kq, b_rows = oz_rows_pad(n, OZ_BN), b_plane = b_rows * kq;
@@ -286,13 +319,25 @@ cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, i
   const int cols_pad = static_cast<int>(oz_rows_pad(cols, OZ_BN));
   ozaki_slice_kernel<S><<<rows, 256, 0, stream>>>(a, sa, ea, a_plane, n, kq, row0, rows, row0);
   ozaki_slice_kernel<S><<<cols_pad, 256, 0, stream>>>(bt, sb, eb, b_plane, n, kq, col0, cols, 0);
-  CUtensorMap map_a, map_b;
-  if (!make_slice_map(&map_a, sa, static_cast<size_t>(n), kq, OZ_BM, S) || !make_slice_map(&map_b, sb, b_rows, kq, OZ_BN, S))
+  CUtensorMap map_a, map_a_part, map_b;
+  if (!make_slice_map(&map_a, sa, static_cast<size_t>(n), kq, BK, OZ_BM, S, S) ||
+      !make_slice_map(&map_a_part, sa, static_cast<size_t>(n), kq, BK, OZ_BM / C, S, 1) || !make_slice_map(&map_b, sb, b_rows, kq, BK, OZ_BN, S, S))
     return cudaErrorNotSupported;
-  dim3 grid((cols + OZ_BN - 1) / OZ_BN, (rows + OZ_BM - 1) / OZ_BM);
-  matmul_ozaki_kernel<S><<<grid, OZ_THREADS, OzShape<S>::SMEM_BYTES, stream>>>(c, map_a, map_b, ea, eb, n, kq, row0, rows, col0, cols,
-                                                                              raster_group(OZ_BM, static_cast<size_t>(kq)));
-  return cudaGetLastError();
+  const int col_tiles = (cols + OZ_BN - 1) / OZ_BN;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((col_tiles + C - 1) / C * C, (rows + OZ_BM - 1) / OZ_BM);  // whole clusters; surplus tiles are masked
+  cfg.blockDim = dim3(OZ_THREADS);
+  cfg.dynamicSmemBytes = OzShape<S, BK>::SMEM_BYTES;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = C > 1 ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, matmul_ozaki_kernel<S, C, BK>, c, map_a, map_a_part, map_b, static_cast<const int*>(ea), static_cast<const int*>(eb), n,
+                            kq, row0, rows, col0, cols, raster_group(OZ_BM, static_cast<size_t>(kq)));
 }
 
 }  // namespace
@@ -301,8 +346,11 @@ bool matmul_ozaki_usable(int n) { return n >= 1 && encode_tiled() != nullptr; }
 
 cudaError_t matmul_ozaki_prepare() {
   if (encode_tiled() == nullptr) return cudaErrorNotSupported;
-  if (cudaError_t e = oz_configure<7>(); e != cudaSuccess) return e;
-  return oz_configure<6>();
+  if (cudaError_t e = oz_configure<7, 1, 32>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_configure<7, 1, 64>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_configure<7, 2, 64>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_configure<7, 4, 64>(); e != cudaSuccess) return e;
+  return oz_configure<6, 1, 64>();
 }
 
 size_t matmul_ozaki_scratch_bytes(int n) {
@@ -314,8 +362,14 @@ cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, vo
                                 int slices, cudaStream_t stream) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr) return cudaErrorInvalidValue;
-  if (slices == 6) return oz_go<6>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
-  return oz_go<7>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+  // tuning hooks (tools/ozaki_cluster_sweep.sh): CTAs per cluster sharing the a slices by multicast, k bytes per stage
+  static const int cluster = [] { const char* e = getenv("MMX_OZ_CLUSTER"); return e ? atoi(e) : 1; }();
+  static const int bk = [] { const char* e = getenv("MMX_OZ_BK"); return e ? atoi(e) : 64; }();
+  if (slices == 6) return oz_go<6, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+  if (cluster == 4) return oz_go<7, 4, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+  if (cluster == 2) return oz_go<7, 2, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+  if (bk == 32) return oz_go<7, 1, 32>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+  return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
 }
 
 }  // namespace mmx

@@ -10,15 +10,13 @@
 
 namespace mmx {
 
-// (bx, by) = tile column / tile row served by this CTA; gridDim = (tile columns, tile rows)
-__device__ __forceinline__ void raster_tile(int group, int& bx, int& by) {
-  const int gx = static_cast<int>(gridDim.x), gy = static_cast<int>(gridDim.y);
+// linear dispatch index `lin` over a gx x gy grid of tiles -> (bx, by)
+__device__ __forceinline__ void raster_map(int group, int gx, int gy, int lin, int& bx, int& by) {
   if (group <= 1 || gy == 1) {
-    bx = static_cast<int>(blockIdx.x);
-    by = static_cast<int>(blockIdx.y);
+    bx = lin % gx;
+    by = lin / gx;
     return;
   }
-  const int lin = static_cast<int>(blockIdx.y) * gx + static_cast<int>(blockIdx.x);
   const int per_group = group * gx;
   const int grp = lin / per_group;
   const int first = grp * group;
@@ -26,6 +24,12 @@ __device__ __forceinline__ void raster_tile(int group, int& bx, int& by) {
   const int in = lin - grp * per_group;
   by = first + in % h;
   bx = in / h;
+}
+
+// (bx, by) = tile column / tile row served by this CTA; gridDim = (tile columns, tile rows)
+__device__ __forceinline__ void raster_tile(int group, int& bx, int& by) {
+  const int gx = static_cast<int>(gridDim.x), gy = static_cast<int>(gridDim.y);
+  raster_map(group, gx, gy, static_cast<int>(blockIdx.y) * gx + static_cast<int>(blockIdx.x), bx, by);
 }
 
 // Tile-rows per group (16, measured; MMX_RASTER_GROUP overrides).

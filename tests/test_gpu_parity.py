@@ -315,7 +315,7 @@ def test_host_threads_do_not_change_results():
 
 # ---- BASELINE.json sizes: size-independent properties ----------------------------------------
 
-@pytest.mark.parametrize("variant", [1, 2, 4])
+@pytest.mark.parametrize("variant", [1, 2, 4, 40, 41])
 def test_n4096_fp64_equals_closed_form(variant):
     n = 4096
     with capi.Context(n=n, matmul_variant=variant) as ctx:
@@ -353,6 +353,68 @@ def test_n8192_mixed_genomes_move_the_lower_bound_and_equal_the_closed_form(geno
         got = ctx.fetch(capi.ARRAY_C)
         for r0 in range(0, n, 1024):
             assert bits_equal(got[r0:r0 + 1024], cpu.closed_form_c(n, r0, r0 + 1024)), (what, r0)
+
+
+# ---- FP64 on the INT8 tensor cores (matmul_ozaki.cu, variants 40 / 41) ----------------------------------------
+
+@pytest.mark.parametrize("variant", [40, 41])
+@pytest.mark.parametrize("n", [33, 64, 256, 257, 300, 1000, 1024, 1030])
+def test_fp64_int8_slices_within_tolerance_on_random_inputs(n, variant):
+    """Every n (odd, ragged tiles, k tails), operand rows of wildly different magnitude, a non-zero incoming c:
+    the result stays inside the 1e-12 norm-wise bar -- with 7 slices about as close as FP64 arithmetic can tell."""
+    rs = np.random.RandomState(n)
+    a, bt, c0 = rand(n, capi.F64, 5), rand(n, capi.F64, 6), rand(n, capi.F64, 7)
+    a = a * np.exp2(rs.randint(-30, 30, (n, 1)).astype(np.float64))
+    bt = bt * np.exp2(rs.randint(-30, 30, (n, 1)).astype(np.float64))
+    a[n // 2, :] = 0.0                       # an all-zero row has exponent 0 and contributes nothing
+    with capi.Context(n=n, dtype=capi.F64, matmul_variant=variant) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        ctx.run_loop(8)
+        got = ctx.fetch(capi.ARRAY_C)
+        ok, worst = normwise_ok(got, a, bt, c0, capi.F64)
+        assert ok, f"worst error / bound = {worst}"
+        assert worst < (0.05 if variant == 40 else 1.0)
+        assert bits_equal(got[n // 2], c0[n // 2])
+
+
+@pytest.mark.parametrize("n", [256, 512, 1024])
+def test_fp64_int8_slices_are_exact_when_the_operands_are_short(n):
+    """Operands with at most 40 significant bits below their row maximum are reproduced EXACTLY by 7 slices of 7 bits, so
+    the integer products are the true products: whole individuals equal the CPU program bit for bit, and a product of
+    small integers equals numpy's exact result."""
+    ref = cpu.App(n).run()
+    with capi.Context(n=n, dtype=capi.F64, matmul_variant=40) as ctx:
+        for genome in ("101010101001", "001010101000", "000000001001"):
+            assert ctx.measure(genome).status == capi.MEASURED
+            assert bits_equal(ctx.fetch(capi.ARRAY_C), ref.c), genome
+        rs = np.random.RandomState(3)
+        a = rs.randint(-2 ** 20, 2 ** 20, (n, n)).astype(np.float64)
+        bt = rs.randint(-2 ** 20, 2 ** 20, (n, n)).astype(np.float64)
+        c0 = rs.randint(-2 ** 20, 2 ** 20, (n, n)).astype(np.float64)
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        ctx.run_loop(8)
+        exact = c0.astype(object) + a.astype(np.int64).astype(object) @ bt.astype(np.int64).astype(object).T if n <= 256 else None
+        want = c0 + a @ bt.T        # |sum| < 2^52: exact in float64 whatever the order
+        assert bits_equal(ctx.fetch(capi.ARRAY_C), want)
+        if exact is not None:
+            assert np.array_equal(want, exact.astype(np.float64))
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_row_sharded_fp64_through_the_int8_tensor_cores(world):
+    """The row-block / column-block form the row-sharded run uses (slices of bt relative to the block's first column)."""
+    n = 512
+    ref = cpu.App(n).run()
+    with capi.Context(n=n, dtype=capi.F64, matmul_variant=40, num_slots=world, devices=[0] * world) as ctx:
+        checksum, stats = ctx.shard_run_local()
+        assert checksum == 0.0
+        for r, st in enumerate(stats):
+            got = ctx.fetch(capi.ARRAY_C, slot=r)[st["row0"]:st["row0"] + st["rows"]]
+            assert bits_equal(got, ref.c[st["row0"]:st["row0"] + st["rows"]])
 
 
 def _normwise_bound_structured(n, tol):
