@@ -77,7 +77,7 @@ template <int S, int C, int BK>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_a_part,
                     const __grid_constant__ CUtensorMap map_b, const int* __restrict__ exp_a, const int* __restrict__ exp_b, int n, int kq, int row0, int rows, int col0, int cols,
-                    int group) {
+                    int group, int debug_noload) {
   using Sh = OzShape<S, BK>;
   constexpr int OZ_STAGES = Sh::STAGES, OZ_BK = BK;
   extern __shared__ unsigned char smem_raw[];
@@ -125,6 +125,10 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
         const int s = kb % OZ_STAGES;
         mbar_wait(empty_bar(s), ((kb / OZ_STAGES) & 1) ^ 1);
         const unsigned st = base + s * Sh::STAGE_BYTES;
+        if (debug_noload) {  // rate probe: the MMAs run on whatever the stage buffers hold
+          mbar_arrive(full_bar(s));
+          continue;
+        }
         mbar_expect_tx(full_bar(s), Sh::STAGE_BYTES);
         if constexpr (C == 1) {
           tma_load_3d(st, &map_a, kb * OZ_BK, m_base, 0, full_bar(s));
@@ -324,6 +328,7 @@ cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, i
       !make_slice_map(&map_a_part, sa, static_cast<size_t>(n), kq, BK, OZ_BM / C, S, 1) || !make_slice_map(&map_b, sb, b_rows, kq, BK, OZ_BN, S, S))
     return cudaErrorNotSupported;
   const int col_tiles = (cols + OZ_BN - 1) / OZ_BN;
+  static const int noload = [] { const char* e = getenv("MMX_OZ_NOLOAD"); return (e && C == 1) ? atoi(e) : 0; }();
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((col_tiles + C - 1) / C * C, (rows + OZ_BM - 1) / OZ_BM);  // whole clusters; surplus tiles are masked
   cfg.blockDim = dim3(OZ_THREADS);
@@ -337,7 +342,7 @@ cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, i
   cfg.attrs = attr;
   cfg.numAttrs = C > 1 ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, matmul_ozaki_kernel<S, C, BK>, c, map_a, map_a_part, map_b, static_cast<const int*>(ea), static_cast<const int*>(eb), n,
-                            kq, row0, rows, col0, cols, raster_group(OZ_BM, static_cast<size_t>(kq)));
+                            kq, row0, rows, col0, cols, raster_group(OZ_BM, static_cast<size_t>(kq)), noload);
 }
 
 }  // namespace
