@@ -45,7 +45,7 @@ template <int S, int BK> struct OzShape {
   static constexpr int A_BYTES = S * A_SLICE, B_BYTES = S * B_SLICE;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int STAGES = (227 * 1024 - 2048) / STAGE_BYTES;
-  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 256;
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 + 512;  // alignment slack; barriers + column exponents
 };
 
 // K-major operand tile whose rows are one swizzle span (BK = 64 or 32 bytes) wide; 8-row groups 8 * BK bytes apart
@@ -69,6 +69,13 @@ __device__ __forceinline__ void tc_mma_i8(unsigned d_tmem, unsigned long long ad
 }
 
 __device__ __forceinline__ double pow2(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
+
+constexpr int kNonFinite = 0x7fffffff;  // row exponent of a row that holds an Inf or a NaN: its products are NaN
+// acc * 2^(ea + eb - 12): exact scaling (ldexp also covers results that leave the normal range)
+__device__ __forceinline__ double scaled(double acc, int ea, int eb) {
+  if (ea == kNonFinite || eb == kNonFinite) return __longlong_as_double(0x7ff8000000000000ll);
+  return ldexp(acc, ea + eb - 12);
+}
 
 // C = CTAs per cluster: C consecutive column tiles of one tile-row share their a slices -- every CTA fetches 1/C of the rows
 // of each slice and multicasts them (the kernel is bound by L2 -> SM traffic otherwise: 84 KB per 64-k stage against
@@ -172,18 +179,40 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
       tc_commit(done_bar);
     }
   } else {
-    // epilogue: thread = one row of the tile (TMEM lane), 8 columns at a time
+    // epilogue: thread = one row of the tile (TMEM lane).  Its 64 incoming c values and the tile's column exponents do not
+    // depend on the MMAs: they are fetched NOW and sit in registers / shared memory while the K loop runs, so that after
+    // the last MMA only TMEM reads, the Horner sums and the stores remain (the dependent load-add-store chain per 8 columns
+    // cost ~25 us per tile, a quarter of the tile time at N = 4096)
     const int q = warp % 4;
-    mbar_wait(done_bar, 0);
-    tc_fence_after();
     const int m = m_base + q * 32 + lane;
     const int m_limit = row0 + rows;
     const bool row_ok = m < m_limit;
-    const double scale_i = row_ok ? pow2(exp_a[m] - 12) : 0.0;
+    const int ei = row_ok ? exp_a[m] : 0;  // kNonFinite marks a row that holds an Inf or a NaN
     double* crow = c + static_cast<size_t>(row_ok ? m : 0) * n;
-    const unsigned t0 = tmem_base + (static_cast<unsigned>(q * 32) << 16);
     const bool vec_ok = (n % 2 == 0) && (col0 % 2 == 0);
-#pragma unroll 1
+    int* eb_sh = reinterpret_cast<int*>(smem_raw + (bars + 128 - raw));  // 64 column exponents of this tile
+    {
+      const int t = threadIdx.x - 64;  // 0..127 over the four epilogue warps
+      if (t < OZ_BN) eb_sh[t] = n_rel + t < cols ? exp_b[n_rel + t] : 0;
+    }
+    double cpre[OZ_BN];
+#pragma unroll
+    for (int e = 0; e < OZ_BN; e += 2) {
+      const int jr = n_rel + e;
+      if (row_ok && vec_ok && jr + 2 <= cols) {
+        const double2 x = *reinterpret_cast<const double2*>(crow + col0 + jr);
+        cpre[e] = x.x;
+        cpre[e + 1] = x.y;
+      } else {
+        cpre[e] = (row_ok && jr < cols) ? crow[col0 + jr] : 0.0;
+        cpre[e + 1] = (row_ok && jr + 1 < cols) ? crow[col0 + jr + 1] : 0.0;
+      }
+    }
+    asm volatile("bar.sync 1, 128;\n" ::: "memory");  // eb_sh is complete (the four epilogue warps only)
+    mbar_wait(done_bar, 0);
+    tc_fence_after();
+    const unsigned t0 = tmem_base + (static_cast<unsigned>(q * 32) << 16);
+#pragma unroll
     for (int cb = 0; cb < OZ_BN / 8; ++cb) {
       unsigned lv[S][8];
 #pragma unroll
@@ -198,19 +227,16 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
           double acc = static_cast<double>(static_cast<int>(lv[S - 1][e + h]));
 #pragma unroll
           for (int g = S - 2; g >= 0; --g) acc = fma(acc, 0.0078125, static_cast<double>(static_cast<int>(lv[g][e + h])));
-          v[h] = acc;
+          v[h] = cpre[cb * 8 + e + h] + scaled(acc, ei, eb_sh[cb * 8 + e + h]);
         }
         if (!row_ok) continue;
         const int j = col0 + jr;
         if (vec_ok && jr + 2 <= cols) {
-          double2 x = *reinterpret_cast<const double2*>(crow + j);
-          x.x += v[0] * scale_i * pow2(exp_b[jr]);
-          x.y += v[1] * scale_i * pow2(exp_b[jr + 1]);
-          *reinterpret_cast<double2*>(crow + j) = x;
+          *reinterpret_cast<double2*>(crow + j) = make_double2(v[0], v[1]);
         } else {
 #pragma unroll
           for (int h = 0; h < 2; ++h)
-            if (jr + h < cols) crow[j + h] += v[h] * scale_i * pow2(exp_b[jr + h]);
+            if (jr + h < cols) crow[j + h] = v[h];
         }
       }
     }
@@ -238,8 +264,14 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
   const bool live = r < nrows;
   const double* x = src + static_cast<size_t>(src_row0 + (live ? r : 0)) * n;
   double mx = 0.0;
+  int bad = 0;
   if (live)
-    for (int k = tid; k < n; k += 256) mx = fmax(mx, fabs(x[k]));
+    for (int k = tid; k < n; k += 256) {
+      const double v = x[k];
+      bad |= !isfinite(v);
+      mx = fmax(mx, fabs(v));
+    }
+  bad = __syncthreads_or(bad);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
   if (tid % 32 == 0) red[tid / 32] = mx;
@@ -248,12 +280,12 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
     double m = red[0];
 #pragma unroll
     for (int w = 1; w < 8; ++w) m = fmax(m, red[w]);
-    const int e = m > 0.0 ? ilogb(m) + 1 : 0;
+    const int e = (m > 0.0 && !bad) ? ilogb(m) + 1 : 0;
     e_sh = e;
-    exps[dst_row0 + r] = e;
+    exps[dst_row0 + r] = bad ? kNonFinite : e;
   }
   __syncthreads();
-  const double inv = live ? scalbn(1.0, -e_sh) : 0.0;  // exact power of two (rows of normal doubles)
+  const double inv = (live && !bad) ? scalbn(1.0, -e_sh) : 0.0;  // exact power of two; a non-finite row gets zero digits
   signed char* drow = dst + static_cast<size_t>(dst_row0 + r) * kq;
   // 4 consecutive k per thread and iteration: a warp reads 1 KB and writes 128 bytes per slice, both contiguous
   for (int k0 = tid * 4; k0 < kq; k0 += 256 * 4) {
@@ -268,7 +300,7 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
     int dig[S] = {};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      double rem = v[q] * inv;
+      double rem = bad ? 0.0 : v[q] * inv;
 #pragma unroll
       for (int t = 0; t < S; ++t) {
         const double up = pow2(7 * (t + 1) - 1), down = pow2(-(7 * (t + 1) - 1));
@@ -347,7 +379,8 @@ cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, i
 
 }  // namespace
 
-bool matmul_ozaki_usable(int n) { return n >= 1 && encode_tiled() != nullptr; }
+// |L_g| <= 7 * K * 2^12 must stay below 2^31
+bool matmul_ozaki_usable(int n) { return n >= 1 && n <= 65536 && encode_tiled() != nullptr; }
 
 cudaError_t matmul_ozaki_prepare() {
   if (encode_tiled() == nullptr) return cudaErrorNotSupported;

@@ -404,6 +404,39 @@ def test_fp64_int8_slices_are_exact_when_the_operands_are_short(n):
             assert np.array_equal(want, exact.astype(np.float64))
 
 
+def test_fp64_int8_slices_extreme_exponents_and_non_finite_rows():
+    """Rows near the ends of the exponent range scale exactly (ldexp), and a row holding an Inf or a NaN poisons exactly the
+    outputs that depend on it."""
+    n = 128
+    rs = np.random.RandomState(9)
+    a, bt, c0 = rs.uniform(-1, 1, (n, n)), rs.uniform(-1, 1, (n, n)), np.zeros((n, n))
+    a[3] *= 2.0 ** 500
+    bt[5] *= 2.0 ** 400        # c[3][5] ~ 2^900: finite
+    a[7] *= 2.0 ** -600
+    bt[9] *= 2.0 ** -450       # c[7][9] ~ 2^-1050: a denormal
+    a[11, 17] = np.inf
+    bt[13, 19] = np.nan
+    with capi.Context(n=n, dtype=capi.F64, matmul_variant=40) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        ctx.run_loop(8)
+        got = ctx.fetch(capi.ARRAY_C)
+    with np.errstate(all="ignore"):
+        want = a @ bt.T
+    finite = np.ones((n, n), bool)
+    finite[11, :] = False
+    finite[:, 13] = False
+    assert np.isnan(got[11]).all() and np.isnan(got[:, 13]).all()
+    assert np.isfinite(got[finite]).all()
+    with np.errstate(all="ignore"):
+        bound = 1e-12 * (np.abs(np.nan_to_num(a, nan=0.0, posinf=0.0)) @ np.abs(np.nan_to_num(bt, nan=0.0, posinf=0.0)).T)
+    err = np.abs(got - want)
+    normal = finite & (np.abs(want) > 2.0 ** -1000)               # away from the denormal range: the usual bar
+    assert (err[normal] <= bound[normal]).all()
+    assert abs(got[7, 9] - want[7, 9]) <= 2.0 ** -1070            # a few ulps of the denormal grid
+
+
 @pytest.mark.parametrize("world", [2, 3])
 def test_row_sharded_fp64_through_the_int8_tensor_cores(world):
     """The row-block / column-block form the row-sharded run uses (slices of bt relative to the block's first column)."""
