@@ -128,8 +128,7 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
     case 6: return launch_transpose<T>(bt, b, n, row0, rows, s.stream);
     case 7: return launch_transpose_row<T>(bt, b, n, iter, s.stream);
     case 8: {
-      int variant = ctx->cfg.matmul_variant;
-      if (variant == 0 && sizeof(T) == 8) variant = 4;  // FP64 auto: DMMA, tile by size (best of the tuning points, profiles/)
+      const int variant = ctx->cfg.matmul_variant;  // 0 = auto (matmul.cu)
       return launch_matmul<T>(c, a, bt, n, row0, rows, 0, n, strict, variant, s.d_scratch, s.stream);
     }
     case 9: return launch_gemv_row<T>(c, a, bt, n, iter, strict, s.stream);
@@ -633,7 +632,7 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
       if ((e = cudaMalloc(&sl.d_scratch, matmul_3xtf32_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
     }
     if (cfg->dtype == MMX_F64 && cfg->numerics == MMX_NUMERICS_FAST && matmul_ozaki_usable(cfg->n) &&
-        (cfg->matmul_variant == 40 || cfg->matmul_variant == 41)) {
+        (cfg->matmul_variant == 40 || cfg->matmul_variant == 41 || (cfg->matmul_variant == 0 && cfg->n >= kOzMinN))) {
       if ((e = matmul_ozaki_prepare()) != cudaSuccess) return fail(e, "matmul_ozaki_prepare");
       if ((e = cudaMalloc(&sl.d_scratch, matmul_ozaki_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
     }
@@ -916,8 +915,7 @@ template <typename T>
 int shard_phase2(mmx_ctx* ctx, Slot& s) {
   const int n = ctx->cfg.n;
   const bool strict = ctx->cfg.numerics == MMX_NUMERICS_STRICT;
-  int variant = ctx->cfg.matmul_variant;
-  if (variant == 0 && sizeof(T) == 8) variant = 4;
+  const int variant = ctx->cfg.matmul_variant;
   int r0 = 0, rows = 0;
   shard_block(n, s.shard_world, s.shard_rank, &r0, &rows);
   T* a = static_cast<T*>(s.d_arr[MMX_ARRAY_A]);

@@ -75,8 +75,18 @@ cudaError_t launch_matmul_3xtf32(float* c, const float* a, const float* bt, void
 bool matmul_ozaki_usable(int n);
 size_t matmul_ozaki_scratch_bytes(int n);
 cudaError_t matmul_ozaki_prepare();  // per device, before the first launch (not inside a stream capture)
+// guard_out (may be NULL): the slice pass also records in a device flag whether any operand element lost bits (or is not
+// finite); the contraction then runs only if none did, and *guard_out receives the flag's address so that the caller can
+// enqueue the FP64-pipe kernel under the opposite condition (FP64 auto mode: tensor cores exactly when they are error-free)
+constexpr int kOzMinN = 1024;
+// The guard: g[0] != 0 when some element has bits below its last digit (or is not finite); g[1], g[2] = highest non-zero digit
+// (1-based) anywhere in a / in bt.  The 7-slice contraction keeps the digit pairs with t + u <= 8, so it is error-free
+// exactly when no element is cut AND every non-zero pair is kept.
+#ifdef __CUDACC__
+__device__ __forceinline__ bool ozaki_guard_lossy(const int* g) { return g[0] != 0 || g[1] + g[2] > 8; }
+#endif
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0,
-                                int cols, int slices, cudaStream_t stream);
+                                int cols, int slices, cudaStream_t stream, int** guard_out = nullptr);
 // gene 9: row i of the same (GEMV against bt)
 template <typename T>
 cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, bool strict, cudaStream_t stream);

@@ -223,7 +223,9 @@ __device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double
 template <int DK, int DSTAGES, int WM, int WN, int MT, int NT>
 __global__ void __launch_bounds__(32 * WM * WN, (WM * WN <= 4 && MT * NT <= 16) ? 3 : 1)
 matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const double* __restrict__ bt, int n,
-                   int row0, int rows, int col0, int cols, int group) {
+                   int row0, int rows, int col0, int cols, int group, const int* __restrict__ run_if) {
+  // guarded launch (FP64 auto mode): the tensor-core kernel took this contraction
+  if (run_if != nullptr && !ozaki_guard_lossy(run_if)) return;
   constexpr int THREADS = 32 * WM * WN;
   constexpr int TM = WM * MT * 8, TN = WN * NT * 8;
   constexpr int DLD = DK + 4;  // padded row: (DK+4)*8 B = 32 mod 128 for DK in {16, 32} => conflict-free fragments
@@ -479,7 +481,8 @@ cudaError_t simt_go(T* c, const T* a, const T* bt, int n, int row0, int rows, in
 }
 
 template <int DK, int DSTAGES, int WM, int WN, int MT, int NT>
-cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row0, int rows, int col0, int cols, cudaStream_t stream) {
+cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row0, int rows, int col0, int cols, cudaStream_t stream,
+                    const int* run_if = nullptr) {
   constexpr int TM = WM * MT * 8, TN = WN * NT * 8;
   const size_t smem = static_cast<size_t>(DSTAGES) * (TM + TN) * (DK + 4) * sizeof(double);
   static PerDeviceOnce once;  // function attributes are per device
@@ -492,7 +495,7 @@ cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row
   }
   dim3 grid((cols + TN - 1) / TN, (rows + TM - 1) / TM);
   matmul_dmma_kernel<DK, DSTAGES, WM, WN, MT, NT><<<grid, 32 * WM * WN, smem, stream>>>(c, a, bt, n, row0, rows, col0, cols,
-                                                                                         raster_group(TM, static_cast<size_t>(n) * sizeof(double)));
+                                                                                         raster_group(TM, static_cast<size_t>(n) * sizeof(double)), run_if);
   return cudaGetLastError();
 }
 
@@ -511,12 +514,22 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
   // tensor cores (INT8 slice products, matmul_ozaki.cu): on request
   if (!strict && scratch != nullptr && (variant == 40 || variant == 41))
     return launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, variant == 41 ? 6 : 7, stream);
+  const bool dmma_ok = n % 2 == 0 && col0 % 2 == 0 && cols % 2 == 0;  // 16-byte aligned double2 accesses of c
+  // auto: the INT8 tensor cores whenever their 7 x 7-bit slices reproduce every operand element exactly (then the result is the
+  // error-free product rounded once -- bit-identical to the CPU program on the application's inputs), the FP64 pipe otherwise.
+  // Both kernels are enqueued; a device flag written by the slice pass lets exactly one of them run.
+  if (!strict && variant == 0 && scratch != nullptr && n >= kOzMinN && dmma_ok) {
+    int* lossy = nullptr;
+    if (cudaError_t e = launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 7, stream, &lossy); e != cudaSuccess) return e;
+    return dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, stream, lossy);
+  }
+  if (variant == 0) variant = 4;  // the FP64 pipe: DMMA, tile by size (best of the tuning points, profiles/)
   if (strict) {
     if (n % 2 == 0 && variant == 20) return simt2_go<double, true, 128, 128, 4>(c, a, bt, n, row0, rows, col0, cols, stream);
     if (n % 2 == 0 && variant != 1) return simt2_go<double, true, 64, 64, 3>(c, a, bt, n, row0, rows, col0, cols, stream);
     return simt_go<double, true>(c, a, bt, n, row0, rows, col0, cols, stream);
   }
-  if (n % 2 == 0 && col0 % 2 == 0 && cols % 2 == 0) {  // 16-byte aligned double2 accesses of c
+  if (dmma_ok) {
     switch (variant) {
       case 2: return dmma_go<16, 3, 2, 4, 8, 4>(c, a, bt, n, row0, rows, col0, cols, stream);   // 128x128, BK=16 (first tuning point)
       case 5: return dmma_go<32, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, stream);   // 64x64

@@ -84,8 +84,10 @@ template <int S, int C, int BK>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_a_part,
                     const __grid_constant__ CUtensorMap map_b, const int* __restrict__ exp_a, const int* __restrict__ exp_b, int n, int kq, int row0, int rows, int col0, int cols,
-                    int group, int debug_noload) {
+                    int group, int debug_noload, const int* __restrict__ skip_if) {
   using Sh = OzShape<S, BK>;
+  // guarded launch (FP64 auto mode): the slices lost bits of some operand, the FP64-pipe kernel runs instead
+  if (skip_if != nullptr && ozaki_guard_lossy(skip_if)) return;
   constexpr int OZ_STAGES = Sh::STAGES, OZ_BK = BK;
   extern __shared__ unsigned char smem_raw[];
   const unsigned raw = smem_u32(smem_raw);
@@ -256,8 +258,10 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
 // written as zeros with exponent 0 (tile overhang inside the tensor map).
 template <int S>
 __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restrict__ src, signed char* __restrict__ dst, int* __restrict__ exps,
-                                                          size_t plane, int n, int kq, int src_row0, int nrows, int dst_row0) {
+                                                          size_t plane, int n, int kq, int src_row0, int nrows, int dst_row0,
+                                                          int* __restrict__ guard, int guard_slot) {
   __shared__ double red[8];
+  __shared__ int top_sh[8];
   __shared__ int e_sh;
   const int r = blockIdx.x;  // relative row
   const int tid = threadIdx.x;
@@ -287,6 +291,7 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
   __syncthreads();
   const double inv = (live && !bad) ? scalbn(1.0, -e_sh) : 0.0;  // exact power of two; a non-finite row gets zero digits
   signed char* drow = dst + static_cast<size_t>(dst_row0 + r) * kq;
+  int lossy = bad, top = 0;  // top = highest non-zero digit (1-based) this thread has seen
   // 4 consecutive k per thread and iteration: a warp reads 1 KB and writes 128 bytes per slice, both contiguous
   for (int k0 = tid * 4; k0 < kq; k0 += 256 * 4) {
     double v[4];
@@ -307,10 +312,24 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
         const int d = __double2int_rn(rem * up);
         rem = fma(-static_cast<double>(d), down, rem);  // exact: removes a prefix of rem's bits
         dig[t] |= (d & 0xff) << (8 * q);
+        if (d != 0) top = max(top, t + 1);
       }
+      lossy |= rem != 0.0;  // bits below the last digit: the slices do not reproduce this element exactly
     }
 #pragma unroll
     for (int t = 0; t < S; ++t) *reinterpret_cast<int*>(drow + t * plane + k0) = dig[t];
+  }
+  if (guard != nullptr) {
+    lossy = __syncthreads_or(lossy);
+    top = __reduce_max_sync(0xffffffffu, top);
+    if (tid % 32 == 0) top_sh[tid / 32] = top;
+    __syncthreads();
+    if (tid == 0) {
+#pragma unroll
+      for (int w = 1; w < 8; ++w) top = max(top, top_sh[w]);
+      if (lossy && guard[0] == 0) atomicOr(guard, 1);
+      if (top > guard[guard_slot]) atomicMax(guard + guard_slot, top);  // read first: after a few rows nobody needs the atomic
+    }
   }
 }
 
@@ -341,9 +360,11 @@ cudaError_t oz_configure() {
   return cudaSuccess;
 }
 
+// guard_out != nullptr: also record whether the slices are lossy in a device flag (returned through *guard_out) and let the
+// kernel run only when they are not
 template <int S, int C, int BK>
 cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                  cudaStream_t stream) {
+                  cudaStream_t stream, int** guard_out = nullptr) {
   if (cudaError_t e = oz_configure<S, C, BK>(); e != cudaSuccess) return e;
   const int kq = oz_kq(n);
   // scratch: a slices [S][n][kq] (absolute rows), bt slices [S][pad64(n)][kq] (rows relative to col0), exponents
@@ -353,8 +374,14 @@ cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, i
   int* ea = reinterpret_cast<int*>(sb + S * b_plane);
   int* eb = ea + n;
   const int cols_pad = static_cast<int>(oz_rows_pad(cols, OZ_BN));
-  ozaki_slice_kernel<S><<<rows, 256, 0, stream>>>(a, sa, ea, a_plane, n, kq, row0, rows, row0);
-  ozaki_slice_kernel<S><<<cols_pad, 256, 0, stream>>>(bt, sb, eb, b_plane, n, kq, col0, cols, 0);
+  int* flag = nullptr;
+  if (guard_out != nullptr) {
+    flag = eb + n + OZ_BN;  // {lossy, top digit of a, top digit of bt}
+    *guard_out = flag;
+    if (cudaError_t e = cudaMemsetAsync(flag, 0, 3 * sizeof(int), stream); e != cudaSuccess) return e;
+  }
+  ozaki_slice_kernel<S><<<rows, 256, 0, stream>>>(a, sa, ea, a_plane, n, kq, row0, rows, row0, flag, 1);
+  ozaki_slice_kernel<S><<<cols_pad, 256, 0, stream>>>(bt, sb, eb, b_plane, n, kq, col0, cols, 0, flag, 2);
   CUtensorMap map_a, map_a_part, map_b;
   if (!make_slice_map(&map_a, sa, static_cast<size_t>(n), kq, BK, OZ_BM, S, S) ||
       !make_slice_map(&map_a_part, sa, static_cast<size_t>(n), kq, BK, OZ_BM / C, S, 1) || !make_slice_map(&map_b, sb, b_rows, kq, BK, OZ_BN, S, S))
@@ -374,7 +401,7 @@ cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, i
   cfg.attrs = attr;
   cfg.numAttrs = C > 1 ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, matmul_ozaki_kernel<S, C, BK>, c, map_a, map_a_part, map_b, static_cast<const int*>(ea), static_cast<const int*>(eb), n,
-                            kq, row0, rows, col0, cols, raster_group(OZ_BM, static_cast<size_t>(kq)), noload);
+                            kq, row0, rows, col0, cols, raster_group(OZ_BM, static_cast<size_t>(kq)), noload, static_cast<const int*>(flag));
 }
 
 }  // namespace
@@ -393,13 +420,14 @@ cudaError_t matmul_ozaki_prepare() {
 
 size_t matmul_ozaki_scratch_bytes(int n) {
   const size_t kq = static_cast<size_t>(oz_kq(n));
-  return 7 * (static_cast<size_t>(n) + oz_rows_pad(n, OZ_BN)) * kq + 2 * (static_cast<size_t>(n) + OZ_BN) * sizeof(int) + 256;
+  return 7 * (static_cast<size_t>(n) + oz_rows_pad(n, OZ_BN)) * kq + 2 * (static_cast<size_t>(n) + OZ_BN) * sizeof(int) + 256;  // + the guard flag
 }
 
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                int slices, cudaStream_t stream) {
+                                int slices, cudaStream_t stream, int** guard_out) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr) return cudaErrorInvalidValue;
+  if (guard_out != nullptr) return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream, guard_out);
   // tuning hooks (tools/ozaki_cluster_sweep.sh): CTAs per cluster sharing the a slices by multicast, k bytes per stage
   static const int cluster = [] { const char* e = getenv("MMX_OZ_CLUSTER"); return e ? atoi(e) : 1; }();
   static const int bk = [] { const char* e = getenv("MMX_OZ_BK"); return e ? atoi(e) : 64; }();

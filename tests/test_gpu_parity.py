@@ -404,6 +404,45 @@ def test_fp64_int8_slices_are_exact_when_the_operands_are_short(n):
             assert np.array_equal(want, exact.astype(np.float64))
 
 
+def test_fp64_auto_uses_the_tensor_cores_exactly_when_they_are_error_free():
+    """matmul_variant 0 from N = 1024: the slice pass records whether any operand element is cut and how many digits the
+    operands use; the INT8 kernel runs iff the product is then error-free, the DMMA kernel otherwise."""
+    n = 1024
+    rs = np.random.RandomState(11)
+
+    def run(variant, a, bt, c0):
+        with capi.Context(n=n, dtype=capi.F64, matmul_variant=variant) as ctx:
+            ctx.upload(capi.ARRAY_A, a)
+            ctx.upload(capi.ARRAY_BT, bt)
+            ctx.upload(capi.ARRAY_C, c0)
+            ctx.run_loop(8)
+            return ctx.fetch(capi.ARRAY_C)
+
+    # full-mantissa operands: every element is cut -> the FP64 pipe, bit for bit the DMMA result
+    a, bt, c0 = rand(n, capi.F64, 5), rand(n, capi.F64, 6), rand(n, capi.F64, 7)
+    assert bits_equal(run(0, a, bt, c0), run(4, a, bt, c0))
+    # 21-bit integers: 3 digits each, all pairs kept -> tensor cores, and the result is the exact product
+    a, bt, c0 = (rs.randint(-2 ** 20, 2 ** 20, (n, n)).astype(np.float64) for _ in range(3))
+    assert bits_equal(run(0, a, bt, c0), c0 + a @ bt.T)
+    # 33-bit integers: nothing is cut, but digit pairs beyond t + u = 8 would be dropped -> the FP64 pipe again
+    a, bt = (rs.randint(-2 ** 32, 2 ** 32, (n, n)).astype(np.float64) for _ in range(2))
+    assert bits_equal(run(0, a, bt, c0), run(4, a, bt, c0))
+
+
+def test_fp64_auto_on_the_application_is_bit_exact_and_fast():
+    n = 4096
+    with capi.Context(n=n, dtype=capi.F64, matmul_variant=4) as ctx:
+        assert ctx.measure("101010101001").status == capi.MEASURED
+        ms_pipe = ctx.time_loop(8, 3, True)
+    with capi.Context(n=n, dtype=capi.F64) as ctx:
+        assert ctx.measure("101010101001").status == capi.MEASURED
+        got = ctx.fetch(capi.ARRAY_C)
+        for r0 in range(0, n, 1024):
+            assert bits_equal(got[r0:r0 + 1024], cpu.closed_form_c(n, r0, r0 + 1024))
+        ms_auto = ctx.time_loop(8, 3, True)
+    assert ms_auto < 0.6 * ms_pipe, (ms_auto, ms_pipe)      # slices + INT8 contraction + the skipped DMMA launch
+
+
 def test_fp64_int8_slices_extreme_exponents_and_non_finite_rows():
     """Rows near the ends of the exponent range scale exactly (ldexp), and a row holding an Inf or a NaN poisons exactly the
     outputs that depend on it."""
