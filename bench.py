@@ -12,7 +12,7 @@ EvalBackend::measure would call).  Metric: matrix-app GFLOP/s = 2 N^3 / time (SU
           torch.cuda.synchronize() on both sides: includes planning, launches, the D2H of the checksum.
           The program generates its own inputs (matmul.c:8-18), so for this genome the planner moves
           0 bytes up and 8 bytes down per step; `e2e_mixed` adds a genome with host-produced operands.
-  roofline  dominant kernel (the FP64 contraction, gene 8) timed live with CUDA events
+  roofline  dominant kernel (the FP64 contraction, gene 8: on this workload the INT8 tensor-core form) timed live with CUDA events
   cpu_baseline  the oracle port (oracle/matmul_oracle.c) on this box's host cores, bounded sample
 
 `--impl reference` times the reference's CPU implementation of the same path (the oracle port of
@@ -49,7 +49,7 @@ def parse_args():
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 arm of the configuration")
-    ap.add_argument("--no-fp64-tensor", action="store_true", help="skip the FP64-on-INT8-tensor-cores arm")
+    ap.add_argument("--no-fp64-pipe", action="store_true", help="skip the arm that forces gene 8 onto the FP64 pipe (DMMA)")
     ap.add_argument("--ga", action="store_true", help="also run the GA search (M=12, T=12) with real timings")
     return ap.parse_args()
 
@@ -256,15 +256,28 @@ def run_ours(args):
     if rank == 0:
         peaks, peaks_kind = load_measured_peaks()
         ms8 = ctx.time_loop(8, 5, True)
-        pipe_peak = capi.peak_probe(capi.PEAK_FP64_FMA if dtype == capi.F64 else capi.PEAK_FP32_FMA, local_rank)
         ach = flops / (ms8 * 1e-3) / 1e12
         share = ms8 * 1e-3 / (device_s / args.steps)
-        roof = {"bound": "tensor", "pipe": "fp64 (DMMA.8x8x4 via mma.sync)" if dtype == capi.F64 else "fp32 (FFMA)",
-                "kernel": "matmul_nt (gene 8)", "achieved": ach, "peak": pipe_peak, "unit": "TFLOP/s", "frac": ach / pipe_peak,
-                "traffic": ncu_traffic("matmul_dmma" if dtype == capi.F64 else "matmul_3xtf32s", n), "ms_per_launch": ms8,
-                "share_of_step": share,
-                "peak_source": "FMA-issue peak of the same pipe measured in this run by csrc/peaks.cu "
-                               "(MEASURED_PEAKS.json carries only HBM and bf16 figures)"}
+        if dtype == capi.F64 and n >= 1024:
+            # auto mode: this workload's operands are reproduced exactly by 7 x 7-bit slices, so gene 8 runs on the INT8 tensor
+            # cores (matmul_ozaki.cu); ms8 covers the two slice passes, the contraction and the skipped FP64-pipe launch
+            int8_peak = 2.0 * peaks["bf16_tflops"]
+            ops = 28.0 * flops / (ms8 * 1e-3) / 1e12
+            roof = {"bound": "tensor", "pipe": "int8 (tcgen05.mma.kind::i8, INT32 accumulators in TMEM)",
+                    "kernel": "matmul_ozaki (gene 8: 7 exact 7-bit INT8 slices per operand, 28 slice products per FP64 term; slice passes included)",
+                    "achieved": ops, "peak": int8_peak, "unit": "TOP/s", "frac": ops / int8_peak,
+                    "traffic": ncu_traffic("matmul_ozaki", n), "ms_per_launch": ms8, "share_of_step": share,
+                    "effective_fp64_tflops": ach,
+                    "peak_source": "twice MEASURED_PEAKS.json bf16_tflops (INT8 runs at twice the bf16 rate); achieved counts the 28 INT8 "
+                                   "slice products issued per FP64 term"}
+        else:
+            pipe_peak = capi.peak_probe(capi.PEAK_FP64_FMA if dtype == capi.F64 else capi.PEAK_FP32_FMA, local_rank)
+            roof = {"bound": "tensor", "pipe": "fp64 (DMMA.8x8x4 via mma.sync)" if dtype == capi.F64 else "fp32 (FFMA)",
+                    "kernel": "matmul_nt (gene 8)", "achieved": ach, "peak": pipe_peak, "unit": "TFLOP/s", "frac": ach / pipe_peak,
+                    "traffic": ncu_traffic("matmul_dmma" if dtype == capi.F64 else "matmul_3xtf32s", n), "ms_per_launch": ms8,
+                    "share_of_step": share,
+                    "peak_source": "FMA-issue peak of the same pipe measured in this run by csrc/peaks.cu "
+                                   "(MEASURED_PEAKS.json carries only HBM and bf16 figures)"}
         ms6 = ctx.time_loop(6, 10, True)
         gb = 2.0 * esz * n * n / (ms6 * 1e-3) / 1e9
         hbm_roof = {"bound": "hbm", "kernel": "transpose_tiled (gene 6)", "achieved": gb, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -277,10 +290,10 @@ def run_ours(args):
     if rank == 0 and dtype == capi.F64 and not args.no_fp32:
         fp32 = fp32_arm(n, local_rank, max(10, args.steps // 4), peaks)
 
-    # FP64 with the contraction on the INT8 tensor cores (matmul_variant 40: exact 7-bit slices, matmul_ozaki.cu)
-    fp64_tensor = None
-    if rank == 0 and dtype == capi.F64 and not args.no_fp64_tensor:
-        fp64_tensor = fp64_tensor_arm(n, local_rank, max(10, args.steps // 4), peaks, checksum)
+    # the same configuration with gene 8 forced onto the FP64 pipe (matmul_variant 4: DMMA), for comparison
+    fp64_pipe = None
+    if rank == 0 and dtype == capi.F64 and n >= 1024 and not args.no_fp64_pipe:
+        fp64_pipe = fp64_pipe_arm(n, local_rank, max(10, args.steps // 4), checksum)
 
     # the sampler covers the timed region plus the (equally loaded) mixed-genome and roofline phases
     clocks = sampler.stop()
@@ -301,20 +314,24 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (the program generates its own inputs: a=(i+j)/N, b=(i-j)/N)",
             "config": {"workload": f"matrix app N={n} {args.dtype}, genome {GENOME_ALL_NESTS} (all six loop nests offloaded)",
+                       "gene8": ("auto: INT8 tensor cores (7 exact slices; this workload's operands are reproduced exactly), FP64 pipe otherwise"
+                                 if (dtype == capi.F64 and n >= 1024) else "default kernel for this dtype and size"),
                        "n": n, "genome": GENOME_ALL_NESTS, "individuals_per_step_per_gpu": 1,
                        "l2": "working set 4*N^2*E per step exceeds L2; no flush needed"},
             "e2e": {"value": flops * args.steps * world / wall_s / 1e9, "unit": "GFLOP/s",
                     "h2d_bytes_per_step": int(plan.h2d_bytes), "d2h_bytes_per_step": int(plan.d2h_bytes),
                     "note": "host clock around mmx_measure (plan + 6 launches + checksum D2H + sync); this genome has no host-side inputs"},
             "e2e_mixed": mixed, "e2e_host_buffers": host_io,
-            "gpu_launches": int(plan.kernel_launches) * args.steps,
+            # the plan counts one launch per offloaded nest; in FP64 auto mode gene 8 is four kernels (two slice passes, the
+            # tensor-core contraction, the guarded FP64-pipe launch that exits at once)
+            "gpu_launches": (int(plan.kernel_launches) + (3 if (dtype == capi.F64 and n >= 1024) else 0)) * args.steps,
             "clocks": clocks, "roofline": roof, "roofline_hbm": hbm_roof, "cpu_baseline": base,
             "checksum": checksum,
         }
         if fp32 is not None:
             line["fp32"] = fp32
-        if fp64_tensor is not None:
-            line["fp64_tensor"] = fp64_tensor
+        if fp64_pipe is not None:
+            line["fp64_pipe"] = fp64_pipe
         if ga is not None:
             line["ga_search"] = ga
         print(json.dumps(line), flush=True)
@@ -392,12 +409,12 @@ def fp32_arm(n, device, steps, peaks):
             "vs_ffma_pipe_peak": flops / ms8 / 1e9 / ffma_peak, "ffma_pipe_peak_tflops": ffma_peak}
 
 
-def fp64_tensor_arm(n, device, steps, peaks, reference_checksum):
-    """The same steps with gene 8 on the tcgen05 INT8 tensor cores.  Results are bit-identical to the default path on this
-    workload (checked here on c's corner and the checksum; tests compare all of c), within 1e-12 norm-wise in general."""
+def fp64_pipe_arm(n, device, steps, reference_checksum):
+    """The same steps with gene 8 on the FP64 pipe (DMMA).  Results are bit-identical to the default path on this workload
+    (checked here on c's corners and the checksum; tests compare all of c)."""
     from paper_1806_01430_b200 import capi
     flops = 2.0 * n ** 3
-    with capi.Context(n=n, dtype=capi.F64, matmul_variant=40, devices=[device], timeout_s=600.0) as ctx:
+    with capi.Context(n=n, dtype=capi.F64, matmul_variant=4, devices=[device], timeout_s=600.0) as ctx:
         for _ in range(3):
             ctx.measure(GENOME_ALL_NESTS)
         dev_s = 0.0
@@ -408,19 +425,16 @@ def fp64_tensor_arm(n, device, steps, peaks, reference_checksum):
         checksum = ctx.stats().checksum
         c = ctx.fetch(capi.ARRAY_C)
         ms8 = ctx.time_loop(8, 5, True)
+        pipe_peak = capi.peak_probe(capi.PEAK_FP64_FMA, device)
     s2 = (n - 1) * n * (2 * n - 1) / 6
-    int8_peak = 2.0 * peaks["bf16_tflops"]
-    ops = 28.0 * flops            # 28 slice products per term
+    ach = flops / ms8 / 1e9
     return {"value": flops * steps / dev_s / 1e9, "unit": "GFLOP/s", "steps": steps, "e2e": flops * steps / wall / 1e9,
-            "kernel": "matmul_ozaki (gene 8: 7 exact 7-bit INT8 slices per operand, 28 slice products on tcgen05.mma.kind::i8 with "
-                      "INT32 accumulation in TMEM; slice passes included)",
-            "ms_per_launch": ms8, "effective_fp64_tflops": flops / ms8 / 1e9,
+            "kernel": "matmul_dmma (gene 8: mma.sync.m8n8k4.f64, 64x64 tiles, 3 CTAs per SM)", "ms_per_launch": ms8,
             "bit_identical_to_default_path": bool(checksum == reference_checksum and float(c[0, 0]) == s2 / (n * n)
                                                   and float(c[1, 2]) == (s2 - n * (n - 1) / 2 - 2 * n) / (n * n)),
-            "roofline": {"bound": "tensor", "achieved": ops / ms8 / 1e9, "peak": int8_peak, "unit": "TOP/s", "frac": ops / ms8 / 1e9 / int8_peak,
-                         "traffic": ncu_traffic("matmul_ozaki", n),
-                         "peak_source": "twice MEASURED_PEAKS.json bf16_tflops (INT8 runs at twice the bf16 rate); achieved counts the "
-                                        "28 INT8 slice products issued per FP64 term"}}
+            "roofline": {"bound": "tensor", "pipe": "fp64 (DMMA.8x8x4 via mma.sync)", "achieved": ach, "peak": pipe_peak, "unit": "TFLOP/s",
+                         "frac": ach / pipe_peak, "traffic": ncu_traffic("matmul_dmma", n),
+                         "peak_source": "FMA-issue peak of the FP64 pipe measured in this run by csrc/peaks.cu"}}
 
 
 def run_ga_search(n, dtype, devices, population=12, generations=12, seed=1, timeout_s=0.5):

@@ -267,14 +267,42 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
   const int tid = threadIdx.x;
   const bool live = r < nrows;
   const double* x = src + static_cast<size_t>(src_row0 + (live ? r : 0)) * n;
+  // 4 consecutive k per thread and iteration: a warp reads 1 KB and writes 128 bytes per slice, both contiguous.  The first
+  // KEEP iterations (rows up to 4096 elements) stay in registers between the two passes, so the row is read once.
+  constexpr int KEEP = 4;
+  const bool vec = n % 2 == 0;
+  auto load4 = [&](int k0, double (&v)[4]) {
+    if (live && vec && k0 + 4 <= n) {
+      const double2 p = *reinterpret_cast<const double2*>(x + k0), q2 = *reinterpret_cast<const double2*>(x + k0 + 2);
+      v[0] = p.x; v[1] = p.y; v[2] = q2.x; v[3] = q2.y;
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q] = (live && k0 + q < n) ? x[k0 + q] : 0.0;
+    }
+  };
   double mx = 0.0;
   int bad = 0;
-  if (live)
-    for (int k = tid; k < n; k += 256) {
-      const double v = x[k];
-      bad |= !isfinite(v);
-      mx = fmax(mx, fabs(v));
+  auto scan4 = [&](const double (&v)[4]) {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      bad |= !isfinite(v[q]);
+      mx = fmax(mx, fabs(v[q]));
     }
+  };
+  double keep[KEEP][4];
+#pragma unroll
+  for (int it = 0; it < KEEP; ++it) {
+    const int k0 = (it * 256 + tid) * 4;
+    if (k0 < kq) {
+      load4(k0, keep[it]);
+      scan4(keep[it]);
+    }
+  }
+  for (int k0 = (KEEP * 256 + tid) * 4; k0 < kq; k0 += 256 * 4) {
+    double v[4];
+    load4(k0, v);
+    scan4(v);
+  }
   bad = __syncthreads_or(bad);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
@@ -292,16 +320,7 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
   const double inv = (live && !bad) ? scalbn(1.0, -e_sh) : 0.0;  // exact power of two; a non-finite row gets zero digits
   signed char* drow = dst + static_cast<size_t>(dst_row0 + r) * kq;
   int lossy = bad, top = 0;  // top = highest non-zero digit (1-based) this thread has seen
-  // 4 consecutive k per thread and iteration: a warp reads 1 KB and writes 128 bytes per slice, both contiguous
-  for (int k0 = tid * 4; k0 < kq; k0 += 256 * 4) {
-    double v[4];
-    if (live && k0 + 4 <= n && n % 2 == 0) {
-      const double2 p = *reinterpret_cast<const double2*>(x + k0), q2 = *reinterpret_cast<const double2*>(x + k0 + 2);
-      v[0] = p.x; v[1] = p.y; v[2] = q2.x; v[3] = q2.y;
-    } else {
-#pragma unroll
-      for (int q = 0; q < 4; ++q) v[q] = (live && k0 + q < n) ? x[k0 + q] : 0.0;
-    }
+  auto emit4 = [&](int k0, const double (&v)[4]) {
     int dig[S] = {};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -318,6 +337,16 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
     }
 #pragma unroll
     for (int t = 0; t < S; ++t) *reinterpret_cast<int*>(drow + t * plane + k0) = dig[t];
+  };
+#pragma unroll
+  for (int it = 0; it < KEEP; ++it) {
+    const int k0 = (it * 256 + tid) * 4;
+    if (k0 < kq) emit4(k0, keep[it]);
+  }
+  for (int k0 = (KEEP * 256 + tid) * 4; k0 < kq; k0 += 256 * 4) {
+    double v[4];
+    load4(k0, v);
+    emit4(k0, v);
   }
   if (guard != nullptr) {
     lossy = __syncthreads_or(lossy);
