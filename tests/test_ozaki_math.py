@@ -1,0 +1,91 @@
+"""The arithmetic behind the FP64-on-INT8 contraction (csrc/matmul_ozaki.cu), restated with numpy integers: the digit
+decomposition is exact, level sums stay inside INT32, truncating the levels gives the stated bound, and the guard of the
+auto mode (nothing cut, every non-zero digit pair kept) is exactly the condition for an error-free product.  The GPU kernel
+itself is checked against the CPU program in tests/test_gpu_parity.py; this file pins the scheme it implements."""
+import numpy as np
+import pytest
+
+S = 7
+
+
+def slices(x):
+    """rows of x -> (exponents e, digits d[t] as int64 arrays, remainder r) with x = 2^e (sum_t d_t 2^-(7t-1)) + 2^e r."""
+    mx = np.abs(x).max(axis=1)
+    e = np.where(mx > 0, np.floor(np.log2(np.maximum(mx, 1e-300))).astype(np.int64) + 1, 0)
+    rem = x * np.exp2(-e.astype(np.float64))[:, None]
+    assert (np.abs(rem) < 1).all()
+    digits = []
+    for t in range(1, S + 1):
+        d = np.rint(rem * 2.0 ** (7 * t - 1))
+        rem = rem - d * 2.0 ** -(7 * t - 1)          # exact in float64
+        assert (np.abs(d) <= 64).all()
+        digits.append(d.astype(np.int64))
+    return e, digits, rem
+
+
+def contract(a, bt, c0, keep=S + 1):
+    ea, da, _ = slices(a)
+    eb, db, _ = slices(bt)
+    acc = np.zeros(a.shape[0:1] + bt.shape[0:1])
+    for g in range(keep, 1, -1):                     # Horner from the smallest level, as the epilogue does
+        level = sum(da[t - 1] @ db[g - t - 1].T for t in range(1, S + 1) if 1 <= g - t <= S)
+        assert np.abs(level).max() < 2 ** 31         # INT32 accumulators
+        acc = acc / 128.0 + level
+    return c0 + np.ldexp(acc, (ea[:, None] + eb[None, :] - 12).astype(np.int64))
+
+
+def app_operands(n):
+    i = np.arange(n, dtype=np.float64)
+    return (i[:, None] + i[None, :]) / n, (i[None, :] - i[:, None]) / n      # a, bt = b^T
+
+
+@pytest.mark.parametrize("n", [128, 256])
+def test_application_operands_use_two_digits_and_the_product_is_exact(n):
+    a, bt = app_operands(n)
+    for x in (a, bt):
+        _, d, rem = slices(x)
+        assert (rem == 0).all() and all((dt == 0).all() for dt in d[2:])     # 14 bits: digits 1 and 2 only
+    i = np.arange(n, dtype=np.float64)
+    s1, s2 = n * (n - 1) / 2, (n - 1) * n * (2 * n - 1) / 6
+    closed = (s2 + (i[:, None] - i[None, :]) * s1 - n * i[:, None] * i[None, :]) / n ** 2
+    assert np.array_equal(contract(a, bt, np.zeros((n, n))), closed)
+
+
+def test_random_operands_meet_the_stated_bound():
+    rs = np.random.RandomState(0)
+    n = 192
+    a = rs.uniform(-1, 1, (n, n)) * np.exp2(rs.randint(-30, 30, (n, 1)))
+    bt = rs.uniform(-1, 1, (n, n)) * np.exp2(rs.randint(-30, 30, (n, 1)))
+    c0 = rs.uniform(-1, 1, (n, n))
+    got = contract(a, bt, c0)
+    exact = (c0.astype(np.longdouble) + a.astype(np.longdouble) @ bt.astype(np.longdouble).T)
+    err = np.abs(got.astype(np.longdouble) - exact).astype(np.float64)
+    stated = (S + 3) * n * 2.0 ** (-7 * S) * np.abs(a).max(axis=1)[:, None] * np.abs(bt).max(axis=1)[None, :]
+    ulp = 2.0 ** -52 * np.abs(exact).astype(np.float64)                      # the final rounding of c itself
+    assert (err <= stated + ulp).all()
+    bar = 1e-12 * (np.abs(c0) + np.abs(a) @ np.abs(bt).T)
+    assert (err <= 0.05 * bar).all()                                         # far inside the norm-wise tolerance
+
+
+def test_guard_condition_is_the_error_free_condition():
+    rs = np.random.RandomState(1)
+    n = 96
+    c0 = np.zeros((n, n))
+
+    def top(x):
+        _, d, rem = slices(x)
+        return (rem != 0).any(), max((t + 1 for t in range(S) if (d[t] != 0).any()), default=0)
+
+    # 21-bit integers: nothing cut, 3 + 3 digits -> every pair kept -> exact
+    a, bt = (rs.randint(-2 ** 20, 2 ** 20, (n, n)).astype(np.float64) for _ in range(2))
+    (cut_a, ta), (cut_b, tb) = top(a), top(bt)
+    assert not cut_a and not cut_b and ta + tb <= S + 1
+    assert np.array_equal(contract(a, bt, c0), a @ bt.T)
+    # 33-bit integers: nothing cut, but 5 + 5 digits: pairs beyond level 8 are dropped -> not exact, the guard says so
+    a, bt = (rs.randint(-2 ** 32, 2 ** 32, (n, n)).astype(np.float64) for _ in range(2))
+    (cut_a, ta), (cut_b, tb) = top(a), top(bt)
+    assert not cut_a and not cut_b and ta + tb > S + 1
+    exact = a.astype(np.int64).astype(object) @ bt.astype(np.int64).astype(object).T
+    assert (contract(a, bt, c0).astype(object) != exact).any()
+    # full-mantissa doubles: elements are cut
+    assert top(rs.uniform(-1, 1, (n, n)))[0]
