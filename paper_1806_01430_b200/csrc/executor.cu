@@ -927,7 +927,9 @@ int shard_phase2(mmx_ctx* ctx, Slot& s) {
     int c0 = 0, cols = 0;
     shard_block(n, s.shard_world, src, &c0, &cols);
     if (src != s.shard_rank) MMX_CUDA(ctx, cudaStreamWaitEvent(s.stream, s.peer_ready[src], 0));
-    if (rows > 0 && cols > 0) MMX_CUDA(ctx, launch_matmul<T>(c, a, bt, n, r0, rows, c0, cols, strict, variant, s.d_scratch, s.stream));
+    // the member's rows of a are re-encoded for the tensor-core forms by the first column block only
+    if (rows > 0 && cols > 0)
+      MMX_CUDA(ctx, launch_matmul<T>(c, a, bt, n, r0, rows, c0, cols, strict, variant | (d > 0 ? kReuseOperandA : 0), s.d_scratch, s.stream));
   }
   MMX_CUDA(ctx, cudaEventRecord(s.ev_m1, s.stream));
   MMX_CUDA(ctx, launch_trace<T>(static_cast<T*>(s.d_sum), c, n, r0, rows, strict, s.stream));

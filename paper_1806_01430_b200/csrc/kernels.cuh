@@ -69,7 +69,7 @@ size_t matmul_3xtf32_scratch_bytes(int n);
 cudaError_t matmul_3xtf32_prepare();  // per device, before the first launch (not inside a stream capture)
 // wide: 128 x 256 tile with plain FP32 masters (faster, looser); default 128 x 128 with compensated masters
 cudaError_t launch_matmul_3xtf32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0,
-                                 int cols, bool wide, cudaStream_t stream);
+                                 int cols, bool wide, cudaStream_t stream, bool reuse_a = false);
 // FP64 on the 5th-generation tensor cores as exact INT8 slice products (Ozaki scheme, matmul_ozaki.cu); `slices` = 7 (default,
 // |error| <= 2e-14 K max|a| max|b|, bit-identical on the application's inputs) or 6
 bool matmul_ozaki_usable(int n);
@@ -79,14 +79,17 @@ cudaError_t matmul_ozaki_prepare();  // per device, before the first launch (not
 // finite); the contraction then runs only if none did, and *guard_out receives the flag's address so that the caller can
 // enqueue the FP64-pipe kernel under the opposite condition (FP64 auto mode: tensor cores exactly when they are error-free)
 constexpr int kOzMinN = 1024;
-// The guard: g[0] != 0 when some element has bits below its last digit (or is not finite); g[1], g[2] = highest non-zero digit
-// (1-based) anywhere in a / in bt.  The 7-slice contraction keeps the digit pairs with t + u <= 8, so it is error-free
-// exactly when no element is cut AND every non-zero pair is kept.
+// The guard: g[0] / g[3] != 0 when some element of a / of bt has bits below its last digit (or is not finite); g[1], g[2] =
+// highest non-zero digit (1-based) anywhere in a / in bt.  The 7-slice contraction keeps the digit pairs with t + u <= 8, so it
+// is error-free exactly when no element is cut AND every non-zero pair is kept.
 #ifdef __CUDACC__
-__device__ __forceinline__ bool ozaki_guard_lossy(const int* g) { return g[0] != 0 || g[1] + g[2] > 8; }
+__device__ __forceinline__ bool ozaki_guard_lossy(const int* g) { return (g[0] | g[3]) != 0 || g[1] + g[2] > 8; }
 #endif
+// OR-ed into `variant`: the rows [row0, row0 + rows) of a were already re-encoded into `scratch` by the previous launch_matmul
+// on it (the row-sharded run contracts the same rows of a against one column block after another)
+constexpr int kReuseOperandA = 0x1000;
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0,
-                                int cols, int slices, cudaStream_t stream, int** guard_out = nullptr);
+                                int cols, int slices, cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false);
 // gene 9: row i of the same (GEMV against bt)
 template <typename T>
 cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, bool strict, cudaStream_t stream);

@@ -511,16 +511,19 @@ int raster_group(int /*tile_m*/, size_t /*row_bytes*/) {
 template <>
 cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, int n, int row0, int rows, int col0, int cols,
                                   bool strict, int variant, void* scratch, cudaStream_t stream) {
+  const bool reuse_a = (variant & kReuseOperandA) != 0;
+  variant &= ~kReuseOperandA;
   // tensor cores (INT8 slice products, matmul_ozaki.cu): on request
   if (!strict && scratch != nullptr && (variant == 40 || variant == 41))
-    return launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, variant == 41 ? 6 : 7, stream);
+    return launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, variant == 41 ? 6 : 7, stream, nullptr,
+                               reuse_a && variant == 40);
   const bool dmma_ok = n % 2 == 0 && col0 % 2 == 0 && cols % 2 == 0;  // 16-byte aligned double2 accesses of c
   // auto: the INT8 tensor cores whenever their 7 x 7-bit slices reproduce every operand element exactly (then the result is the
   // error-free product rounded once -- bit-identical to the CPU program on the application's inputs), the FP64 pipe otherwise.
   // Both kernels are enqueued; a device flag written by the slice pass lets exactly one of them run.
   if (!strict && variant == 0 && scratch != nullptr && n >= kOzMinN && dmma_ok) {
     int* lossy = nullptr;
-    if (cudaError_t e = launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 7, stream, &lossy); e != cudaSuccess) return e;
+    if (cudaError_t e = launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 7, stream, &lossy, reuse_a); e != cudaSuccess) return e;
     return dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, stream, lossy);
   }
   if (variant == 0) variant = 4;  // the FP64 pipe: DMMA, tile by size (best of the tuning points, profiles/)
@@ -553,9 +556,11 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
 template <>
 cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int n, int row0, int rows, int col0, int cols,
                                  bool strict, int variant, void* scratch, cudaStream_t stream) {
+  const bool reuse_a = (variant & kReuseOperandA) != 0;
+  variant &= ~kReuseOperandA;
   // tensor cores (split-precision TF32, matmul_tc.cu): large matrices by default, any n % 4 == 0 on request
   if (!strict && scratch != nullptr && n % 4 == 0 && (variant == 30 || variant == 31 || (variant == 0 && n >= kTcMinN)))
-    return launch_matmul_3xtf32(c, a, bt, scratch, n, row0, rows, col0, cols, variant == 31, stream);
+    return launch_matmul_3xtf32(c, a, bt, scratch, n, row0, rows, col0, cols, variant == 31, stream, reuse_a);
   // variant 1 keeps the first-generation kernel (k-major smem, register-staged) for A/B runs and
   // for n % 4 != 0, where rows are not 16-byte aligned
   if (variant != 1 && n % 4 == 0) {

@@ -259,7 +259,7 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
 template <int S>
 __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restrict__ src, signed char* __restrict__ dst, int* __restrict__ exps,
                                                           size_t plane, int n, int kq, int src_row0, int nrows, int dst_row0,
-                                                          int* __restrict__ guard, int guard_slot) {
+                                                          int* __restrict__ guard, int lossy_slot, int top_slot) {
   __shared__ double red[8];
   __shared__ int top_sh[8];
   __shared__ int e_sh;
@@ -363,8 +363,8 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
     if (tid == 0) {
 #pragma unroll
       for (int w = 1; w < 8; ++w) top = max(top, top_sh[w]);
-      if (lossy && guard[0] == 0) atomicOr(guard, 1);
-      if (top > guard[guard_slot]) atomicMax(guard + guard_slot, top);  // read first: after a few rows nobody needs the atomic
+      if (lossy && guard[lossy_slot] == 0) atomicOr(guard + lossy_slot, 1);
+      if (top > guard[top_slot]) atomicMax(guard + top_slot, top);  // read first: after a few rows nobody needs the atomic
     }
   }
 }
@@ -400,7 +400,7 @@ cudaError_t oz_configure() {
 // kernel run only when they are not
 template <int S, int C, int BK>
 cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                  cudaStream_t stream, int** guard_out = nullptr) {
+                  cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false) {
   if (cudaError_t e = oz_configure<S, C, BK>(); e != cudaSuccess) return e;
   const int kq = oz_kq(n);
   // scratch: a slices [S][n][kq] (absolute rows), bt slices [S][pad64(n)][kq] (rows relative to col0), exponents
@@ -412,12 +412,14 @@ cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, i
   const int cols_pad = static_cast<int>(oz_rows_pad(cols, OZ_BN));
   int* flag = nullptr;
   if (guard_out != nullptr) {
-    flag = eb + n + OZ_BN;  // {lossy, top digit of a, top digit of bt}
+    flag = eb + n + OZ_BN;  // {a is cut, top digit of a, top digit of bt, bt is cut}
     *guard_out = flag;
-    if (cudaError_t e = cudaMemsetAsync(flag, 0, 3 * sizeof(int), stream); e != cudaSuccess) return e;
+    if (cudaError_t e = reuse_a ? cudaMemsetAsync(flag + 2, 0, 2 * sizeof(int), stream) : cudaMemsetAsync(flag, 0, 4 * sizeof(int), stream);
+        e != cudaSuccess)
+      return e;
   }
-  ozaki_slice_kernel<S><<<rows, 256, 0, stream>>>(a, sa, ea, a_plane, n, kq, row0, rows, row0, flag, 1);
-  ozaki_slice_kernel<S><<<cols_pad, 256, 0, stream>>>(bt, sb, eb, b_plane, n, kq, col0, cols, 0, flag, 2);
+  if (!reuse_a) ozaki_slice_kernel<S><<<rows, 256, 0, stream>>>(a, sa, ea, a_plane, n, kq, row0, rows, row0, flag, 0, 1);
+  ozaki_slice_kernel<S><<<cols_pad, 256, 0, stream>>>(bt, sb, eb, b_plane, n, kq, col0, cols, 0, flag, 3, 2);
   CUtensorMap map_a, map_a_part, map_b;
   if (!make_slice_map(&map_a, sa, static_cast<size_t>(n), kq, BK, OZ_BM, S, S) ||
       !make_slice_map(&map_a_part, sa, static_cast<size_t>(n), kq, BK, OZ_BM / C, S, 1) || !make_slice_map(&map_b, sb, b_rows, kq, BK, OZ_BN, S, S))
@@ -460,10 +462,10 @@ size_t matmul_ozaki_scratch_bytes(int n) {
 }
 
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                int slices, cudaStream_t stream, int** guard_out) {
+                                int slices, cudaStream_t stream, int** guard_out, bool reuse_a) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr) return cudaErrorInvalidValue;
-  if (guard_out != nullptr) return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream, guard_out);
+  if (guard_out != nullptr || reuse_a) return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream, guard_out, reuse_a);
   // tuning hooks (tools/ozaki_cluster_sweep.sh): CTAs per cluster sharing the a slices by multicast, k bytes per stage
   static const int cluster = [] { const char* e = getenv("MMX_OZ_CLUSTER"); return e ? atoi(e) : 1; }();
   static const int bk = [] { const char* e = getenv("MMX_OZ_BK"); return e ? atoi(e) : 64; }();

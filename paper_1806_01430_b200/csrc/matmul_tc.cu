@@ -623,14 +623,15 @@ cudaError_t ts_configure() {
 // split + contraction in the stacked form
 template <int CS>
 cudaError_t ts_go(cudaStream_t stream, float* c, const float* a, const float* bt, float* scratch, int n, int row0, int rows, int col0,
-                  int cols) {
+                  int cols, bool reuse_a) {
   if (cudaError_t e = ts_configure<CS>(); e != cudaSuccess) return e;
   const int kq = plane_row(n);
   float* pa = scratch;                                      // [2][n][kq]
   const size_t a_plane = static_cast<size_t>(n) * kq;
   float* pb = scratch + 2 * a_plane;                        // [blocks][256][kq], relative to col0
   auto blocks_for = [](size_t total) { return static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 16)); };
-  split_planes_kernel<<<blocks_for(static_cast<size_t>(rows) * (kq / 4)), 256, 0, stream>>>(a, pa, a_plane, n, kq, row0, rows, rows, row0, 0);
+  if (!reuse_a)  // the row-sharded run contracts the same rows of a against one column block after another
+    split_planes_kernel<<<blocks_for(static_cast<size_t>(rows) * (kq / 4)), 256, 0, stream>>>(a, pa, a_plane, n, kq, row0, rows, rows, row0, 0);
   const int cols_pad = (cols + 127) / 128 * 128;
   split_planes_kernel<<<blocks_for(static_cast<size_t>(cols_pad) * (kq / 4)), 256, 0, stream>>>(bt, pb, 0, n, kq, col0, cols, cols_pad, 0, 1);
   CUtensorMap map_ahi, map_alo, map_b;
@@ -663,7 +664,7 @@ size_t matmul_3xtf32_scratch_bytes(int n) {
 }
 
 cudaError_t launch_matmul_3xtf32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0,
-                                 int cols, bool wide, cudaStream_t stream) {
+                                 int cols, bool wide, cudaStream_t stream, bool reuse_a) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr || n % 4 != 0) return cudaErrorInvalidValue;
   // tuning hook (tools/tc_probe.py): 14800 + chunk stages = stacked form (32 k per stage); BN * 100 + chunk stages (16 k per
@@ -671,11 +672,11 @@ cudaError_t launch_matmul_3xtf32(float* c, const float* a, const float* bt, void
   static const int mode_env = env_int("MMX_TC_MODE", 0);
   const int mode = mode_env ? mode_env : (wide ? 25604 : 14802);
   switch (mode) {
-    case 14801: return ts_go<1>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols);
-    case 14802: return ts_go<2>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols);
-    case 14803: return ts_go<3>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols);
-    case 14804: return ts_go<4>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols);
-    case 14816: return ts_go<16>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols);
+    case 14801: return ts_go<1>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a);
+    case 14802: return ts_go<2>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a);
+    case 14803: return ts_go<3>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a);
+    case 14804: return ts_go<4>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a);
+    case 14816: return ts_go<16>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a);
     default: break;
   }
   const int kp = packed_row(n);
