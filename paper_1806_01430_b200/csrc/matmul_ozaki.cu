@@ -257,7 +257,7 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
 // index) is dst + t * plane + r * kq; k >= n is zero.  Rows [src_row0, src_row0 + nrows) of src; rows up to nrows_pad are
 // written as zeros with exponent 0 (tile overhang inside the tensor map).
 template <int S>
-__global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restrict__ src, signed char* __restrict__ dst, int* __restrict__ exps,
+__global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const double* __restrict__ src, signed char* __restrict__ dst, int* __restrict__ exps,
                                                           size_t plane, int n, int kq, int src_row0, int nrows, int dst_row0,
                                                           int* __restrict__ guard, int lossy_slot, int top_slot) {
   __shared__ double red[8];
@@ -338,12 +338,14 @@ __global__ void __launch_bounds__(256) ozaki_slice_kernel(const double* __restri
         const int d = __double2loint(shifted);
         rem = fma(-(shifted - 6755399441055744.0), down, rem);  // exact: removes a prefix of rem's bits
         dig[t] |= (d & 0xff) << (8 * q);
-        if (d != 0) top = max(top, t + 1);
       }
       lossy |= rem != 0.0;  // bits below the last digit: the slices do not reproduce this element exactly
     }
 #pragma unroll
-    for (int t = 0; t < S; ++t) *reinterpret_cast<int*>(drow + t * plane + k0) = dig[t];
+    for (int t = 0; t < S; ++t) {
+      if (dig[t] != 0) top = max(top, t + 1);
+      *reinterpret_cast<int*>(drow + t * plane + k0) = dig[t];
+    }
   };
 #pragma unroll
   for (int it = 0; it < KEEP; ++it) {
