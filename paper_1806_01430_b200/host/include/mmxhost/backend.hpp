@@ -15,13 +15,52 @@
 #include <cstddef>
 #include <functional>
 #include <mutex>
+#include <optional>
+#include <string_view>
 #include <vector>
 
 #include "mmx.h"
-#include "mmxhost/evaluation.hpp"
-#include "mmxhost/sim_model.hpp"
+#include "mmxhost/genome.hpp"
+#include "mmxhost/cost_model.hpp"
 
 namespace mmxhost {
+
+// ---- what a measurement returns (/root/reference/proj/include/acctune/evaluation.hpp:13-37, src/evaluation.cpp:5-25) ----
+
+// Numeric values are part of the C ABI (mmx_status in include/mmx.h).
+enum class EvalStatus : int { Measured = 0, CompileError = 1, RuntimeError = 2, Timeout = 3 };
+
+inline std::string_view to_string(EvalStatus s) {
+  switch (s) {
+    case EvalStatus::Measured: return "measured";
+    case EvalStatus::CompileError: return "compile_error";
+    case EvalStatus::Timeout: return "timeout";
+    case EvalStatus::RuntimeError: break;
+  }
+  return "runtime_error";
+}
+
+inline std::optional<EvalStatus> eval_status_from_string(std::string_view s) {
+  for (EvalStatus st : {EvalStatus::Measured, EvalStatus::CompileError, EvalStatus::RuntimeError, EvalStatus::Timeout})
+    if (s == to_string(st)) return st;
+  return std::nullopt;
+}
+
+struct EvaluationOutcome {
+  EvalStatus status = EvalStatus::RuntimeError;
+  double time_s = 0.0;       // Measured: benchmark time; Timeout: the budget; otherwise 0
+  double wall_cost_s = 0.0;  // cost of producing the outcome the first time
+};
+
+struct EvalCounters {
+  std::uint64_t requests = 0;       // evaluate() calls
+  std::uint64_t distinct = 0;       // unique genomes seen this run
+  std::uint64_t cache_hits = 0;     // requests - distinct
+  std::uint64_t backend_calls = 0;  // real measurements (disk-cache hits excluded)
+  double elapsed_s = 0.0;           // sum of wall_cost_s over distinct genomes, in genome order
+};
+
+// ---- backends -------------------------------------------------------------------------------------------------
 
 class EvalBackend {
  public:

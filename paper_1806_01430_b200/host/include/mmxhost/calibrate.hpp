@@ -25,7 +25,7 @@
 
 #include "mmx.h"
 #include "mmxhost/genome.hpp"
-#include "mmxhost/sim_model.hpp"
+#include "mmxhost/cost_model.hpp"
 
 namespace mmxhost {
 

@@ -1,4 +1,4 @@
-// sim_model.hpp -- the additive synthetic cost model and its brute-force optimum.
+// cost_model.hpp -- the additive synthetic cost model and its brute-force optimum.
 //
 // Deterministic stand-in for real timings: the parity oracle for the GA trajectory tests and the
 // format cost-model calibration would emit.  Semantics follow

@@ -22,9 +22,23 @@
 #include <vector>
 
 #include "mmxhost/backend.hpp"
-#include "mmxhost/evaluation.hpp"
 
 namespace mmxhost {
+
+// What run_ga needs (/root/reference/proj/include/acctune/evaluation.hpp:39-56; ga.cpp:100-107,191-201,255,272).  evaluate_all returns outcomes aligned
+// with its input.
+class GenomeEvaluator {
+ public:
+  virtual ~GenomeEvaluator() = default;
+  virtual EvaluationOutcome evaluate(const Genome& genome) = 0;
+  virtual std::vector<EvaluationOutcome> evaluate_all(const std::vector<Genome>& genomes) {
+    std::vector<EvaluationOutcome> out;
+    out.reserve(genomes.size());
+    for (const Genome& g : genomes) out.push_back(evaluate(g));
+    return out;
+  }
+  virtual EvalCounters counters() const = 0;
+};
 
 class Evaluator : public GenomeEvaluator {
  public:

@@ -14,17 +14,40 @@
 // fitness of the population (0 if nothing measured).
 #pragma once
 
+#include <random>
+#include <cstddef>
 #include <cstdint>
 #include <iosfwd>
 #include <string>
 #include <utility>
 #include <vector>
 
-#include "mmxhost/evaluation.hpp"
+#include "mmxhost/evaluator.hpp"
 #include "mmxhost/genome.hpp"
-#include "mmxhost/rng.hpp"
 
 namespace mmxhost {
+
+// ---- the random stream (/root/reference/proj/include/acctune/rng.hpp:13-31): the draw order is part of the GA contract ----
+
+
+class Rng {
+ public:
+  explicit Rng(std::uint64_t seed) : engine_(seed) {}
+
+  std::uint64_t raw() { return engine_(); }
+  // low bit of one draw
+  bool bit() { return (raw() & 1u) == 1u; }
+  // top 53 bits of one draw scaled into [0, 1)
+  double real01() { return static_cast<double>(raw() >> 11) * (1.0 / 9007199254740992.0); }
+  // one draw modulo n
+  std::size_t index(std::size_t n) { return static_cast<std::size_t>(raw() % n); }
+
+ private:
+  std::mt19937_64 engine_;
+};
+
+
+// ---- the GA ------------------------------------------------------------------------------------------------------
 
 struct GAParams {
   int population = 12;          // M

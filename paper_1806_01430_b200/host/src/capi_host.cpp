@@ -15,7 +15,7 @@
 #include "mmxhost/ga.hpp"
 #include "mmxhost/json_lite.hpp"
 #include "mmxhost/kernel_match.hpp"
-#include "mmxhost/sim_model.hpp"
+#include "mmxhost/cost_model.hpp"
 
 using namespace mmxhost;
 

@@ -19,7 +19,7 @@
 #include "mmxhost/ga.hpp"
 #include "mmxhost/json_lite.hpp"
 #include "mmxhost/kernel_match.hpp"
-#include "mmxhost/sim_model.hpp"
+#include "mmxhost/cost_model.hpp"
 #include "mmxhost/source_model.hpp"
 
 namespace fs = std::filesystem;

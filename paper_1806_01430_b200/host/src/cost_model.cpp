@@ -1,4 +1,4 @@
-#include "mmxhost/sim_model.hpp"
+#include "mmxhost/cost_model.hpp"
 
 #include <cstdint>
 #include <fstream>
