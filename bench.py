@@ -259,16 +259,17 @@ def run_ours(args):
         ach = flops / (ms8 * 1e-3) / 1e12
         share = ms8 * 1e-3 / (device_s / args.steps)
         if dtype == capi.F64 and n >= 1024:
-            # auto mode: this workload's operands are reproduced exactly by 7 x 7-bit slices, so gene 8 runs on the INT8 tensor
-            # cores (matmul_ozaki.cu); ms8 covers the two slice passes, the contraction and the skipped FP64-pipe launch
+            # auto mode: this workload's operands carry two 7-bit digits, so the cheapest error-free form is the 6-slice one (21
+            # INT8 slice products per term, matmul_ozaki.cu); ms8 covers the two slice passes, that contraction and the two
+            # guarded launches that exit at once (7-slice form, FP64 pipe)
             int8_peak = 2.0 * peaks["bf16_tflops"]
-            ops = 28.0 * flops / (ms8 * 1e-3) / 1e12
+            ops = 21.0 * flops / (ms8 * 1e-3) / 1e12
             roof = {"bound": "tensor", "pipe": "int8 (tcgen05.mma.kind::i8, INT32 accumulators in TMEM)",
-                    "kernel": "matmul_ozaki (gene 8: 7 exact 7-bit INT8 slices per operand, 28 slice products per FP64 term; slice passes included)",
+                    "kernel": "matmul_ozaki<6> (gene 8: exact 7-bit INT8 slices, 21 slice products per FP64 term; slice passes included)",
                     "achieved": ops, "peak": int8_peak, "unit": "TOP/s", "frac": ops / int8_peak,
                     "traffic": ncu_traffic("matmul_ozaki", n), "ms_per_launch": ms8, "share_of_step": share,
                     "effective_fp64_tflops": ach,
-                    "peak_source": "twice MEASURED_PEAKS.json bf16_tflops (INT8 runs at twice the bf16 rate); achieved counts the 28 INT8 "
+                    "peak_source": "twice MEASURED_PEAKS.json bf16_tflops (INT8 runs at twice the bf16 rate); achieved counts the 21 INT8 "
                                    "slice products issued per FP64 term"}
         else:
             pipe_peak = capi.peak_probe(capi.PEAK_FP64_FMA if dtype == capi.F64 else capi.PEAK_FP32_FMA, local_rank)
@@ -314,7 +315,7 @@ def run_ours(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
             "data": "synthetic (the program generates its own inputs: a=(i+j)/N, b=(i-j)/N)",
             "config": {"workload": f"matrix app N={n} {args.dtype}, genome {GENOME_ALL_NESTS} (all six loop nests offloaded)",
-                       "gene8": ("auto: INT8 tensor cores (7 exact slices; this workload's operands are reproduced exactly), FP64 pipe otherwise"
+                       "gene8": ("auto: INT8 tensor cores in the cheapest error-free form (6 slices for this workload's operands), FP64 pipe otherwise"
                                  if (dtype == capi.F64 and n >= 1024) else "default kernel for this dtype and size"),
                        "n": n, "genome": GENOME_ALL_NESTS, "individuals_per_step_per_gpu": 1,
                        "l2": "working set 4*N^2*E per step exceeds L2; no flush needed"},
@@ -322,9 +323,9 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(plan.h2d_bytes), "d2h_bytes_per_step": int(plan.d2h_bytes),
                     "note": "host clock around mmx_measure (plan + 6 launches + checksum D2H + sync); this genome has no host-side inputs"},
             "e2e_mixed": mixed, "e2e_host_buffers": host_io,
-            # the plan counts one launch per offloaded nest; in FP64 auto mode gene 8 is four kernels (two slice passes, the
-            # tensor-core contraction, the guarded FP64-pipe launch that exits at once)
-            "gpu_launches": (int(plan.kernel_launches) + (3 if (dtype == capi.F64 and n >= 1024) else 0)) * args.steps,
+            # the plan counts one launch per offloaded nest; in FP64 auto mode gene 8 is five kernels (two slice passes, the
+            # tensor-core contraction, and the guarded 7-slice and FP64-pipe launches that exit at once)
+            "gpu_launches": (int(plan.kernel_launches) + (4 if (dtype == capi.F64 and n >= 1024) else 0)) * args.steps,
             "clocks": clocks, "roofline": roof, "roofline_hbm": hbm_roof, "cpu_baseline": base,
             "checksum": checksum,
         }

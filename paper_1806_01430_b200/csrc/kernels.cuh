@@ -79,11 +79,14 @@ cudaError_t matmul_ozaki_prepare();  // per device, before the first launch (not
 // finite); the contraction then runs only if none did, and *guard_out receives the flag's address so that the caller can
 // enqueue the FP64-pipe kernel under the opposite condition (FP64 auto mode: tensor cores exactly when they are error-free)
 constexpr int kOzMinN = 1024;
-// The guard: g[0] / g[3] != 0 when some element of a / of bt has bits below its last digit (or is not finite); g[1], g[2] =
-// highest non-zero digit (1-based) anywhere in a / in bt.  The 7-slice contraction keeps the digit pairs with t + u <= 8, so it
-// is error-free exactly when no element is cut AND every non-zero pair is kept.
+// The guard: g[0] / g[3] != 0 when some element of a / of bt has bits below its 7th digit (or is not finite); g[1], g[2] =
+// highest non-zero digit (1-based) anywhere in a / in bt.  The S-slice contraction uses digits 1..S and keeps the digit pairs
+// with t + u <= S + 1, so it is error-free exactly when no element is cut, no digit beyond S is set and every non-zero pair
+// is kept.  Auto mode runs the cheapest error-free form: 6 slices, else 7 slices, else the FP64 pipe.
 #ifdef __CUDACC__
-__device__ __forceinline__ bool ozaki_guard_lossy(const int* g) { return (g[0] | g[3]) != 0 || g[1] + g[2] > 8; }
+__device__ __forceinline__ bool ozaki_guard_lossy(const int* g, int slices) {
+  return (g[0] | g[3]) != 0 || g[1] > slices || g[2] > slices || g[1] + g[2] > slices + 1;
+}
 #endif
 // OR-ed into `variant`: the rows [row0, row0 + rows) of a were already re-encoded into `scratch` by the previous launch_matmul
 // on it (the row-sharded run contracts the same rows of a against one column block after another)

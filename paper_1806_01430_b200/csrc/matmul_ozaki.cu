@@ -84,10 +84,13 @@ template <int S, int C, int BK>
 __global__ void __launch_bounds__(OZ_THREADS, 1)
 matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_a_part,
                     const __grid_constant__ CUtensorMap map_b, const int* __restrict__ exp_a, const int* __restrict__ exp_b, int n, int kq, int row0, int rows, int col0, int cols,
-                    int group, int debug_noload, const int* __restrict__ skip_if) {
+                    int group, int debug_noload, const int* __restrict__ guard) {
   using Sh = OzShape<S, BK>;
   // guarded launch (FP64 auto mode): the slices lost bits of some operand, the FP64-pipe kernel runs instead
-  if (skip_if != nullptr && ozaki_guard_lossy(skip_if)) return;
+  if (guard != nullptr) {  // run iff this is the cheapest error-free form: 6 slices when they suffice, else 7
+    const bool ok6 = !ozaki_guard_lossy(guard, 6);
+    if (S == 6 ? !ok6 : (ok6 || ozaki_guard_lossy(guard, 7))) return;
+  }
   constexpr int OZ_STAGES = Sh::STAGES, OZ_BK = BK;
   extern __shared__ unsigned char smem_raw[];
   const unsigned raw = smem_u32(smem_raw);
@@ -398,33 +401,52 @@ cudaError_t oz_configure() {
   return cudaSuccess;
 }
 
-// guard_out != nullptr: also record whether the slices are lossy in a device flag (returned through *guard_out) and let the
-// kernel run only when they are not
-template <int S, int C, int BK>
-cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                  cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false) {
-  if (cudaError_t e = oz_configure<S, C, BK>(); e != cudaSuccess) return e;
-  const int kq = oz_kq(n);
-  // scratch: a slices [S][n][kq] (absolute rows), bt slices [S][pad64(n)][kq] (rows relative to col0), exponents
-  const size_t a_plane = static_cast<size_t>(n) * kq, b_rows = oz_rows_pad(n, OZ_BN), b_plane = b_rows * kq;
-  signed char* sa = static_cast<signed char*>(scratch);
-  signed char* sb = sa + S * a_plane;
-  int* ea = reinterpret_cast<int*>(sb + S * b_plane);
-  int* eb = ea + n;
-  const int cols_pad = static_cast<int>(oz_rows_pad(cols, OZ_BN));
-  int* flag = nullptr;
-  if (guard_out != nullptr) {
-    flag = eb + n + OZ_BN;  // {a is cut, top digit of a, top digit of bt, bt is cut}
-    *guard_out = flag;
+// Where things live in `scratch` for P digit planes: a slices [P][n][kq] (absolute rows), bt slices [P][pad64(n)][kq] (rows
+// relative to the launch's first column), row exponents, the guard words.
+struct OzLayout {
+  int kq;
+  size_t a_plane, b_rows, b_plane;
+  signed char *sa, *sb;
+  int *ea, *eb, *guard;
+  OzLayout(void* scratch, int n, int planes) {
+    kq = oz_kq(n);
+    a_plane = static_cast<size_t>(n) * kq;
+    b_rows = oz_rows_pad(n, OZ_BN);
+    b_plane = b_rows * kq;
+    sa = static_cast<signed char*>(scratch);
+    sb = sa + planes * a_plane;
+    ea = reinterpret_cast<int*>(sb + planes * b_plane);
+    eb = ea + n;
+    guard = eb + n + OZ_BN;  // {a is cut, top digit of a, top digit of bt, bt is cut}
+  }
+};
+
+// the slice passes (P planes); with_guard: also record whether anything was cut and the highest digits in use
+template <int P>
+cudaError_t oz_slices(const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols, cudaStream_t stream,
+                      bool with_guard, bool reuse_a) {
+  const OzLayout L(scratch, n, P);
+  int* flag = with_guard ? L.guard : nullptr;
+  if (with_guard)
     if (cudaError_t e = reuse_a ? cudaMemsetAsync(flag + 2, 0, 2 * sizeof(int), stream) : cudaMemsetAsync(flag, 0, 4 * sizeof(int), stream);
         e != cudaSuccess)
       return e;
-  }
-  if (!reuse_a) ozaki_slice_kernel<S><<<rows, 256, 0, stream>>>(a, sa, ea, a_plane, n, kq, row0, rows, row0, flag, 0, 1);
-  ozaki_slice_kernel<S><<<cols_pad, 256, 0, stream>>>(bt, sb, eb, b_plane, n, kq, col0, cols, 0, flag, 3, 2);
+  const int cols_pad = static_cast<int>(oz_rows_pad(cols, OZ_BN));
+  if (!reuse_a) ozaki_slice_kernel<P><<<rows, 256, 0, stream>>>(a, L.sa, L.ea, L.a_plane, n, L.kq, row0, rows, row0, flag, 0, 1);
+  ozaki_slice_kernel<P><<<cols_pad, 256, 0, stream>>>(bt, L.sb, L.eb, L.b_plane, n, L.kq, col0, cols, 0, flag, 3, 2);
+  return cudaGetLastError();
+}
+
+// the contraction over the first S of P planes; guarded: the kernel reads the guard and runs only if it is the cheapest
+// error-free form
+template <int S, int C, int BK>
+cudaError_t oz_contract(double* c, void* scratch, int planes, int n, int row0, int rows, int col0, int cols, cudaStream_t stream, bool guarded) {
+  if (cudaError_t e = oz_configure<S, C, BK>(); e != cudaSuccess) return e;
+  const OzLayout L(scratch, n, planes);
   CUtensorMap map_a, map_a_part, map_b;
-  if (!make_slice_map(&map_a, sa, static_cast<size_t>(n), kq, BK, OZ_BM, S, S) ||
-      !make_slice_map(&map_a_part, sa, static_cast<size_t>(n), kq, BK, OZ_BM / C, S, 1) || !make_slice_map(&map_b, sb, b_rows, kq, BK, OZ_BN, S, S))
+  if (!make_slice_map(&map_a, L.sa, static_cast<size_t>(n), L.kq, BK, OZ_BM, planes, S) ||
+      !make_slice_map(&map_a_part, L.sa, static_cast<size_t>(n), L.kq, BK, OZ_BM / C, planes, 1) ||
+      !make_slice_map(&map_b, L.sb, L.b_rows, L.kq, BK, OZ_BN, planes, S))
     return cudaErrorNotSupported;
   const int col_tiles = (cols + OZ_BN - 1) / OZ_BN;
   static const int noload = [] { const char* e = getenv("MMX_OZ_NOLOAD"); return (e && C == 1) ? atoi(e) : 0; }();
@@ -440,8 +462,17 @@ cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, i
   attr[0].val.clusterDim.z = 1;
   cfg.attrs = attr;
   cfg.numAttrs = C > 1 ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, matmul_ozaki_kernel<S, C, BK>, c, map_a, map_a_part, map_b, static_cast<const int*>(ea), static_cast<const int*>(eb), n,
-                            kq, row0, rows, col0, cols, raster_group(OZ_BM, static_cast<size_t>(kq)), noload, static_cast<const int*>(flag));
+  return cudaLaunchKernelEx(&cfg, matmul_ozaki_kernel<S, C, BK>, c, map_a, map_a_part, map_b, static_cast<const int*>(L.ea),
+                            static_cast<const int*>(L.eb), n, L.kq, row0, rows, col0, cols, raster_group(OZ_BM, static_cast<size_t>(L.kq)), noload,
+                            static_cast<const int*>(guarded ? L.guard : nullptr));
+}
+
+// slices + contraction with S planes (the explicit variants)
+template <int S, int C, int BK>
+cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
+                  cudaStream_t stream, bool reuse_a = false) {
+  if (cudaError_t e = oz_slices<S>(a, bt, scratch, n, row0, rows, col0, cols, stream, false, reuse_a); e != cudaSuccess) return e;
+  return oz_contract<S, C, BK>(c, scratch, S, n, row0, rows, col0, cols, stream, false);
 }
 
 }  // namespace
@@ -467,7 +498,15 @@ cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, vo
                                 int slices, cudaStream_t stream, int** guard_out, bool reuse_a) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr) return cudaErrorInvalidValue;
-  if (guard_out != nullptr || reuse_a) return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream, guard_out, reuse_a);
+  if (guard_out != nullptr) {
+    // auto mode: 7 digit planes and the guard once, then the 6-slice and the 7-slice contraction, each guarded; the caller
+    // adds the FP64-pipe kernel under the remaining condition
+    *guard_out = OzLayout(scratch, n, 7).guard;
+    if (cudaError_t e = oz_slices<7>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a); e != cudaSuccess) return e;
+    if (cudaError_t e = oz_contract<6, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true); e != cudaSuccess) return e;
+    return oz_contract<7, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true);
+  }
+  if (reuse_a) return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream, true);
   // tuning hooks (tools/ozaki_cluster_sweep.sh): CTAs per cluster sharing the a slices by multicast, k bytes per stage
   static const int cluster = [] { const char* e = getenv("MMX_OZ_CLUSTER"); return e ? atoi(e) : 1; }();
   static const int bk = [] { const char* e = getenv("MMX_OZ_BK"); return e ? atoi(e) : 64; }();

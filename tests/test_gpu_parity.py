@@ -424,6 +424,13 @@ def test_fp64_auto_uses_the_tensor_cores_exactly_when_they_are_error_free():
     # 21-bit integers: 3 digits each, all pairs kept -> tensor cores, and the result is the exact product
     a, bt, c0 = (rs.randint(-2 ** 20, 2 ** 20, (n, n)).astype(np.float64) for _ in range(3))
     assert bits_equal(run(0, a, bt, c0), c0 + a @ bt.T)
+    # 27-bit integers: 4 + 4 digits: too many for the 6-slice form (pairs up to t + u = 7), exactly what the 7-slice form keeps.
+    # The sums (~2^57) are beyond what FP64 accumulation carries exactly, the integer levels are not.
+    a, bt = (rs.randint(-2 ** 26, 2 ** 26, (n, n)).astype(np.float64) for _ in range(2))
+    exact = (a.astype(np.int64) @ bt.astype(np.int64).T).astype(np.float64)       # |sum| < 2^62: exact in int64
+    two_ulp = 2.0 * np.exp2(np.floor(np.log2(np.maximum(np.abs(exact), 1.0))) - 52)
+    assert (np.abs(run(0, a, bt, np.zeros((n, n))) - exact) <= two_ulp).all()     # only the final Horner roundings
+    assert (np.abs(run(4, a, bt, np.zeros((n, n))) - exact) > two_ulp).any()      # the FP64 pipe rounds at every step
     # 33-bit integers: nothing is cut, but digit pairs beyond t + u = 8 would be dropped -> the FP64 pipe again
     a, bt = (rs.randint(-2 ** 32, 2 ** 32, (n, n)).astype(np.float64) for _ in range(2))
     assert bits_equal(run(0, a, bt, c0), run(4, a, bt, c0))

@@ -44,7 +44,8 @@ def test_application_operands_use_two_digits_and_the_product_is_exact(n):
     a, bt = app_operands(n)
     for x in (a, bt):
         _, d, rem = slices(x)
-        assert (rem == 0).all() and all((dt == 0).all() for dt in d[2:])     # 14 bits: digits 1 and 2 only
+        assert (rem == 0).all() and all((dt == 0).all() for dt in d[2:])     # 14 bits: digits 1 and 2 only, so even the
+        # 6-slice form (digits <= 6, pairs t + u <= 7) keeps every non-zero pair: the cheapest error-free form of auto mode
     i = np.arange(n, dtype=np.float64)
     s1, s2 = n * (n - 1) / 2, (n - 1) * n * (2 * n - 1) / 6
     closed = (s2 + (i[:, None] - i[None, :]) * s1 - n * i[:, None] * i[None, :]) / n ** 2
