@@ -334,6 +334,7 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const double* __res
       double rem = bad ? 0.0 : v[q] * inv;
 #pragma unroll
       for (int t = 0; t < S; ++t) {
+        if (rem == 0.0) break;  // nothing left: the remaining digits are zero (short operands finish after a digit or two)
         const double up = pow2(7 * (t + 1) - 1), down = pow2(-(7 * (t + 1) - 1));
         // rint without the conversion units (they would bound this pass): adding 1.5 * 2^52 rounds to the integer grid
         // (ties to even) and leaves the integer in the low word of the sum
