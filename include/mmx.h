@@ -106,8 +106,9 @@ typedef struct mmx_config {
   const int32_t* devices;   /* CUDA ordinal per slot; NULL = slot s -> device s % deviceCount  */
   int32_t host_threads;     /* threads for CPU-mapped nests; 1 = the reference program         */
   int32_t launch_batching;  /* 1: inner-loop launch trains are submitted as CUDA graphs        */
-  int32_t matmul_variant;   /* gene-8 kernel: 0 auto (FP64: below N = 1024 DMMA; from there the INT8 tensor cores whenever their slices
-                             * reproduce every operand exactly -- the application's inputs always do -- and DMMA otherwise; FP32: tcgen05 split-TF32 with compensated
+  int32_t matmul_variant;   /* gene-8 kernel: 0 auto (FP64: below N = 1024 DMMA; from there the INT8 tensor cores whenever their 7-bit
+                             * slices give the error-free product -- 6 slices if that suffices, else 7; the application's inputs
+                             * always qualify -- and DMMA otherwise; FP32: tcgen05 split-TF32 with compensated
                              * accumulation for N >= 1024, FFMA below); 1 first SIMT kernel; 2, 4-13 DMMA tile shapes (FP64);
                              * 20, 22 SIMT tile shapes; 30 FP32 tcgen05 at any N % 4 == 0; 31 its wide-tile uncompensated form;
                              * 40 FP64 on the tcgen05 INT8 tensor cores (7 exact 7-bit slices per operand, error <= 2e-14 K max|a| max|b|,
