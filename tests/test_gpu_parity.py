@@ -436,6 +436,15 @@ def test_fp64_auto_uses_the_tensor_cores_exactly_when_they_are_error_free():
     assert bits_equal(run(0, a, bt, c0), run(4, a, bt, c0))
 
 
+def test_fp64_auto_falls_back_on_the_application_when_n_is_not_a_power_of_two():
+    """(i +- k) / 1536 has a full mantissa: every element is cut, so the whole individual is the FP64-pipe one, bit for bit."""
+    n = 1536
+    with capi.Context(n=n, dtype=capi.F64) as auto, capi.Context(n=n, dtype=capi.F64, matmul_variant=4) as pipe:
+        assert auto.measure("101010101001").status == capi.MEASURED and pipe.measure("101010101001").status == capi.MEASURED
+        assert bits_equal(auto.fetch(capi.ARRAY_C), pipe.fetch(capi.ARRAY_C))
+        assert auto.stats().checksum == pipe.stats().checksum
+
+
 def test_fp64_auto_on_the_application_is_bit_exact_and_fast():
     n = 4096
     with capi.Context(n=n, dtype=capi.F64, matmul_variant=4) as ctx:
