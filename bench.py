@@ -313,6 +313,9 @@ def run_ours(args):
             "metric": "matrix_app_gflops", "value": flops * args.steps * world / device_s / 1e9, "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": args.dtype,
+            "dtype_note": ("operands, results and every kernel but gene 8 are f64; gene 8 multiplies exact int8 digits of the f64 operands "
+                           "on the tensor cores (int32 sums) and rebuilds the f64 result, bit-identical to the f64 pipe here; the "
+                           "fp64_pipe arm is the same run without that" if (dtype == capi.F64 and n >= 1024) else None),
             "data": "synthetic (the program generates its own inputs: a=(i+j)/N, b=(i-j)/N)",
             "config": {"workload": f"matrix app N={n} {args.dtype}, genome {GENOME_ALL_NESTS} (all six loop nests offloaded)",
                        "gene8": ("auto: INT8 tensor cores in the cheapest error-free form (6 slices for this workload's operands), FP64 pipe otherwise"
