@@ -1,0 +1,15 @@
+#!/bin/bash
+# compute-sanitizer passes over small individuals (memcheck: out-of-bounds / misaligned accesses; racecheck: shared-memory
+# hazards; synccheck: barrier misuse).  Run under gpurun from the repo root:  bash tools/sanitize.sh <tag>
+tag=${1:-r1}
+out=gpurun_out/${tag}_sanitizer.txt
+: > $out
+for tool in memcheck synccheck; do
+  for cfg in "f64 1024" "f32 1024" "f64 256"; do
+    echo "== compute-sanitizer --tool $tool  one_individual.py $cfg" >> $out
+    timeout 600 compute-sanitizer --tool $tool --print-limit 5 python tools/one_individual.py $cfg 2>&1 | grep -E "ERROR SUMMARY|Error|error|Invalid|hazard|=========.*at " | head -12 >> $out
+  done
+done
+echo "== compute-sanitizer --tool racecheck  one_individual.py f64 256 (FP64 pipe kernels, fills, transpose, trace)" >> $out
+timeout 600 compute-sanitizer --tool racecheck --print-limit 5 python tools/one_individual.py f64 256 2>&1 | grep -E "RACECHECK SUMMARY|hazard|Error" | head -12 >> $out
+cat $out
