@@ -505,6 +505,18 @@ def test_row_sharded_fp64_through_the_int8_tensor_cores(world):
             assert bits_equal(got, ref.c[st["row0"]:st["row0"] + st["rows"]])
 
 
+def test_n16384_fp64_equals_closed_form():
+    """BASELINE config 5 size: the whole individual at N=16384 (2 GiB per array, K = 16384 terms per element) equals the exact
+    closed form bit for bit -- through the INT8 tensor-core contraction, whose level sums reach 2^29 here."""
+    n = 16384
+    with capi.Context(n=n, timeout_s=120.0) as ctx:
+        assert ctx.measure("101010101001").status == capi.MEASURED
+        assert ctx.stats().checksum == 0.0
+        got = ctx.fetch(capi.ARRAY_C)
+    for r0 in range(0, n, 2048):
+        assert bits_equal(got[r0:r0 + 2048], cpu.closed_form_c(n, r0, r0 + 2048)), r0
+
+
 def _normwise_bound_structured(n, tol):
     """tol * sum_k |a_ik| |bt_jk| for the program's own inputs: sum_k (i+k)|k-j| / N^2 = (i A_j + B_j) / N^2."""
     k = np.arange(n, dtype=np.float64)
