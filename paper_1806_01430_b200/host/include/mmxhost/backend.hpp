@@ -126,12 +126,14 @@ class CudaBackend : public EvalBackend {
   int num_slots() const;
   mmx_ctx* handle() const { return ctx_; }
   mmx_run_stats last_stats(int slot) const;
+  const CudaBackendConfig& config() const { return config_; }
 
  private:
   int acquire_slot();
   void release_slot(int slot);
 
   mmx_ctx* ctx_ = nullptr;
+  CudaBackendConfig config_;
   std::mutex mu_;
   std::condition_variable cv_;
   std::vector<char> busy_;

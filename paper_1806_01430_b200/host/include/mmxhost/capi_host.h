@@ -80,6 +80,10 @@ MMXH_API int mmxh_evaluator_gene_length(void* h);
 MMXH_API int mmxh_evaluator_evaluate(void* h, const uint8_t* bits, size_t n, mmxh_outcome* out);
 MMXH_API int mmxh_evaluator_evaluate_all(void* h, const uint8_t* bits, size_t count, size_t n, mmxh_outcome* outs);
 MMXH_API int mmxh_evaluator_counters(void* h, uint64_t c4[4], double* elapsed_s);
+/* longest-first scheduling of evaluate_all: costs[k] is the predicted cost of genome k (bits: count x n); unknown genomes cost 0 */
+MMXH_API int mmxh_evaluator_set_costs(void* h, const uint8_t* bits, const double* costs, size_t count, size_t n);
+/* the static estimate MultiGpuEvaluator schedules by (seconds, order of magnitude) */
+MMXH_API double mmxh_predicted_cost(const mmxh_cuda_config* cfg, const uint8_t* bits, size_t n);
 /* call counters of a callback backend: calls, max_in_flight */
 MMXH_API int mmxh_evaluator_cb_stats(void* h, int32_t out2[2]);
 

@@ -16,6 +16,7 @@
 #include <condition_variable>
 #include <exception>
 #include <filesystem>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -51,6 +52,14 @@ class Evaluator : public GenomeEvaluator {
   std::size_t gene_length() const { return backend_->gene_length(); }
   EvalBackend& backend() { return *backend_; }
 
+  // Scheduling hint for evaluate_all: genomes with a larger predicted cost are handed to the workers first (longest
+  // processing time first), so that one slow individual -- a genome that leaves the matmul nest on the CPU takes
+  // seconds, an all-offloaded one milliseconds -- does not start last and stretch the batch.  Outcomes stay aligned with
+  // the input and nothing else changes; without a hint the batch is pulled in input order, as the reference does
+  // (/root/reference/proj/src/evaluator.cpp:254-273).
+  using CostHint = std::function<double(const Genome&)>;
+  void set_cost_hint(CostHint hint) { cost_hint_ = std::move(hint); }
+
  protected:
   // Hook for subclasses that bind worker threads to resources (MultiGpuEvaluator): called by
   // worker `worker` of evaluate_all (0 for plain evaluate()).
@@ -72,6 +81,7 @@ class Evaluator : public GenomeEvaluator {
   void append_to_cache(const Genome& genome, const EvaluationOutcome& outcome);
 
   std::unique_ptr<EvalBackend> backend_;
+  CostHint cost_hint_;
   int jobs_;
   std::filesystem::path cache_file_;
 
@@ -84,7 +94,8 @@ class Evaluator : public GenomeEvaluator {
 // Population-parallel evaluation over the device slots of one CudaBackend: worker thread s of a
 // batch always measures on slot s (one stream / one set of device arrays / one GPU each), so
 // `jobs` == number of slots and no two workers contend for a device.  Memoisation, cache file
-// and counters are the Evaluator's.  No collective: each worker writes its outcome into the
+// and counters are the Evaluator's.  Batches are scheduled longest-first by a static estimate from the
+// residency plan (predicted_cost: host-side flops, launch counts, bytes over the bus).  No collective: each worker writes its outcome into the
 // aligned output slot and the gather is the thread join.
 class MultiGpuEvaluator : public Evaluator {
  public:
@@ -92,6 +103,10 @@ class MultiGpuEvaluator : public Evaluator {
 
  protected:
   EvaluationOutcome measure_with(int worker, const Genome& genome) override;
+
+ public:
+  // seconds, order-of-magnitude: only the ranking matters
+  static double predicted_cost(const Genome& genome, const CudaBackendConfig& config);
 
  private:
   CudaBackend* cuda_;

@@ -47,7 +47,7 @@ void throw_for_code(int code, const std::string& message) {
   }
 }
 
-CudaBackend::CudaBackend(const CudaBackendConfig& config) {
+CudaBackend::CudaBackend(const CudaBackendConfig& config) : config_(config) {
   if (config.devices.empty()) throw ConfigError("CudaBackend needs at least one device slot");
   mmx_config c;
   mmx_default_config(&c);

@@ -3,6 +3,7 @@
 #include "mmxhost/source_model.hpp"
 
 #include <cstring>
+#include <map>
 #include <memory>
 #include <sstream>
 #include <string>
@@ -237,6 +238,36 @@ MMXH_API void* mmxh_evaluator_create_cb(size_t genes, mmxh_measure_cb cb, void* 
     g_error = e.what();
     return nullptr;
   }
+}
+
+MMXH_API int mmxh_evaluator_set_costs(void* h, const uint8_t* bits, const double* costs, size_t count, size_t n) {
+  return guarded([&] {
+    auto table = std::make_shared<std::map<Genome, double>>();
+    for (std::size_t k = 0; k < count; ++k) (*table)[Genome(std::vector<std::uint8_t>(bits + k * n, bits + (k + 1) * n))] = costs[k];
+    static_cast<Handle*>(h)->ev->set_cost_hint([table](const Genome& g) {
+      const auto it = table->find(g);
+      return it == table->end() ? 0.0 : it->second;
+    });
+    return 0;
+  });
+}
+
+namespace {
+CudaBackendConfig cuda_config_of(const mmxh_cuda_config* cfg) {
+  CudaBackendConfig c;
+  c.n = cfg->n;
+  c.dtype = cfg->dtype;
+  c.numerics = cfg->numerics;
+  c.timeout_s = cfg->timeout_s;
+  c.repetitions = cfg->repetitions;
+  c.warmup = cfg->warmup;
+  c.host_threads = cfg->host_threads;
+  return c;
+}
+}  // namespace
+
+MMXH_API double mmxh_predicted_cost(const mmxh_cuda_config* cfg, const uint8_t* bits, size_t n) {
+  return MultiGpuEvaluator::predicted_cost(Genome(std::vector<std::uint8_t>(bits, bits + n)), cuda_config_of(cfg));
 }
 
 MMXH_API void* mmxh_evaluator_create_cuda(const mmxh_cuda_config* cfg, const char* cache_file) {

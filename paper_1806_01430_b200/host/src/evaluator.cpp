@@ -122,11 +122,20 @@ std::vector<EvaluationOutcome> Evaluator::evaluate_all(const std::vector<Genome>
     for (std::size_t i = 0; i < genomes.size(); ++i) results[i] = evaluate_as(0, genomes[i]);
     return results;
   }
+  // the order the workers pull in: longest predicted cost first when a hint is installed, input order otherwise
+  std::vector<std::size_t> order(genomes.size());
+  for (std::size_t i = 0; i < order.size(); ++i) order[i] = i;
+  if (cost_hint_) {
+    std::vector<double> cost(genomes.size());
+    for (std::size_t i = 0; i < genomes.size(); ++i) cost[i] = cost_hint_(genomes[i]);
+    std::stable_sort(order.begin(), order.end(), [&](std::size_t x, std::size_t y) { return cost[x] > cost[y]; });
+  }
   std::atomic<std::size_t> cursor{0};
   std::mutex failure_mu;
   std::exception_ptr first_failure;
   auto body = [&](int worker) {
-    for (std::size_t i = cursor.fetch_add(1); i < genomes.size(); i = cursor.fetch_add(1)) {
+    for (std::size_t at = cursor.fetch_add(1); at < order.size(); at = cursor.fetch_add(1)) {
+      const std::size_t i = order[at];
       try {
         results[i] = evaluate_as(worker, genomes[i]);
       } catch (...) {
@@ -161,7 +170,33 @@ EvalCounters Evaluator::counters() const {
 
 MultiGpuEvaluator::MultiGpuEvaluator(std::unique_ptr<CudaBackend> backend, std::filesystem::path cache_file)
     : Evaluator(std::unique_ptr<EvalBackend>(backend.get()), backend->num_slots(), std::move(cache_file)),
-      cuda_(backend.release()) {}
+      cuda_(backend.release()) {
+  const CudaBackendConfig config = cuda_->config();
+  set_cost_hint([config](const Genome& g) { return predicted_cost(g, config); });
+}
+
+double MultiGpuEvaluator::predicted_cost(const Genome& genome, const CudaBackendConfig& config) {
+  mmx_plan_info plan;
+  if (genome.size() != MMX_GENE_LENGTH || mmx_plan(genome.bits().data(), genome.size(), config.n, config.dtype, &plan) != MMX_OK ||
+      !plan.feasible)
+    return 0.0;  // infeasible genomes are outcomes produced on the spot
+  const double n = config.n, threads = std::max(1, config.host_threads);
+  double s = 0.0;
+  for (int k = 0; k < plan.num_steps; ++k) {
+    const mmx_plan_step& st = plan.steps[k];
+    switch (st.kind) {
+      case MMX_STEP_CPU:  // ~2 GFLOP/s per host core on the contraction, ~1 G element/s on the O(N^2) nests
+        s += st.nest == MMX_NEST_MATMUL ? 2.0 * n * n * n / (2.0e9 * threads) : n * n / 1.0e9;
+        break;
+      case MMX_STEP_GPU:  // ~3 us per launch of a launch train; the whole-nest kernels are the small term
+        s += 3.0e-6 * static_cast<double>(st.launches) + (st.nest == MMX_NEST_MATMUL ? 2.0 * n * n * n / 3.0e13 : n * n / 5.0e11);
+        break;
+      default:  // transfers: ~25 GB/s over the bus
+        s += 1.0e-5 + static_cast<double>(st.bytes) / 2.5e10;
+    }
+  }
+  return std::min(s, config.timeout_s) * std::max(1, config.repetitions + config.warmup);
+}
 
 EvaluationOutcome MultiGpuEvaluator::measure_with(int worker, const Genome& genome) {
   return cuda_->measure_on(worker % cuda_->num_slots(), genome);

@@ -207,6 +207,15 @@ class Evaluator:
         self.api.check(self.api.f("evaluator_evaluate_all")(self.h, flat.ctypes.data_as(C.POINTER(C.c_uint8)), C.c_size_t(len(genomes)), C.c_size_t(n), outs))
         return [o.as_tuple() for o in outs]
 
+    def set_costs(self, genomes, costs):
+        """Longest-first scheduling of evaluate_all (mmxhost only): genomes with a larger predicted cost start first."""
+        n = len(genomes[0])
+        flat = np.ascontiguousarray(np.concatenate([_bits(g) for g in genomes]))
+        arr = np.ascontiguousarray(costs, dtype=np.float64)
+        assert arr.size == len(genomes)
+        self.api.check(self.api.f("evaluator_set_costs")(self.h, flat.ctypes.data_as(C.POINTER(C.c_uint8)),
+                                                         arr.ctypes.data_as(C.POINTER(C.c_double)), C.c_size_t(len(genomes)), C.c_size_t(n)))
+
     def counters(self):
         c4, el = (C.c_uint64 * 4)(), C.c_double()
         self.api.check(self.api.f("evaluator_counters")(self.h, c4, C.byref(el)))
@@ -221,6 +230,16 @@ class Evaluator:
         n = self.api.check(self.api.f("run_ga")(self.h, C.byref(p), csv, C.c_size_t(1 << 16), best, C.byref(best_s), C.byref(base_s)))
         assert n < (1 << 16)
         return {"csv": csv.value.decode(), "best_genome": _str(best[:genes]), "best_s": best_s.value, "baseline_s": base_s.value}
+
+
+def predicted_cost(genome, n=256, dtype=0, numerics=0, timeout_s=120.0, repetitions=1, warmup=0, host_threads=1) -> float:
+    """The static estimate MultiGpuEvaluator orders a batch by (seconds, order of magnitude; 0 for infeasible genomes)."""
+    api = mine()
+    fn = api.lib.mmxh_predicted_cost
+    fn.restype = C.c_double
+    cfg = CudaConfig(n, dtype, numerics, timeout_s, repetitions, warmup, host_threads, 1, 0, 0, None)
+    bits = _bits(genome)
+    return float(fn(C.byref(cfg), bits.ctypes.data_as(C.POINTER(C.c_uint8)), C.c_size_t(bits.size)))
 
 
 class ToolchainMissingSignal(Exception):

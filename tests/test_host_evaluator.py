@@ -177,3 +177,60 @@ def test_cache_number_formatting_matches_nlohmann():
              5.5e-3: "0.0055", 2.5e-7: "2.5e-07", -0.5: "-0.5"}
     for v, want in cases.items():
         assert H.dump_number(v) == want
+
+
+# ---- longest-first scheduling of a batch (mmxhost only: the reference pulls in input order, evaluator.cpp:254-273) ----
+
+def test_cost_hint_starts_the_longest_genome_first():
+    api = H.mine()
+    started, lock = [], threading.Lock()
+
+    def record(g):
+        with lock:
+            started.append(g)
+        return (MEASURED, 1.0 + g.count("1"), 0.1)
+    batch = ["0001", "0011", "0111", "1111", "0000"]
+    with H.Evaluator.from_callback(api, 4, record, jobs=1) as ev:
+        ev.set_costs(batch, [g.count("1") for g in batch])
+        # jobs == 1 evaluates in input order (the serial path is the reference's); the hint only orders the worker pull
+        ev.evaluate_all(batch)
+        assert started == batch
+    started.clear()
+    with H.Evaluator.from_callback(api, 4, record, jobs=2) as ev:
+        ev.set_costs(batch, [g.count("1") for g in batch])
+        outs = ev.evaluate_all(batch)
+        assert [o[1] for o in outs] == [1.0 + g.count("1") for g in batch]      # outcomes stay aligned with the input
+        assert set(started[:2]) == {"1111", "0111"}                             # the two dearest start first
+        assert started[-1] == "0000"
+
+
+def test_cost_hint_shortens_a_batch_with_one_slow_genome():
+    api = H.mine()
+
+    def run(hint):
+        def timed(g):
+            time.sleep(0.30 if g == "1111" else 0.05)
+            return (MEASURED, 1.0, 0.0)
+        batch = ["0001", "0010", "0100", "1000", "0011", "0110", "1111"]       # the slow one is last in input order
+        with H.Evaluator.from_callback(api, 4, timed, jobs=2) as ev:
+            if hint:
+                ev.set_costs(batch, [0.30 if g == "1111" else 0.05 for g in batch])
+            t0 = time.perf_counter()
+            ev.evaluate_all(batch)
+            return time.perf_counter() - t0
+    unhinted, hinted = run(False), run(True)
+    assert unhinted > 0.42          # 3 rounds of 0.05 on two workers, then 0.30 alone
+    assert hinted < 0.38            # 0.30 on one worker while the other takes the six short ones
+
+
+def test_predicted_cost_ranks_host_contraction_and_launch_trains_over_offload():
+    n = 1024
+    all_offloaded, cpu_matmul, cpu_small_nest, all_cpu = "101010101001", "101010100001", "101010001001", "0" * 12
+    k_train = "101010100011"                                                    # gene 10: one launch per (i, j)
+    c = {g: H.predicted_cost(g, n=n) for g in (all_offloaded, cpu_matmul, cpu_small_nest, all_cpu, k_train)}
+    assert c[all_offloaded] < c[cpu_small_nest] < c[cpu_matmul] <= c[all_cpu]
+    assert c[k_train] > 1000 * c[all_offloaded]                                 # N^2 launches dominate
+    assert H.predicted_cost("110000000000", n=n) == 0.0                         # infeasible: produced on the spot
+    assert H.predicted_cost(all_cpu, n=n, host_threads=8) < c[all_cpu]
+    assert H.predicted_cost(all_cpu, n=n, repetitions=3, warmup=1) == pytest.approx(4 * c[all_cpu])
+    assert H.predicted_cost(all_cpu, n=8192, timeout_s=1.0) == 1.0              # capped at the timeout
