@@ -107,12 +107,12 @@ typedef struct mmx_config {
   int32_t host_threads;     /* threads for CPU-mapped nests; 1 = the reference program         */
   int32_t launch_batching;  /* 1: inner-loop launch trains are submitted as CUDA graphs        */
   int32_t matmul_variant;   /* gene-8 kernel: 0 auto (FP64: below N = 1024 DMMA; from there the INT8 tensor cores whenever their 7-bit
-                             * slices give the error-free product -- 6 slices if that suffices, else 7; the application's inputs
-                             * always qualify -- and DMMA otherwise; FP32: tcgen05 split-TF32 with compensated
+                             * slices give the error-free product -- with the fewest slices that do, 2 .. 7, chosen on the device; the application's
+                             * inputs at N = 2^p qualify with 3 -- and DMMA otherwise; FP32: tcgen05 split-TF32 with compensated
                              * accumulation for N >= 1024, FFMA below); 1 first SIMT kernel; 2, 4-13 DMMA tile shapes (FP64);
                              * 20, 22 SIMT tile shapes; 30 FP32 tcgen05 at any N % 4 == 0; 31 its wide-tile uncompensated form;
                              * 40 FP64 on the tcgen05 INT8 tensor cores (7 exact 7-bit slices per operand, error <= 2e-14 K max|a| max|b|,
-                             * bit-identical on the application's inputs), 41 the same with 6 slices */
+                             * bit-identical on the application's inputs), 41 .. 45 the same with 6 .. 2 slices */
   int32_t warmup;           /* untimed runs per genome before the timed repetitions (default 0) */
 } mmx_config;
 
@@ -241,6 +241,11 @@ MMX_API int mmx_run_loop_rows(mmx_ctx* ctx, int slot, int gene, int row0, int ro
 /* Device address of a slot's array (n*n elements of the context dtype), so that a collective library
  * can exchange it in place (the all-gather of bt); valid until mmx_destroy. */
 MMX_API int mmx_device_ptr(mmx_ctx* ctx, int slot, int array, void** ptr_out);
+
+/* Which form the last FP64 auto-mode launch of gene 8 on this slot took (decided on the device from the operands, csrc/matmul_ozaki.cu):
+ * 2 .. 7 = INT8 tensor cores with that many exact 7-bit slices per operand (3 .. 28 slice products per term), 0 = the FP64
+ * pipe (the slices would not have been error-free), -1 = no such launch yet / not an FP64 auto-mode context.  Synchronises the slot. */
+MMX_API int mmx_gene8_form(mmx_ctx* ctx, int slot, int32_t* form_out);
 
 /* ---- row-sharded run across a group of GPUs (BASELINE.json config 5) -----------------
  * One individual (every nest offloaded) spread over `world` <= 8 members, one device slot each.  Member r

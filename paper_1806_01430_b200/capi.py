@@ -112,6 +112,7 @@ _SIGNATURES = {
     "mmx_run_loop": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "mmx_run_loop_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "mmx_device_ptr": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
+    "mmx_gene8_form": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int32)]),
     "mmx_shard_run_local": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int, C.POINTER(ShardStats), C.POINTER(C.c_double)]),
     "mmx_shard_export": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(ShardHandle)]),
     "mmx_shard_bind": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(ShardHandle), C.POINTER(C.c_int32)]),
@@ -280,6 +281,12 @@ class Context:
         s = C.c_double(0.0)
         self._check(self._lib.mmx_run_loop_rows(self._h, slot, gene, row0, rows, C.byref(s)))
         return s.value
+
+    def gene8_form(self, slot: int = 0) -> int:
+        """Form the last FP64 auto-mode gene-8 launch took: 2..7 INT8 slices, 0 the FP64 pipe, -1 not applicable."""
+        v = C.c_int32()
+        self._check(self._lib.mmx_gene8_form(self._h, slot, C.byref(v)))
+        return v.value
 
     def device_ptr(self, array: int, slot: int = 0) -> int:
         p = C.c_void_p()

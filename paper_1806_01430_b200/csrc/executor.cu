@@ -48,6 +48,7 @@ struct Slot {
   void* d_scrub = nullptr;
   std::size_t scrub_bytes = 0;
   void* d_scratch = nullptr;  // operands re-encoded for the tensor-core contractions (FP32: matmul_tc.cu; FP64: matmul_ozaki.cu)
+  bool gene8_form_valid = false;  // FP64 auto mode: the scratch carries the word mmx_gene8_form reads
   bool host_valid[MMX_NUM_ARRAYS] = {};
   bool dev_valid[MMX_NUM_ARRAYS] = {};
   bool host_diag_only = false;  // host c holds only its diagonal
@@ -582,7 +583,7 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
   if (cfg->n < 1 || cfg->n > 65536 || (cfg->dtype != MMX_F64 && cfg->dtype != MMX_F32) ||
       (cfg->numerics != MMX_NUMERICS_FAST && cfg->numerics != MMX_NUMERICS_STRICT) || !(cfg->timeout_s > 0.0) ||
       cfg->repetitions < 1 || cfg->num_slots < 1 || cfg->num_slots > 64 || cfg->host_threads < 1 || cfg->warmup < 0 ||
-      cfg->matmul_variant < 0 || cfg->matmul_variant > 41) {
+      cfg->matmul_variant < 0 || cfg->matmul_variant > 45) {
     g_create_error = "invalid configuration value";
     return MMX_E_INVALID;
   }
@@ -632,9 +633,13 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
       if ((e = cudaMalloc(&sl.d_scratch, matmul_3xtf32_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
     }
     if (cfg->dtype == MMX_F64 && cfg->numerics == MMX_NUMERICS_FAST && matmul_ozaki_usable(cfg->n) &&
-        (cfg->matmul_variant == 40 || cfg->matmul_variant == 41 || (cfg->matmul_variant == 0 && cfg->n >= kOzMinN))) {
+        ((cfg->matmul_variant >= 40 && cfg->matmul_variant <= 45) || (cfg->matmul_variant == 0 && cfg->n >= kOzMinN))) {
       if ((e = matmul_ozaki_prepare()) != cudaSuccess) return fail(e, "matmul_ozaki_prepare");
       if ((e = cudaMalloc(&sl.d_scratch, matmul_ozaki_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
+      if (cfg->matmul_variant == 0) {
+        if ((e = cudaMemset(matmul_ozaki_form_word(sl.d_scratch, cfg->n), 0xff, sizeof(int))) != cudaSuccess) return fail(e, "cudaMemset(form)");
+        sl.gene8_form_valid = true;
+      }
     }
     if ((e = cudaMalloc(&sl.d_sum, 16)) != cudaSuccess) return fail(e, "cudaMalloc(sum)");
     if ((e = cudaMalloc(reinterpret_cast<void**>(&sl.d_iter), sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(iter)");
@@ -804,6 +809,18 @@ MMX_API int mmx_device_ptr(mmx_ctx* ctx, int slot, int array, void** ptr_out) {
       array >= MMX_NUM_ARRAYS)
     return MMX_E_INVALID;
   *ptr_out = ctx->slots[slot]->d_arr[array];
+  return MMX_OK;
+}
+
+MMX_API int mmx_gene8_form(mmx_ctx* ctx, int slot, int32_t* form_out) {
+  if (ctx == nullptr || form_out == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size())) return MMX_E_INVALID;
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  *form_out = -1;
+  if (!s.gene8_form_valid) return MMX_OK;
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  MMX_CUDA(ctx, cudaStreamSynchronize(s.stream));
+  MMX_CUDA(ctx, cudaMemcpy(form_out, matmul_ozaki_form_word(s.d_scratch, ctx->cfg.n), sizeof(int32_t), cudaMemcpyDeviceToHost));
   return MMX_OK;
 }
 

@@ -82,17 +82,40 @@ constexpr int kOzMinN = 1024;
 // The guard: g[0] / g[3] != 0 when some element of a / of bt has bits below its 7th digit (or is not finite); g[1], g[2] =
 // highest non-zero digit (1-based) anywhere in a / in bt.  The S-slice contraction uses digits 1..S and keeps the digit pairs
 // with t + u <= S + 1, so it is error-free exactly when no element is cut, no digit beyond S is set and every non-zero pair
-// is kept.  Auto mode runs the cheapest error-free form: 6 slices, else 7 slices, else the FP64 pipe.
+// is kept.  Auto mode runs the cheapest error-free form: 2 .. 7 slices, else the FP64 pipe.
 #ifdef __CUDACC__
 __device__ __forceinline__ bool ozaki_guard_lossy(const int* g, int slices) {
   return (g[0] | g[3]) != 0 || g[1] > slices || g[2] > slices || g[1] + g[2] > slices + 1;
 }
 #endif
+// The cheapest error-free form for the operands the guard describes (g = {a cut, top digit of a, top digit of bt, bt cut}), as
+// OzPShape::CODE; 0 when none is (the FP64-pipe kernel runs).  Rectangular forms where both operands use at most four
+// digits; beyond that the triangular forms, which are error-free when every non-zero pair lies inside the triangle.
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int ozaki_pick_form(int cut, int top_a, int top_b) {
+  if (cut) return 0;
+  const int ta = top_a < 1 ? 1 : top_a, tb = top_b < 1 ? 1 : top_b;
+  if (ta <= 2 && tb <= 2) return 223;
+  if (ta <= 3 && tb <= 2) return 324;
+  if (ta <= 2 && tb <= 3) return 234;
+  if (ta <= 3 && tb <= 3) return 335;
+  if (ta <= 4 && tb <= 3) return 436;
+  if (ta <= 3 && tb <= 4) return 346;
+  if (ta <= 4 && tb <= 4) return 447;
+  for (int s = 5; s <= 7; ++s)
+    if (ta <= s && tb <= s && ta + tb <= s + 1) return s * 111;
+  return 0;
+}
+
 // OR-ed into `variant`: the rows [row0, row0 + rows) of a were already re-encoded into `scratch` by the previous launch_matmul
 // on it (the row-sharded run contracts the same rows of a against one column block after another)
 constexpr int kReuseOperandA = 0x1000;
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0,
                                 int cols, int slices, cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false);
+// device word in `scratch` where the auto launch records the form it ran: 2 .. 7 slices, 0 = left to the FP64 pipe
+int* matmul_ozaki_form_word(void* scratch, int n);
 // gene 9: row i of the same (GEMV against bt)
 template <typename T>
 cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, bool strict, cudaStream_t stream);

@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(32 * WM * WN, (WM * WN <= 4 && MT * NT <= 16) 
 matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const double* __restrict__ bt, int n,
                    int row0, int rows, int col0, int cols, int group, const int* __restrict__ run_if) {
   // guarded launch (FP64 auto mode): the tensor-core kernel took this contraction
-  if (run_if != nullptr && !ozaki_guard_lossy(run_if, 7)) return;
+  if (run_if != nullptr && ozaki_pick_form(run_if[0] | run_if[3], run_if[1], run_if[2]) != 0) return;  // the tensor-core launch took it
   constexpr int THREADS = 32 * WM * WN;
   constexpr int TM = WM * MT * 8, TN = WN * NT * 8;
   constexpr int DLD = DK + 4;  // padded row: (DK+4)*8 B = 32 mod 128 for DK in {16, 32} => conflict-free fragments
@@ -514,9 +514,8 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
   const bool reuse_a = (variant & kReuseOperandA) != 0;
   variant &= ~kReuseOperandA;
   // tensor cores (INT8 slice products, matmul_ozaki.cu): on request
-  if (!strict && scratch != nullptr && (variant == 40 || variant == 41))
-    return launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, variant == 41 ? 6 : 7, stream, nullptr,
-                               reuse_a && variant == 40);
+  if (!strict && scratch != nullptr && variant >= 40 && variant <= 45)  // 40 .. 45: 7 .. 2 slices
+    return launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 47 - variant, stream, nullptr, reuse_a);
   const bool dmma_ok = n % 2 == 0 && col0 % 2 == 0 && cols % 2 == 0;  // 16-byte aligned double2 accesses of c
   // auto: the INT8 tensor cores whenever their 7-bit slices reproduce every operand element exactly and every non-zero digit
   // pair is kept (then the result is the error-free product rounded once -- bit-identical to the CPU program on the

@@ -265,6 +265,457 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
   if constexpr (C > 1) cluster_sync_all();  // no CTA leaves while a peer may still signal its barriers
 }
 
+// ---- persistent form (the default): one CTA per SM walks the tiles of c in raster order ----------------------------------
+// What it adds over the kernel above:
+//  (1) Which digit pairs are multiplied is a template shape <SA, SB, LV, BN>: slices a_1..a_SA against b_1..b_SB, pairs kept
+//      up to level t + u <= LV + 1, on a 128 x BN tile.  <S, S, S, 64> is the triangular S-slice form of the header (a general
+//      kernel with its truncation bound: matmul_variant 40 .. 45).  <SA, SB, SA + SB - 1, BN> is the RECTANGULAR form: every
+//      pair of the first SA x SB digits, error-free iff a has no digit beyond SA and bt none beyond SB -- operands with few
+//      significant bits cost proportionally less (the application's carry log2(N) + 2 bits = two digits each up to N = 4096:
+//      4 slice products per FP64 term instead of 28).  With few levels the tile is 128 wide: each a_t meets [b_1 | b_2]
+//      stacked along N in ONE N = 256 instruction, the shape at which the operand reads (4 KB of a + 8 KB of b per 128 clocks)
+//      stay under the 128 B/clk of shared memory.
+//  (2) The form is a run-time choice inside ONE launch: the auto kernel reads the guard the slice pass wrote (anything cut?
+//      highest digit in use per operand) and runs the cheapest error-free form, or leaves at once (the FP64-pipe kernel then
+//      runs).  A launch that leaves retires 148 CTAs, not thousands.
+//  (3) The TMA producer runs ahead into the next tile while the epilogue drains, and where 2 * LV * BN <= 512 columns the level
+//      accumulators are double-buffered in TMEM, so the MMAs of tile i+1 overlap the epilogue of tile i entirely.
+// Slices arrive as one TMA box per slice and operand (the shared-memory layout is the one the 3-D box of the kernel above gives).
+// CR = 16-column chunks of c staged in shared memory (0: the epilogue reads and writes c from registers, one row per thread)
+template <int SA, int SB, int LV, int BN, int CR> struct OzPShape {
+  static_assert(BN == 64 || BN == 128, "tile width");
+  static_assert(LV * BN <= 512, "the level accumulators of a tile must fit TMEM");
+  static_assert(LV >= SA && LV >= SB && LV <= SA + SB - 1, "levels");
+  static constexpr int BK = 64;
+  static constexpr int A_SLICE = OZ_BM * BK, B_SLICE = BN * BK;
+  static constexpr int A_BYTES = SA * A_SLICE, B_BYTES = SB * B_SLICE;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int C_CHUNK = OZ_BM * 16 * 8;  // 128 rows x 16 doubles = one 128-byte-swizzled TMA box
+  static constexpr int C_BYTES = CR * C_CHUNK;
+  static constexpr int TAIL = 3584;               // barriers, column exponents and scale factors
+  static constexpr int STAGES_FIT = (227 * 1024 - 1024 - TAIL - C_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static_assert(STAGES >= 2, "stage ring");
+  static constexpr int NBUF = 2 * LV * BN <= 512 ? 2 : 1;  // accumulator sets in TMEM
+  static constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + C_BYTES + 1024 + TAIL;
+};
+constexpr int kOzPersistSmemMax = 227 * 1024;  // the auto kernel asks for all of it: each form uses what its rings need
+
+struct OzPArgs {
+  double* c;
+  const int *exp_a, *exp_b;
+  int n, kq, row0, rows, col0, cols, group;
+};
+
+// sum * 2^(ea + eb - 12).  Fast path (both exponents moderate): two multiplications by exact powers of two, pa = 2^(ea - 12)
+// and pb = 2^eb -- neither product leaves the normal range, so the result is the one ldexp gives.
+__device__ __forceinline__ double scaled_fast(double sum, int ea, double pa, bool row_fast, int eb, double pb) {
+  if (row_fast && eb > -400 && eb < 400) return (sum * pa) * pb;
+  return scaled(sum, ea, eb);
+}
+
+// CX x CY = CTAs per cluster working on CX x CY adjacent tiles: the a slices of a tile-row are fetched once per cluster row
+// (each of its CX CTAs loads 128 / CX rows of every slice and multicasts them), the bt slices of a column tile once per cluster
+// column.  The operand traffic is what bounds the short forms (the 2 x 2 form at 128 x 128 needs 32 KB per 512 tensor-pipe
+// clocks and SM: 8.3 TB/s measured against the 11.8 TB/s the L2 can put on the crossbar); a 2 x 2 cluster halves it.
+template <int SA, int SB, int LV, int BN, int CR, int CX, int CY>
+__device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensorMap* map_a, const CUtensorMap* map_b, const CUtensorMap* map_c,
+                                                unsigned char* smem_raw) {
+  using Sh = OzPShape<SA, SB, LV, BN, CR>;
+  constexpr int C = CX * CY;
+  const unsigned rank = C > 1 ? cluster_ctarank() : 0u;
+  const int rx = static_cast<int>(rank) % CX, ry = static_cast<int>(rank) / CX;
+  constexpr unsigned short kMaskAll = static_cast<unsigned short>((1u << C) - 1u);
+  const unsigned short mask_row = static_cast<unsigned short>(((1u << CX) - 1u) << (ry * CX));          // the CTAs that share my a slices
+  const unsigned short mask_col = static_cast<unsigned short>((CY > 1 ? (1u | (1u << CX)) : 1u) << rx);  // ... my bt slices
+  constexpr int STAGES = Sh::STAGES, NBUF = Sh::NBUF, BK = Sh::BK;
+  constexpr int PER_MMA = 256 / BN;  // b slices one instruction can take (N <= 256)
+  const unsigned raw = smem_u32(smem_raw);
+  const unsigned base = (raw + 1023u) & ~1023u;
+  const unsigned cbuf = base + STAGES * Sh::STAGE_BYTES;  // CR chunk buffers of c (1024-byte aligned: every stage is a multiple)
+  const unsigned bars = cbuf + Sh::C_BYTES;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (8 + s); };
+  auto acc_full = [&](int b) { return bars + 8u * (16 + b); };   // the MMAs of a tile have completed into set b
+  auto acc_empty = [&](int b) { return bars + 8u * (18 + b); };  // the epilogue has read set b
+  auto c_full = [&](int b) { return bars + 8u * (20 + b); };     // chunk buffer b holds the incoming c values
+  const unsigned tmem_slot = bars + 8u * 24;
+  volatile unsigned* tmem_slot_ptr = reinterpret_cast<volatile unsigned*>(smem_raw + (tmem_slot - raw));
+  int* eb_sh = reinterpret_cast<int*>(smem_raw + (bars + 256 - raw));            // [2][BN] column exponents, alternating per tile
+  double* pb_sh = reinterpret_cast<double*>(smem_raw + (bars + 256 + 1024 - raw));  // [2][BN] 2^exponent (clamped) of the same
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // the cluster walks super-tiles of CX x CY tiles in raster order; CTA (rx, ry) takes its tile of each (a tile beyond the
+  // edge is computed on zero-filled operands and never stored: its peers need this CTA's share of the loads)
+  const int super_x = ((g.cols + BN - 1) / BN + CX - 1) / CX, super_y = ((g.rows + OZ_BM - 1) / OZ_BM + CY - 1) / CY;
+  const int supers = super_x * super_y;
+  const int first = static_cast<int>(blockIdx.x) / C, stride = static_cast<int>(gridDim.x) / C;
+  const int my_tiles = first < supers ? (supers - 1 - first) / stride + 1 : 0;
+  const int group = g.group / CY > 0 ? g.group / CY : 1;
+  auto tile_at = [&](int k, int& bx, int& by) {  // the k-th tile of this CTA
+    int sx, sy;
+    raster_map(group, super_x, super_y, first + k * stride, sx, sy);
+    bx = sx * CX + rx;
+    by = sy * CY + ry;
+  };
+  const int k_stages = g.kq / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 1);
+      mbar_init(empty_bar(s), C);  // the MMAs of every CTA of the cluster have left the stage (what lands in it comes from peers too)
+    }
+    for (int b = 0; b < NBUF; ++b) {
+      mbar_init(acc_full(b), 1);
+      mbar_init(acc_empty(b), 4);  // one arrival per epilogue warp
+    }
+    for (int b = 0; b < CR; ++b) mbar_init(c_full(b), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tmem_slot), "n"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  if constexpr (C > 1) cluster_sync_all();  // peers' barriers are initialised before anything is multicast at them
+  tc_fence_after();
+  const unsigned tmem_base = *tmem_slot_ptr;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;  // stages filled so far, over all tiles of this CTA
+      for (int tile = 0; tile < my_tiles; ++tile) {
+        int bx, by;
+        tile_at(tile, bx, by);
+        const int m_base = g.row0 + by * OZ_BM, n_rel = bx * BN;
+        for (int kb = 0; kb < k_stages; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
+          const unsigned st = base + s * Sh::STAGE_BYTES;
+          mbar_expect_tx(full_bar(s), Sh::STAGE_BYTES);
+          if constexpr (C == 1) {
+#pragma unroll
+            for (int t = 0; t < SA; ++t) tma_load_3d(st + t * Sh::A_SLICE, map_a, kb * BK, m_base, t, full_bar(s));
+#pragma unroll
+            for (int t = 0; t < SB; ++t) tma_load_3d(st + Sh::A_BYTES + t * Sh::B_SLICE, map_b, kb * BK, n_rel, t, full_bar(s));
+          } else {
+            constexpr int PA = OZ_BM / CX, PB = BN / CY;  // rows of every slice this CTA fetches for its cluster row / column
+#pragma unroll
+            for (int t = 0; t < SA; ++t)
+              tma_load_3d_mc(st + t * Sh::A_SLICE + rx * (PA * BK), map_a, kb * BK, m_base + rx * PA, t, full_bar(s), mask_row);
+#pragma unroll
+            for (int t = 0; t < SB; ++t)
+              tma_load_3d_mc(st + Sh::A_BYTES + t * Sh::B_SLICE + ry * (PB * BK), map_b, kb * BK, n_rel + ry * PB, t, full_bar(s), mask_col);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = 0; tile < my_tiles; ++tile) {
+        const int buf = tile % NBUF;
+        mbar_wait(acc_empty(buf), ((tile / NBUF) & 1) ^ 1);
+        tc_fence_after();
+        const unsigned acc = tmem_base + buf * (LV * BN);
+        for (int kb = 0; kb < k_stages; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(full_bar(s), (it / STAGES) & 1);
+          tc_fence_after();
+          const unsigned st = base + s * Sh::STAGE_BYTES;
+#pragma unroll
+          for (int ks = 0; ks < BK / 32; ++ks) {
+            const unsigned long long adv = 2ull * ks;  // 32 bytes along K inside the 64-byte swizzle row
+#pragma unroll
+            for (int t = 1; t <= SA; ++t) {
+              const unsigned long long a_t = umma_desc_sw<BK>(st + (t - 1) * Sh::A_SLICE) + adv;
+              // slices b_1 .. b_count pair with a_t: levels t+1 .. t+count = TMEM column blocks t-1 .. t+count-2
+              constexpr int kAll = SB;
+              const int count = kAll < LV + 1 - t ? kAll : LV + 1 - t;
+#pragma unroll
+              for (int u0 = 0; u0 < count; u0 += PER_MMA) {
+                const int nsl = count - u0 < PER_MMA ? count - u0 : PER_MMA;
+                const unsigned long long b_u = umma_desc_sw<BK>(st + Sh::A_BYTES + u0 * Sh::B_SLICE) + adv;
+                // a block is initialised by the first product that lands on it in the tile's first k step: a_1 opens blocks
+                // 0 .. SB-1, every further a_t the one block (t + SB - 2) nobody before it reached
+                unsigned accumulate = 1;
+                if (kb == 0 && ks == 0) {
+                  if (t == 1) {
+                    accumulate = 0;
+                  } else if (u0 + nsl == count && count == SB) {
+                    // the last block of this instruction is new; the others are not: issue that slice on its own
+                    if (nsl > 1) {
+                      tc_mma_i8(acc + (t - 1 + u0) * BN, a_t, b_u, idesc_i8((nsl - 1) * BN), 1);
+                    }
+                    const unsigned long long b_last = umma_desc_sw<BK>(st + Sh::A_BYTES + (count - 1) * Sh::B_SLICE) + adv;
+                    tc_mma_i8(acc + (t - 1 + count - 1) * BN, a_t, b_last, idesc_i8(BN), 0);
+                    continue;
+                  }
+                }
+                tc_mma_i8(acc + (t - 1 + u0) * BN, a_t, b_u, idesc_i8(nsl * BN), accumulate);
+              }
+            }
+          }
+          if constexpr (C == 1) tc_commit(empty_bar(s));
+          else tc_commit_mc(empty_bar(s), kMaskAll);
+        }
+        tc_commit(acc_full(buf));
+      }
+    }
+  } else {
+    // epilogue warps: thread = one row of the tile (TMEM lane)
+    const int q = warp % 4;
+    const int r = q * 32 + lane;  // row inside the tile
+    const int m_limit = g.row0 + g.rows;
+    int tile = 0;
+    if constexpr (CR > 0) {
+      // c travels by TMA through shared memory in chunks of 16 columns (128 rows x 128 bytes, SWIZZLE_128B): a ring of CR
+      // chunk buffers is filled ahead (the first ones before the tile's MMAs have finished), each thread adds its row's 16
+      // results in place (16-byte accesses, conflict-free under the swizzle), and the chunk goes back with one TMA store --
+      // global memory sees full 128-byte lines instead of one 16-byte piece per thread and row.  The tensor map of c ends
+      // at (row0 + rows, col0 + cols): loads beyond it read zeros and stores beyond it are dropped, which is all the edge
+      // handling there is.
+      constexpr int NCH = BN / 16;
+      const int total_chunks = my_tiles * NCH;
+      const bool elected = threadIdx.x == 64;
+      auto load_chunk = [&](int J) {  // elected thread only
+        int bx, by;
+        tile_at(J / NCH, bx, by);
+        const int b = J % CR;
+        mbar_expect_tx(c_full(b), Sh::C_CHUNK);
+        tma_load_2d(cbuf + b * Sh::C_CHUNK, map_c, g.col0 + bx * BN + (J % NCH) * 16, g.row0 + by * OZ_BM, c_full(b));
+      };
+      if (elected)
+        for (int J = 0; J < CR - 1 && J < total_chunks; ++J) load_chunk(J);
+      int J = 0;
+      for (; tile < my_tiles; ++tile) {
+        int bx, by;
+        tile_at(tile, bx, by);
+        const int m_base = g.row0 + by * OZ_BM, n_tile = bx * BN;
+        const int buf = tile % NBUF;
+        const int m = m_base + r;
+        const int ei = m < m_limit ? g.exp_a[m] : 0;  // kNonFinite marks a row that holds an Inf or a NaN
+        const bool row_fast = ei > -400 && ei < 400;
+        const double pa = pow2(row_fast ? ei - 12 : 0);
+        int* eb = eb_sh + (tile & 1) * BN;
+        double* pb = pb_sh + (tile & 1) * BN;
+        if (r < BN) {
+          const int e = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
+          eb[r] = e;
+          pb[r] = pow2(e > -400 && e < 400 ? e : 0);
+        }
+        // the exponents of this tile are complete; nobody is still reading the other copy (that was two tiles ago, and
+        // everyone has passed the barrier of the tile in between)
+        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        mbar_wait(acc_full(buf), (tile / NBUF) & 1);
+        tc_fence_after();
+        const unsigned t0 = tmem_base + (static_cast<unsigned>(q * 32) << 16) + buf * (LV * BN);
+#pragma unroll 1
+        for (int j = 0; j < NCH; ++j, ++J) {
+          unsigned lv[LV][16];
+#pragma unroll
+          for (int l = 0; l < LV; ++l) tc_ld16_issue(t0 + l * BN + j * 16, lv[l]);
+          tc_ld_wait();
+          if (j == NCH - 1) {  // every level of this set has been read: the MMAs of a later tile may overwrite it
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(acc_empty(buf));
+          }
+          double v[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const int ebj = eb[j * 16 + e];
+            if constexpr (LV <= 4) {
+              // the level sum as ONE integer (|L| < 2^31 and three shifts of 7 bits: exact in 64 bits and in a double), scaled
+              // by adding to the exponent field: two FP64-pipe operations per element (conversion, the addition into c)
+              // instead of eight -- with one warp per scheduler the epilogue runs at the latency of its FP64 chain
+              long long acc = static_cast<int>(lv[0][e]);
+#pragma unroll
+              for (int l = 1; l < LV; ++l) acc = (acc << 7) + static_cast<int>(lv[l][e]);
+              const double d = static_cast<double>(acc);
+              if (row_fast && static_cast<unsigned>(ebj + 399) < 799u) {
+                long long bits = __double_as_longlong(d);
+                if (acc != 0) bits += static_cast<long long>(ei + ebj - 12 - 7 * (LV - 1)) << 52;  // stays a normal number
+                v[e] = __longlong_as_double(bits);
+              } else {
+                v[e] = scaled(d * pow2(-7 * (LV - 1)), ei, ebj);
+              }
+            } else {
+              double sum = static_cast<double>(static_cast<int>(lv[LV - 1][e]));
+#pragma unroll
+              for (int l = LV - 2; l >= 0; --l) sum = fma(sum, 0.0078125, static_cast<double>(static_cast<int>(lv[l][e])));
+              v[e] = scaled_fast(sum, ei, pa, row_fast, ebj, pb[j * 16 + e]);
+            }
+          }
+          const int b = J % CR;
+          mbar_wait(c_full(b), (J / CR) & 1);
+          const unsigned crow = cbuf + b * Sh::C_CHUNK + r * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch) {
+            const unsigned cell = crow + ((ch ^ (r & 7)) << 4);
+            double x0, x1;
+            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x0), "=d"(x1) : "r"(cell) : "memory");
+            x0 += v[2 * ch];
+            x1 += v[2 * ch + 1];
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(cell), "d"(x0), "d"(x1) : "memory");
+          }
+          fence_proxy_async_smem();
+          asm volatile("bar.sync 1, 128;\n" ::: "memory");
+          if (elected) {
+            tma_store_2d(map_c, cbuf + b * Sh::C_CHUNK, g.col0 + n_tile + j * 16, m_base);
+            tma_store_commit();
+            const int Jn = J + CR - 1;  // goes into the buffer of chunk J - 1: its store has to have left shared memory
+            if (Jn < total_chunks) {
+              tma_store_wait_read<1>();
+              load_chunk(Jn);
+            }
+          }
+        }
+      }
+      if (elected) tma_store_wait<0>();
+    } else {
+      // c straight from registers (any n, odd ones included): 64 columns at a time; the first 64 incoming values and the
+      // tile's column exponents are fetched before the tile's MMAs are waited for
+      const bool vec_ok = (g.n % 2 == 0) && (g.col0 % 2 == 0);
+      for (; tile < my_tiles; ++tile) {
+        int bx, by;
+        tile_at(tile, bx, by);
+        const int m_base = g.row0 + by * OZ_BM, n_tile = bx * BN;
+        const int buf = tile % NBUF;
+        const int m = m_base + r;
+        const bool row_ok = m < m_limit;
+        const int ei = row_ok ? g.exp_a[m] : 0;  // kNonFinite marks a row that holds an Inf or a NaN
+        const bool row_fast = ei > -400 && ei < 400;
+        const double pa = pow2(row_fast ? ei - 12 : 0);
+        double* crow = g.c + static_cast<size_t>(row_ok ? m : 0) * g.n;
+        int* eb = eb_sh + (tile & 1) * BN;
+        double* pb = pb_sh + (tile & 1) * BN;
+        if (r < BN) {
+          const int e = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
+          eb[r] = e;
+          pb[r] = pow2(e > -400 && e < 400 ? e : 0);
+        }
+#pragma unroll 1
+        for (int half = 0; half < BN / 64; ++half) {
+          const int n_rel = n_tile + half * 64;
+          double cpre[64];
+#pragma unroll
+          for (int e = 0; e < 64; e += 2) {
+            const int jr = n_rel + e;
+            if (row_ok && vec_ok && jr + 2 <= g.cols) {
+              const double2 x = *reinterpret_cast<const double2*>(crow + g.col0 + jr);
+              cpre[e] = x.x;
+              cpre[e + 1] = x.y;
+            } else {
+              cpre[e] = (row_ok && jr < g.cols) ? crow[g.col0 + jr] : 0.0;
+              cpre[e + 1] = (row_ok && jr + 1 < g.cols) ? crow[g.col0 + jr + 1] : 0.0;
+            }
+          }
+          if (half == 0) {
+            asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the exponents of this tile are complete (see above)
+            mbar_wait(acc_full(buf), (tile / NBUF) & 1);
+            tc_fence_after();
+          }
+          const unsigned t0 = tmem_base + (static_cast<unsigned>(q * 32) << 16) + buf * (LV * BN) + half * 64;
+#pragma unroll
+          for (int cb = 0; cb < 8; ++cb) {
+            unsigned lv[LV][8];
+#pragma unroll
+            for (int l = 0; l < LV; ++l) tc_ld8_issue(t0 + l * BN + cb * 8, lv[l]);
+            tc_ld_wait();
+            if (cb == 7 && half == BN / 64 - 1) {  // every level of this set is in registers
+              tc_fence_before();
+              __syncwarp();
+              if (lane == 0) mbar_arrive(acc_empty(buf));
+            }
+#pragma unroll
+            for (int e = 0; e < 8; e += 2) {
+              const int jr = n_rel + cb * 8 + e;  // relative to col0
+              double v[2];
+#pragma unroll
+              for (int h = 0; h < 2; ++h) {
+                double sum = static_cast<double>(static_cast<int>(lv[LV - 1][e + h]));
+#pragma unroll
+                for (int l = LV - 2; l >= 0; --l) sum = fma(sum, 0.0078125, static_cast<double>(static_cast<int>(lv[l][e + h])));
+                const int col = half * 64 + cb * 8 + e + h;
+                v[h] = cpre[cb * 8 + e + h] + scaled_fast(sum, ei, pa, row_fast, eb[col], pb[col]);
+              }
+              if (!row_ok) continue;
+              const int j = g.col0 + jr;
+              if (vec_ok && jr + 2 <= g.cols) {
+                *reinterpret_cast<double2*>(crow + j) = make_double2(v[0], v[1]);
+              } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h)
+                  if (jr + h < g.cols) crow[j + h] = v[h];
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(512) : "memory");
+  }
+  if constexpr (C > 1) cluster_sync_all();  // no CTA leaves while a peer may still multicast into it or signal its barriers
+}
+
+// the tensor maps a launch may need: slices of a in boxes of 128 / 64 rows, slices of bt in boxes of 128 / 64 / 32 rows (whole
+// tiles, or the share one CTA of a cluster fetches), c
+struct OzMaps {
+  CUtensorMap a128, a64, b128, b64, b32, c;
+};
+template <int ROWS> __device__ __forceinline__ const CUtensorMap* oz_map_a(const OzMaps& m) {
+  static_assert(ROWS == 128 || ROWS == 64, "a box");
+  return ROWS == 128 ? &m.a128 : &m.a64;
+}
+template <int ROWS> __device__ __forceinline__ const CUtensorMap* oz_map_b(const OzMaps& m) {
+  static_assert(ROWS == 128 || ROWS == 64 || ROWS == 32, "bt box");
+  return ROWS == 128 ? &m.b128 : ROWS == 64 ? &m.b64 : &m.b32;
+}
+template <int SA, int SB, int LV, int BN, int CR, int CX, int CY>
+__device__ __forceinline__ void oz_persist_form(const OzPArgs& g, const OzMaps& m, unsigned char* smem_raw) {
+  oz_persist_body<SA, SB, LV, BN, CR, CX, CY>(g, oz_map_a<OZ_BM / CX>(m), oz_map_b<BN / CY>(m), &m.c, smem_raw);
+}
+
+// auto mode: the cheapest error-free form, decided on the device (n is even here: c goes through TMA).  Launched as clusters of
+// CX x CY CTAs, which the rectangular forms use to share operand loads; the triangular ones run every CTA on its own.
+template <int CX, int CY>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+matmul_ozaki_auto_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, const int* __restrict__ guard, int* __restrict__ ran) {
+  extern __shared__ unsigned char smem_raw[];
+  const int form = ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ran = form;
+  switch (form) {
+    case 223: oz_persist_form<2, 2, 3, 128, 2, CX, CY>(g, maps, smem_raw); break;
+    case 324: oz_persist_form<3, 2, 4, 128, 2, CX, CY>(g, maps, smem_raw); break;
+    case 234: oz_persist_form<2, 3, 4, 128, 2, CX, CY>(g, maps, smem_raw); break;
+    case 335: oz_persist_form<3, 3, 5, 64, 4, CX, CY>(g, maps, smem_raw); break;
+    case 436: oz_persist_form<4, 3, 6, 64, 4, CX, CY>(g, maps, smem_raw); break;
+    case 346: oz_persist_form<3, 4, 6, 64, 4, CX, CY>(g, maps, smem_raw); break;
+    case 447: oz_persist_form<4, 4, 7, 64, 4, CX, CY>(g, maps, smem_raw); break;
+    case 555: oz_persist_form<5, 5, 5, 64, 2, 1, 1>(g, maps, smem_raw); break;
+    case 666: oz_persist_form<6, 6, 6, 64, 0, 1, 1>(g, maps, smem_raw); break;
+    case 777: oz_persist_form<7, 7, 7, 64, 0, 1, 1>(g, maps, smem_raw); break;
+    default: break;  // not error-free in any form: not this kernel's launch
+  }
+}
+
+// a fixed triangular slice count (matmul_variant 40 .. 45: general kernels with a truncation bound, no guard); CR = 0 where c
+// cannot go through TMA (odd n) or the stage ring needs the space
+template <int S, int CR>
+__global__ void __launch_bounds__(OZ_THREADS, 1)
+matmul_ozaki_fixed_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps) {
+  extern __shared__ unsigned char smem_raw[];
+  oz_persist_form<S, S, S, 64, CR, 1, 1>(g, maps, smem_raw);
+}
+
 // One CTA per row: row maximum -> exponent e (|x| < 2^e), then S digits per element.  dst plane t of row r (relative
 // index) is dst + t * plane + r * kq; k >= n is zero.  Rows [src_row0, src_row0 + nrows) of src; rows up to nrows_pad are
 // written as zeros with exponent 0 (tile overhang inside the tensor map).
@@ -477,6 +928,186 @@ cudaError_t oz_contract(double* c, void* scratch, int planes, int n, int row0, i
                             static_cast<const int*>(guarded ? L.guard : nullptr));
 }
 
+// ---- persistent form: host side ------------------------------------------------------------------------------------------
+int oz_sm_count() {
+  static PerDeviceOnce once;
+  static int count[64] = {};
+  int d = 0;
+  cudaGetDevice(&d);
+  bool& known = once.here();
+  if (!known) {
+    if (cudaDeviceGetAttribute(&count[d & 63], cudaDevAttrMultiProcessorCount, d) != cudaSuccess || count[d & 63] <= 0) count[d & 63] = 148;
+    known = true;
+  }
+  return count[d & 63];
+}
+
+template <typename Kernel>
+cudaError_t oz_persist_configure(Kernel kernel, int smem, PerDeviceOnce& once) {
+  bool& configured = once.here();
+  if (!configured) {
+    if (cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem); e != cudaSuccess) return e;
+    configured = true;
+  }
+  return cudaSuccess;
+}
+template <int CX, int CY> cudaError_t oz_auto_configure() {
+  static PerDeviceOnce once;
+  return oz_persist_configure(matmul_ozaki_auto_kernel<CX, CY>, kOzPersistSmemMax, once);
+}
+
+// clusters of CX x CY CTAs the device can keep resident with one CTA per SM (0 on failure)
+template <int CX, int CY> int oz_auto_max_clusters() {
+  if (oz_auto_configure<CX, CY>() != cudaSuccess) return 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(static_cast<unsigned>(oz_sm_count() / (CX * CY) * (CX * CY)));
+  cfg.blockDim = dim3(OZ_THREADS);
+  cfg.dynamicSmemBytes = kOzPersistSmemMax;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = CX * CY;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  int clusters = 0;
+  if (cudaOccupancyMaxActiveClusters(&clusters, matmul_ozaki_auto_kernel<CX, CY>, &cfg) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return 0;
+  }
+  return clusters;
+}
+
+// The cluster shape of the auto launch on this device: 2 x 2 when (nearly) every SM can sit in such a cluster, else 2 x 1, else
+// none.  {shape code 22 / 21 / 11, resident clusters}.  MMX_OZ_CLUSTER_SHAPE forces a shape (measurement).
+struct OzClusterChoice {
+  int shape = 0, clusters = 0;
+};
+OzClusterChoice oz_auto_cluster_choice() {
+  static PerDeviceOnce once;
+  static OzClusterChoice choice[64];
+  int d = 0;
+  cudaGetDevice(&d);
+  bool& known = once.here();
+  if (!known) {
+    static const int forced = [] { const char* e = getenv("MMX_OZ_CLUSTER_SHAPE"); return e ? atoi(e) : 0; }();
+    const int sms = oz_sm_count();
+    OzClusterChoice c;
+    const int n22 = (forced == 0 || forced == 22) ? oz_auto_max_clusters<2, 2>() : 0;
+    if (n22 > 0 && (forced == 22 || 4 * n22 >= sms - 8)) {
+      c.shape = 22;
+      c.clusters = n22;
+    } else {
+      const int n21 = (forced == 0 || forced == 21) ? oz_auto_max_clusters<2, 1>() : 0;
+      if (n21 > 0 && (forced == 21 || 2 * n21 >= sms - 4)) {
+        c.shape = 21;
+        c.clusters = n21;
+      } else {
+        c.shape = 11;
+        c.clusters = sms;
+      }
+    }
+    choice[d & 63] = c;
+    known = true;
+  }
+  return choice[d & 63];
+}
+
+template <int S, int CR> cudaError_t oz_fixed_configure() {
+  static PerDeviceOnce once;
+  return oz_persist_configure(matmul_ozaki_fixed_kernel<S, CR>, OzPShape<S, S, S, 64, CR>::SMEM_BYTES, once);
+}
+constexpr int oz_fixed_ring(int s) { return s <= 4 ? 4 : 0;  /* chunk buffers of c where the stage ring leaves room */ }
+
+// c as a 2-D tensor of doubles that ends at (rows_end, cols_end): box = 128 rows x 16 columns, 128-byte swizzle
+bool make_c_map(CUtensorMap* map, double* c, int n, int rows_end, int cols_end) {
+  EncodeTiledFn enc = encode_tiled();
+  if (enc == nullptr) return false;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols_end), static_cast<cuuint64_t>(rows_end)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n) * sizeof(double)};
+  const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(OZ_BM)};
+  const cuuint32_t elem[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, c, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// slices == 0: the auto kernel (reads the guard, records the form it ran in guard[4]); otherwise the fixed triangular form over
+// the first `slices` of `planes` planes
+cudaError_t oz_persist_contract(double* c, void* scratch, int planes, int slices, int n, int row0, int rows, int col0, int cols, cudaStream_t stream) {
+  const OzLayout L(scratch, n, planes);
+  const bool c_by_tma = n % 2 == 0;  // row pitch a multiple of 16 bytes
+  if (slices == 0 && !c_by_tma) return cudaErrorInvalidValue;
+  OzMaps maps;
+  if (!make_slice_map(&maps.a128, L.sa, static_cast<size_t>(n), L.kq, 64, 128, planes, 1) ||
+      !make_slice_map(&maps.a64, L.sa, static_cast<size_t>(n), L.kq, 64, 64, planes, 1) ||
+      !make_slice_map(&maps.b128, L.sb, L.b_rows, L.kq, 64, 128, planes, 1) || !make_slice_map(&maps.b64, L.sb, L.b_rows, L.kq, 64, 64, planes, 1) ||
+      !make_slice_map(&maps.b32, L.sb, L.b_rows, L.kq, 64, 32, planes, 1))
+    return cudaErrorNotSupported;
+  if (c_by_tma) {
+    if (!make_c_map(&maps.c, c, n, row0 + rows, col0 + cols)) return cudaErrorNotSupported;
+  } else {
+    maps.c = maps.a128;  // never dereferenced
+  }
+  OzPArgs g;
+  g.c = c;
+  g.exp_a = L.ea;
+  g.exp_b = L.eb;
+  g.n = n;
+  g.kq = L.kq;
+  g.row0 = row0;
+  g.rows = rows;
+  g.col0 = col0;
+  g.cols = cols;
+  g.group = raster_group(OZ_BM, static_cast<size_t>(L.kq));
+  // the grid covers the 64-wide tiling (the forms with 128-wide tiles leave the surplus CTAs without a tile)
+  const int tiles_x = (cols + 63) / 64, tiles_y = (rows + OZ_BM - 1) / OZ_BM;
+  const dim3 grid(static_cast<unsigned>(std::min(tiles_x * tiles_y, oz_sm_count())));
+  switch (slices) {
+    case 0: {
+      const OzClusterChoice cc = oz_auto_cluster_choice();
+      const int cx = cc.shape / 10, cy = cc.shape % 10;
+      const int supers = ((tiles_x + cx - 1) / cx) * ((tiles_y + cy - 1) / cy);
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(std::min(supers, cc.clusters) * cx * cy));
+      cfg.blockDim = dim3(OZ_THREADS);
+      cfg.dynamicSmemBytes = kOzPersistSmemMax;
+      cfg.stream = stream;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = static_cast<unsigned>(cx * cy);
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = cx * cy > 1 ? 1 : 0;
+      const int* guard = L.guard;
+      int* ran = L.guard + 4;
+      if (cc.shape == 22) return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_kernel<2, 2>, g, maps, guard, ran);
+      if (cc.shape == 21) return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_kernel<2, 1>, g, maps, guard, ran);
+      if (cudaError_t e = oz_auto_configure<1, 1>(); e != cudaSuccess) return e;
+      return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_kernel<1, 1>, g, maps, guard, ran);
+    }
+#define MMX_OZ_FIXED(S)                                                                                                                       \
+  case S:                                                                                                                                     \
+    if (c_by_tma && oz_fixed_ring(S) > 0) {                                                                                                   \
+      if (cudaError_t e = oz_fixed_configure<S, oz_fixed_ring(S)>(); e != cudaSuccess) return e;                                              \
+      matmul_ozaki_fixed_kernel<S, oz_fixed_ring(S)><<<grid, OZ_THREADS, OzPShape<S, S, S, 64, oz_fixed_ring(S)>::SMEM_BYTES, stream>>>(g, maps); \
+    } else {                                                                                                                                  \
+      if (cudaError_t e = oz_fixed_configure<S, 0>(); e != cudaSuccess) return e;                                                             \
+      matmul_ozaki_fixed_kernel<S, 0><<<grid, OZ_THREADS, OzPShape<S, S, S, 64, 0>::SMEM_BYTES, stream>>>(g, maps);           \
+    }                                                                                                                                         \
+    break;
+      MMX_OZ_FIXED(2)
+      MMX_OZ_FIXED(3)
+      MMX_OZ_FIXED(4)
+      MMX_OZ_FIXED(5)
+      MMX_OZ_FIXED(6)
+      MMX_OZ_FIXED(7)
+#undef MMX_OZ_FIXED
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 // slices + contraction with S planes (the explicit variants)
 template <int S, int C, int BK>
 cudaError_t oz_go(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
@@ -496,7 +1127,17 @@ cudaError_t matmul_ozaki_prepare() {
   if (cudaError_t e = oz_configure<7, 1, 64>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_configure<7, 2, 64>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_configure<7, 4, 64>(); e != cudaSuccess) return e;
-  return oz_configure<6, 1, 64>();
+  if (cudaError_t e = oz_configure<6, 1, 64>(); e != cudaSuccess) return e;
+  (void)oz_auto_cluster_choice();  // configures the auto kernel of the chosen cluster shape
+  if (cudaError_t e = oz_fixed_configure<2, 0>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_fixed_configure<3, 0>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_fixed_configure<4, 0>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_fixed_configure<2, 4>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_fixed_configure<3, 4>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_fixed_configure<4, 4>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_fixed_configure<5, 0>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_fixed_configure<6, 0>(); e != cudaSuccess) return e;
+  return oz_fixed_configure<7, 0>();
 }
 
 size_t matmul_ozaki_scratch_bytes(int n) {
@@ -504,27 +1145,47 @@ size_t matmul_ozaki_scratch_bytes(int n) {
   return 7 * (static_cast<size_t>(n) + oz_rows_pad(n, OZ_BN)) * kq + 2 * (static_cast<size_t>(n) + OZ_BN) * sizeof(int) + 256;  // + the guard flag
 }
 
+int* matmul_ozaki_form_word(void* scratch, int n) { return scratch == nullptr ? nullptr : OzLayout(scratch, n, 7).guard + 4; }
+
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
                                 int slices, cudaStream_t stream, int** guard_out, bool reuse_a) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr) return cudaErrorInvalidValue;
+  // MMX_OZ_LEGACY=1: the one-tile-per-CTA kernels of the first version (A/B comparison, tools/ozaki_cluster_sweep.sh)
+  static const int legacy = [] { const char* e = getenv("MMX_OZ_LEGACY"); return e ? atoi(e) : 0; }();
   if (guard_out != nullptr) {
-    // auto mode: 7 digit planes and the guard once, then the 6-slice and the 7-slice contraction, each guarded; the caller
-    // adds the FP64-pipe kernel under the remaining condition
+    // auto mode: 7 digit planes and the guard once, then ONE persistent launch that reads the guard and runs the cheapest
+    // error-free form (2 .. 7 slices) or nothing; the caller adds the FP64-pipe kernel under the remaining condition
     *guard_out = OzLayout(scratch, n, 7).guard;
     if (cudaError_t e = oz_slices<7>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a); e != cudaSuccess) return e;
+    if (!legacy) return oz_persist_contract(c, scratch, 7, 0, n, row0, rows, col0, cols, stream);
     if (cudaError_t e = oz_contract<6, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true); e != cudaSuccess) return e;
     return oz_contract<7, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true);
   }
-  if (reuse_a) return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream, true);
-  // tuning hooks (tools/ozaki_cluster_sweep.sh): CTAs per cluster sharing the a slices by multicast, k bytes per stage
-  static const int cluster = [] { const char* e = getenv("MMX_OZ_CLUSTER"); return e ? atoi(e) : 1; }();
-  static const int bk = [] { const char* e = getenv("MMX_OZ_BK"); return e ? atoi(e) : 64; }();
-  if (slices == 6) return oz_go<6, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
-  if (cluster == 4) return oz_go<7, 4, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
-  if (cluster == 2) return oz_go<7, 2, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
-  if (bk == 32) return oz_go<7, 1, 32>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
-  return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+  if (legacy) {
+    if (reuse_a) return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream, true);
+    // tuning hooks: CTAs per cluster sharing the a slices by multicast, k bytes per stage
+    static const int cluster = [] { const char* e = getenv("MMX_OZ_CLUSTER"); return e ? atoi(e) : 1; }();
+    static const int bk = [] { const char* e = getenv("MMX_OZ_BK"); return e ? atoi(e) : 64; }();
+    if (slices == 6) return oz_go<6, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+    if (cluster == 4) return oz_go<7, 4, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+    if (cluster == 2) return oz_go<7, 2, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+    if (bk == 32) return oz_go<7, 1, 32>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+    return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
+  }
+  // a fixed slice count: S planes are written and contracted (a general kernel with the truncation bound of the header)
+  cudaError_t e = cudaErrorInvalidValue;
+  switch (slices) {
+    case 2: e = oz_slices<2>(a, bt, scratch, n, row0, rows, col0, cols, stream, false, reuse_a); break;
+    case 3: e = oz_slices<3>(a, bt, scratch, n, row0, rows, col0, cols, stream, false, reuse_a); break;
+    case 4: e = oz_slices<4>(a, bt, scratch, n, row0, rows, col0, cols, stream, false, reuse_a); break;
+    case 5: e = oz_slices<5>(a, bt, scratch, n, row0, rows, col0, cols, stream, false, reuse_a); break;
+    case 6: e = oz_slices<6>(a, bt, scratch, n, row0, rows, col0, cols, stream, false, reuse_a); break;
+    case 7: e = oz_slices<7>(a, bt, scratch, n, row0, rows, col0, cols, stream, false, reuse_a); break;
+    default: break;
+  }
+  if (e != cudaSuccess) return e;
+  return oz_persist_contract(c, scratch, slices, slices, n, row0, rows, col0, cols, stream);
 }
 
 }  // namespace mmx

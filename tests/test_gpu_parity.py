@@ -436,6 +436,76 @@ def test_fp64_auto_uses_the_tensor_cores_exactly_when_they_are_error_free():
     assert bits_equal(run(0, a, bt, c0), run(4, a, bt, c0))
 
 
+@pytest.mark.parametrize("digits_a,digits_bt,form", [(1, 1, 223), (1, 2, 223), (2, 2, 223), (3, 2, 324), (2, 3, 234), (3, 3, 335), (4, 3, 436), (3, 4, 346), (4, 4, 447),
+                                                   (5, 1, 555), (6, 1, 666), (5, 3, 777), (4, 5, 0), (8, 1, 0)])
+def test_fp64_auto_runs_the_cheapest_error_free_form(digits_a, digits_bt, form):
+    """One persistent launch reads the guard the slice pass wrote and picks the cheapest error-free form: the rectangular
+    SA x SB digit-pair forms up to four digits per operand, the triangular 5 / 6 / 7-slice forms beyond (every non-zero
+    pair t + u <= S + 1 kept); integers of 7t - 1 bits plus sign take t digits.  mmx_gene8_form reports the choice as
+    100 SA + 10 SB + levels; the result is the exact integer product (rounded once per Horner step, or not at all below
+    2^53); 0 = no form qualifies and the FP64 pipe produced the result."""
+    n = 1024
+    rs = np.random.RandomState(100 * digits_a + digits_bt)
+
+    def ints(digits):
+        top = 2 ** (7 * digits - 1)
+        x = rs.randint(-top + 1, top, (n, n)).astype(np.float64)
+        x[:, 0] = top - 1                     # every row uses its top digit
+        return x
+    a, bt, c0 = ints(digits_a), ints(digits_bt), rs.randint(-1000, 1000, (n, n)).astype(np.float64)
+    with capi.Context(n=n, dtype=capi.F64) as ctx:
+        assert ctx.gene8_form() == -1                                          # nothing launched yet
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        ctx.run_loop(8)
+        got = ctx.fetch(capi.ARRAY_C)
+        assert ctx.gene8_form() == form
+    if form == 0:
+        with capi.Context(n=n, dtype=capi.F64, matmul_variant=4) as pipe:
+            pipe.upload(capi.ARRAY_A, a)
+            pipe.upload(capi.ARRAY_BT, bt)
+            pipe.upload(capi.ARRAY_C, c0)
+            pipe.run_loop(8)
+            assert bits_equal(got, pipe.fetch(capi.ARRAY_C))
+        return
+    exact = a.astype(np.int64) @ bt.astype(np.int64).T + c0.astype(np.int64)   # |sum| < 2^62: exact in int64
+    if 7 * (digits_a + digits_bt) - 2 + 10 < 53:
+        assert np.array_equal(got.astype(np.int64), exact) and bits_equal(got, exact.astype(np.float64))
+    else:
+        ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(exact.astype(np.float64)), 1.0))) - 52)
+        assert (np.abs(got - exact.astype(np.float64)) <= 2.0 * ulp).all()
+
+
+def test_fp64_auto_form_on_the_application():
+    """(i +- k) / N at N = 2^p carries log2(N) + 2 bits: two digits per operand up to N = 4096 -> the 2 x 2 form, 4 slice
+    products per term instead of the 28 of the widest form; the whole individual stays bit-identical to the CPU program."""
+    for n, form in ((1024, 223), (2048, 223)):
+        with capi.Context(n=n, dtype=capi.F64) as ctx:
+            assert ctx.measure("101010101001").status == capi.MEASURED
+            assert ctx.gene8_form() == form
+            got = ctx.fetch(capi.ARRAY_C)
+            for r0 in range(0, n, 1024):
+                assert bits_equal(got[r0:r0 + 1024], cpu.closed_form_c(n, r0, r0 + 1024))
+
+
+@pytest.mark.parametrize("variant,slices", [(42, 5), (43, 4), (44, 3), (45, 2)])
+@pytest.mark.parametrize("n", [300, 1024])
+def test_fp64_int8_fixed_forms_meet_their_truncation_bound(n, variant, slices):
+    """Variants 41 .. 45 run 6 .. 2 slices on any operands: |error| <= (S + 3) K 2^(-7S) max_k|a_ik| max_k|bt_jk| (matmul_ozaki.cu)."""
+    a, bt, c0 = rand(n, capi.F64, 15), rand(n, capi.F64, 16), rand(n, capi.F64, 17)
+    with capi.Context(n=n, dtype=capi.F64, matmul_variant=variant) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        ctx.run_loop(8)
+        got = ctx.fetch(capi.ARRAY_C)
+    bound = (slices + 3) * n * 2.0 ** (-7 * slices) * np.abs(a).max(axis=1)[:, None] * np.abs(bt).max(axis=1)[None, :]
+    err = np.abs(got - (c0 + a @ bt.T))
+    assert (err <= bound + 1e-13 * n).all(), (err / bound).max()
+    assert err.max() > 0.0 if slices <= 4 else True                            # it really is the truncated form
+
+
 def test_fp64_auto_falls_back_on_the_application_when_n_is_not_a_power_of_two():
     """(i +- k) / 1536 has a full mantissa: every element is cut, so the whole individual is the FP64-pipe one, bit for bit."""
     n = 1536
