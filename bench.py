@@ -258,19 +258,26 @@ def run_ours(args):
         ms8 = ctx.time_loop(8, 5, True)
         ach = flops / (ms8 * 1e-3) / 1e12
         share = ms8 * 1e-3 / (device_s / args.steps)
-        if dtype == capi.F64 and n >= 1024:
-            # auto mode: this workload's operands carry two 7-bit digits, so the cheapest error-free form is the 6-slice one (21
-            # INT8 slice products per term, matmul_ozaki.cu); ms8 covers the two slice passes, that contraction and the two
-            # guarded launches that exit at once (7-slice form, FP64 pipe)
+        form = ctx.gene8_form() if dtype == capi.F64 else -1
+        if form > 0:
+            # auto mode picked an INT8 tensor-core form on the device (mmx_gene8_form: 100 SA + 10 SB + levels): digits a_1..a_SA
+            # against b_1..b_SB, pairs kept up to level t + u <= levels + 1.  This workload's operands carry log2(N) + 2 bits =
+            # two 7-bit digits each up to N = 4096: the 2 x 2 form, 4 INT8 slice products per FP64 term.  ms8 covers the two
+            # slice passes, that contraction and the guarded FP64-pipe launch that exits at once.
+            sa, sb, lv = form // 100, form // 10 % 10, form % 10
+            products = sum(1 for t in range(1, sa + 1) for u in range(1, sb + 1) if t + u <= lv + 1)
             int8_peak = 2.0 * peaks["bf16_tflops"]
-            ops = 21.0 * flops / (ms8 * 1e-3) / 1e12
+            ops = products * flops / (ms8 * 1e-3) / 1e12
             roof = {"bound": "tensor", "pipe": "int8 (tcgen05.mma.kind::i8, INT32 accumulators in TMEM)",
-                    "kernel": "matmul_ozaki<6> (gene 8: exact 7-bit INT8 slices, 21 slice products per FP64 term; slice passes included)",
+                    "kernel": f"matmul_ozaki_auto form {form} (gene 8: exact 7-bit INT8 slices, {sa} x {sb} digit pairs = {products} slice "
+                              f"products per FP64 term; slice passes included)",
+                    "form": form, "slice_products_per_term": products,
                     "achieved": ops, "peak": int8_peak, "unit": "TOP/s", "frac": ops / int8_peak,
-                    "traffic": ncu_traffic("matmul_ozaki", n), "ms_per_launch": ms8, "share_of_step": share,
+                    "traffic": ncu_traffic("matmul_ozaki_auto", n), "ms_per_launch": ms8, "share_of_step": share,
                     "effective_fp64_tflops": ach,
-                    "peak_source": "twice MEASURED_PEAKS.json bf16_tflops (INT8 runs at twice the bf16 rate); achieved counts the 21 INT8 "
-                                   "slice products issued per FP64 term"}
+                    "vs_fp64_pipe_peak": ach / capi.peak_probe(capi.PEAK_FP64_FMA, local_rank),
+                    "peak_source": "twice MEASURED_PEAKS.json bf16_tflops (INT8 runs at twice the bf16 rate); achieved counts the INT8 "
+                                   "slice products issued per FP64 term, over the time of the whole nest (slice passes included)"}
         else:
             pipe_peak = capi.peak_probe(capi.PEAK_FP64_FMA if dtype == capi.F64 else capi.PEAK_FP32_FMA, local_rank)
             roof = {"bound": "tensor", "pipe": "fp64 (DMMA.8x8x4 via mma.sync)" if dtype == capi.F64 else "fp32 (FFMA)",
@@ -318,17 +325,18 @@ def run_ours(args):
                            "fp64_pipe arm is the same run without that" if (dtype == capi.F64 and n >= 1024) else None),
             "data": "synthetic (the program generates its own inputs: a=(i+j)/N, b=(i-j)/N)",
             "config": {"workload": f"matrix app N={n} {args.dtype}, genome {GENOME_ALL_NESTS} (all six loop nests offloaded)",
-                       "gene8": ("auto: INT8 tensor cores in the cheapest error-free form (6 slices for this workload's operands), FP64 pipe otherwise"
-                                 if (dtype == capi.F64 and n >= 1024) else "default kernel for this dtype and size"),
+                       "gene8": ("auto: INT8 tensor cores in the cheapest error-free form, chosen on the device from the operands "
+                                 f"(form {roof.get('form')} here), FP64 pipe otherwise"
+                                 if (dtype == capi.F64 and n >= 1024 and roof) else "default kernel for this dtype and size"),
                        "n": n, "genome": GENOME_ALL_NESTS, "individuals_per_step_per_gpu": 1,
                        "l2": "working set 4*N^2*E per step exceeds L2; no flush needed"},
             "e2e": {"value": flops * args.steps * world / wall_s / 1e9, "unit": "GFLOP/s",
                     "h2d_bytes_per_step": int(plan.h2d_bytes), "d2h_bytes_per_step": int(plan.d2h_bytes),
                     "note": "host clock around mmx_measure (plan + 6 launches + checksum D2H + sync); this genome has no host-side inputs"},
             "e2e_mixed": mixed, "e2e_host_buffers": host_io,
-            # the plan counts one launch per offloaded nest; in FP64 auto mode gene 8 is five kernels (two slice passes, the
-            # tensor-core contraction, and the guarded 7-slice and FP64-pipe launches that exit at once)
-            "gpu_launches": (int(plan.kernel_launches) + (4 if (dtype == capi.F64 and n >= 1024) else 0)) * args.steps,
+            # the plan counts one launch per offloaded nest; in FP64 auto mode gene 8 is four kernels (two slice passes, the
+            # tensor-core contraction, and the guarded FP64-pipe launch that exits at once)
+            "gpu_launches": (int(plan.kernel_launches) + (3 if (dtype == capi.F64 and n >= 1024) else 0)) * args.steps,
             "clocks": clocks, "roofline": roof, "roofline_hbm": hbm_roof, "cpu_baseline": base,
             "checksum": checksum,
         }

@@ -247,6 +247,11 @@ MMX_API int mmx_device_ptr(mmx_ctx* ctx, int slot, int array, void** ptr_out);
  * pipe (the slices would not have been error-free), -1 = no such launch yet / not an FP64 auto-mode context.  Synchronises the slot. */
 MMX_API int mmx_gene8_form(mmx_ctx* ctx, int slot, int32_t* form_out);
 
+/* The rule behind mmx_gene8_form, evaluated on the host (no device needed): the form the auto launch takes for operands of which
+ * `cut` != 0 says some element has bits below its 7th digit, and top_a / top_bt are the highest non-zero 7-bit digits (1-based)
+ * anywhere in a / bt.  Returns 100 SA + 10 SB + levels, or 0 for the FP64 pipe. */
+MMX_API int mmx_gene8_pick_form(int cut, int top_a, int top_bt);
+
 /* ---- row-sharded run across a group of GPUs (BASELINE.json config 5) -----------------
  * One individual (every nest offloaded) spread over `world` <= 8 members, one device slot each.  Member r
  * owns a contiguous block of rows of a, c and bt (64-row aligned when N allows).  The single exchange of

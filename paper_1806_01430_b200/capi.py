@@ -113,6 +113,7 @@ _SIGNATURES = {
     "mmx_run_loop_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "mmx_device_ptr": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "mmx_gene8_form": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int32)]),
+    "mmx_gene8_pick_form": (C.c_int, [C.c_int, C.c_int, C.c_int]),
     "mmx_shard_run_local": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int, C.POINTER(ShardStats), C.POINTER(C.c_double)]),
     "mmx_shard_export": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(ShardHandle)]),
     "mmx_shard_bind": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(ShardHandle), C.POINTER(C.c_int32)]),
@@ -179,6 +180,11 @@ def plan_steps(info: PlanInfo) -> list[tuple]:
         what = NEST_NAMES[s.nest] if s.nest >= 0 else (s.array if s.array >= 0 else None)
         out.append((STEP_NAMES[s.kind], what, s.mode, s.bytes, s.launches))
     return out
+
+
+def gene8_pick_form(cut: bool, top_a: int, top_bt: int) -> int:
+    """The auto-mode rule of gene 8 in FP64 (include/mmx.h: mmx_gene8_pick_form): 100 SA + 10 SB + levels, 0 = FP64 pipe."""
+    return int(load().mmx_gene8_pick_form(int(bool(cut)), int(top_a), int(top_bt)))
 
 
 def peak_probe(kind: int, device: int = 0) -> float:

@@ -637,6 +637,8 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
       if ((e = matmul_ozaki_prepare()) != cudaSuccess) return fail(e, "matmul_ozaki_prepare");
       if ((e = cudaMalloc(&sl.d_scratch, matmul_ozaki_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
       if (cfg->matmul_variant == 0) {
+        // auto mode relies on a zero-filled scratch (digit planes nobody has written yet are zero, matmul_ozaki.cu)
+        if ((e = cudaMemset(sl.d_scratch, 0, matmul_ozaki_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMemset(scratch)");
         if ((e = cudaMemset(matmul_ozaki_form_word(sl.d_scratch, cfg->n), 0xff, sizeof(int))) != cudaSuccess) return fail(e, "cudaMemset(form)");
         sl.gene8_form_valid = true;
       }
@@ -811,6 +813,8 @@ MMX_API int mmx_device_ptr(mmx_ctx* ctx, int slot, int array, void** ptr_out) {
   *ptr_out = ctx->slots[slot]->d_arr[array];
   return MMX_OK;
 }
+
+MMX_API int mmx_gene8_pick_form(int cut, int top_a, int top_bt) { return ozaki_pick_form(cut, top_a, top_bt); }
 
 MMX_API int mmx_gene8_form(mmx_ctx* ctx, int slot, int32_t* form_out) {
   if (ctx == nullptr || form_out == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size())) return MMX_E_INVALID;

@@ -338,7 +338,6 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
   auto empty_bar = [&](int s) { return bars + 8u * (8 + s); };
   auto acc_full = [&](int b) { return bars + 8u * (16 + b); };   // the MMAs of a tile have completed into set b
   auto acc_empty = [&](int b) { return bars + 8u * (18 + b); };  // the epilogue has read set b
-  auto c_full = [&](int b) { return bars + 8u * (20 + b); };     // chunk buffer b holds the incoming c values
   const unsigned tmem_slot = bars + 8u * 24;
   volatile unsigned* tmem_slot_ptr = reinterpret_cast<volatile unsigned*>(smem_raw + (tmem_slot - raw));
   int* eb_sh = reinterpret_cast<int*>(smem_raw + (bars + 256 - raw));            // [2][BN] column exponents, alternating per tile
@@ -369,7 +368,6 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
       mbar_init(acc_full(b), 1);
       mbar_init(acc_empty(b), 4);  // one arrival per epilogue warp
     }
-    for (int b = 0; b < CR; ++b) mbar_init(c_full(b), 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   if (warp == 2) {
@@ -470,24 +468,14 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
     const int m_limit = g.row0 + g.rows;
     int tile = 0;
     if constexpr (CR > 0) {
-      // c travels by TMA through shared memory in chunks of 16 columns (128 rows x 128 bytes, SWIZZLE_128B): a ring of CR
-      // chunk buffers is filled ahead (the first ones before the tile's MMAs have finished), each thread adds its row's 16
-      // results in place (16-byte accesses, conflict-free under the swizzle), and the chunk goes back with one TMA store --
-      // global memory sees full 128-byte lines instead of one 16-byte piece per thread and row.  The tensor map of c ends
-      // at (row0 + rows, col0 + cols): loads beyond it read zeros and stores beyond it are dropped, which is all the edge
-      // handling there is.
+      // c += through TMA REDUCTIONS, 16 columns at a time: each epilogue warp owns 32 rows of the tile; it writes their 16
+      // results into its 4 KB slab of a chunk buffer (128-byte rows under SWIZZLE_128B: 16-byte stores, conflict-free) and
+      // one lane sends the slab off as cp.reduce.async.bulk.tensor .add -- the L2 performs c[i][j] += v (one IEEE addition,
+      // what the thread would have done), so c is never loaded by the SM, global memory sees whole 128-byte lines instead of
+      // one 16-byte piece per thread and row, and nothing waits for a round trip.  The warps are decoupled: a slab is reused
+      // once its reduction has left shared memory (ring of CR per warp), with no CTA-wide barrier per chunk.  The tensor map
+      // of c ends at (row0 + rows, col0 + cols): what lies beyond is dropped, which is all the edge handling there is.
       constexpr int NCH = BN / 16;
-      const int total_chunks = my_tiles * NCH;
-      const bool elected = threadIdx.x == 64;
-      auto load_chunk = [&](int J) {  // elected thread only
-        int bx, by;
-        tile_at(J / NCH, bx, by);
-        const int b = J % CR;
-        mbar_expect_tx(c_full(b), Sh::C_CHUNK);
-        tma_load_2d(cbuf + b * Sh::C_CHUNK, map_c, g.col0 + bx * BN + (J % NCH) * 16, g.row0 + by * OZ_BM, c_full(b));
-      };
-      if (elected)
-        for (int J = 0; J < CR - 1 && J < total_chunks; ++J) load_chunk(J);
       int J = 0;
       for (; tile < my_tiles; ++tile) {
         int bx, by;
@@ -528,8 +516,8 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
             const int ebj = eb[j * 16 + e];
             if constexpr (LV <= 4) {
               // the level sum as ONE integer (|L| < 2^31 and three shifts of 7 bits: exact in 64 bits and in a double), scaled
-              // by adding to the exponent field: two FP64-pipe operations per element (conversion, the addition into c)
-              // instead of eight -- with one warp per scheduler the epilogue runs at the latency of its FP64 chain
+              // by adding to the exponent field: one FP64-pipe operation per element (the conversion) instead of seven --
+              // with one warp per scheduler the epilogue runs at the latency of its FP64 chain
               long long acc = static_cast<int>(lv[0][e]);
 #pragma unroll
               for (int l = 1; l < LV; ++l) acc = (acc << 7) + static_cast<int>(lv[l][e]);
@@ -548,32 +536,22 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
               v[e] = scaled_fast(sum, ei, pa, row_fast, ebj, pb[j * 16 + e]);
             }
           }
-          const int b = J % CR;
-          mbar_wait(c_full(b), (J / CR) & 1);
-          const unsigned crow = cbuf + b * Sh::C_CHUNK + r * 128;
+          const unsigned slab = cbuf + (J % CR) * Sh::C_CHUNK + q * 4096;
+          if (lane == 0) tma_store_wait_read<CR - 1>();  // the reduction that last used this slab has left shared memory
+          __syncwarp();
+          const unsigned crow = slab + lane * 128;
 #pragma unroll
-          for (int ch = 0; ch < 8; ++ch) {
-            const unsigned cell = crow + ((ch ^ (r & 7)) << 4);
-            double x0, x1;
-            asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x0), "=d"(x1) : "r"(cell) : "memory");
-            x0 += v[2 * ch];
-            x1 += v[2 * ch + 1];
-            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(cell), "d"(x0), "d"(x1) : "memory");
-          }
+          for (int ch = 0; ch < 8; ++ch)
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(crow + ((ch ^ (lane & 7)) << 4)), "d"(v[2 * ch]), "d"(v[2 * ch + 1]) : "memory");
           fence_proxy_async_smem();
-          asm volatile("bar.sync 1, 128;\n" ::: "memory");
-          if (elected) {
-            tma_store_2d(map_c, cbuf + b * Sh::C_CHUNK, g.col0 + n_tile + j * 16, m_base);
+          __syncwarp();
+          if (lane == 0) {
+            tma_reduce_add_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
             tma_store_commit();
-            const int Jn = J + CR - 1;  // goes into the buffer of chunk J - 1: its store has to have left shared memory
-            if (Jn < total_chunks) {
-              tma_store_wait_read<1>();
-              load_chunk(Jn);
-            }
           }
         }
       }
-      if (elected) tma_store_wait<0>();
+      if (lane == 0) tma_store_wait<0>();
     } else {
       // c straight from registers (any n, odd ones included): 64 columns at a time; the first 64 incoming values and the
       // tile's column exponents are fetched before the tile's MMAs are waited for
@@ -693,9 +671,9 @@ matmul_ozaki_auto_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, c
   const int form = ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]);
   if (blockIdx.x == 0 && threadIdx.x == 0) *ran = form;
   switch (form) {
-    case 223: oz_persist_form<2, 2, 3, 128, 2, CX, CY>(g, maps, smem_raw); break;
-    case 324: oz_persist_form<3, 2, 4, 128, 2, CX, CY>(g, maps, smem_raw); break;
-    case 234: oz_persist_form<2, 3, 4, 128, 2, CX, CY>(g, maps, smem_raw); break;
+    case 223: oz_persist_form<2, 2, 3, 128, 1, CX, CY>(g, maps, smem_raw); break;
+    case 324: oz_persist_form<3, 2, 4, 128, 1, CX, CY>(g, maps, smem_raw); break;
+    case 234: oz_persist_form<2, 3, 4, 128, 1, CX, CY>(g, maps, smem_raw); break;
     case 335: oz_persist_form<3, 3, 5, 64, 4, CX, CY>(g, maps, smem_raw); break;
     case 436: oz_persist_form<4, 3, 6, 64, 4, CX, CY>(g, maps, smem_raw); break;
     case 346: oz_persist_form<3, 4, 6, 64, 4, CX, CY>(g, maps, smem_raw); break;
@@ -722,7 +700,7 @@ matmul_ozaki_fixed_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps) 
 template <int S>
 __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const double* __restrict__ src, signed char* __restrict__ dst, int* __restrict__ exps,
                                                           size_t plane, int n, int kq, int src_row0, int nrows, int dst_row0,
-                                                          int* __restrict__ guard, int lossy_slot, int top_slot) {
+                                                          int* __restrict__ guard, int lossy_slot, int top_slot, int dirty_slot) {
   __shared__ double red[8];
   __shared__ int top_sh[8];
   __shared__ int e_sh;
@@ -787,6 +765,11 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const double* __res
   const double inv = (live && !bad && !tiny) ? scalbn(1.0, -e_sh) : 0.0;
   signed char* drow = dst + static_cast<size_t>(dst_row0 + r) * kq;
   int lossy = bad | tiny, top = 0;  // top = highest non-zero digit (1-based) this thread has seen
+  // Auto mode keeps an invariant on its scratch (zero-filled when the context is created): planes beyond guard[dirty_slot] hold
+  // only zeros.  So zero words need not be written there -- short operands (the application's: two digits) move 2 planes per
+  // element instead of 7.  The word only ever grows, to the highest plane any launch wrote a non-zero digit into; a CTA that
+  // reads it after a neighbour has raised it merely writes more zeros.
+  const int dirty = dirty_slot >= 0 ? guard[dirty_slot] : S;
   auto emit4 = [&](int k0, const double (&v)[4]) {
     int dig[S] = {};
 #pragma unroll
@@ -808,7 +791,7 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const double* __res
 #pragma unroll
     for (int t = 0; t < S; ++t) {
       if (dig[t] != 0) top = max(top, t + 1);
-      *reinterpret_cast<int*>(drow + t * plane + k0) = dig[t];
+      if (t < dirty || dig[t] != 0) *reinterpret_cast<int*>(drow + t * plane + k0) = dig[t];
     }
   };
 #pragma unroll
@@ -831,6 +814,7 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const double* __res
       for (int w = 1; w < 8; ++w) top = max(top, top_sh[w]);
       if (lossy && guard[lossy_slot] == 0) atomicOr(guard + lossy_slot, 1);
       if (top > guard[top_slot]) atomicMax(guard + top_slot, top);  // read first: after a few rows nobody needs the atomic
+      if (dirty_slot >= 0 && top > guard[dirty_slot]) atomicMax(guard + dirty_slot, top);
     }
   }
 }
@@ -893,8 +877,10 @@ cudaError_t oz_slices(const double* a, const double* bt, void* scratch, int n, i
         e != cudaSuccess)
       return e;
   const int cols_pad = static_cast<int>(oz_rows_pad(cols, OZ_BN));
-  if (!reuse_a) ozaki_slice_kernel<P><<<rows, 256, 0, stream>>>(a, L.sa, L.ea, L.a_plane, n, L.kq, row0, rows, row0, flag, 0, 1);
-  ozaki_slice_kernel<P><<<cols_pad, 256, 0, stream>>>(bt, L.sb, L.eb, L.b_plane, n, L.kq, col0, cols, 0, flag, 3, 2);
+  // guard words: 0 a is cut, 1 top digit of a, 2 top digit of bt, 3 bt is cut (reset per launch); 4 the form the auto kernel took;
+  // 5 / 6 highest plane of the a / bt scratch that may hold non-zero bytes (auto mode only; never reset)
+  if (!reuse_a) ozaki_slice_kernel<P><<<rows, 256, 0, stream>>>(a, L.sa, L.ea, L.a_plane, n, L.kq, row0, rows, row0, flag, 0, 1, with_guard ? 5 : -1);
+  ozaki_slice_kernel<P><<<cols_pad, 256, 0, stream>>>(bt, L.sb, L.eb, L.b_plane, n, L.kq, col0, cols, 0, flag, 3, 2, with_guard ? 6 : -1);
   return cudaGetLastError();
 }
 
@@ -978,8 +964,10 @@ template <int CX, int CY> int oz_auto_max_clusters() {
   return clusters;
 }
 
-// The cluster shape of the auto launch on this device: 2 x 2 when (nearly) every SM can sit in such a cluster, else 2 x 1, else
-// none.  {shape code 22 / 21 / 11, resident clusters}.  MMX_OZ_CLUSTER_SHAPE forces a shape (measurement).
+// The cluster shape of the auto launch on this device: {shape code 22 / 21 / 11, resident clusters}.  Default 11 (no clusters):
+// measured on B200 (profiles/r1e_cluster_shapes.txt) sharing the operand loads changes nothing at 2 x 1 and costs 8-12 % at
+// 2 x 2 -- the short forms wait on the epilogue and on refill latency, not on L2 bandwidth (6.3 of 11.8 TB/s).  MMX_OZ_CLUSTER_SHAPE
+// = 21 / 22 selects the multicast forms (kept as a measured tuning point, and for devices where the balance differs).
 struct OzClusterChoice {
   int shape = 0, clusters = 0;
 };
@@ -993,19 +981,18 @@ OzClusterChoice oz_auto_cluster_choice() {
     static const int forced = [] { const char* e = getenv("MMX_OZ_CLUSTER_SHAPE"); return e ? atoi(e) : 0; }();
     const int sms = oz_sm_count();
     OzClusterChoice c;
-    const int n22 = (forced == 0 || forced == 22) ? oz_auto_max_clusters<2, 2>() : 0;
-    if (n22 > 0 && (forced == 22 || 4 * n22 >= sms - 8)) {
+    const int n22 = forced == 22 ? oz_auto_max_clusters<2, 2>() : 0;
+    const int n21 = forced == 21 ? oz_auto_max_clusters<2, 1>() : 0;
+    if (n22 > 0) {
       c.shape = 22;
       c.clusters = n22;
+    } else if (n21 > 0) {
+      c.shape = 21;
+      c.clusters = n21;
     } else {
-      const int n21 = (forced == 0 || forced == 21) ? oz_auto_max_clusters<2, 1>() : 0;
-      if (n21 > 0 && (forced == 21 || 2 * n21 >= sms - 4)) {
-        c.shape = 21;
-        c.clusters = n21;
-      } else {
-        c.shape = 11;
-        c.clusters = sms;
-      }
+      (void)oz_auto_configure<1, 1>();
+      c.shape = 11;
+      c.clusters = sms;
     }
     choice[d & 63] = c;
     known = true;
@@ -1019,13 +1006,13 @@ template <int S, int CR> cudaError_t oz_fixed_configure() {
 }
 constexpr int oz_fixed_ring(int s) { return s <= 4 ? 4 : 0;  /* chunk buffers of c where the stage ring leaves room */ }
 
-// c as a 2-D tensor of doubles that ends at (rows_end, cols_end): box = 128 rows x 16 columns, 128-byte swizzle
+// c as a 2-D tensor of doubles that ends at (rows_end, cols_end): box = 32 rows x 16 columns (one warp's slab), 128-byte swizzle
 bool make_c_map(CUtensorMap* map, double* c, int n, int rows_end, int cols_end) {
   EncodeTiledFn enc = encode_tiled();
   if (enc == nullptr) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols_end), static_cast<cuuint64_t>(rows_end)};
   const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n) * sizeof(double)};
-  const cuuint32_t box[2] = {16, static_cast<cuuint32_t>(OZ_BM)};
+  const cuuint32_t box[2] = {16, 32};
   const cuuint32_t elem[2] = {1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, c, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;

@@ -45,6 +45,12 @@ __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map
 __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, unsigned src, int c0, int c1) {
   asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(map), "r"(src), "r"(c0), "r"(c1) : "memory");
 }
+// shared -> global tile REDUCTION: global[box] += shared[box], element-wise in the tensor map's type (FP64 here: one IEEE
+// addition per element, performed at the L2), clipped to the tensor like a store
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, unsigned src, int c0, int c1) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];\n" ::"l"(map), "r"(src), "r"(c0), "r"(c1)
+               : "memory");
+}
 __device__ __forceinline__ void tma_store_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 // at most N of this thread's most recent bulk groups may still be READING shared memory / be incomplete
 template <int N> __device__ __forceinline__ void tma_store_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;\n" ::"n"(N) : "memory"); }

@@ -477,6 +477,40 @@ def test_fp64_auto_runs_the_cheapest_error_free_form(digits_a, digits_bt, form):
         assert (np.abs(got - exact.astype(np.float64)) <= 2.0 * ulp).all()
 
 
+def test_fp64_auto_digit_planes_stay_consistent_from_launch_to_launch():
+    """The slice pass skips zero words in planes no launch has used yet (the scratch starts zero-filled).  Long operands
+    followed by short ones on the same context: the planes the long ones dirtied are rewritten with zeros, and the short
+    product is exact; then long again, then a row-sparse case where only one row is long."""
+    n = 1024
+    rs = np.random.RandomState(77)
+
+    def ints(digits):
+        top = 2 ** (7 * digits - 1)
+        x = rs.randint(-top + 1, top, (n, n)).astype(np.float64)
+        x[:, 0] = top - 1
+        return x
+    with capi.Context(n=n, dtype=capi.F64) as ctx:
+        def product(a, bt):
+            ctx.upload(capi.ARRAY_A, a)
+            ctx.upload(capi.ARRAY_BT, bt)
+            ctx.upload(capi.ARRAY_C, np.zeros((n, n)))
+            ctx.run_loop(8)
+            return ctx.fetch(capi.ARRAY_C), ctx.gene8_form()
+        for da, db, form in ((4, 3, 436), (1, 1, 223), (3, 3, 335), (2, 1, 223), (4, 4, 447), (2, 2, 223)):
+            a, bt = ints(da), ints(db)
+            got, ran = product(a, bt)
+            assert ran == form
+            exact = (a.astype(np.int64) @ bt.astype(np.int64).T).astype(np.float64)
+            ulp = np.exp2(np.floor(np.log2(np.maximum(np.abs(exact), 1.0))) - 52)
+            assert (np.abs(got - exact) <= 2.0 * ulp).all(), (da, db)
+            if 7 * (da + db) + 8 < 53:
+                assert bits_equal(got, exact), (da, db)
+        a, bt = ints(1), ints(1)
+        a[5, :] = ints(3)[5, :]                # one long row after short launches: its digits land in planes others skipped
+        got, ran = product(a, bt)
+        assert ran == 324 and bits_equal(got, (a.astype(np.int64) @ bt.astype(np.int64).T).astype(np.float64))
+
+
 def test_fp64_auto_form_on_the_application():
     """(i +- k) / N at N = 2^p carries log2(N) + 2 bits: two digits per operand up to N = 4096 -> the 2 x 2 form, 4 slice
     products per term instead of the 28 of the widest form; the whole individual stays bit-identical to the CPU program."""

@@ -90,3 +90,52 @@ def test_guard_condition_is_the_error_free_condition():
     assert (contract(a, bt, c0).astype(object) != exact).any()
     # full-mantissa doubles: elements are cut
     assert top(rs.uniform(-1, 1, (n, n)))[0]
+
+
+# ---- the forms of the persistent kernel (matmul_ozaki.cu: <SA, SB, LV>) and the rule that picks one -------------------------
+
+FORMS = [(2, 2, 3), (3, 2, 4), (2, 3, 4), (3, 3, 5), (4, 3, 6), (3, 4, 6), (4, 4, 7), (5, 5, 5), (6, 6, 6), (7, 7, 7)]
+
+
+def pairs_of(form):
+    sa, sb, lv = form
+    return {(t, u) for t in range(1, sa + 1) for u in range(1, sb + 1) if t + u <= lv + 1}
+
+
+def test_rectangular_form_reproduces_the_product_exactly():
+    """Digits a_1..a_SA against b_1..b_SB, every pair: when no operand has a digit beyond (SA, SB) the level sums, weighted
+    2^(-7 (t + u)), are the exact product -- with integers only."""
+    rs = np.random.RandomState(5)
+    k = 96
+    for sa, sb in ((2, 2), (3, 2), (2, 3), (4, 4)):
+        a = rs.randint(-(2 ** (7 * sa - 1)) + 1, 2 ** (7 * sa - 1), (8, k)).astype(np.float64)
+        b = rs.randint(-(2 ** (7 * sb - 1)) + 1, 2 ** (7 * sb - 1), (8, k)).astype(np.float64)
+        ea, da, ra = slices(a)
+        eb, db, rb = slices(b)
+        assert not ra.any() and not rb.any()
+        assert not any(d.any() for d in da[sa:]) and not any(d.any() for d in db[sb:])   # nothing beyond the form's digits
+        total = np.zeros((8, 8), dtype=object)
+        for t in range(1, sa + 1):
+            for u in range(1, sb + 1):
+                level = da[t - 1].astype(np.int64) @ db[u - 1].astype(np.int64).T
+                assert np.abs(level).max() < 2 ** 31
+                total = total + level.astype(object) * 2 ** (7 * (7 + 7 - t - u))      # common denominator 2^(7 * 14)
+        exact = a.astype(np.int64).astype(object) @ b.astype(np.int64).astype(object).T
+        scale = np.array([[2 ** (int(x) + int(y) + 2) for y in eb] for x in ea], dtype=object)
+        assert (total * scale == exact * 2 ** (7 * 14)).all()
+
+
+def test_pick_form_takes_the_cheapest_error_free_form():
+    from paper_1806_01430_b200 import capi
+    for ta in range(0, 9):
+        for tb in range(0, 9):
+            got = capi.gene8_pick_form(False, ta, tb)
+            need = {(t, u) for t in range(1, max(ta, 1) + 1) for u in range(1, max(tb, 1) + 1)}
+            ok = [f for f in FORMS if need <= pairs_of(f)]
+            if not ok:
+                assert got == 0, (ta, tb, got)
+                continue
+            form = (got // 100, got // 10 % 10, got % 10)
+            assert form in ok, (ta, tb, got)
+            assert len(pairs_of(form)) == min(len(pairs_of(f)) for f in ok), (ta, tb, got)
+            assert capi.gene8_pick_form(True, ta, tb) == 0                # anything cut: the FP64 pipe

@@ -14,4 +14,4 @@ ncu --set full --clock-control none --import-source on -k regex:'matmul_3xtf32|s
     -o $out/${tag}_prof_f32 python tools/one_individual.py f32 4096 > $out/${tag}_ncu_f32.log 2>&1
 ls -la $out | tail -8
 ncu --set full --clock-control none --import-source on -k regex:'ozaki' -s 3 -c 3 -f \
-    -o $out/${tag}_prof_ozaki python tools/ozaki_one.py 4096 40 > $out/${tag}_ncu_ozaki.log 2>&1
+    -o $out/${tag}_prof_ozaki python tools/ozaki_one.py 4096 0 > $out/${tag}_ncu_ozaki.log 2>&1
