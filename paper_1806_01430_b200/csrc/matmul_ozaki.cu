@@ -772,22 +772,29 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const double* __res
   const int dirty = dirty_slot >= 0 ? guard[dirty_slot] : S;
   auto emit4 = [&](int k0, const double (&v)[4]) {
     int dig[S] = {};
+    double rem[4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      double rem = bad ? 0.0 : v[q] * inv;
+    for (int q = 0; q < 4; ++q) rem[q] = bad ? 0.0 : v[q] * inv;
 #pragma unroll
-      for (int t = 0; t < S; ++t) {
-        if (rem == 0.0) break;  // nothing left: the remaining digits are zero (short operands finish after a digit or two)
-        const double up = pow2(7 * (t + 1) - 1), down = pow2(-(7 * (t + 1) - 1));
+    for (int t = 0; t < S; ++t) {
+      // four elements per digit level, branch-free (a zero remainder yields a zero digit); one test per level ends the walk
+      // once nothing is left -- short operands finish after a digit or two
+      if (t >= 1 && rem[0] == 0.0 && rem[1] == 0.0 && rem[2] == 0.0 && rem[3] == 0.0) break;
+      const double up = pow2(7 * (t + 1) - 1), down = pow2(-(7 * (t + 1) - 1));
+      int word = 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
         // rint without the conversion units (they would bound this pass): adding 1.5 * 2^52 rounds to the integer grid
         // (ties to even) and leaves the integer in the low word of the sum
-        const double shifted = fma(rem, up, 6755399441055744.0);
+        const double shifted = fma(rem[q], up, 6755399441055744.0);
         const int d = __double2loint(shifted);
-        rem = fma(-(shifted - 6755399441055744.0), down, rem);  // exact: removes a prefix of rem's bits
-        dig[t] |= (d & 0xff) << (8 * q);
+        rem[q] = fma(-(shifted - 6755399441055744.0), down, rem[q]);  // exact: removes a prefix of rem's bits
+        word |= (d & 0xff) << (8 * q);
       }
-      lossy |= rem != 0.0;  // bits below the last digit: the slices do not reproduce this element exactly
+      dig[t] = word;
     }
+    // bits below the last digit: the slices do not reproduce this element exactly
+    lossy |= (rem[0] != 0.0) | (rem[1] != 0.0) | (rem[2] != 0.0) | (rem[3] != 0.0);
 #pragma unroll
     for (int t = 0; t < S; ++t) {
       if (dig[t] != 0) top = max(top, t + 1);
