@@ -42,6 +42,7 @@ namespace {
 constexpr int OZ_BM = 128, OZ_BN = 64;               // tile of c
 constexpr int OZ_THREADS = 192;                      // warp 0 TMA, warp 1 MMA, warps 2-5 epilogue (one per TMEM lane quarter)
 constexpr int OZ_KPAD = 64;                          // slice rows are padded to this many k
+constexpr int OZP_THREADS = 320;                     // persistent form: warp 0 TMA, warp 1 MMA, warps 2-9 epilogue (two per TMEM lane quarter)
 
 // BK = k bytes per pipeline stage = bytes per shared-memory row (SWIZZLE_64B or SWIZZLE_32B).  All S slices of both operands
 // have to be resident per stage, so a stage is S * 192 * BK bytes: 84 KB (2 stages) at BK = 64, 42 KB (5 stages) at BK = 32.
@@ -281,7 +282,8 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
 //  (3) The TMA producer runs ahead into the next tile while the epilogue drains, and where 2 * LV * BN <= 512 columns the level
 //      accumulators are double-buffered in TMEM, so the MMAs of tile i+1 overlap the epilogue of tile i entirely.
 // Slices arrive as one TMA box per slice and operand (the shared-memory layout is the one the 3-D box of the kernel above gives).
-// CR = 16-column chunks of c staged in shared memory (0: the epilogue reads and writes c from registers, one row per thread)
+// CR = slabs (32 rows x 16 columns of results on their way to c) per epilogue warp (0: the epilogue reads and writes c from
+// registers, one row per thread, with four epilogue warps)
 template <int SA, int SB, int LV, int BN, int CR> struct OzPShape {
   static_assert(BN == 64 || BN == 128, "tile width");
   static_assert(LV * BN <= 512, "the level accumulators of a tile must fit TMEM");
@@ -290,8 +292,9 @@ template <int SA, int SB, int LV, int BN, int CR> struct OzPShape {
   static constexpr int A_SLICE = OZ_BM * BK, B_SLICE = BN * BK;
   static constexpr int A_BYTES = SA * A_SLICE, B_BYTES = SB * B_SLICE;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int C_CHUNK = OZ_BM * 16 * 8;  // 128 rows x 16 doubles = one 128-byte-swizzled TMA box
-  static constexpr int C_BYTES = CR * C_CHUNK;
+  static constexpr int C_SLAB = 32 * 16 * 8;      // 32 rows x 16 doubles = one 128-byte-swizzled TMA box
+  static constexpr int EPI_WARPS = CR > 0 ? 8 : 4;
+  static constexpr int C_BYTES = CR * 8 * C_SLAB;
   static constexpr int TAIL = 3584;               // barriers, column exponents and scale factors
   static constexpr int STAGES_FIT = (227 * 1024 - 1024 - TAIL - C_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
@@ -366,7 +369,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
     }
     for (int b = 0; b < NBUF; ++b) {
       mbar_init(acc_full(b), 1);
-      mbar_init(acc_empty(b), 4);  // one arrival per epilogue warp
+      mbar_init(acc_empty(b), Sh::EPI_WARPS);  // one arrival per epilogue warp
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -476,7 +479,9 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
       // once its reduction has left shared memory (ring of CR per warp), with no CTA-wide barrier per chunk.  The tensor map
       // of c ends at (row0 + rows, col0 + cols): what lies beyond is dropped, which is all the edge handling there is.
       constexpr int NCH = BN / 16;
-      int J = 0;
+      const int grp = (warp - 2) / 4;  // the two warps of a lane quarter take alternate chunks
+      const unsigned slab0 = cbuf + (warp - 2) * Sh::C_SLAB;
+      int sent = 0;  // chunks this warp has sent
       for (; tile < my_tiles; ++tile) {
         int bx, by;
         tile_at(tile, bx, by);
@@ -488,24 +493,24 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
         const double pa = pow2(row_fast ? ei - 12 : 0);
         int* eb = eb_sh + (tile & 1) * BN;
         double* pb = pb_sh + (tile & 1) * BN;
-        if (r < BN) {
+        if (grp == 0 && r < BN) {
           const int e = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
           eb[r] = e;
           pb[r] = pow2(e > -400 && e < 400 ? e : 0);
         }
         // the exponents of this tile are complete; nobody is still reading the other copy (that was two tiles ago, and
         // everyone has passed the barrier of the tile in between)
-        asm volatile("bar.sync 1, 128;\n" ::: "memory");
+        asm volatile("bar.sync 1, 256;\n" ::: "memory");
         mbar_wait(acc_full(buf), (tile / NBUF) & 1);
         tc_fence_after();
         const unsigned t0 = tmem_base + (static_cast<unsigned>(q * 32) << 16) + buf * (LV * BN);
 #pragma unroll 1
-        for (int j = 0; j < NCH; ++j, ++J) {
+        for (int j = grp; j < NCH; j += 2, ++sent) {
           unsigned lv[LV][16];
 #pragma unroll
           for (int l = 0; l < LV; ++l) tc_ld16_issue(t0 + l * BN + j * 16, lv[l]);
           tc_ld_wait();
-          if (j == NCH - 1) {  // every level of this set has been read: the MMAs of a later tile may overwrite it
+          if (j + 2 >= NCH) {  // this warp has read its share of the set: the MMAs of a later tile may overwrite it
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(acc_empty(buf));
@@ -516,8 +521,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
             const int ebj = eb[j * 16 + e];
             if constexpr (LV <= 4) {
               // the level sum as ONE integer (|L| < 2^31 and three shifts of 7 bits: exact in 64 bits and in a double), scaled
-              // by adding to the exponent field: one FP64-pipe operation per element (the conversion) instead of seven --
-              // with one warp per scheduler the epilogue runs at the latency of its FP64 chain
+              // by adding to the exponent field: one FP64-pipe operation per element (the conversion) instead of seven
               long long acc = static_cast<int>(lv[0][e]);
 #pragma unroll
               for (int l = 1; l < LV; ++l) acc = (acc << 7) + static_cast<int>(lv[l][e]);
@@ -536,7 +540,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
               v[e] = scaled_fast(sum, ei, pa, row_fast, ebj, pb[j * 16 + e]);
             }
           }
-          const unsigned slab = cbuf + (J % CR) * Sh::C_CHUNK + q * 4096;
+          const unsigned slab = slab0 + (sent % CR) * (8 * Sh::C_SLAB);
           if (lane == 0) tma_store_wait_read<CR - 1>();  // the reduction that last used this slab has left shared memory
           __syncwarp();
           const unsigned crow = slab + lane * 128;
@@ -556,7 +560,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
       // c straight from registers (any n, odd ones included): 64 columns at a time; the first 64 incoming values and the
       // tile's column exponents are fetched before the tile's MMAs are waited for
       const bool vec_ok = (g.n % 2 == 0) && (g.col0 % 2 == 0);
-      for (; tile < my_tiles; ++tile) {
+      for (; warp < 6 && tile < my_tiles; ++tile) {  // warps 2-5; the other four have nothing to do in this form
         int bx, by;
         tile_at(tile, bx, by);
         const int m_base = g.row0 + by * OZ_BM, n_tile = bx * BN;
@@ -575,11 +579,11 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
           pb[r] = pow2(e > -400 && e < 400 ? e : 0);
         }
 #pragma unroll 1
-        for (int half = 0; half < BN / 64; ++half) {
-          const int n_rel = n_tile + half * 64;
-          double cpre[64];
+        for (int part = 0; part < BN / 32; ++part) {
+          const int n_rel = n_tile + part * 32;
+          double cpre[32];
 #pragma unroll
-          for (int e = 0; e < 64; e += 2) {
+          for (int e = 0; e < 32; e += 2) {
             const int jr = n_rel + e;
             if (row_ok && vec_ok && jr + 2 <= g.cols) {
               const double2 x = *reinterpret_cast<const double2*>(crow + g.col0 + jr);
@@ -590,19 +594,19 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
               cpre[e + 1] = (row_ok && jr + 1 < g.cols) ? crow[g.col0 + jr + 1] : 0.0;
             }
           }
-          if (half == 0) {
+          if (part == 0) {
             asm volatile("bar.sync 1, 128;\n" ::: "memory");  // the exponents of this tile are complete (see above)
             mbar_wait(acc_full(buf), (tile / NBUF) & 1);
             tc_fence_after();
           }
-          const unsigned t0 = tmem_base + (static_cast<unsigned>(q * 32) << 16) + buf * (LV * BN) + half * 64;
+          const unsigned t0 = tmem_base + (static_cast<unsigned>(q * 32) << 16) + buf * (LV * BN) + part * 32;
 #pragma unroll
-          for (int cb = 0; cb < 8; ++cb) {
+          for (int cb = 0; cb < 4; ++cb) {
             unsigned lv[LV][8];
 #pragma unroll
             for (int l = 0; l < LV; ++l) tc_ld8_issue(t0 + l * BN + cb * 8, lv[l]);
             tc_ld_wait();
-            if (cb == 7 && half == BN / 64 - 1) {  // every level of this set is in registers
+            if (cb == 3 && part == BN / 32 - 1) {  // every level of this set is in registers
               tc_fence_before();
               __syncwarp();
               if (lane == 0) mbar_arrive(acc_empty(buf));
@@ -616,7 +620,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
                 double sum = static_cast<double>(static_cast<int>(lv[LV - 1][e + h]));
 #pragma unroll
                 for (int l = LV - 2; l >= 0; --l) sum = fma(sum, 0.0078125, static_cast<double>(static_cast<int>(lv[l][e + h])));
-                const int col = half * 64 + cb * 8 + e + h;
+                const int col = part * 32 + cb * 8 + e + h;
                 v[h] = cpre[cb * 8 + e + h] + scaled_fast(sum, ei, pa, row_fast, eb[col], pb[col]);
               }
               if (!row_ok) continue;
@@ -665,7 +669,7 @@ __device__ __forceinline__ void oz_persist_form(const OzPArgs& g, const OzMaps& 
 // auto mode: the cheapest error-free form, decided on the device (n is even here: c goes through TMA).  Launched as clusters of
 // CX x CY CTAs, which the rectangular forms use to share operand loads; the triangular ones run every CTA on its own.
 template <int CX, int CY>
-__global__ void __launch_bounds__(OZ_THREADS, 1)
+__global__ void __launch_bounds__(OZP_THREADS, 1)
 matmul_ozaki_auto_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, const int* __restrict__ guard, int* __restrict__ ran) {
   extern __shared__ unsigned char smem_raw[];
   const int form = ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]);
@@ -674,11 +678,11 @@ matmul_ozaki_auto_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, c
     case 223: oz_persist_form<2, 2, 3, 128, 1, CX, CY>(g, maps, smem_raw); break;
     case 324: oz_persist_form<3, 2, 4, 128, 1, CX, CY>(g, maps, smem_raw); break;
     case 234: oz_persist_form<2, 3, 4, 128, 1, CX, CY>(g, maps, smem_raw); break;
-    case 335: oz_persist_form<3, 3, 5, 64, 4, CX, CY>(g, maps, smem_raw); break;
-    case 436: oz_persist_form<4, 3, 6, 64, 4, CX, CY>(g, maps, smem_raw); break;
-    case 346: oz_persist_form<3, 4, 6, 64, 4, CX, CY>(g, maps, smem_raw); break;
-    case 447: oz_persist_form<4, 4, 7, 64, 4, CX, CY>(g, maps, smem_raw); break;
-    case 555: oz_persist_form<5, 5, 5, 64, 2, 1, 1>(g, maps, smem_raw); break;
+    case 335: oz_persist_form<3, 3, 5, 64, 1, CX, CY>(g, maps, smem_raw); break;
+    case 436: oz_persist_form<4, 3, 6, 64, 1, CX, CY>(g, maps, smem_raw); break;
+    case 346: oz_persist_form<3, 4, 6, 64, 1, CX, CY>(g, maps, smem_raw); break;
+    case 447: oz_persist_form<4, 4, 7, 64, 1, CX, CY>(g, maps, smem_raw); break;
+    case 555: oz_persist_form<5, 5, 5, 64, 1, 1, 1>(g, maps, smem_raw); break;
     case 666: oz_persist_form<6, 6, 6, 64, 0, 1, 1>(g, maps, smem_raw); break;
     case 777: oz_persist_form<7, 7, 7, 64, 0, 1, 1>(g, maps, smem_raw); break;
     default: break;  // not error-free in any form: not this kernel's launch
@@ -688,7 +692,7 @@ matmul_ozaki_auto_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, c
 // a fixed triangular slice count (matmul_variant 40 .. 45: general kernels with a truncation bound, no guard); CR = 0 where c
 // cannot go through TMA (odd n) or the stage ring needs the space
 template <int S, int CR>
-__global__ void __launch_bounds__(OZ_THREADS, 1)
+__global__ void __launch_bounds__(OZP_THREADS, 1)
 matmul_ozaki_fixed_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps) {
   extern __shared__ unsigned char smem_raw[];
   oz_persist_form<S, S, S, 64, CR, 1, 1>(g, maps, smem_raw);
@@ -954,7 +958,7 @@ template <int CX, int CY> int oz_auto_max_clusters() {
   if (oz_auto_configure<CX, CY>() != cudaSuccess) return 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(static_cast<unsigned>(oz_sm_count() / (CX * CY) * (CX * CY)));
-  cfg.blockDim = dim3(OZ_THREADS);
+  cfg.blockDim = dim3(OZP_THREADS);
   cfg.dynamicSmemBytes = kOzPersistSmemMax;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -1011,7 +1015,7 @@ template <int S, int CR> cudaError_t oz_fixed_configure() {
   static PerDeviceOnce once;
   return oz_persist_configure(matmul_ozaki_fixed_kernel<S, CR>, OzPShape<S, S, S, 64, CR>::SMEM_BYTES, once);
 }
-constexpr int oz_fixed_ring(int s) { return s <= 4 ? 4 : 0;  /* chunk buffers of c where the stage ring leaves room */ }
+constexpr int oz_fixed_ring(int s) { return s <= 4 ? 1 : 0;  /* chunk buffers of c where the stage ring leaves room */ }
 
 // c as a 2-D tensor of doubles that ends at (rows_end, cols_end): box = 32 rows x 16 columns (one warp's slab), 128-byte swizzle
 bool make_c_map(CUtensorMap* map, double* c, int n, int rows_end, int cols_end) {
@@ -1063,7 +1067,7 @@ cudaError_t oz_persist_contract(double* c, void* scratch, int planes, int slices
       const int supers = ((tiles_x + cx - 1) / cx) * ((tiles_y + cy - 1) / cy);
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(static_cast<unsigned>(std::min(supers, cc.clusters) * cx * cy));
-      cfg.blockDim = dim3(OZ_THREADS);
+      cfg.blockDim = dim3(OZP_THREADS);
       cfg.dynamicSmemBytes = kOzPersistSmemMax;
       cfg.stream = stream;
       cudaLaunchAttribute attr[1];
@@ -1084,10 +1088,10 @@ cudaError_t oz_persist_contract(double* c, void* scratch, int planes, int slices
   case S:                                                                                                                                     \
     if (c_by_tma && oz_fixed_ring(S) > 0) {                                                                                                   \
       if (cudaError_t e = oz_fixed_configure<S, oz_fixed_ring(S)>(); e != cudaSuccess) return e;                                              \
-      matmul_ozaki_fixed_kernel<S, oz_fixed_ring(S)><<<grid, OZ_THREADS, OzPShape<S, S, S, 64, oz_fixed_ring(S)>::SMEM_BYTES, stream>>>(g, maps); \
+      matmul_ozaki_fixed_kernel<S, oz_fixed_ring(S)><<<grid, OZP_THREADS, OzPShape<S, S, S, 64, oz_fixed_ring(S)>::SMEM_BYTES, stream>>>(g, maps); \
     } else {                                                                                                                                  \
       if (cudaError_t e = oz_fixed_configure<S, 0>(); e != cudaSuccess) return e;                                                             \
-      matmul_ozaki_fixed_kernel<S, 0><<<grid, OZ_THREADS, OzPShape<S, S, S, 64, 0>::SMEM_BYTES, stream>>>(g, maps);           \
+      matmul_ozaki_fixed_kernel<S, 0><<<grid, OZP_THREADS, OzPShape<S, S, S, 64, 0>::SMEM_BYTES, stream>>>(g, maps);           \
     }                                                                                                                                         \
     break;
       MMX_OZ_FIXED(2)
@@ -1126,9 +1130,9 @@ cudaError_t matmul_ozaki_prepare() {
   if (cudaError_t e = oz_fixed_configure<2, 0>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_fixed_configure<3, 0>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_fixed_configure<4, 0>(); e != cudaSuccess) return e;
-  if (cudaError_t e = oz_fixed_configure<2, 4>(); e != cudaSuccess) return e;
-  if (cudaError_t e = oz_fixed_configure<3, 4>(); e != cudaSuccess) return e;
-  if (cudaError_t e = oz_fixed_configure<4, 4>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_fixed_configure<2, 1>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_fixed_configure<3, 1>(); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_fixed_configure<4, 1>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_fixed_configure<5, 0>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_fixed_configure<6, 0>(); e != cudaSuccess) return e;
   return oz_fixed_configure<7, 0>();
