@@ -11,24 +11,25 @@
 // S = 7 -- below what FP64 accumulation over K terms itself guarantees -- and ZERO whenever the operands carry <= 7S bits
 // below their row maximum: on the application's inputs ((i +- k) / N, 14 bits) the result is bit-identical to the CPU program.
 //
-// Who runs it.  matmul_variant 40 / 41: always, with S = 7 / 6 (general kernels: ~2^-49 / ~2^-42 of K max max).  Auto mode
-// (variant 0, N >= 1024; launch_matmul<double> in matmul.cu): only where it is ERROR-FREE.  The slice pass records in a device
-// guard whether any element was cut at 7 digits and the highest digit in use per operand; the 6-slice contraction, the 7-slice
-// contraction and the FP64-pipe kernel are all enqueued and read the guard: the cheapest error-free form runs, the others leave.
+// Who runs it.  matmul_variant 40 .. 45: always, as the triangular form with S = 7 .. 2 slices (general kernels: ~2^-49 .. of
+// K max max).  Auto mode (variant 0, N >= 1024; launch_matmul<double> in matmul.cu): only where it is ERROR-FREE.  The slice pass
+// records in a device guard whether any element was cut at 7 digits and the highest digit in use per operand; ONE persistent launch
+// reads the guard and runs the cheapest error-free form (rectangular SA x SB digit pairs up to four digits per operand, the
+// triangular 5 / 6 / 7-slice forms beyond), or leaves at once, in which case the FP64-pipe kernel enqueued behind it runs
+// (ozaki_pick_form in kernels.cuh is the rule; mmx_gene8_form reports the choice).
 //
-// Kernel (one CTA per 128 x 64 tile of c, 1 CTA per SM, the S level accumulators of the tile live in TMEM for the whole
-// K loop -- S * 64 <= 448 columns -- so there is no mid-loop drain at all):
-//   slice pass  x -> P int8 planes [t][row][k] + one exponent per row (+ the guard)  ((8 + P) N^2 bytes per operand)
-//   warp 0      TMA producer: per 64-k stage ONE 3-D box per operand brings the S slices in use ([t][row][64 B], SWIZZLE_64B);
-//               2 stages of 84 KB for S = 7, 3 stages of 72 KB for S = 6 (optionally the a slices are multicast over a cluster
-//               of column tiles)
-//   warp 1      MMA issuer: per 32 k, for t = 1..S: a_t against the slices b_1..b_(S+1-t) STACKED along N (they are
-//               contiguous in shared memory, and their products belong to consecutive levels = consecutive TMEM column
-//               blocks), split into instructions of N <= 256: 10 MMAs carry the 28 slice products of S = 7, 8 the 21 of S = 6
-//   warps 2-5   epilogue: the tile's incoming c and column exponents are fetched before the K loop ends; then L_g -> FP64
-//               Horner sum -> exact scaling by 2^(ea_i + eb_j - 12) (ldexp) -> c += .
-// Measured on B200, slice passes included (profiles/r1d_*): S = 7 96 / 110 / 119 TFLOP/s of FP64 work at N = 4096 / 8192 /
-// 16384; S = 6 as auto mode runs it on the application 133 / 161 / 178 (contraction alone 3.24 POP/s at N = 4096); DMMA 34-35.
+// Kernels, in file order:
+//   matmul_ozaki_kernel<S, C, BK>   the first version, one CTA per 128 x 64 tile (MMX_OZ_LEGACY=1; kept as the A/B reference
+//                                   and for its cluster / stage-width tuning hooks)
+//   oz_persist_body<SA, SB, LV, BN, CR, CX, CY>   the persistent form described at its definition: one CTA per SM walks the
+//                                   tiles; warp 0 = TMA producer, warp 1 = MMA issuer, warps 2-9 = epilogue.  Per 32 k, slice
+//                                   a_t meets the slices b_1..b_count STACKED along N (contiguous in shared memory, products of
+//                                   consecutive levels = consecutive TMEM column blocks) in instructions of N <= 256; the level
+//                                   accumulators of a tile stay in TMEM for the whole K loop; the epilogue turns the levels into
+//                                   one integer, scales by exponent arithmetic and adds into c with TMA reductions
+//   ozaki_slice_kernel<S>           x -> int8 digit planes [t][row][k] + one exponent per row (+ the guard)
+// Measured on B200 (profiles/r1e_*), whole application N = 4096 / 8192 / 16384: 334 / 421 / 301 TFLOP/s of FP64 work with the
+// forms 2x2 / 3x2 / 3x3 the operands allow (first version, 6-slice triangular form for all: 119 / 151 / 172); DMMA 33-35.
 #include <algorithm>
 #include <cstdlib>
 
