@@ -309,6 +309,7 @@ struct OzPArgs {
   double* c;
   const int *exp_a, *exp_b;
   int n, kq, row0, rows, col0, cols, group;
+  long long group_l2_bytes;  // budget for a raster group's rows of a (0: default; MMX_OZ_GROUP_MB overrides -- tuning hook)
 };
 
 // sum * 2^(ea + eb - 12).  Fast path (both exponents moderate): two multiplications by exact powers of two, pa = 2^(ea - 12)
@@ -354,7 +355,12 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
   const int supers = super_x * super_y;
   const int first = static_cast<int>(blockIdx.x) / C, stride = static_cast<int>(gridDim.x) / C;
   const int my_tiles = first < supers ? (supers - 1 - first) / stride + 1 : 0;
-  const int group = g.group / CY > 0 ? g.group / CY : 1;
+  // tile-rows per raster group: the group's rows of a (SA planes) are meant to stay in the 126 MB L2 while bt streams by, so
+  // the group shrinks when they would not fit (g.group = 16 tile-rows = 100 MB at N = 16384 with three planes, 200 MB at 32768)
+  const long long strip_bytes = static_cast<long long>(OZ_BM) * g.kq * SA;
+  const int fit = static_cast<int>((g.group_l2_bytes > 0 ? g.group_l2_bytes : (64ll << 20)) / strip_bytes);
+  const int rows_per_group = fit < g.group ? (fit > 2 ? fit : 2) : g.group;
+  const int group = rows_per_group / CY > 0 ? rows_per_group / CY : 1;
   auto tile_at = [&](int k, int& bx, int& by) {  // the k-th tile of this CTA
     int sx, sy;
     raster_map(group, super_x, super_y, first + k * stride, sx, sy);
@@ -1058,6 +1064,8 @@ cudaError_t oz_persist_contract(double* c, void* scratch, int planes, int slices
   g.col0 = col0;
   g.cols = cols;
   g.group = raster_group(OZ_BM, static_cast<size_t>(L.kq));
+  static const long long group_mb = [] { const char* e = getenv("MMX_OZ_GROUP_MB"); return e ? atoll(e) : 0ll; }();
+  g.group_l2_bytes = group_mb << 20;
   // the grid covers the 64-wide tiling (the forms with 128-wide tiles leave the surplus CTAs without a tile)
   const int tiles_x = (cols + 63) / 64, tiles_y = (rows + OZ_BM - 1) / OZ_BM;
   const dim3 grid(static_cast<unsigned>(std::min(tiles_x * tiles_y, oz_sm_count())));
