@@ -247,6 +247,12 @@ MMX_API int mmx_device_ptr(mmx_ctx* ctx, int slot, int array, void** ptr_out);
  * pipe (the slices would not have been error-free), -1 = no such launch yet / not an FP64 auto-mode context.  Synchronises the slot. */
 MMX_API int mmx_gene8_form(mmx_ctx* ctx, int slot, int32_t* form_out);
 
+/* FP64 auto-mode contexts: time the CONTRACTION of gene 8 alone (mmx_time_loop(8) times the whole nest: two slice passes, the
+ * contraction, the guarded FP64-pipe launch).  One full launch encodes the operands; each of the `iters` timed launches reuses the
+ * digit planes and runs the contraction kernel plus the guarded FP64-pipe launch (c accumulates).  CUDA events on the slot's stream,
+ * L2 flushed before each launch when flush_l2 != 0; ms_out = mean per launch.  The roofline of the dominant kernel (bench.py). */
+MMX_API int mmx_time_gene8_contraction(mmx_ctx* ctx, int slot, int iters, int flush_l2, double* ms_out);
+
 /* The rule behind mmx_gene8_form, evaluated on the host (no device needed): the form the auto launch takes for operands of which
  * `cut` != 0 says some element has bits below its 7th digit, and top_a / top_bt are the highest non-zero 7-bit digits (1-based)
  * anywhere in a / bt.  Returns 100 SA + 10 SB + levels, or 0 for the FP64 pipe. */

@@ -114,6 +114,7 @@ _SIGNATURES = {
     "mmx_device_ptr": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.POINTER(C.c_void_p)]),
     "mmx_gene8_form": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int32)]),
     "mmx_gene8_pick_form": (C.c_int, [C.c_int, C.c_int, C.c_int]),
+    "mmx_time_gene8_contraction": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "mmx_shard_run_local": (C.c_int, [C.c_void_p, C.POINTER(C.c_int32), C.c_int, C.POINTER(ShardStats), C.POINTER(C.c_double)]),
     "mmx_shard_export": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(ShardHandle)]),
     "mmx_shard_bind": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.POINTER(ShardHandle), C.POINTER(C.c_int32)]),
@@ -293,6 +294,12 @@ class Context:
         v = C.c_int32()
         self._check(self._lib.mmx_gene8_form(self._h, slot, C.byref(v)))
         return v.value
+
+    def time_gene8_contraction(self, iters: int = 5, flush_l2: bool = True, slot: int = 0) -> float:
+        """ms per launch of the gene-8 contraction alone (FP64 auto mode): operands encoded once, reused by the timed launches."""
+        ms = C.c_double()
+        self._check(self._lib.mmx_time_gene8_contraction(self._h, slot, iters, int(flush_l2), C.byref(ms)))
+        return ms.value
 
     def device_ptr(self, array: int, slot: int = 0) -> int:
         p = C.c_void_p()

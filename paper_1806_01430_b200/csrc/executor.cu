@@ -814,6 +814,38 @@ MMX_API int mmx_device_ptr(mmx_ctx* ctx, int slot, int array, void** ptr_out) {
   return MMX_OK;
 }
 
+MMX_API int mmx_time_gene8_contraction(mmx_ctx* ctx, int slot, int iters, int flush_l2, double* ms_out) {
+  if (ctx == nullptr || ms_out == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size()) || iters < 1) return MMX_E_INVALID;
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  if (!s.gene8_form_valid) return MMX_E_INVALID;  // FP64 auto-mode contexts only
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  const int n = ctx->cfg.n;
+  double *a = static_cast<double*>(s.d_arr[MMX_ARRAY_A]), *bt = static_cast<double*>(s.d_arr[MMX_ARRAY_BT]), *c = static_cast<double*>(s.d_arr[MMX_ARRAY_C]);
+  // one full launch encodes the operands (and tells which form they take); the timed ones reuse the encoding
+  MMX_CUDA(ctx, launch_matmul<double>(c, a, bt, n, 0, n, 0, n, false, 0, s.d_scratch, s.stream));
+  if (flush_l2 && s.d_scrub == nullptr) {
+    s.scrub_bytes = std::size_t{256} << 20;  // 256 MiB > 126 MB L2
+    MMX_CUDA(ctx, cudaMalloc(&s.d_scrub, s.scrub_bytes));
+    MMX_CUDA(ctx, launch_scrub(s.d_scrub, s.scrub_bytes, s.stream));
+  }
+  double total = 0.0;
+  for (int it = 0; it < iters; ++it) {
+    if (flush_l2) MMX_CUDA(ctx, launch_evict(s.d_scrub, s.scrub_bytes, s.stream));
+    MMX_CUDA(ctx, cudaEventRecord(s.ev_begin, s.stream));
+    MMX_CUDA(ctx, launch_matmul<double>(c, a, bt, n, 0, n, 0, n, false, kReuseOperands, s.d_scratch, s.stream));
+    MMX_CUDA(ctx, cudaEventRecord(s.ev_end, s.stream));
+    MMX_CUDA(ctx, cudaEventSynchronize(s.ev_end));
+    float ms = 0.f;
+    MMX_CUDA(ctx, cudaEventElapsedTime(&ms, s.ev_begin, s.ev_end));
+    total += ms;
+  }
+  s.dev_valid[MMX_ARRAY_C] = true;
+  s.host_valid[MMX_ARRAY_C] = false;
+  *ms_out = total / iters;
+  return MMX_OK;
+}
+
 MMX_API int mmx_gene8_pick_form(int cut, int top_a, int top_bt) { return ozaki_pick_form(cut, top_a, top_bt); }
 
 MMX_API int mmx_gene8_form(mmx_ctx* ctx, int slot, int32_t* form_out) {

@@ -112,8 +112,11 @@ inline int ozaki_pick_form(int cut, int top_a, int top_b) {
 // OR-ed into `variant`: the rows [row0, row0 + rows) of a were already re-encoded into `scratch` by the previous launch_matmul
 // on it (the row-sharded run contracts the same rows of a against one column block after another)
 constexpr int kReuseOperandA = 0x1000;
+// OR-ed into `variant` (FP64 auto mode): BOTH operands are as the previous launch_matmul on this scratch encoded them -- the launch is
+// the contraction (and the guarded FP64-pipe launch) alone.  For timing the contraction kernel by itself (mmx_time_gene8_contraction).
+constexpr int kReuseOperands = 0x2000;
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0,
-                                int cols, int slices, cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false);
+                                int cols, int slices, cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false, bool reuse_bt = false);
 // device word in `scratch` where the auto launch records the form it ran: 2 .. 7 slices, 0 = left to the FP64 pipe
 int* matmul_ozaki_form_word(void* scratch, int n);
 // gene 9: row i of the same (GEMV against bt)

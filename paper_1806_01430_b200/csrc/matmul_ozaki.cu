@@ -296,7 +296,10 @@ template <int SA, int SB, int LV, int BN, int CR> struct OzPShape {
   static constexpr int C_SLAB = 32 * 16 * 8;      // 32 rows x 16 doubles = one 128-byte-swizzled TMA box
   static constexpr int EPI_WARPS = CR > 0 ? 8 : 4;
   static constexpr int C_BYTES = CR * 8 * C_SLAB;
-  static constexpr int TAIL = 3584;               // barriers, column exponents and scale factors
+  // barriers (256 B), column exponents [2][BN] int, and -- where the epilogue multiplies instead of adding to the exponent field --
+  // the column scale factors [2][BN] double
+  static constexpr bool SCALE_TABLE = !(CR > 0 && LV <= 4);
+  static constexpr int TAIL = SCALE_TABLE ? 3584 : 1536;
   static constexpr int STAGES_FIT = (227 * 1024 - 1024 - TAIL - C_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
   static_assert(STAGES >= 2, "stage ring");
@@ -503,7 +506,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
         if (grp == 0 && r < BN) {
           const int e = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
           eb[r] = e;
-          pb[r] = pow2(e > -400 && e < 400 ? e : 0);
+          if constexpr (Sh::SCALE_TABLE) pb[r] = pow2(e > -400 && e < 400 ? e : 0);
         }
         // the exponents of this tile are complete; nobody is still reading the other copy (that was two tiles ago, and
         // everyone has passed the barrier of the tile in between)
@@ -1155,7 +1158,7 @@ size_t matmul_ozaki_scratch_bytes(int n) {
 int* matmul_ozaki_form_word(void* scratch, int n) { return scratch == nullptr ? nullptr : OzLayout(scratch, n, 7).guard + 4; }
 
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                int slices, cudaStream_t stream, int** guard_out, bool reuse_a) {
+                                int slices, cudaStream_t stream, int** guard_out, bool reuse_a, bool reuse_bt) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr) return cudaErrorInvalidValue;
   // MMX_OZ_LEGACY=1: the one-tile-per-CTA kernels of the first version (A/B comparison, tools/ozaki_cluster_sweep.sh)
@@ -1164,7 +1167,8 @@ cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, vo
     // auto mode: 7 digit planes and the guard once, then ONE persistent launch that reads the guard and runs the cheapest
     // error-free form (2 .. 7 slices) or nothing; the caller adds the FP64-pipe kernel under the remaining condition
     *guard_out = OzLayout(scratch, n, 7).guard;
-    if (cudaError_t e = oz_slices<7>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a); e != cudaSuccess) return e;
+    if (!(reuse_a && reuse_bt))  // both reused: the digit planes and the guard stand as the previous launch left them
+      if (cudaError_t e = oz_slices<7>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a); e != cudaSuccess) return e;
     if (!legacy) return oz_persist_contract(c, scratch, 7, 0, n, row0, rows, col0, cols, stream);
     if (cudaError_t e = oz_contract<6, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true); e != cudaSuccess) return e;
     return oz_contract<7, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true);

@@ -511,6 +511,26 @@ def test_fp64_auto_digit_planes_stay_consistent_from_launch_to_launch():
         assert ran == 324 and bits_equal(got, (a.astype(np.int64) @ bt.astype(np.int64).T).astype(np.float64))
 
 
+def test_time_gene8_contraction_reuses_the_encoded_operands():
+    """mmx_time_gene8_contraction: one full launch, then launches of the contraction alone on the same digit planes; c
+    accumulates one product per launch, and the contraction alone is faster than the whole nest."""
+    n = 1024
+    rs = np.random.RandomState(3)
+    a, bt = (rs.randint(-2 ** 12, 2 ** 12, (n, n)).astype(np.float64) for _ in range(2))
+    with capi.Context(n=n, dtype=capi.F64) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, np.zeros((n, n)))
+        ms_k = ctx.time_gene8_contraction(3, False)
+        assert ctx.gene8_form() == 223
+        assert bits_equal(ctx.fetch(capi.ARRAY_C), 4.0 * (a @ bt.T))          # 1 + 3 launches, integers: exact
+        ms_nest = ctx.time_loop(8, 3, False)
+        assert 0.0 < ms_k < ms_nest
+    with capi.Context(n=n, dtype=capi.F64, matmul_variant=4) as ctx:
+        with pytest.raises(capi.MmxError):
+            ctx.time_gene8_contraction(1, False)
+
+
 def test_fp64_auto_form_on_the_application():
     """(i +- k) / N at N = 2^p carries log2(N) + 2 bits: two digits per operand up to N = 4096 -> the 2 x 2 form, 4 slice
     products per term instead of the 28 of the widest form; the whole individual stays bit-identical to the CPU program."""
