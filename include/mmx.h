@@ -242,9 +242,11 @@ MMX_API int mmx_run_loop_rows(mmx_ctx* ctx, int slot, int gene, int row0, int ro
  * can exchange it in place (the all-gather of bt); valid until mmx_destroy. */
 MMX_API int mmx_device_ptr(mmx_ctx* ctx, int slot, int array, void** ptr_out);
 
-/* Which form the last FP64 auto-mode launch of gene 8 on this slot took (decided on the device from the operands, csrc/matmul_ozaki.cu):
- * 2 .. 7 = INT8 tensor cores with that many exact 7-bit slices per operand (3 .. 28 slice products per term), 0 = the FP64
- * pipe (the slices would not have been error-free), -1 = no such launch yet / not an FP64 auto-mode context.  Synchronises the slot. */
+/* Which form the last auto-mode launch of gene 8 on this slot took (decided on the device from the operands, csrc/matmul_ozaki.cu;
+ * FP64, and FP32 -- where the fallback is split TF32 instead of the FP64 pipe):
+ * 100 SA + 10 SB + levels = INT8 tensor cores, digits a_1..a_SA against b_1..b_SB (223 = 2 x 2 pairs, 4 slice products per term;
+ * 777 = the widest triangular form, 28), 0 = the FP64 pipe / split TF32 (no form would have been error-free), -1 = no such launch
+ * yet / not an auto-mode context with N >= 1024.  Synchronises the slot. */
 MMX_API int mmx_gene8_form(mmx_ctx* ctx, int slot, int32_t* form_out);
 
 /* FP64 auto-mode contexts: time the CONTRACTION of gene 8 alone (mmx_time_loop(8) times the whole nest: two slice passes, the

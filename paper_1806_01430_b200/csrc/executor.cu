@@ -48,7 +48,8 @@ struct Slot {
   void* d_scrub = nullptr;
   std::size_t scrub_bytes = 0;
   void* d_scratch = nullptr;  // operands re-encoded for the tensor-core contractions (FP32: matmul_tc.cu; FP64: matmul_ozaki.cu)
-  bool gene8_form_valid = false;  // FP64 auto mode: the scratch carries the word mmx_gene8_form reads
+  bool gene8_form_valid = false;  // FP64 auto mode (mmx_time_gene8_contraction applies)
+  int* gene8_form_word = nullptr;  // auto mode, either precision: the device word mmx_gene8_form reads
   bool host_valid[MMX_NUM_ARRAYS] = {};
   bool dev_valid[MMX_NUM_ARRAYS] = {};
   bool host_diag_only = false;  // host c holds only its diagonal
@@ -630,7 +631,18 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
         (cfg->matmul_variant == 30 || cfg->matmul_variant == 31 || (cfg->matmul_variant == 0 && cfg->n >= kTcMinN)))
     {
       if ((e = matmul_3xtf32_prepare()) != cudaSuccess) return fail(e, "matmul_3xtf32_prepare");
-      if ((e = cudaMalloc(&sl.d_scratch, matmul_3xtf32_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
+      if (cfg->matmul_variant == 0 && fp32_int8_enabled(cfg->n)) {
+        // FP32 auto mode: the split-TF32 area, then the digit planes of the INT8 forms (zero-filled: matmul_ozaki.cu)
+        const std::size_t off = fp32_int8_scratch_offset(cfg->n), planes = matmul_ozaki_scratch_bytes(cfg->n);
+        if ((e = matmul_ozaki_prepare()) != cudaSuccess) return fail(e, "matmul_ozaki_prepare");
+        if ((e = cudaMalloc(&sl.d_scratch, off + planes)) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
+        void* oz = static_cast<char*>(sl.d_scratch) + off;
+        if ((e = cudaMemset(oz, 0, planes)) != cudaSuccess) return fail(e, "cudaMemset(scratch)");
+        sl.gene8_form_word = matmul_ozaki_form_word(oz, cfg->n);
+        if ((e = cudaMemset(sl.gene8_form_word, 0xff, sizeof(int))) != cudaSuccess) return fail(e, "cudaMemset(form)");
+      } else if ((e = cudaMalloc(&sl.d_scratch, matmul_3xtf32_scratch_bytes(cfg->n))) != cudaSuccess) {
+        return fail(e, "cudaMalloc(scratch)");
+      }
     }
     if (cfg->dtype == MMX_F64 && cfg->numerics == MMX_NUMERICS_FAST && matmul_ozaki_usable(cfg->n) &&
         ((cfg->matmul_variant >= 40 && cfg->matmul_variant <= 45) || (cfg->matmul_variant == 0 && cfg->n >= kOzMinN))) {
@@ -639,7 +651,8 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
       if (cfg->matmul_variant == 0) {
         // auto mode relies on a zero-filled scratch (digit planes nobody has written yet are zero, matmul_ozaki.cu)
         if ((e = cudaMemset(sl.d_scratch, 0, matmul_ozaki_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMemset(scratch)");
-        if ((e = cudaMemset(matmul_ozaki_form_word(sl.d_scratch, cfg->n), 0xff, sizeof(int))) != cudaSuccess) return fail(e, "cudaMemset(form)");
+        sl.gene8_form_word = matmul_ozaki_form_word(sl.d_scratch, cfg->n);
+        if ((e = cudaMemset(sl.gene8_form_word, 0xff, sizeof(int))) != cudaSuccess) return fail(e, "cudaMemset(form)");
         sl.gene8_form_valid = true;
       }
     }
@@ -853,10 +866,10 @@ MMX_API int mmx_gene8_form(mmx_ctx* ctx, int slot, int32_t* form_out) {
   Slot& s = *ctx->slots[slot];
   std::lock_guard<std::mutex> g(s.mu);
   *form_out = -1;
-  if (!s.gene8_form_valid) return MMX_OK;
+  if (s.gene8_form_word == nullptr) return MMX_OK;
   MMX_CUDA(ctx, cudaSetDevice(s.device));
   MMX_CUDA(ctx, cudaStreamSynchronize(s.stream));
-  MMX_CUDA(ctx, cudaMemcpy(form_out, matmul_ozaki_form_word(s.d_scratch, ctx->cfg.n), sizeof(int32_t), cudaMemcpyDeviceToHost));
+  MMX_CUDA(ctx, cudaMemcpy(form_out, s.gene8_form_word, sizeof(int32_t), cudaMemcpyDeviceToHost));
   return MMX_OK;
 }
 

@@ -69,7 +69,7 @@ size_t matmul_3xtf32_scratch_bytes(int n);
 cudaError_t matmul_3xtf32_prepare();  // per device, before the first launch (not inside a stream capture)
 // wide: 128 x 256 tile with plain FP32 masters (faster, looser); default 128 x 128 with compensated masters
 cudaError_t launch_matmul_3xtf32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0,
-                                 int cols, bool wide, cudaStream_t stream, bool reuse_a = false);
+                                 int cols, bool wide, cudaStream_t stream, bool reuse_a = false, const int* run_if = nullptr);
 // FP64 on the 5th-generation tensor cores as exact INT8 slice products (Ozaki scheme, matmul_ozaki.cu); `slices` = 7 (default,
 // |error| <= 2e-14 K max|a| max|b|, bit-identical on the application's inputs) or 6
 bool matmul_ozaki_usable(int n);
@@ -109,6 +109,20 @@ inline int ozaki_pick_form(int cut, int top_a, int top_b) {
   return 0;
 }
 
+// FP32 auto mode has the forms whose epilogue is the TMA reduction (all but the 6 / 7-slice ones); beyond them: split TF32
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline int ozaki_pick_form_f32(int cut, int top_a, int top_b) {
+  const int f = ozaki_pick_form(cut, top_a, top_b);
+  return (f == 666 || f == 777) ? 0 : f;
+}
+
+// FP32 auto mode (variant 0, FAST, n >= kOzMinN, n % 4 == 0): the INT8 forms first, split TF32 as the guarded fallback.  The
+// context's scratch then holds the split-TF32 area followed (1 KB aligned) by the digit planes.  MMX_F32_INT8=0 switches it off.
+bool fp32_int8_enabled(int n);
+size_t fp32_int8_scratch_offset(int n);
+
 // OR-ed into `variant`: the rows [row0, row0 + rows) of a were already re-encoded into `scratch` by the previous launch_matmul
 // on it (the row-sharded run contracts the same rows of a against one column block after another)
 constexpr int kReuseOperandA = 0x1000;
@@ -117,6 +131,8 @@ constexpr int kReuseOperandA = 0x1000;
 constexpr int kReuseOperands = 0x2000;
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0,
                                 int cols, int slices, cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false, bool reuse_bt = false);
+cudaError_t launch_matmul_ozaki_f32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
+                                    cudaStream_t stream, int** guard_out, bool reuse_a = false);
 // device word in `scratch` where the auto launch records the form it ran: 2 .. 7 slices, 0 = left to the FP64 pipe
 int* matmul_ozaki_form_word(void* scratch, int n);
 // gene 9: row i of the same (GEMV against bt)

@@ -501,6 +501,12 @@ cudaError_t dmma_go(double* c, const double* a, const double* bt, int n, int row
 
 }  // namespace
 
+bool fp32_int8_enabled(int n) {
+  static const int on = [] { const char* e = getenv("MMX_F32_INT8"); return e ? atoi(e) : 1; }();
+  return on != 0 && n >= kOzMinN && n % 4 == 0 && matmul_ozaki_usable(n) && matmul_3xtf32_usable(n);
+}
+size_t fp32_int8_scratch_offset(int n) { return (matmul_3xtf32_scratch_bytes(n) + 1023) / 1024 * 1024; }
+
 int raster_group(int /*tile_m*/, size_t /*row_bytes*/) {
   static const int forced = [] { const char* e = getenv("MMX_RASTER_GROUP"); return e ? atoi(e) : 0; }();  // tuning hook
   // measured (tools/raster_sweep.sh, profiles/r1d_raster.txt): 16 tile-rows per group minimises DRAM traffic for both
@@ -559,6 +565,16 @@ cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int 
                                  bool strict, int variant, void* scratch, cudaStream_t stream) {
   const bool reuse_a = (variant & kReuseOperandA) != 0;
   variant &= ~kReuseOperandA;
+  // auto, large matrices: the INT8 tensor cores exactly when their digit products are error-free for the operands at hand (one
+  // rounding to float at the end: closer to the exact product than any FP32 accumulation), split TF32 otherwise -- the same
+  // device-side guard as in FP64 (matmul_ozaki.cu); the split-TF32 launches read it and leave when the product has been taken
+  if (!strict && scratch != nullptr && variant == 0 && fp32_int8_enabled(n)) {
+    int* guard = nullptr;
+    void* planes = static_cast<char*>(scratch) + fp32_int8_scratch_offset(n);
+    if (cudaError_t e = launch_matmul_ozaki_f32(c, a, bt, planes, n, row0, rows, col0, cols, stream, &guard, reuse_a); e != cudaSuccess) return e;
+    // (a fallback launch always re-splits its rows of a: the earlier column block may have gone the INT8 way)
+    return launch_matmul_3xtf32(c, a, bt, scratch, n, row0, rows, col0, cols, false, stream, false, guard);
+  }
   // tensor cores (split-precision TF32, matmul_tc.cu): large matrices by default, any n % 4 == 0 on request
   if (!strict && scratch != nullptr && n % 4 == 0 && (variant == 30 || variant == 31 || (variant == 0 && n >= kTcMinN)))
     return launch_matmul_3xtf32(c, a, bt, scratch, n, row0, rows, col0, cols, variant == 31, stream, reuse_a);

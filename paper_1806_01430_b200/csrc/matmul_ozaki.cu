@@ -309,7 +309,7 @@ template <int SA, int SB, int LV, int BN, int CR> struct OzPShape {
 constexpr int kOzPersistSmemMax = 227 * 1024;  // the auto kernel asks for all of it: each form uses what its rings need
 
 struct OzPArgs {
-  double* c;
+  void* c;  // double (or float: the FP32 auto mode, reduction epilogue only)
   const int *exp_a, *exp_b;
   int n, kq, row0, rows, col0, cols, group;
   long long group_l2_bytes;  // budget for a raster group's rows of a (0: default; MMX_OZ_GROUP_MB overrides -- tuning hook)
@@ -326,7 +326,7 @@ __device__ __forceinline__ double scaled_fast(double sum, int ea, double pa, boo
 // (each of its CX CTAs loads 128 / CX rows of every slice and multicasts them), the bt slices of a column tile once per cluster
 // column.  The operand traffic is what bounds the short forms (the 2 x 2 form at 128 x 128 needs 32 KB per 512 tensor-pipe
 // clocks and SM: 8.3 TB/s measured against the 11.8 TB/s the L2 can put on the crossbar); a 2 x 2 cluster halves it.
-template <int SA, int SB, int LV, int BN, int CR, int CX, int CY>
+template <int SA, int SB, int LV, int BN, int CR, int CX, int CY, typename CT = double>
 __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensorMap* map_a, const CUtensorMap* map_b, const CUtensorMap* map_c,
                                                 unsigned char* smem_raw) {
   using Sh = OzPShape<SA, SB, LV, BN, CR>;
@@ -553,10 +553,20 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
           const unsigned slab = slab0 + (sent % CR) * (8 * Sh::C_SLAB);
           if (lane == 0) tma_store_wait_read<CR - 1>();  // the reduction that last used this slab has left shared memory
           __syncwarp();
-          const unsigned crow = slab + lane * 128;
+          if constexpr (sizeof(CT) == 8) {
+            const unsigned crow = slab + lane * 128;
 #pragma unroll
-          for (int ch = 0; ch < 8; ++ch)
-            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(crow + ((ch ^ (lane & 7)) << 4)), "d"(v[2 * ch]), "d"(v[2 * ch + 1]) : "memory");
+            for (int ch = 0; ch < 8; ++ch)
+              asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(crow + ((ch ^ (lane & 7)) << 4)), "d"(v[2 * ch]), "d"(v[2 * ch + 1]) : "memory");
+          } else {
+            // FP32 output: the exact value rounded ONCE to float; 64-byte rows under SWIZZLE_64B (16-byte piece ^ bits 1-2 of the row)
+            const unsigned crow = slab + lane * 64;
+#pragma unroll
+            for (int ch = 0; ch < 4; ++ch)
+              asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(crow + ((ch ^ ((lane >> 1) & 3)) << 4)), "f"(static_cast<float>(v[4 * ch])),
+                           "f"(static_cast<float>(v[4 * ch + 1])), "f"(static_cast<float>(v[4 * ch + 2])), "f"(static_cast<float>(v[4 * ch + 3]))
+                           : "memory");
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -567,6 +577,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
       }
       if (lane == 0) tma_store_wait<0>();
     } else {
+      static_assert(sizeof(CT) == 8, "the register epilogue exists for FP64 only");
       // c straight from registers (any n, odd ones included): 64 columns at a time; the first 64 incoming values and the
       // tile's column exponents are fetched before the tile's MMAs are waited for
       const bool vec_ok = (g.n % 2 == 0) && (g.col0 % 2 == 0);
@@ -580,7 +591,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
         const int ei = row_ok ? g.exp_a[m] : 0;  // kNonFinite marks a row that holds an Inf or a NaN
         const bool row_fast = ei > -400 && ei < 400;
         const double pa = pow2(row_fast ? ei - 12 : 0);
-        double* crow = g.c + static_cast<size_t>(row_ok ? m : 0) * g.n;
+        double* crow = static_cast<double*>(g.c) + static_cast<size_t>(row_ok ? m : 0) * g.n;
         int* eb = eb_sh + (tile & 1) * BN;
         double* pb = pb_sh + (tile & 1) * BN;
         if (r < BN) {
@@ -671,31 +682,34 @@ template <int ROWS> __device__ __forceinline__ const CUtensorMap* oz_map_b(const
   static_assert(ROWS == 128 || ROWS == 64 || ROWS == 32, "bt box");
   return ROWS == 128 ? &m.b128 : ROWS == 64 ? &m.b64 : &m.b32;
 }
-template <int SA, int SB, int LV, int BN, int CR, int CX, int CY>
+template <int SA, int SB, int LV, int BN, int CR, int CX, int CY, typename CT = double>
 __device__ __forceinline__ void oz_persist_form(const OzPArgs& g, const OzMaps& m, unsigned char* smem_raw) {
-  oz_persist_body<SA, SB, LV, BN, CR, CX, CY>(g, oz_map_a<OZ_BM / CX>(m), oz_map_b<BN / CY>(m), &m.c, smem_raw);
+  oz_persist_body<SA, SB, LV, BN, CR, CX, CY, CT>(g, oz_map_a<OZ_BM / CX>(m), oz_map_b<BN / CY>(m), &m.c, smem_raw);
 }
 
 // auto mode: the cheapest error-free form, decided on the device (n is even here: c goes through TMA).  Launched as clusters of
 // CX x CY CTAs, which the rectangular forms use to share operand loads; the triangular ones run every CTA on its own.
-template <int CX, int CY>
+template <int CX, int CY, typename CT>
 __global__ void __launch_bounds__(OZP_THREADS, 1)
 matmul_ozaki_auto_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, const int* __restrict__ guard, int* __restrict__ ran) {
   extern __shared__ unsigned char smem_raw[];
-  const int form = ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]);
+  const int form = sizeof(CT) == 8 ? ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]) : ozaki_pick_form_f32(guard[0] | guard[3], guard[1], guard[2]);
   if (blockIdx.x == 0 && threadIdx.x == 0) *ran = form;
   switch (form) {
-    case 223: oz_persist_form<2, 2, 3, 128, 1, CX, CY>(g, maps, smem_raw); break;
-    case 324: oz_persist_form<3, 2, 4, 128, 1, CX, CY>(g, maps, smem_raw); break;
-    case 234: oz_persist_form<2, 3, 4, 128, 1, CX, CY>(g, maps, smem_raw); break;
-    case 335: oz_persist_form<3, 3, 5, 64, 1, CX, CY>(g, maps, smem_raw); break;
-    case 436: oz_persist_form<4, 3, 6, 64, 1, CX, CY>(g, maps, smem_raw); break;
-    case 346: oz_persist_form<3, 4, 6, 64, 1, CX, CY>(g, maps, smem_raw); break;
-    case 447: oz_persist_form<4, 4, 7, 64, 1, CX, CY>(g, maps, smem_raw); break;
-    case 555: oz_persist_form<5, 5, 5, 64, 1, 1, 1>(g, maps, smem_raw); break;
-    case 666: oz_persist_form<6, 6, 6, 64, 0, 1, 1>(g, maps, smem_raw); break;
-    case 777: oz_persist_form<7, 7, 7, 64, 0, 1, 1>(g, maps, smem_raw); break;
-    default: break;  // not error-free in any form: not this kernel's launch
+    case 223: oz_persist_form<2, 2, 3, 128, 1, CX, CY, CT>(g, maps, smem_raw); break;
+    case 324: oz_persist_form<3, 2, 4, 128, 1, CX, CY, CT>(g, maps, smem_raw); break;
+    case 234: oz_persist_form<2, 3, 4, 128, 1, CX, CY, CT>(g, maps, smem_raw); break;
+    case 335: oz_persist_form<3, 3, 5, 64, 1, CX, CY, CT>(g, maps, smem_raw); break;
+    case 436: oz_persist_form<4, 3, 6, 64, 1, CX, CY, CT>(g, maps, smem_raw); break;
+    case 346: oz_persist_form<3, 4, 6, 64, 1, CX, CY, CT>(g, maps, smem_raw); break;
+    case 447: oz_persist_form<4, 4, 7, 64, 1, CX, CY, CT>(g, maps, smem_raw); break;
+    case 555: oz_persist_form<5, 5, 5, 64, 1, 1, 1, CT>(g, maps, smem_raw); break;
+    default:
+      if constexpr (sizeof(CT) == 8) {  // the 6 / 7-slice forms keep the register epilogue (FP64 only)
+        if (form == 666) oz_persist_form<6, 6, 6, 64, 0, 1, 1>(g, maps, smem_raw);
+        if (form == 777) oz_persist_form<7, 7, 7, 64, 0, 1, 1>(g, maps, smem_raw);
+      }
+      break;  // 0: not error-free in any form -- not this kernel's launch
   }
 }
 
@@ -711,8 +725,9 @@ matmul_ozaki_fixed_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps) 
 // One CTA per row: row maximum -> exponent e (|x| < 2^e), then S digits per element.  dst plane t of row r (relative
 // index) is dst + t * plane + r * kq; k >= n is zero.  Rows [src_row0, src_row0 + nrows) of src; rows up to nrows_pad are
 // written as zeros with exponent 0 (tile overhang inside the tensor map).
-template <int S>
-__global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const double* __restrict__ src, signed char* __restrict__ dst, int* __restrict__ exps,
+// T = double or float: a float converts to double exactly, so the digits (and everything after) are those of the same number.
+template <int S, typename T>
+__global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const T* __restrict__ src, signed char* __restrict__ dst, int* __restrict__ exps,
                                                           size_t plane, int n, int kq, int src_row0, int nrows, int dst_row0,
                                                           int* __restrict__ guard, int lossy_slot, int top_slot, int dirty_slot) {
   __shared__ double red[8];
@@ -721,15 +736,20 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const double* __res
   const int r = blockIdx.x;  // relative row
   const int tid = threadIdx.x;
   const bool live = r < nrows;
-  const double* x = src + static_cast<size_t>(src_row0 + (live ? r : 0)) * n;
+  const T* x = src + static_cast<size_t>(src_row0 + (live ? r : 0)) * n;
   // 4 consecutive k per thread and iteration: a warp reads 1 KB and writes 128 bytes per slice, both contiguous.  The first
   // KEEP iterations (rows up to 4096 elements) stay in registers between the two passes, so the row is read once.
   constexpr int KEEP = 4;
-  const bool vec = n % 2 == 0;
+  const bool vec = sizeof(T) == 8 ? n % 2 == 0 : n % 4 == 0;  // 16-byte aligned rows
   auto load4 = [&](int k0, double (&v)[4]) {
     if (live && vec && k0 + 4 <= n) {
-      const double2 p = *reinterpret_cast<const double2*>(x + k0), q2 = *reinterpret_cast<const double2*>(x + k0 + 2);
-      v[0] = p.x; v[1] = p.y; v[2] = q2.x; v[3] = q2.y;
+      if constexpr (sizeof(T) == 8) {
+        const double2 p = *reinterpret_cast<const double2*>(x + k0), q2 = *reinterpret_cast<const double2*>(x + k0 + 2);
+        v[0] = p.x; v[1] = p.y; v[2] = q2.x; v[3] = q2.y;
+      } else {
+        const float4 p = *reinterpret_cast<const float4*>(x + k0);
+        v[0] = p.x; v[1] = p.y; v[2] = p.z; v[3] = p.w;
+      }
     } else {
 #pragma unroll
       for (int q = 0; q < 4; ++q) v[q] = (live && k0 + q < n) ? x[k0 + q] : 0.0;
@@ -888,8 +908,8 @@ struct OzLayout {
 };
 
 // the slice passes (P planes); with_guard: also record whether anything was cut and the highest digits in use
-template <int P>
-cudaError_t oz_slices(const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols, cudaStream_t stream,
+template <int P, typename T = double>
+cudaError_t oz_slices(const T* a, const T* bt, void* scratch, int n, int row0, int rows, int col0, int cols, cudaStream_t stream,
                       bool with_guard, bool reuse_a) {
   const OzLayout L(scratch, n, P);
   int* flag = with_guard ? L.guard : nullptr;
@@ -900,8 +920,8 @@ cudaError_t oz_slices(const double* a, const double* bt, void* scratch, int n, i
   const int cols_pad = static_cast<int>(oz_rows_pad(cols, OZ_BN));
   // guard words: 0 a is cut, 1 top digit of a, 2 top digit of bt, 3 bt is cut (reset per launch); 4 the form the auto kernel took;
   // 5 / 6 highest plane of the a / bt scratch that may hold non-zero bytes (auto mode only; never reset)
-  if (!reuse_a) ozaki_slice_kernel<P><<<rows, 256, 0, stream>>>(a, L.sa, L.ea, L.a_plane, n, L.kq, row0, rows, row0, flag, 0, 1, with_guard ? 5 : -1);
-  ozaki_slice_kernel<P><<<cols_pad, 256, 0, stream>>>(bt, L.sb, L.eb, L.b_plane, n, L.kq, col0, cols, 0, flag, 3, 2, with_guard ? 6 : -1);
+  if (!reuse_a) ozaki_slice_kernel<P, T><<<rows, 256, 0, stream>>>(a, L.sa, L.ea, L.a_plane, n, L.kq, row0, rows, row0, flag, 0, 1, with_guard ? 5 : -1);
+  ozaki_slice_kernel<P, T><<<cols_pad, 256, 0, stream>>>(bt, L.sb, L.eb, L.b_plane, n, L.kq, col0, cols, 0, flag, 3, 2, with_guard ? 6 : -1);
   return cudaGetLastError();
 }
 
@@ -958,9 +978,9 @@ cudaError_t oz_persist_configure(Kernel kernel, int smem, PerDeviceOnce& once) {
   }
   return cudaSuccess;
 }
-template <int CX, int CY> cudaError_t oz_auto_configure() {
+template <int CX, int CY, typename CT = double> cudaError_t oz_auto_configure() {
   static PerDeviceOnce once;
-  return oz_persist_configure(matmul_ozaki_auto_kernel<CX, CY>, kOzPersistSmemMax, once);
+  return oz_persist_configure(matmul_ozaki_auto_kernel<CX, CY, CT>, kOzPersistSmemMax, once);
 }
 
 // clusters of CX x CY CTAs the device can keep resident with one CTA per SM (0 on failure)
@@ -978,7 +998,7 @@ template <int CX, int CY> int oz_auto_max_clusters() {
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   int clusters = 0;
-  if (cudaOccupancyMaxActiveClusters(&clusters, matmul_ozaki_auto_kernel<CX, CY>, &cfg) != cudaSuccess) {
+  if (cudaOccupancyMaxActiveClusters(&clusters, matmul_ozaki_auto_kernel<CX, CY, double>, &cfg) != cudaSuccess) {
     (void)cudaGetLastError();
     return 0;
   }
@@ -1028,22 +1048,24 @@ template <int S, int CR> cudaError_t oz_fixed_configure() {
 constexpr int oz_fixed_ring(int s) { return s <= 4 ? 1 : 0;  /* chunk buffers of c where the stage ring leaves room */ }
 
 // c as a 2-D tensor of doubles that ends at (rows_end, cols_end): box = 32 rows x 16 columns (one warp's slab), 128-byte swizzle
-bool make_c_map(CUtensorMap* map, double* c, int n, int rows_end, int cols_end) {
+bool make_c_map(CUtensorMap* map, void* c, size_t elem, int n, int rows_end, int cols_end) {
   EncodeTiledFn enc = encode_tiled();
   if (enc == nullptr) return false;
   const cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols_end), static_cast<cuuint64_t>(rows_end)};
-  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n) * sizeof(double)};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(n) * elem};
   const cuuint32_t box[2] = {16, 32};
-  const cuuint32_t elem[2] = {1, 1};
-  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, c, dims, strides, box, elem, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+  const cuuint32_t ones[2] = {1, 1};
+  return enc(map, elem == 8 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT64 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, c, dims, strides, box, ones, CU_TENSOR_MAP_INTERLEAVE_NONE,
+             elem == 8 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_64B,
              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // slices == 0: the auto kernel (reads the guard, records the form it ran in guard[4]); otherwise the fixed triangular form over
 // the first `slices` of `planes` planes
-cudaError_t oz_persist_contract(double* c, void* scratch, int planes, int slices, int n, int row0, int rows, int col0, int cols, cudaStream_t stream) {
+template <typename CT = double>
+cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, int n, int row0, int rows, int col0, int cols, cudaStream_t stream) {
   const OzLayout L(scratch, n, planes);
-  const bool c_by_tma = n % 2 == 0;  // row pitch a multiple of 16 bytes
+  const bool c_by_tma = (n * sizeof(CT)) % 16 == 0;  // row pitch a multiple of 16 bytes
   if (slices == 0 && !c_by_tma) return cudaErrorInvalidValue;
   OzMaps maps;
   if (!make_slice_map(&maps.a128, L.sa, static_cast<size_t>(n), L.kq, 64, 128, planes, 1) ||
@@ -1052,7 +1074,7 @@ cudaError_t oz_persist_contract(double* c, void* scratch, int planes, int slices
       !make_slice_map(&maps.b32, L.sb, L.b_rows, L.kq, 64, 32, planes, 1))
     return cudaErrorNotSupported;
   if (c_by_tma) {
-    if (!make_c_map(&maps.c, c, n, row0 + rows, col0 + cols)) return cudaErrorNotSupported;
+    if (!make_c_map(&maps.c, c, sizeof(CT), n, row0 + rows, col0 + cols)) return cudaErrorNotSupported;
   } else {
     maps.c = maps.a128;  // never dereferenced
   }
@@ -1074,7 +1096,11 @@ cudaError_t oz_persist_contract(double* c, void* scratch, int planes, int slices
   const dim3 grid(static_cast<unsigned>(std::min(tiles_x * tiles_y, oz_sm_count())));
   switch (slices) {
     case 0: {
-      const OzClusterChoice cc = oz_auto_cluster_choice();
+      OzClusterChoice cc = oz_auto_cluster_choice();
+      if (sizeof(CT) != 8 && cc.shape != 11) {  // the multicast forms are instantiated for FP64 only
+        cc.shape = 11;
+        cc.clusters = oz_sm_count();
+      }
       const int cx = cc.shape / 10, cy = cc.shape % 10;
       const int supers = ((tiles_x + cx - 1) / cx) * ((tiles_y + cy - 1) / cy);
       cudaLaunchConfig_t cfg = {};
@@ -1091,13 +1117,16 @@ cudaError_t oz_persist_contract(double* c, void* scratch, int planes, int slices
       cfg.numAttrs = cx * cy > 1 ? 1 : 0;
       const int* guard = L.guard;
       int* ran = L.guard + 4;
-      if (cc.shape == 22) return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_kernel<2, 2>, g, maps, guard, ran);
-      if (cc.shape == 21) return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_kernel<2, 1>, g, maps, guard, ran);
-      if (cudaError_t e = oz_auto_configure<1, 1>(); e != cudaSuccess) return e;
-      return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_kernel<1, 1>, g, maps, guard, ran);
+      if constexpr (sizeof(CT) == 8) {
+        if (cc.shape == 22) return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_kernel<2, 2, double>, g, maps, guard, ran);
+        if (cc.shape == 21) return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_kernel<2, 1, double>, g, maps, guard, ran);
+      }
+      if (cudaError_t e = oz_auto_configure<1, 1, CT>(); e != cudaSuccess) return e;
+      return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_kernel<1, 1, CT>, g, maps, guard, ran);
     }
 #define MMX_OZ_FIXED(S)                                                                                                                       \
   case S:                                                                                                                                     \
+    if constexpr (sizeof(CT) != 8) return cudaErrorInvalidValue;                                                                              \
     if (c_by_tma && oz_fixed_ring(S) > 0) {                                                                                                   \
       if (cudaError_t e = oz_fixed_configure<S, oz_fixed_ring(S)>(); e != cudaSuccess) return e;                                              \
       matmul_ozaki_fixed_kernel<S, oz_fixed_ring(S)><<<grid, OZP_THREADS, OzPShape<S, S, S, 64, oz_fixed_ring(S)>::SMEM_BYTES, stream>>>(g, maps); \
@@ -1139,6 +1168,7 @@ cudaError_t matmul_ozaki_prepare() {
   if (cudaError_t e = oz_configure<7, 4, 64>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_configure<6, 1, 64>(); e != cudaSuccess) return e;
   (void)oz_auto_cluster_choice();  // configures the auto kernel of the chosen cluster shape
+  if (cudaError_t e = oz_auto_configure<1, 1, float>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_fixed_configure<2, 0>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_fixed_configure<3, 0>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_fixed_configure<4, 0>(); e != cudaSuccess) return e;
@@ -1153,6 +1183,18 @@ cudaError_t matmul_ozaki_prepare() {
 size_t matmul_ozaki_scratch_bytes(int n) {
   const size_t kq = static_cast<size_t>(oz_kq(n));
   return 7 * (static_cast<size_t>(n) + oz_rows_pad(n, OZ_BN)) * kq + 2 * (static_cast<size_t>(n) + OZ_BN) * sizeof(int) + 256;  // + the guard flag
+}
+
+// FP32 auto mode: the same digit planes from float operands (a float is a double), the same contraction, c in float (the exact
+// value rounded once, added by a FLOAT32 TMA reduction).  *guard_out receives the guard; the caller enqueues the split-TF32 path
+// under ozaki_pick_form_f32(...) == 0.
+cudaError_t launch_matmul_ozaki_f32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
+                                    cudaStream_t stream, int** guard_out, bool reuse_a) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  if (scratch == nullptr || guard_out == nullptr || n % 4 != 0) return cudaErrorInvalidValue;
+  *guard_out = OzLayout(scratch, n, 7).guard;
+  if (cudaError_t e = oz_slices<7, float>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a); e != cudaSuccess) return e;
+  return oz_persist_contract<float>(c, scratch, 7, 0, n, row0, rows, col0, cols, stream);
 }
 
 int* matmul_ozaki_form_word(void* scratch, int n) { return scratch == nullptr ? nullptr : OzLayout(scratch, n, 7).guard + 4; }

@@ -351,7 +351,8 @@ template <int CHUNK_STAGES>
 __global__ void __launch_bounds__(TS_THREADS, 1)
 matmul_3xtf32s_kernel(float* __restrict__ c, const __grid_constant__ CUtensorMap map_ahi, const __grid_constant__ CUtensorMap map_alo,
                       const __grid_constant__ CUtensorMap map_b, int n, int row0, int rows, int col0, int cols, int debug_noload,
-                      int group) {
+                      int group, const int* __restrict__ run_if) {
+  if (run_if != nullptr && ozaki_pick_form_f32(run_if[0] | run_if[3], run_if[1], run_if[2]) != 0) return;  // see split_planes_kernel
   constexpr int STAGES = TS_STAGES;
   constexpr int BUF_COLS = 256;  // TMEM columns per chunk buffer: 128 leading sums + 128 correction sums
   extern __shared__ unsigned char smem_raw[];
@@ -525,7 +526,10 @@ matmul_3xtf32s_kernel(float* __restrict__ c, const __grid_constant__ CUtensorMap
 //   stacked == 1:  row (i / 128) * 256 + i % 128 is hi, + 128 is lo                        (operand b, blocks of 128)
 // kq floats per destination row; k >= n is zero.
 __global__ void __launch_bounds__(256) split_planes_kernel(const float* __restrict__ src, float* __restrict__ dst, size_t lo_offset, int n,
-                                                           int kq, int src_row0, int nrows, int nrows_pad, int dst_row0, int stacked) {
+                                                           int kq, int src_row0, int nrows, int nrows_pad, int dst_row0, int stacked,
+                                                           const int* __restrict__ run_if) {
+  // guarded launch (FP32 auto mode): the INT8 tensor-core launch before this one took the product
+  if (run_if != nullptr && ozaki_pick_form_f32(run_if[0] | run_if[3], run_if[1], run_if[2]) != 0) return;
   const int quads = kq / 4;
   const size_t total = static_cast<size_t>(nrows_pad) * quads;
   const size_t stride = static_cast<size_t>(gridDim.x) * blockDim.x;
@@ -623,7 +627,7 @@ cudaError_t ts_configure() {
 // split + contraction in the stacked form
 template <int CS>
 cudaError_t ts_go(cudaStream_t stream, float* c, const float* a, const float* bt, float* scratch, int n, int row0, int rows, int col0,
-                  int cols, bool reuse_a) {
+                  int cols, bool reuse_a, const int* run_if) {
   if (cudaError_t e = ts_configure<CS>(); e != cudaSuccess) return e;
   const int kq = plane_row(n);
   float* pa = scratch;                                      // [2][n][kq]
@@ -631,9 +635,9 @@ cudaError_t ts_go(cudaStream_t stream, float* c, const float* a, const float* bt
   float* pb = scratch + 2 * a_plane;                        // [blocks][256][kq], relative to col0
   auto blocks_for = [](size_t total) { return static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 16)); };
   if (!reuse_a)  // the row-sharded run contracts the same rows of a against one column block after another
-    split_planes_kernel<<<blocks_for(static_cast<size_t>(rows) * (kq / 4)), 256, 0, stream>>>(a, pa, a_plane, n, kq, row0, rows, rows, row0, 0);
+    split_planes_kernel<<<blocks_for(static_cast<size_t>(rows) * (kq / 4)), 256, 0, stream>>>(a, pa, a_plane, n, kq, row0, rows, rows, row0, 0, run_if);
   const int cols_pad = (cols + 127) / 128 * 128;
-  split_planes_kernel<<<blocks_for(static_cast<size_t>(cols_pad) * (kq / 4)), 256, 0, stream>>>(bt, pb, 0, n, kq, col0, cols, cols_pad, 0, 1);
+  split_planes_kernel<<<blocks_for(static_cast<size_t>(cols_pad) * (kq / 4)), 256, 0, stream>>>(bt, pb, 0, n, kq, col0, cols, cols_pad, 0, 1, run_if);
   CUtensorMap map_ahi, map_alo, map_b;
   if (!make_plane_map(&map_ahi, pa, static_cast<size_t>(n), kq, TC_BM) || !make_plane_map(&map_alo, pa + a_plane, static_cast<size_t>(n), kq, TC_BM) ||
       !make_plane_map(&map_b, pb, stacked_rows(cols), kq, 256))
@@ -641,7 +645,7 @@ cudaError_t ts_go(cudaStream_t stream, float* c, const float* a, const float* bt
   static const int noload = env_int("MMX_TC_NOLOAD", 0);
   dim3 grid((cols + 127) / 128, (rows + TC_BM - 1) / TC_BM);
   matmul_3xtf32s_kernel<CS><<<grid, TS_THREADS, TS_SMEM_BYTES, stream>>>(c, map_ahi, map_alo, map_b, n, row0, rows, col0, cols, noload,
-                                                                        raster_group(TC_BM, static_cast<size_t>(kq) * sizeof(float)));
+                                                                        raster_group(TC_BM, static_cast<size_t>(kq) * sizeof(float)), run_if);
   return cudaGetLastError();
 }
 
@@ -664,7 +668,7 @@ size_t matmul_3xtf32_scratch_bytes(int n) {
 }
 
 cudaError_t launch_matmul_3xtf32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0,
-                                 int cols, bool wide, cudaStream_t stream, bool reuse_a) {
+                                 int cols, bool wide, cudaStream_t stream, bool reuse_a, const int* run_if) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr || n % 4 != 0) return cudaErrorInvalidValue;
   // tuning hook (tools/tc_probe.py): 14800 + chunk stages = stacked form (32 k per stage); BN * 100 + chunk stages (16 k per
@@ -672,13 +676,14 @@ cudaError_t launch_matmul_3xtf32(float* c, const float* a, const float* bt, void
   static const int mode_env = env_int("MMX_TC_MODE", 0);
   const int mode = mode_env ? mode_env : (wide ? 25604 : 14802);
   switch (mode) {
-    case 14801: return ts_go<1>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a);
-    case 14802: return ts_go<2>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a);
-    case 14803: return ts_go<3>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a);
-    case 14804: return ts_go<4>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a);
-    case 14816: return ts_go<16>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a);
+    case 14801: return ts_go<1>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a, run_if);
+    case 14802: return ts_go<2>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a, run_if);
+    case 14803: return ts_go<3>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a, run_if);
+    case 14804: return ts_go<4>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a, run_if);
+    case 14816: return ts_go<16>(stream, c, a, bt, static_cast<float*>(scratch), n, row0, rows, col0, cols, reuse_a, run_if);
     default: break;
   }
+  if (run_if != nullptr) return cudaErrorInvalidValue;  // only the stacked form carries the guard
   const int kp = packed_row(n);
   float* pa = static_cast<float*>(scratch);
   float* pb = pa + static_cast<size_t>(n) * kp;

@@ -696,6 +696,53 @@ def test_fp32_tensor_core_contraction_within_tolerance(n, variant, slack):
             assert worst <= slack, worst
 
 
+@pytest.mark.parametrize("digits_a,digits_bt,form", [(1, 1, 223), (2, 2, 223), (3, 2, 324), (2, 3, 234), (3, 3, 335)])
+def test_fp32_auto_runs_the_int8_forms_when_they_are_error_free(digits_a, digits_bt, form):
+    """FP32 auto mode from N = 1024: float operands are sliced like doubles (a float is a double), the same INT8 forms run,
+    and c receives the exact product rounded ONCE to float (then one float addition into the incoming c)."""
+    n = 1024
+    rs = np.random.RandomState(10 * digits_a + digits_bt)
+
+    def ints(digits):
+        top = 2 ** (7 * digits - 1)
+        x = rs.randint(-top + 1, top, (n, n)).astype(np.float32)
+        x[:, 0] = top - 1
+        return x
+    a, bt, c0 = ints(digits_a), ints(digits_bt), rs.randint(-1000, 1000, (n, n)).astype(np.float32)
+    with capi.Context(n=n, dtype=capi.F32) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        ctx.run_loop(8)
+        got = ctx.fetch(capi.ARRAY_C)
+        assert ctx.gene8_form() == form
+    exact = a.astype(np.int64) @ bt.astype(np.int64).T
+    want = c0 + exact.astype(np.float64).astype(np.float32)          # one rounding of the product, one float addition
+    assert bits_equal(got, want)
+
+
+def test_fp32_auto_falls_back_to_split_tf32_and_is_exact_on_the_application():
+    n = 2048
+    a, bt, c0 = rand(n, capi.F32, 41), rand(n, capi.F32, 42), rand(n, capi.F32, 43)
+
+    def run(variant, a, bt, c0):
+        with capi.Context(n=n, dtype=capi.F32, matmul_variant=variant) as ctx:
+            ctx.upload(capi.ARRAY_A, a)
+            ctx.upload(capi.ARRAY_BT, bt)
+            ctx.upload(capi.ARRAY_C, c0)
+            ctx.run_loop(8)
+            return ctx.fetch(capi.ARRAY_C), ctx.gene8_form()
+    # full-mantissa floats of mixed magnitude: no INT8 form is error-free -> the split-TF32 kernel, bit for bit
+    got, form = run(0, a, bt, c0)
+    want, none = run(30, a, bt, c0)
+    assert form == 0 and none == -1 and bits_equal(got, want)
+    # the application at N = 2^p: two digits per operand -> 2 x 2; every c is the exact value rounded once
+    with capi.Context(n=n, dtype=capi.F32) as ctx:
+        assert ctx.measure("101010101001").status == capi.MEASURED
+        assert ctx.gene8_form() == 223
+        assert bits_equal(ctx.fetch(capi.ARRAY_C), cpu.closed_form_c(n).astype(np.float32))
+
+
 @pytest.mark.parametrize("n", [64, 256, 300, 260])
 def test_fp32_tensor_core_contraction_small_and_ragged(n):
     """Forced onto the tensor cores at sizes below one tile / not a tile multiple: TMA zero-fill and the masked
