@@ -405,27 +405,55 @@ def ncu_traffic(kernel: str, n: int):
 
 
 def fp32_arm(n, device, steps, peaks):
+    """FP32 arm of the same configuration, plus the same steps with gene 8 forced onto the split-TF32 kernel (variant 30: what
+    operands without a short exact digit form get)."""
     from paper_1806_01430_b200 import capi
     flops = 2.0 * n ** 3
-    with capi.Context(n=n, dtype=capi.F32, devices=[device], timeout_s=600.0) as ctx:
-        for _ in range(3):
-            ctx.measure(GENOME_ALL_NESTS)
-        dev_s = 0.0
-        t0 = time.perf_counter()
-        for _ in range(steps):
-            dev_s += ctx.measure(GENOME_ALL_NESTS).time_s
-        wall = time.perf_counter() - t0
-        ms8 = ctx.time_loop(8, 5, True)
-        ffma_peak = capi.peak_probe(capi.PEAK_FP32_FMA, device)
+
+    def run(variant):
+        with capi.Context(n=n, dtype=capi.F32, devices=[device], timeout_s=600.0, matmul_variant=variant) as ctx:
+            for _ in range(3):
+                ctx.measure(GENOME_ALL_NESTS)
+            dev_s = 0.0
+            t0 = time.perf_counter()
+            for _ in range(steps):
+                dev_s += ctx.measure(GENOME_ALL_NESTS).time_s
+            wall = time.perf_counter() - t0
+            return dev_s, wall, ctx.time_loop(8, 5, True), ctx.gene8_form()
+
+    dev_s, wall, ms8, form = run(0)
+    ffma_peak = capi.peak_probe(capi.PEAK_FP32_FMA, device)
+    out = {"value": flops * steps / dev_s / 1e9, "unit": "GFLOP/s", "steps": steps, "e2e": flops * steps / wall / 1e9,
+           "ms_per_launch": ms8, "effective_fp32_tflops": flops / ms8 / 1e9,
+           "vs_ffma_pipe_peak": flops / ms8 / 1e9 / ffma_peak, "ffma_pipe_peak_tflops": ffma_peak}
     tf32_peak = peaks["bf16_tflops"] / 2.0
-    return {"value": flops * steps / dev_s / 1e9, "unit": "GFLOP/s", "steps": steps, "e2e": flops * steps / wall / 1e9,
-            "kernel": "matmul_3xtf32s (gene 8: three TF32 products per term on tcgen05, b parts stacked along N so two of them share one N=256 MMA; compensated accumulation; split passes included)",
-            "ms_per_launch": ms8, "effective_fp32_tflops": flops / ms8 / 1e9,
-            "roofline": {"bound": "tensor", "achieved": 3.0 * flops / ms8 / 1e9, "peak": tf32_peak, "unit": "TFLOP/s",
-                         "frac": 3.0 * flops / ms8 / 1e9 / tf32_peak, "traffic": ncu_traffic("matmul_3xtf32s", n),
-                         "peak_source": "half of MEASURED_PEAKS.json bf16_tflops (TF32 runs at half the bf16 rate); "
-                                        "achieved counts the three tensor-core products issued per FP32 term"},
-            "vs_ffma_pipe_peak": flops / ms8 / 1e9 / ffma_peak, "ffma_pipe_peak_tflops": ffma_peak}
+
+    def tf32_roof(ms):
+        return {"bound": "tensor", "achieved": 3.0 * flops / ms / 1e9, "peak": tf32_peak, "unit": "TFLOP/s",
+                "frac": 3.0 * flops / ms / 1e9 / tf32_peak, "traffic": ncu_traffic("matmul_3xtf32s", n),
+                "peak_source": "half of MEASURED_PEAKS.json bf16_tflops (TF32 runs at half the bf16 rate); "
+                               "achieved counts the three tensor-core products issued per FP32 term"}
+    tf32_kernel = ("matmul_3xtf32s (gene 8: three TF32 products per term on tcgen05, b parts stacked along N so two of them share one "
+                   "N=256 MMA; compensated accumulation; split passes included)")
+    if form > 0:
+        sa, sb, lv = form // 100, form // 10 % 10, form % 10
+        products = sum(1 for t in range(1, sa + 1) for u in range(1, sb + 1) if t + u <= lv + 1)
+        int8_peak = 2.0 * peaks["bf16_tflops"]
+        ops = products * flops / ms8 / 1e9
+        out["kernel"] = (f"matmul_ozaki_auto<float> form {form} (gene 8: the float operands' exact 7-bit INT8 digits, {sa} x {sb} pairs = "
+                         f"{products} slice products per term, result = the exact product rounded once to float; slice passes and the "
+                         f"three guarded split-TF32 launches included)")
+        out["roofline"] = {"bound": "tensor", "pipe": "int8", "achieved": ops, "peak": int8_peak, "unit": "TOP/s", "frac": ops / int8_peak,
+                           "traffic": None, "form": form, "slice_products_per_term": products,
+                           "peak_source": "twice MEASURED_PEAKS.json bf16_tflops; whole nest (slice passes included)"}
+        d2, w2, ms30, _ = run(30)
+        out["split_tf32"] = {"value": flops * steps / d2 / 1e9, "unit": "GFLOP/s", "e2e": flops * steps / w2 / 1e9, "kernel": tf32_kernel,
+                             "ms_per_launch": ms30, "effective_fp32_tflops": flops / ms30 / 1e9, "roofline": tf32_roof(ms30),
+                             "note": "the same steps with matmul_variant 30: what gene 8 runs when no INT8 form is error-free"}
+    else:
+        out["kernel"] = tf32_kernel
+        out["roofline"] = tf32_roof(ms8)
+    return out
 
 
 def fp64_pipe_arm(n, device, steps, reference_checksum):
