@@ -106,13 +106,14 @@ typedef struct mmx_config {
   const int32_t* devices;   /* CUDA ordinal per slot; NULL = slot s -> device s % deviceCount  */
   int32_t host_threads;     /* threads for CPU-mapped nests; 1 = the reference program         */
   int32_t launch_batching;  /* 1: inner-loop launch trains are submitted as CUDA graphs        */
-  int32_t matmul_variant;   /* gene-8 kernel: 0 auto (FP64: below N = 1024 DMMA; from there the INT8 tensor cores whenever their 7-bit
-                             * slices give the error-free product -- with the fewest slices that do, 2 .. 7, chosen on the device; the application's
-                             * inputs at N = 2^p qualify with 3 -- and DMMA otherwise; FP32: tcgen05 split-TF32 with compensated
-                             * accumulation for N >= 1024, FFMA below); 1 first SIMT kernel; 2, 4-13 DMMA tile shapes (FP64);
-                             * 20, 22 SIMT tile shapes; 30 FP32 tcgen05 at any N % 4 == 0; 31 its wide-tile uncompensated form;
-                             * 40 FP64 on the tcgen05 INT8 tensor cores (7 exact 7-bit slices per operand, error <= 2e-14 K max|a| max|b|,
-                             * bit-identical on the application's inputs), 41 .. 45 the same with 6 .. 2 slices */
+  int32_t matmul_variant;   /* gene-8 kernel: 0 auto (below N = 1024: DMMA in FP64, FFMA in FP32; from there the INT8 tensor cores
+                             * whenever exact 7-bit digit products give the error-free result, in the cheapest digit-pair form
+                             * that does, chosen on the device from the operands -- the application's inputs at N = 2^p qualify
+                             * with 2 x 2 .. 3 x 3 pairs -- and otherwise DMMA in FP64, tcgen05 split-TF32 with compensated
+                             * accumulation in FP32); 1 first SIMT kernel; 2, 4-13 DMMA tile shapes (FP64);
+                             * 20, 22 SIMT tile shapes; 30 FP32 tcgen05 split-TF32 at any N % 4 == 0; 31 its wide-tile
+                             * uncompensated form; 40 FP64 on the tcgen05 INT8 tensor cores with 7 exact 7-bit slices per operand
+                             * whatever the operands (error <= 2e-14 K max|a| max|b|), 41 .. 45 the same with 6 .. 2 slices */
   int32_t warmup;           /* untimed runs per genome before the timed repetitions (default 0) */
 } mmx_config;
 

@@ -188,6 +188,7 @@ def test_cost_hint_starts_the_longest_genome_first():
     def record(g):
         with lock:
             started.append(g)
+        time.sleep(0.05)        # long enough that every worker has pulled its first genome before any pulls a second
         return (MEASURED, 1.0 + g.count("1"), 0.1)
     batch = ["0001", "0011", "0111", "1111", "0000"]
     with H.Evaluator.from_callback(api, 4, record, jobs=1) as ev:
