@@ -23,6 +23,10 @@
 // "Wide" (variant 31, 128 x 256 tile, plain FP32 masters): ~1.45x faster, 1.6-2.9 of the bar on the
 // application's smooth inputs (still 3-5x more accurate than the CPU float program), 0.1 on random inputs.
 //
+// Who runs it.  matmul_variant 30 / 31 always; FP32 auto mode (variant 0, N >= 1024) as the FALLBACK of the exact INT8 forms
+// (matmul_ozaki.cu): its three launches are enqueued behind the auto kernel with `run_if` = the guard, and do nothing when an
+// INT8 form took the product.
+//
 // Two kernels share this scheme:
 //   matmul_3xtf32s_kernel  (default, "stacked", below)  128 x 128 output tile, compensated masters; the two parts of b are
 //               stacked along N so that two of the three products run as ONE N = 256 MMA (the N = 128 shape reaches only

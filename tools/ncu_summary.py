@@ -44,8 +44,8 @@ def traffic(rep, n, out_path):
         name = (m.group(1) if m else r[ik])[: -len("_kernel")] if m else r[ik]
         b = float(r[ir]) * scale[units[ir]] + float(r[iw]) * scale[units[iw]]
         dur_us = float(r[it]) * {"ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}.get(units[it], 1.0)
-        if ("ozaki" in name or "dmma" in name) and dur_us < 20.0:
-            continue   # a guarded launch that exited at once (FP64 auto mode): not the kernel's traffic
+        if any(k in name for k in ("ozaki", "dmma", "3xtf32", "split_planes")) and dur_us < 20.0:
+            continue   # a guarded launch that did nothing (auto mode: the other path took the product): not the kernel's traffic
         acc.setdefault(name, []).append((b, float(r[it])))
     p = Path(out_path)
     table = json.loads(p.read_text()) if p.exists() else {}

@@ -11,7 +11,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-fil
 ncu --set full --clock-control none --import-source on -k regex:'matmul_dmma|transpose_tile|fill2d|trace' -s 12 -c 6 -f \
     -o $out/${tag}_prof_f64 python tools/one_individual.py f64 4096 > $out/${tag}_ncu_f64.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:'matmul_3xtf32|split_tf32|split_planes' -s 6 -c 3 -f \
-    -o $out/${tag}_prof_f32 python tools/one_individual.py f32 4096 > $out/${tag}_ncu_f32.log 2>&1
+    -o $out/${tag}_prof_f32 python tools/one_individual.py f32 4096 30 > $out/${tag}_ncu_f32.log 2>&1   # variant 30: the split-TF32 path itself
 ls -la $out | tail -8
 ncu --set full --clock-control none --import-source on -k regex:'ozaki' -s 3 -c 3 -f \
     -o $out/${tag}_prof_ozaki python tools/ozaki_one.py 4096 0 > $out/${tag}_ncu_ozaki.log 2>&1
