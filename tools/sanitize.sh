@@ -5,7 +5,7 @@ tag=${1:-r1}
 out=gpurun_out/${tag}_sanitizer.txt
 : > $out
 for tool in memcheck synccheck; do
-  for cfg in "f64 1024" "f32 1024" "f64 256"; do
+  for cfg in "f64 1024" "f32 1024" "f32 1024 30" "f64 2048" "f64 256"; do   # 1024+: INT8 forms (persistent tcgen05 kernel, TMA reductions); "30": split TF32
     echo "== compute-sanitizer --tool $tool  one_individual.py $cfg" >> $out
     timeout 600 compute-sanitizer --tool $tool --print-limit 5 python tools/one_individual.py $cfg 2>&1 | grep -E "ERROR SUMMARY|Error|error|Invalid|hazard|=========.*at " | head -12 >> $out
   done
