@@ -526,28 +526,45 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
             if (lane == 0) mbar_arrive(acc_empty(buf));
           }
           double v[16];
+          if constexpr (LV <= 4) {
+            // the level sum as ONE integer (|L| < 2^31 and three shifts of 7 bits: exact in 64 bits and in a double), scaled by
+            // adding to the exponent field: one FP64-pipe operation per element (the conversion) instead of seven.  Whether the
+            // 16 columns of the chunk all have moderate exponents is decided once (the same for every lane), so the common case
+            // is a branch-free loop the scheduler can interleave across elements.
+            int ebv[16];
+            bool cols_fast = true;
 #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int ebj = eb[j * 16 + e];
-            if constexpr (LV <= 4) {
-              // the level sum as ONE integer (|L| < 2^31 and three shifts of 7 bits: exact in 64 bits and in a double), scaled
-              // by adding to the exponent field: one FP64-pipe operation per element (the conversion) instead of seven
-              long long acc = static_cast<int>(lv[0][e]);
+            for (int e = 0; e < 16; ++e) {
+              ebv[e] = eb[j * 16 + e];
+              cols_fast &= static_cast<unsigned>(ebv[e] + 399) < 799u;
+            }
+            if (cols_fast && row_fast) {
+              const int e_row = ei - 12 - 7 * (LV - 1);
 #pragma unroll
-              for (int l = 1; l < LV; ++l) acc = (acc << 7) + static_cast<int>(lv[l][e]);
-              const double d = static_cast<double>(acc);
-              if (row_fast && static_cast<unsigned>(ebj + 399) < 799u) {
-                long long bits = __double_as_longlong(d);
-                if (acc != 0) bits += static_cast<long long>(ei + ebj - 12 - 7 * (LV - 1)) << 52;  // stays a normal number
-                v[e] = __longlong_as_double(bits);
-              } else {
-                v[e] = scaled(d * pow2(-7 * (LV - 1)), ei, ebj);
+              for (int e = 0; e < 16; ++e) {
+                long long acc = static_cast<int>(lv[0][e]);
+#pragma unroll
+                for (int l = 1; l < LV; ++l) acc = (acc << 7) + static_cast<int>(lv[l][e]);
+                const double d = static_cast<double>(acc);
+                const int hi = __double2hiint(d) + (acc != 0 ? (e_row + ebv[e]) * (1 << 20) : 0);  // stays a normal number
+                v[e] = __hiloint2double(hi, __double2loint(d));
               }
             } else {
+#pragma unroll  // (a rolled loop would index lv and v dynamically and push them to local memory for both branches)
+              for (int e = 0; e < 16; ++e) {
+                long long acc = static_cast<int>(lv[0][e]);
+#pragma unroll
+                for (int l = 1; l < LV; ++l) acc = (acc << 7) + static_cast<int>(lv[l][e]);
+                v[e] = scaled(static_cast<double>(acc) * pow2(-7 * (LV - 1)), ei, ebv[e]);
+              }
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
               double sum = static_cast<double>(static_cast<int>(lv[LV - 1][e]));
 #pragma unroll
               for (int l = LV - 2; l >= 0; --l) sum = fma(sum, 0.0078125, static_cast<double>(static_cast<int>(lv[l][e])));
-              v[e] = scaled_fast(sum, ei, pa, row_fast, ebj, pb[j * 16 + e]);
+              v[e] = scaled_fast(sum, ei, pa, row_fast, eb[j * 16 + e], pb[j * 16 + e]);
             }
           }
           const unsigned slab = slab0 + (sent % CR) * (8 * Sh::C_SLAB);

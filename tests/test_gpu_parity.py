@@ -531,6 +531,53 @@ def test_time_gene8_contraction_reuses_the_encoded_operands():
             ctx.time_gene8_contraction(1, False)
 
 
+def test_fp64_auto_extreme_exponents_and_non_finite_rows_in_the_short_forms():
+    """The reduction epilogue scales by exponent arithmetic when row and column exponents are moderate and by ldexp otherwise;
+    rows near the ends of the exponent range, denormal results and a row holding an Inf / a NaN come out as from exact
+    arithmetic (integers times powers of two: every product and sum is exact)."""
+    n = 1024
+    rs = np.random.RandomState(19)
+    a = rs.randint(-60, 61, (n, n)).astype(np.float64)
+    bt = rs.randint(-60, 61, (n, n)).astype(np.float64)
+    a[3] *= 2.0 ** 500
+    bt[5] *= 2.0 ** 450          # c[3][5] ~ 2^970: finite
+    a[7] *= 2.0 ** -600
+    bt[9] *= 2.0 ** -440         # c[7][9] ~ 2^-1020: at the edge of the normal range
+    bt[200] *= 2.0 ** -470       # c[7][200]: denormal
+    a[700] *= 2.0 ** 300         # moderate but beyond the fast range only together with bt[5]
+    a[11, 17] = np.inf
+    bt[13, 19] = np.nan
+    with capi.Context(n=n, dtype=capi.F64) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, np.zeros((n, n)))
+        ctx.run_loop(8)
+        got = ctx.fetch(capi.ARRAY_C)
+        assert ctx.gene8_form() == 0 or ctx.gene8_form() == 223
+        form = ctx.gene8_form()
+    # a non-finite element marks its operand as cut: the FP64 pipe takes the whole product (form 0); without them the short form runs
+    assert form == 0
+    a[11, 17] = 1.0
+    bt[13, 19] = 1.0
+    with capi.Context(n=n, dtype=capi.F64) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, np.zeros((n, n)))
+        ctx.run_loop(8)
+        got = ctx.fetch(capi.ARRAY_C)
+        assert ctx.gene8_form() == 223
+    ma, ea = np.frexp(np.abs(a).max(axis=1))
+    mb, eb = np.frexp(np.abs(bt).max(axis=1))
+    ai = np.rint(np.ldexp(a, (-ea + 7)[:, None])).astype(np.int64)      # rows as small integers times 2^(ea - 7)
+    bi = np.rint(np.ldexp(bt, (-eb + 7)[:, None])).astype(np.int64)
+    assert np.array_equal(np.ldexp(ai.astype(np.float64), (ea - 7)[:, None]), a)
+    with np.errstate(all="ignore"):
+        want = np.ldexp((ai @ bi.T).astype(np.float64), (ea[:, None] + eb[None, :] - 14))
+    assert np.isfinite(want).all()
+    assert bits_equal(got, want)
+    assert got[7, 200] != 0.0 and abs(got[7, 200]) < 2.2250738585072014e-308 or (ai[7] @ bi[200]) == 0     # a denormal came through
+
+
 def test_fp64_auto_form_on_the_application():
     """(i +- k) / N at N = 2^p carries log2(N) + 2 bits: two digits per operand up to N = 4096 -> the 2 x 2 form, 4 slice
     products per term instead of the 28 of the widest form; the whole individual stays bit-identical to the CPU program."""
