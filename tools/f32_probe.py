@@ -1,3 +1,5 @@
+"""FP32 gene 8 at N=4096: auto mode (INT8 forms, split TF32 as the guarded fallback) against matmul_variant 30 (split TF32 always).
+MMX_F32_INT8=0 switches the INT8 forms off.  usage: python tools/f32_probe.py"""
 import sys, os
 sys.path.insert(0, ".")
 from paper_1806_01430_b200 import capi
