@@ -824,6 +824,7 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const T* __restrict
   const int dirty = dirty_slot >= 0 ? guard[dirty_slot] : S;
   auto emit4 = [&](int k0, const double (&v)[4]) {
     int dig[S] = {};
+    int levels = S;  // digit levels walked: the planes beyond hold zeros for these four elements
     double rem[4];
 #pragma unroll
     for (int q = 0; q < 4; ++q) rem[q] = bad ? 0.0 : v[q] * inv;
@@ -831,7 +832,10 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const T* __restrict
     for (int t = 0; t < S; ++t) {
       // four elements per digit level, branch-free (a zero remainder yields a zero digit); one test per level ends the walk
       // once nothing is left -- short operands finish after a digit or two
-      if (t >= 1 && rem[0] == 0.0 && rem[1] == 0.0 && rem[2] == 0.0 && rem[3] == 0.0) break;
+      if (t >= 1 && rem[0] == 0.0 && rem[1] == 0.0 && rem[2] == 0.0 && rem[3] == 0.0) {
+        levels = t;
+        break;
+      }
       const double up = pow2(7 * (t + 1) - 1), down = pow2(-(7 * (t + 1) - 1));
       int word = 0;
 #pragma unroll
@@ -847,8 +851,10 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const T* __restrict
     }
     // bits below the last digit: the slices do not reproduce this element exactly
     lossy |= (rem[0] != 0.0) | (rem[1] != 0.0) | (rem[2] != 0.0) | (rem[3] != 0.0);
+    const int planes_to_write = max(levels, dirty);  // beyond: zero digits into planes that hold only zeros
 #pragma unroll
     for (int t = 0; t < S; ++t) {
+      if (t >= planes_to_write) break;
       if (dig[t] != 0) top = max(top, t + 1);
       if (t < dirty || dig[t] != 0) *reinterpret_cast<int*>(drow + t * plane + k0) = dig[t];
     }
