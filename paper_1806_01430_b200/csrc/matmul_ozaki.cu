@@ -28,8 +28,8 @@
 //                                   accumulators of a tile stay in TMEM for the whole K loop; the epilogue turns the levels into
 //                                   one integer, scales by exponent arithmetic and adds into c with TMA reductions
 //   ozaki_slice_kernel<S>           x -> int8 digit planes [t][row][k] + one exponent per row (+ the guard)
-// Measured on B200 (profiles/r1f_*), whole application N = 4096 / 8192 / 16384: 341-348 / 428 / 310 TFLOP/s of FP64 work (FP32:
-// 403-407 / 469 / 318) with the forms 2x2 / 3x2 / 3x3 the operands allow (first version, 6-slice triangular form for all: 119 / 151 /
+// Measured on B200 (profiles/r1f_*), whole application N = 4096 / 8192 / 16384: 350 / 430 / 309 TFLOP/s of FP64 work (FP32:
+// 406 / 473 / 314) with the forms 2x2 / 3x2 / 3x3 the operands allow (first version, 6-slice triangular form for all: 119 / 151 /
 // 172); DMMA 33-35.
 #include <algorithm>
 #include <cstdlib>
