@@ -393,7 +393,7 @@ matmul_3xtf32s_kernel(float* __restrict__ c, const __grid_constant__ CUtensorMap
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == 2 && !skip) {  // a skipped launch touches no tensor memory
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tmem_slot), "n"(512) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
   }
@@ -525,7 +525,7 @@ matmul_3xtf32s_kernel(float* __restrict__ c, const __grid_constant__ CUtensorMap
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 2 && !skip) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(512) : "memory");
   }
