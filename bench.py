@@ -45,12 +45,17 @@ def parse_args():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=4096)
+    ap.add_argument("--n", "--size", dest="n", type=int, default=4096, help="matrix size (use --size under torchrun: its own parser finds --n ambiguous)")
     ap.add_argument("--dtype", default="f64", choices=["f64", "f32"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 arm of the configuration")
     ap.add_argument("--no-fp64-pipe", action="store_true", help="skip the arm that forces gene 8 onto the FP64 pipe (DMMA)")
-    ap.add_argument("--ga", action="store_true", help="also run the GA search (M=12, T=12) with real timings")
+    ap.add_argument("--ga", action="store_true", help="run the config-4 GA block (64 x 40, seed 1) also on one GPU (on by default with --gpus > 1)")
+    ap.add_argument("--no-multi", action="store_true", help="with --gpus > 1: skip the config-4 (GA) and config-5 (row-sharded) blocks")
+    ap.add_argument("--ga-population", type=int, default=64)
+    ap.add_argument("--ga-generations", type=int, default=40)
+    ap.add_argument("--ga-timeout", type=float, default=2.0, help="budget per individual in the GA block (a run over it scores the budget)")
+    ap.add_argument("--rowshard-n", type=int, nargs="*", default=[16384, 32768], help="sizes of the row-sharded block (config 5)")
     return ap.parse_args()
 
 
@@ -182,9 +187,21 @@ def run_ours(args):
     rank, local_rank, world = dist_env()
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device: the product has no CPU fallback")
-    torch.cuda.set_device(local_rank)
+    # MMX_BENCH_SHARE_DEVICE=1 is a test hook for one-GPU boxes: every rank uses cuda:0 and the process group is gloo (NCCL refuses
+    # two ranks on one device); everything else -- the sharding, the IPC handles, the barriers -- is the code the 8-GPU run uses
+    share = os.environ.get("MMX_BENCH_SHARE_DEVICE") == "1"
+    device = 0 if share else local_rank
+    torch.cuda.set_device(device)
+    ctl = None            # gloo group for host-side control (handles, barriers, outcomes): the data path never uses a collective
+    red_dev = "cuda"
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if share:
+            dist.init_process_group("gloo")
+            ctl, red_dev = dist.group.WORLD, "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", device))
+            ctl = dist.new_group(backend="gloo")
+    local_rank = device
 
     n, dtype = args.n, capi.F64 if args.dtype == "f64" else capi.F32
     esz = 8 if dtype == capi.F64 else 4
@@ -198,7 +215,7 @@ def run_ours(args):
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        t = torch.tensor([x], dtype=torch.float64, device=red_dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
@@ -317,9 +334,15 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         base = cpu_baseline(n, 0 if dtype == capi.F64 else 1, os.cpu_count() or 1)
 
-    ga = None
-    if rank == 0 and args.ga:
-        ga = run_ga_search(n, dtype, [local_rank])
+    # config 4 / config 5 (every rank takes part): the GA search with the population sharded over the ranks, and the row-sharded
+    # individual with the fused transpose + exchange over peer memory
+    multi = None
+    if (world > 1 and not args.no_multi) or args.ga:
+        multi = {"ga": ga_block(args, n, dtype, device, rank, world, ctl, barrier)}
+        if world > 1:
+            multi["rowshard"] = rowshard_block(args, dtype, device, rank, world, ctl, max_over_ranks, barrier)
+        else:
+            multi["rowshard"] = {"skipped": "needs --gpus >= 2 (one process per GPU under torchrun)"}
 
     if rank == 0:
         ms_per_step = 1e3 * wall_s / args.steps
@@ -351,8 +374,8 @@ def run_ours(args):
             line["fp32"] = fp32
         if fp64_pipe is not None:
             line["fp64_pipe"] = fp64_pipe
-        if ga is not None:
-            line["ga_search"] = ga
+        if multi is not None:
+            line["multi_gpu"] = multi
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
@@ -484,22 +507,126 @@ def fp64_pipe_arm(n, device, steps, reference_checksum):
                          "peak_source": "FMA-issue peak of the FP64 pipe measured in this run by csrc/peaks.cu"}}
 
 
-def run_ga_search(n, dtype, devices, population=12, generations=12, seed=1, timeout_s=0.5):
-    """GA wall-time to best pattern with real CUDA-event timings (MultiGpuEvaluator over the C ABI)."""
-    from paper_1806_01430_b200 import hostapi as H
-    api = H.mine()
-    t0 = time.perf_counter()
-    with H.Evaluator.from_cuda(api, n=n, dtype=dtype, timeout_s=timeout_s, devices=tuple(devices)) as ev:
-        res = ev.run_ga(population=population, generations=generations, seed=seed)
+def ga_block(args, n, dtype, device, rank, world, ctl, barrier):
+    """BASELINE config 4: GA 64 x 40, seed 1, real CUDA-event fitness at N=4096, population sharded over the ranks
+    (sharded.ShardedEvaluator: every rank walks the same GA, measures its share of each generation's unseen genomes on its own GPU,
+    outcomes gathered as 4 doubles per genome over gloo -- the pool semantics of evaluator.cpp:246-276 across processes)."""
+    import torch.distributed as dist
+
+    from paper_1806_01430_b200 import capi
+    from paper_1806_01430_b200.sharded import ShardedEvaluator
+    cores = os.cpu_count() or 1
+    team = max(1, cores // world)                 # host threads for CPU-mapped nests: the ranks share the box's cores
+    zero = "0" * capi.GENE_LENGTH
+    # the all-CPU baseline genome must be MEASURED (ga.cpp:254-258); at N=4096 it takes seconds even on every core, so it is measured
+    # once, on rank 0, on all cores, outside the search (budget 300 s) and preloaded like a line of eval_cache.jsonl
+    base = [None]
+    t_base = time.perf_counter()
+    if rank == 0:
+        with capi.Context(n=n, dtype=dtype, devices=[device], timeout_s=300.0, host_threads=cores) as bctx:
+            base[0] = bctx.measure(zero).as_tuple()
+    if world > 1:
+        dist.broadcast_object_list(base, src=0, group=ctl)
+    t_base = time.perf_counter() - t_base
+    if base[0][0] != capi.MEASURED:
+        return {"skipped": f"the all-CPU baseline genome could not be measured within 300 s (status {capi.STATUS_NAMES[base[0][0]]})"}
+    with capi.Context(n=n, dtype=dtype, devices=[device], timeout_s=args.ga_timeout, host_threads=team) as ctx:
+        ev = ShardedEvaluator(lambda g: ctx.measure(g).as_tuple(), capi.GENE_LENGTH, group=ctl, device="cpu")
+        ev.preload(zero, base[0])
+        barrier()
+        t0 = time.perf_counter()
+        res = ev.run_ga(population=args.ga_population, generations=args.ga_generations, seed=1)
+        barrier()
+        wall = time.perf_counter() - t0
         c = ev.counters()
-    wall = time.perf_counter() - t0
+        local = ev.local_measurements
+        walls = list(ev.batch_wall)
     rows = res["csv"].splitlines()[1:]
     first_best = next(int(r.split(",")[0]) for r in rows if r.split(",")[3] == res["best_genome"])
-    return {"population": population, "generations": generations, "seed": seed, "timeout_s": timeout_s,
-            "wall_s": wall, "best_genome": res["best_genome"], "best_s": res["best_s"], "baseline_s": res["baseline_s"],
-            "speedup_vs_all_cpu_genome": res["baseline_s"] / res["best_s"], "generation_of_best": first_best,
-            "distinct": c["distinct"], "requests": c["requests"],
-            "note": "all-CPU baseline genome hits the timeout budget when N is large; then baseline_s = budget"}
+    feasible = sum(1 for o in ev.memo.values() if o[0] != capi.COMPILE_ERROR)
+    timeouts = sum(1 for o in ev.memo.values() if o[0] == capi.TIMEOUT)
+    per_rank = [local]
+    if world > 1:
+        per_rank = [None] * world
+        dist.all_gather_object(per_rank, local, group=ctl)
+    out = {"config": f"GA {args.ga_population} x {args.ga_generations}, seed 1, N={n}, budget {args.ga_timeout} s per individual, "
+                     f"{team} host thread(s) per rank for CPU-mapped nests",
+           "wall_s": wall, "wall_to_best_s": walls[first_best] - (walls[0] if walls else 0.0) if first_best < len(walls) else None,
+           "generation_of_best": first_best, "best_genome": res["best_genome"], "best_s": res["best_s"],
+           "baseline_s": res["baseline_s"], "baseline_measure_s": t_base,
+           "speedup_vs_all_cpu_genome": res["baseline_s"] / res["best_s"],
+           "requests": c["requests"], "distinct": c["distinct"], "cache_hits": c["cache_hits"],
+           "feasible_measured": feasible, "timeouts": timeouts, "measured_per_rank": per_rank,
+           "individuals_per_s": c["distinct"] / wall, "feasible_individuals_per_s": feasible / wall,
+           "paper_budget_fraction": (wall + t_base) / 3600.0,
+           "note": "wall_s covers the whole search (2522 requests); infeasible genomes are rejected by the planner without GPU work; "
+                   "genomes that leave the matmul nest on the host run into the budget and score it (evaluator.cpp:103-108)"}
+    out["key"] = [n, args.ga_population, args.ga_generations, args.ga_timeout]
+    try:   # the same block measured on ONE GPU (committed evidence: bench.py --ga on one B200), for the efficiency figure
+        one = json.loads((ROOT / "profiles" / "r2_ga_n1.json").read_text())
+        if world > 1 and one.get("key") == out["key"]:
+            out["n1_wall_s"] = one["wall_s"]
+            out["speedup_vs_n1"] = one["wall_s"] / wall
+            out["efficiency_vs_n1"] = one["wall_s"] / wall / world
+            out["n1_source"] = "profiles/r2_ga_n1.json"
+    except (OSError, ValueError, KeyError):
+        pass
+    return out
+
+
+def rowshard_block(args, dtype, device, rank, world, ctl, max_over_ranks, barrier):
+    """BASELINE config 5: one individual row-sharded over the ranks (rowshard.RowShardedRun over mmx_shard_*): the transpose stores
+    its rows of bt into every member's bt through peer-mapped pointers (the exchange IS the transpose kernel), the contraction walks
+    the column blocks in ring order gated by the owners' events.  Per N: TFLOP/s of the sharded individual (max gpu_ms over the
+    ranks), the single-GPU individual on rank 0 for comparison, the exchange against the 900 GB/s per direction NVLink 5 bound."""
+    import torch
+
+    from paper_1806_01430_b200 import capi
+    from paper_1806_01430_b200.rowshard import GpuMember, RowShardedRun
+    esz = 8 if dtype == capi.F64 else 4
+    out = []
+    for n in args.rowshard_n:
+        flops = 2.0 * n ** 3
+        need = 4 * n * n * esz + 15 * n * n + (1 << 30)       # arrays + digit planes + slack
+        free, _total = torch.cuda.mem_get_info(device)
+        share = os.environ.get("MMX_BENCH_SHARE_DEVICE") == "1"
+        ok = max_over_ranks(1.0 if need * (world if share else 1) > free else 0.0) == 0.0
+        if not ok:
+            out.append({"n": n, "skipped": f"needs {need / 2**30:.0f} GiB per member, {free / 2**30:.0f} GiB free"})
+            continue
+        with capi.Context(n=n, dtype=dtype, devices=[device], timeout_s=600.0) as ctx:
+            run = RowShardedRun(GpuMember(ctx), ctl, dtype == capi.F32)
+            run.run()                                           # warm-up (first-use work, graph-free path)
+            reps = 3
+            barrier()
+            t0 = time.perf_counter()
+            rs = [run.run() for _ in range(reps)]
+            barrier()
+            wall = (time.perf_counter() - t0) / reps
+            gpu_ms = max_over_ranks(sum(r["gpu_ms"] for r in rs) / reps)
+            x_ms = max_over_ranks(sum(r["exchange_ms"] for r in rs) / reps)
+            mm_ms = max_over_ranks(sum(r["matmul_ms"] for r in rs) / reps)
+            peer_bytes = rs[-1]["peer_bytes"]
+            checksum = rs[-1]["checksum"]
+            barrier()
+            single = None
+            if rank == 0:                                       # the same individual on one GPU, same context
+                ctx.measure(GENOME_ALL_NESTS)
+                o = ctx.measure(GENOME_ALL_NESTS)
+                single = {"ms": o.time_s * 1e3, "tflops": flops / o.time_s / 1e12, "checksum": ctx.stats().checksum}
+            barrier()
+        row = {"n": n, "world": world, "ms": gpu_ms, "tflops": flops / (gpu_ms * 1e-3) / 1e12, "wall_ms": wall * 1e3,
+               "exchange_ms": x_ms, "matmul_ms": mm_ms, "peer_bytes_per_member": peer_bytes,
+               "exchange_gbs_per_member": peer_bytes / (x_ms * 1e-3) / 1e9 if x_ms > 0 else None,
+               "exchange_frac_of_nvlink": peer_bytes / (x_ms * 1e-3) / 1e9 / 900.0 if x_ms > 0 else None,
+               "nvlink_peak_gbs_per_direction": 900.0, "checksum": checksum, "single_gpu": single}
+        if single is not None:
+            row["speedup_vs_single_gpu"] = single["ms"] / gpu_ms
+            row["frac_of_n_x_single_gpu"] = single["ms"] / gpu_ms / world
+        if share:
+            row["note"] = "MMX_BENCH_SHARE_DEVICE=1: all members on ONE device (peer stores are local stores); not a scaling number"
+        out.append(row)
+    return out
 
 
 def main():

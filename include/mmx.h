@@ -306,7 +306,9 @@ MMX_API int mmx_time_loop(mmx_ctx* ctx, int slot, int gene, int iters, int flush
 
 /* On-device peak probes (roofline denominators the driver file does not carry).
  * kind: 0 copy GB/s, 1 write-only GB/s, 2 FP64 FMA TFLOP/s, 3 FP64 DMMA TFLOP/s,
- *       4 FP32 FMA TFLOP/s, 5 read-only GB/s */
+ *       4 FP32 FMA TFLOP/s, 5 read-only GB/s,
+ *       6 / 7 / 8 the tcgen05 tensor pipe's issue peak for kind::i8 (TOP/s), kind::tf32, kind::f16 with bf16 inputs (TFLOP/s):
+ *       M = 128 x N = 256 instructions back to back on operands resident in shared memory, one issuing thread per SM */
 MMX_API int mmx_peak_probe(int device, int kind, double* value_out);
 
 #ifdef __cplusplus

@@ -29,7 +29,7 @@ NEST_NAMES = ("init_a", "init_b", "zero_c", "transpose", "matmul", "trace")
 MODE_CPU, MODE_GPU_NEST, MODE_GPU_INNER, MODE_GPU_INNER2 = range(4)
 STEP_H2D, STEP_D2H, STEP_D2H_DIAG, STEP_CPU, STEP_GPU, STEP_D2H_SUM, STEP_H2D_DIAG = range(7)
 STEP_NAMES = ("h2d", "d2h", "d2h_diag", "cpu", "gpu", "d2h_sum", "h2d_diag")
-PEAK_COPY, PEAK_WRITE, PEAK_FP64_FMA, PEAK_FP64_DMMA, PEAK_FP32_FMA, PEAK_READ = range(6)
+PEAK_COPY, PEAK_WRITE, PEAK_FP64_FMA, PEAK_FP64_DMMA, PEAK_FP32_FMA, PEAK_READ, PEAK_UMMA_I8, PEAK_UMMA_TF32, PEAK_UMMA_BF16 = range(9)
 
 
 class Config(C.Structure):

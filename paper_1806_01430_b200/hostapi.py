@@ -1,8 +1,8 @@
 """ctypes binding of host/include/mmxhost/capi_host.h (the C window onto the C++ host layer).
 
-The same wrapper class can be pointed at oracle/_ref/libacctune_ref.so (the unmodified reference
-behind oracle/ref_shim.cpp, which exports the same function shapes with a `ref_` prefix): tests
-drive both with identical inputs.
+`Api` takes a library and a symbol prefix, so the tests can point the same wrapper at the unmodified reference
+behind oracle/ref_shim.cpp (same function shapes with a `ref_` prefix; the loader for that lives in tests/refapi.py --
+nothing in this package opens anything under oracle/).
 """
 from __future__ import annotations
 
@@ -247,8 +247,6 @@ class ToolchainMissingSignal(Exception):
 
 
 _mine = None
-_ref = None
-
 
 def mine() -> Api:
     global _mine
@@ -258,17 +256,6 @@ def mine() -> Api:
             raise FileNotFoundError(f"{path} is missing: run `python -m paper_1806_01430_b200.build`")
         _mine = Api(C.CDLL(str(path)), "mmxh")
     return _mine
-
-
-def reference() -> Api | None:
-    """The unmodified reference behind oracle/ref_shim.cpp, or None when oracle/_ref is not built."""
-    global _ref
-    if _ref is None:
-        path = Path(__file__).resolve().parent.parent / "oracle" / "_ref" / "libacctune_ref.so"
-        if not path.exists():
-            return None
-        _ref = Api(C.CDLL(str(path)), "ref")
-    return _ref
 
 
 def dump_number(v: float) -> str:
@@ -346,15 +333,6 @@ def match_kernels(text: str, label: str = "<text>") -> dict:
     buf = C.create_string_buffer(1 << 16)
     api.check(api.f("match_kernels")(label.encode(), text.encode(), buf, C.c_size_t(len(buf))))
     return json.loads(buf.value.decode())
-
-
-def ref_probe_text(text: str, basename: str, compile_cmd: str, workdir) -> tuple[int, list[dict]]:
-    """The reference's build_candidate_set with `compile_cmd` as the compiler (oracle/ref_shim.cpp: ref_probe_text)."""
-    import json
-    api = reference()
-    buf = C.create_string_buffer(1 << 16)
-    rc = api.f("probe_text")(text.encode(), basename.encode(), compile_cmd.encode(), str(workdir).encode(), buf, C.c_size_t(len(buf)))
-    return rc, [json.loads(line) for line in buf.value.decode().splitlines() if line]
 
 
 # ---- calibration (calibrate.hpp) ------------------------------------------------------------------------------

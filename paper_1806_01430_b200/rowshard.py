@@ -1,32 +1,40 @@
-"""Row-sharded run of the matrix application across the GPUs of one box.
+"""Row-sharded run of the matrix application across the GPUs of one box -- the torchrun binding
+of the fused path in the C ABI (`mmx_shard_export / bind / phase1 / phase2`, include/mmx.h, csrc/executor.cu).
 
 For very large N one individual is spread over G ranks (one process per GPU):
 
     rank g owns rows R_g = [r0, r1) of a, c and bt          (contiguous blocks, 64-row aligned when possible)
     init-a, zero-c       : rows R_g only                     (index-generated: no communication)
     init-b               : the whole of b, locally            (index-generated; cheaper than exchanging it)
-    transpose            : bt[R_g][:] = b[:][R_g]^T           (rows R_g of bt = columns R_g of b)
-    ALL-GATHER bt        : the one exchange step of the path  (E*N^2*(G-1)/G bytes received per GPU)
-    matmul               : c[R_g][:] += a[R_g][:] . bt^T      (needs all of bt)
-    trace                : partial sum over the diagonal entries in R_g, then a rank-ordered sum
+    transpose + exchange : ONE kernel.  bt[R_g][:] = b[:][R_g]^T is stored into the bt of EVERY member through
+                           peer-mapped pointers (NVLink stores): the transpose is the all-gather.  No collective
+                           library, no staging buffer.  E*N^2*(G-1)/G bytes leave each GPU.
+    matmul               : c[R_g][:] += a[R_g][:] . bt^T, walked column block by column block in ring order
+                           starting with the member's own rows of bt; block s waits (on the device) only for member
+                           s's "stored everywhere" event, so the math on blocks that have arrived overlaps the
+                           transfers still in flight
+    trace                : partial sum over the diagonal entries in R_g, then a rank-ordered sum on the host
 
-The collective runs through torch.distributed on a tensor that ALIASES the library's own device array
-(`mmx_device_ptr`), so no staging copy is made: NCCL writes straight into the bt that the matmul kernel
-reads.  The engine interface below is what the orchestration needs from a rank; `GpuEngine` drives the C ABI,
-and the CPU (gloo) tests plug in a numpy engine to check the partition / gather / reduction logic bit for bit.
+What crosses the process boundary through torch.distributed is CONTROL only: the 128-byte handles of each member's bt
+and ready event (once, `all_gather_object`), two host barriers per run (every ready event is recorded before a peer
+enqueues its wait; nobody overwrites a bt a peer is still reading), and the 8-byte partial traces.  Use a gloo group
+for it (`control_group()`): the data path never touches NCCL.
+
+`Member` is what the orchestration needs from a rank.  `GpuMember` drives the C ABI; the CPU (gloo) tests plug in a
+member whose "peer-mapped bt" is a file-backed shared mapping, so the handle exchange, the ring order, the barriers
+and the rank-ordered trace are exercised across real processes without a GPU.
 """
 from __future__ import annotations
 
+import time
 from typing import Protocol
 
-import numpy as np
-import torch
 import torch.distributed as dist
 
 
 def row_block(n: int, world: int, rank: int, align: int = 64) -> tuple[int, int]:
     """Contiguous, nearly equal row blocks; boundaries are multiples of `align` when n allows it (the tiled
-    transpose and the GEMM tiles then never straddle a block edge)."""
+    transpose and the GEMM tiles then never straddle a block edge).  Same rule as shard_block in executor.cu."""
     unit = align if n % align == 0 and n // align >= world else 1
     units = n // unit
     lo = (units * rank) // world * unit
@@ -34,92 +42,105 @@ def row_block(n: int, world: int, rank: int, align: int = 64) -> tuple[int, int]
     return lo, hi
 
 
-class Engine(Protocol):
+def ring_order(rank: int, world: int) -> list[int]:
+    """Owners of the column blocks in the order member `rank` consumes them (its own first): at any instant the
+    members read -- and, in the exchange kernel, write -- different peers."""
+    return [(rank + d) % world for d in range(world)]
+
+
+class Member(Protocol):
+    """One rank's share of the row-sharded individual (mirrors mmx_shard_* one to one)."""
+
     n: int
 
-    def fill_rows(self, gene: int, r0: int, r1: int) -> None: ...      # genes 0, 2, 4
-    def transpose_rows(self, r0: int, r1: int) -> None: ...             # gene 6
-    def matmul_rows(self, r0: int, r1: int) -> None: ...                # gene 8
-    def trace_rows(self, r0: int, r1: int) -> float: ...                # gene 11
-    def bt_tensor(self) -> torch.Tensor: ...                            # (n, n) view of bt for the collective
-    def sync(self) -> None: ...
+    def export_handle(self) -> bytes: ...                                  # mmx_shard_export
+    def bind(self, rank: int, world: int, handles: list[bytes]) -> None: ...  # mmx_shard_bind
+    def phase1(self) -> None: ...   # fills + fused transpose/exchange; records the member's ready event
+    def phase2(self) -> dict: ...   # ring-ordered column blocks gated by the owners' events, partial trace; waits
 
 
-class _CudaAlias:
-    """Minimal __cuda_array_interface__ carrier so torch can alias a raw device pointer."""
+class GpuMember:
+    """The member on this rank's GPU: a capi.Context with one slot (include/mmx.h)."""
 
-    def __init__(self, ptr: int, n: int, np_dtype):
-        self.__cuda_array_interface__ = {
-            "shape": (n, n), "typestr": np.dtype(np_dtype).str, "data": (ptr, False), "version": 3, "strides": None,
-        }
+    def __init__(self, ctx, slot: int = 0):
+        self.ctx, self.slot, self.n = ctx, slot, ctx.n
 
+    def export_handle(self) -> bytes:
+        return self.ctx.shard_export(self.slot)
 
-class GpuEngine:
-    def __init__(self, ctx, device: int = 0):
-        from . import capi
-        self.ctx, self.n, self.capi = ctx, ctx.n, capi
-        alias = _CudaAlias(ctx.device_ptr(capi.ARRAY_BT), ctx.n, ctx.np_dtype)
-        self._bt = torch.as_tensor(alias, device=torch.device("cuda", device))
+    def bind(self, rank, world, handles):
+        self.ctx.shard_bind(rank, world, handles, self.slot)
 
-    def fill_rows(self, gene, r0, r1):
-        self.ctx.run_loop_rows(gene, r0, r1 - r0)
+    def phase1(self):
+        self.ctx.shard_phase1(self.slot)
 
-    def transpose_rows(self, r0, r1):
-        self.ctx.run_loop_rows(6, r0, r1 - r0)
-
-    def matmul_rows(self, r0, r1):
-        self.ctx.run_loop_rows(8, r0, r1 - r0)
-
-    def trace_rows(self, r0, r1):
-        return self.ctx.run_loop_rows(11, r0, r1 - r0)
-
-    def bt_tensor(self):
-        return self._bt
-
-    def sync(self):
-        torch.cuda.synchronize()
+    def phase2(self):
+        return self.ctx.shard_phase2(self.slot)
 
 
-def run_row_sharded(engine: Engine, group=None) -> dict:
-    """One pass of the application with rows sharded over the ranks of `group`.  Every rank returns the same
-    checksum; `rows` says which block of c this rank holds."""
-    world = dist.get_world_size(group) if dist.is_initialized() else 1
-    rank = dist.get_rank(group) if dist.is_initialized() else 0
-    n = engine.n
-    r0, r1 = row_block(n, world, rank)
+def control_group(timeout_s: float = 600.0):
+    """A gloo group over all ranks for handles, barriers and the 8-byte partial traces (host-side control only)."""
+    import datetime
+    return dist.new_group(backend="gloo", timeout=datetime.timedelta(seconds=timeout_s))
 
-    engine.fill_rows(0, r0, r1)        # a[R_g]
-    engine.fill_rows(2, 0, n)          # all of b (local, index-generated)
-    engine.fill_rows(4, r0, r1)        # c[R_g] = 0
-    engine.transpose_rows(r0, r1)      # bt[R_g] = b[:, R_g]^T
-    engine.sync()
 
-    gathered_bytes = 0
-    if world > 1:
-        bt = engine.bt_tensor()
-        blocks = [row_block(n, world, r) for r in range(world)]
-        if len({hi - lo for lo, hi in blocks}) == 1:
-            # equal blocks: in-place all-gather (this rank's input is its own slice of the output)
-            dist.all_gather_into_tensor(bt, bt[r0:r1], group=group)
+class RowShardedRun:
+    """Binds a member into the group once (handle exchange), then runs individuals.
+
+    Every rank constructs it with its own member and calls run() the same number of times."""
+
+    def __init__(self, member: Member, group=None, dtype_is_f32: bool = False):
+        self.member, self.group, self.f32 = member, group, dtype_is_f32
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        mine = member.export_handle()
+        if self.world > 1:
+            table: list = [None] * self.world
+            dist.all_gather_object(table, mine, group=group)
         else:
-            for src, (lo, hi) in enumerate(blocks):   # ragged blocks: one broadcast per owner
-                if hi > lo:
-                    dist.broadcast(bt[lo:hi], src=dist.get_global_rank(group, src) if group is not None else src, group=group)
-        gathered_bytes = bt.element_size() * n * (n - (r1 - r0))
-        engine.sync()
+            table = [mine]
+        member.bind(self.rank, self.world, table)
+        self._barrier()   # every member is bound (its peers' mappings are open) before anyone stores into a peer
 
-    engine.matmul_rows(r0, r1)
-    partial = engine.trace_rows(r0, r1)
+    def _barrier(self):
+        if self.world > 1:
+            dist.barrier(group=self.group)
 
-    if world > 1:
-        parts = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
-        dev = engine.bt_tensor().device
-        mine = torch.tensor([partial], dtype=torch.float64, device=dev)
-        parts = [p.to(dev) for p in parts]
-        dist.all_gather(parts, mine, group=group)
-        checksum = 0.0
-        for p in parts:                # rank order: the same association on every rank
-            checksum += float(p.item())
-    else:
-        checksum = partial
-    return {"checksum": checksum, "rows": (r0, r1), "rank": rank, "world": world, "gathered_bytes": gathered_bytes}
+    def run(self) -> dict:
+        """One pass of the application.  Every rank returns the same checksum; `rows` is this rank's block of c."""
+        t0 = time.perf_counter()
+        self.member.phase1()
+        self._barrier()          # every ready event is recorded before anyone enqueues a wait on it
+        st = self.member.phase2()
+        self._barrier()          # nobody starts the next run's stores while a peer still reads this run's bt
+        wall = time.perf_counter() - t0
+        partial = float(st["partial_trace"])
+        if self.world > 1:
+            parts: list = [None] * self.world
+            dist.all_gather_object(parts, partial, group=self.group)
+        else:
+            parts = [partial]
+        checksum = sum_in_rank_order(parts, self.f32)
+        return {"checksum": checksum, "rows": (st["row0"], st["row0"] + st["rows"]), "rank": self.rank, "world": self.world,
+                "peer_bytes": int(st["peer_bytes"]), "gpu_ms": st["gpu_ms"], "exchange_ms": st["exchange_ms"],
+                "matmul_ms": st["matmul_ms"], "wall_s": wall}
+
+
+def sum_in_rank_order(parts, f32: bool) -> float:
+    """Block by block in rank order, in the program's dtype: the association the program's own running sum would use
+    across the blocks (mmx_shard_run_local does the same in-process)."""
+    if f32:
+        import numpy as np
+        s = np.float32(0.0)
+        for p in parts:
+            s = np.float32(s + np.float32(p))
+        return float(s)
+    s = 0.0
+    for p in parts:
+        s += float(p)
+    return s
+
+
+def run_row_sharded(member: Member, group=None, dtype_is_f32: bool = False) -> dict:
+    """Bind + one run (convenience for tests)."""
+    return RowShardedRun(member, group, dtype_is_f32).run()

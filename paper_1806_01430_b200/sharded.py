@@ -20,6 +20,7 @@ rank's GPU in production, a cost-model function in the CPU (gloo) tests.
 from __future__ import annotations
 
 import ctypes as C
+import time
 from typing import Callable, Sequence
 
 import numpy as np
@@ -29,6 +30,10 @@ import torch.distributed as dist
 from . import hostapi as H
 
 Outcome = tuple  # (status, time_s, wall_cost_s)
+
+
+class ShardedMeasureError(RuntimeError):
+    """A rank's measure callable raised; raised on every rank of the group after the collective."""
 
 
 def default_cost(genome: str) -> float:
@@ -76,6 +81,17 @@ class ShardedEvaluator:
         self.memo: dict[str, Outcome] = {}
         self.requests = self.distinct = self.cache_hits = self.backend_calls = 0
         self.local_measurements = 0    # what THIS rank measured (tests pin the sharding with it)
+        self._t0 = time.perf_counter()
+        self.batch_wall: list[float] = []   # seconds since construction at the end of every evaluate_all call (run_ga: call g = generation g)
+
+    def preload(self, genome: str, outcome: Outcome) -> None:
+        """Seed the memo with an outcome obtained elsewhere, like the reference's Evaluator loading eval_cache.jsonl at
+        construction (evaluator.cpp:150-176): later requests for the genome are cache hits on every rank and,
+        as there, loading moves no counter.  Every rank must
+        preload the same outcomes."""
+        if len(genome) != self.gene_length:
+            raise H.HostError(H.E_LENGTH, f"preload: genome length {len(genome)} does not match candidate count {self.gene_length}")
+        self.memo[genome] = (int(outcome[0]), float(outcome[1]), float(outcome[2]))
 
     # -- GenomeEvaluator ---------------------------------------------------------------------------
     def evaluate(self, genome: str) -> Outcome:
@@ -98,10 +114,20 @@ class ShardedEvaluator:
                 self.backend_calls += 1
         if fresh:
             owner = assign_lpt(fresh, self.world, self.cost)
-            mine = torch.zeros((len(fresh), 3), dtype=torch.float64)
+            # columns: status, time_s, wall_cost_s, failed.  A rank whose measurement raises (MMX_E_CUDA, out of memory, ...)
+            # still takes part in the collective and flags its row, so that no rank is left waiting in the all-reduce and a
+            # failed row cannot be mistaken for a legitimate all-zero one (status 0 = Measured, time 0); the same error is
+            # then raised on EVERY rank and nothing of the batch is memoised.
+            mine = torch.zeros((len(fresh), 4), dtype=torch.float64)
+            local_error: BaseException | None = None
             for i, g in enumerate(fresh):
                 if owner[i] == self.rank:
-                    status, t, w = self.measure(g)
+                    try:
+                        status, t, w = self.measure(g)
+                    except Exception as e:  # noqa: BLE001 - reported on every rank below
+                        local_error = local_error or e
+                        mine[i, 3] = 1.0
+                        continue
                     self.local_measurements += 1
                     mine[i, 0], mine[i, 1], mine[i, 2] = float(status), t, w
             if self.world > 1:
@@ -109,8 +135,21 @@ class ShardedEvaluator:
                 buf = mine.to(self.device)
                 dist.all_reduce(buf, op=dist.ReduceOp.SUM, group=self.group)
                 mine = buf.cpu()
+            failed = [fresh[i] for i in range(len(fresh)) if mine[i, 3].item() != 0.0]
+            if failed:
+                # roll the counters back: the batch did not happen (the reference memoises an exception per genome,
+                # evaluator.cpp:206-211; across ranks the error object itself cannot travel, its existence does)
+                self.requests -= len(genomes)
+                self.cache_hits -= len(genomes) - len(fresh)
+                self.distinct -= len(fresh)
+                self.backend_calls -= len(fresh)
+                msg = f"measurement failed on rank(s) owning {failed[:4]}{'...' if len(failed) > 4 else ''}"
+                if local_error is not None:
+                    raise ShardedMeasureError(f"{msg}: {local_error}") from local_error
+                raise ShardedMeasureError(msg)
             for i, g in enumerate(fresh):
                 self.memo[g] = (int(mine[i, 0].item()), float(mine[i, 1].item()), float(mine[i, 2].item()))
+        self.batch_wall.append(time.perf_counter() - self._t0)
         return [self.memo[g] for g in genomes]
 
     def counters(self) -> dict:

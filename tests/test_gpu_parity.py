@@ -917,59 +917,81 @@ def _check_sharded_trace(got, ref, dtype):
         assert abs(got - ref.checksum) <= 2 * n * u * float(np.abs(np.diag(ref.c)).astype(np.float64).sum())
 
 
-def _shard_member(rank, world, n, dtype, numerics, conns, barrier, out_q):
+def _shard_member(rank, world, port, n, dtype, numerics, devices, out_dir):
+    """One rank of the torchrun launch shape: gloo control group, rowshard.RowShardedRun over the C ABI."""
+    import json
+    import os
     import sys
     from pathlib import Path
     sys.path.insert(0, str(Path(__file__).resolve().parent.parent))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+
     from paper_1806_01430_b200 import capi as K
-    with K.Context(n=n, dtype=dtype, numerics=numerics, devices=[0]) as ctx:
-        mine = ctx.shard_export()
-        for q in conns:
-            q.put((rank, mine))
-        table = {rank: mine}
-        while len(table) < world:
-            r, h = conns[rank].get(timeout=60)
-            table[r] = h
-        ctx.shard_bind(rank, world, [table[r] for r in range(world)])
-        barrier.wait(60)
-        for _ in range(2):
-            ctx.shard_phase1()
-            barrier.wait(60)      # every ready event is recorded before anyone waits on it
-            st = ctx.shard_phase2()
-            barrier.wait(60)      # nobody overwrites a bt that a peer is still reading
-        lo, hi = st["row0"], st["row0"] + st["rows"]
-        out_q.put((rank, st, ctx.fetch(K.ARRAY_C)[lo:hi].copy(), ctx.fetch(K.ARRAY_BT).copy()))
-        barrier.wait(60)          # keep the exported allocation alive until every peer is done
+    from paper_1806_01430_b200.rowshard import GpuMember, RowShardedRun, control_group
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    with K.Context(n=n, dtype=dtype, numerics=numerics, devices=[devices[rank]]) as ctx:
+        run = RowShardedRun(GpuMember(ctx), control_group(120.0), dtype == K.F32)
+        res = run.run()
+        res = run.run()           # a second individual over the same binding
+        lo, hi = res["rows"]
+        np.save(Path(out_dir, f"c_rank{rank}.npy"), ctx.fetch(K.ARRAY_C)[lo:hi])
+        np.save(Path(out_dir, f"bt_rank{rank}.npy"), ctx.fetch(K.ARRAY_BT))
+        Path(out_dir, f"rank{rank}.json").write_text(json.dumps(res))
+        dist.barrier()            # keep the exported allocation alive until every peer is done
+    dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("n,dtype,numerics", [(512, capi.F64, capi.FAST), (300, capi.F32, capi.STRICT)])
-def test_row_sharded_across_processes_through_ipc_handles(n, dtype, numerics):
-    """One process per member (both on GPU 0 here), peers' bt and ready events opened from IPC handles: the
-    launch shape bench.py uses under torchrun."""
-    import multiprocessing as mp
+def _free_port():
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _gpu_count():
+    import torch
+    return torch.cuda.device_count()
+
+
+@pytest.mark.parametrize("placement", ["one_device", "distinct_devices"])
+@pytest.mark.parametrize("n,dtype,numerics", [(512, capi.F64, capi.FAST), (300, capi.F32, capi.STRICT), (1024, capi.F64, capi.FAST)])
+def test_row_sharded_across_processes_through_the_torchrun_binding(tmp_path, n, dtype, numerics, placement):
+    """One process per member, peers' bt and ready events opened from IPC handles moved over torch.distributed (gloo): exactly what
+    bench.py --gpus N runs.  On a one-GPU box both members sit on GPU 0; with >= 2 GPUs they also sit on distinct devices (NVLink
+    peer stores)."""
+    import json
+    import torch.multiprocessing as tmp_mp
     world = 2
-    ref = cpu.App(n, dtype).run()
-    mpc = mp.get_context("spawn")
-    conns = [mpc.Queue() for _ in range(world)]
-    barrier, out_q = mpc.Barrier(world), mpc.Queue()
-    procs = [mpc.Process(target=_shard_member, args=(r, world, n, dtype, numerics, conns, barrier, out_q)) for r in range(world)]
-    for p in procs:
-        p.start()
-    got = {}
-    try:
-        for _ in range(world):
-            r, st, c_rows, bt = out_q.get(timeout=180)
-            got[r] = (st, c_rows, bt)
-    finally:
-        for p in procs:
-            p.join(60)
-            if p.is_alive():
-                p.kill()
-    assert all(p.exitcode == 0 for p in procs)
+    if placement == "distinct_devices" and _gpu_count() < world:
+        pytest.skip("needs >= 2 GPUs")
+    devices = [0] * world if placement == "one_device" else list(range(world))
+    ref = cpu.App(n, dtype, threads=4).run()
+    tmp_mp.spawn(_shard_member, args=(world, _free_port(), n, dtype, numerics, devices, str(tmp_path)), nprocs=world, join=True)
     total = ref.c.dtype.type(0)
     for r in range(world):
-        st, c_rows, bt = got[r]
-        assert bits_equal(bt, ref.bt)
-        assert bits_equal(c_rows, ref.c[st["row0"]: st["row0"] + st["rows"]])
-        total = ref.c.dtype.type(total + ref.c.dtype.type(st["partial_trace"]))
-    _check_sharded_trace(float(total), ref, dtype)
+        res = json.loads((tmp_path / f"rank{r}.json").read_text())
+        lo, hi = res["rows"]
+        assert bits_equal(np.load(tmp_path / f"bt_rank{r}.npy"), ref.bt), f"member {r} lacks part of bt"
+        assert bits_equal(np.load(tmp_path / f"c_rank{r}.npy"), ref.c[lo:hi])
+        assert res["peer_bytes"] == (hi - lo) * n * ref.c.itemsize * (world - 1)
+        _check_sharded_trace(res["checksum"], ref, dtype)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_row_sharded_in_process_on_distinct_devices(world):
+    """mmx_shard_run_local with one slot per GPU: the cudaDeviceEnablePeerAccess branch of mmx_shard_bind (needs >= world GPUs)."""
+    if _gpu_count() < world:
+        pytest.skip(f"needs >= {world} GPUs")
+    n = 1024
+    ref = cpu.App(n, capi.F64, threads=4).run()
+    with capi.Context(n=n, num_slots=world, devices=list(range(world))) as ctx:
+        checksum, stats = ctx.shard_run_local()
+        checksum, stats = ctx.shard_run_local()
+        c = np.zeros_like(ref.c)
+        for r, st in enumerate(stats):
+            lo, hi = st["row0"], st["row0"] + st["rows"]
+            assert bits_equal(ctx.fetch(capi.ARRAY_BT, slot=r), ref.bt), f"member {r} lacks part of bt"
+            c[lo:hi] = ctx.fetch(capi.ARRAY_C, slot=r)[lo:hi]
+        assert bits_equal(c, ref.c)
+        _check_sharded_trace(checksum, ref, capi.F64)

@@ -5,10 +5,15 @@ fit, the projection onto the reference's additive form and the file format can b
 this repo's parse_model and, where oracle/_ref is built, by the reference's (sim_model.cpp:157-236).  The GPU run of the
 same pipeline is tools/calibrate.py.
 """
+import sys
+from pathlib import Path
 import numpy as np
 import pytest
 
 from paper_1806_01430_b200 import hostapi as H
+
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+import refapi  # noqa: E402  (test-only loader of the compiled reference)
 
 N = 256
 # serial, cpu[6], loop[12], h2d s/B, d2h s/B, per-transfer s -- the shape of a B200 at the fixture size
@@ -82,7 +87,7 @@ def test_projection_onto_the_reference_cost_model(truth_times, tmp_path):
     assert cal["cost_best"] == cal["plan_best"]
     best, t = H.mine().exhaustive_best(path, 12)
     assert best == cal["cost_best"] and t == pytest.approx(cal["report"]["cost_best_s"], rel=1e-12)
-    ref = H.reference()
+    ref = refapi.reference()
     if ref is not None:                                            # the reference parses the same file to the same times
         theirs = ref.model_time_all(path, 12)
         assert np.array_equal(theirs < 0, mine < 0)

@@ -1,6 +1,8 @@
 """The Evaluator contract, transcribed from the reference's tests/test_evaluator.cpp:103-262 and
 run against this repo's mmxhost::Evaluator through a scripted callback backend -- and, where
 oracle/_ref is present, run identically against the reference's own Evaluator."""
+import sys
+from pathlib import Path
 import threading
 import time
 
@@ -8,9 +10,12 @@ import pytest
 
 from paper_1806_01430_b200 import hostapi as H
 
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+import refapi  # noqa: E402  (test-only loader of the compiled reference)
+
 APIS = [pytest.param(H.mine(), id="mmxhost")]
-if H.reference() is not None:
-    APIS.append(pytest.param(H.reference(), id="reference"))
+if refapi.reference() is not None:
+    APIS.append(pytest.param(refapi.reference(), id="reference"))
 
 MEASURED, COMPILE_ERROR, RUNTIME_ERROR, TIMEOUT = range(4)
 

@@ -5,6 +5,7 @@ build_candidate_set driving its bundled compiler (probe.cpp:187, tools/mockacc.c
 diagnostics on the reference-rendered variant of every genome (tests/golden/generate_golden.py: gen_probe_cases).
 Where oracle/_ref is built and /root/reference is present, the reference's own corpus is probed side by side.
 """
+import sys
 import json
 import re
 import tempfile
@@ -13,6 +14,9 @@ from pathlib import Path
 import pytest
 
 from paper_1806_01430_b200 import hostapi as H
+
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+import refapi  # noqa: E402  (test-only loader of the compiled reference)
 
 GOLD = Path(__file__).parent / "golden"
 CASES = json.loads((GOLD / "probe_cases.json").read_text())
@@ -114,7 +118,7 @@ def test_kernel_matcher_idioms(name):
         assert (row["kernel"] == "") == (row["why"] != "")
 
 
-@pytest.mark.skipif(not (REF_FIXTURES.is_dir() and MOCKACC.exists() and H.reference() is not None),
+@pytest.mark.skipif(not (REF_FIXTURES.is_dir() and MOCKACC.exists() and refapi.reference() is not None),
                     reason="needs /root/reference and oracle/_ref (build container only)")
 @pytest.mark.parametrize("rel", ["corpus/data_dep.c", "corpus/early_exit.c", "corpus/ext_call.c", "corpus/nested.c", "matmul.c"])
 def test_reference_corpus_side_by_side(rel):
@@ -123,7 +127,7 @@ def test_reference_corpus_side_by_side(rel):
     name = Path(rel).name
     rc, rows = H.probe_source(text, name)
     with tempfile.TemporaryDirectory() as td:
-        rrc, rrows = H.ref_probe_text(text, name, f"{MOCKACC} -acc {{src}} -o {{out}}", td)
+        rrc, rrows = refapi.ref_probe_text(text, name, f"{MOCKACC} -acc {{src}} -o {{out}}", td)
     assert rc == rrc and len(rows) == len(rrows)
     for mine, ref in zip(rows, rrows):
         assert {k: mine[k] for k in ("id", "line", "verdict", "reject_class")} == {k: ref[k] for k in ("id", "line", "verdict", "reject_class")}

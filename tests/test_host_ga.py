@@ -2,6 +2,7 @@
 the unmodified reference (tests/golden/generate_golden.py) and -- where oracle/_ref travels with
 the snapshot -- against the reference itself, side by side.  Everything here is integer / RNG /
 ordering work: the bar is bit-exact (byte-identical generations.csv)."""
+import sys
 import json
 from pathlib import Path
 
@@ -9,6 +10,9 @@ import numpy as np
 import pytest
 
 from paper_1806_01430_b200 import hostapi as H
+
+sys.path.insert(0, str(Path(__file__).resolve().parent))
+import refapi  # noqa: E402  (test-only loader of the compiled reference)
 
 GOLDEN = Path(__file__).resolve().parent / "golden"
 MODELS = GOLDEN / "models"
@@ -183,7 +187,7 @@ def test_timeouts_score_as_measured_and_failures_are_penalised(api):
     assert res["best_genome"][0] == "0"   # a timed-out genome never wins against measured ones
 
 
-REF = H.reference()
+REF = refapi.reference()
 
 
 @pytest.mark.skipif(REF is None, reason="oracle/_ref not built (needs /root/reference)")

@@ -72,6 +72,46 @@ def test_two_ranks_share_the_population_and_replay_the_reference_trajectory(tmp_
     assert got == want
 
 
+def _failing_worker(rank: int, world: int, port: int, out_dir: str):
+    sys.path.insert(0, str(ROOT))
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank), WORLD_SIZE=str(world))
+    import torch.distributed as dist
+
+    from paper_1806_01430_b200.sharded import ShardedEvaluator, ShardedMeasureError
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+
+    def measure(genome: str):
+        if genome == "111100000000":
+            raise RuntimeError("device fell over")
+        return (0, 1.0 + genome.count("1"), 0.5)
+
+    ev = ShardedEvaluator(measure, 12, cost=lambda g: 1.0)
+    batch = ["000000000000", "111100000000", "100000000000", "010000000000"]
+    raised = None
+    try:
+        ev.evaluate_all(batch)
+    except ShardedMeasureError as e:
+        raised = str(e)
+    before = ev.counters()
+    ok = ev.evaluate_all([g for g in batch if g != "111100000000"])     # the group is still in step afterwards
+    Path(out_dir, f"rank{rank}.json").write_text(json.dumps({"raised": raised, "before": before, "ok": ok, "after": ev.counters()}))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_a_failing_measurement_raises_on_every_rank_and_leaves_the_group_in_step(tmp_path):
+    world = 2
+    mp.spawn(_failing_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
+    outs = [json.loads((tmp_path / f"rank{r}.json").read_text()) for r in range(world)]
+    for o in outs:
+        assert o["raised"] is not None and "111100000000" in o["raised"]
+        assert o["before"]["requests"] == o["before"]["distinct"] == 0       # the failed batch left no trace
+        assert [tuple(x) for x in o["ok"]] == [(0, 1.0, 0.5), (0, 2.0, 0.5), (0, 2.0, 0.5)]
+        assert o["after"]["distinct"] == 3
+    assert sum("device fell over" in o["raised"] for o in outs) == 1         # the owner reports the cause, the other the fact
+
+
 def test_assignment_is_deterministic_and_balanced():
     sys.path.insert(0, str(ROOT))
     from paper_1806_01430_b200.sharded import assign_lpt, default_cost

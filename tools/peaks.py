@@ -21,8 +21,12 @@ def main():
         "fp64_fma_tflops": capi.peak_probe(capi.PEAK_FP64_FMA),
         "fp64_dmma_tflops": capi.peak_probe(capi.PEAK_FP64_DMMA),
         "fp32_fma_tflops": capi.peak_probe(capi.PEAK_FP32_FMA),
+        "umma_i8_tops": capi.peak_probe(capi.PEAK_UMMA_I8),
+        "umma_tf32_tflops": capi.peak_probe(capi.PEAK_UMMA_TF32),
+        "umma_bf16_tflops": capi.peak_probe(capi.PEAK_UMMA_BF16),
         "how": "csrc/peaks.cu: best of N CUDA-event-timed launches after 3 warm-ups; 16 independent FMA/DMMA chains "
-               "per thread, 4 CTAs x 256 threads per SM; HBM probes move 2 GiB buffers with 128-bit accesses",
+               "per thread, 4 CTAs x 256 threads per SM; HBM probes move 2 GiB buffers with 128-bit accesses; umma_*: tcgen05.mma "
+               "M=128 x N=256 instructions back to back on operands resident in shared memory, one issuing thread per SM (issue peak of the tensor pipe)",
     }
     text = json.dumps(res, indent=1)
     print(text)
