@@ -50,6 +50,9 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-fp32", action="store_true", help="skip the FP32 arm of the configuration")
     ap.add_argument("--no-fp64-pipe", action="store_true", help="skip the arm that forces gene 8 onto the FP64 pipe (DMMA)")
+    ap.add_argument("--no-fp64-random", action="store_true", help="skip the arm with uniform(-1,1) operands")
+    ap.add_argument("--no-sustained", action="store_true", help="skip the >= 3 s sustained block")
+    ap.add_argument("--sustained-seconds", type=float, default=3.0)
     ap.add_argument("--ga", action="store_true", help="run the config-4 GA block (64 x 40, seed 1) also on one GPU (on by default with --gpus > 1)")
     ap.add_argument("--no-multi", action="store_true", help="with --gpus > 1: skip the config-4 (GA) and config-5 (row-sharded) blocks")
     ap.add_argument("--ga-population", type=int, default=64)
@@ -154,6 +157,10 @@ def run_reference(args):
             times.append(t)
     ms = 1e3 * sum(times) / len(times)
     value = flops / (ms * 1e-3) / 1e9
+    # the reference program itself has no threading (fixtures/matmul.c): the same nests on ONE core, matmul on ~4 s worth of rows
+    rows1 = int(min(n, max(1, 4.0 / (per_row_wall * cores))))
+    r1 = cpu.time_app(n, dtype, 1, rows1)
+    t1 = sum(v for k, v in r1["seconds"].items() if k != "matmul") + r1["seconds"]["matmul"] * n / r1["matmul_rows"]
     sample = (f"per step: all six nests at N={n}, matmul nest on rows [0,{rows}) of {n} scaled to the full nest; "
               f"{cores} host threads; oracle port of fixtures/matmul.c (the fixture is fixed at N=256)")
     line = {
@@ -161,7 +168,10 @@ def run_reference(args):
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": args.dtype, "data": "synthetic (the program generates its own inputs)",
         "config": {"workload": f"matrix app N={n} {args.dtype}, all six nests (reference CPU path)", "n": n},
-        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample},
+        "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port", "sample": sample,
+                         "single_thread_value": flops / t1 / 1e9, "single_thread_app_seconds_scaled": t1,
+                         "single_thread_sample": f"all six nests on one core, matmul nest on rows [0,{rows1}) of {n} scaled: the reference "
+                                                 "program as written (fixtures/matmul.c has no threading)"},
         "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
@@ -283,7 +293,8 @@ def run_ours(args):
             # slice passes, that contraction and the guarded FP64-pipe launch that exits at once.
             sa, sb, lv = form // 100, form // 10 % 10, form % 10
             products = sum(1 for t in range(1, sa + 1) for u in range(1, sb + 1) if t + u <= lv + 1)
-            int8_peak = 2.0 * peaks["bf16_tflops"]
+            int8_inferred = 2.0 * peaks["bf16_tflops"]
+            int8_peak = capi.peak_probe(capi.PEAK_UMMA_I8, local_rank)     # measured in this run (csrc/peaks.cu)
             # the dominant kernel by itself: the contraction launch (plus the guarded FP64-pipe launch that retires at once)
             # on operands encoded once -- mmx_time_gene8_contraction; then the whole nest as the step runs it
             msk = ctx.time_gene8_contraction(5, True)
@@ -294,14 +305,18 @@ def run_ours(args):
                               f"slice products per FP64 term)",
                     "form": form, "slice_products_per_term": products,
                     "achieved": ops, "peak": int8_peak, "unit": "TOP/s", "frac": ops / int8_peak,
+                    "peak_inferred": int8_inferred, "frac_vs_inferred": ops / int8_inferred,
                     "traffic": ncu_traffic("matmul_ozaki_auto", n), "ms_per_launch": msk, "share_of_step": msk * 1e-3 / (device_s / args.steps),
                     "effective_fp64_tflops": flops / (msk * 1e-3) / 1e12,
-                    "nest": {"what": "gene 8 as the step runs it: two slice passes + the contraction + the guarded FP64-pipe launch",
+                    "nest": {"what": "gene 8 as the step runs it: the digit planes (written by the fill / transpose kernels when those run "
+                                     "on the device, else two slice passes) + the contraction + the guarded FP64-pipe launch",
                              "ms": ms8, "achieved": ops_nest, "frac": ops_nest / int8_peak, "share_of_step": share,
                              "effective_fp64_tflops": ach,
                              "vs_fp64_pipe_peak": ach / capi.peak_probe(capi.PEAK_FP64_FMA, local_rank)},
-                    "peak_source": "twice MEASURED_PEAKS.json bf16_tflops (INT8 runs at twice the bf16 rate); achieved counts the INT8 "
-                                   "slice products issued per FP64 term (algorithmic work of this form: products x 2N^3)"}
+                    "peak_source": "tcgen05.mma.kind::i8 issue peak measured in this run by csrc/peaks.cu (M=128 x N=256 instructions back to back "
+                                   "on operands resident in shared memory, one issuing thread per SM); peak_inferred = twice "
+                                   "MEASURED_PEAKS.json bf16_tflops (cuBLAS bf16, loads included); achieved counts the INT8 slice products "
+                                   "issued per FP64 term (algorithmic work of this form: products x 2N^3)"}
         else:
             pipe_peak = capi.peak_probe(capi.PEAK_FP64_FMA if dtype == capi.F64 else capi.PEAK_FP32_FMA, local_rank)
             roof = {"bound": "tensor", "pipe": "fp64 (DMMA.8x8x4 via mma.sync)" if dtype == capi.F64 else "fp32 (FFMA)",
@@ -327,8 +342,18 @@ def run_ours(args):
     if rank == 0 and dtype == capi.F64 and n >= 1024 and not args.no_fp64_pipe:
         fp64_pipe = fp64_pipe_arm(n, local_rank, max(10, args.steps // 4), checksum)
 
+    # the same configuration on operands WITHOUT the application's special structure (SURVEY 8d config 2's optional run)
+    fp64_random = None
+    if rank == 0 and dtype == capi.F64 and n >= 1024 and not args.no_fp64_random:
+        fp64_random = fp64_random_arm(n, local_rank)
+
     # the sampler covers the timed region plus the (equally loaded) mixed-genome and roofline phases
     clocks = sampler.stop()
+
+    # >= 3 s of individuals back to back, then ~2 s of the dominant kernel back to back: the numbers above are burst-clock figures
+    sustained = None
+    if rank == 0 and not args.no_sustained:
+        sustained = sustained_block(ctx, n, dtype, local_rank, roof, args.sustained_seconds)
 
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -374,6 +399,10 @@ def run_ours(args):
             line["fp32"] = fp32
         if fp64_pipe is not None:
             line["fp64_pipe"] = fp64_pipe
+        if fp64_random is not None:
+            line["fp64_random"] = fp64_random
+        if sustained is not None:
+            line["sustained"] = sustained
         if multi is not None:
             line["multi_gpu"] = multi
         print(json.dumps(line), flush=True)
@@ -415,6 +444,76 @@ def e2e_host_buffers(ctx, n, dtype, esz, reps):
             "note": "mmx_upload_array x3 (pinned host -> device) + gene-8 kernel + mmx_fetch_array of c (device -> pinned host), host clock"}
 
 
+def fp64_random_arm(n, device):
+    """Gene 8 on uniform(-1, 1) operands from MT19937(seed 1) -- NOT the reference's inputs (the program generates its own): full
+    53-bit mantissas, so no INT8 digit form is error-free and auto mode takes the FP64 pipe (DMMA).  Beside it the opt-in general
+    tensor-core kernel (matmul_variant 40: 7 exact 7-bit slices per operand, 28 slice products per term, truncation bound
+    2e-14 K max|a| max|b|), with its measured norm-wise error on a sample of rows."""
+    import numpy as np
+
+    from paper_1806_01430_b200 import capi
+    rng = np.random.Generator(np.random.MT19937(1))
+    a = rng.uniform(-1.0, 1.0, (n, n))
+    b = rng.uniform(-1.0, 1.0, (n, n))
+    flops = 2.0 * n ** 3
+    rows = np.arange(0, n, max(1, n // 16))[:16]
+    exact = a[rows] @ b                                  # float64 dot of the sampled rows (host; 16 rows only)
+    bound = np.abs(a[rows]) @ np.abs(b)                  # sum_k |a_ik| |b_kj|: the norm-wise bar's scale
+    out = {"data": "uniform(-1,1), numpy MT19937 seed 1 (non-reference inputs)"}
+    for label, variant in (("auto", 0), ("int8_7_slices", 40)):
+        with capi.Context(n=n, dtype=capi.F64, devices=[device], matmul_variant=variant, timeout_s=600.0) as ctx:
+            ctx.upload(capi.ARRAY_A, a)
+            ctx.upload(capi.ARRAY_B, b)
+            ctx.run_loop(4)
+            ctx.run_loop(6)
+            ctx.run_loop(8)
+            c = ctx.fetch(capi.ARRAY_C)[rows]
+            err = float((np.abs(c - exact) / bound).max())
+            ms8 = ctx.time_loop(8, 3, True)
+            form = ctx.gene8_form() if variant == 0 else 777
+            pipe_peak = capi.peak_probe(capi.PEAK_FP64_FMA, device)
+        out[label] = {"gene8_form": form, "ms_per_launch": ms8, "effective_fp64_tflops": flops / ms8 / 1e9,
+                      "vs_fp64_pipe_peak": flops / ms8 / 1e9 / pipe_peak, "max_normwise_error": err, "tolerance": 1e-12,
+                      "kernel": ("matmul_dmma on the FP64 pipe (auto mode found no error-free INT8 form: gene8_form 0); slice passes and the "
+                                 "auto launch that retires at once included" if variant == 0 else
+                                 "matmul_ozaki fixed 7-slice triangular form on the INT8 tensor cores (opt-in: its bound is relative to "
+                                 "the row maxima, not to sum|a||b|, so auto mode does not take it)")}
+    return out
+
+
+def sustained_block(ctx, n, dtype, device, roof, seconds):
+    """The timed region of the headline is milliseconds long (burst clocks).  Here: individuals back to back for >= `seconds`, clocks
+    sampled, then the dominant kernel back to back for ~2 s inside one event pair (mmx_time_gene8_contraction, flush_l2 = 2)."""
+    from paper_1806_01430_b200 import capi
+    flops = 2.0 * n ** 3
+    sampler = ClockSampler(device)
+    sampler.start()
+    t0 = time.perf_counter()
+    dev_s, k = 0.0, 0
+    while time.perf_counter() - t0 < seconds:
+        for _ in range(50):
+            dev_s += ctx.measure(GENOME_ALL_NESTS).time_s
+        k += 50
+    wall = time.perf_counter() - t0
+    clocks_ind = sampler.stop()
+    out = {"individuals": k, "wall_s": wall, "value": flops * k / dev_s / 1e9, "e2e": flops * k / wall / 1e9, "unit": "GFLOP/s",
+           "ms_per_individual": 1e3 * dev_s / k, "clocks": clocks_ind}
+    if roof is not None and roof.get("form"):
+        iters = max(100, int(2.0 / (roof["ms_per_launch"] * 1e-3)))
+        sampler = ClockSampler(device)
+        sampler.start()
+        ms = ctx.time_gene8_contraction(iters, 2)
+        clocks_k = sampler.stop()
+        ops = roof["slice_products_per_term"] * flops / (ms * 1e-3) / 1e12
+        scale = (clocks_k["sm_mhz"] / clocks_k["sm_max_mhz"]) if clocks_k.get("sm_mhz") and clocks_k.get("sm_max_mhz") else None
+        out["contraction"] = {"launches": iters, "ms_per_launch": ms, "achieved": ops, "unit": "TOP/s", "peak": roof["peak"],
+                              "frac": ops / roof["peak"], "clocks": clocks_k,
+                              "frac_at_the_sampled_clock": ops / (roof["peak"] * scale) if scale else None,
+                              "note": "back to back inside one CUDA-event pair, operands encoded once; peak = the burst issue peak of "
+                                      "roofline.peak, frac_at_the_sampled_clock scales it by median SM clock / max SM clock"}
+    return out
+
+
 def ncu_traffic(kernel: str, n: int):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel`, from the committed `ncu --set full`
     summary (profiles/ncu_traffic.json, written by tools/ncu_summary.py --traffic); None when not captured at this N."""
@@ -449,26 +548,30 @@ def fp32_arm(n, device, steps, peaks):
     out = {"value": flops * steps / dev_s / 1e9, "unit": "GFLOP/s", "steps": steps, "e2e": flops * steps / wall / 1e9,
            "ms_per_launch": ms8, "effective_fp32_tflops": flops / ms8 / 1e9,
            "vs_ffma_pipe_peak": flops / ms8 / 1e9 / ffma_peak, "ffma_pipe_peak_tflops": ffma_peak}
-    tf32_peak = peaks["bf16_tflops"] / 2.0
+    tf32_inferred = peaks["bf16_tflops"] / 2.0
+    tf32_peak = capi.peak_probe(capi.PEAK_UMMA_TF32, device)
 
     def tf32_roof(ms):
         return {"bound": "tensor", "achieved": 3.0 * flops / ms / 1e9, "peak": tf32_peak, "unit": "TFLOP/s",
-                "frac": 3.0 * flops / ms / 1e9 / tf32_peak, "traffic": ncu_traffic("matmul_3xtf32s", n),
-                "peak_source": "half of MEASURED_PEAKS.json bf16_tflops (TF32 runs at half the bf16 rate); "
-                               "achieved counts the three tensor-core products issued per FP32 term"}
+                "frac": 3.0 * flops / ms / 1e9 / tf32_peak, "peak_inferred": tf32_inferred,
+                "frac_vs_inferred": 3.0 * flops / ms / 1e9 / tf32_inferred, "traffic": ncu_traffic("matmul_3xtf32s", n),
+                "peak_source": "tcgen05.mma.kind::tf32 issue peak measured in this run (csrc/peaks.cu); peak_inferred = half of "
+                               "MEASURED_PEAKS.json bf16_tflops; achieved counts the three tensor-core products issued per FP32 term"}
     tf32_kernel = ("matmul_3xtf32s (gene 8: three TF32 products per term on tcgen05, b parts stacked along N so two of them share one "
                    "N=256 MMA; compensated accumulation; split passes included)")
     if form > 0:
         sa, sb, lv = form // 100, form // 10 % 10, form % 10
         products = sum(1 for t in range(1, sa + 1) for u in range(1, sb + 1) if t + u <= lv + 1)
-        int8_peak = 2.0 * peaks["bf16_tflops"]
+        int8_inferred = 2.0 * peaks["bf16_tflops"]
+        int8_peak = capi.peak_probe(capi.PEAK_UMMA_I8, device)
         ops = products * flops / ms8 / 1e9
         out["kernel"] = (f"matmul_ozaki_auto<float> form {form} (gene 8: the float operands' exact 7-bit INT8 digits, {sa} x {sb} pairs = "
                          f"{products} slice products per term, result = the exact product rounded once to float; slice passes and the "
                          f"three guarded split-TF32 launches included)")
         out["roofline"] = {"bound": "tensor", "pipe": "int8", "achieved": ops, "peak": int8_peak, "unit": "TOP/s", "frac": ops / int8_peak,
+                           "peak_inferred": int8_inferred, "frac_vs_inferred": ops / int8_inferred,
                            "traffic": None, "form": form, "slice_products_per_term": products,
-                           "peak_source": "twice MEASURED_PEAKS.json bf16_tflops; whole nest (slice passes included)"}
+                           "peak_source": "tcgen05.mma.kind::i8 issue peak measured in this run (csrc/peaks.cu); whole nest (digit planes included)"}
         d2, w2, ms30, _ = run(30)
         out["split_tf32"] = {"value": flops * steps / d2 / 1e9, "unit": "GFLOP/s", "e2e": flops * steps / w2 / 1e9, "kernel": tf32_kernel,
                              "ms_per_launch": ms30, "effective_fp32_tflops": flops / ms30 / 1e9, "roofline": tf32_roof(ms30),

@@ -253,7 +253,9 @@ MMX_API int mmx_gene8_form(mmx_ctx* ctx, int slot, int32_t* form_out);
 /* FP64 auto-mode contexts: time the CONTRACTION of gene 8 alone (mmx_time_loop(8) times the whole nest: two slice passes, the
  * contraction, the guarded FP64-pipe launch).  One full launch encodes the operands; each of the `iters` timed launches reuses the
  * digit planes and runs the contraction kernel plus the guarded FP64-pipe launch (c accumulates).  CUDA events on the slot's stream,
- * L2 flushed before each launch when flush_l2 != 0; ms_out = mean per launch.  The roofline of the dominant kernel (bench.py). */
+ * L2 flushed before each launch when flush_l2 == 1; flush_l2 == 2: the `iters` launches back to back inside ONE event pair (the sustained
+ * rate of the kernel; c and the digit planes stay where the cache leaves them); ms_out = mean per launch.  The roofline of the dominant
+ * kernel (bench.py). */
 MMX_API int mmx_time_gene8_contraction(mmx_ctx* ctx, int slot, int iters, int flush_l2, double* ms_out);
 
 /* The rule behind mmx_gene8_form, evaluated on the host (no device needed): the form the auto launch takes for operands of which

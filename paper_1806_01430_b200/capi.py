@@ -295,8 +295,9 @@ class Context:
         self._check(self._lib.mmx_gene8_form(self._h, slot, C.byref(v)))
         return v.value
 
-    def time_gene8_contraction(self, iters: int = 5, flush_l2: bool = True, slot: int = 0) -> float:
-        """ms per launch of the gene-8 contraction alone (FP64 auto mode): operands encoded once, reused by the timed launches."""
+    def time_gene8_contraction(self, iters: int = 5, flush_l2: bool | int = True, slot: int = 0) -> float:
+        """ms per launch of the gene-8 contraction alone (FP64 auto mode): operands encoded once, reused by the timed launches.
+        flush_l2 = 2: the launches back to back inside one event pair (sustained rate)."""
         ms = C.c_double()
         self._check(self._lib.mmx_time_gene8_contraction(self._h, slot, iters, int(flush_l2), C.byref(ms)))
         return ms.value
