@@ -13,6 +13,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -53,8 +54,19 @@ struct Slot {
   bool host_valid[MMX_NUM_ARRAYS] = {};
   bool dev_valid[MMX_NUM_ARRAYS] = {};
   bool host_diag_only = false;  // host c holds only its diagonal
+  // Digit planes of gene 8's operands (auto mode, csrc/ozaki_digits.cuh).  When a plan runs the matmul nest as one launch, the
+  // kernels that PRODUCE a and bt (init-a fill, transpose) write the planes from their registers (`fuse_planes`), and gene 8 skips
+  // the slice pass of every operand whose planes are still valid.  Any other write to the array drops the flag.
+  void* oz_planes = nullptr;       // base of the planes inside d_scratch (FP32: behind the split-TF32 area)
+  bool fuse_planes = false;        // set per plan / per API call
+  bool planes_a_valid = false, planes_bt_valid = false;
+  bool b_colexp_valid = false;     // the exponents of bt's rows were written by the init-b kernel (closed form of its own output)
   std::map<int, Train> trains;  // by gene
-  std::map<unsigned, cudaGraphExec_t> plan_graphs;  // by genome mask: whole device-only individuals
+  struct PlanGraph {
+    cudaGraphExec_t exec = nullptr;
+    bool planes_a = false, planes_bt = false, colexp = false;  // the flags as the captured sequence leaves them
+  };
+  std::map<unsigned, PlanGraph> plan_graphs;  // by genome mask: whole device-only individuals
   mmx_run_stats stats{};
   std::mutex mu;
   // row-sharded group membership (mmx_shard_*): this slot is member `shard_rank` of `shard_world`
@@ -120,17 +132,50 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
   T* b = static_cast<T*>(s.d_arr[MMX_ARRAY_B]);
   T* c = static_cast<T*>(s.d_arr[MMX_ARRAY_C]);
   T* bt = static_cast<T*>(s.d_arr[MMX_ARRAY_BT]);
+  // fused producers: whole-nest launches of a plan whose matmul nest is one launch, auto mode, sizes without plane padding
+  const bool fuse = s.fuse_planes && s.oz_planes != nullptr && row0 == 0 && rows == n && ozaki_fusable(n);
   switch (gene) {
-    case 0: return launch_fill2d<T>(FILL_INIT_A, a, n, row0, rows, s.stream);
-    case 1: return launch_fill_row<T>(FILL_INIT_A, a, n, iter, s.stream);
-    case 2: return launch_fill2d<T>(FILL_INIT_B, b, n, row0, rows, s.stream);
-    case 3: return launch_fill_row<T>(FILL_INIT_B, b, n, iter, s.stream);
+    case 0:
+      s.planes_a_valid = false;
+      if (fuse) {
+        const cudaError_t e = launch_fill_a_planes<T>(a, n, matmul_ozaki_operand(s.oz_planes, n, 0), s.stream);
+        s.planes_a_valid = e == cudaSuccess;
+        return e;
+      }
+      return launch_fill2d<T>(FILL_INIT_A, a, n, row0, rows, s.stream);
+    case 1: s.planes_a_valid = false; return launch_fill_row<T>(FILL_INIT_A, a, n, iter, s.stream);
+    case 2:
+      s.b_colexp_valid = false;
+      if (fuse) {
+        const cudaError_t e = launch_fill_b_colexp<T>(b, n, matmul_ozaki_operand(s.oz_planes, n, 1).exps, s.stream);
+        s.b_colexp_valid = e == cudaSuccess;
+        return e;
+      }
+      return launch_fill2d<T>(FILL_INIT_B, b, n, row0, rows, s.stream);
+    case 3: s.b_colexp_valid = false; return launch_fill_row<T>(FILL_INIT_B, b, n, iter, s.stream);
     case 4: return launch_fill2d<T>(FILL_ZERO, c, n, row0, rows, s.stream);
     case 5: return launch_fill_row<T>(FILL_ZERO, c, n, iter, s.stream);
-    case 6: return launch_transpose<T>(bt, b, n, row0, rows, s.stream);
-    case 7: return launch_transpose_row<T>(bt, b, n, iter, s.stream);
+    case 6:
+      s.planes_bt_valid = false;
+      if (fuse && s.b_colexp_valid) {
+        const cudaError_t e = launch_transpose_planes<T>(bt, b, n, matmul_ozaki_operand(s.oz_planes, n, 1), s.stream);
+        s.planes_bt_valid = e == cudaSuccess;
+        return e;
+      }
+      return launch_transpose<T>(bt, b, n, row0, rows, s.stream);
+    case 7: s.planes_bt_valid = false; return launch_transpose_row<T>(bt, b, n, iter, s.stream);
     case 8: {
-      const int variant = ctx->cfg.matmul_variant;  // 0 = auto (matmul.cu)
+      int variant = ctx->cfg.matmul_variant;  // 0 = auto (matmul.cu)
+      if (variant == 0 && row0 == 0 && rows == n && s.oz_planes != nullptr) {
+        if (s.planes_a_valid) variant |= kReuseOperandA;
+        if (s.planes_bt_valid) variant |= kReuseOperandBt;
+        else s.b_colexp_valid = false;  // the slice pass of bt writes its own row exponents
+      } else {
+        s.b_colexp_valid = false;  // row / column blocks re-encode parts of the planes
+      }
+      // one consumer per encoding: the next launch of gene 8 encodes again unless a producer has rewritten the planes by then
+      // (mmx_time_loop(8) therefore times the whole nest, slice passes included, whatever ran before)
+      s.planes_a_valid = s.planes_bt_valid = false;
       return launch_matmul<T>(c, a, bt, n, row0, rows, 0, n, strict, variant, s.d_scratch, s.stream);
     }
     case 9: return launch_gemv_row<T>(c, a, bt, n, iter, strict, s.stream);
@@ -147,6 +192,14 @@ cudaError_t launch_gene_rows(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter
 
 cudaError_t launch_gene_any(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter) {
   return launch_gene_rows(ctx, s, gene, iter, 0, ctx->cfg.n);
+}
+
+// Start of a sequence of launches (a plan run, a capture, a single-kernel API call): no planes are valid yet, and the producers
+// of a and bt write them iff the matmul nest will consume them as ONE launch (MMX_FUSE_PLANES=0 switches the fusion off: A/B runs)
+void begin_sequence(Slot& s, bool matmul_is_one_launch) {
+  static const bool enabled = [] { const char* e = getenv("MMX_FUSE_PLANES"); return e == nullptr || atoi(e) != 0; }();
+  s.fuse_planes = enabled && matmul_is_one_launch && s.oz_planes != nullptr;
+  s.planes_a_valid = s.planes_bt_valid = s.b_colexp_valid = false;
 }
 
 // gene that serves `nest` in `mode`
@@ -283,11 +336,14 @@ cudaError_t prepare_plan_graph(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan,
   if (!ctx->cfg.launch_batching || !device_only(plan) || s.plan_graphs.count(mask)) return cudaSuccess;
   // first-use work (function attributes, module load) must not happen inside a capture
   cudaError_t e = cudaSuccess;
+  const bool one_launch = plan.modes[MMX_NEST_MATMUL] == MMX_MODE_GPU_NEST;
+  begin_sequence(s, one_launch);
   for (int si = 0; si < plan.num_steps && e == cudaSuccess; ++si)
     if (plan.steps[si].kind == MMX_STEP_GPU) e = launch_gene_any(ctx, s, gene_of(plan.steps[si].nest, plan.steps[si].mode), IterRef{nullptr, 0});
   if (e == cudaSuccess) e = cudaStreamSynchronize(s.stream);
   if (e != cudaSuccess) return e;
   cudaGraph_t graph = nullptr;
+  begin_sequence(s, one_launch);
   if ((e = cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
   const std::size_t esz = elem_size(ctx->cfg.dtype);
   for (int si = 0; si < plan.num_steps && e == cudaSuccess; ++si) {
@@ -297,15 +353,18 @@ cudaError_t prepare_plan_graph(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan,
   }
   const cudaError_t e2 = cudaStreamEndCapture(s.stream, &graph);
   if (e == cudaSuccess) e = e2;
-  cudaGraphExec_t exec = nullptr;
-  if (e == cudaSuccess) e = cudaGraphInstantiate(&exec, graph, 0);
+  Slot::PlanGraph pg;
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&pg.exec, graph, 0);
   if (graph) cudaGraphDestroy(graph);
-  if (e == cudaSuccess) s.plan_graphs[mask] = exec;
+  pg.planes_a = s.planes_a_valid;
+  pg.planes_bt = s.planes_bt_valid;
+  pg.colexp = s.b_colexp_valid;
+  if (e == cudaSuccess) s.plan_graphs[mask] = pg;
   return e;
 }
 
 // One benchmark run of a feasible plan on a prepared slot.
-RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, cudaGraphExec_t whole) {
+RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const Slot::PlanGraph* whole) {
   RunResult rr;
   const std::size_t mbytes = matrix_bytes(ctx);
   const std::size_t esz = elem_size(ctx->cfg.dtype);
@@ -320,12 +379,16 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, cudaGr
   bool any_gpu = false, timed_out = false, sum_on_device = false;
   cudaError_t e = cudaSuccess;
 
+  begin_sequence(s, plan.modes[MMX_NEST_MATMUL] == MMX_MODE_GPU_NEST);
   const Clock::time_point t0 = Clock::now();
   const Deadline dl{t0 + std::chrono::duration_cast<Clock::duration>(Seconds(budget))};
   e = cudaEventRecord(s.ev_begin, s.stream);
 
   if (whole != nullptr) {
-    if (e == cudaSuccess) e = cudaGraphLaunch(whole, s.stream);
+    if (e == cudaSuccess) e = cudaGraphLaunch(whole->exec, s.stream);
+    s.planes_a_valid = whole->planes_a;
+    s.planes_bt_valid = whole->planes_bt;
+    s.b_colexp_valid = whole->colexp;
     s.stats.graph_launches = 1;
     any_gpu = true;
     for (int si = 0; si < plan.num_steps; ++si) {
@@ -343,6 +406,9 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, cudaGr
       case MMX_STEP_H2D:
         e = cudaMemcpyAsync(s.d_arr[st.array], s.h_arr[st.array], mbytes, cudaMemcpyHostToDevice, s.stream);
         s.dev_valid[st.array] = true;
+        if (st.array == MMX_ARRAY_A) s.planes_a_valid = false;
+        if (st.array == MMX_ARRAY_BT) s.planes_bt_valid = false;
+        if (st.array == MMX_ARRAY_B) s.b_colexp_valid = false;
         any_gpu = true;
         break;
       case MMX_STEP_D2H:
@@ -474,7 +540,7 @@ int measure_on_slot(mmx_ctx* ctx, int slot, const std::uint8_t* bits, std::size_
   for (std::size_t k = 0; k < gene_len; ++k) mask |= (bits[k] ? 1u : 0u) << k;
   MMX_CUDA(ctx, prepare_plan_graph(ctx, s, plan, mask));
   const auto whole_it = s.plan_graphs.find(mask);
-  const cudaGraphExec_t whole = whole_it == s.plan_graphs.end() ? nullptr : whole_it->second;
+  const Slot::PlanGraph* whole = whole_it == s.plan_graphs.end() ? nullptr : &whole_it->second;
 
   for (int w = 0; w < ctx->cfg.warmup; ++w) {
     const RunResult r = run_plan_once(ctx, s, plan, whole);
@@ -505,7 +571,7 @@ void destroy_slot(Slot& s) {
   for (auto& kv : s.trains)
     if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   for (auto& kv : s.plan_graphs)
-    if (kv.second) cudaGraphExecDestroy(kv.second);
+    if (kv.second.exec) cudaGraphExecDestroy(kv.second.exec);
   for (int q = 0; q < MMX_NUM_ARRAYS; ++q) {
     if (s.d_arr[q]) cudaFree(s.d_arr[q]);
     if (s.h_arr[q]) cudaFreeHost(s.h_arr[q]);
@@ -637,6 +703,7 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
         if ((e = matmul_ozaki_prepare()) != cudaSuccess) return fail(e, "matmul_ozaki_prepare");
         if ((e = cudaMalloc(&sl.d_scratch, off + planes)) != cudaSuccess) return fail(e, "cudaMalloc(scratch)");
         void* oz = static_cast<char*>(sl.d_scratch) + off;
+        sl.oz_planes = oz;
         if ((e = cudaMemset(oz, 0, planes)) != cudaSuccess) return fail(e, "cudaMemset(scratch)");
         sl.gene8_form_word = matmul_ozaki_form_word(oz, cfg->n);
         if ((e = cudaMemset(sl.gene8_form_word, 0xff, sizeof(int))) != cudaSuccess) return fail(e, "cudaMemset(form)");
@@ -652,6 +719,7 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
         // auto mode relies on a zero-filled scratch (digit planes nobody has written yet are zero, matmul_ozaki.cu)
         if ((e = cudaMemset(sl.d_scratch, 0, matmul_ozaki_scratch_bytes(cfg->n))) != cudaSuccess) return fail(e, "cudaMemset(scratch)");
         sl.gene8_form_word = matmul_ozaki_form_word(sl.d_scratch, cfg->n);
+        sl.oz_planes = sl.d_scratch;
         if ((e = cudaMemset(sl.gene8_form_word, 0xff, sizeof(int))) != cudaSuccess) return fail(e, "cudaMemset(form)");
         sl.gene8_form_valid = true;
       }
@@ -767,6 +835,9 @@ MMX_API int mmx_upload_array(mmx_ctx* ctx, int slot, int array, const void* host
   MMX_CUDA(ctx, cudaStreamSynchronize(s.stream));
   s.dev_valid[array] = true;
   s.host_valid[array] = false;
+  if (array == MMX_ARRAY_A) s.planes_a_valid = false;
+  if (array == MMX_ARRAY_BT) s.planes_bt_valid = false;
+  if (array == MMX_ARRAY_B) s.b_colexp_valid = false;
   return MMX_OK;
 }
 
@@ -779,6 +850,7 @@ MMX_API int mmx_run_loop(mmx_ctx* ctx, int slot, int gene, int i, int j, double*
   std::lock_guard<std::mutex> g(s.mu);
   MMX_CUDA(ctx, cudaSetDevice(s.device));
   const int it = gene == 10 ? i * n + j : i;
+  s.fuse_planes = false;  // single kernels: producers write their array only, gene 8 encodes what it needs
   MMX_CUDA(ctx, launch_gene_any(ctx, s, gene, IterRef{nullptr, it}));
   const int w = written_array(kCatalogue[gene].nest);
   if (w >= 0) {
@@ -806,6 +878,7 @@ MMX_API int mmx_run_loop_rows(mmx_ctx* ctx, int slot, int gene, int row0, int ro
   Slot& s = *ctx->slots[slot];
   std::lock_guard<std::mutex> g(s.mu);
   MMX_CUDA(ctx, cudaSetDevice(s.device));
+  s.fuse_planes = false;
   MMX_CUDA(ctx, launch_gene_rows(ctx, s, gene, IterRef{nullptr, 0}, row0, rows));
   const int w = written_array(kCatalogue[gene].nest);
   if (w >= 0) {
@@ -897,6 +970,7 @@ MMX_API int mmx_time_loop(mmx_ctx* ctx, int slot, int gene, int iters, int flush
     MMX_CUDA(ctx, launch_scrub(s.d_scrub, s.scrub_bytes, s.stream));
   }
   double total = 0.0;
+  s.fuse_planes = false;
   for (int it = 0; it < iters; ++it) {
     if (flush_l2) MMX_CUDA(ctx, launch_evict(s.d_scrub, s.scrub_bytes, s.stream));
     MMX_CUDA(ctx, cudaEventRecord(s.ev_begin, s.stream));
@@ -972,6 +1046,7 @@ int shard_phase1(mmx_ctx* ctx, Slot& s) {
   const int n = ctx->cfg.n;
   int r0 = 0, rows = 0;
   shard_block(n, s.shard_world, s.shard_rank, &r0, &rows);
+  begin_sequence(s, false);  // row blocks: the contraction encodes what it needs, block by block
   MMX_CUDA(ctx, cudaEventRecord(s.ev_begin, s.stream));
   MMX_CUDA(ctx, launch_fill2d<T>(FILL_INIT_A, static_cast<T*>(s.d_arr[MMX_ARRAY_A]), n, r0, rows, s.stream));
   MMX_CUDA(ctx, launch_fill2d<T>(FILL_INIT_B, static_cast<T*>(s.d_arr[MMX_ARRAY_B]), n, 0, n, s.stream));

@@ -8,6 +8,7 @@
 // multiply (POW2 path) -- same bits, and it keeps the nest write-bound instead of
 // FP64-divide-bound.
 #include "kernels.cuh"
+#include "ozaki_digits.cuh"
 
 namespace mmx {
 namespace {
@@ -68,6 +69,56 @@ __global__ void __launch_bounds__(256) fill_row_kernel(T* __restrict__ dst, int 
 }
 
 inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// ---- init-a + the digit planes of a (gene 0 fused with the encoding gene 8 needs; ozaki_digits.cuh) -----------------------------
+// A CTA covers 8 rows x 1024 columns; a thread owns 4 consecutive columns of each of its 8 rows: it stores them (128-bit stores) and,
+// from the same registers, their 7-bit digits (one 32-bit store per plane).  The row exponent needs the row's largest magnitude:
+// (i + j) / N is non-negative and grows with j, so it is the row's last element -- every thread computes it for itself.
+template <typename T, bool POW2>
+__global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst, int n, T nn, T inv_n, OzOperand P) {
+  const int j0 = (blockIdx.x * 256 + threadIdx.x) * 4;
+  const int i0 = blockIdx.y * kRowsPerThread;
+  const int dirty = P.guard[P.dirty_slot];
+  int lossy = 0, top = 0;
+  if (j0 < n) {
+#pragma unroll
+    for (int r = 0; r < kRowsPerThread; ++r) {
+      const int i = i0 + r;
+      if (i >= n) break;
+      T x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = fill_value<T, FILL_INIT_A, POW2>(i, j0 + q, nn, inv_n);
+      T* at = dst + static_cast<size_t>(i) * n + j0;
+      if constexpr (sizeof(T) == 8) {
+        *reinterpret_cast<double2*>(at) = make_double2(x[0], x[1]);
+        *reinterpret_cast<double2*>(at + 2) = make_double2(x[2], x[3]);
+      } else {
+        *reinterpret_cast<float4*>(at) = make_float4(x[0], x[1], x[2], x[3]);
+      }
+      const double m = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, n - 1, nn, inv_n));
+      const int e = oz_row_exponent(m, false);
+      bool tiny;
+      const double inv = oz_row_scale(e, true, false, &tiny);
+      lossy |= tiny;
+      if (j0 == 0) P.exps[i] = e;
+      const double v[4] = {static_cast<double>(x[0]), static_cast<double>(x[1]), static_cast<double>(x[2]), static_cast<double>(x[3])};
+      oz_emit<7, 4>(v, inv, false, dirty, P.planes + static_cast<size_t>(i) * P.kq, P.plane, j0, lossy, top);
+    }
+  }
+  oz_guard_commit(lossy, top, P.guard, P.lossy_slot, P.top_slot, P.dirty_slot);
+}
+
+// ---- init-b + the digit exponent of every COLUMN of b (= row of bt) ------------------------------------------------------------------
+// |i - j| / N over a column j is largest at i = 0 or i = N - 1: a one-thread-per-column kernel behind the fill writes the exponents
+// the transpose kernel needs before it can emit the digits of bt.
+template <typename T, bool POW2>
+__global__ void __launch_bounds__(256) colexp_b_kernel(int* __restrict__ colexp, int n, T nn, T inv_n) {
+  const int j = blockIdx.x * 256 + threadIdx.x;
+  if (j >= n) return;
+  const double top = fabs(static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(0, j, nn, inv_n)));
+  const double bot = fabs(static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(n - 1, j, nn, inv_n)));
+  colexp[j] = oz_row_exponent(fmax(top, bot), false);
+}
 
 template <typename T, int OP, bool POW2, int V>
 cudaError_t fill2d_go(T* dst, int n, int row0, int rows, cudaStream_t stream) {
@@ -132,6 +183,33 @@ cudaError_t launch_fill_row(int op, T* dst, int n, IterRef iter, cudaStream_t st
   if (op == FILL_ZERO) return vec ? fill_row_go<T, FILL_ZERO, true, W>(dst, n, iter, stream) : fill_row_go<T, FILL_ZERO, true, 1>(dst, n, iter, stream);
   return cudaErrorInvalidValue;
 }
+
+
+template <typename T>
+cudaError_t launch_fill_a_planes(T* a, int n, const OzOperand& pa, cudaStream_t stream) {
+  if (!ozaki_fusable(n) || pa.kq != n) return cudaErrorInvalidValue;
+  // the guard words of a start from zero for this encoding (the slice pass does the same before it runs)
+  if (cudaError_t e = cudaMemsetAsync(pa.guard + pa.lossy_slot, 0, 2 * sizeof(int), stream); e != cudaSuccess) return e;   // words 0, 1
+  const dim3 grid((n + 1023) / 1024, (n + kRowsPerThread - 1) / kRowsPerThread);
+  const T nn = static_cast<T>(n), inv = static_cast<T>(1.0) / static_cast<T>(n);
+  if (is_pow2(n)) fill_a_planes_kernel<T, true><<<grid, 256, 0, stream>>>(a, n, nn, inv, pa);
+  else fill_a_planes_kernel<T, false><<<grid, 256, 0, stream>>>(a, n, nn, inv, pa);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_fill_b_colexp(T* b, int n, int* colexp, cudaStream_t stream) {
+  if (cudaError_t e = launch_fill2d<T>(FILL_INIT_B, b, n, 0, n, stream); e != cudaSuccess) return e;
+  const T nn = static_cast<T>(n), inv = static_cast<T>(1.0) / static_cast<T>(n);
+  if (is_pow2(n)) colexp_b_kernel<T, true><<<(n + 255) / 256, 256, 0, stream>>>(colexp, n, nn, inv);
+  else colexp_b_kernel<T, false><<<(n + 255) / 256, 256, 0, stream>>>(colexp, n, nn, inv);
+  return cudaGetLastError();
+}
+
+template cudaError_t launch_fill_a_planes<double>(double*, int, const OzOperand&, cudaStream_t);
+template cudaError_t launch_fill_a_planes<float>(float*, int, const OzOperand&, cudaStream_t);
+template cudaError_t launch_fill_b_colexp<double>(double*, int, int*, cudaStream_t);
+template cudaError_t launch_fill_b_colexp<float>(float*, int, int*, cudaStream_t);
 
 template cudaError_t launch_fill2d<double>(int, double*, int, int, int, cudaStream_t);
 template cudaError_t launch_fill2d<float>(int, float*, int, int, int, cudaStream_t);

@@ -52,6 +52,30 @@ template <typename T> cudaError_t launch_transpose_push(const BtPeers& peers, co
 // gene 7: row i of bt = column i of b
 template <typename T> cudaError_t launch_transpose_row(T* bt, const T* b, int n, IterRef iter, cudaStream_t stream);
 
+// ---- producers that also write an operand's digit planes for gene 8 (ozaki_digits.cuh, matmul_ozaki.cu) -----------------
+// Where one operand's planes live inside a context's scratch (matmul_ozaki_operand): plane t of row r at planes + t * plane +
+// r * kq, one exponent per row, the guard words and which of them belong to this operand.
+struct OzOperand {
+  signed char* planes = nullptr;
+  size_t plane = 0;
+  int kq = 0;
+  int* exps = nullptr;
+  int* guard = nullptr;
+  int lossy_slot = 0, top_slot = 0, dirty_slot = 0;
+};
+// which = 0: a (rows absolute), 1: bt (rows relative to the launch's first column: whole-nest launches only)
+OzOperand matmul_ozaki_operand(void* scratch, int n, int which);
+// the fused producers cover whole-nest launches of sizes whose planes need no padding
+inline bool ozaki_fusable(int n) { return n >= 1024 && n % 64 == 0; }
+// gene 0 over the whole array + the digit planes, row exponents and guard words of a (the values are in registers; the row
+// maximum of (i + j) / N is its last element)
+template <typename T> cudaError_t launch_fill_a_planes(T* a, int n, const OzOperand& pa, cudaStream_t stream);
+// gene 2 over the whole array + colexp[j] = digit exponent of COLUMN j of b (= row j of bt), known in closed form for
+// (i - j) / N: what launch_transpose_planes needs before it can emit digits
+template <typename T> cudaError_t launch_fill_b_colexp(T* b, int n, int* colexp, cudaStream_t stream);
+// gene 6 over the whole array + the digit planes and guard words of bt, given pb.exps[j] for every row j of bt
+template <typename T> cudaError_t launch_transpose_planes(T* bt, const T* b, int n, const OzOperand& pb, cudaStream_t stream);
+
 // gene 8: c[i][j] += sum_k a[i][k] * bt[j][k] (matmul.c:25-28).  variant: 1 SIMT, 2 DMMA (FP64 only).
 // Rows [row0, row0+rows) of a and c, columns [col0, col0+cols) of c (= rows of bt) only: the whole nest is
 // (0, n, 0, n); the row-sharded multi-GPU path passes its row block and walks the column blocks in the
@@ -129,10 +153,13 @@ constexpr int kReuseOperandA = 0x1000;
 // OR-ed into `variant` (FP64 auto mode): BOTH operands are as the previous launch_matmul on this scratch encoded them -- the launch is
 // the contraction (and the guarded FP64-pipe launch) alone.  For timing the contraction kernel by itself (mmx_time_gene8_contraction).
 constexpr int kReuseOperands = 0x2000;
+// OR-ed into `variant` (auto mode): the digit planes, row exponents and guard words of bt are valid for this launch's columns -- the
+// kernel that produced bt wrote them (launch_transpose_planes).  kReuseOperandA | kReuseOperandBt == kReuseOperands in effect.
+constexpr int kReuseOperandBt = 0x4000;
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0,
                                 int cols, int slices, cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false, bool reuse_bt = false);
 cudaError_t launch_matmul_ozaki_f32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                    cudaStream_t stream, int** guard_out, bool reuse_a = false);
+                                    cudaStream_t stream, int** guard_out, bool reuse_a = false, bool reuse_bt = false);
 // device word in `scratch` where the auto launch records the form it ran: 2 .. 7 slices, 0 = left to the FP64 pipe
 int* matmul_ozaki_form_word(void* scratch, int n);
 // gene 9: row i of the same (GEMV against bt)

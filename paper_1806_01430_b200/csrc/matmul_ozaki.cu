@@ -35,6 +35,7 @@
 #include <cstdlib>
 
 #include "kernels.cuh"
+#include "ozaki_digits.cuh"
 #include "raster.cuh"
 #include "tc_ptx.cuh"
 
@@ -80,9 +81,9 @@ __device__ __forceinline__ void tc_mma_i8(unsigned d_tmem, unsigned long long ad
       : "memory");
 }
 
-__device__ __forceinline__ double pow2(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
+__device__ __forceinline__ double pow2(int e) { return oz_pow2(e); }
 
-constexpr int kNonFinite = 0x7fffffff;  // row exponent of a row that holds an Inf or a NaN: its products are NaN
+constexpr int kNonFinite = kOzNonFinite;  // row exponent of a row that holds an Inf or a NaN: its products are NaN
 // acc * 2^(ea + eb - 12): exact scaling (ldexp also covers results that leave the normal range)
 __device__ __forceinline__ double scaled(double acc, int ea, int eb) {
   if (ea == kNonFinite || eb == kNonFinite) return __longlong_as_double(0x7ff8000000000000ll);
@@ -749,7 +750,6 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const T* __restrict
                                                           size_t plane, int n, int kq, int src_row0, int nrows, int dst_row0,
                                                           int* __restrict__ guard, int lossy_slot, int top_slot, int dirty_slot) {
   __shared__ double red[8];
-  __shared__ int top_sh[8];
   __shared__ int e_sh;
   const int r = blockIdx.x;  // relative row
   const int tid = threadIdx.x;
@@ -805,16 +805,16 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const T* __restrict
     double m = red[0];
 #pragma unroll
     for (int w = 1; w < 8; ++w) m = fmax(m, red[w]);
-    const int e = (m > 0.0 && !bad) ? ilogb(m) + 1 : 0;
+    const int e = oz_row_exponent(m, bad != 0);
     e_sh = e;
     exps[dst_row0 + r] = bad ? kNonFinite : e;
   }
   __syncthreads();
   // exact power of two; a non-finite row gets zero digits, and so does a row whose maximum is below 2^-970 (1 / 2^e would
   // overflow): both are flagged as lossy.  (Digit extraction by 64-bit integer arithmetic was measured slower than
-  // the FP64 form below: 85 us against 70 us per operand at N = 4096.)
-  const bool tiny = e_sh < -970;
-  const double inv = (live && !bad && !tiny) ? scalbn(1.0, -e_sh) : 0.0;
+  // the FP64 form of oz_emit: 85 us against 70 us per operand at N = 4096.)
+  bool tiny;
+  const double inv = oz_row_scale(e_sh, live, bad != 0, &tiny);
   signed char* drow = dst + static_cast<size_t>(dst_row0 + r) * kq;
   int lossy = bad | tiny, top = 0;  // top = highest non-zero digit (1-based) this thread has seen
   // Auto mode keeps an invariant on its scratch (zero-filled when the context is created): planes beyond guard[dirty_slot] hold
@@ -822,66 +822,17 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const T* __restrict
   // element instead of 7.  The word only ever grows, to the highest plane any launch wrote a non-zero digit into; a CTA that
   // reads it after a neighbour has raised it merely writes more zeros.
   const int dirty = dirty_slot >= 0 ? guard[dirty_slot] : S;
-  auto emit4 = [&](int k0, const double (&v)[4]) {
-    int dig[S] = {};
-    int levels = S;  // digit levels walked: the planes beyond hold zeros for these four elements
-    double rem[4];
-#pragma unroll
-    for (int q = 0; q < 4; ++q) rem[q] = bad ? 0.0 : v[q] * inv;
-#pragma unroll
-    for (int t = 0; t < S; ++t) {
-      // four elements per digit level, branch-free (a zero remainder yields a zero digit); one test per level ends the walk
-      // once nothing is left -- short operands finish after a digit or two
-      if (t >= 1 && rem[0] == 0.0 && rem[1] == 0.0 && rem[2] == 0.0 && rem[3] == 0.0) {
-        levels = t;
-        break;
-      }
-      const double up = pow2(7 * (t + 1) - 1), down = pow2(-(7 * (t + 1) - 1));
-      int word = 0;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        // rint without the conversion units (they would bound this pass): adding 1.5 * 2^52 rounds to the integer grid
-        // (ties to even) and leaves the integer in the low word of the sum
-        const double shifted = fma(rem[q], up, 6755399441055744.0);
-        const int d = __double2loint(shifted);
-        rem[q] = fma(-(shifted - 6755399441055744.0), down, rem[q]);  // exact: removes a prefix of rem's bits
-        word |= (d & 0xff) << (8 * q);
-      }
-      dig[t] = word;
-    }
-    // bits below the last digit: the slices do not reproduce this element exactly
-    lossy |= (rem[0] != 0.0) | (rem[1] != 0.0) | (rem[2] != 0.0) | (rem[3] != 0.0);
-    const int planes_to_write = max(levels, dirty);  // beyond: zero digits into planes that hold only zeros
-#pragma unroll
-    for (int t = 0; t < S; ++t) {
-      if (t >= planes_to_write) break;
-      if (dig[t] != 0) top = max(top, t + 1);
-      if (t < dirty || dig[t] != 0) *reinterpret_cast<int*>(drow + t * plane + k0) = dig[t];
-    }
-  };
 #pragma unroll
   for (int it = 0; it < KEEP; ++it) {
     const int k0 = (it * 256 + tid) * 4;
-    if (k0 < kq) emit4(k0, keep[it]);
+    if (k0 < kq) oz_emit<S, 4>(keep[it], inv, bad != 0, dirty, drow, plane, k0, lossy, top);
   }
   for (int k0 = (KEEP * 256 + tid) * 4; k0 < kq; k0 += 256 * 4) {
     double v[4];
     load4(k0, v);
-    emit4(k0, v);
+    oz_emit<S, 4>(v, inv, bad != 0, dirty, drow, plane, k0, lossy, top);
   }
-  if (guard != nullptr) {
-    lossy = __syncthreads_or(lossy);
-    top = __reduce_max_sync(0xffffffffu, top);
-    if (tid % 32 == 0) top_sh[tid / 32] = top;
-    __syncthreads();
-    if (tid == 0) {
-#pragma unroll
-      for (int w = 1; w < 8; ++w) top = max(top, top_sh[w]);
-      if (lossy && guard[lossy_slot] == 0) atomicOr(guard + lossy_slot, 1);
-      if (top > guard[top_slot]) atomicMax(guard + top_slot, top);  // read first: after a few rows nobody needs the atomic
-      if (dirty_slot >= 0 && top > guard[dirty_slot]) atomicMax(guard + dirty_slot, top);
-    }
-  }
+  if (guard != nullptr) oz_guard_commit(lossy, top, guard, lossy_slot, top_slot, dirty_slot);
 }
 
 // [S][rows][kq] bytes; box = 64 bytes x box_rows rows x S slices; 64-byte swizzle
@@ -934,18 +885,20 @@ struct OzLayout {
 // the slice passes (P planes); with_guard: also record whether anything was cut and the highest digits in use
 template <int P, typename T = double>
 cudaError_t oz_slices(const T* a, const T* bt, void* scratch, int n, int row0, int rows, int col0, int cols, cudaStream_t stream,
-                      bool with_guard, bool reuse_a) {
+                      bool with_guard, bool reuse_a, bool reuse_bt = false) {
   const OzLayout L(scratch, n, P);
   int* flag = with_guard ? L.guard : nullptr;
-  if (with_guard)
-    if (cudaError_t e = reuse_a ? cudaMemsetAsync(flag + 2, 0, 2 * sizeof(int), stream) : cudaMemsetAsync(flag, 0, 4 * sizeof(int), stream);
-        e != cudaSuccess)
-      return e;
+  if (with_guard && !(reuse_a && reuse_bt)) {
+    // the words of the operand(s) sliced here: {0, 1} belong to a, {2, 3} to bt
+    int* first = reuse_a ? flag + 2 : flag;
+    const size_t words = (reuse_a || reuse_bt) ? 2 : 4;
+    if (cudaError_t e = cudaMemsetAsync(first, 0, words * sizeof(int), stream); e != cudaSuccess) return e;
+  }
   const int cols_pad = static_cast<int>(oz_rows_pad(cols, OZ_BN));
   // guard words: 0 a is cut, 1 top digit of a, 2 top digit of bt, 3 bt is cut (reset per launch); 4 the form the auto kernel took;
   // 5 / 6 highest plane of the a / bt scratch that may hold non-zero bytes (auto mode only; never reset)
   if (!reuse_a) ozaki_slice_kernel<P, T><<<rows, 256, 0, stream>>>(a, L.sa, L.ea, L.a_plane, n, L.kq, row0, rows, row0, flag, 0, 1, with_guard ? 5 : -1);
-  ozaki_slice_kernel<P, T><<<cols_pad, 256, 0, stream>>>(bt, L.sb, L.eb, L.b_plane, n, L.kq, col0, cols, 0, flag, 3, 2, with_guard ? 6 : -1);
+  if (!reuse_bt) ozaki_slice_kernel<P, T><<<cols_pad, 256, 0, stream>>>(bt, L.sb, L.eb, L.b_plane, n, L.kq, col0, cols, 0, flag, 3, 2, with_guard ? 6 : -1);
   return cudaGetLastError();
 }
 
@@ -1213,12 +1166,25 @@ size_t matmul_ozaki_scratch_bytes(int n) {
 // value rounded once, added by a FLOAT32 TMA reduction).  *guard_out receives the guard; the caller enqueues the split-TF32 path
 // under ozaki_pick_form_f32(...) == 0.
 cudaError_t launch_matmul_ozaki_f32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                    cudaStream_t stream, int** guard_out, bool reuse_a) {
+                                    cudaStream_t stream, int** guard_out, bool reuse_a, bool reuse_bt) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr || guard_out == nullptr || n % 4 != 0) return cudaErrorInvalidValue;
   *guard_out = OzLayout(scratch, n, 7).guard;
-  if (cudaError_t e = oz_slices<7, float>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a); e != cudaSuccess) return e;
+  if (cudaError_t e = oz_slices<7, float>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a, reuse_bt); e != cudaSuccess) return e;
   return oz_persist_contract<float>(c, scratch, 7, 0, n, row0, rows, col0, cols, stream);
+}
+
+OzOperand matmul_ozaki_operand(void* scratch, int n, int which) {
+  const OzLayout L(scratch, n, 7);
+  OzOperand o;
+  o.kq = L.kq;
+  o.guard = L.guard;
+  if (which == 0) {
+    o.planes = L.sa; o.plane = L.a_plane; o.exps = L.ea; o.lossy_slot = 0; o.top_slot = 1; o.dirty_slot = 5;
+  } else {
+    o.planes = L.sb; o.plane = L.b_plane; o.exps = L.eb; o.lossy_slot = 3; o.top_slot = 2; o.dirty_slot = 6;
+  }
+  return o;
 }
 
 int* matmul_ozaki_form_word(void* scratch, int n) { return scratch == nullptr ? nullptr : OzLayout(scratch, n, 7).guard + 4; }
@@ -1233,8 +1199,8 @@ cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, vo
     // auto mode: 7 digit planes and the guard once, then ONE persistent launch that reads the guard and runs the cheapest
     // error-free form (2 .. 7 slices) or nothing; the caller adds the FP64-pipe kernel under the remaining condition
     *guard_out = OzLayout(scratch, n, 7).guard;
-    if (!(reuse_a && reuse_bt))  // both reused: the digit planes and the guard stand as the previous launch left them
-      if (cudaError_t e = oz_slices<7>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a); e != cudaSuccess) return e;
+    if (!(reuse_a && reuse_bt))  // both reused: the digit planes and the guard stand as their producers left them
+      if (cudaError_t e = oz_slices<7>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a, reuse_bt); e != cudaSuccess) return e;
     if (!legacy) return oz_persist_contract(c, scratch, 7, 0, n, row0, rows, col0, cols, stream);
     if (cudaError_t e = oz_contract<6, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true); e != cudaSuccess) return e;
     return oz_contract<7, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true);

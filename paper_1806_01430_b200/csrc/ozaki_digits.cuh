@@ -1,0 +1,105 @@
+// ozaki_digits.cuh -- the digit encoding of matmul_ozaki.cu as a device function, so that the kernels which PRODUCE an operand of
+// gene 8 (the init-a fill, the transpose) can write its int8 digit planes while the values are still in registers, instead of a
+// separate slice pass reading the operand back from HBM (the slice pass stays for operands that arrive any other way).
+//
+// Encoding (matmul_ozaki.cu header): row r of an operand is scaled by 2^-e_r, e_r = ilogb(max_k |x_rk|) + 1, and cut into signed
+// 7-bit digits d_1 .. d_S, x = 2^e (d_1 2^-6 + d_2 2^-13 + ...) + remainder, every step exact in FP64.  Plane t of row r lives
+// at planes + t * plane + r * kq.  The guard words record whether any element has bits below its 7th digit (or is not finite)
+// and the highest non-zero digit of each operand; the contraction kernel picks its form from them (ozaki_pick_form).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace mmx {
+
+constexpr int kOzNonFinite = 0x7fffffff;  // row exponent of a row that holds an Inf or a NaN: its products are NaN
+
+#ifdef __CUDACC__
+
+__device__ __forceinline__ double oz_pow2(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
+
+// exponent of a row whose largest magnitude is m (bad: the row holds a non-finite value): |x| < 2^e for every element
+__device__ __forceinline__ int oz_row_exponent(double m, bool bad) { return (m > 0.0 && !bad) ? ilogb(m) + 1 : 0; }
+
+// 2^-e as the exact scale factor; 0 for rows that get zero digits (non-finite rows, and rows whose maximum is below 2^-970, where
+// 1 / 2^e would overflow: both are flagged as lossy by the caller through `tiny` / `bad`)
+__device__ __forceinline__ double oz_row_scale(int e, bool live, bool bad, bool* tiny) {
+  *tiny = e < -970;
+  return (live && !bad && !*tiny) ? scalbn(1.0, -e) : 0.0;
+}
+
+// The digits of W (2 or 4) consecutive elements v[0..W) of one row, starting at column k0 (a multiple of W), packed W to a store.
+// `inv` = oz_row_scale of the row; `dirty` = guard[dirty_slot]: planes beyond it hold only zeros (auto mode keeps its scratch that
+// way), so zero digits need not be written there -- short operands move 2 planes per element instead of S.  `lossy` / `top`
+// accumulate per thread: anything below the last digit? highest non-zero digit (1-based) seen.
+template <int S, int W>
+__device__ __forceinline__ void oz_emit(const double (&v)[W], double inv, bool bad, int dirty, signed char* __restrict__ drow, size_t plane, int k0,
+                                        int& lossy, int& top) {
+  static_assert(W == 2 || W == 4, "digits are packed two or four to a store");
+  int dig[S] = {};
+  int levels = S;  // digit levels walked: the planes beyond hold zeros for these elements
+  double rem[W];
+#pragma unroll
+  for (int q = 0; q < W; ++q) rem[q] = bad ? 0.0 : v[q] * inv;
+#pragma unroll
+  for (int t = 0; t < S; ++t) {
+    // W elements per digit level, branch-free (a zero remainder yields a zero digit); one test per level ends the walk
+    // once nothing is left -- short operands finish after a digit or two
+    bool none = t >= 1;
+#pragma unroll
+    for (int q = 0; q < W; ++q) none = none && rem[q] == 0.0;
+    if (none) {
+      levels = t;
+      break;
+    }
+    const double up = oz_pow2(7 * (t + 1) - 1), down = oz_pow2(-(7 * (t + 1) - 1));
+    int word = 0;
+#pragma unroll
+    for (int q = 0; q < W; ++q) {
+      // rint without the conversion units (they would bound this pass): adding 1.5 * 2^52 rounds to the integer grid
+      // (ties to even) and leaves the integer in the low word of the sum
+      const double shifted = fma(rem[q], up, 6755399441055744.0);
+      const int d = __double2loint(shifted);
+      rem[q] = fma(-(shifted - 6755399441055744.0), down, rem[q]);  // exact: removes a prefix of rem's bits
+      word |= (d & 0xff) << (8 * q);
+    }
+    dig[t] = word;
+  }
+  // bits below the last digit: the slices do not reproduce this element exactly
+#pragma unroll
+  for (int q = 0; q < W; ++q) lossy |= rem[q] != 0.0;
+  const int planes_to_write = max(levels, dirty);  // beyond: zero digits into planes that hold only zeros
+#pragma unroll
+  for (int t = 0; t < S; ++t) {
+    if (t >= planes_to_write) break;
+    if (dig[t] != 0) top = max(top, t + 1);
+    if (t < dirty || dig[t] != 0) {
+      if constexpr (W == 4) *reinterpret_cast<int*>(drow + t * plane + k0) = dig[t];
+      else *reinterpret_cast<unsigned short*>(drow + t * plane + k0) = static_cast<unsigned short>(dig[t]);
+    }
+  }
+}
+
+// End of a CTA's work on an operand: fold the threads' lossy / top into the guard words (every thread of a 256-thread CTA calls).
+// The words are read first: after a few CTAs nobody needs the atomic any more.
+__device__ __forceinline__ void oz_guard_commit(int lossy, int top, int* __restrict__ guard, int lossy_slot, int top_slot, int dirty_slot) {
+  __shared__ int oz_top_sh[8];
+  const int tid = threadIdx.x + threadIdx.y * blockDim.x;
+  lossy = __syncthreads_or(lossy);
+  top = __reduce_max_sync(0xffffffffu, top);
+  if (tid % 32 == 0) oz_top_sh[tid / 32] = top;
+  __syncthreads();
+  if (tid == 0) {
+#pragma unroll
+    for (int w = 1; w < 8; ++w) top = max(top, oz_top_sh[w]);
+    if (lossy && guard[lossy_slot] == 0) atomicOr(guard + lossy_slot, 1);
+    if (top > guard[top_slot]) atomicMax(guard + top_slot, top);
+    if (dirty_slot >= 0 && top > guard[dirty_slot]) atomicMax(guard + dirty_slot, top);
+  }
+}
+
+#endif  // __CUDACC__
+
+}  // namespace mmx

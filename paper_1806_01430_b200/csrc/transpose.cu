@@ -13,6 +13,7 @@
 // gene 7 (one row of bt per launch): row i of bt is column i of b -- a strided gather; each
 // 8-byte element costs a 32-byte sector, which is the sector amplification the catalogue notes.
 #include "kernels.cuh"
+#include "ozaki_digits.cuh"
 
 namespace mmx {
 namespace {
@@ -37,9 +38,11 @@ __device__ __forceinline__ void transpose_micro(const float4 (&in)[4], float4 (&
 // grid = (rows/64, n/64); block = 256 threads.  PUSH: the finished tile is stored into every destination
 // of `peers` (this GPU's bt and, through peer-mapped pointers, the bt of every other GPU of a row-sharded
 // run): the all-gather of bt happens inside the kernel that produces it, as NVLink stores.
-template <typename T, bool PUSH>
+// PLANES: the digit planes of bt for gene 8 (ozaki_digits.cuh) are written from the same registers as bt itself; P.exps[j] must
+// already hold the exponent of row j of bt (launch_fill_b_colexp).
+template <typename T, bool PUSH, bool PLANES = false>
 __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt, const T* __restrict__ b, int n, int first_row,
-                                                             BtPeers peers) {
+                                                             BtPeers peers, OzOperand P = OzOperand{}) {
   using VT = typename VecOf<T>::type;
   constexpr int V = VecOf<T>::V;
   constexpr int MB = kTile / V;         // micro-blocks per tile side == 16-byte chunks per tile row
@@ -69,6 +72,9 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
   __syncthreads();
 
   // phase 2: lanes along the output row (coalesced 128-bit stores)
+  int lossy = 0, top = 0;
+  int dirty = 0;
+  if constexpr (PLANES) dirty = P.guard[P.dirty_slot];
 #pragma unroll
   for (int v = tid; v < kTile * MB; v += 256) {
     const int out_row = v / MB;
@@ -80,7 +86,25 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
     } else {
       *reinterpret_cast<VT*>(bt + at) = val;
     }
+    if constexpr (PLANES) {
+      // the V elements just stored, as digits: V bytes per plane and thread, a warp covers 64 (FP64) / 128 (FP32) contiguous bytes
+      const int row = in_col0 + out_row;  // row of bt
+      bool tiny;
+      const double inv = oz_row_scale(P.exps[row], true, false, &tiny);
+      lossy |= tiny;
+      signed char* drow = P.planes + static_cast<size_t>(row) * P.kq;
+      if constexpr (V == 2) {
+        const double e2[2] = {val.x, val.y};
+        lossy |= !isfinite(val.x) | !isfinite(val.y);
+        oz_emit<7, 2>(e2, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
+      } else {
+        const double e4[4] = {static_cast<double>(val.x), static_cast<double>(val.y), static_cast<double>(val.z), static_cast<double>(val.w)};
+        lossy |= !isfinite(val.x) | !isfinite(val.y) | !isfinite(val.z) | !isfinite(val.w);
+        oz_emit<7, 4>(e4, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
+      }
+    }
   }
+  if constexpr (PLANES) oz_guard_commit(lossy, top, P.guard, P.lossy_slot, P.top_slot, P.dirty_slot);
 }
 
 // Any n: 32x32 tile, scalar accesses, +1 padding.  block = (32, 8).
@@ -135,6 +159,16 @@ cudaError_t launch_transpose(T* bt, const T* b, int n, int row0, int rows, cudaS
 }
 
 template <typename T>
+cudaError_t launch_transpose_planes(T* bt, const T* b, int n, const OzOperand& pb, cudaStream_t stream) {
+  if (!ozaki_fusable(n) || pb.kq != n) return cudaErrorInvalidValue;
+  // the guard words of bt start from zero for this encoding (the slice pass does the same before it runs)
+  if (cudaError_t e = cudaMemsetAsync(pb.guard + pb.top_slot, 0, 2 * sizeof(int), stream); e != cudaSuccess) return e;   // words 2, 3
+  dim3 grid(n / kTile, n / kTile);
+  transpose_tile_kernel<T, false, true><<<grid, 256, 0, stream>>>(bt, b, n, 0, BtPeers{}, pb);
+  return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_transpose_push(const BtPeers& peers, const T* b, int n, int row0, int rows, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   if (peers.count < 1 || peers.count > kMaxPeers) return cudaErrorInvalidValue;
@@ -157,6 +191,8 @@ cudaError_t launch_transpose_row(T* bt, const T* b, int n, IterRef iter, cudaStr
 
 template cudaError_t launch_transpose<double>(double*, const double*, int, int, int, cudaStream_t);
 template cudaError_t launch_transpose<float>(float*, const float*, int, int, int, cudaStream_t);
+template cudaError_t launch_transpose_planes<double>(double*, const double*, int, const OzOperand&, cudaStream_t);
+template cudaError_t launch_transpose_planes<float>(float*, const float*, int, const OzOperand&, cudaStream_t);
 template cudaError_t launch_transpose_push<double>(const BtPeers&, const double*, int, int, int, cudaStream_t);
 template cudaError_t launch_transpose_push<float>(const BtPeers&, const float*, int, int, int, cudaStream_t);
 template cudaError_t launch_transpose_row<double>(double*, const double*, int, IterRef, cudaStream_t);

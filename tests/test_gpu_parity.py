@@ -995,3 +995,57 @@ def test_row_sharded_in_process_on_distinct_devices(world):
             c[lo:hi] = ctx.fetch(capi.ARRAY_C, slot=r)[lo:hi]
         assert bits_equal(c, ref.c)
         _check_sharded_trace(checksum, ref, capi.F64)
+
+
+# ---- digit planes written by the kernels that produce a and bt (csrc/ozaki_digits.cuh) ----------------------------------------------------
+FUSED_GENOMES = [
+    "101010101001",   # init-a and the transpose write the planes; gene 8 runs the contraction alone
+    "001010101001",   # a comes from the host: its planes are sliced by gene 8, bt's come from the transpose
+    "100010101001",   # b comes from the host: no closed-form column exponents, the transpose does not emit; a's planes are fused
+    "101000101001",   # zero-c on the host
+    "101010001001",   # bt comes from the host
+    "011010101001",   # init-a as N row launches: they do not emit planes
+    "101001101001",   # zero-c as N row launches
+]
+
+
+@pytest.mark.parametrize("launch_batching", [1, 0])
+@pytest.mark.parametrize("dtype", [capi.F64, capi.F32])
+@pytest.mark.parametrize("n", [1024, 2048])
+def test_planes_from_the_producing_kernels_give_the_same_individuals(n, dtype, launch_batching):
+    """Whichever kernels encode the operands -- the fused producers or gene 8's own slice passes -- c is the oracle's, bit for bit, the
+    INT8 form the device picks is the same, and a second run of the same genome (CUDA-graph replay) repeats it."""
+    if dtype == capi.F64:
+        want = cpu.App(n, dtype, threads=8).run().c
+    else:  # the exact product rounded once (the CPU float program itself is further from it)
+        want = cpu.closed_form_c(n).astype(np.float32)
+    with capi.Context(n=n, dtype=dtype, launch_batching=launch_batching, timeout_s=60.0) as ctx:
+        for genome in FUSED_GENOMES:
+            for rep in range(2):
+                out = ctx.measure(genome)
+                assert out.status == capi.MEASURED, (genome, out.status)
+                assert ctx.gene8_form() == 223, (genome, ctx.gene8_form())
+                assert bits_equal(ctx.fetch(capi.ARRAY_C), want), (genome, rep)
+                assert ctx.stats().checksum == 0.0
+
+
+def test_planes_from_the_producers_track_later_writes_to_the_operands():
+    """The planes a producer wrote are dropped when the array is written any other way: an upload between the individual and a
+    single-kernel launch of gene 8 must be seen by that launch."""
+    n = 1024
+    with capi.Context(n=n) as ctx:
+        assert ctx.measure("101010101001").status == capi.MEASURED
+        a = rand(n, capi.F64, 5)
+        bt = rand(n, capi.F64, 6)
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.run_loop(4)
+        ctx.run_loop(8)
+        got = ctx.fetch(capi.ARRAY_C)
+        assert ctx.gene8_form() == 0                       # full mantissas: the FP64 pipe took it
+        want = oracle_matmul(a, bt, np.zeros((n, n)), capi.F64)
+        bound = 1e-12 * (np.abs(a) @ np.abs(bt).T)
+        assert (np.abs(got - want) <= bound).all()
+        # and back: the application's operands again, fused planes again
+        assert ctx.measure("101010101001").status == capi.MEASURED and ctx.gene8_form() == 223
+        assert bits_equal(ctx.fetch(capi.ARRAY_C), cpu.App(n, capi.F64, threads=8).run().c)
