@@ -219,7 +219,12 @@ cudaError_t prepare_train(mmx_ctx* ctx, Slot& s, int gene, long long total) {
   tr.exec = nullptr;
   tr.k = 0;
   cudaGraph_t graph = nullptr;
-  cudaError_t e = cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal);
+  // first-use work (cudaFuncSetAttribute in launch_gemv_row, lazy module load) must not happen inside a capture: one plain launch
+  // of iteration 0 first -- harmless, every run re-initialises its arrays before the train runs
+  cudaError_t e = launch_gene_any(ctx, s, gene, IterRef{nullptr, 0});
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s.stream);
+  if (e != cudaSuccess) return e;
+  e = cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal);
   if (e != cudaSuccess) return e;
   for (int q = 0; q < k && e == cudaSuccess; ++q) e = launch_gene_any(ctx, s, gene, IterRef{s.d_iter, q});
   if (e == cudaSuccess) e = launch_advance(s.d_iter, k, s.stream);
@@ -1142,53 +1147,93 @@ MMX_API int mmx_shard_bind(mmx_ctx* ctx, int slot, int rank, int world, const mm
     if (ctx) ctx->set_error("mmx_shard_bind: need 1 <= world <= 8, 0 <= rank < world and exactly one of handles / local_slots");
     return MMX_E_INVALID;
   }
+  // validate everything that can be validated before touching the slot
+  if (local_slots != nullptr)
+    for (int r = 0; r < world; ++r)
+      if (r != rank && (!shard_slot_ok(ctx, local_slots[r]) || local_slots[r] == slot)) {
+        ctx->set_error("mmx_shard_bind: local_slots must name distinct slots of this context");
+        return MMX_E_INVALID;
+      }
   Slot& s = *ctx->slots[slot];
+  // peers' ready events live on the peers' slots: create the missing ones first, one slot lock at a time (never two at once, so
+  // concurrent binds of different slots cannot deadlock or race on a peer's events)
+  if (local_slots != nullptr)
+    for (int r = 0; r < world; ++r) {
+      if (r == rank) continue;
+      Slot& o = *ctx->slots[local_slots[r]];
+      std::lock_guard<std::mutex> go(o.mu);
+      if (o.ev_ready == nullptr) {
+        MMX_CUDA(ctx, cudaSetDevice(o.device));
+        if (int rc = shard_events(ctx, o)) return rc;
+      }
+    }
   std::lock_guard<std::mutex> g(s.mu);
   MMX_CUDA(ctx, cudaSetDevice(s.device));
   if (int rc = shard_events(ctx, s)) return rc;
-  for (int r = 0; r < kMaxPeers; ++r) {  // drop an earlier binding
-    if (s.peer_ipc[r]) {
-      if (s.peer_bt[r]) cudaIpcCloseMemHandle(s.peer_bt[r]);
-      if (s.peer_ready[r]) cudaEventDestroy(s.peer_ready[r]);
-    }
-    s.peer_bt[r] = nullptr;
-    s.peer_ready[r] = nullptr;
-    s.peer_ipc[r] = false;
-  }
+  // the new peer table is built in locals and committed together with rank and world only when every entry is in place; until
+  // then the slot counts as unbound (phase1 / phase2 refuse to run), never as half bound
+  void* new_bt[kMaxPeers] = {};
+  cudaEvent_t new_ready[kMaxPeers] = {};
+  bool new_ipc[kMaxPeers] = {};
+  auto undo = [&]() {
+    for (int r = 0; r < kMaxPeers; ++r)
+      if (new_ipc[r]) {
+        if (new_bt[r]) cudaIpcCloseMemHandle(new_bt[r]);
+        if (new_ready[r]) cudaEventDestroy(new_ready[r]);
+      }
+    cudaGetLastError();
+  };
   for (int r = 0; r < world; ++r) {
     if (r == rank) {
-      s.peer_bt[r] = s.d_arr[MMX_ARRAY_BT];
-      s.peer_ready[r] = s.ev_ready;
+      new_bt[r] = s.d_arr[MMX_ARRAY_BT];
+      new_ready[r] = s.ev_ready;
     } else if (local_slots != nullptr) {
-      if (!shard_slot_ok(ctx, local_slots[r]) || local_slots[r] == slot) return MMX_E_INVALID;
       Slot& o = *ctx->slots[local_slots[r]];
       if (o.device != s.device) {
         int can = 0;
-        MMX_CUDA(ctx, cudaDeviceCanAccessPeer(&can, s.device, o.device));
-        if (!can) {
+        cudaError_t e = cudaDeviceCanAccessPeer(&can, s.device, o.device);
+        if (e == cudaSuccess && !can) {
           ctx->set_error("mmx_shard_bind: devices " + std::to_string(s.device) + " and " + std::to_string(o.device) + " have no peer access");
+          undo();
           return MMX_E_CUDA;
         }
-        const cudaError_t e = cudaDeviceEnablePeerAccess(o.device, 0);
-        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) MMX_CUDA(ctx, e);
+        if (e == cudaSuccess) e = cudaDeviceEnablePeerAccess(o.device, 0);
+        if (e == cudaErrorPeerAccessAlreadyEnabled) e = cudaSuccess;
         cudaGetLastError();
+        if (e != cudaSuccess) {
+          ctx->set_error(std::string("mmx_shard_bind: enabling peer access: ") + cudaGetErrorString(e));
+          undo();
+          return MMX_E_CUDA;
+        }
       }
-      if (o.ev_ready == nullptr) {  // created on the owner's device
-        MMX_CUDA(ctx, cudaSetDevice(o.device));
-        if (int rc = shard_events(ctx, o)) return rc;
-        MMX_CUDA(ctx, cudaSetDevice(s.device));
-      }
-      s.peer_bt[r] = o.d_arr[MMX_ARRAY_BT];
-      s.peer_ready[r] = o.ev_ready;
+      new_bt[r] = o.d_arr[MMX_ARRAY_BT];
+      new_ready[r] = o.ev_ready;
     } else {
       cudaIpcMemHandle_t mh;
       cudaIpcEventHandle_t eh;
       std::memcpy(&mh, handles[r].mem, 64);
       std::memcpy(&eh, handles[r].event, 64);
-      MMX_CUDA(ctx, cudaIpcOpenMemHandle(&s.peer_bt[r], mh, cudaIpcMemLazyEnablePeerAccess));
-      s.peer_ipc[r] = true;
-      MMX_CUDA(ctx, cudaIpcOpenEventHandle(&s.peer_ready[r], eh));
+      cudaError_t e = cudaIpcOpenMemHandle(&new_bt[r], mh, cudaIpcMemLazyEnablePeerAccess);
+      if (e == cudaSuccess) {
+        new_ipc[r] = true;
+        e = cudaIpcOpenEventHandle(&new_ready[r], eh);
+      }
+      if (e != cudaSuccess) {
+        ctx->set_error(std::string("mmx_shard_bind: opening the handle of member ") + std::to_string(r) + ": " + cudaGetErrorString(e));
+        undo();
+        return MMX_E_CUDA;
+      }
     }
+  }
+  // commit: drop the earlier binding, install the new one
+  for (int r = 0; r < kMaxPeers; ++r) {
+    if (s.peer_ipc[r]) {
+      if (s.peer_bt[r]) cudaIpcCloseMemHandle(s.peer_bt[r]);
+      if (s.peer_ready[r]) cudaEventDestroy(s.peer_ready[r]);
+    }
+    s.peer_bt[r] = new_bt[r];
+    s.peer_ready[r] = new_ready[r];
+    s.peer_ipc[r] = new_ipc[r];
   }
   s.shard_rank = rank;
   s.shard_world = world;

@@ -516,23 +516,56 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
         mbar_wait(acc_full(buf), (tile / NBUF) & 1);
         tc_fence_after();
         const unsigned t0 = tmem_base + (static_cast<unsigned>(q * 32) << 16) + buf * (LV * BN);
-#pragma unroll 1
-        for (int j = grp; j < NCH; j += 2, ++sent) {
-          unsigned lv[LV][16];
+        // Phase A -- empty the accumulators: this warp's chunks (alternate 16-column chunks of its 32 rows) leave TMEM as ONE
+        // number per element, held in registers: the level sum as a 64-bit integer where LV <= 4 (|L| < 2^31 and three shifts of
+        // 7 bits: exact), the Horner sum in FP64 beyond.  Nothing else happens before the set is handed back, so the MMAs of the
+        // next tile start after ~LV x MY TMEM loads instead of after the whole epilogue (conversions, shared-memory slabs, TMA
+        // reductions, each waiting for the previous one to leave its slab: ~7 us of the 24 us a 2 x 2 tile took at N = 4096).
+        constexpr int MY = NCH / 2;                 // chunks per warp and tile
+        constexpr int LD = 8;                       // columns per TMEM load group (registers in flight: LV x LD)
+        long long acc[LV <= 4 ? MY : 1][16];
+        double hsum[LV <= 4 ? 1 : MY][16];
 #pragma unroll
-          for (int l = 0; l < LV; ++l) tc_ld16_issue(t0 + l * BN + j * 16, lv[l]);
-          tc_ld_wait();
-          if (j + 2 >= NCH) {  // this warp has read its share of the set: the MMAs of a later tile may overwrite it
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(acc_empty(buf));
+        for (int jj = 0; jj < MY; ++jj) {
+          const int j = grp + 2 * jj;
+#pragma unroll
+          for (int h = 0; h < 16 / LD; ++h) {
+            unsigned lv[LV][LD];
+#pragma unroll
+            for (int l = 0; l < LV; ++l) {
+              if constexpr (LD == 16) tc_ld16_issue(t0 + l * BN + j * 16, lv[l]);
+              else tc_ld8_issue(t0 + l * BN + j * 16 + h * 8, lv[l]);
+            }
+            tc_ld_wait();
+#pragma unroll
+            for (int e = 0; e < LD; ++e) {
+              if constexpr (LV <= 4) {
+                long long x = static_cast<int>(lv[0][e]);
+#pragma unroll
+                for (int l = 1; l < LV; ++l) x = (x << 7) + static_cast<int>(lv[l][e]);
+                acc[jj][h * LD + e] = x;
+              } else {
+                double x = static_cast<double>(static_cast<int>(lv[LV - 1][e]));
+#pragma unroll
+                for (int l = LV - 2; l >= 0; --l) x = fma(x, 0.0078125, static_cast<double>(static_cast<int>(lv[l][e])));
+                hsum[jj][h * LD + e] = x;
+              }
+            }
           }
+        }
+        // this warp has read its share of the set: the MMAs of a later tile may overwrite it
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(acc_empty(buf));
+        // Phase B -- scale, stage, reduce into c (overlaps the next tile's MMAs)
+#pragma unroll
+        for (int jj = 0; jj < MY; ++jj, ++sent) {
+          const int j = grp + 2 * jj;
           double v[16];
           if constexpr (LV <= 4) {
-            // the level sum as ONE integer (|L| < 2^31 and three shifts of 7 bits: exact in 64 bits and in a double), scaled by
-            // adding to the exponent field: one FP64-pipe operation per element (the conversion) instead of seven.  Whether the
-            // 16 columns of the chunk all have moderate exponents is decided once (the same for every lane), so the common case
-            // is a branch-free loop the scheduler can interleave across elements.
+            // scaled by adding to the exponent field: one FP64-pipe operation per element (the conversion) instead of seven.
+            // Whether the 16 columns of the chunk all have moderate exponents is decided once (the same for every lane), so the
+            // common case is a branch-free loop the scheduler can interleave across elements.
             int ebv[16];
             bool cols_fast = true;
 #pragma unroll
@@ -544,30 +577,18 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
               const int e_row = ei - 12 - 7 * (LV - 1);
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
-                long long acc = static_cast<int>(lv[0][e]);
-#pragma unroll
-                for (int l = 1; l < LV; ++l) acc = (acc << 7) + static_cast<int>(lv[l][e]);
-                const double d = static_cast<double>(acc);
-                const int hi = __double2hiint(d) + (acc != 0 ? (e_row + ebv[e]) * (1 << 20) : 0);  // stays a normal number
+                const long long x = acc[jj][e];
+                const double d = static_cast<double>(x);
+                const int hi = __double2hiint(d) + (x != 0 ? (e_row + ebv[e]) * (1 << 20) : 0);  // stays a normal number
                 v[e] = __hiloint2double(hi, __double2loint(d));
               }
             } else {
-#pragma unroll  // (a rolled loop would index lv and v dynamically and push them to local memory for both branches)
-              for (int e = 0; e < 16; ++e) {
-                long long acc = static_cast<int>(lv[0][e]);
-#pragma unroll
-                for (int l = 1; l < LV; ++l) acc = (acc << 7) + static_cast<int>(lv[l][e]);
-                v[e] = scaled(static_cast<double>(acc) * pow2(-7 * (LV - 1)), ei, ebv[e]);
-              }
+#pragma unroll  // (a rolled loop would index acc and v dynamically and push them to local memory for both branches)
+              for (int e = 0; e < 16; ++e) v[e] = scaled(static_cast<double>(acc[jj][e]) * pow2(-7 * (LV - 1)), ei, ebv[e]);
             }
           } else {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              double sum = static_cast<double>(static_cast<int>(lv[LV - 1][e]));
-#pragma unroll
-              for (int l = LV - 2; l >= 0; --l) sum = fma(sum, 0.0078125, static_cast<double>(static_cast<int>(lv[l][e])));
-              v[e] = scaled_fast(sum, ei, pa, row_fast, eb[j * 16 + e], pb[j * 16 + e]);
-            }
+            for (int e = 0; e < 16; ++e) v[e] = scaled_fast(hsum[jj][e], ei, pa, row_fast, eb[j * 16 + e], pb[j * 16 + e]);
           }
           const unsigned slab = slab0 + (sent % CR) * (8 * Sh::C_SLAB);
           if (lane == 0) tma_store_wait_read<CR - 1>();  // the reduction that last used this slab has left shared memory

@@ -109,6 +109,9 @@ class MultiGpuEvaluator : public Evaluator {
   static double predicted_cost(const Genome& genome, const CudaBackendConfig& config);
 
  private:
+  // the public constructor releases the backend FIRST and delegates here, so that exactly one owner exists while the base is built
+  // (if the base constructor throws -- bad_alloc, an unreadable cache file -- its argument deletes the backend once)
+  MultiGpuEvaluator(CudaBackend* adopted, std::filesystem::path cache_file);
   CudaBackend* cuda_;
 };
 

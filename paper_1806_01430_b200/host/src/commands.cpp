@@ -2,7 +2,10 @@
 #include "mmxhost/commands.hpp"
 
 #include <algorithm>
+#include <cerrno>
+#include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <filesystem>
 #include <fstream>
 #include <memory>
@@ -169,29 +172,47 @@ struct CsvRow {
   std::string best_genome;
 };
 
+// C-library number parsing with the acceptance rules of std::stoi / std::stod (leading blanks, signs; the whole cell must be
+// consumed; out-of-range values are refused), without exceptions
+bool cell_to_double(const std::string& cell, double& value) {
+  if (cell.empty()) return false;
+  errno = 0;
+  char* stop = nullptr;
+  value = std::strtod(cell.c_str(), &stop);
+  return stop == cell.c_str() + cell.size() && errno != ERANGE;
+}
+
+bool cell_to_int(const std::string& cell, int& value) {
+  if (cell.empty()) return false;
+  errno = 0;
+  char* stop = nullptr;
+  const long wide = std::strtol(cell.c_str(), &stop, 10);
+  if (stop != cell.c_str() + cell.size() || errno == ERANGE || wide < INT_MIN || wide > INT_MAX) return false;
+  value = static_cast<int>(wide);
+  return true;
+}
+
+// One data row of generations.csv: generation,best_time_s,best_speedup,best_genome,mean_fitness,distinct_evals,cache_hits.  The report
+// needs the first four columns; a row with any other number of cells, or a genome cell that is not a bit string, is malformed.
 bool parse_csv_row(const std::string& line, CsvRow& row) {
-  std::vector<std::string> fields;
-  std::string::size_type start = 0;
-  for (;;) {
-    const auto comma = line.find(',', start);
-    fields.push_back(line.substr(start, comma == std::string::npos ? comma : comma - start));
-    if (comma == std::string::npos) break;
-    start = comma + 1;
+  constexpr int kColumns = 7;
+  std::string cell[kColumns];
+  int filled = 0;
+  std::istringstream cells(line);
+  for (std::string piece; std::getline(cells, piece, ',');) {
+    if (filled == kColumns) return false;
+    cell[filled++] = std::move(piece);
   }
-  if (fields.size() != 7) return false;
-  try {
-    std::size_t used = 0;
-    row.generation = std::stoi(fields[0], &used);
-    if (used != fields[0].size()) return false;
-    row.best_time_s = std::stod(fields[1], &used);
-    if (used != fields[1].size()) return false;
-    row.best_speedup = std::stod(fields[2], &used);
-    if (used != fields[2].size()) return false;
-  } catch (const std::exception&) {
-    return false;
+  if (!line.empty() && line.back() == ',') {  // getline drops a trailing empty cell
+    if (filled == kColumns) return false;
+    ++filled;
   }
-  row.best_genome = fields[3];
-  return !row.best_genome.empty() && row.best_genome.find_first_not_of("01") == std::string::npos;
+  if (filled != kColumns) return false;
+  if (!cell_to_int(cell[0], row.generation) || !cell_to_double(cell[1], row.best_time_s) || !cell_to_double(cell[2], row.best_speedup)) return false;
+  const bool bits_only = std::all_of(cell[3].begin(), cell[3].end(), [](char ch) { return ch == '0' || ch == '1'; });
+  if (cell[3].empty() || !bits_only) return false;
+  row.best_genome = cell[3];
+  return true;
 }
 
 }  // namespace

@@ -169,8 +169,10 @@ EvalCounters Evaluator::counters() const {
 }
 
 MultiGpuEvaluator::MultiGpuEvaluator(std::unique_ptr<CudaBackend> backend, std::filesystem::path cache_file)
-    : Evaluator(std::unique_ptr<EvalBackend>(backend.get()), backend->num_slots(), std::move(cache_file)),
-      cuda_(backend.release()) {
+    : MultiGpuEvaluator(backend.release(), std::move(cache_file)) {}
+
+MultiGpuEvaluator::MultiGpuEvaluator(CudaBackend* adopted, std::filesystem::path cache_file)
+    : Evaluator(std::unique_ptr<EvalBackend>(adopted), adopted->num_slots(), std::move(cache_file)), cuda_(adopted) {
   const CudaBackendConfig config = cuda_->config();
   set_cost_hint([config](const Genome& g) { return predicted_cost(g, config); });
 }
