@@ -223,6 +223,10 @@ MMX_API int mmx_last_stats(mmx_ctx* ctx, int slot, mmx_run_stats* out);
  * valid) into `host` (n*n elements of the context dtype). */
 MMX_API int mmx_fetch_array(mmx_ctx* ctx, int slot, int array, void* host, size_t bytes);
 
+/* The same for a block of rows [row0, row0 + rows) only (`host` receives rows * n elements): parity checks at sizes where the
+ * whole array is gigabytes (N = 32768: 8 GiB) compare sampled row blocks against the closed form. */
+MMX_API int mmx_fetch_rows(mmx_ctx* ctx, int slot, int array, int row0, int rows, void* host, size_t bytes);
+
 /* ---- single kernels: parity tests and roofline measurement ----------------------- */
 
 /* Put host data into a slot's device array (marks it device-valid). */

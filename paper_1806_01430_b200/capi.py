@@ -108,6 +108,7 @@ _SIGNATURES = {
     "mmx_measure_batch": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_size_t, C.POINTER(Outcome)]),
     "mmx_last_stats": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(RunStats)]),
     "mmx_fetch_array": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t]),
+    "mmx_fetch_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_size_t]),
     "mmx_upload_array": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_size_t]),
     "mmx_run_loop": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
     "mmx_run_loop_rows": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_double)]),
@@ -272,6 +273,11 @@ class Context:
     def fetch(self, array: int, slot: int = 0) -> np.ndarray:
         out = np.empty((self.n, self.n), dtype=self.np_dtype)
         self._check(self._lib.mmx_fetch_array(self._h, slot, array, out.ctypes.data, out.nbytes))
+        return out
+
+    def fetch_rows(self, array: int, row0: int, rows: int, slot: int = 0) -> np.ndarray:
+        out = np.empty((rows, self.n), dtype=self.np_dtype)
+        self._check(self._lib.mmx_fetch_rows(self._h, slot, array, row0, rows, out.ctypes.data, out.nbytes))
         return out
 
     def upload(self, array: int, data: np.ndarray, slot: int = 0):

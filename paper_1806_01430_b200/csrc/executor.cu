@@ -40,6 +40,9 @@ struct Train {  // a captured train of K inner-loop launches + the counter bump
 struct Slot {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t cur = nullptr;       // the stream launch_gene enqueues on: `stream`, or a side lane while a forked graph is captured
+  cudaStream_t lane[2] = {};        // side lanes of the whole-individual graph (init-a, zero-c beside init-b -> transpose)
+  cudaEvent_t ev_fork = nullptr, ev_join[2] = {};
   cudaEvent_t ev_begin = nullptr, ev_end = nullptr;
   void* d_arr[MMX_NUM_ARRAYS] = {};
   void* h_arr[MMX_NUM_ARRAYS] = {};  // pinned, allocated on first need
@@ -138,32 +141,32 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
     case 0:
       s.planes_a_valid = false;
       if (fuse) {
-        const cudaError_t e = launch_fill_a_planes<T>(a, n, matmul_ozaki_operand(s.oz_planes, n, 0), s.stream);
+        const cudaError_t e = launch_fill_a_planes<T>(a, n, matmul_ozaki_operand(s.oz_planes, n, 0), s.cur);
         s.planes_a_valid = e == cudaSuccess;
         return e;
       }
-      return launch_fill2d<T>(FILL_INIT_A, a, n, row0, rows, s.stream);
-    case 1: s.planes_a_valid = false; return launch_fill_row<T>(FILL_INIT_A, a, n, iter, s.stream);
+      return launch_fill2d<T>(FILL_INIT_A, a, n, row0, rows, s.cur);
+    case 1: s.planes_a_valid = false; return launch_fill_row<T>(FILL_INIT_A, a, n, iter, s.cur);
     case 2:
       s.b_colexp_valid = false;
       if (fuse) {
-        const cudaError_t e = launch_fill_b_colexp<T>(b, n, matmul_ozaki_operand(s.oz_planes, n, 1).exps, s.stream);
+        const cudaError_t e = launch_fill_b_colexp<T>(b, n, matmul_ozaki_operand(s.oz_planes, n, 1).exps, s.cur);
         s.b_colexp_valid = e == cudaSuccess;
         return e;
       }
-      return launch_fill2d<T>(FILL_INIT_B, b, n, row0, rows, s.stream);
-    case 3: s.b_colexp_valid = false; return launch_fill_row<T>(FILL_INIT_B, b, n, iter, s.stream);
-    case 4: return launch_fill2d<T>(FILL_ZERO, c, n, row0, rows, s.stream);
-    case 5: return launch_fill_row<T>(FILL_ZERO, c, n, iter, s.stream);
+      return launch_fill2d<T>(FILL_INIT_B, b, n, row0, rows, s.cur);
+    case 3: s.b_colexp_valid = false; return launch_fill_row<T>(FILL_INIT_B, b, n, iter, s.cur);
+    case 4: return launch_fill2d<T>(FILL_ZERO, c, n, row0, rows, s.cur);
+    case 5: return launch_fill_row<T>(FILL_ZERO, c, n, iter, s.cur);
     case 6:
       s.planes_bt_valid = false;
       if (fuse && s.b_colexp_valid) {
-        const cudaError_t e = launch_transpose_planes<T>(bt, b, n, matmul_ozaki_operand(s.oz_planes, n, 1), s.stream);
+        const cudaError_t e = launch_transpose_planes<T>(bt, b, n, matmul_ozaki_operand(s.oz_planes, n, 1), s.cur);
         s.planes_bt_valid = e == cudaSuccess;
         return e;
       }
-      return launch_transpose<T>(bt, b, n, row0, rows, s.stream);
-    case 7: s.planes_bt_valid = false; return launch_transpose_row<T>(bt, b, n, iter, s.stream);
+      return launch_transpose<T>(bt, b, n, row0, rows, s.cur);
+    case 7: s.planes_bt_valid = false; return launch_transpose_row<T>(bt, b, n, iter, s.cur);
     case 8: {
       int variant = ctx->cfg.matmul_variant;  // 0 = auto (matmul.cu)
       if (variant == 0 && row0 == 0 && rows == n && s.oz_planes != nullptr) {
@@ -176,11 +179,11 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
       // one consumer per encoding: the next launch of gene 8 encodes again unless a producer has rewritten the planes by then
       // (mmx_time_loop(8) therefore times the whole nest, slice passes included, whatever ran before)
       s.planes_a_valid = s.planes_bt_valid = false;
-      return launch_matmul<T>(c, a, bt, n, row0, rows, 0, n, strict, variant, s.d_scratch, s.stream);
+      return launch_matmul<T>(c, a, bt, n, row0, rows, 0, n, strict, variant, s.d_scratch, s.cur);
     }
-    case 9: return launch_gemv_row<T>(c, a, bt, n, iter, strict, s.stream);
-    case 10: return launch_dot<T>(c, a, bt, n, iter, strict, s.stream);
-    case 11: return launch_trace<T>(static_cast<T*>(s.d_sum), c, n, row0, rows, strict, s.stream);
+    case 9: return launch_gemv_row<T>(c, a, bt, n, iter, strict, s.cur);
+    case 10: return launch_dot<T>(c, a, bt, n, iter, strict, s.cur);
+    case 11: return launch_trace<T>(static_cast<T*>(s.d_sum), c, n, row0, rows, strict, s.cur);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -351,11 +354,45 @@ cudaError_t prepare_plan_graph(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan,
   begin_sequence(s, one_launch);
   if ((e = cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
   const std::size_t esz = elem_size(ctx->cfg.dtype);
+  // The program's data flow leaves three independent chains in front of the matmul nest: init-a, init-b -> transpose, zero-c
+  // (derive_dataflow finds the same edges in the source).  In the graph they are three branches: init-a and zero-c
+  // run on side lanes beside the longest chain and join before the contraction, so the issue-bound producers (the fill and the
+  // transpose that also emit digit planes) overlap the bandwidth-bound ones.  MMX_GRAPH_FORK=0 keeps one chain (A/B runs).
+  static const bool fork_enabled = [] { const char* v = getenv("MMX_GRAPH_FORK"); return v == nullptr || atoi(v) != 0; }();
+  const bool fork = fork_enabled;
+  bool forked = false, joined = false;
   for (int si = 0; si < plan.num_steps && e == cudaSuccess; ++si) {
     const mmx_plan_step& st = plan.steps[si];
-    if (st.kind == MMX_STEP_GPU) e = launch_gene_any(ctx, s, gene_of(st.nest, st.mode), IterRef{nullptr, 0});
-    else e = cudaMemcpyAsync(s.h_sum, s.d_sum, esz, cudaMemcpyDeviceToHost, s.stream);
+    if (st.kind != MMX_STEP_GPU) {
+      e = cudaMemcpyAsync(s.h_sum, s.d_sum, esz, cudaMemcpyDeviceToHost, s.stream);
+      continue;
+    }
+    if (fork && !forked) {
+      e = cudaEventRecord(s.ev_fork, s.stream);
+      for (int q = 0; q < 2 && e == cudaSuccess; ++q) e = cudaStreamWaitEvent(s.lane[q], s.ev_fork, 0);
+      forked = true;
+      if (e != cudaSuccess) break;
+    }
+    if (fork && !joined && (st.nest == MMX_NEST_MATMUL || st.nest == MMX_NEST_TRACE)) {
+      for (int q = 0; q < 2 && e == cudaSuccess; ++q) {
+        e = cudaEventRecord(s.ev_join[q], s.lane[q]);
+        if (e == cudaSuccess) e = cudaStreamWaitEvent(s.stream, s.ev_join[q], 0);
+      }
+      joined = true;
+      if (e != cudaSuccess) break;
+    }
+    if (fork && !joined && st.nest == MMX_NEST_INIT_A) s.cur = s.lane[0];
+    if (fork && !joined && st.nest == MMX_NEST_ZERO_C) s.cur = s.lane[1];
+    e = launch_gene_any(ctx, s, gene_of(st.nest, st.mode), IterRef{nullptr, 0});
+    s.cur = s.stream;
   }
+  if (forked && !joined) {  // (a device-only plan always has the matmul nest; kept for safety: every lane must rejoin the origin stream)
+    for (int q = 0; q < 2; ++q) {
+      cudaEventRecord(s.ev_join[q], s.lane[q]);
+      cudaStreamWaitEvent(s.stream, s.ev_join[q], 0);
+    }
+  }
+  s.cur = s.stream;
   const cudaError_t e2 = cudaStreamEndCapture(s.stream, &graph);
   if (e == cudaSuccess) e = e2;
   Slot::PlanGraph pg;
@@ -595,6 +632,11 @@ void destroy_slot(Slot& s) {
     }
   for (cudaEvent_t e : {s.ev_ready, s.ev_x0, s.ev_x1, s.ev_m0, s.ev_m1})
     if (e) cudaEventDestroy(e);
+  for (int q = 0; q < 2; ++q) {
+    if (s.ev_join[q]) cudaEventDestroy(s.ev_join[q]);
+    if (s.lane[q]) cudaStreamDestroy(s.lane[q]);
+  }
+  if (s.ev_fork) cudaEventDestroy(s.ev_fork);
   if (s.stream) cudaStreamDestroy(s.stream);
 }
 
@@ -693,6 +735,12 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
     cudaError_t e;
     if ((e = cudaSetDevice(sl.device)) != cudaSuccess) return fail(e, "cudaSetDevice");
     if ((e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "cudaStreamCreate");
+    sl.cur = sl.stream;
+    for (int q = 0; q < 2; ++q) {
+      if ((e = cudaStreamCreateWithFlags(&sl.lane[q], cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "cudaStreamCreate");
+      if ((e = cudaEventCreateWithFlags(&sl.ev_join[q], cudaEventDisableTiming)) != cudaSuccess) return fail(e, "cudaEventCreate");
+    }
+    if ((e = cudaEventCreateWithFlags(&sl.ev_fork, cudaEventDisableTiming)) != cudaSuccess) return fail(e, "cudaEventCreate");
     if ((e = cudaEventCreate(&sl.ev_begin)) != cudaSuccess) return fail(e, "cudaEventCreate");
     if ((e = cudaEventCreate(&sl.ev_end)) != cudaSuccess) return fail(e, "cudaEventCreate");
     for (int q = 0; q < MMX_NUM_ARRAYS; ++q)
@@ -822,6 +870,31 @@ MMX_API int mmx_fetch_array(mmx_ctx* ctx, int slot, int array, void* host, size_
     return MMX_OK;
   }
   ctx->set_error("mmx_fetch_array: array is not valid on either side");
+  return MMX_E_STATE;
+}
+
+MMX_API int mmx_fetch_rows(mmx_ctx* ctx, int slot, int array, int row0, int rows, void* host, size_t bytes) {
+  if (ctx == nullptr || host == nullptr || slot < 0 || slot >= static_cast<int>(ctx->slots.size()) || array < 0 || array >= MMX_NUM_ARRAYS)
+    return MMX_E_INVALID;
+  const std::size_t row_bytes = static_cast<std::size_t>(ctx->cfg.n) * elem_size(ctx->cfg.dtype);
+  if (row0 < 0 || rows < 0 || row0 + rows > ctx->cfg.n || bytes != row_bytes * static_cast<std::size_t>(rows)) {
+    ctx->set_error("mmx_fetch_rows: row block outside the array or size mismatch");
+    return MMX_E_INVALID;
+  }
+  Slot& s = *ctx->slots[slot];
+  std::lock_guard<std::mutex> g(s.mu);
+  MMX_CUDA(ctx, cudaSetDevice(s.device));
+  const std::size_t offset = row_bytes * static_cast<std::size_t>(row0);
+  if (s.dev_valid[array]) {
+    MMX_CUDA(ctx, cudaMemcpyAsync(host, static_cast<const char*>(s.d_arr[array]) + offset, bytes, cudaMemcpyDeviceToHost, s.stream));
+    MMX_CUDA(ctx, cudaStreamSynchronize(s.stream));
+    return MMX_OK;
+  }
+  if (s.host_valid[array] && s.h_arr[array] != nullptr && !(array == MMX_ARRAY_C && s.host_diag_only)) {
+    std::memcpy(host, static_cast<const char*>(s.h_arr[array]) + offset, bytes);
+    return MMX_OK;
+  }
+  ctx->set_error("mmx_fetch_rows: array is not valid on either side");
   return MMX_E_STATE;
 }
 

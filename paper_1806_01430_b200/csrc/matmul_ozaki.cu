@@ -315,6 +315,7 @@ struct OzPArgs {
   const int *exp_a, *exp_b;
   int n, kq, row0, rows, col0, cols, group;
   long long group_l2_bytes;  // budget for a raster group's rows of a (0: default; MMX_OZ_GROUP_MB overrides -- tuning hook)
+  int debug;  // MMX_OZ_DEBUG (rate probes, results are WRONG): 1 the producer signals stages without loading them, 2 the epilogue drops phase B
 };
 
 // sum * 2^(ea + eb - 12).  Fast path (both exponents moderate): two multiplications by exact powers of two, pa = 2^(ea - 12)
@@ -406,8 +407,20 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
           const int s = it % STAGES;
           mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
           const unsigned st = base + s * Sh::STAGE_BYTES;
+          if ((g.debug & 1) && it >= STAGES) {  // rate probe: the MMAs run on whatever the stage buffers hold
+            mbar_arrive(full_bar(s));
+            continue;
+          }
           mbar_expect_tx(full_bar(s), Sh::STAGE_BYTES);
           if constexpr (C == 1) {
+            if (g.debug & 128) {
+              const unsigned long long keep = l2_policy_evict_last();
+#pragma unroll
+              for (int t = 0; t < SA; ++t) tma_load_3d_hint(st + t * Sh::A_SLICE, map_a, kb * BK, m_base, t, full_bar(s), keep);
+#pragma unroll
+              for (int t = 0; t < SB; ++t) tma_load_3d_hint(st + Sh::A_BYTES + t * Sh::B_SLICE, map_b, kb * BK, n_rel, t, full_bar(s), keep);
+              continue;
+            }
 #pragma unroll
             for (int t = 0; t < SA; ++t) tma_load_3d(st + t * Sh::A_SLICE, map_a, kb * BK, m_base, t, full_bar(s));
 #pragma unroll
@@ -558,6 +571,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
         __syncwarp();
         if (lane == 0) mbar_arrive(acc_empty(buf));
         // Phase B -- scale, stage, reduce into c (overlaps the next tile's MMAs)
+        if (g.debug & 2) continue;
 #pragma unroll
         for (int jj = 0; jj < MY; ++jj, ++sent) {
           const int j = grp + 2 * jj;
@@ -591,6 +605,13 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
             for (int e = 0; e < 16; ++e) v[e] = scaled_fast(hsum[jj][e], ei, pa, row_fast, eb[j * 16 + e], pb[j * 16 + e]);
           }
           const unsigned slab = slab0 + (sent % CR) * (8 * Sh::C_SLAB);
+          if (g.debug & 16) {  // rate probe: conversions only
+            double keep = 0.0;
+#pragma unroll
+            for (int e = 0; e < 16; ++e) keep += v[e];
+            if (keep == 1.2345e300) *reinterpret_cast<volatile double*>(smem_raw) = keep;
+            continue;
+          }
           if (lane == 0) tma_store_wait_read<CR - 1>();  // the reduction that last used this slab has left shared memory
           __syncwarp();
           if constexpr (sizeof(CT) == 8) {
@@ -607,10 +628,53 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
                            "f"(static_cast<float>(v[4 * ch + 1])), "f"(static_cast<float>(v[4 * ch + 2])), "f"(static_cast<float>(v[4 * ch + 3]))
                            : "memory");
           }
+          if (g.debug & (32 | 64)) {
+            // c through the load/store units: the slab is read back row-wise (8 lanes = one 128-byte row, 4 rows per instruction)
+            // and goes out as whole lines -- plain stores (bit 32: c is known to be zero) or FP64 reductions at the L2 (bit 64)
+            __syncwarp();
+            CT* cbase = static_cast<CT*>(g.c);
+            if constexpr (sizeof(CT) == 8) {
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int rr = 4 * i + (lane >> 3), pp = lane & 7;
+                double x, y;
+                asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];\n" : "=d"(x), "=d"(y) : "r"(slab + rr * 128 + ((pp ^ (rr & 7)) << 4)) : "memory");
+                const int row = m_base + q * 32 + rr, col = n_tile + j * 16 + 2 * pp;
+                if (row < m_limit && col + 2 <= g.cols) {
+                  double* at = cbase + static_cast<size_t>(row) * g.n + g.col0 + col;
+                  if (g.debug & 32) {
+                    *reinterpret_cast<double2*>(at) = make_double2(x, y);
+                  } else {
+                    asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(at), "d"(x) : "memory");
+                    asm volatile("red.global.add.f64 [%0], %1;\n" ::"l"(at + 1), "d"(y) : "memory");
+                  }
+                }
+              }
+            } else {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const int rr = 8 * i + (lane >> 2), pp = lane & 3;
+                float x0, x1, x2, x3;
+                asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];\n" : "=f"(x0), "=f"(x1), "=f"(x2), "=f"(x3) : "r"(slab + rr * 64 + ((pp ^ ((rr >> 1) & 3)) << 4)) : "memory");
+                const int row = m_base + q * 32 + rr, col = n_tile + j * 16 + 4 * pp;
+                if (row < m_limit && col + 4 <= g.cols) {
+                  float* at = reinterpret_cast<float*>(cbase) + static_cast<size_t>(row) * g.n + g.col0 + col;
+                  if (g.debug & 32) *reinterpret_cast<float4*>(at) = make_float4(x0, x1, x2, x3);
+                  else asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"l"(at), "f"(x0), "f"(x1), "f"(x2), "f"(x3) : "memory");
+                }
+              }
+            }
+            __syncwarp();  // the slab may be rewritten
+            continue;
+          }
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
-            tma_reduce_add_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
+          if (g.debug & 512) __nanosleep(jj == 0 ? 200u + 400u * (warp - 2) : 2500u);
+          if (g.debug & 1024) __nanosleep(jj == 0 ? 100u + 200u * (warp - 2) : 1200u);
+          if (lane == 0 && !(g.debug & 8)) {
+            if (g.debug & 4) tma_store_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
+            else if (g.debug & 256) tma_reduce_add_2d_hint(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32, l2_policy_evict_first());
+            else tma_reduce_add_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
             tma_store_commit();
           }
         }
@@ -1089,6 +1153,8 @@ cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, in
   g.group = raster_group(OZ_BM, static_cast<size_t>(L.kq));
   static const long long group_mb = [] { const char* e = getenv("MMX_OZ_GROUP_MB"); return e ? atoll(e) : 0ll; }();
   g.group_l2_bytes = group_mb << 20;
+  static const int debug = [] { const char* e = getenv("MMX_OZ_DEBUG"); return e ? atoi(e) : 0; }();
+  g.debug = debug;
   // the grid covers the 64-wide tiling (the forms with 128-wide tiles leave the surplus CTAs without a tile)
   const int tiles_x = (cols + 63) / 64, tiles_y = (rows + OZ_BM - 1) / OZ_BM;
   const dim3 grid(static_cast<unsigned>(std::min(tiles_x * tiles_y, oz_sm_count())));

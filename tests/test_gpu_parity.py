@@ -1049,3 +1049,28 @@ def test_planes_from_the_producers_track_later_writes_to_the_operands():
         # and back: the application's operands again, fused planes again
         assert ctx.measure("101010101001").status == capi.MEASURED and ctx.gene8_form() == 223
         assert bits_equal(ctx.fetch(capi.ARRAY_C), cpu.App(n, capi.F64, threads=8).run().c)
+
+
+@pytest.mark.timeout(600)
+def test_largest_configuration_matches_the_closed_form_on_sampled_row_blocks():
+    """N = 32768 (BASELINE config 5's top size): c is 8 GiB, so row blocks of it -- first, last, around the middle, a few in
+    between -- are fetched and compared bit for bit with the closed form (exact for N = 2^p), together with
+    the matching rows of a and bt; an all-zero c would pass a checksum test but not this one."""
+    import torch
+    n = 32768
+    free, _ = torch.cuda.mem_get_info(0)
+    if free < 60 * 2 ** 30:
+        pytest.skip("needs ~50 GiB of device memory")
+    with capi.Context(n=n, dtype=capi.F64, timeout_s=600.0) as ctx:
+        out = ctx.measure("101010101001")
+        assert out.status == capi.MEASURED and ctx.stats().checksum == 0.0
+        assert ctx.gene8_form() == 335
+        j = np.arange(n, dtype=np.float64)
+        for r0 in (0, 64, 4096 - 32, 16384 - 64, 16384, 21845, 32768 - 128, 32768 - 64):
+            rows = 64
+            got = ctx.fetch_rows(capi.ARRAY_C, r0, rows)
+            assert bits_equal(got, cpu.closed_form_c(n, r0, r0 + rows)), f"rows [{r0}, {r0 + rows}) of c"
+            assert np.abs(got).max() > 1000.0                          # not an all-zero block
+            i = np.arange(r0, r0 + rows, dtype=np.float64)[:, None]
+            assert bits_equal(ctx.fetch_rows(capi.ARRAY_A, r0, rows), (i + j[None, :]) / n)
+            assert bits_equal(ctx.fetch_rows(capi.ARRAY_BT, r0, rows), (j[None, :] - i) / n)
