@@ -633,7 +633,9 @@ def ga_block(args, n, dtype, device, rank, world, ctl, barrier):
     t_base = time.perf_counter() - t_base
     if base[0][0] != capi.MEASURED:
         return {"skipped": f"the all-CPU baseline genome could not be measured within 300 s (status {capi.STATUS_NAMES[base[0][0]]})"}
-    with capi.Context(n=n, dtype=dtype, devices=[device], timeout_s=args.ga_timeout, host_threads=team) as ctx:
+    # each rank's CPU-mapped nests run on the rank's own share of the host's CPUs (mmx_config.pin_host)
+    with capi.Context(n=n, dtype=dtype, devices=[device], timeout_s=args.ga_timeout, host_threads=team,
+                      host_core_first=(rank % max(1, cores // team)) * team, host_core_count=team) as ctx:
         ev = ShardedEvaluator(lambda g: ctx.measure(g).as_tuple(), capi.GENE_LENGTH, group=ctl, device="cpu")
         ev.preload(zero, base[0])
         barrier()

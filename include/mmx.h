@@ -115,6 +115,15 @@ typedef struct mmx_config {
                              * uncompensated form; 40 FP64 on the tcgen05 INT8 tensor cores with 7 exact 7-bit slices per operand
                              * whatever the operands (error <= 2e-14 K max|a| max|b|), 41 .. 45 the same with 6 .. 2 slices */
   int32_t warmup;           /* untimed runs per genome before the timed repetitions (default 0) */
+  /* Host-side isolation of concurrent measurements (the reference bounds the contention with `jobs`,
+   * evaluator.cpp:254-273): with pin_host != 0 (default 1) the CPUs this process may run on -- ordered so that SMT siblings are
+   * adjacent, restricted to [host_core_first, host_core_first + host_core_count) of that list when host_core_count > 0 (one
+   * process per GPU: each rank passes its own share) -- are split evenly among the slots; a measurement runs on its slot's CPUs
+   * only (the calling thread for its duration, and every thread of a CPU-mapped nest's team), so the time of a genome with
+   * CPU-mapped nests does not depend on what the other slots are running. */
+  int32_t pin_host;
+  int32_t host_core_first;
+  int32_t host_core_count;
 } mmx_config;
 
 /* EvaluationOutcome, evaluation.hpp:19-28. */
@@ -134,6 +143,9 @@ typedef struct mmx_run_stats {
   double gpu_ms;            /* last run: CUDA-event time of the whole individual          */
   double host_s;            /* last run: time spent inside CPU-mapped nests               */
   double nest_s[MMX_NUM_NESTS]; /* last run: host wall time attributed to each nest       */
+  double host_loadavg;      /* 1-minute load average of the box when the last run started */
+  int32_t host_cpus;        /* CPUs the slot is pinned to (0: not pinned)                  */
+  int32_t host_first_cpu;   /* the first of them (OS numbering), -1 when not pinned        */
 } mmx_run_stats;
 
 /* One step of a plan, as text-free data for tests and reports. */

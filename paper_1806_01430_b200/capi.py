@@ -38,6 +38,7 @@ class Config(C.Structure):
         ("timeout_s", C.c_double), ("repetitions", C.c_int32), ("num_slots", C.c_int32),
         ("devices", C.POINTER(C.c_int32)), ("host_threads", C.c_int32), ("launch_batching", C.c_int32),
         ("matmul_variant", C.c_int32), ("warmup", C.c_int32),
+        ("pin_host", C.c_int32), ("host_core_first", C.c_int32), ("host_core_count", C.c_int32),
     ]
 
 
@@ -53,6 +54,7 @@ class RunStats(C.Structure):
         ("h2d_bytes", C.c_uint64), ("d2h_bytes", C.c_uint64), ("kernel_launches", C.c_uint64),
         ("graph_launches", C.c_uint64), ("checksum", C.c_double), ("gpu_ms", C.c_double),
         ("host_s", C.c_double), ("nest_s", C.c_double * NUM_NESTS),
+        ("host_loadavg", C.c_double), ("host_cpus", C.c_int32), ("host_first_cpu", C.c_int32),
     ]
 
 
@@ -202,7 +204,8 @@ class Context:
 
     def __init__(self, n: int = 256, dtype: int = F64, numerics: int = FAST, timeout_s: float = 120.0,
                  repetitions: int = 1, num_slots: int = 1, devices=None, host_threads: int = 1,
-                 launch_batching: int = 1, matmul_variant: int = 0, warmup: int = 0):
+                 launch_batching: int = 1, matmul_variant: int = 0, warmup: int = 0, pin_host: int = 1,
+                 host_core_first: int = 0, host_core_count: int = 0):
         self._lib = load()
         cfg = Config()
         self._lib.mmx_default_config(C.byref(cfg))
@@ -210,6 +213,7 @@ class Context:
         cfg.timeout_s, cfg.repetitions, cfg.num_slots = timeout_s, repetitions, num_slots
         cfg.host_threads, cfg.launch_batching = host_threads, launch_batching
         cfg.matmul_variant, cfg.warmup = matmul_variant, warmup
+        cfg.pin_host, cfg.host_core_first, cfg.host_core_count = pin_host, host_core_first, host_core_count
         self._devices = None
         if devices is not None:
             self._devices = (C.c_int32 * len(devices))(*devices)

@@ -9,12 +9,16 @@
 // The timed region of a run starts with every array invalid on both sides (a fresh process, as
 // in the reference) and ends when the checksum is on the host; allocation happens before it
 // (the program's arrays are static storage, matmul.c:5).
+#include <pthread.h>
+#include <sched.h>
+
 #include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <fstream>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -70,6 +74,7 @@ struct Slot {
     bool planes_a = false, planes_bt = false, colexp = false;  // the flags as the captured sequence leaves them
   };
   std::map<unsigned, PlanGraph> plan_graphs;  // by genome mask: whole device-only individuals
+  std::vector<int> cpus;  // pin_host: the CPUs this slot's measurements run on (OS numbering); empty = not pinned
   mmx_run_stats stats{};
   std::mutex mu;
   // row-sharded group membership (mmx_shard_*): this slot is member `shard_rank` of `shard_world`
@@ -113,6 +118,51 @@ inline double since(Clock::time_point t0) { return Seconds(Clock::now() - t0).co
       return e__ == cudaErrorMemoryAllocation ? MMX_E_NOMEM : MMX_E_CUDA;                        \
     }                                                                                            \
   } while (0)
+
+// The CPUs this process may run on, ordered so that SMT siblings are adjacent (a slot's share is then made of whole cores
+// wherever the split allows): sorted by (lowest sibling id, own id) as sysfs reports the topology; OS order where it does not.
+std::vector<int> allowed_cpus_by_core() {
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  std::vector<int> cpus;
+  if (sched_getaffinity(0, sizeof(set), &set) != 0) return cpus;
+  std::vector<std::pair<int, int>> keyed;
+  for (int c = 0; c < CPU_SETSIZE; ++c) {
+    if (!CPU_ISSET(c, &set)) continue;
+    int first = c;
+    std::ifstream f("/sys/devices/system/cpu/cpu" + std::to_string(c) + "/topology/thread_siblings_list");
+    if (f) {
+      int v = 0;
+      if (f >> v) first = v;  // "0,8" or "0-1": the list starts with the lowest sibling
+    }
+    keyed.emplace_back(first, c);
+  }
+  std::sort(keyed.begin(), keyed.end());
+  for (const auto& kc : keyed) cpus.push_back(kc.second);
+  return cpus;
+}
+
+// Pins the calling thread to a slot's CPUs for the duration of a measurement and restores its mask afterwards.
+class ScopedAffinity {
+ public:
+  explicit ScopedAffinity(const std::vector<int>& cpus) {
+    if (cpus.empty()) return;
+    if (pthread_getaffinity_np(pthread_self(), sizeof(old_), &old_) != 0) return;
+    cpu_set_t set;
+    CPU_ZERO(&set);
+    for (int c : cpus) CPU_SET(c, &set);
+    active_ = pthread_setaffinity_np(pthread_self(), sizeof(set), &set) == 0;
+  }
+  ~ScopedAffinity() {
+    if (active_) pthread_setaffinity_np(pthread_self(), sizeof(old_), &old_);
+  }
+  ScopedAffinity(const ScopedAffinity&) = delete;
+  ScopedAffinity& operator=(const ScopedAffinity&) = delete;
+
+ private:
+  cpu_set_t old_;
+  bool active_ = false;
+};
 
 std::size_t matrix_bytes(const mmx_ctx* ctx) {
   return static_cast<std::size_t>(ctx->cfg.n) * ctx->cfg.n * elem_size(ctx->cfg.dtype);
@@ -281,7 +331,11 @@ cudaError_t run_train(mmx_ctx* ctx, Slot& s, int gene, long long total, const De
 
 template <typename T>
 bool run_host_nest(const mmx_ctx* ctx, Slot& s, int nest, const Deadline& dl, double* checksum) {
-  const int n = ctx->cfg.n, th = ctx->cfg.host_threads;
+  const int n = ctx->cfg.n;
+  HostTeam th;
+  th.threads = ctx->cfg.host_threads;
+  th.cpus = s.cpus.empty() ? nullptr : s.cpus.data();
+  th.ncpus = static_cast<int>(s.cpus.size());
   T* a = static_cast<T*>(s.h_arr[MMX_ARRAY_A]);
   T* b = static_cast<T*>(s.h_arr[MMX_ARRAY_B]);
   T* c = static_cast<T*>(s.h_arr[MMX_ARRAY_C]);
@@ -415,6 +469,12 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const 
   for (int q = 0; q < MMX_NUM_ARRAYS; ++q) s.host_valid[q] = s.dev_valid[q] = false;
   s.host_diag_only = false;
   s.stats.host_s = 0.0;
+  {
+    double load = 0.0;
+    s.stats.host_loadavg = getloadavg(&load, 1) == 1 ? load : -1.0;
+  }
+  s.stats.host_cpus = static_cast<int32_t>(s.cpus.size());
+  s.stats.host_first_cpu = s.cpus.empty() ? -1 : s.cpus.front();
   s.stats.graph_launches = 0;
   for (double& x : s.stats.nest_s) x = 0.0;
   double checksum = 0.0;
@@ -562,6 +622,7 @@ int measure_on_slot(mmx_ctx* ctx, int slot, const std::uint8_t* bits, std::size_
   }
   Slot& s = *ctx->slots[slot];
   std::lock_guard<std::mutex> guard(s.mu);
+  const ScopedAffinity pinned(s.cpus);  // the slot's own CPUs: launches, host loops and their thread team
   MMX_CUDA(ctx, cudaSetDevice(s.device));
   // allocation is outside the timed region: host mirrors for every array a step touches on the host
   for (int si = 0; si < plan.num_steps; ++si) {
@@ -682,6 +743,9 @@ MMX_API void mmx_default_config(mmx_config* cfg) {
   cfg->launch_batching = 1;
   cfg->matmul_variant = 0;
   cfg->warmup = 0;
+  cfg->pin_host = 1;
+  cfg->host_core_first = 0;
+  cfg->host_core_count = 0;  // all the CPUs the process may run on
 }
 
 MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
@@ -697,7 +761,7 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
   if (cfg->n < 1 || cfg->n > 65536 || (cfg->dtype != MMX_F64 && cfg->dtype != MMX_F32) ||
       (cfg->numerics != MMX_NUMERICS_FAST && cfg->numerics != MMX_NUMERICS_STRICT) || !(cfg->timeout_s > 0.0) ||
       cfg->repetitions < 1 || cfg->num_slots < 1 || cfg->num_slots > 64 || cfg->host_threads < 1 || cfg->warmup < 0 ||
-      cfg->matmul_variant < 0 || cfg->matmul_variant > 45) {
+      cfg->matmul_variant < 0 || cfg->matmul_variant > 45 || cfg->host_core_first < 0 || cfg->host_core_count < 0) {
     g_create_error = "invalid configuration value";
     return MMX_E_INVALID;
   }
@@ -781,6 +845,26 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
     if ((e = cudaMalloc(reinterpret_cast<void**>(&sl.d_iter), sizeof(int))) != cudaSuccess) return fail(e, "cudaMalloc(iter)");
     if ((e = cudaHostAlloc(&sl.h_sum, 16, cudaHostAllocDefault)) != cudaSuccess) return fail(e, "cudaHostAlloc(sum)");
     std::memset(sl.h_sum, 0, 16);
+  }
+  if (cfg->pin_host) {
+    // this context's share of the allowed CPUs, split evenly among its slots (whole SMT cores where the numbers allow it); with
+    // fewer CPUs than slots the slots take turns on them
+    std::vector<int> all = allowed_cpus_by_core();
+    if (cfg->host_core_count > 0 && !all.empty()) {
+      const std::size_t first = std::min<std::size_t>(static_cast<std::size_t>(cfg->host_core_first), all.size() - 1);
+      const std::size_t count = std::min<std::size_t>(static_cast<std::size_t>(cfg->host_core_count), all.size() - first);
+      all = std::vector<int>(all.begin() + static_cast<std::ptrdiff_t>(first), all.begin() + static_cast<std::ptrdiff_t>(first + count));
+    }
+    const std::size_t slots = ctx->slots.size();
+    for (std::size_t q = 0; q < slots && !all.empty(); ++q) {
+      Slot& sl = *ctx->slots[q];
+      if (all.size() >= slots) {
+        const std::size_t lo = all.size() * q / slots, hi = all.size() * (q + 1) / slots;
+        sl.cpus.assign(all.begin() + static_cast<std::ptrdiff_t>(lo), all.begin() + static_cast<std::ptrdiff_t>(hi));
+      } else {
+        sl.cpus.assign(1, all[q % all.size()]);
+      }
+    }
   }
   *out = ctx.release();
   return MMX_OK;

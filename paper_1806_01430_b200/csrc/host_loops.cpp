@@ -1,5 +1,8 @@
 #include "host_loops.hpp"
 
+#include <pthread.h>
+#include <sched.h>
+
 #include <atomic>
 #include <thread>
 #include <vector>
@@ -12,8 +15,16 @@ namespace {
 // the deadline passes.  The deadline is polled once per row (every 16 rows for cheap nests
 // would be enough, but a row is never shorter than the clock read by much at the sizes
 // where it matters).
+void pin_self(int cpu) {
+  cpu_set_t set;
+  CPU_ZERO(&set);
+  CPU_SET(cpu, &set);
+  pthread_setaffinity_np(pthread_self(), sizeof(set), &set);  // best effort: an unpinned thread is slower, not wrong
+}
+
 template <typename Body>
-bool for_rows(int n, int threads, const Deadline& dl, int poll_every, Body body) {
+bool for_rows(int n, const HostTeam& team, const Deadline& dl, int poll_every, Body body) {
+  int threads = team.threads;
   if (threads < 1) threads = 1;
   if (threads > n) threads = n;
   std::atomic<bool> expired{false};
@@ -34,7 +45,10 @@ bool for_rows(int n, int threads, const Deadline& dl, int poll_every, Body body)
     for (int t = 0; t < threads; ++t) {
       const int r0 = static_cast<int>(static_cast<long long>(n) * t / threads);
       const int r1 = static_cast<int>(static_cast<long long>(n) * (t + 1) / threads);
-      pool.emplace_back(block, r0, r1);
+      pool.emplace_back([&, t, r0, r1] {
+        if (team.cpus != nullptr && team.ncpus > 0) pin_self(team.cpus[t % team.ncpus]);
+        block(r0, r1);
+      });
     }
     for (auto& th : pool) th.join();
   }
@@ -44,40 +58,40 @@ bool for_rows(int n, int threads, const Deadline& dl, int poll_every, Body body)
 }  // namespace
 
 template <typename T>
-bool host_init_a(T* a, int n, int threads, const Deadline& dl) {
-  return for_rows(n, threads, dl, 64, [=](int i) {
+bool host_init_a(T* a, int n, const HostTeam& team, const Deadline& dl) {
+  return for_rows(n, team, dl, 64, [=](int i) {
     T* row = a + static_cast<std::size_t>(i) * n;
     for (int j = 0; j < n; ++j) row[j] = static_cast<T>(i + j) / n;  // matmul.c:10
   });
 }
 
 template <typename T>
-bool host_init_b(T* b, int n, int threads, const Deadline& dl) {
-  return for_rows(n, threads, dl, 64, [=](int i) {
+bool host_init_b(T* b, int n, const HostTeam& team, const Deadline& dl) {
+  return for_rows(n, team, dl, 64, [=](int i) {
     T* row = b + static_cast<std::size_t>(i) * n;
     for (int j = 0; j < n; ++j) row[j] = static_cast<T>(i - j) / n;  // matmul.c:14
   });
 }
 
 template <typename T>
-bool host_zero_c(T* c, int n, int threads, const Deadline& dl) {
-  return for_rows(n, threads, dl, 64, [=](int i) {
+bool host_zero_c(T* c, int n, const HostTeam& team, const Deadline& dl) {
+  return for_rows(n, team, dl, 64, [=](int i) {
     T* row = c + static_cast<std::size_t>(i) * n;
     for (int j = 0; j < n; ++j) row[j] = static_cast<T>(0.0);  // matmul.c:18
   });
 }
 
 template <typename T>
-bool host_transpose(T* bt, const T* b, int n, int threads, const Deadline& dl) {
-  return for_rows(n, threads, dl, 16, [=](int i) {
+bool host_transpose(T* bt, const T* b, int n, const HostTeam& team, const Deadline& dl) {
+  return for_rows(n, team, dl, 16, [=](int i) {
     T* row = bt + static_cast<std::size_t>(i) * n;
     for (int j = 0; j < n; ++j) row[j] = b[static_cast<std::size_t>(j) * n + i];  // matmul.c:23
   });
 }
 
 template <typename T>
-bool host_matmul(T* c, const T* a, const T* bt, int n, int threads, const Deadline& dl) {
-  return for_rows(n, threads, dl, 1, [=](int i) {
+bool host_matmul(T* c, const T* a, const T* bt, int n, const HostTeam& team, const Deadline& dl) {
+  return for_rows(n, team, dl, 1, [=](int i) {
     T* crow = c + static_cast<std::size_t>(i) * n;
     const T* arow = a + static_cast<std::size_t>(i) * n;
     for (int j = 0; j < n; ++j) {
@@ -95,11 +109,11 @@ double host_trace(const T* c, int n) {
 }
 
 #define MMX_INSTANTIATE(T)                                                           \
-  template bool host_init_a<T>(T*, int, int, const Deadline&);                      \
-  template bool host_init_b<T>(T*, int, int, const Deadline&);                      \
-  template bool host_zero_c<T>(T*, int, int, const Deadline&);                      \
-  template bool host_transpose<T>(T*, const T*, int, int, const Deadline&);         \
-  template bool host_matmul<T>(T*, const T*, const T*, int, int, const Deadline&);  \
+  template bool host_init_a<T>(T*, int, const HostTeam&, const Deadline&);                      \
+  template bool host_init_b<T>(T*, int, const HostTeam&, const Deadline&);                      \
+  template bool host_zero_c<T>(T*, int, const HostTeam&, const Deadline&);                      \
+  template bool host_transpose<T>(T*, const T*, int, const HostTeam&, const Deadline&);         \
+  template bool host_matmul<T>(T*, const T*, const T*, int, const HostTeam&, const Deadline&);  \
   template double host_trace<T>(const T*, int);
 MMX_INSTANTIATE(double)
 MMX_INSTANTIATE(float)

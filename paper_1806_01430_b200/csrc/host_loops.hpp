@@ -17,14 +17,21 @@ struct Deadline {
   bool expired() const { return Clock::now() >= at; }
 };
 
-// Each returns false when the deadline passed before the nest finished (rows are the unit
-// of the check).  `threads` > 1 splits the outer loop into contiguous row blocks; per-element
-// arithmetic is unchanged, so results do not depend on it.
-template <typename T> bool host_init_a(T* a, int n, int threads, const Deadline& dl);
-template <typename T> bool host_init_b(T* b, int n, int threads, const Deadline& dl);
-template <typename T> bool host_zero_c(T* c, int n, int threads, const Deadline& dl);
-template <typename T> bool host_transpose(T* bt, const T* b, int n, int threads, const Deadline& dl);
-template <typename T> bool host_matmul(T* c, const T* a, const T* bt, int n, int threads, const Deadline& dl);
+// The threads a CPU-mapped nest runs on: `threads` > 1 splits the outer loop into contiguous row blocks (per-element arithmetic is
+// unchanged, so results do not depend on it); with `cpus` set, thread t pins itself to cpus[t % ncpus] -- the slot's own CPUs, so
+// that concurrent measurements on other slots do not share cores with it.
+struct HostTeam {
+  int threads = 1;
+  const int* cpus = nullptr;
+  int ncpus = 0;
+};
+
+// Each returns false when the deadline passed before the nest finished (rows are the unit of the check).
+template <typename T> bool host_init_a(T* a, int n, const HostTeam& team, const Deadline& dl);
+template <typename T> bool host_init_b(T* b, int n, const HostTeam& team, const Deadline& dl);
+template <typename T> bool host_zero_c(T* c, int n, const HostTeam& team, const Deadline& dl);
+template <typename T> bool host_transpose(T* bt, const T* b, int n, const HostTeam& team, const Deadline& dl);
+template <typename T> bool host_matmul(T* c, const T* a, const T* bt, int n, const HostTeam& team, const Deadline& dl);
 // matmul.c:30-32; the accumulator has the array's type, the result is widened for printf.
 template <typename T> double host_trace(const T* c, int n);
 

@@ -107,6 +107,11 @@ struct CudaBackendConfig {
   int host_threads = 1;
   bool launch_batching = true;
   int matmul_variant = 0;
+  // every slot measures on its own share of the host's CPUs (mmx_config.pin_host); first / count restrict the
+  // context to a sub-range of the allowed CPUs (one process per GPU: each rank passes its share); count 0 = all of them
+  bool pin_host = true;
+  int host_core_first = 0;
+  int host_core_count = 0;
 };
 
 // Throws ToolchainMissing when there is no CUDA device (there is no CPU fallback), ConfigError

@@ -63,6 +63,9 @@ CudaBackend::CudaBackend(const CudaBackendConfig& config) : config_(config) {
   c.host_threads = config.host_threads;
   c.launch_batching = config.launch_batching ? 1 : 0;
   c.matmul_variant = config.matmul_variant;
+  c.pin_host = config.pin_host ? 1 : 0;
+  c.host_core_first = config.host_core_first;
+  c.host_core_count = config.host_core_count;
   const int rc = mmx_create(&c, &ctx_);
   if (rc != MMX_OK) throw_for_code(rc, std::string("mmx_create: ") + mmx_last_error(nullptr));
   busy_.assign(config.devices.size(), 0);

@@ -68,6 +68,9 @@ std::string render_resolved_config(const RunConfig& cfg) {
     }
     o.s += "\n" + std::string(static_cast<std::size_t>(o.indent), ' ') + "]";
     o.integer("matmul_variant", c.matmul_variant);
+    o.integer("pin_host", c.pin_host ? 1 : 0);
+    o.integer("host_core_first", c.host_core_first);
+    o.integer("host_core_count", c.host_core_count);
     o.close();
   } else {
     o.str("sim_model", *cfg.sim_model);

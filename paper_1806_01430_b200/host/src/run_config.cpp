@@ -127,6 +127,9 @@ CudaBackendConfig read_cuda(const Value& obj) {
   c.warmup = at_least(s.integer("warmup", c.warmup), 0, "warmup", "must not be negative");
   c.host_threads = at_least(s.integer("host_threads", c.host_threads), 1, "host_threads", "must be at least 1");
   c.matmul_variant = s.integer("matmul_variant", c.matmul_variant);
+  c.pin_host = s.integer("pin_host", c.pin_host ? 1 : 0) != 0;
+  c.host_core_first = at_least(s.integer("host_core_first", c.host_core_first), 0, "host_core_first", "must not be negative");
+  c.host_core_count = at_least(s.integer("host_core_count", c.host_core_count), 0, "host_core_count", "must not be negative");
   if (const Value* d = s.peek("devices")) {
     if (!d->is_array() || d->array->empty()) throw ConfigError("'devices' in 'cuda' must be a non-empty array of device ordinals");
     c.devices.clear();

@@ -1074,3 +1074,52 @@ def test_largest_configuration_matches_the_closed_form_on_sampled_row_blocks():
             i = np.arange(r0, r0 + rows, dtype=np.float64)[:, None]
             assert bits_equal(ctx.fetch_rows(capi.ARRAY_A, r0, rows), (i + j[None, :]) / n)
             assert bits_equal(ctx.fetch_rows(capi.ARRAY_BT, r0, rows), (j[None, :] - i) / n)
+
+
+# ---- host isolation of concurrent measurements -----------------------------------------------------------------------------
+def _physical_cores():
+    import os
+    cores = set()
+    for c in sorted(os.sched_getaffinity(0)):
+        try:
+            first = int(open(f"/sys/devices/system/cpu/cpu{c}/topology/thread_siblings_list").read().replace("-", ",").split(",")[0])
+        except (OSError, ValueError):
+            first = c
+        cores.add(first)
+    return len(cores)
+
+
+@pytest.mark.timeout(600)
+def test_a_cpu_nest_genome_is_timed_the_same_with_busy_neighbours():
+    """Every slot measures on its own CPUs (mmx_config.pin_host): a genome whose matmul nest runs on the host must get (within 10 %)
+    the same time whether the other slots are idle or all run CPU-mapped nests themselves.  The reference bounds this contention with
+    `jobs` (evaluator.cpp:254-273); here the slots are pinned to disjoint cores."""
+    slots = min(8, _physical_cores())
+    if slots < 2:
+        pytest.skip("needs >= 2 physical cores")
+    n = 512
+    genome = "101010100001"      # matmul nest on the host (one thread): ~0.1-0.2 s of compute-bound host work
+    with capi.Context(n=n, num_slots=slots, devices=[0] * slots, host_threads=1, timeout_s=60.0) as ctx:
+        st0 = None
+        alone = []
+        for _ in range(3):
+            out = ctx.measure(genome, slot=0)
+            assert out.status == capi.MEASURED
+            alone.append(out.time_s)
+            st0 = ctx.stats(0)
+        assert st0.host_cpus >= 1 and st0.host_first_cpu >= 0 and st0.host_loadavg >= 0.0
+        firsts = set()
+        for s in range(slots):
+            ctx.measure("101010101001", slot=s)
+            firsts.add(ctx.stats(s).host_first_cpu)
+        assert len(firsts) == slots                     # disjoint CPU sets
+        crowded = []
+        for _ in range(3):
+            outs = ctx.measure_batch([genome] * slots)  # one per slot, all at once
+            assert all(o.status == capi.MEASURED for o in outs)
+            crowded.append(max(o.time_s for o in outs))
+        t_alone, t_crowded = sorted(alone)[1], sorted(crowded)[1]
+        print(f"alone {t_alone * 1e3:.1f} ms, with {slots - 1} busy neighbours {t_crowded * 1e3:.1f} ms (worst slot)")
+        assert t_crowded <= 1.10 * t_alone, (t_alone, t_crowded)
+        c = ctx.fetch(capi.ARRAY_C, slot=slots - 1)
+        assert bits_equal(c, cpu.App(n, capi.F64, threads=4).run().c)
