@@ -773,6 +773,258 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
   if constexpr (C > 1) cluster_sync_all();  // no CTA leaves while a peer may still multicast into it or signal its barriers
 }
 
+// ---- CTA pairs (tcgen05 cta_group::2) for the forms whose b slices stack to N = 256: SA x 2 digit pairs on 128-wide tiles -----
+// What bounds the short forms in the one-CTA body is operand traffic, not the tensor pipe (profiles/r2f_contraction_rate_probes.txt:
+// 0.175 ms at N = 4096 becomes 0.159 without the loads; the L2 puts 9.2 TB/s on the crossbar of 11.8, and every 128-clock
+// instruction reads 4 KB of a and 8 KB of bt from shared memory while TMA writes the next stage into it).  Two CTAs on the SMs
+// of one TPC execute ONE instruction of M = 256: each holds its own 128 rows of every a slice and ONE of the two b slices
+// (CTA 0: b_1, CTA 1: b_2 -- the hardware takes the first 128 rows of the N = 256 operand from the leader and the rest from its
+// peer), so per SM and k step the instruction reads 4 + 4 KB instead of 4 + 8, a stage is (SA + 1) x 8 KB instead of
+// (SA + 2) x 8, and a pair tile of 256 x 128 moves 25 % fewer operand bytes per flop across the crossbar than two 128 x 128 tiles.
+//   * barriers live at the same offsets in both CTAs.  full[s] of the LEADER counts both producers (2 arrivals + both CTAs' bytes:
+//     cp.async.bulk.tensor .cta_group::2 signals a barrier of the pair's other CTA); empty[s], acc_full are signalled in BOTH CTAs
+//     by multicast commits; acc_empty of the leader counts the epilogue warps of both CTAs (remote arrivals).
+//   * the leader's warp 1 issues every MMA; both CTAs run a TMA producer (warp 0) and eight epilogue warps over their own 128
+//     TMEM lanes (the two-phase epilogue of the body above).
+//   * level blocks 2 .. LV-1 receive a product with "accumulate" set in the tile's first k step (a_t opens block t, which the
+//     one-CTA body initialises with a separate N = 128 instruction -- not expressible here, where halving N means halving each
+//     CTA's share): the epilogue stores zeros into them right after reading them (and once before the first tile).
+template <int SA, int LV> struct OzPairShape {
+  static_assert(LV == SA + 1, "SA x 2 digit pairs have SA + 1 levels");
+  static constexpr int BN = 128, BK = 64;
+  static_assert(LV * BN <= 512, "the level accumulators of a tile must fit TMEM");
+  static constexpr int A_SLICE = OZ_BM * BK, B_SLICE = BN * BK;
+  static constexpr int A_BYTES = SA * A_SLICE;
+  static constexpr int STAGE_BYTES = A_BYTES + B_SLICE;  // per CTA
+  static constexpr int C_SLAB = 32 * 16 * 8;
+  static constexpr int C_BYTES = 8 * C_SLAB;               // one slab per epilogue warp
+  static constexpr int TAIL = 1536;
+  static constexpr int STAGES_FIT = (227 * 1024 - 1024 - TAIL - C_BYTES) / STAGE_BYTES;
+  static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+};
+
+template <int SA, int LV, typename CT>
+__device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap* map_a, const CUtensorMap* map_b, const CUtensorMap* map_c,
+                                             unsigned char* smem_raw) {
+  using Sh = OzPairShape<SA, LV>;
+  constexpr int STAGES = Sh::STAGES, BK = Sh::BK, BN = Sh::BN;
+  const unsigned rank = cluster_ctarank();  // 0 = leader
+  const unsigned raw = smem_u32(smem_raw);
+  const unsigned base = (raw + 1023u) & ~1023u;
+  const unsigned cbuf = base + STAGES * Sh::STAGE_BYTES;
+  const unsigned bars = cbuf + Sh::C_BYTES;
+  auto full_bar = [&](int s) { return bars + 8u * s; };
+  auto empty_bar = [&](int s) { return bars + 8u * (8 + s); };
+  const unsigned acc_full = bars + 8u * 16, acc_empty = bars + 8u * 18;
+  const unsigned tmem_slot = bars + 8u * 24;
+  volatile unsigned* tmem_slot_ptr = reinterpret_cast<volatile unsigned*>(smem_raw + (tmem_slot - raw));
+  int* eb_sh = reinterpret_cast<int*>(smem_raw + (bars + 256 - raw));  // [2][BN] column exponents, alternating per tile
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // pair tiles of 256 rows x 128 columns in raster order; CTA `rank` owns rows [256 sy + 128 rank, + 128)
+  const int tiles_x = (g.cols + BN - 1) / BN, tiles_y2 = ((g.rows + OZ_BM - 1) / OZ_BM + 1) / 2;
+  const int supers = tiles_x * tiles_y2;
+  const int first = static_cast<int>(blockIdx.x) / 2, stride = static_cast<int>(gridDim.x) / 2;
+  const int my_tiles = first < supers ? (supers - 1 - first) / stride + 1 : 0;
+  const long long strip_bytes = static_cast<long long>(OZ_BM) * g.kq * SA;
+  const int fit = static_cast<int>((g.group_l2_bytes > 0 ? g.group_l2_bytes : (64ll << 20)) / strip_bytes);
+  const int rows_per_group = fit < g.group ? (fit > 2 ? fit : 2) : g.group;
+  const int group = rows_per_group / 2 > 0 ? rows_per_group / 2 : 1;
+  auto tile_at = [&](int k, int& bx, int& by) {
+    int sx, sy;
+    raster_map(group, tiles_x, tiles_y2, first + k * stride, sx, sy);
+    bx = sx;
+    by = sy * 2 + static_cast<int>(rank);
+  };
+  const int k_stages = g.kq / BK;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full_bar(s), 2);   // one arrival (with its byte count) per producer of the pair; only the leader's is used
+      mbar_init(empty_bar(s), 1);  // the pair's MMAs have left the stage (multicast commit)
+    }
+    mbar_init(acc_full, 1);
+    mbar_init(acc_empty, 2 * 8);   // the epilogue warps of both CTAs; only the leader's is used
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tmem_slot), "n"(512) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // both CTAs' barriers and allocations are in place before anything crosses the pair
+  tc_fence_after();
+  const unsigned tmem_base = *tmem_slot_ptr;
+  const unsigned lead_acc_empty = mapa_cluster(acc_empty, 0);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int it = 0;
+      for (int tile = 0; tile < my_tiles; ++tile) {
+        int bx, by;
+        tile_at(tile, bx, by);
+        const int m_base = g.row0 + by * OZ_BM, n_rel = bx * BN;
+        for (int kb = 0; kb < k_stages; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
+          const unsigned st = base + s * Sh::STAGE_BYTES;
+          const unsigned lead_full = mapa_cluster(full_bar(s), 0);
+          mbar_expect_tx_cluster(lead_full, Sh::STAGE_BYTES);
+#pragma unroll
+          for (int t = 0; t < SA; ++t) tma_load_3d_2sm(st + t * Sh::A_SLICE, map_a, kb * BK, m_base, t, lead_full);
+          tma_load_3d_2sm(st + Sh::A_BYTES, map_b, kb * BK, n_rel, static_cast<int>(rank), lead_full);  // b_1 here, b_2 in the peer
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && rank == 0) {
+      // cute::UMMA::InstrDescriptor for kind::i8 with M = 256 (the pair), N = 256: D = S32, A = B = signed 8 bit, both K-major
+      constexpr unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<unsigned>(256 >> 3) << 17) | (static_cast<unsigned>(256 >> 4) << 24);
+      int it = 0;
+      for (int tile = 0; tile < my_tiles; ++tile) {
+        mbar_wait(acc_empty, tile & 1);  // completion #tile: the initial zero fill, then one per drained tile
+        tc_fence_after();
+        for (int kb = 0; kb < k_stages; ++kb, ++it) {
+          const int s = it % STAGES;
+          mbar_wait(full_bar(s), (it / STAGES) & 1);
+          tc_fence_after();
+          const unsigned st = base + s * Sh::STAGE_BYTES;
+          const unsigned long long b_st = umma_desc_sw<BK>(st + Sh::A_BYTES);
+#pragma unroll
+          for (int ks = 0; ks < BK / 32; ++ks) {
+            const unsigned long long adv = 2ull * ks;
+#pragma unroll
+            for (int t = 1; t <= SA; ++t) {
+              // a_t x [b_1 | b_2]: levels t + 1, t + 2 = column blocks t - 1, t.  Only a_1 of the tile's first k step overwrites
+              // (blocks 0 and 1); block t of every later a_t starts from the zeros the epilogue left there.
+              const unsigned long long a_t = umma_desc_sw<BK>(st + (t - 1) * Sh::A_SLICE) + adv;
+              tc_mma2_i8(tmem_base + (t - 1) * BN, a_t, b_st + adv, idesc, (kb | ks | (t - 1)) != 0 ? 1u : 0u);
+            }
+          }
+          tc_commit2_mc(empty_bar(s), 3);
+        }
+        tc_commit2_mc(acc_full, 3);
+      }
+    }
+  } else {
+    const int q = warp % 4;
+    const int r = q * 32 + lane;
+    const int m_limit = g.row0 + g.rows;
+    constexpr int NCH = BN / 16, MY = NCH / 2, LD = 8;
+    const int grp = (warp - 2) / 4;
+    const unsigned slab = cbuf + (warp - 2) * Sh::C_SLAB;
+    const unsigned lane_base = tmem_base + (static_cast<unsigned>(q * 32) << 16);
+    const unsigned zeros[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    // before the first tile: this warp's share of the level blocks that are only ever accumulated into starts from zero
+#pragma unroll
+    for (int jj = 0; jj < MY; ++jj)
+#pragma unroll
+      for (int h = 0; h < 16 / LD; ++h)
+#pragma unroll
+        for (int l = 2; l < LV; ++l) tc_st8_issue(lane_base + l * BN + (grp + 2 * jj) * 16 + h * 8, zeros);
+    tc_st_wait();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive_cluster(lead_acc_empty);
+    for (int tile = 0; tile < my_tiles; ++tile) {
+      int bx, by;
+      tile_at(tile, bx, by);
+      const int m_base = g.row0 + by * OZ_BM, n_tile = bx * BN;
+      const int m = m_base + r;
+      const int ei = m < m_limit ? g.exp_a[m] : 0;
+      const bool row_fast = ei > -400 && ei < 400;
+      int* eb = eb_sh + (tile & 1) * BN;
+      if (grp == 0 && r < BN) eb[r] = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
+      asm volatile("bar.sync 1, 256;\n" ::: "memory");
+      mbar_wait(acc_full, tile & 1);
+      tc_fence_after();
+      // phase A: the accumulators leave TMEM as one 64-bit integer per element; blocks >= 2 are zeroed behind the read
+      long long acc[MY][16];
+#pragma unroll
+      for (int jj = 0; jj < MY; ++jj) {
+        const int j = grp + 2 * jj;
+#pragma unroll
+        for (int h = 0; h < 16 / LD; ++h) {
+          unsigned lv[LV][LD];
+#pragma unroll
+          for (int l = 0; l < LV; ++l) tc_ld8_issue(lane_base + l * BN + j * 16 + h * 8, lv[l]);
+          tc_ld_wait();
+#pragma unroll
+          for (int l = 2; l < LV; ++l) tc_st8_issue(lane_base + l * BN + j * 16 + h * 8, zeros);
+#pragma unroll
+          for (int e = 0; e < LD; ++e) {
+            long long x = static_cast<int>(lv[0][e]);
+#pragma unroll
+            for (int l = 1; l < LV; ++l) x = (x << 7) + static_cast<int>(lv[l][e]);
+            acc[jj][h * LD + e] = x;
+          }
+        }
+      }
+      tc_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(lead_acc_empty);
+      // phase B: scale, stage, reduce into c (overlaps the next tile's MMAs); tiles beyond the edge are dropped by the tensor map
+#pragma unroll
+      for (int jj = 0; jj < MY; ++jj) {
+        const int j = grp + 2 * jj;
+        double v[16];
+        int ebv[16];
+        bool cols_fast = true;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          ebv[e] = eb[j * 16 + e];
+          cols_fast &= static_cast<unsigned>(ebv[e] + 399) < 799u;
+        }
+        if (cols_fast && row_fast) {
+          const int e_row = ei - 12 - 7 * (LV - 1);
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const long long x = acc[jj][e];
+            const double d = static_cast<double>(x);
+            const int hi = __double2hiint(d) + (x != 0 ? (e_row + ebv[e]) * (1 << 20) : 0);
+            v[e] = __hiloint2double(hi, __double2loint(d));
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = scaled(static_cast<double>(acc[jj][e]) * pow2(-7 * (LV - 1)), ei, ebv[e]);
+        }
+        if (lane == 0) tma_store_wait_read<0>();
+        __syncwarp();
+        if constexpr (sizeof(CT) == 8) {
+          const unsigned crow = slab + lane * 128;
+#pragma unroll
+          for (int ch = 0; ch < 8; ++ch)
+            asm volatile("st.shared.v2.f64 [%0], {%1, %2};\n" ::"r"(crow + ((ch ^ (lane & 7)) << 4)), "d"(v[2 * ch]), "d"(v[2 * ch + 1]) : "memory");
+        } else {
+          const unsigned crow = slab + lane * 64;
+#pragma unroll
+          for (int ch = 0; ch < 4; ++ch)
+            asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};\n" ::"r"(crow + ((ch ^ ((lane >> 1) & 3)) << 4)), "f"(static_cast<float>(v[4 * ch])),
+                         "f"(static_cast<float>(v[4 * ch + 1])), "f"(static_cast<float>(v[4 * ch + 2])), "f"(static_cast<float>(v[4 * ch + 3]))
+                         : "memory");
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_reduce_add_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
+          tma_store_commit();
+        }
+      }
+    }
+    if (lane == 0) tma_store_wait<0>();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  cluster_sync_all();  // neither CTA frees tensor memory or leaves while its peer may still use or signal it
+  if (warp == 2) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "n"(512) : "memory");
+  }
+}
+
 // the tensor maps a launch may need: slices of a in boxes of 128 / 64 rows, slices of bt in boxes of 128 / 64 / 32 rows (whole
 // tiles, or the share one CTA of a cluster fetches), c
 struct OzMaps {
@@ -814,6 +1066,32 @@ matmul_ozaki_auto_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, c
         if (form == 777) oz_persist_form<7, 7, 7, 64, 0, 1, 1>(g, maps, smem_raw);
       }
       break;  // 0: not error-free in any form -- not this kernel's launch
+  }
+}
+
+// auto mode as CTA pairs (clusters of two): the forms with two b slices on 128-wide tiles run as pairs (oz_pair_body), every
+// other form runs each CTA of the cluster on its own as in the kernel above
+template <typename CT>
+__global__ void __launch_bounds__(OZP_THREADS, 1)
+matmul_ozaki_auto_pair_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, const int* __restrict__ guard, int* __restrict__ ran) {
+  extern __shared__ unsigned char smem_raw[];
+  const int form = sizeof(CT) == 8 ? ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]) : ozaki_pick_form_f32(guard[0] | guard[3], guard[1], guard[2]);
+  if (blockIdx.x == 0 && threadIdx.x == 0) *ran = form;
+  switch (form) {
+    case 223: oz_pair_body<2, 3, CT>(g, &maps.a128, &maps.b128, &maps.c, smem_raw); break;
+    case 324: oz_pair_body<3, 4, CT>(g, &maps.a128, &maps.b128, &maps.c, smem_raw); break;
+    case 234: oz_persist_form<2, 3, 4, 128, 1, 1, 1, CT>(g, maps, smem_raw); break;
+    case 335: oz_persist_form<3, 3, 5, 64, 1, 1, 1, CT>(g, maps, smem_raw); break;
+    case 436: oz_persist_form<4, 3, 6, 64, 1, 1, 1, CT>(g, maps, smem_raw); break;
+    case 346: oz_persist_form<3, 4, 6, 64, 1, 1, 1, CT>(g, maps, smem_raw); break;
+    case 447: oz_persist_form<4, 4, 7, 64, 1, 1, 1, CT>(g, maps, smem_raw); break;
+    case 555: oz_persist_form<5, 5, 5, 64, 1, 1, 1, CT>(g, maps, smem_raw); break;
+    default:
+      if constexpr (sizeof(CT) == 8) {
+        if (form == 666) oz_persist_form<6, 6, 6, 64, 0, 1, 1>(g, maps, smem_raw);
+        if (form == 777) oz_persist_form<7, 7, 7, 64, 0, 1, 1>(g, maps, smem_raw);
+      }
+      break;
   }
 }
 
@@ -1103,6 +1381,38 @@ OzClusterChoice oz_auto_cluster_choice() {
   return choice[d & 63];
 }
 
+// The pair kernel (clusters of two CTAs): configured once per device; `clusters` = pairs the device keeps resident with one CTA per
+// SM (0: pairs unavailable -- the one-CTA auto kernel is used).  MMX_OZ_PAIR=0 switches the pairs off (A/B runs).
+template <typename CT> int oz_pair_clusters() {
+  static PerDeviceOnce once;
+  static int clusters[64] = {};
+  int d = 0;
+  cudaGetDevice(&d);
+  bool& known = once.here();
+  if (!known) {
+    known = true;
+    clusters[d & 63] = 0;
+    static const int enabled = [] { const char* e = getenv("MMX_OZ_PAIR"); return e ? atoi(e) : 1; }();
+    if (enabled && cudaFuncSetAttribute(matmul_ozaki_auto_pair_kernel<CT>, cudaFuncAttributeMaxDynamicSharedMemorySize, kOzPersistSmemMax) == cudaSuccess) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(static_cast<unsigned>(oz_sm_count() / 2 * 2));
+      cfg.blockDim = dim3(OZP_THREADS);
+      cfg.dynamicSmemBytes = kOzPersistSmemMax;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeClusterDimension;
+      attr[0].val.clusterDim.x = 2;
+      attr[0].val.clusterDim.y = 1;
+      attr[0].val.clusterDim.z = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, matmul_ozaki_auto_pair_kernel<CT>, &cfg) == cudaSuccess && n > 0) clusters[d & 63] = std::min(n, oz_sm_count() / 2);
+    }
+    (void)cudaGetLastError();
+  }
+  return clusters[d & 63];
+}
+
 template <int S, int CR> cudaError_t oz_fixed_configure() {
   static PerDeviceOnce once;
   return oz_persist_configure(matmul_ozaki_fixed_kernel<S, CR>, OzPShape<S, S, S, 64, CR>::SMEM_BYTES, once);
@@ -1160,6 +1470,24 @@ cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, in
   const dim3 grid(static_cast<unsigned>(std::min(tiles_x * tiles_y, oz_sm_count())));
   switch (slices) {
     case 0: {
+      if (const int pairs = oz_pair_clusters<CT>(); pairs > 0) {
+        // every resident pair is launched: a pair (or, in the one-CTA forms, a CTA) beyond the tile count finds no tile
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(static_cast<unsigned>(2 * pairs));
+        cfg.blockDim = dim3(OZP_THREADS);
+        cfg.dynamicSmemBytes = kOzPersistSmemMax;
+        cfg.stream = stream;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 2;
+        attr[0].val.clusterDim.y = 1;
+        attr[0].val.clusterDim.z = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        const int* guard_words = L.guard;
+        int* ran_word = L.guard + 4;
+        return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_pair_kernel<CT>, g, maps, guard_words, ran_word);
+      }
       OzClusterChoice cc = oz_auto_cluster_choice();
       if (sizeof(CT) != 8 && cc.shape != 11) {  // the multicast forms are instantiated for FP64 only
         cc.shape = 11;
@@ -1233,6 +1561,8 @@ cudaError_t matmul_ozaki_prepare() {
   if (cudaError_t e = oz_configure<6, 1, 64>(); e != cudaSuccess) return e;
   (void)oz_auto_cluster_choice();  // configures the auto kernel of the chosen cluster shape
   if (cudaError_t e = oz_auto_configure<1, 1, float>(); e != cudaSuccess) return e;
+  (void)oz_pair_clusters<double>();  // ... and the pair kernels (first-use work must not happen inside a stream capture)
+  (void)oz_pair_clusters<float>();
   if (cudaError_t e = oz_fixed_configure<2, 0>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_fixed_configure<3, 0>(); e != cudaSuccess) return e;
   if (cudaError_t e = oz_fixed_configure<4, 0>(); e != cudaSuccess) return e;

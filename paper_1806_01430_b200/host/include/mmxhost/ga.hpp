@@ -24,6 +24,7 @@
 
 #include "mmxhost/evaluator.hpp"
 #include "mmxhost/genome.hpp"
+#include "mmxhost/source_model.hpp"
 
 namespace mmxhost {
 
@@ -101,9 +102,10 @@ struct RunningBest {
   bool update(double t, const Genome& g);
 };
 
-// Baseline (all-zero genome) + T generations.  The reference takes a CandidateSet only to read
-// its gene length and to render the winner's source; here the gene length is passed directly
-// and rendering is the caller's business.
+// Baseline (all-zero genome) + T generations.  Same signature as the reference's (include/acctune/ga.hpp:107); it reads the
+// candidate set's gene length only (ga.cpp:247-250) -- rendering the winner's source is the caller's business in both.
+TuningResult run_ga(const CandidateSet& cs, const GAParams& params, GenomeEvaluator& evaluator);
+// The same search for callers that have a gene length but no source model (the C window used by the rank-sharded evaluator).
 TuningResult run_ga(std::size_t gene_length, const GAParams& params, GenomeEvaluator& evaluator);
 
 // generation,best_time_s,best_speedup,best_genome,mean_fitness,distinct_evals,cache_hits  (%.9g)

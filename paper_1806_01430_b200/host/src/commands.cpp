@@ -287,7 +287,7 @@ int cmd_tune(const std::string& config_path, const TuneOptions& options, std::os
     }
     out << "candidates: " << cs.gene_length() << " of " << cs.all_loops.size() << " loops\n";
 
-    const TuningResult result = run_ga(cs.gene_length(), cfg.ga, *evaluator);
+    const TuningResult result = run_ga(cs, cfg.ga, *evaluator);
     const EvalCounters counters = evaluator->counters();
     {
       std::ofstream csv(cfg.generations_csv_path(), std::ios::binary);
