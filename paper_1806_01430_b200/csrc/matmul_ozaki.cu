@@ -781,47 +781,56 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
 // (CTA 0: b_1, CTA 1: b_2 -- the hardware takes the first 128 rows of the N = 256 operand from the leader and the rest from its
 // peer), so per SM and k step the instruction reads 4 + 4 KB instead of 4 + 8, a stage is (SA + 1) x 8 KB instead of
 // (SA + 2) x 8, and a pair tile of 256 x 128 moves 25 % fewer operand bytes per flop across the crossbar than two 128 x 128 tiles.
-//   * barriers live at the same offsets in both CTAs.  full[s] of the LEADER counts both producers (2 arrivals + both CTAs' bytes:
-//     cp.async.bulk.tensor .cta_group::2 signals a barrier of the pair's other CTA); empty[s], acc_full are signalled in BOTH CTAs
+//   * barriers live at the same offsets in both CTAs.  full[s] of the LEADER counts both CTAs' bytes (announced by the leader's
+//     producer; cp.async.bulk.tensor .cta_group::2 signals a barrier of the pair's other CTA); empty[s], acc_full are signalled in BOTH CTAs
 //     by multicast commits; acc_empty of the leader counts the epilogue warps of both CTAs (remote arrivals).
 //   * the leader's warp 1 issues every MMA; both CTAs run a TMA producer (warp 0) and eight epilogue warps over their own 128
 //     TMEM lanes (the two-phase epilogue of the body above).
 //   * level blocks 2 .. LV-1 receive a product with "accumulate" set in the tile's first k step (a_t opens block t, which the
 //     one-CTA body initialises with a separate N = 128 instruction -- not expressible here, where halving N means halving each
 //     CTA's share): the epilogue stores zeros into them right after reading them (and once before the first tile).
-template <int SA, int LV> struct OzPairShape {
-  static_assert(LV == SA + 1, "SA x 2 digit pairs have SA + 1 levels");
-  static constexpr int BN = 128, BK = 64;
+//   * SA x 3 pairs (the application from N = 16384): tiles are 96 wide so that five levels fit TMEM (480 columns); a_t meets
+//     [b_1 | b_2] in an N = 192 instruction (CTA 0 holds b_1, CTA 1 holds b_2) and b_3 in an N = 96 one (each CTA holds 48 of its
+//     rows).  Every level block is opened by an overwriting instruction here, so nothing needs zeroing.
+template <int SA, int SB, int LV> struct OzPairShape {
+  static_assert(SB == 2 || SB == 3, "two or three b slices");
+  static_assert(LV == SA + SB - 1, "rectangular forms");
+  static constexpr int BN = SB == 2 ? 128 : 96, BK = 64;
   static_assert(LV * BN <= 512, "the level accumulators of a tile must fit TMEM");
-  static constexpr int A_SLICE = OZ_BM * BK, B_SLICE = BN * BK;
+  static constexpr int A_SLICE = OZ_BM * BK;
   static constexpr int A_BYTES = SA * A_SLICE;
-  static constexpr int STAGE_BYTES = A_BYTES + B_SLICE;  // per CTA
+  static constexpr int B1_BYTES = BN * BK;                        // this CTA's slice of the [b_1 | b_2] operand
+  static constexpr int B2_BYTES = SB == 3 ? (BN / 2) * BK : 0;    // its half of b_3
+  static constexpr int STAGE_BYTES = A_BYTES + B1_BYTES + B2_BYTES;  // per CTA
   static constexpr int C_SLAB = 32 * 16 * 8;
   static constexpr int C_BYTES = 8 * C_SLAB;               // one slab per epilogue warp
-  static constexpr int TAIL = 1536;
+  static constexpr bool SCALE_TABLE = LV > 4;
+  static constexpr int TAIL = SCALE_TABLE ? 3584 : 1536;
   static constexpr int STAGES_FIT = (227 * 1024 - 1024 - TAIL - C_BYTES) / STAGE_BYTES;
   static constexpr int STAGES = STAGES_FIT > 8 ? 8 : STAGES_FIT;
+  static_assert(STAGES >= 3, "stage ring");
 };
 
-template <int SA, int LV, typename CT>
-__device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap* map_a, const CUtensorMap* map_b, const CUtensorMap* map_c,
-                                             unsigned char* smem_raw) {
-  using Sh = OzPairShape<SA, LV>;
+template <int SA, int SB, int LV, typename CT>
+__device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap* map_a, const CUtensorMap* map_b, const CUtensorMap* map_b_half,
+                                             const CUtensorMap* map_c, unsigned char* smem_raw) {
+  using Sh = OzPairShape<SA, SB, LV>;
   constexpr int STAGES = Sh::STAGES, BK = Sh::BK, BN = Sh::BN;
   const unsigned rank = cluster_ctarank();  // 0 = leader
   const unsigned raw = smem_u32(smem_raw);
   const unsigned base = (raw + 1023u) & ~1023u;
   const unsigned cbuf = base + STAGES * Sh::STAGE_BYTES;
-  const unsigned bars = cbuf + Sh::C_BYTES;
+  const unsigned bars = (cbuf + Sh::C_BYTES + 127u) & ~127u;
   auto full_bar = [&](int s) { return bars + 8u * s; };
   auto empty_bar = [&](int s) { return bars + 8u * (8 + s); };
   const unsigned acc_full = bars + 8u * 16, acc_empty = bars + 8u * 18;
   const unsigned tmem_slot = bars + 8u * 24;
   volatile unsigned* tmem_slot_ptr = reinterpret_cast<volatile unsigned*>(smem_raw + (tmem_slot - raw));
-  int* eb_sh = reinterpret_cast<int*>(smem_raw + (bars + 256 - raw));  // [2][BN] column exponents, alternating per tile
+  int* eb_sh = reinterpret_cast<int*>(smem_raw + (bars + 256 - raw));               // [2][BN] column exponents, alternating per tile
+  double* pb_sh = reinterpret_cast<double*>(smem_raw + (bars + 256 + 1024 - raw));  // [2][BN] 2^exponent (clamped) of the same
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  // pair tiles of 256 rows x 128 columns in raster order; CTA `rank` owns rows [256 sy + 128 rank, + 128)
+  // pair tiles of 256 rows x BN columns in raster order; CTA `rank` owns rows [256 sy + 128 rank, + 128)
   const int tiles_x = (g.cols + BN - 1) / BN, tiles_y2 = ((g.rows + OZ_BM - 1) / OZ_BM + 1) / 2;
   const int supers = tiles_x * tiles_y2;
   const int first = static_cast<int>(blockIdx.x) / 2, stride = static_cast<int>(gridDim.x) / 2;
@@ -840,7 +849,7 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(full_bar(s), 2);   // one arrival (with its byte count) per producer of the pair; only the leader's is used
+      mbar_init(full_bar(s), 1);   // the leader's arrival carries the byte count of both CTAs' loads; only the leader's is used
       mbar_init(empty_bar(s), 1);  // the pair's MMAs have left the stage (multicast commit)
     }
     mbar_init(acc_full, 1);
@@ -870,36 +879,51 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
           mbar_wait(empty_bar(s), ((it / STAGES) & 1) ^ 1);
           const unsigned st = base + s * Sh::STAGE_BYTES;
           const unsigned lead_full = mapa_cluster(full_bar(s), 0);
-          mbar_expect_tx_cluster(lead_full, Sh::STAGE_BYTES);
+          if ((g.debug & 1) && it >= STAGES) {  // rate probe: the MMAs run on whatever the stage buffers hold
+            if (rank == 0) mbar_arrive(full_bar(s));
+            continue;
+          }
+          // the leader announces the bytes of BOTH CTAs on its own barrier (a local operation); the peer only issues its loads,
+          // whose bytes are counted there too -- a remote arrive.expect_tx per stage cost ~0.5 us of the peer's producer,
+          // twice the time the pair needs to consume a stage
+          if (rank == 0) mbar_expect_tx(full_bar(s), 2 * Sh::STAGE_BYTES);
 #pragma unroll
           for (int t = 0; t < SA; ++t) tma_load_3d_2sm(st + t * Sh::A_SLICE, map_a, kb * BK, m_base, t, lead_full);
           tma_load_3d_2sm(st + Sh::A_BYTES, map_b, kb * BK, n_rel, static_cast<int>(rank), lead_full);  // b_1 here, b_2 in the peer
+          if constexpr (SB == 3)  // and this CTA's half of b_3's rows
+            tma_load_3d_2sm(st + Sh::A_BYTES + Sh::B1_BYTES, map_b_half, kb * BK, n_rel + static_cast<int>(rank) * (BN / 2), 2, lead_full);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0 && rank == 0) {
-      // cute::UMMA::InstrDescriptor for kind::i8 with M = 256 (the pair), N = 256: D = S32, A = B = signed 8 bit, both K-major
-      constexpr unsigned idesc = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<unsigned>(256 >> 3) << 17) | (static_cast<unsigned>(256 >> 4) << 24);
+      // cute::UMMA::InstrDescriptor for kind::i8 with M = 256 (the pair): D = S32, A = B = signed 8 bit, both K-major, N >> 3 @17
+      constexpr unsigned idesc_m = (2u << 4) | (1u << 7) | (1u << 10) | (static_cast<unsigned>(256 >> 4) << 24);
+      constexpr unsigned idesc_12 = idesc_m | (static_cast<unsigned>((2 * BN) >> 3) << 17);  // a_t x [b_1 | b_2]
+      constexpr unsigned idesc_3 = idesc_m | (static_cast<unsigned>(BN >> 3) << 17);         // a_t x b_3
       int it = 0;
       for (int tile = 0; tile < my_tiles; ++tile) {
-        mbar_wait(acc_empty, tile & 1);  // completion #tile: the initial zero fill, then one per drained tile
+        mbar_wait(acc_empty, tile & 1);  // completion #tile: the epilogue warps' initial arrival, then one per drained tile
         tc_fence_after();
         for (int kb = 0; kb < k_stages; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(full_bar(s), (it / STAGES) & 1);
           tc_fence_after();
           const unsigned st = base + s * Sh::STAGE_BYTES;
-          const unsigned long long b_st = umma_desc_sw<BK>(st + Sh::A_BYTES);
+          const unsigned long long b12 = umma_desc_sw<BK>(st + Sh::A_BYTES), b3 = umma_desc_sw<BK>(st + Sh::A_BYTES + Sh::B1_BYTES);
 #pragma unroll
           for (int ks = 0; ks < BK / 32; ++ks) {
             const unsigned long long adv = 2ull * ks;
 #pragma unroll
             for (int t = 1; t <= SA; ++t) {
-              // a_t x [b_1 | b_2]: levels t + 1, t + 2 = column blocks t - 1, t.  Only a_1 of the tile's first k step overwrites
-              // (blocks 0 and 1); block t of every later a_t starts from the zeros the epilogue left there.
               const unsigned long long a_t = umma_desc_sw<BK>(st + (t - 1) * Sh::A_SLICE) + adv;
-              tc_mma2_i8(tmem_base + (t - 1) * BN, a_t, b_st + adv, idesc, (kb | ks | (t - 1)) != 0 ? 1u : 0u);
+              const bool opening = kb == 0 && ks == 0;  // the tile's first k step
+              // a_t x [b_1 | b_2]: levels t + 1, t + 2 = column blocks t - 1, t.  a_1 opens both (overwrite); with two b slices a
+              // later a_t accumulates into a block t nobody has written (the epilogue left zeros there), with three it was
+              // opened by a_(t-1) x b_3
+              tc_mma2_i8(tmem_base + (t - 1) * BN, a_t, b12 + adv, idesc_12, (opening && t == 1) ? 0u : 1u);
+              if constexpr (SB == 3)  // a_t x b_3: level t + 3 = block t + 1, always a block of its own in the first k step
+                tc_mma2_i8(tmem_base + (t + 1) * BN, a_t, b3 + adv, idesc_3, opening ? 0u : 1u);
             }
           }
           tc_commit2_mc(empty_bar(s), 3);
@@ -912,18 +936,21 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
     const int r = q * 32 + lane;
     const int m_limit = g.row0 + g.rows;
     constexpr int NCH = BN / 16, MY = NCH / 2, LD = 8;
+    constexpr bool ZERO_FILL = SB == 2;  // blocks 2 .. LV-1 are only ever accumulated into
     const int grp = (warp - 2) / 4;
     const unsigned slab = cbuf + (warp - 2) * Sh::C_SLAB;
     const unsigned lane_base = tmem_base + (static_cast<unsigned>(q * 32) << 16);
     const unsigned zeros[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    // before the first tile: this warp's share of the level blocks that are only ever accumulated into starts from zero
+    if constexpr (ZERO_FILL) {
+      // before the first tile: this warp's share of the level blocks that are only ever accumulated into starts from zero
 #pragma unroll
-    for (int jj = 0; jj < MY; ++jj)
+      for (int jj = 0; jj < MY; ++jj)
 #pragma unroll
-      for (int h = 0; h < 16 / LD; ++h)
+        for (int h = 0; h < 16 / LD; ++h)
 #pragma unroll
-        for (int l = 2; l < LV; ++l) tc_st8_issue(lane_base + l * BN + (grp + 2 * jj) * 16 + h * 8, zeros);
-    tc_st_wait();
+          for (int l = 2; l < LV; ++l) tc_st8_issue(lane_base + l * BN + (grp + 2 * jj) * 16 + h * 8, zeros);
+      tc_st_wait();
+    }
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive_cluster(lead_acc_empty);
@@ -934,13 +961,21 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
       const int m = m_base + r;
       const int ei = m < m_limit ? g.exp_a[m] : 0;
       const bool row_fast = ei > -400 && ei < 400;
+      const double pa = pow2(row_fast ? ei - 12 : 0);
       int* eb = eb_sh + (tile & 1) * BN;
-      if (grp == 0 && r < BN) eb[r] = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
+      double* pb = pb_sh + (tile & 1) * BN;
+      if (grp == 0 && r < BN) {
+        const int e = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
+        eb[r] = e;
+        if constexpr (Sh::SCALE_TABLE) pb[r] = pow2(e > -400 && e < 400 ? e : 0);
+      }
       asm volatile("bar.sync 1, 256;\n" ::: "memory");
       mbar_wait(acc_full, tile & 1);
       tc_fence_after();
-      // phase A: the accumulators leave TMEM as one 64-bit integer per element; blocks >= 2 are zeroed behind the read
-      long long acc[MY][16];
+      // phase A: the accumulators leave TMEM as one number per element (a 64-bit integer up to four levels, the Horner sum in
+      // FP64 beyond); blocks that are only accumulated into are zeroed behind the read
+      long long acc[LV <= 4 ? MY : 1][16];
+      double hsum[LV <= 4 ? 1 : MY][16];
 #pragma unroll
       for (int jj = 0; jj < MY; ++jj) {
         const int j = grp + 2 * jj;
@@ -950,45 +985,60 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
 #pragma unroll
           for (int l = 0; l < LV; ++l) tc_ld8_issue(lane_base + l * BN + j * 16 + h * 8, lv[l]);
           tc_ld_wait();
+          if constexpr (ZERO_FILL) {
 #pragma unroll
-          for (int l = 2; l < LV; ++l) tc_st8_issue(lane_base + l * BN + j * 16 + h * 8, zeros);
+            for (int l = 2; l < LV; ++l) tc_st8_issue(lane_base + l * BN + j * 16 + h * 8, zeros);
+          }
 #pragma unroll
           for (int e = 0; e < LD; ++e) {
-            long long x = static_cast<int>(lv[0][e]);
+            if constexpr (LV <= 4) {
+              long long x = static_cast<int>(lv[0][e]);
 #pragma unroll
-            for (int l = 1; l < LV; ++l) x = (x << 7) + static_cast<int>(lv[l][e]);
-            acc[jj][h * LD + e] = x;
+              for (int l = 1; l < LV; ++l) x = (x << 7) + static_cast<int>(lv[l][e]);
+              acc[jj][h * LD + e] = x;
+            } else {
+              double x = static_cast<double>(static_cast<int>(lv[LV - 1][e]));
+#pragma unroll
+              for (int l = LV - 2; l >= 0; --l) x = fma(x, 0.0078125, static_cast<double>(static_cast<int>(lv[l][e])));
+              hsum[jj][h * LD + e] = x;
+            }
           }
         }
       }
-      tc_st_wait();
+      if constexpr (ZERO_FILL) tc_st_wait();
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(lead_acc_empty);
       // phase B: scale, stage, reduce into c (overlaps the next tile's MMAs); tiles beyond the edge are dropped by the tensor map
+      if (g.debug & 2) continue;
 #pragma unroll
       for (int jj = 0; jj < MY; ++jj) {
         const int j = grp + 2 * jj;
         double v[16];
-        int ebv[16];
-        bool cols_fast = true;
-#pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          ebv[e] = eb[j * 16 + e];
-          cols_fast &= static_cast<unsigned>(ebv[e] + 399) < 799u;
-        }
-        if (cols_fast && row_fast) {
-          const int e_row = ei - 12 - 7 * (LV - 1);
+        if constexpr (LV <= 4) {
+          int ebv[16];
+          bool cols_fast = true;
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            const long long x = acc[jj][e];
-            const double d = static_cast<double>(x);
-            const int hi = __double2hiint(d) + (x != 0 ? (e_row + ebv[e]) * (1 << 20) : 0);
-            v[e] = __hiloint2double(hi, __double2loint(d));
+            ebv[e] = eb[j * 16 + e];
+            cols_fast &= static_cast<unsigned>(ebv[e] + 399) < 799u;
+          }
+          if (cols_fast && row_fast) {
+            const int e_row = ei - 12 - 7 * (LV - 1);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              const long long x = acc[jj][e];
+              const double d = static_cast<double>(x);
+              const int hi = __double2hiint(d) + (x != 0 ? (e_row + ebv[e]) * (1 << 20) : 0);
+              v[e] = __hiloint2double(hi, __double2loint(d));
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = scaled(static_cast<double>(acc[jj][e]) * pow2(-7 * (LV - 1)), ei, ebv[e]);
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) v[e] = scaled(static_cast<double>(acc[jj][e]) * pow2(-7 * (LV - 1)), ei, ebv[e]);
+          for (int e = 0; e < 16; ++e) v[e] = scaled_fast(hsum[jj][e], ei, pa, row_fast, eb[j * 16 + e], pb[j * 16 + e]);
         }
         if (lane == 0) tma_store_wait_read<0>();
         __syncwarp();
@@ -1028,7 +1078,7 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
 // the tensor maps a launch may need: slices of a in boxes of 128 / 64 rows, slices of bt in boxes of 128 / 64 / 32 rows (whole
 // tiles, or the share one CTA of a cluster fetches), c
 struct OzMaps {
-  CUtensorMap a128, a64, b128, b64, b32, c;
+  CUtensorMap a128, a64, b128, b64, b32, c, b96, b48;  // b96 / b48: the 96-wide tiles of the three-slice pair forms
 };
 template <int ROWS> __device__ __forceinline__ const CUtensorMap* oz_map_a(const OzMaps& m) {
   static_assert(ROWS == 128 || ROWS == 64, "a box");
@@ -1078,10 +1128,10 @@ matmul_ozaki_auto_pair_kernel(const OzPArgs g, const __grid_constant__ OzMaps ma
   const int form = sizeof(CT) == 8 ? ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]) : ozaki_pick_form_f32(guard[0] | guard[3], guard[1], guard[2]);
   if (blockIdx.x == 0 && threadIdx.x == 0) *ran = form;
   switch (form) {
-    case 223: oz_pair_body<2, 3, CT>(g, &maps.a128, &maps.b128, &maps.c, smem_raw); break;
-    case 324: oz_pair_body<3, 4, CT>(g, &maps.a128, &maps.b128, &maps.c, smem_raw); break;
-    case 234: oz_persist_form<2, 3, 4, 128, 1, 1, 1, CT>(g, maps, smem_raw); break;
-    case 335: oz_persist_form<3, 3, 5, 64, 1, 1, 1, CT>(g, maps, smem_raw); break;
+    case 223: oz_pair_body<2, 2, 3, CT>(g, &maps.a128, &maps.b128, nullptr, &maps.c, smem_raw); break;
+    case 324: oz_pair_body<3, 2, 4, CT>(g, &maps.a128, &maps.b128, nullptr, &maps.c, smem_raw); break;
+    case 234: oz_pair_body<2, 3, 4, CT>(g, &maps.a128, &maps.b96, &maps.b48, &maps.c, smem_raw); break;
+    case 335: oz_pair_body<3, 3, 5, CT>(g, &maps.a128, &maps.b96, &maps.b48, &maps.c, smem_raw); break;
     case 436: oz_persist_form<4, 3, 6, 64, 1, 1, 1, CT>(g, maps, smem_raw); break;
     case 346: oz_persist_form<3, 4, 6, 64, 1, 1, 1, CT>(g, maps, smem_raw); break;
     case 447: oz_persist_form<4, 4, 7, 64, 1, 1, 1, CT>(g, maps, smem_raw); break;
@@ -1443,7 +1493,8 @@ cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, in
   if (!make_slice_map(&maps.a128, L.sa, static_cast<size_t>(n), L.kq, 64, 128, planes, 1) ||
       !make_slice_map(&maps.a64, L.sa, static_cast<size_t>(n), L.kq, 64, 64, planes, 1) ||
       !make_slice_map(&maps.b128, L.sb, L.b_rows, L.kq, 64, 128, planes, 1) || !make_slice_map(&maps.b64, L.sb, L.b_rows, L.kq, 64, 64, planes, 1) ||
-      !make_slice_map(&maps.b32, L.sb, L.b_rows, L.kq, 64, 32, planes, 1))
+      !make_slice_map(&maps.b32, L.sb, L.b_rows, L.kq, 64, 32, planes, 1) || !make_slice_map(&maps.b96, L.sb, L.b_rows, L.kq, 64, 96, planes, 1) ||
+      !make_slice_map(&maps.b48, L.sb, L.b_rows, L.kq, 64, 48, planes, 1))
     return cudaErrorNotSupported;
   if (c_by_tma) {
     if (!make_c_map(&maps.c, c, sizeof(CT), n, row0 + rows, col0 + cols)) return cudaErrorNotSupported;
