@@ -330,7 +330,7 @@ cudaError_t run_train(mmx_ctx* ctx, Slot& s, int gene, long long total, const De
 }
 
 template <typename T>
-bool run_host_nest(const mmx_ctx* ctx, Slot& s, int nest, const Deadline& dl, double* checksum) {
+bool run_host_nest(const mmx_ctx* ctx, Slot& s, int nest, int row0, int row1, const Deadline& dl, double* checksum) {
   const int n = ctx->cfg.n;
   HostTeam th;
   th.threads = ctx->cfg.host_threads;
@@ -341,11 +341,11 @@ bool run_host_nest(const mmx_ctx* ctx, Slot& s, int nest, const Deadline& dl, do
   T* c = static_cast<T*>(s.h_arr[MMX_ARRAY_C]);
   T* bt = static_cast<T*>(s.h_arr[MMX_ARRAY_BT]);
   switch (nest) {
-    case MMX_NEST_INIT_A: return host_init_a<T>(a, n, th, dl);
-    case MMX_NEST_INIT_B: return host_init_b<T>(b, n, th, dl);
-    case MMX_NEST_ZERO_C: return host_zero_c<T>(c, n, th, dl);
-    case MMX_NEST_TRANSPOSE: return host_transpose<T>(bt, b, n, th, dl);
-    case MMX_NEST_MATMUL: return host_matmul<T>(c, a, bt, n, th, dl);
+    case MMX_NEST_INIT_A: return host_init_a<T>(a, n, row0, row1, th, dl);
+    case MMX_NEST_INIT_B: return host_init_b<T>(b, n, row0, row1, th, dl);
+    case MMX_NEST_ZERO_C: return host_zero_c<T>(c, n, row0, row1, th, dl);
+    case MMX_NEST_TRANSPOSE: return host_transpose<T>(bt, b, n, row0, row1, th, dl);
+    case MMX_NEST_MATMUL: return host_matmul<T>(c, a, bt, n, row0, row1, th, dl);
     case MMX_NEST_TRACE: *checksum = host_trace<T>(c, n); return true;
     default: return false;
   }
@@ -378,6 +378,16 @@ unsigned nest_arrays(int nest) {
     case MMX_NEST_MATMUL: return 1u << MMX_ARRAY_A | 1u << MMX_ARRAY_BT | 1u << MMX_ARRAY_C;
     case MMX_NEST_TRACE: return 1u << MMX_ARRAY_C;
     default: return 0;
+  }
+}
+
+// bit q set: step `st` touches array q (bit 4 = the checksum scalar)
+unsigned step_arrays(const mmx_plan_step& st) {
+  switch (st.kind) {
+    case MMX_STEP_CPU:
+    case MMX_STEP_GPU: return nest_arrays(st.nest) | (st.nest == MMX_NEST_TRACE ? 1u << 4 : 0u);
+    case MMX_STEP_D2H_SUM: return 1u << 4;
+    default: return st.array >= 0 ? 1u << st.array : 0u;
   }
 }
 
@@ -501,7 +511,32 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const 
       if (st.nest == MMX_NEST_TRACE) sum_on_device = true;
     }
   }
+  // Steps run in plan order with two exceptions that keep the device and the bus busy while a CPU-mapped nest computes
+  // (MMX_OVERLAP=0 switches both off: A/B runs):
+  //  * hoisting: before a CPU nest starts, every later whole-nest GPU step that touches none of the arrays of the steps it would
+  //    overtake is enqueued (launches are asynchronous: they run beside the host loop);
+  //  * streaming: when the array a CPU nest writes is copied to the device later in the plan (and nothing in between touches it),
+  //    the nest runs block by block and each finished block of rows is copied at once -- only the last block's transfer is left
+  //    when the nest ends.  Bytes moved are the plan's: the same transfer, cut into pieces.
+  static const bool overlap_enabled = [] { const char* v = getenv("MMX_OVERLAP"); return v == nullptr || atoi(v) != 0; }();
+  bool issued[MMX_MAX_PLAN_STEPS] = {};
+  auto run_gpu_step = [&](const mmx_plan_step& st) {
+    any_gpu = true;
+    const int gene = gene_of(st.nest, st.mode);
+    if (st.mode == MMX_MODE_GPU_NEST) {
+      e = launch_gene_any(ctx, s, gene, IterRef{nullptr, 0});
+    } else {
+      e = run_train(ctx, s, gene, static_cast<long long>(st.launches), dl, &timed_out, &s.stats.graph_launches);
+    }
+    const int w = written_array(st.nest);
+    if (w >= 0) {
+      s.dev_valid[w] = true;
+      s.host_valid[w] = false;
+    }
+    if (st.nest == MMX_NEST_TRACE) sum_on_device = true;
+  };
   for (int si = 0; whole == nullptr && si < plan.num_steps && e == cudaSuccess && !timed_out; ++si) {
+    if (issued[si]) continue;
     const mmx_plan_step& st = plan.steps[si];
     const Clock::time_point ts = Clock::now();
     switch (st.kind) {
@@ -532,34 +567,62 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const 
         any_gpu = true;
         break;
       case MMX_STEP_CPU: {
-        const bool ok = ctx->cfg.dtype == MMX_F64 ? run_host_nest<double>(ctx, s, st.nest, dl, &checksum)
-                                                  : run_host_nest<float>(ctx, s, st.nest, dl, &checksum);
-        if (!ok) timed_out = true;
         const int w = written_array(st.nest);
+        int stream_to = -1;  // the later H2D of the array this nest writes, if its rows can be sent as they are produced
+        if (overlap_enabled) {
+          unsigned blocked = step_arrays(st);
+          for (int sj = si + 1; sj < plan.num_steps && e == cudaSuccess; ++sj) {
+            const mmx_plan_step& later = plan.steps[sj];
+            const unsigned touches = step_arrays(later);
+            if (later.kind == MMX_STEP_GPU && later.mode == MMX_MODE_GPU_NEST && (touches & blocked) == 0 && !issued[sj]) {
+              const Clock::time_point tj = Clock::now();
+              run_gpu_step(later);
+              issued[sj] = true;
+              s.stats.nest_s[later.nest] += since(tj);
+              continue;
+            }
+            if (later.kind == MMX_STEP_H2D && w >= 0 && later.array == w && stream_to < 0 && st.nest != MMX_NEST_TRACE) {
+              // nothing between here and there touched w: `blocked` holds it only because of this nest itself
+              bool clean = true;
+              for (int sk = si + 1; sk < sj; ++sk) clean = clean && (issued[sk] || (step_arrays(plan.steps[sk]) >> w & 1u) == 0);
+              if (clean) stream_to = sj;
+            }
+            blocked |= touches;
+          }
+        }
+        bool ok = true;
+        if (stream_to >= 0 && e == cudaSuccess) {
+          // one thread team per block: with many threads a block must stay long enough to pay for starting them
+          const std::size_t want = static_cast<std::size_t>(std::max(1, 16 / std::max(1, ctx->cfg.host_threads)));
+          const int blocks = static_cast<int>(std::min<std::size_t>(want, std::max<std::size_t>(1, n / 64)));
+          const std::size_t row_bytes = n * esz;
+          for (int blk = 0; blk < blocks && ok && e == cudaSuccess; ++blk) {
+            const int r0 = static_cast<int>(n * blk / blocks), r1 = static_cast<int>(n * (blk + 1) / blocks);
+            ok = ctx->cfg.dtype == MMX_F64 ? run_host_nest<double>(ctx, s, st.nest, r0, r1, dl, &checksum)
+                                           : run_host_nest<float>(ctx, s, st.nest, r0, r1, dl, &checksum);
+            if (ok)
+              e = cudaMemcpyAsync(static_cast<char*>(s.d_arr[w]) + row_bytes * r0, static_cast<const char*>(s.h_arr[w]) + row_bytes * r0,
+                                  row_bytes * (r1 - r0), cudaMemcpyHostToDevice, s.stream);
+          }
+          issued[stream_to] = true;
+          any_gpu = true;
+          if (w == MMX_ARRAY_A) s.planes_a_valid = false;
+          if (w == MMX_ARRAY_BT) s.planes_bt_valid = false;
+          if (w == MMX_ARRAY_B) s.b_colexp_valid = false;
+        } else {
+          ok = ctx->cfg.dtype == MMX_F64 ? run_host_nest<double>(ctx, s, st.nest, 0, static_cast<int>(n), dl, &checksum)
+                                         : run_host_nest<float>(ctx, s, st.nest, 0, static_cast<int>(n), dl, &checksum);
+        }
+        if (!ok) timed_out = true;
         if (w >= 0) {
           s.host_valid[w] = true;
-          s.dev_valid[w] = false;
+          s.dev_valid[w] = stream_to >= 0 && ok;  // streamed: valid on both sides, as after the plan's own H2D
           if (w == MMX_ARRAY_C) s.host_diag_only = false;
         }
         s.stats.host_s += since(ts);
         break;
       }
-      case MMX_STEP_GPU: {
-        any_gpu = true;
-        const int gene = gene_of(st.nest, st.mode);
-        if (st.mode == MMX_MODE_GPU_NEST) {
-          e = launch_gene_any(ctx, s, gene, IterRef{nullptr, 0});
-        } else {
-          e = run_train(ctx, s, gene, static_cast<long long>(st.launches), dl, &timed_out, &s.stats.graph_launches);
-        }
-        const int w = written_array(st.nest);
-        if (w >= 0) {
-          s.dev_valid[w] = true;
-          s.host_valid[w] = false;
-        }
-        if (st.nest == MMX_NEST_TRACE) sum_on_device = true;
-        break;
-      }
+      case MMX_STEP_GPU: run_gpu_step(st); break;
       case MMX_STEP_D2H_SUM:
         e = cudaMemcpyAsync(s.h_sum, s.d_sum, esz, cudaMemcpyDeviceToHost, s.stream);
         break;

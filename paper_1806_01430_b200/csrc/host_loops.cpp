@@ -23,7 +23,9 @@ void pin_self(int cpu) {
 }
 
 template <typename Body>
-bool for_rows(int n, const HostTeam& team, const Deadline& dl, int poll_every, Body body) {
+bool for_rows(int row0, int row1, const HostTeam& team, const Deadline& dl, int poll_every, Body body) {
+  const int n = row1 - row0;
+  if (n <= 0) return !dl.expired();
   int threads = team.threads;
   if (threads < 1) threads = 1;
   if (threads > n) threads = n;
@@ -38,13 +40,13 @@ bool for_rows(int n, const HostTeam& team, const Deadline& dl, int poll_every, B
     }
   };
   if (threads == 1) {
-    block(0, n);
+    block(row0, row1);
   } else {
     std::vector<std::thread> pool;
     pool.reserve(threads);
     for (int t = 0; t < threads; ++t) {
-      const int r0 = static_cast<int>(static_cast<long long>(n) * t / threads);
-      const int r1 = static_cast<int>(static_cast<long long>(n) * (t + 1) / threads);
+      const int r0 = row0 + static_cast<int>(static_cast<long long>(n) * t / threads);
+      const int r1 = row0 + static_cast<int>(static_cast<long long>(n) * (t + 1) / threads);
       pool.emplace_back([&, t, r0, r1] {
         if (team.cpus != nullptr && team.ncpus > 0) pin_self(team.cpus[t % team.ncpus]);
         block(r0, r1);
@@ -58,40 +60,40 @@ bool for_rows(int n, const HostTeam& team, const Deadline& dl, int poll_every, B
 }  // namespace
 
 template <typename T>
-bool host_init_a(T* a, int n, const HostTeam& team, const Deadline& dl) {
-  return for_rows(n, team, dl, 64, [=](int i) {
+bool host_init_a(T* a, int n, int row0, int row1, const HostTeam& team, const Deadline& dl) {
+  return for_rows(row0, row1, team, dl, 64, [=](int i) {
     T* row = a + static_cast<std::size_t>(i) * n;
     for (int j = 0; j < n; ++j) row[j] = static_cast<T>(i + j) / n;  // matmul.c:10
   });
 }
 
 template <typename T>
-bool host_init_b(T* b, int n, const HostTeam& team, const Deadline& dl) {
-  return for_rows(n, team, dl, 64, [=](int i) {
+bool host_init_b(T* b, int n, int row0, int row1, const HostTeam& team, const Deadline& dl) {
+  return for_rows(row0, row1, team, dl, 64, [=](int i) {
     T* row = b + static_cast<std::size_t>(i) * n;
     for (int j = 0; j < n; ++j) row[j] = static_cast<T>(i - j) / n;  // matmul.c:14
   });
 }
 
 template <typename T>
-bool host_zero_c(T* c, int n, const HostTeam& team, const Deadline& dl) {
-  return for_rows(n, team, dl, 64, [=](int i) {
+bool host_zero_c(T* c, int n, int row0, int row1, const HostTeam& team, const Deadline& dl) {
+  return for_rows(row0, row1, team, dl, 64, [=](int i) {
     T* row = c + static_cast<std::size_t>(i) * n;
     for (int j = 0; j < n; ++j) row[j] = static_cast<T>(0.0);  // matmul.c:18
   });
 }
 
 template <typename T>
-bool host_transpose(T* bt, const T* b, int n, const HostTeam& team, const Deadline& dl) {
-  return for_rows(n, team, dl, 16, [=](int i) {
+bool host_transpose(T* bt, const T* b, int n, int row0, int row1, const HostTeam& team, const Deadline& dl) {
+  return for_rows(row0, row1, team, dl, 16, [=](int i) {
     T* row = bt + static_cast<std::size_t>(i) * n;
     for (int j = 0; j < n; ++j) row[j] = b[static_cast<std::size_t>(j) * n + i];  // matmul.c:23
   });
 }
 
 template <typename T>
-bool host_matmul(T* c, const T* a, const T* bt, int n, const HostTeam& team, const Deadline& dl) {
-  return for_rows(n, team, dl, 1, [=](int i) {
+bool host_matmul(T* c, const T* a, const T* bt, int n, int row0, int row1, const HostTeam& team, const Deadline& dl) {
+  return for_rows(row0, row1, team, dl, 1, [=](int i) {
     T* crow = c + static_cast<std::size_t>(i) * n;
     const T* arow = a + static_cast<std::size_t>(i) * n;
     for (int j = 0; j < n; ++j) {
@@ -109,11 +111,11 @@ double host_trace(const T* c, int n) {
 }
 
 #define MMX_INSTANTIATE(T)                                                           \
-  template bool host_init_a<T>(T*, int, const HostTeam&, const Deadline&);                      \
-  template bool host_init_b<T>(T*, int, const HostTeam&, const Deadline&);                      \
-  template bool host_zero_c<T>(T*, int, const HostTeam&, const Deadline&);                      \
-  template bool host_transpose<T>(T*, const T*, int, const HostTeam&, const Deadline&);         \
-  template bool host_matmul<T>(T*, const T*, const T*, int, const HostTeam&, const Deadline&);  \
+  template bool host_init_a<T>(T*, int, int, int, const HostTeam&, const Deadline&);                      \
+  template bool host_init_b<T>(T*, int, int, int, const HostTeam&, const Deadline&);                      \
+  template bool host_zero_c<T>(T*, int, int, int, const HostTeam&, const Deadline&);                      \
+  template bool host_transpose<T>(T*, const T*, int, int, int, const HostTeam&, const Deadline&);         \
+  template bool host_matmul<T>(T*, const T*, const T*, int, int, int, const HostTeam&, const Deadline&);  \
   template double host_trace<T>(const T*, int);
 MMX_INSTANTIATE(double)
 MMX_INSTANTIATE(float)

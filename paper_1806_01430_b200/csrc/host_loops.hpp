@@ -26,12 +26,14 @@ struct HostTeam {
   int ncpus = 0;
 };
 
-// Each returns false when the deadline passed before the nest finished (rows are the unit of the check).
-template <typename T> bool host_init_a(T* a, int n, const HostTeam& team, const Deadline& dl);
-template <typename T> bool host_init_b(T* b, int n, const HostTeam& team, const Deadline& dl);
-template <typename T> bool host_zero_c(T* c, int n, const HostTeam& team, const Deadline& dl);
-template <typename T> bool host_transpose(T* bt, const T* b, int n, const HostTeam& team, const Deadline& dl);
-template <typename T> bool host_matmul(T* c, const T* a, const T* bt, int n, const HostTeam& team, const Deadline& dl);
+// Iterations [row0, row1) of the nest's outer loop (the whole nest is [0, n)): the executor runs a nest block by block when the
+// array it writes is needed on the device next, so that finished rows cross the bus while the later ones are still being computed.
+// Each returns false when the deadline passed before the block finished (rows are the unit of the check).
+template <typename T> bool host_init_a(T* a, int n, int row0, int row1, const HostTeam& team, const Deadline& dl);
+template <typename T> bool host_init_b(T* b, int n, int row0, int row1, const HostTeam& team, const Deadline& dl);
+template <typename T> bool host_zero_c(T* c, int n, int row0, int row1, const HostTeam& team, const Deadline& dl);
+template <typename T> bool host_transpose(T* bt, const T* b, int n, int row0, int row1, const HostTeam& team, const Deadline& dl);
+template <typename T> bool host_matmul(T* c, const T* a, const T* bt, int n, int row0, int row1, const HostTeam& team, const Deadline& dl);
 // matmul.c:30-32; the accumulator has the array's type, the result is widened for printf.
 template <typename T> double host_trace(const T* c, int n);
 
