@@ -306,7 +306,7 @@ def run_ours(args):
                     "form": form, "slice_products_per_term": products,
                     "achieved": ops, "peak": int8_peak, "unit": "TOP/s", "frac": ops / int8_peak,
                     "peak_inferred": int8_inferred, "frac_vs_inferred": ops / int8_inferred,
-                    "traffic": ncu_traffic("matmul_ozaki_auto", n), "ms_per_launch": msk, "share_of_step": msk * 1e-3 / (device_s / args.steps),
+                    "traffic": ncu_traffic("matmul_ozaki_auto_pair", n) or ncu_traffic("matmul_ozaki_auto", n), "ms_per_launch": msk, "share_of_step": msk * 1e-3 / (device_s / args.steps),
                     "effective_fp64_tflops": flops / (msk * 1e-3) / 1e12,
                     "nest": {"what": "gene 8 as the step runs it: the digit planes (written by the fill / transpose kernels when those run "
                                      "on the device, else two slice passes) + the contraction + the guarded FP64-pipe launch",
@@ -389,9 +389,11 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(plan.h2d_bytes), "d2h_bytes_per_step": int(plan.d2h_bytes),
                     "note": "host clock around mmx_measure (plan + 6 launches + checksum D2H + sync); this genome has no host-side inputs"},
             "e2e_mixed": mixed, "e2e_host_buffers": host_io,
-            # the plan counts one launch per offloaded nest; in FP64 auto mode gene 8 is four kernels (two slice passes, the
-            # tensor-core contraction, and the guarded FP64-pipe launch that exits at once)
-            "gpu_launches": (int(plan.kernel_launches) + (3 if (dtype == capi.F64 and n >= 1024) else 0)) * args.steps,
+            # the plan counts one launch per offloaded nest; in FP64 auto mode at N % 64 == 0 the individual is eight kernels: init-a
+            # (+ digit planes), init-b, its column exponents, zero-c, transpose (+ digit planes), the tensor-core contraction, the
+            # guarded FP64-pipe launch that exits at once, the trace (profiles/*_launches.csv)
+            "gpu_launches": (int(plan.kernel_launches) + (2 if (dtype == capi.F64 and n >= 1024 and n % 64 == 0) else
+                                                          3 if (dtype == capi.F64 and n >= 1024) else 0)) * args.steps,
             "clocks": clocks, "roofline": roof, "roofline_hbm": hbm_roof, "cpu_baseline": base,
             "checksum": checksum,
         }

@@ -68,6 +68,7 @@ struct Slot {
   bool fuse_planes = false;        // set per plan / per API call
   bool planes_a_valid = false, planes_bt_valid = false;
   bool b_colexp_valid = false;     // the exponents of bt's rows were written by the init-b kernel (closed form of its own output)
+  bool c_zero = false;             // the zero-c kernel filled c on the device and nothing has written c since (kCIsZero)
   std::map<int, Train> trains;  // by gene
   struct PlanGraph {
     cudaGraphExec_t exec = nullptr;
@@ -206,8 +207,12 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
       }
       return launch_fill2d<T>(FILL_INIT_B, b, n, row0, rows, s.cur);
     case 3: s.b_colexp_valid = false; return launch_fill_row<T>(FILL_INIT_B, b, n, iter, s.cur);
-    case 4: return launch_fill2d<T>(FILL_ZERO, c, n, row0, rows, s.cur);
-    case 5: return launch_fill_row<T>(FILL_ZERO, c, n, iter, s.cur);
+    case 4: {
+      const cudaError_t e = launch_fill2d<T>(FILL_ZERO, c, n, row0, rows, s.cur);
+      s.c_zero = e == cudaSuccess && row0 == 0 && rows == n;
+      return e;
+    }
+    case 5: s.c_zero = false; return launch_fill_row<T>(FILL_ZERO, c, n, iter, s.cur);
     case 6:
       s.planes_bt_valid = false;
       if (fuse && s.b_colexp_valid) {
@@ -222,6 +227,7 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
       if (variant == 0 && row0 == 0 && rows == n && s.oz_planes != nullptr) {
         if (s.planes_a_valid) variant |= kReuseOperandA;
         if (s.planes_bt_valid) variant |= kReuseOperandBt;
+        if (s.c_zero) variant |= kCIsZero;
         else s.b_colexp_valid = false;  // the slice pass of bt writes its own row exponents
       } else {
         s.b_colexp_valid = false;  // row / column blocks re-encode parts of the planes
@@ -229,10 +235,11 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
       // one consumer per encoding: the next launch of gene 8 encodes again unless a producer has rewritten the planes by then
       // (mmx_time_loop(8) therefore times the whole nest, slice passes included, whatever ran before)
       s.planes_a_valid = s.planes_bt_valid = false;
+      s.c_zero = false;
       return launch_matmul<T>(c, a, bt, n, row0, rows, 0, n, strict, variant, s.d_scratch, s.cur);
     }
-    case 9: return launch_gemv_row<T>(c, a, bt, n, iter, strict, s.cur);
-    case 10: return launch_dot<T>(c, a, bt, n, iter, strict, s.cur);
+    case 9: s.c_zero = false; return launch_gemv_row<T>(c, a, bt, n, iter, strict, s.cur);
+    case 10: s.c_zero = false; return launch_dot<T>(c, a, bt, n, iter, strict, s.cur);
     case 11: return launch_trace<T>(static_cast<T*>(s.d_sum), c, n, row0, rows, strict, s.cur);
     default: return cudaErrorInvalidValue;
   }
@@ -253,6 +260,7 @@ void begin_sequence(Slot& s, bool matmul_is_one_launch) {
   static const bool enabled = [] { const char* e = getenv("MMX_FUSE_PLANES"); return e == nullptr || atoi(e) != 0; }();
   s.fuse_planes = enabled && matmul_is_one_launch && s.oz_planes != nullptr;
   s.planes_a_valid = s.planes_bt_valid = s.b_colexp_valid = false;
+  s.c_zero = false;
 }
 
 // gene that serves `nest` in `mode`
@@ -546,6 +554,7 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const 
         if (st.array == MMX_ARRAY_A) s.planes_a_valid = false;
         if (st.array == MMX_ARRAY_BT) s.planes_bt_valid = false;
         if (st.array == MMX_ARRAY_B) s.b_colexp_valid = false;
+        if (st.array == MMX_ARRAY_C) s.c_zero = false;
         any_gpu = true;
         break;
       case MMX_STEP_D2H:
@@ -564,6 +573,7 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const 
       case MMX_STEP_H2D_DIAG:
         e = cudaMemcpy2DAsync(s.d_arr[st.array], (n + 1) * esz, s.h_arr[st.array], (n + 1) * esz, esz, n,
                               cudaMemcpyHostToDevice, s.stream);
+        if (st.array == MMX_ARRAY_C) s.c_zero = false;
         any_gpu = true;
         break;
       case MMX_STEP_CPU: {
@@ -609,6 +619,7 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const 
           if (w == MMX_ARRAY_A) s.planes_a_valid = false;
           if (w == MMX_ARRAY_BT) s.planes_bt_valid = false;
           if (w == MMX_ARRAY_B) s.b_colexp_valid = false;
+          if (w == MMX_ARRAY_C) s.c_zero = false;
         } else {
           ok = ctx->cfg.dtype == MMX_F64 ? run_host_nest<double>(ctx, s, st.nest, 0, static_cast<int>(n), dl, &checksum)
                                          : run_host_nest<float>(ctx, s, st.nest, 0, static_cast<int>(n), dl, &checksum);
@@ -1063,6 +1074,7 @@ MMX_API int mmx_upload_array(mmx_ctx* ctx, int slot, int array, const void* host
   if (array == MMX_ARRAY_A) s.planes_a_valid = false;
   if (array == MMX_ARRAY_BT) s.planes_bt_valid = false;
   if (array == MMX_ARRAY_B) s.b_colexp_valid = false;
+  if (array == MMX_ARRAY_C) s.c_zero = false;
   return MMX_OK;
 }
 

@@ -48,11 +48,23 @@ __device__ __forceinline__ void store_vec(T* dst, int i, int j0, T nn, T inv) {
 constexpr int kRowsPerThread = 8;
 
 // blockDim = (bx, by), bx*by = 256.  A block covers bx*V columns x by*kRowsPerThread rows.
+// colexp (init-b with the digit planes of bt to follow, else NULL): the threads of the first row block also write the digit
+// exponent of each of their COLUMNS of b (= rows of bt): |i - j| / N over a column j is largest at i = 0 or i = N - 1, so the
+// kernel knows it in closed form with its own arithmetic -- what transpose_tile<PLANES> needs before it can emit digits.
 template <typename T, int OP, bool POW2, int V>
-__global__ void __launch_bounds__(256) fill2d_kernel(T* __restrict__ dst, int n, int first_row, int row_limit, T nn, T inv) {
+__global__ void __launch_bounds__(256) fill2d_kernel(T* __restrict__ dst, int n, int first_row, int row_limit, T nn, T inv, int* __restrict__ colexp) {
   const int jv = blockIdx.x * blockDim.x + threadIdx.x;  // vector column
   const int j0 = jv * V;
   if (j0 >= n) return;
+  if (OP == FILL_INIT_B && colexp != nullptr && blockIdx.y == 0 && threadIdx.y == 0) {
+#pragma unroll
+    for (int q = 0; q < V; ++q) {
+      if (j0 + q >= n) break;
+      const double top = fabs(static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(0, j0 + q, nn, inv)));
+      const double bot = fabs(static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(n - 1, j0 + q, nn, inv)));
+      colexp[j0 + q] = oz_row_exponent(fmax(top, bot), false);
+    }
+  }
   const int row0 = first_row + (blockIdx.y * blockDim.y + threadIdx.y) * kRowsPerThread;
 #pragma unroll
   for (int r = 0; r < kRowsPerThread; ++r) {
@@ -108,20 +120,8 @@ __global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst,
   oz_guard_commit(lossy, top, P.guard, P.lossy_slot, P.top_slot, P.dirty_slot);
 }
 
-// ---- init-b + the digit exponent of every COLUMN of b (= row of bt) ------------------------------------------------------------------
-// |i - j| / N over a column j is largest at i = 0 or i = N - 1: a one-thread-per-column kernel behind the fill writes the exponents
-// the transpose kernel needs before it can emit the digits of bt.
-template <typename T, bool POW2>
-__global__ void __launch_bounds__(256) colexp_b_kernel(int* __restrict__ colexp, int n, T nn, T inv_n) {
-  const int j = blockIdx.x * 256 + threadIdx.x;
-  if (j >= n) return;
-  const double top = fabs(static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(0, j, nn, inv_n)));
-  const double bot = fabs(static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(n - 1, j, nn, inv_n)));
-  colexp[j] = oz_row_exponent(fmax(top, bot), false);
-}
-
 template <typename T, int OP, bool POW2, int V>
-cudaError_t fill2d_go(T* dst, int n, int row0, int rows, cudaStream_t stream) {
+cudaError_t fill2d_go(T* dst, int n, int row0, int rows, cudaStream_t stream, int* colexp = nullptr) {
   const int nvec = (n + V - 1) / V;
   int bx = 32;
   while (bx < 256 && bx < nvec) bx <<= 1;
@@ -130,7 +130,7 @@ cudaError_t fill2d_go(T* dst, int n, int row0, int rows, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   dim3 grid((nvec + bx - 1) / bx, (rows + by * kRowsPerThread - 1) / (by * kRowsPerThread));
   fill2d_kernel<T, OP, POW2, V><<<grid, block, 0, stream>>>(dst, n, row0, row0 + rows, static_cast<T>(n),
-                                                            static_cast<T>(1.0) / static_cast<T>(n));
+                                                            static_cast<T>(1.0) / static_cast<T>(n), colexp);
   return cudaGetLastError();
 }
 
@@ -199,11 +199,10 @@ cudaError_t launch_fill_a_planes(T* a, int n, const OzOperand& pa, cudaStream_t 
 
 template <typename T>
 cudaError_t launch_fill_b_colexp(T* b, int n, int* colexp, cudaStream_t stream) {
-  if (cudaError_t e = launch_fill2d<T>(FILL_INIT_B, b, n, 0, n, stream); e != cudaSuccess) return e;
-  const T nn = static_cast<T>(n), inv = static_cast<T>(1.0) / static_cast<T>(n);
-  if (is_pow2(n)) colexp_b_kernel<T, true><<<(n + 255) / 256, 256, 0, stream>>>(colexp, n, nn, inv);
-  else colexp_b_kernel<T, false><<<(n + 255) / 256, 256, 0, stream>>>(colexp, n, nn, inv);
-  return cudaGetLastError();
+  constexpr int W = vec_width<T>();
+  if (!ozaki_fusable(n) || n % W != 0) return cudaErrorInvalidValue;
+  if (is_pow2(n)) return fill2d_go<T, FILL_INIT_B, true, W>(b, n, 0, n, stream, colexp);
+  return fill2d_go<T, FILL_INIT_B, false, W>(b, n, 0, n, stream, colexp);
 }
 
 template cudaError_t launch_fill_a_planes<double>(double*, int, const OzOperand&, cudaStream_t);

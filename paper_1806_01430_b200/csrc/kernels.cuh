@@ -156,10 +156,15 @@ constexpr int kReuseOperands = 0x2000;
 // OR-ed into `variant` (auto mode): the digit planes, row exponents and guard words of bt are valid for this launch's columns -- the
 // kernel that produced bt wrote them (launch_transpose_planes).  kReuseOperandA | kReuseOperandBt == kReuseOperands in effect.
 constexpr int kReuseOperandBt = 0x4000;
+// OR-ed into `variant` (auto mode): every element of c this launch covers is +0 (the zero-c kernel ran and nothing has written c
+// since): the tensor-core epilogue then STORES its results instead of asking the L2 to add them to c (0 + v == v bit for bit; the
+// exact integer level sums never produce -0), which spares the read of c.  The FP64-pipe / split-TF32 fallbacks ignore it.
+constexpr int kCIsZero = 0x8000;
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0,
-                                int cols, int slices, cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false, bool reuse_bt = false);
+                                int cols, int slices, cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false, bool reuse_bt = false,
+                                bool c_zero = false);
 cudaError_t launch_matmul_ozaki_f32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                    cudaStream_t stream, int** guard_out, bool reuse_a = false, bool reuse_bt = false);
+                                    cudaStream_t stream, int** guard_out, bool reuse_a = false, bool reuse_bt = false, bool c_zero = false);
 // device word in `scratch` where the auto launch records the form it ran: 2 .. 7 slices, 0 = left to the FP64 pipe
 int* matmul_ozaki_form_word(void* scratch, int n);
 // gene 9: row i of the same (GEMV against bt)

@@ -519,7 +519,8 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
                                   bool strict, int variant, void* scratch, cudaStream_t stream) {
   const bool reuse_a = (variant & (kReuseOperandA | kReuseOperands)) != 0;
   const bool reuse_bt = (variant & (kReuseOperandBt | kReuseOperands)) != 0;
-  variant &= ~(kReuseOperandA | kReuseOperandBt | kReuseOperands);
+  const bool c_zero = (variant & kCIsZero) != 0;
+  variant &= ~(kReuseOperandA | kReuseOperandBt | kReuseOperands | kCIsZero);
   // tensor cores (INT8 slice products, matmul_ozaki.cu): on request
   if (!strict && scratch != nullptr && variant >= 40 && variant <= 45)  // 40 .. 45: 7 .. 2 slices
     return launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 47 - variant, stream, nullptr, reuse_a);
@@ -530,7 +531,7 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
   // pipe.  All three kernels are enqueued; a device guard written by the slice pass lets exactly one of them run.
   if (!strict && variant == 0 && scratch != nullptr && n >= kOzMinN && dmma_ok) {
     int* lossy = nullptr;
-    if (cudaError_t e = launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 7, stream, &lossy, reuse_a, reuse_bt); e != cudaSuccess) return e;
+    if (cudaError_t e = launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 7, stream, &lossy, reuse_a, reuse_bt, c_zero); e != cudaSuccess) return e;
     return dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, stream, lossy);
   }
   if (variant == 0) variant = 4;  // the FP64 pipe: DMMA, tile by size (best of the tuning points, profiles/)
@@ -565,14 +566,15 @@ cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int 
                                  bool strict, int variant, void* scratch, cudaStream_t stream) {
   const bool reuse_a = (variant & (kReuseOperandA | kReuseOperands)) != 0;
   const bool reuse_bt = (variant & (kReuseOperandBt | kReuseOperands)) != 0;
-  variant &= ~(kReuseOperandA | kReuseOperandBt | kReuseOperands);
+  const bool c_zero = (variant & kCIsZero) != 0;
+  variant &= ~(kReuseOperandA | kReuseOperandBt | kReuseOperands | kCIsZero);
   // auto, large matrices: the INT8 tensor cores exactly when their digit products are error-free for the operands at hand (one
   // rounding to float at the end: closer to the exact product than any FP32 accumulation), split TF32 otherwise -- the same
   // device-side guard as in FP64 (matmul_ozaki.cu); the split-TF32 launches read it and leave when the product has been taken
   if (!strict && scratch != nullptr && variant == 0 && fp32_int8_enabled(n)) {
     int* guard = nullptr;
     void* planes = static_cast<char*>(scratch) + fp32_int8_scratch_offset(n);
-    if (cudaError_t e = launch_matmul_ozaki_f32(c, a, bt, planes, n, row0, rows, col0, cols, stream, &guard, reuse_a, reuse_bt); e != cudaSuccess) return e;
+    if (cudaError_t e = launch_matmul_ozaki_f32(c, a, bt, planes, n, row0, rows, col0, cols, stream, &guard, reuse_a, reuse_bt, c_zero); e != cudaSuccess) return e;
     // (a fallback launch always re-splits its rows of a: the earlier column block may have gone the INT8 way)
     return launch_matmul_3xtf32(c, a, bt, scratch, n, row0, rows, col0, cols, false, stream, false, guard);
   }

@@ -315,6 +315,7 @@ struct OzPArgs {
   const int *exp_a, *exp_b;
   int n, kq, row0, rows, col0, cols, group;
   long long group_l2_bytes;  // budget for a raster group's rows of a (0: default; MMX_OZ_GROUP_MB overrides -- tuning hook)
+  int c_zero;  // every element of c this launch covers is +0: results are stored, not added (kCIsZero)
   int debug;  // MMX_OZ_DEBUG (rate probes, results are WRONG): 1 the producer signals stages without loading them, 2 the epilogue drops phase B
 };
 
@@ -672,7 +673,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
           if (g.debug & 512) __nanosleep(jj == 0 ? 200u + 400u * (warp - 2) : 2500u);
           if (g.debug & 1024) __nanosleep(jj == 0 ? 100u + 200u * (warp - 2) : 1200u);
           if (lane == 0 && !(g.debug & 8)) {
-            if (g.debug & 4) tma_store_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
+            if (g.c_zero || (g.debug & 4)) tma_store_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
             else if (g.debug & 256) tma_reduce_add_2d_hint(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32, l2_policy_evict_first());
             else tma_reduce_add_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
             tma_store_commit();
@@ -1058,7 +1059,8 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_reduce_add_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
+          if (g.c_zero) tma_store_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
+          else tma_reduce_add_2d(map_c, slab, g.col0 + n_tile + j * 16, m_base + q * 32);
           tma_store_commit();
         }
       }
@@ -1485,7 +1487,8 @@ bool make_c_map(CUtensorMap* map, void* c, size_t elem, int n, int rows_end, int
 // slices == 0: the auto kernel (reads the guard, records the form it ran in guard[4]); otherwise the fixed triangular form over
 // the first `slices` of `planes` planes
 template <typename CT = double>
-cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, int n, int row0, int rows, int col0, int cols, cudaStream_t stream) {
+cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, int n, int row0, int rows, int col0, int cols, cudaStream_t stream,
+                                bool c_zero = false) {
   const OzLayout L(scratch, n, planes);
   const bool c_by_tma = (n * sizeof(CT)) % 16 == 0;  // row pitch a multiple of 16 bytes
   if (slices == 0 && !c_by_tma) return cudaErrorInvalidValue;
@@ -1514,6 +1517,7 @@ cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, in
   g.group = raster_group(OZ_BM, static_cast<size_t>(L.kq));
   static const long long group_mb = [] { const char* e = getenv("MMX_OZ_GROUP_MB"); return e ? atoll(e) : 0ll; }();
   g.group_l2_bytes = group_mb << 20;
+  g.c_zero = (c_zero && c_by_tma) ? 1 : 0;  // (the register epilogue adds: it reads c anyway)
   static const int debug = [] { const char* e = getenv("MMX_OZ_DEBUG"); return e ? atoi(e) : 0; }();
   g.debug = debug;
   // the grid covers the 64-wide tiling (the forms with 128-wide tiles leave the surplus CTAs without a tile)
@@ -1634,12 +1638,12 @@ size_t matmul_ozaki_scratch_bytes(int n) {
 // value rounded once, added by a FLOAT32 TMA reduction).  *guard_out receives the guard; the caller enqueues the split-TF32 path
 // under ozaki_pick_form_f32(...) == 0.
 cudaError_t launch_matmul_ozaki_f32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                    cudaStream_t stream, int** guard_out, bool reuse_a, bool reuse_bt) {
+                                    cudaStream_t stream, int** guard_out, bool reuse_a, bool reuse_bt, bool c_zero) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr || guard_out == nullptr || n % 4 != 0) return cudaErrorInvalidValue;
   *guard_out = OzLayout(scratch, n, 7).guard;
   if (cudaError_t e = oz_slices<7, float>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a, reuse_bt); e != cudaSuccess) return e;
-  return oz_persist_contract<float>(c, scratch, 7, 0, n, row0, rows, col0, cols, stream);
+  return oz_persist_contract<float>(c, scratch, 7, 0, n, row0, rows, col0, cols, stream, c_zero);
 }
 
 OzOperand matmul_ozaki_operand(void* scratch, int n, int which) {
@@ -1658,7 +1662,7 @@ OzOperand matmul_ozaki_operand(void* scratch, int n, int which) {
 int* matmul_ozaki_form_word(void* scratch, int n) { return scratch == nullptr ? nullptr : OzLayout(scratch, n, 7).guard + 4; }
 
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                int slices, cudaStream_t stream, int** guard_out, bool reuse_a, bool reuse_bt) {
+                                int slices, cudaStream_t stream, int** guard_out, bool reuse_a, bool reuse_bt, bool c_zero) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr) return cudaErrorInvalidValue;
   // MMX_OZ_LEGACY=1: the one-tile-per-CTA kernels of the first version (A/B comparison, tools/ozaki_cluster_sweep.sh)
@@ -1669,7 +1673,7 @@ cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, vo
     *guard_out = OzLayout(scratch, n, 7).guard;
     if (!(reuse_a && reuse_bt))  // both reused: the digit planes and the guard stand as their producers left them
       if (cudaError_t e = oz_slices<7>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a, reuse_bt); e != cudaSuccess) return e;
-    if (!legacy) return oz_persist_contract(c, scratch, 7, 0, n, row0, rows, col0, cols, stream);
+    if (!legacy) return oz_persist_contract(c, scratch, 7, 0, n, row0, rows, col0, cols, stream, c_zero);
     if (cudaError_t e = oz_contract<6, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true); e != cudaSuccess) return e;
     return oz_contract<7, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true);
   }
