@@ -284,7 +284,7 @@ def run_ours(args):
         peaks, peaks_kind = load_measured_peaks()
         ms8 = ctx.time_loop(8, 5, True)
         ach = flops / (ms8 * 1e-3) / 1e12
-        share = ms8 * 1e-3 / (device_s / args.steps)
+        share_ms8 = ms8 * 1e-3 / (device_s / args.steps)
         form = ctx.gene8_form() if dtype == capi.F64 else -1
         if form > 0:
             # auto mode picked an INT8 tensor-core form on the device (mmx_gene8_form: 100 SA + 10 SB + levels): digits a_1..a_SA
@@ -308,11 +308,12 @@ def run_ours(args):
                     "peak_inferred": int8_inferred, "frac_vs_inferred": ops / int8_inferred,
                     "traffic": ncu_traffic("matmul_ozaki_auto_pair", n) or ncu_traffic("matmul_ozaki_auto", n), "ms_per_launch": msk, "share_of_step": msk * 1e-3 / (device_s / args.steps),
                     "effective_fp64_tflops": flops / (msk * 1e-3) / 1e12,
-                    "nest": {"what": "gene 8 as the step runs it: the digit planes (written by the fill / transpose kernels when those run "
-                                     "on the device, else two slice passes) + the contraction + the guarded FP64-pipe launch",
-                             "ms": ms8, "achieved": ops_nest, "frac": ops_nest / int8_peak, "share_of_step": share,
-                             "effective_fp64_tflops": ach,
-                             "vs_fp64_pipe_peak": ach / capi.peak_probe(capi.PEAK_FP64_FMA, local_rank)},
+                    "nest_standalone": {"what": "gene 8 launched by itself (mmx_time_loop): its own two slice passes + the contraction + the guarded "
+                                                "FP64-pipe launch -- what a genome pays whose a / bt do not come from the device's fill / transpose "
+                                                "kernels; in the timed step those kernels write the digit planes and gene 8 is the contraction alone",
+                                        "ms": ms8, "achieved": ops_nest, "frac": ops_nest / int8_peak,
+                                        "effective_fp64_tflops": ach,
+                                        "vs_fp64_pipe_peak": ach / capi.peak_probe(capi.PEAK_FP64_FMA, local_rank)},
                     "peak_source": "tcgen05.mma.kind::i8 issue peak measured in this run by csrc/peaks.cu (M=128 x N=256 instructions back to back "
                                    "on operands resident in shared memory, one issuing thread per SM); peak_inferred = twice "
                                    "MEASURED_PEAKS.json bf16_tflops (cuBLAS bf16, loads included); achieved counts the INT8 slice products "
@@ -322,7 +323,7 @@ def run_ours(args):
             roof = {"bound": "tensor", "pipe": "fp64 (DMMA.8x8x4 via mma.sync)" if dtype == capi.F64 else "fp32 (FFMA)",
                     "kernel": "matmul_nt (gene 8)", "achieved": ach, "peak": pipe_peak, "unit": "TFLOP/s", "frac": ach / pipe_peak,
                     "traffic": ncu_traffic("matmul_dmma" if dtype == capi.F64 else "matmul_3xtf32s", n), "ms_per_launch": ms8,
-                    "share_of_step": share,
+                    "share_of_step": share_ms8,
                     "peak_source": "FMA-issue peak of the same pipe measured in this run by csrc/peaks.cu "
                                    "(MEASURED_PEAKS.json carries only HBM and bf16 figures)"}
         ms6 = ctx.time_loop(6, 10, True)
