@@ -488,8 +488,11 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const 
   s.host_diag_only = false;
   s.stats.host_s = 0.0;
   {
+    // the box's load matters to plans with host-side nests; an all-device plan does not pay the /proc read (microseconds per run)
+    bool host_work = false;
+    for (int si = 0; si < plan.num_steps; ++si) host_work = host_work || plan.steps[si].kind == MMX_STEP_CPU;
     double load = 0.0;
-    s.stats.host_loadavg = getloadavg(&load, 1) == 1 ? load : -1.0;
+    s.stats.host_loadavg = (host_work && getloadavg(&load, 1) == 1) ? load : -1.0;
   }
   s.stats.host_cpus = static_cast<int32_t>(s.cpus.size());
   s.stats.host_first_cpu = s.cpus.empty() ? -1 : s.cpus.front();
@@ -696,7 +699,12 @@ int measure_on_slot(mmx_ctx* ctx, int slot, const std::uint8_t* bits, std::size_
   }
   Slot& s = *ctx->slots[slot];
   std::lock_guard<std::mutex> guard(s.mu);
-  const ScopedAffinity pinned(s.cpus);  // the slot's own CPUs: launches, host loops and their thread team
+  // the slot's own CPUs for the host loops and their thread team; a plan without host-side nests has nothing to isolate
+  // and skips the three affinity system calls
+  bool host_work = false;
+  for (int si = 0; si < plan.num_steps; ++si) host_work = host_work || plan.steps[si].kind == MMX_STEP_CPU;
+  static const std::vector<int> no_cpus;
+  const ScopedAffinity pinned(host_work ? s.cpus : no_cpus);
   MMX_CUDA(ctx, cudaSetDevice(s.device));
   // allocation is outside the timed region: host mirrors for every array a step touches on the host
   for (int si = 0; si < plan.num_steps; ++si) {

@@ -27,7 +27,10 @@ __device__ __forceinline__ int oz_row_exponent(double m, bool bad) { return (m >
 // 1 / 2^e would overflow: both are flagged as lossy by the caller through `tiny` / `bad`)
 __device__ __forceinline__ double oz_row_scale(int e, bool live, bool bad, bool* tiny) {
   *tiny = e < -970;
-  return (live && !bad && !*tiny) ? scalbn(1.0, -e) : 0.0;
+  if (!(live && !bad && !*tiny)) return 0.0;
+  // 2^-e is a normal number for e <= 1022: two integer operations instead of scalbn's general path (the fused producers compute
+  // this once per row AND thread)
+  return e <= 1022 ? oz_pow2(-e) : scalbn(1.0, -e);
 }
 
 // The digits of W (2 or 4) consecutive elements v[0..W) of one row, starting at column k0 (a multiple of W), packed W to a store.
