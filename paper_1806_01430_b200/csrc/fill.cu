@@ -83,38 +83,67 @@ __global__ void __launch_bounds__(256) fill_row_kernel(T* __restrict__ dst, int 
 inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 
 // ---- init-a + the digit planes of a (gene 0 fused with the encoding gene 8 needs; ozaki_digits.cuh) -----------------------------
-// A CTA covers 8 rows x 1024 columns; a thread owns 4 consecutive columns of each of its 8 rows: it stores them (128-bit stores) and,
-// from the same registers, their 7-bit digits (one 32-bit store per plane).  The row exponent needs the row's largest magnitude:
-// (i + j) / N is non-negative and grows with j, so it is the row's last element -- every thread computes it for itself.
+// A CTA covers 8 rows x 1024 columns.  Per row a thread owns two 16-byte pieces, half a CTA-row apart, so that every store
+// instruction of a warp is one contiguous run of whole sectors (a thread owning 32 consecutive bytes would write each sector in two
+// halves, from two instructions): it stores them and, from the same registers, their 7-bit digits (16 / 32 bits per plane and
+// piece).  The row exponent needs the row's largest magnitude: (i + j) / N is non-negative and grows with j, so it is the row's
+// last element -- every thread computes it for itself.
 template <typename T, bool POW2>
 __global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst, int n, T nn, T inv_n, OzOperand P) {
-  const int j0 = (blockIdx.x * 256 + threadIdx.x) * 4;
+  constexpr int W = 16 / sizeof(T);          // elements per piece: 2 doubles / 4 floats
+  constexpr int PIECES = 4 / W;              // pieces per thread and row: 4 elements either way
+  const int c0 = blockIdx.x * 1024 + threadIdx.x * W;   // piece q starts at column c0 + q * 256 * W
   const int i0 = blockIdx.y * kRowsPerThread;
   const int dirty = P.guard[P.dirty_slot];
   int lossy = 0, top = 0;
-  if (j0 < n) {
+  if (c0 < n) {
+    // pass 1, straight-line over the thread's 8 rows: the values, their stores, the row exponents and the first two digit levels
+    // (independent FP64 chains in one basic block); `more` collects the rows that have something below the second digit
+    unsigned more = 0;
 #pragma unroll
     for (int r = 0; r < kRowsPerThread; ++r) {
-      const int i = i0 + r;
-      if (i >= n) break;
-      T x[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) x[q] = fill_value<T, FILL_INIT_A, POW2>(i, j0 + q, nn, inv_n);
-      T* at = dst + static_cast<size_t>(i) * n + j0;
-      if constexpr (sizeof(T) == 8) {
-        *reinterpret_cast<double2*>(at) = make_double2(x[0], x[1]);
-        *reinterpret_cast<double2*>(at + 2) = make_double2(x[2], x[3]);
-      } else {
-        *reinterpret_cast<float4*>(at) = make_float4(x[0], x[1], x[2], x[3]);
-      }
+      const int i = i0 + r;  // (n is a multiple of 64 here: every row of the block exists -- no test, one basic block)
       const double m = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, n - 1, nn, inv_n));
       const int e = oz_row_exponent(m, false);
       bool tiny;
       const double inv = oz_row_scale(e, true, false, &tiny);
       lossy |= tiny;
-      if (j0 == 0) P.exps[i] = e;
-      const double v[4] = {static_cast<double>(x[0]), static_cast<double>(x[1]), static_cast<double>(x[2]), static_cast<double>(x[3])};
-      oz_emit<7, 4>(v, inv, false, dirty, P.planes + static_cast<size_t>(i) * P.kq, P.plane, j0, lossy, top);
+      if (c0 == 0) P.exps[i] = e;
+      signed char* drow = P.planes + static_cast<size_t>(i) * P.kq;
+#pragma unroll
+      for (int q = 0; q < PIECES; ++q) {
+        const int j0 = c0 + q * 256 * W;
+        T x[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) x[w] = fill_value<T, FILL_INIT_A, POW2>(i, j0 + w, nn, inv_n);
+        T* at = dst + static_cast<size_t>(i) * n + j0;
+        double v[W];
+#pragma unroll
+        for (int w = 0; w < W; ++w) v[w] = static_cast<double>(x[w]);
+        if constexpr (sizeof(T) == 8) *reinterpret_cast<double2*>(at) = make_double2(x[0], x[1]);
+        else *reinterpret_cast<float4*>(at) = make_float4(x[0], x[1], x[2], x[3]);
+        int top2;
+        const bool left = oz_emit_first_two<W>(v, inv, drow, P.plane, j0, top2);
+        top = max(top, top2);
+        more |= (left ? 1u : 0u) << r;
+      }
+    }
+    // pass 2 (rare): rows with longer elements, or planes beyond the second that earlier launches have used and that must be zeroed
+    if (more != 0 || dirty > 2) {
+      for (int r = 0; r < kRowsPerThread; ++r) {
+        if (!(more >> r & 1u) && dirty <= 2) continue;
+        const int i = i0 + r;
+        const double m = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, n - 1, nn, inv_n));
+        bool tiny;
+        const double inv = oz_row_scale(oz_row_exponent(m, false), true, false, &tiny);
+        for (int q = 0; q < PIECES; ++q) {
+          const int j0 = c0 + q * 256 * W;
+          double v[W];
+#pragma unroll
+          for (int w = 0; w < W; ++w) v[w] = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, j0 + w, nn, inv_n));
+          oz_emit<7, W>(v, inv, false, dirty, P.planes + static_cast<size_t>(i) * P.kq, P.plane, j0, lossy, top);
+        }
+      }
     }
   }
   oz_guard_commit(lossy, top, P.guard, P.lossy_slot, P.top_slot, P.dirty_slot);

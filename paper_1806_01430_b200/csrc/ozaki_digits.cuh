@@ -85,6 +85,39 @@ __device__ __forceinline__ void oz_emit(const double (&v)[W], double inv, bool b
   }
 }
 
+// The first two digit levels of W consecutive elements, straight-line: no early exits, both planes stored unconditionally, so that a
+// caller that encodes several rows per thread gives the compiler ONE basic block of independent FP64 chains (the walk of oz_emit is
+// a chain of dependent FP64 operations per element and level with a branch after each level; on B200 those are long-latency
+// operations, and the producers that used oz_emit row by row spent half their issue slots waiting on them -- ncu, r2r_producers).
+// Returns true when something is left below the second digit: the caller then runs oz_emit on the same elements (rare path; it
+// rewrites the two planes with the same digits and continues).  top2: 0 / 1 / 2 = highest non-zero digit among the two.
+template <int W>
+__device__ __forceinline__ bool oz_emit_first_two(const double (&v)[W], double inv, signed char* __restrict__ drow, size_t plane, int k0, int& top2) {
+  static_assert(W == 2 || W == 4, "digits are packed two or four to a store");
+  int word0 = 0, word1 = 0;
+  bool left = false;
+#pragma unroll
+  for (int q = 0; q < W; ++q) {
+    double rem = v[q] * inv;
+    const double s0 = fma(rem, 64.0, 6755399441055744.0);                 // digit 1: unit 2^-6
+    rem = fma(-(s0 - 6755399441055744.0), 0.015625, rem);
+    const double s1 = fma(rem, 8192.0, 6755399441055744.0);               // digit 2: unit 2^-13
+    rem = fma(-(s1 - 6755399441055744.0), 0.0001220703125, rem);
+    word0 |= (__double2loint(s0) & 0xff) << (8 * q);
+    word1 |= (__double2loint(s1) & 0xff) << (8 * q);
+    left = left || rem != 0.0;
+  }
+  if constexpr (W == 4) {
+    *reinterpret_cast<int*>(drow + k0) = word0;
+    *reinterpret_cast<int*>(drow + plane + k0) = word1;
+  } else {
+    *reinterpret_cast<unsigned short*>(drow + k0) = static_cast<unsigned short>(word0);
+    *reinterpret_cast<unsigned short*>(drow + plane + k0) = static_cast<unsigned short>(word1);
+  }
+  top2 = word1 != 0 ? 2 : (word0 != 0 ? 1 : 0);
+  return left;
+}
+
 // End of a CTA's work on an operand: fold the threads' lossy / top into the guard words (every thread of a 256-thread CTA calls).
 // The words are read first: after a few CTAs nobody needs the atomic any more.
 __device__ __forceinline__ void oz_guard_commit(int lossy, int top, int* __restrict__ guard, int lossy_slot, int top_slot, int dirty_slot) {

@@ -52,6 +52,16 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
   const int in_col0 = first_row + blockIdx.x * kTile;   // cols of b  == rows of bt
   const int tid = threadIdx.x;
 
+  // PLANES: what phase 2 needs from global memory besides the tile is requested first, so that it arrives with the tile
+  constexpr int kSteps = kTile * MB / 256;
+  int row_exp[PLANES ? kSteps : 1];
+  int dirty = 0;
+  if constexpr (PLANES) {
+    dirty = P.guard[P.dirty_slot];
+#pragma unroll
+    for (int k = 0; k < kSteps; ++k) row_exp[k] = P.exps[in_col0 + (tid + 256 * k) / MB];
+  }
+
   // phase 1: micro-blocks, lanes along the input row (coalesced 128-bit loads)
 #pragma unroll
   for (int mb = tid; mb < MB * MB; mb += 256) {
@@ -73,38 +83,75 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
 
   // phase 2: lanes along the output row (coalesced 128-bit stores)
   int lossy = 0, top = 0;
-  int dirty = 0;
-  if constexpr (PLANES) dirty = P.guard[P.dirty_slot];
+  constexpr int STEPS = kTile * MB / 256;  // pieces per thread
+  if constexpr (PLANES) {
+    // the exponents of this thread's rows of bt and the dirty mark were requested before the tile was loaded (below): nothing in
+    // the store loop waits on global memory.  Pass 1 is straight-line: store the piece, walk its first two digit levels
+    // (oz_emit_first_two: independent FP64 chains, no branches); pass 2 (rare) re-reads from the tile the pieces that have more.
+    unsigned more = 0;
 #pragma unroll
-  for (int v = tid; v < kTile * MB; v += 256) {
-    const int out_row = v / MB;
-    const int chunk = v % MB;
-    const VT val = tile[out_row * MB + (chunk ^ ((out_row / V) & 7))];
-    const size_t at = static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V;
-    if constexpr (PUSH) {
-      for (int d = 0; d < peers.count; ++d) *reinterpret_cast<VT*>(static_cast<T*>(peers.p[d]) + at) = val;
-    } else {
-      *reinterpret_cast<VT*>(bt + at) = val;
-    }
-    if constexpr (PLANES) {
-      // the V elements just stored, as digits: V bytes per plane and thread, a warp covers 64 (FP64) / 128 (FP32) contiguous bytes
-      const int row = in_col0 + out_row;  // row of bt
+    for (int k = 0; k < STEPS; ++k) {
+      const int v = tid + 256 * k;
+      const int out_row = v / MB, chunk = v % MB;
+      const VT val = tile[out_row * MB + (chunk ^ ((out_row / V) & 7))];
+      *reinterpret_cast<VT*>(bt + static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V) = val;
       bool tiny;
-      const double inv = oz_row_scale(P.exps[row], true, false, &tiny);
-      lossy |= tiny;
-      signed char* drow = P.planes + static_cast<size_t>(row) * P.kq;
+      const double inv = oz_row_scale(row_exp[k], true, false, &tiny);
+      signed char* drow = P.planes + static_cast<size_t>(in_col0 + out_row) * P.kq;
+      int top2;
+      bool left;
       if constexpr (V == 2) {
         const double e2[2] = {val.x, val.y};
-        lossy |= !isfinite(val.x) | !isfinite(val.y);
-        oz_emit<7, 2>(e2, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
+        // not finite, or beyond what the exponent covers (it cannot happen while the executor's flags are right): cut
+        left = tiny || !(fabs(val.x) * inv < 1.0) || !(fabs(val.y) * inv < 1.0);
+        left = oz_emit_first_two<2>(e2, inv, drow, P.plane, in_row0 + chunk * V, top2) || left;
       } else {
         const double e4[4] = {static_cast<double>(val.x), static_cast<double>(val.y), static_cast<double>(val.z), static_cast<double>(val.w)};
-        lossy |= !isfinite(val.x) | !isfinite(val.y) | !isfinite(val.z) | !isfinite(val.w);
-        oz_emit<7, 4>(e4, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
+        left = tiny;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) left = left || !(fabs(e4[q]) * inv < 1.0);
+        left = oz_emit_first_two<4>(e4, inv, drow, P.plane, in_row0 + chunk * V, top2) || left;
+      }
+      top = max(top, top2);
+      more |= (left ? 1u : 0u) << k;
+    }
+    if (more != 0 || dirty > 2) {
+      for (int k = 0; k < STEPS; ++k) {
+        if (!(more >> k & 1u) && dirty <= 2) continue;
+        const int v = tid + 256 * k;
+        const int out_row = v / MB, chunk = v % MB;
+        const VT val = tile[out_row * MB + (chunk ^ ((out_row / V) & 7))];
+        bool tiny;
+        const double inv = oz_row_scale(row_exp[k], true, false, &tiny);
+        lossy |= tiny;
+        signed char* drow = P.planes + static_cast<size_t>(in_col0 + out_row) * P.kq;
+        if constexpr (V == 2) {
+          const double e2[2] = {val.x, val.y};
+          lossy |= !(fabs(val.x) * inv < 1.0) | !(fabs(val.y) * inv < 1.0);
+          oz_emit<7, 2>(e2, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
+        } else {
+          const double e4[4] = {static_cast<double>(val.x), static_cast<double>(val.y), static_cast<double>(val.z), static_cast<double>(val.w)};
+#pragma unroll
+          for (int q = 0; q < 4; ++q) lossy |= !(fabs(e4[q]) * inv < 1.0);
+          oz_emit<7, 4>(e4, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
+        }
+      }
+    }
+    oz_guard_commit(lossy, top, P.guard, P.lossy_slot, P.top_slot, P.dirty_slot);
+  } else {
+#pragma unroll
+    for (int v = tid; v < kTile * MB; v += 256) {
+      const int out_row = v / MB;
+      const int chunk = v % MB;
+      const VT val = tile[out_row * MB + (chunk ^ ((out_row / V) & 7))];
+      const size_t at = static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V;
+      if constexpr (PUSH) {
+        for (int d = 0; d < peers.count; ++d) *reinterpret_cast<VT*>(static_cast<T*>(peers.p[d]) + at) = val;
+      } else {
+        *reinterpret_cast<VT*>(bt + at) = val;
       }
     }
   }
-  if constexpr (PLANES) oz_guard_commit(lossy, top, P.guard, P.lossy_slot, P.top_slot, P.dirty_slot);
 }
 
 // Any n: 32x32 tile, scalar accesses, +1 padding.  block = (32, 8).
