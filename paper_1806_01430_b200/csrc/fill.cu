@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst,
 #pragma unroll
       for (int q = 0; q < PIECES; ++q) {
         const int j0 = c0 + q * 256 * W;
+        if (q > 0 && j0 >= n) break;  // the last CTA of a row when n is not a multiple of 1024 (pieces never straddle the edge)
         T x[W];
 #pragma unroll
         for (int w = 0; w < W; ++w) x[w] = fill_value<T, FILL_INIT_A, POW2>(i, j0 + w, nn, inv_n);
@@ -138,6 +139,7 @@ __global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst,
         const double inv = oz_row_scale(oz_row_exponent(m, false), true, false, &tiny);
         for (int q = 0; q < PIECES; ++q) {
           const int j0 = c0 + q * 256 * W;
+          if (j0 >= n) break;
           double v[W];
 #pragma unroll
           for (int w = 0; w < W; ++w) v[w] = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, j0 + w, nn, inv_n));
