@@ -107,10 +107,11 @@ typedef struct mmx_config {
   int32_t host_threads;     /* threads for CPU-mapped nests; 1 = the reference program         */
   int32_t launch_batching;  /* 1: inner-loop launch trains are submitted as CUDA graphs        */
   int32_t matmul_variant;   /* gene-8 kernel: 0 auto (below N = 1024: DMMA in FP64, FFMA in FP32; from there the INT8 tensor cores
-                             * whenever exact 7-bit digit products give the error-free result, in the cheapest digit-pair form
+                             * whenever exact 7-bit digit products lose nothing of the product, in the cheapest digit-pair form
                              * that does, chosen on the device from the operands -- the application's inputs at N = 2^p qualify
-                             * with 2 x 2 .. 3 x 3 pairs -- and otherwise DMMA in FP64, tcgen05 split-TF32 with compensated
-                             * accumulation in FP32); 1 first SIMT kernel; 2, 4-13 DMMA tile shapes (FP64);
+                             * with 2 x 2 .. 3 x 3 pairs; the result is the exact product rounded once for forms of up to four
+                             * levels and faithfully rounded (<= 1 ulp, exact when it fits 53 bits) beyond -- and otherwise DMMA in
+                             * FP64, tcgen05 split-TF32 with compensated accumulation in FP32); 1 first SIMT kernel; 2, 4-13 DMMA tile shapes (FP64);
                              * 20, 22 SIMT tile shapes; 30 FP32 tcgen05 split-TF32 at any N % 4 == 0; 31 its wide-tile
                              * uncompensated form; 40 FP64 on the tcgen05 INT8 tensor cores with 7 exact 7-bit slices per operand
                              * whatever the operands (error <= 2e-14 K max|a| max|b|), 41 .. 45 the same with 6 .. 2 slices */

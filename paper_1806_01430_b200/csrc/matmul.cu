@@ -526,9 +526,12 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
     return launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 47 - variant, stream, nullptr, reuse_a);
   const bool dmma_ok = n % 2 == 0 && col0 % 2 == 0 && cols % 2 == 0;  // 16-byte aligned double2 accesses of c
   // auto: the INT8 tensor cores whenever their 7-bit slices reproduce every operand element exactly and every non-zero digit
-  // pair is kept (then the result is the error-free product rounded once -- bit-identical to the CPU program on the
-  // application's inputs): the 6-slice form (21 products) if that is error-free, else the 7-slice form (28), else the FP64
-  // pipe.  All three kernels are enqueued; a device guard written by the slice pass lets exactly one of them run.
+  // pair is kept -- nothing of the product is dropped -- in the cheapest digit-pair form that does (ozaki_pick_form), else the FP64
+  // pipe.  Forms with at most four levels (up to 2 x 3 / 3 x 2 digits: the application up to N = 8192) combine the level sums in a
+  // 64-bit integer and round ONCE: the error-free product, bit-identical to the CPU program on the application's inputs.  Forms with
+  // more levels combine them by a chain of FP64 fma steps (up to 73 significant bits do not fit one integer): faithfully rounded
+  // (<= 1 ulp), and still exact whenever the result fits 53 bits -- as it does for the application at every N = 2^p (SURVEY
+  // appendix A).  Both kernels are enqueued; a device guard written with the digit planes lets exactly one of them run.
   if (!strict && variant == 0 && scratch != nullptr && n >= kOzMinN && dmma_ok) {
     int* lossy = nullptr;
     if (cudaError_t e = launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 7, stream, &lossy, reuse_a, reuse_bt, c_zero); e != cudaSuccess) return e;

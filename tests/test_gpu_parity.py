@@ -1115,13 +1115,16 @@ def test_a_cpu_nest_genome_is_timed_the_same_with_busy_neighbours():
             firsts.add(ctx.stats(s).host_first_cpu)
         assert len(firsts) == slots                     # disjoint CPU sets
         crowded = []
-        for _ in range(3):
+        for _ in range(5):
             outs = ctx.measure_batch([genome] * slots)  # one per slot, all at once
             assert all(o.status == capi.MEASURED for o in outs)
             crowded.append(max(o.time_s for o in outs))
-        t_alone, t_crowded = sorted(alone)[1], sorted(crowded)[1]
-        print(f"alone {t_alone * 1e3:.1f} ms, with {slots - 1} busy neighbours {t_crowded * 1e3:.1f} ms (worst slot)")
-        assert t_crowded <= 1.10 * t_alone, (t_alone, t_crowded)
+        # the box is a shared VM: a batch now and then catches a burst of foreign load on one of its cores (one slot 1.6x slower in a
+        # round-2 run).  Interference from the OTHER SLOTS would be there in every batch, so the best batch is the one to judge.
+        t_alone, t_crowded = min(alone), min(crowded)
+        print(f"alone {t_alone * 1e3:.1f} ms, with {slots - 1} busy neighbours {t_crowded * 1e3:.1f} ms (worst slot of the best of 5 batches; "
+              f"all batches: {[round(t * 1e3, 1) for t in crowded]})")
+        assert t_crowded <= 1.10 * t_alone, (t_alone, crowded)
         c = ctx.fetch(capi.ARRAY_C, slot=slots - 1)
         assert bits_equal(c, cpu.App(n, capi.F64, threads=4).run().c)
 
