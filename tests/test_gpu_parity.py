@@ -1092,40 +1092,47 @@ def _physical_cores():
 @pytest.mark.timeout(600)
 def test_a_cpu_nest_genome_is_timed_the_same_with_busy_neighbours():
     """Every slot measures on its own CPUs (mmx_config.pin_host): a genome whose matmul nest runs on the host must get (within 10 %)
-    the same time whether the other slots are idle or all run CPU-mapped nests themselves.  The reference bounds this contention with
-    `jobs` (evaluator.cpp:254-273); here the slots are pinned to disjoint cores."""
+    the same time whether the other slots are idle or all run host-side nests themselves.  The reference bounds this contention with
+    `jobs` (evaluator.cpp:254-273); here the slots are pinned to disjoint cores.  The neighbours run the all-CPU genome -- host work
+    only -- because on this box all slots share ONE GPU, and neighbours with device work would queue in front of the measured slot's
+    kernels and copies (with a GPU per slot they would not); N = 256 keeps each slot's arrays inside its core's own cache."""
+    import threading
     slots = min(8, _physical_cores())
     if slots < 2:
         pytest.skip("needs >= 2 physical cores")
-    n = 512
-    genome = "101010100001"      # matmul nest on the host (one thread): ~0.1-0.2 s of compute-bound host work
+    n = 256
+    genome = "101010100001"      # matmul nest on the host (one thread): ~8 ms of compute-bound host work
     with capi.Context(n=n, num_slots=slots, devices=[0] * slots, host_threads=1, timeout_s=60.0) as ctx:
-        st0 = None
-        alone = []
-        for _ in range(3):
-            out = ctx.measure(genome, slot=0)
-            assert out.status == capi.MEASURED
-            alone.append(out.time_s)
-            st0 = ctx.stats(0)
-        assert st0.host_cpus >= 1 and st0.host_first_cpu >= 0, (st0.host_cpus, st0.host_first_cpu)
-        assert st0.host_loadavg >= 0.0 or st0.host_loadavg == -1.0, st0.host_loadavg      # -1: the box does not report a load average
         firsts = set()
         for s in range(slots):
-            ctx.measure("101010101001", slot=s)
-            firsts.add(ctx.stats(s).host_first_cpu)
+            assert ctx.measure(genome, slot=s).status == capi.MEASURED   # (first use of a slot allocates its pinned host mirrors)
+            st = ctx.stats(s)
+            assert st.host_cpus >= 1 and st.host_first_cpu >= 0, (s, st.host_cpus, st.host_first_cpu)
+            assert st.host_loadavg >= 0.0 or st.host_loadavg == -1.0      # -1: the box does not report a load average
+            firsts.add(st.host_first_cpu)
         assert len(firsts) == slots                     # disjoint CPU sets
-        crowded = []
-        for _ in range(5):
-            outs = ctx.measure_batch([genome] * slots)  # one per slot, all at once
-            assert all(o.status == capi.MEASURED for o in outs)
-            crowded.append(max(o.time_s for o in outs))
-        # the box is a shared VM: a batch now and then catches a burst of foreign load on one of its cores (one slot 1.6x slower in a
-        # round-2 run).  Interference from the OTHER SLOTS would be there in every batch, so the best batch is the one to judge.
-        t_alone, t_crowded = min(alone), min(crowded)
-        print(f"alone {t_alone * 1e3:.1f} ms, with {slots - 1} busy neighbours {t_crowded * 1e3:.1f} ms (worst slot of the best of 5 batches; "
-              f"all batches: {[round(t * 1e3, 1) for t in crowded]})")
-        assert t_crowded <= 1.10 * t_alone, (t_alone, crowded)
-        c = ctx.fetch(capi.ARRAY_C, slot=slots - 1)
+        alone = [ctx.measure(genome, slot=0).time_s for _ in range(9)]
+        stop = threading.Event()
+
+        def neighbour(slot):
+            while not stop.is_set():
+                ctx.measure("000000000000", slot=slot)   # every nest on the host (ctypes releases the GIL during the call)
+
+        threads = [threading.Thread(target=neighbour, args=(s,)) for s in range(1, slots)]
+        for t in threads:
+            t.start()
+        try:
+            crowded = [ctx.measure(genome, slot=0).time_s for _ in range(9)]
+        finally:
+            stop.set()
+            for t in threads:
+                t.join()
+        # the box is a shared VM (bursts of foreign load show up as single slow samples): medians
+        t_alone, t_crowded = sorted(alone)[4], sorted(crowded)[4]
+        print(f"alone {t_alone * 1e3:.2f} ms, with {slots - 1} busy neighbours {t_crowded * 1e3:.2f} ms (medians of 9; "
+              f"crowded samples {[round(t * 1e3, 1) for t in crowded]})")
+        assert t_crowded <= 1.10 * t_alone, (alone, crowded)
+        c = ctx.fetch(capi.ARRAY_C, slot=0)
         assert bits_equal(c, cpu.App(n, capi.F64, threads=4).run().c)
 
 
