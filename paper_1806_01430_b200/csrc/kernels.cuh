@@ -160,11 +160,28 @@ constexpr int kReuseOperandBt = 0x4000;
 // since): the tensor-core epilogue then STORES its results instead of asking the L2 to add them to c (0 + v == v bit for bit; the
 // exact integer level sums never produce -0), which spares the read of c.  The FP64-pipe / split-TF32 fallbacks ignore it.
 constexpr int kCIsZero = 0x8000;
+// Auto mode inside a CUDA-graph capture: instead of enqueueing the fallback (FP64 pipe / split TF32) as guarded launches that retire
+// at once when an INT8 form took the product (5 us in FP64, 19 us in FP32 per individual), the fallback goes into the body of a
+// conditional IF node whose condition the auto kernel sets on the device (cudaGraphSetConditional): no form => run the body.
+// begin() before the auto launch (no-op unless `stream` is capturing), body_begin() after it, the fallback launches on body_stream(),
+// body_end().  Outside a capture everything stays as it was (active == false).  MMX_GRAPH_COND=0 switches it off.
+struct OzFallbackCond {
+  bool active = false;
+  unsigned long long handle = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphNode_t node = nullptr;
+  cudaStream_t side = nullptr;   // the stream the body is captured on
+  cudaError_t begin(cudaStream_t stream);
+  cudaError_t body_begin(cudaStream_t stream);
+  cudaError_t body_end(cudaStream_t stream);
+  cudaStream_t body_stream(cudaStream_t stream) const { return active ? side : stream; }
+};
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0,
                                 int cols, int slices, cudaStream_t stream, int** guard_out = nullptr, bool reuse_a = false, bool reuse_bt = false,
-                                bool c_zero = false);
+                                bool c_zero = false, const OzFallbackCond* cond = nullptr);
 cudaError_t launch_matmul_ozaki_f32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                    cudaStream_t stream, int** guard_out, bool reuse_a = false, bool reuse_bt = false, bool c_zero = false);
+                                    cudaStream_t stream, int** guard_out, bool reuse_a = false, bool reuse_bt = false, bool c_zero = false,
+                                    const OzFallbackCond* cond = nullptr);
 // device word in `scratch` where the auto launch records the form it ran: 2 .. 7 slices, 0 = left to the FP64 pipe
 int* matmul_ozaki_form_word(void* scratch, int n);
 // gene 9: row i of the same (GEMV against bt)

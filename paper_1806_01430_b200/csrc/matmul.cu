@@ -514,6 +514,70 @@ int raster_group(int /*tile_m*/, size_t /*row_bytes*/) {
   return forced > 0 ? forced : 16;
 }
 
+
+// ---- the fallback of auto mode as a conditional graph node (kernels.cuh: OzFallbackCond) ---------------------------------------------
+namespace {
+cudaStream_t cond_side_stream() {  // one per device and host thread, created outside captures (the warm-up pass comes first)
+  static thread_local cudaStream_t streams[64] = {};
+  int d = 0;
+  cudaGetDevice(&d);
+  cudaStream_t& s = streams[d & 63];
+  if (s == nullptr && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+    s = nullptr;
+    (void)cudaGetLastError();
+  }
+  return s;
+}
+}  // namespace
+
+cudaError_t OzFallbackCond::begin(cudaStream_t stream) {
+  active = false;
+  static const bool enabled = [] { const char* e = getenv("MMX_GRAPH_COND"); return e == nullptr || atoi(e) != 0; }();
+  cudaStreamCaptureStatus status = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(stream, &status) != cudaSuccess) {
+    (void)cudaGetLastError();
+    return cudaSuccess;
+  }
+  if (status != cudaStreamCaptureStatusActive) {
+    (void)cond_side_stream();  // make sure it exists before any capture needs it
+    return cudaSuccess;
+  }
+  side = cond_side_stream();
+  if (!enabled || side == nullptr) return cudaSuccess;
+  unsigned long long id = 0;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  if (cudaError_t e = cudaStreamGetCaptureInfo_v2(stream, &status, &id, &graph, &deps, &ndeps); e != cudaSuccess) return e;
+  cudaGraphConditionalHandle h;
+  if (cudaError_t e = cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault); e != cudaSuccess) return e;
+  handle = h;
+  active = true;
+  return cudaSuccess;
+}
+
+cudaError_t OzFallbackCond::body_begin(cudaStream_t stream) {
+  if (!active) return cudaSuccess;
+  cudaStreamCaptureStatus status;
+  unsigned long long id = 0;
+  const cudaGraphNode_t* deps = nullptr;
+  size_t ndeps = 0;
+  if (cudaError_t e = cudaStreamGetCaptureInfo_v2(stream, &status, &id, &graph, &deps, &ndeps); e != cudaSuccess) return e;
+  cudaGraphNodeParams p = {};
+  p.type = cudaGraphNodeTypeConditional;
+  p.conditional.handle = handle;
+  p.conditional.type = cudaGraphCondTypeIf;
+  p.conditional.size = 1;
+  if (cudaError_t e = cudaGraphAddNode(&node, graph, deps, ndeps, &p); e != cudaSuccess) return e;
+  return cudaStreamBeginCaptureToGraph(side, p.conditional.phGraph_out[0], nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+}
+
+cudaError_t OzFallbackCond::body_end(cudaStream_t stream) {
+  if (!active) return cudaSuccess;
+  cudaGraph_t body = nullptr;
+  if (cudaError_t e = cudaStreamEndCapture(side, &body); e != cudaSuccess) return e;
+  return cudaStreamUpdateCaptureDependencies(stream, &node, 1, cudaStreamSetCaptureDependencies);
+}
+
 template <>
 cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, int n, int row0, int rows, int col0, int cols,
                                   bool strict, int variant, void* scratch, cudaStream_t stream) {
@@ -534,8 +598,13 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
   // appendix A).  Both kernels are enqueued; a device guard written with the digit planes lets exactly one of them run.
   if (!strict && variant == 0 && scratch != nullptr && n >= kOzMinN && dmma_ok) {
     int* lossy = nullptr;
-    if (cudaError_t e = launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 7, stream, &lossy, reuse_a, reuse_bt, c_zero); e != cudaSuccess) return e;
-    return dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, stream, lossy);
+    OzFallbackCond cond;
+    if (cudaError_t e = cond.begin(stream); e != cudaSuccess) return e;
+    if (cudaError_t e = launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 7, stream, &lossy, reuse_a, reuse_bt, c_zero, &cond); e != cudaSuccess) return e;
+    if (cudaError_t e = cond.body_begin(stream); e != cudaSuccess) return e;
+    const cudaError_t ef = dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, cond.body_stream(stream), lossy);
+    const cudaError_t ee = cond.body_end(stream);
+    return ef != cudaSuccess ? ef : ee;
   }
   if (variant == 0) variant = 4;  // the FP64 pipe: DMMA, tile by size (best of the tuning points, profiles/)
   if (strict) {
@@ -577,9 +646,14 @@ cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int 
   if (!strict && scratch != nullptr && variant == 0 && fp32_int8_enabled(n)) {
     int* guard = nullptr;
     void* planes = static_cast<char*>(scratch) + fp32_int8_scratch_offset(n);
-    if (cudaError_t e = launch_matmul_ozaki_f32(c, a, bt, planes, n, row0, rows, col0, cols, stream, &guard, reuse_a, reuse_bt, c_zero); e != cudaSuccess) return e;
+    OzFallbackCond cond;
+    if (cudaError_t e = cond.begin(stream); e != cudaSuccess) return e;
+    if (cudaError_t e = launch_matmul_ozaki_f32(c, a, bt, planes, n, row0, rows, col0, cols, stream, &guard, reuse_a, reuse_bt, c_zero, &cond); e != cudaSuccess) return e;
+    if (cudaError_t e = cond.body_begin(stream); e != cudaSuccess) return e;
     // (a fallback launch always re-splits its rows of a: the earlier column block may have gone the INT8 way)
-    return launch_matmul_3xtf32(c, a, bt, scratch, n, row0, rows, col0, cols, false, stream, false, guard);
+    const cudaError_t ef = launch_matmul_3xtf32(c, a, bt, scratch, n, row0, rows, col0, cols, false, cond.body_stream(stream), false, guard);
+    const cudaError_t ee = cond.body_end(stream);
+    return ef != cudaSuccess ? ef : ee;
   }
   // tensor cores (split-precision TF32, matmul_tc.cu): large matrices by default, any n % 4 == 0 on request
   if (!strict && scratch != nullptr && n % 4 == 0 && (variant == 30 || variant == 31 || (variant == 0 && n >= kTcMinN)))

@@ -316,6 +316,10 @@ struct OzPArgs {
   int n, kq, row0, rows, col0, cols, group;
   long long group_l2_bytes;  // budget for a raster group's rows of a (0: default; MMX_OZ_GROUP_MB overrides -- tuning hook)
   int c_zero;  // every element of c this launch covers is +0: results are stored, not added (kCIsZero)
+  // auto kernels inside a captured graph: the fallback (FP64 pipe / split TF32) sits in a conditional node that runs iff no INT8 form
+  // took the product (OzFallbackCond, kernels.cuh); 0 = no conditional, the fallback launches read the guard themselves
+  unsigned long long cond;
+  int use_cond;
   int debug;  // MMX_OZ_DEBUG (rate probes, results are WRONG): 1 the producer signals stages without loading them, 2 the epilogue drops phase B
 };
 
@@ -1102,7 +1106,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1)
 matmul_ozaki_auto_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, const int* __restrict__ guard, int* __restrict__ ran) {
   extern __shared__ unsigned char smem_raw[];
   const int form = sizeof(CT) == 8 ? ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]) : ozaki_pick_form_f32(guard[0] | guard[3], guard[1], guard[2]);
-  if (blockIdx.x == 0 && threadIdx.x == 0) *ran = form;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *ran = form;
+    if (g.use_cond) cudaGraphSetConditional(g.cond, form == 0 ? 1u : 0u);
+  }
   switch (form) {
     case 223: oz_persist_form<2, 2, 3, 128, 1, CX, CY, CT>(g, maps, smem_raw); break;
     case 324: oz_persist_form<3, 2, 4, 128, 1, CX, CY, CT>(g, maps, smem_raw); break;
@@ -1128,7 +1135,10 @@ __global__ void __launch_bounds__(OZP_THREADS, 1)
 matmul_ozaki_auto_pair_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, const int* __restrict__ guard, int* __restrict__ ran) {
   extern __shared__ unsigned char smem_raw[];
   const int form = sizeof(CT) == 8 ? ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]) : ozaki_pick_form_f32(guard[0] | guard[3], guard[1], guard[2]);
-  if (blockIdx.x == 0 && threadIdx.x == 0) *ran = form;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *ran = form;
+    if (g.use_cond) cudaGraphSetConditional(g.cond, form == 0 ? 1u : 0u);
+  }
   switch (form) {
     case 223: oz_pair_body<2, 2, 3, CT>(g, &maps.a128, &maps.b128, nullptr, &maps.c, smem_raw); break;
     case 324: oz_pair_body<3, 2, 4, CT>(g, &maps.a128, &maps.b128, nullptr, &maps.c, smem_raw); break;
@@ -1488,7 +1498,7 @@ bool make_c_map(CUtensorMap* map, void* c, size_t elem, int n, int rows_end, int
 // the first `slices` of `planes` planes
 template <typename CT = double>
 cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, int n, int row0, int rows, int col0, int cols, cudaStream_t stream,
-                                bool c_zero = false) {
+                                bool c_zero = false, const OzFallbackCond* cond = nullptr) {
   const OzLayout L(scratch, n, planes);
   const bool c_by_tma = (n * sizeof(CT)) % 16 == 0;  // row pitch a multiple of 16 bytes
   if (slices == 0 && !c_by_tma) return cudaErrorInvalidValue;
@@ -1518,6 +1528,8 @@ cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, in
   static const long long group_mb = [] { const char* e = getenv("MMX_OZ_GROUP_MB"); return e ? atoll(e) : 0ll; }();
   g.group_l2_bytes = group_mb << 20;
   g.c_zero = (c_zero && c_by_tma) ? 1 : 0;  // (the register epilogue adds: it reads c anyway)
+  g.cond = (cond != nullptr && cond->active) ? cond->handle : 0ull;
+  g.use_cond = (cond != nullptr && cond->active) ? 1 : 0;
   static const int debug = [] { const char* e = getenv("MMX_OZ_DEBUG"); return e ? atoi(e) : 0; }();
   g.debug = debug;
   // the grid covers the 64-wide tiling (the forms with 128-wide tiles leave the surplus CTAs without a tile)
@@ -1638,12 +1650,12 @@ size_t matmul_ozaki_scratch_bytes(int n) {
 // value rounded once, added by a FLOAT32 TMA reduction).  *guard_out receives the guard; the caller enqueues the split-TF32 path
 // under ozaki_pick_form_f32(...) == 0.
 cudaError_t launch_matmul_ozaki_f32(float* c, const float* a, const float* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                    cudaStream_t stream, int** guard_out, bool reuse_a, bool reuse_bt, bool c_zero) {
+                                    cudaStream_t stream, int** guard_out, bool reuse_a, bool reuse_bt, bool c_zero, const OzFallbackCond* cond) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr || guard_out == nullptr || n % 4 != 0) return cudaErrorInvalidValue;
   *guard_out = OzLayout(scratch, n, 7).guard;
   if (cudaError_t e = oz_slices<7, float>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a, reuse_bt); e != cudaSuccess) return e;
-  return oz_persist_contract<float>(c, scratch, 7, 0, n, row0, rows, col0, cols, stream, c_zero);
+  return oz_persist_contract<float>(c, scratch, 7, 0, n, row0, rows, col0, cols, stream, c_zero, cond);
 }
 
 OzOperand matmul_ozaki_operand(void* scratch, int n, int which) {
@@ -1662,7 +1674,7 @@ OzOperand matmul_ozaki_operand(void* scratch, int n, int which) {
 int* matmul_ozaki_form_word(void* scratch, int n) { return scratch == nullptr ? nullptr : OzLayout(scratch, n, 7).guard + 4; }
 
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0, int cols,
-                                int slices, cudaStream_t stream, int** guard_out, bool reuse_a, bool reuse_bt, bool c_zero) {
+                                int slices, cudaStream_t stream, int** guard_out, bool reuse_a, bool reuse_bt, bool c_zero, const OzFallbackCond* cond) {
   if (rows <= 0 || cols <= 0) return cudaSuccess;
   if (scratch == nullptr) return cudaErrorInvalidValue;
   // MMX_OZ_LEGACY=1: the one-tile-per-CTA kernels of the first version (A/B comparison, tools/ozaki_cluster_sweep.sh)
@@ -1673,7 +1685,7 @@ cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, vo
     *guard_out = OzLayout(scratch, n, 7).guard;
     if (!(reuse_a && reuse_bt))  // both reused: the digit planes and the guard stand as their producers left them
       if (cudaError_t e = oz_slices<7>(a, bt, scratch, n, row0, rows, col0, cols, stream, true, reuse_a, reuse_bt); e != cudaSuccess) return e;
-    if (!legacy) return oz_persist_contract(c, scratch, 7, 0, n, row0, rows, col0, cols, stream, c_zero);
+    if (!legacy) return oz_persist_contract(c, scratch, 7, 0, n, row0, rows, col0, cols, stream, c_zero, cond);
     if (cudaError_t e = oz_contract<6, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true); e != cudaSuccess) return e;
     return oz_contract<7, 1, 64>(c, scratch, 7, n, row0, rows, col0, cols, stream, true);
   }
