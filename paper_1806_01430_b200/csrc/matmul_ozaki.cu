@@ -977,6 +977,12 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
       asm volatile("bar.sync 1, 256;\n" ::: "memory");
       mbar_wait(acc_full, tile & 1);
       tc_fence_after();
+      if (g.debug & 2048) {  // rate probe: the set is handed back unread (what the drain costs per tile)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(lead_acc_empty);
+        continue;
+      }
       // phase A: the accumulators leave TMEM as one number per element (a 64-bit integer up to four levels, the Horner sum in
       // FP64 beyond); blocks that are only accumulated into are zeroed behind the read
       long long acc[LV <= 4 ? MY : 1][16];
