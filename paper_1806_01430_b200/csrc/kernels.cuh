@@ -174,6 +174,7 @@ struct OzFallbackCond {
   cudaError_t begin(cudaStream_t stream);
   cudaError_t body_begin(cudaStream_t stream);
   cudaError_t body_end(cudaStream_t stream);
+  void abandon();  // an error between begin() and body_begin(): hand the borrowed stream back
   cudaStream_t body_stream(cudaStream_t stream) const { return active ? side : stream; }
 };
 cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, void* scratch, int n, int row0, int rows, int col0,

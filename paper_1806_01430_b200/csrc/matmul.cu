@@ -16,6 +16,8 @@
 // The DMMA variant keeps the same k-ascending FMA chain per element (the MMA accumulates its
 // four products in order into the running sum), so it produces the same bits as FAST SIMT.
 #include <cstdlib>
+#include <mutex>
+#include <vector>
 
 #include "kernels.cuh"
 #include "raster.cuh"
@@ -517,21 +519,59 @@ int raster_group(int /*tile_m*/, size_t /*row_bytes*/) {
 
 // ---- the fallback of auto mode as a conditional graph node (kernels.cuh: OzFallbackCond) ---------------------------------------------
 namespace {
-cudaStream_t cond_side_stream() {  // one per device and host thread, created outside captures (the warm-up pass comes first)
-  static thread_local cudaStream_t streams[64] = {};
+// Streams the conditional bodies are captured on: a small pool per device, filled outside captures (every capture is preceded by an
+// un-captured warm-up pass through the same launch path), borrowed for the duration of one body capture.  Not thread_local: the
+// batch evaluator's worker threads are short-lived, and a stream per thread would leak one per batch.
+struct SidePool {
+  std::mutex mu;
+  std::vector<cudaStream_t> idle[64];
+  int created[64] = {};
+};
+SidePool& side_pool() {
+  static SidePool pool;
+  return pool;
+}
+constexpr int kSideStreamsPerDevice = 8;  // concurrent captures on one device beyond this fall back to guarded launches
+
+void side_pool_top_up() {
   int d = 0;
   cudaGetDevice(&d);
-  cudaStream_t& s = streams[d & 63];
-  if (s == nullptr && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
-    s = nullptr;
-    (void)cudaGetLastError();
+  SidePool& pool = side_pool();
+  std::lock_guard<std::mutex> g(pool.mu);
+  while (pool.created[d & 63] < kSideStreamsPerDevice) {
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return;
+    }
+    pool.idle[d & 63].push_back(s);
+    ++pool.created[d & 63];
   }
+}
+cudaStream_t side_pool_borrow() {
+  int d = 0;
+  cudaGetDevice(&d);
+  SidePool& pool = side_pool();
+  std::lock_guard<std::mutex> g(pool.mu);
+  auto& idle = pool.idle[d & 63];
+  if (idle.empty()) return nullptr;
+  cudaStream_t s = idle.back();
+  idle.pop_back();
   return s;
+}
+void side_pool_return(cudaStream_t s) {
+  if (s == nullptr) return;
+  int d = 0;
+  cudaGetDevice(&d);
+  SidePool& pool = side_pool();
+  std::lock_guard<std::mutex> g(pool.mu);
+  pool.idle[d & 63].push_back(s);
 }
 }  // namespace
 
 cudaError_t OzFallbackCond::begin(cudaStream_t stream) {
   active = false;
+  side = nullptr;
   static const bool enabled = [] { const char* e = getenv("MMX_GRAPH_COND"); return e == nullptr || atoi(e) != 0; }();
   cudaStreamCaptureStatus status = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(stream, &status) != cudaSuccess) {
@@ -539,20 +579,32 @@ cudaError_t OzFallbackCond::begin(cudaStream_t stream) {
     return cudaSuccess;
   }
   if (status != cudaStreamCaptureStatusActive) {
-    (void)cond_side_stream();  // make sure it exists before any capture needs it
+    if (enabled) side_pool_top_up();  // outside a capture: make sure the pool exists before a capture needs it
     return cudaSuccess;
   }
-  side = cond_side_stream();
-  if (!enabled || side == nullptr) return cudaSuccess;
+  if (!enabled) return cudaSuccess;
+  side = side_pool_borrow();
+  if (side == nullptr) return cudaSuccess;  // no stream to capture the body on: guarded launches, as outside a capture
   unsigned long long id = 0;
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
-  if (cudaError_t e = cudaStreamGetCaptureInfo_v2(stream, &status, &id, &graph, &deps, &ndeps); e != cudaSuccess) return e;
   cudaGraphConditionalHandle h;
-  if (cudaError_t e = cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault); e != cudaSuccess) return e;
+  cudaError_t e = cudaStreamGetCaptureInfo_v2(stream, &status, &id, &graph, &deps, &ndeps);
+  if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&h, graph, 0, cudaGraphCondAssignDefault);
+  if (e != cudaSuccess) {
+    side_pool_return(side);
+    side = nullptr;
+    return e;
+  }
   handle = h;
   active = true;
   return cudaSuccess;
+}
+
+void OzFallbackCond::abandon() {
+  if (side != nullptr) side_pool_return(side);
+  side = nullptr;
+  active = false;
 }
 
 cudaError_t OzFallbackCond::body_begin(cudaStream_t stream) {
@@ -561,20 +613,29 @@ cudaError_t OzFallbackCond::body_begin(cudaStream_t stream) {
   unsigned long long id = 0;
   const cudaGraphNode_t* deps = nullptr;
   size_t ndeps = 0;
-  if (cudaError_t e = cudaStreamGetCaptureInfo_v2(stream, &status, &id, &graph, &deps, &ndeps); e != cudaSuccess) return e;
+  cudaError_t e = cudaStreamGetCaptureInfo_v2(stream, &status, &id, &graph, &deps, &ndeps);
   cudaGraphNodeParams p = {};
   p.type = cudaGraphNodeTypeConditional;
   p.conditional.handle = handle;
   p.conditional.type = cudaGraphCondTypeIf;
   p.conditional.size = 1;
-  if (cudaError_t e = cudaGraphAddNode(&node, graph, deps, ndeps, &p); e != cudaSuccess) return e;
-  return cudaStreamBeginCaptureToGraph(side, p.conditional.phGraph_out[0], nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (e == cudaSuccess) e = cudaGraphAddNode(&node, graph, deps, ndeps, &p);
+  if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(side, p.conditional.phGraph_out[0], nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+  if (e != cudaSuccess) {  // the body was never opened: hand the stream back, the caller fails the capture
+    side_pool_return(side);
+    side = nullptr;
+    active = false;
+  }
+  return e;
 }
 
 cudaError_t OzFallbackCond::body_end(cudaStream_t stream) {
   if (!active) return cudaSuccess;
   cudaGraph_t body = nullptr;
-  if (cudaError_t e = cudaStreamEndCapture(side, &body); e != cudaSuccess) return e;
+  cudaError_t e = cudaStreamEndCapture(side, &body);
+  side_pool_return(side);
+  side = nullptr;
+  if (e != cudaSuccess) return e;
   return cudaStreamUpdateCaptureDependencies(stream, &node, 1, cudaStreamSetCaptureDependencies);
 }
 
@@ -600,7 +661,10 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
     int* lossy = nullptr;
     OzFallbackCond cond;
     if (cudaError_t e = cond.begin(stream); e != cudaSuccess) return e;
-    if (cudaError_t e = launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 7, stream, &lossy, reuse_a, reuse_bt, c_zero, &cond); e != cudaSuccess) return e;
+    if (cudaError_t e = launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 7, stream, &lossy, reuse_a, reuse_bt, c_zero, &cond); e != cudaSuccess) {
+      cond.abandon();
+      return e;
+    }
     if (cudaError_t e = cond.body_begin(stream); e != cudaSuccess) return e;
     const cudaError_t ef = dmma_go<16, 3, 2, 2, 4, 4>(c, a, bt, n, row0, rows, col0, cols, cond.body_stream(stream), lossy);
     const cudaError_t ee = cond.body_end(stream);
@@ -648,7 +712,10 @@ cudaError_t launch_matmul<float>(float* c, const float* a, const float* bt, int 
     void* planes = static_cast<char*>(scratch) + fp32_int8_scratch_offset(n);
     OzFallbackCond cond;
     if (cudaError_t e = cond.begin(stream); e != cudaSuccess) return e;
-    if (cudaError_t e = launch_matmul_ozaki_f32(c, a, bt, planes, n, row0, rows, col0, cols, stream, &guard, reuse_a, reuse_bt, c_zero, &cond); e != cudaSuccess) return e;
+    if (cudaError_t e = launch_matmul_ozaki_f32(c, a, bt, planes, n, row0, rows, col0, cols, stream, &guard, reuse_a, reuse_bt, c_zero, &cond); e != cudaSuccess) {
+      cond.abandon();
+      return e;
+    }
     if (cudaError_t e = cond.body_begin(stream); e != cudaSuccess) return e;
     // (a fallback launch always re-splits its rows of a: the earlier column block may have gone the INT8 way)
     const cudaError_t ef = launch_matmul_3xtf32(c, a, bt, scratch, n, row0, rows, col0, cols, false, cond.body_stream(stream), false, guard);
