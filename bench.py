@@ -58,6 +58,8 @@ def parse_args():
     ap.add_argument("--ga-population", type=int, default=64)
     ap.add_argument("--ga-generations", type=int, default=40)
     ap.add_argument("--ga-timeout", type=float, default=2.0, help="budget per individual in the GA block (a run over it scores the budget)")
+    ap.add_argument("--ga-wait-timeouts", action="store_true", help="GA block: wait out every hopeless run (mmx_config.early_timeout = 0), as the "
+                                                                     "reference's process timeout does")
     ap.add_argument("--rowshard-n", type=int, nargs="*", default=[16384, 32768], help="sizes of the row-sharded block (config 5)")
     return ap.parse_args()
 
@@ -642,7 +644,8 @@ def ga_block(args, n, dtype, device, rank, world, ctl, barrier):
         return {"skipped": f"the all-CPU baseline genome could not be measured within 300 s (status {capi.STATUS_NAMES[base[0][0]]})"}
     # each rank's CPU-mapped nests run on the rank's own share of the host's CPUs (mmx_config.pin_host)
     with capi.Context(n=n, dtype=dtype, devices=[device], timeout_s=args.ga_timeout, host_threads=team,
-                      host_core_first=(rank % max(1, cores // team)) * team, host_core_count=team) as ctx:
+                      host_core_first=(rank % max(1, cores // team)) * team, host_core_count=team,
+                      early_timeout=0 if args.ga_wait_timeouts else 1) as ctx:
         ev = ShardedEvaluator(lambda g: ctx.measure(g).as_tuple(), capi.GENE_LENGTH, group=ctl, device="cpu")
         ev.preload(zero, base[0])
         barrier()
@@ -663,6 +666,7 @@ def ga_block(args, n, dtype, device, rank, world, ctl, barrier):
         dist.all_gather_object(per_rank, local, group=ctl)
     out = {"config": f"GA {args.ga_population} x {args.ga_generations}, seed 1, N={n}, budget {args.ga_timeout} s per individual, "
                      f"{team} host thread(s) per rank for CPU-mapped nests",
+           "early_timeout": not args.ga_wait_timeouts,
            "wall_s": wall, "wall_to_best_s": walls[first_best] - (walls[0] if walls else 0.0) if first_best < len(walls) else None,
            "generation_of_best": first_best, "best_genome": res["best_genome"], "best_s": res["best_s"],
            "baseline_s": res["baseline_s"], "baseline_measure_s": t_base,
@@ -672,8 +676,9 @@ def ga_block(args, n, dtype, device, rank, world, ctl, barrier):
            "individuals_per_s": c["distinct"] / wall, "feasible_individuals_per_s": feasible / wall,
            "paper_budget_fraction": (wall + t_base) / 3600.0,
            "note": "wall_s covers the whole search (2522 requests); infeasible genomes are rejected by the planner without GPU work; "
-                   "genomes that leave the matmul nest on the host run into the budget and score it (evaluator.cpp:103-108)"}
-    out["key"] = [n, args.ga_population, args.ga_generations, args.ga_timeout]
+                   "genomes that leave the matmul nest on the host cannot meet the budget and score it (evaluator.cpp:103-108) -- with "
+                   "early_timeout such a run is given up as soon as its measured progress shows that (same outcome, a fraction of the wall cost)"}
+    out["key"] = [n, args.ga_population, args.ga_generations, args.ga_timeout, not args.ga_wait_timeouts]
     try:   # the same block measured on ONE GPU (committed evidence: bench.py --ga on one B200), for the efficiency figure
         one = json.loads((ROOT / "profiles" / "r2_ga_n1.json").read_text())
         if world > 1 and one.get("key") == out["key"]:

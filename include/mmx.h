@@ -125,6 +125,12 @@ typedef struct mmx_config {
   int32_t pin_host;
   int32_t host_core_first;
   int32_t host_core_count;
+  /* Hopeless runs are given up early (default 1): once a host-side nest or a train of inner-loop launches has run for 20 ms and its
+   * measured progress projects at least twice the time the budget has left, the run ends as MMX_TIMEOUT with time_s = timeout_s --
+   * exactly the outcome the full wait would produce (evaluator.cpp:103-108) -- at a fraction of the wall cost.  A GA search over
+   * this application spends nearly all of its wall time waiting for such runs (the matmul nest on the host at N = 4096 needs a
+   * minute per individual).  0: every run is waited for, as the reference's process timeout does. */
+  int32_t early_timeout;
 } mmx_config;
 
 /* EvaluationOutcome, evaluation.hpp:19-28. */

@@ -39,6 +39,7 @@ class Config(C.Structure):
         ("devices", C.POINTER(C.c_int32)), ("host_threads", C.c_int32), ("launch_batching", C.c_int32),
         ("matmul_variant", C.c_int32), ("warmup", C.c_int32),
         ("pin_host", C.c_int32), ("host_core_first", C.c_int32), ("host_core_count", C.c_int32),
+        ("early_timeout", C.c_int32),
     ]
 
 
@@ -205,7 +206,7 @@ class Context:
     def __init__(self, n: int = 256, dtype: int = F64, numerics: int = FAST, timeout_s: float = 120.0,
                  repetitions: int = 1, num_slots: int = 1, devices=None, host_threads: int = 1,
                  launch_batching: int = 1, matmul_variant: int = 0, warmup: int = 0, pin_host: int = 1,
-                 host_core_first: int = 0, host_core_count: int = 0):
+                 host_core_first: int = 0, host_core_count: int = 0, early_timeout: int = 1):
         self._lib = load()
         cfg = Config()
         self._lib.mmx_default_config(C.byref(cfg))
@@ -214,6 +215,7 @@ class Context:
         cfg.host_threads, cfg.launch_batching = host_threads, launch_batching
         cfg.matmul_variant, cfg.warmup = matmul_variant, warmup
         cfg.pin_host, cfg.host_core_first, cfg.host_core_count = pin_host, host_core_first, host_core_count
+        cfg.early_timeout = early_timeout
         self._devices = None
         if devices is not None:
             self._devices = (C.c_int32 * len(devices))(*devices)

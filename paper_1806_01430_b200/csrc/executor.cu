@@ -310,6 +310,7 @@ cudaError_t run_train(mmx_ctx* ctx, Slot& s, int gene, long long total, const De
     const Train& tr = it_train->second;
     if ((e = cudaMemsetAsync(s.d_iter, 0, sizeof(int), s.stream)) != cudaSuccess) return e;
     const long long trains = total / tr.k;
+    const Clock::time_point started = Clock::now();
     for (long long t = 0; t < trains; ++t) {
       if ((e = cudaGraphLaunch(tr.exec, s.stream)) != cudaSuccess) return e;
       ++*graph_launches;
@@ -317,18 +318,19 @@ cudaError_t run_train(mmx_ctx* ctx, Slot& s, int gene, long long total, const De
       // keep the queue shallow enough that a timeout is noticed within a few trains
       if ((t & 7) == 7) {
         if ((e = cudaStreamSynchronize(s.stream)) != cudaSuccess) return e;
-        if (dl.expired()) {
+        if (dl.expired() || dl.hopeless(started, done, total)) {
           *timed_out = true;
           return cudaSuccess;
         }
       }
     }
   }
+  const Clock::time_point started_plain = Clock::now();
   for (long long it = done; it < total; ++it) {
     if ((e = launch_gene_any(ctx, s, gene, IterRef{nullptr, static_cast<int>(it)})) != cudaSuccess) return e;
     if (((it - done) & 1023) == 1023) {
       if ((e = cudaStreamSynchronize(s.stream)) != cudaSuccess) return e;
-      if (dl.expired()) {
+      if (dl.expired() || dl.hopeless(started_plain, it - done + 1, total - done)) {
         *timed_out = true;
         return cudaSuccess;
       }
@@ -504,7 +506,7 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const 
 
   begin_sequence(s, plan.modes[MMX_NEST_MATMUL] == MMX_MODE_GPU_NEST);
   const Clock::time_point t0 = Clock::now();
-  const Deadline dl{t0 + std::chrono::duration_cast<Clock::duration>(Seconds(budget))};
+  const Deadline dl{t0 + std::chrono::duration_cast<Clock::duration>(Seconds(budget)), ctx->cfg.early_timeout != 0};
   e = cudaEventRecord(s.ev_begin, s.stream);
 
   if (whole != nullptr) {
@@ -828,6 +830,7 @@ MMX_API void mmx_default_config(mmx_config* cfg) {
   cfg->pin_host = 1;
   cfg->host_core_first = 0;
   cfg->host_core_count = 0;  // all the CPUs the process may run on
+  cfg->early_timeout = 1;
 }
 
 MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {

@@ -31,8 +31,11 @@ bool for_rows(int row0, int row1, const HostTeam& team, const Deadline& dl, int 
   if (threads > n) threads = n;
   std::atomic<bool> expired{false};
   auto block = [&](int r0, int r1) {
+    const Clock::time_point started = Clock::now();
     for (int i = r0; i < r1; ++i) {
-      if ((i - r0) % poll_every == 0 && (expired.load(std::memory_order_relaxed) || dl.expired())) {
+      // every thread projects its own block (the rows of a nest cost the same): one hopeless block makes the nest hopeless
+      if ((i - r0) % poll_every == 0 &&
+          (expired.load(std::memory_order_relaxed) || dl.expired() || dl.hopeless(started, i - r0, r1 - r0))) {
         expired.store(true, std::memory_order_relaxed);
         return;
       }

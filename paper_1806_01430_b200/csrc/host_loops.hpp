@@ -14,7 +14,20 @@ using Clock = std::chrono::steady_clock;
 // Budget shared by every step of one benchmark run (ToolchainConfig::timeout_s).
 struct Deadline {
   Clock::time_point at;
+  bool early = false;  // mmx_config.early_timeout: give up as soon as measured progress shows the budget cannot be met
   bool expired() const { return Clock::now() >= at; }
+  // `done` of `total` equal units of work took the time since `start`: is what remains hopeless -- at least twice the time left until
+  // the deadline (plus 10 ms), judged only once 20 ms and 8 units have been measured?  The outcome of a run that is given up is the
+  // one the full wait would produce (Timeout, time = the budget, evaluator.cpp:103-108); only its wall cost is smaller.
+  bool hopeless(Clock::time_point start, long long done, long long total) const {
+    if (!early || done < 8 || done >= total) return false;
+    const Clock::time_point now = Clock::now();
+    const double elapsed = std::chrono::duration<double>(now - start).count();
+    if (elapsed < 0.020) return false;
+    const double remaining = elapsed * static_cast<double>(total - done) / static_cast<double>(done);
+    const double left = std::chrono::duration<double>(at - now).count();
+    return remaining > 2.0 * (left > 0.0 ? left : 0.0) + 0.010;
+  }
 };
 
 // The threads a CPU-mapped nest runs on: `threads` > 1 splits the outer loop into contiguous row blocks (per-element arithmetic is

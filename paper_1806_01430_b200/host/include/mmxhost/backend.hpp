@@ -112,6 +112,9 @@ struct CudaBackendConfig {
   bool pin_host = true;
   int host_core_first = 0;
   int host_core_count = 0;
+  // hopeless runs are given up as soon as their measured progress shows that the budget cannot be met (mmx_config.early_timeout):
+  // the outcome is the full wait's (Timeout, time = budget), the wall cost a fraction of it
+  bool early_timeout = true;
 };
 
 // Throws ToolchainMissing when there is no CUDA device (there is no CPU fallback), ConfigError

@@ -66,6 +66,7 @@ CudaBackend::CudaBackend(const CudaBackendConfig& config) : config_(config) {
   c.pin_host = config.pin_host ? 1 : 0;
   c.host_core_first = config.host_core_first;
   c.host_core_count = config.host_core_count;
+  c.early_timeout = config.early_timeout ? 1 : 0;
   const int rc = mmx_create(&c, &ctx_);
   if (rc != MMX_OK) throw_for_code(rc, std::string("mmx_create: ") + mmx_last_error(nullptr));
   busy_.assign(config.devices.size(), 0);

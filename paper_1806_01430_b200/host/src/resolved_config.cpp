@@ -71,6 +71,7 @@ std::string render_resolved_config(const RunConfig& cfg) {
     o.integer("pin_host", c.pin_host ? 1 : 0);
     o.integer("host_core_first", c.host_core_first);
     o.integer("host_core_count", c.host_core_count);
+    o.integer("early_timeout", c.early_timeout ? 1 : 0);
     o.close();
   } else {
     o.str("sim_model", *cfg.sim_model);

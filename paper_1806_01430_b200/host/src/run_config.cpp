@@ -130,6 +130,7 @@ CudaBackendConfig read_cuda(const Value& obj) {
   c.pin_host = s.integer("pin_host", c.pin_host ? 1 : 0) != 0;
   c.host_core_first = at_least(s.integer("host_core_first", c.host_core_first), 0, "host_core_first", "must not be negative");
   c.host_core_count = at_least(s.integer("host_core_count", c.host_core_count), 0, "host_core_count", "must not be negative");
+  c.early_timeout = s.integer("early_timeout", c.early_timeout ? 1 : 0) != 0;
   if (const Value* d = s.peek("devices")) {
     if (!d->is_array() || d->array->empty()) throw ConfigError("'devices' in 'cuda' must be a non-empty array of device ordinals");
     c.devices.clear();
