@@ -4,11 +4,10 @@
 //
 // gene 6 (whole nest), fast path for N % 64 == 0: a CTA moves one 64x64 tile.  Global loads
 // and stores are both 128-bit and fully coalesced (a warp covers whole 512 B / 256 B row
-// segments).  The exchange goes through shared memory in units of VxV micro-blocks
-// (V = 16 B / E): a thread loads V vectors from V consecutive rows, transposes the VxV block in
-// registers and stores V vectors into the *output-ordered* tile.  The tile is XOR-swizzled at
-// 16-byte granularity (chunk ^= (row / V) & 7) so that both the micro-block stores (lanes walk
-// down the rows) and the row reads (lanes walk along a row) are bank-conflict free.
+// segments).  The tile of b is staged in shared memory as it lies in global memory, by cp.async
+// (16 bytes each, past the registers and L1), XOR-swizzled at 16-byte granularity
+// (chunk ^= (row / V) & 7, V = 16 B / E); a thread then gathers the V elements of one 16-byte
+// piece of a row of bt from V consecutive rows of the staged tile and stores it.
 //
 // gene 7 (one row of bt per launch): row i of bt is column i of b -- a strided gather; each
 // 8-byte element costs a 32-byte sector, which is the sector amplification the catalogue notes.
@@ -24,15 +23,21 @@ template <typename T> struct VecOf;
 template <> struct VecOf<double> { using type = double2; static constexpr int V = 2; };
 template <> struct VecOf<float> { using type = float4; static constexpr int V = 4; };
 
-__device__ __forceinline__ void transpose_micro(const double2 (&in)[2], double2 (&out)[2]) {
-  out[0] = make_double2(in[0].x, in[1].x);
-  out[1] = make_double2(in[0].y, in[1].y);
+// Piece `chunk` of row `out_row` of the transposed tile = column out_row of rows chunk * V .. + V of the staged tile of b: V scalar
+// reads (the lanes of a warp walk down the micro-rows, which the swizzle spreads over the eight 16-byte bank groups: a fourfold
+// conflict on 8-byte reads, a twofold one on 4-byte reads -- the cost of one 16-byte read per lane).
+__device__ __forceinline__ double2 gather_piece(const double2* tile, int out_row, int chunk) {
+  constexpr int MB = kTile / 2;
+  const double* t = reinterpret_cast<const double*>(tile);
+  const int at = ((out_row / 2) ^ (chunk & 7)) * 2 + (out_row & 1);
+  return make_double2(t[(chunk * 2) * (MB * 2) + at], t[(chunk * 2 + 1) * (MB * 2) + at]);
 }
-__device__ __forceinline__ void transpose_micro(const float4 (&in)[4], float4 (&out)[4]) {
-  out[0] = make_float4(in[0].x, in[1].x, in[2].x, in[3].x);
-  out[1] = make_float4(in[0].y, in[1].y, in[2].y, in[3].y);
-  out[2] = make_float4(in[0].z, in[1].z, in[2].z, in[3].z);
-  out[3] = make_float4(in[0].w, in[1].w, in[2].w, in[3].w);
+__device__ __forceinline__ float4 gather_piece(const float4* tile, int out_row, int chunk) {
+  constexpr int MB = kTile / 4;
+  const float* t = reinterpret_cast<const float*>(tile);
+  const int at = ((out_row / 4) ^ (chunk & 7)) * 4 + (out_row & 3);
+  return make_float4(t[(chunk * 4) * (MB * 4) + at], t[(chunk * 4 + 1) * (MB * 4) + at], t[(chunk * 4 + 2) * (MB * 4) + at],
+                     t[(chunk * 4 + 3) * (MB * 4) + at]);
 }
 
 // grid = (rows/64, n/64); block = 256 threads.  PUSH: the finished tile is stored into every destination
@@ -46,7 +51,7 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
   using VT = typename VecOf<T>::type;
   constexpr int V = VecOf<T>::V;
   constexpr int MB = kTile / V;         // micro-blocks per tile side == 16-byte chunks per tile row
-  __shared__ VT tile[kTile * MB];        // output-ordered: tile[out_row][chunk], swizzled
+  __shared__ __align__(16) VT tile[kTile * MB];   // the tile of b, input-ordered: tile[row][chunk], swizzled
 
   const int in_row0 = blockIdx.y * kTile;   // rows of b  == columns of bt
   const int in_col0 = first_row + blockIdx.x * kTile;   // cols of b  == rows of bt
@@ -62,23 +67,19 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
     for (int k = 0; k < kSteps; ++k) row_exp[k] = P.exps[in_col0 + (tid + 256 * k) / MB];
   }
 
-  // phase 1: micro-blocks, lanes along the input row (coalesced 128-bit loads)
+  // phase 1: the tile of b goes to shared memory as it lies in global memory (rows of b), 16 bytes per cp.async, lanes along the
+  // row; chunk c of row r lands at chunk c ^ ((r / V) & 7).  The copies bypass the registers and L1: how many bytes a CTA has in
+  // flight is then not bounded by what L1 can track (with loads into registers the kernel lost 10 % when the shared-memory
+  // carve-out left L1 28 KB instead of 60 -- profiles/r2x_transpose_l1.txt)
+  const unsigned tile_s = static_cast<unsigned>(__cvta_generic_to_shared(tile));
 #pragma unroll
-  for (int mb = tid; mb < MB * MB; mb += 256) {
-    const int C = mb % MB;  // micro column (input cols C*V ..)
-    const int R = mb / MB;  // micro row    (input rows R*V ..)
-    VT in[V], out[V];
-#pragma unroll
-    for (int r = 0; r < V; ++r)
-      in[r] = *reinterpret_cast<const VT*>(b + static_cast<size_t>(in_row0 + R * V + r) * n + in_col0 + C * V);
-    transpose_micro(in, out);
-#pragma unroll
-    for (int r = 0; r < V; ++r) {
-      const int out_row = C * V + r;                 // row of the output tile
-      const int chunk = R ^ ((out_row / V) & 7);     // == R ^ (C & 7)
-      tile[out_row * MB + chunk] = out[r];
-    }
+  for (int k = 0; k < kSteps; ++k) {
+    const int v = tid + 256 * k;
+    const int row = v / MB, chunk = v % MB;
+    const T* src = b + static_cast<size_t>(in_row0 + row) * n + in_col0 + chunk * V;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(tile_s + 16u * (row * MB + (chunk ^ ((row / V) & 7)))), "l"(src) : "memory");
   }
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
 
   // phase 2: lanes along the output row (coalesced 128-bit stores)
@@ -93,7 +94,7 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
     for (int k = 0; k < STEPS; ++k) {
       const int v = tid + 256 * k;
       const int out_row = v / MB, chunk = v % MB;
-      const VT val = tile[out_row * MB + (chunk ^ ((out_row / V) & 7))];
+      const VT val = gather_piece(tile, out_row, chunk);
       *reinterpret_cast<VT*>(bt + static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V) = val;
       bool tiny;
       const double inv = oz_row_scale(row_exp[k], true, false, &tiny);
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
         if (!(more >> k & 1u) && dirty <= 2) continue;
         const int v = tid + 256 * k;
         const int out_row = v / MB, chunk = v % MB;
-        const VT val = tile[out_row * MB + (chunk ^ ((out_row / V) & 7))];
+        const VT val = gather_piece(tile, out_row, chunk);
         bool tiny;
         const double inv = oz_row_scale(row_exp[k], true, false, &tiny);
         lossy |= tiny;
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
     for (int v = tid; v < kTile * MB; v += 256) {
       const int out_row = v / MB;
       const int chunk = v % MB;
-      const VT val = tile[out_row * MB + (chunk ^ ((out_row / V) & 7))];
+      const VT val = gather_piece(tile, out_row, chunk);
       const size_t at = static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V;
       if constexpr (PUSH) {
         for (int d = 0; d < peers.count; ++d) *reinterpret_cast<VT*>(static_cast<T*>(peers.p[d]) + at) = val;
