@@ -89,12 +89,13 @@ __device__ __forceinline__ void oz_emit(const double (&v)[W], double inv, bool b
 // caller that encodes several rows per thread gives the compiler ONE basic block of independent FP64 chains (the walk of oz_emit is
 // a chain of dependent FP64 operations per element and level with a branch after each level; on B200 those are long-latency
 // operations, and the producers that used oz_emit row by row spent half their issue slots waiting on them -- ncu, r2r_producers).
-// Returns true when something is left below the second digit: the caller then runs oz_emit on the same elements (rare path; it
+// (oz_first_two_words hands the two packed words back instead of storing them.)  Returns true when something is left below the second digit: the caller then runs oz_emit on the same elements (rare path; it
 // rewrites the two planes with the same digits and continues).  top2: 0 / 1 / 2 = highest non-zero digit among the two.
 template <int W>
-__device__ __forceinline__ bool oz_emit_first_two(const double (&v)[W], double inv, signed char* __restrict__ drow, size_t plane, int k0, int& top2) {
-  static_assert(W == 2 || W == 4, "digits are packed two or four to a store");
-  int word0 = 0, word1 = 0;
+__device__ __forceinline__ bool oz_first_two_words(const double (&v)[W], double inv, int& word0, int& word1) {
+  static_assert(W == 2 || W == 4, "digits are packed two or four to a word");
+  word0 = 0;
+  word1 = 0;
   bool left = false;
 #pragma unroll
   for (int q = 0; q < W; ++q) {
@@ -107,6 +108,12 @@ __device__ __forceinline__ bool oz_emit_first_two(const double (&v)[W], double i
     word1 |= (__double2loint(s1) & 0xff) << (8 * q);
     left = left || rem != 0.0;
   }
+  return left;
+}
+template <int W>
+__device__ __forceinline__ bool oz_emit_first_two(const double (&v)[W], double inv, signed char* __restrict__ drow, size_t plane, int k0, int& top2) {
+  int word0, word1;
+  const bool left = oz_first_two_words<W>(v, inv, word0, word1);
   if constexpr (W == 4) {
     *reinterpret_cast<int*>(drow + k0) = word0;
     *reinterpret_cast<int*>(drow + plane + k0) = word1;
