@@ -206,6 +206,68 @@ __global__ void __launch_bounds__(256, 2) gemv_row_stream_kernel(T* __restrict__
   }
 }
 
+// FAST, split form: a CTA owns a contiguous block of rows of bt and its eight warps each own an eighth of every row, so that the
+// rows divide evenly over 2 x 148 CTAs whatever N is (with whole rows per warp, N = 4096 leaves 256 CTAs of two rows per warp on
+// 148 SMs: a seventh of the machine idles through the second half of the launch).  The eight partial sums of a row meet in shared
+// memory and are added in warp order by one thread per row: the result does not depend on timing.
+template <typename T>
+__global__ void __launch_bounds__(256, 2) gemv_row_split_kernel(T* __restrict__ c, const T* __restrict__ a, const T* __restrict__ bt, int n,
+                                                                IterRef iter, int rows_max) {
+  using VT = typename V16<T>::type;
+  constexpr int W = V16<T>::W;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  VT* sa = reinterpret_cast<VT*>(smem_raw);                                                  // n / W vectors: row i of a
+  T* part = reinterpret_cast<T*>(smem_raw + static_cast<size_t>(n) * sizeof(T));            // [rows_max][8]
+  const int i = iter.off + (iter.base ? *iter.base : 0);
+  const int tid = threadIdx.x, lane = tid % 32, warp = tid / 32;
+  const int nv = n / W, seg = nv / 8;  // vectors per row, per warp (a multiple of 32: the launcher checks)
+  const VT* av = reinterpret_cast<const VT*>(a + static_cast<size_t>(i) * n);
+  for (int v = tid; v < nv; v += 256) sa[v] = av[v];
+  __syncthreads();
+
+  const int j0 = static_cast<int>(static_cast<long long>(blockIdx.x) * n / gridDim.x);
+  const int j1 = static_cast<int>(static_cast<long long>(blockIdx.x + 1) * n / gridDim.x);
+  const int v0 = warp * seg;
+  for (int j = j0; j < j1; ++j) {
+    const VT* r = reinterpret_cast<const VT*>(bt + static_cast<size_t>(j) * n) + v0;
+    T s0 = 0, s1 = 0;
+    int v = lane;
+    for (; v + 32 * (GEMV_Q - 1) < seg; v += 32 * GEMV_Q) {
+      VT x[GEMV_Q];
+#pragma unroll
+      for (int q = 0; q < GEMV_Q; ++q) x[q] = ld_stream(r + v + 32 * q);
+#pragma unroll
+      for (int q = 0; q < GEMV_Q; q += 2) {
+        s0 = vdot(sa[v0 + v + 32 * q], x[q], s0);
+        s1 = vdot(sa[v0 + v + 32 * (q + 1)], x[q + 1], s1);
+      }
+    }
+    if (v + 32 * 3 < seg) {  // four more (FP32 rows of 4096: the whole segment)
+      VT x[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) x[q] = ld_stream(r + v + 32 * q);
+#pragma unroll
+      for (int q = 0; q < 4; q += 2) {
+        s0 = vdot(sa[v0 + v + 32 * q], x[q], s0);
+        s1 = vdot(sa[v0 + v + 32 * (q + 1)], x[q + 1], s1);
+      }
+      v += 32 * 4;
+    }
+    for (; v < seg; v += 32) s0 = vdot(sa[v0 + v], ld_stream(r + v), s0);
+    s0 = warp_sum(s0 + s1);
+    if (lane == 0) part[(j - j0) * 8 + warp] = s0;
+  }
+  __syncthreads();
+  T* crow = c + static_cast<size_t>(i) * n;
+  for (int t = tid; t < j1 - j0; t += 256) {
+    T tot = 0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) tot += part[t * 8 + w];
+    crow[j0 + t] += tot;
+  }
+  (void)rows_max;
+}
+
 // STRICT: block = 64 threads owns 64 columns j; k is walked in tiles of 64 staged in smem.
 template <typename T>
 __global__ void __launch_bounds__(64) gemv_row_strict_kernel(T* __restrict__ c, const T* __restrict__ a,
@@ -345,7 +407,24 @@ cudaError_t launch_gemv_row(T* c, const T* a, const T* bt, int n, IterRef iter, 
         if (e != cudaSuccess) return e;
         configured = true;
       }
-      static const int form = [] { const char* e = getenv("MMX_GEMV_FORM"); return e ? atoi(e) : 0; }();  // tuning hook
+      static const int form = [] { const char* e = getenv("MMX_GEMV_FORM"); return e ? atoi(e) : 0; }();  // tuning hook: 1 staged, 2 split, 0 by size
+      const int nv = n / V16<T>::W;
+      // the split form wins where a row fills the staging buffer (64 KB: N = 8192 FP64 93 -> 84 us, N = 16384 FP32 168 -> 157) and
+      // loses below (N = 4096 FP32 18.4 -> 20.3): profiles/r2x_gemv_forms.txt
+      if ((form == 2 || (form == 0 && row_bytes >= 64 * 1024)) && nv % 256 == 0) {
+        static PerDeviceOnce once_split;
+        bool& split_ok = once_split.here();
+        if (!split_ok) {
+          if (cudaError_t e = cudaFuncSetAttribute(gemv_row_split_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024); e != cudaSuccess)
+            return e;
+          split_ok = true;
+        }
+        const int grid = n < 2 * kNumSMs ? n : 2 * kNumSMs;
+        const int rows_max = (n + grid - 1) / grid;
+        const size_t smem = row_bytes + static_cast<size_t>(rows_max) * 8 * sizeof(T);
+        gemv_row_split_kernel<T><<<grid, 256, smem, stream>>>(c, a, bt, n, iter, rows_max);
+        return cudaGetLastError();
+      }
       if (form == 1) {
         const int grid = n / 2 < 2 * kNumSMs ? n / 2 : 2 * kNumSMs;
         gemv_row_staged_kernel<T><<<grid, 256, row_bytes, stream>>>(c, a, bt, n, iter);
