@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
   constexpr int MB = kTile / V;         // micro-blocks per tile side == 16-byte chunks per tile row
   __shared__ __align__(16) VT tile[kTile * MB];   // the tile of b, input-ordered: tile[row][chunk], swizzled
 
-  const int in_row0 = blockIdx.y * kTile;   // rows of b  == columns of bt
+  // rows of b == columns of bt, last rows first: what the fill of b wrote last is what L2 still holds
+  const int in_row0 = static_cast<int>(gridDim.y - 1 - blockIdx.y) * kTile;
   const int in_col0 = first_row + blockIdx.x * kTile;   // cols of b  == rows of bt
   const int tid = threadIdx.x;
 
