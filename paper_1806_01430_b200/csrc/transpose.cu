@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
       const int v = tid + 256 * k;
       const int out_row = v / MB, chunk = v % MB;
       const VT val = gather_piece(tile, out_row, chunk);
-      *reinterpret_cast<VT*>(bt + static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V) = val;
+      __stcs(reinterpret_cast<VT*>(bt + static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V), val);
       bool tiny;
       const double inv = oz_row_scale(row_exp[k], true, false, &tiny);
       int top2;
