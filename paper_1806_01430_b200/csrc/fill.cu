@@ -7,6 +7,8 @@
 // When N is a power of two, x / N == x * (1/N) exactly, so the divide is replaced by one
 // multiply (POW2 path) -- same bits, and it keeps the nest write-bound instead of
 // FP64-divide-bound.
+#include <type_traits>
+
 #include "kernels.cuh"
 #include "ozaki_digits.cuh"
 
@@ -96,9 +98,13 @@ __global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst,
   const int i0 = blockIdx.y * kRowsPerThread;
   const int dirty = P.guard[P.dirty_slot];
   int lossy = 0, top = 0;
-  if (c0 < n) {
-    // pass 1, straight-line over the thread's 8 rows: the values, their stores, the row exponents and the first two digit levels
-    // (independent FP64 chains in one basic block); `more` collects the rows that have something below the second digit
+  // L = digit levels of the straight-line pass: two, or three once an earlier encoding of this operand has needed a third (from
+  // N = 8192 half of the application's elements do: (i + j) / N has 14 significant bits there, and with two levels every thread
+  // took the general walk of pass 2 -- 226 us instead of 118 for the 739 MB of this launch at N = 8192)
+  auto body = [&](auto levels) {
+    constexpr int L = decltype(levels)::value;
+    // pass 1, straight-line over the thread's 8 rows: the values, their stores, the row exponents and the first L digit levels
+    // (independent FP64 chains in one basic block); `more` collects the rows that have something below the last of them
     unsigned more = 0;
 #pragma unroll
     for (int r = 0; r < kRowsPerThread; ++r) {
@@ -123,16 +129,16 @@ __global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst,
         for (int w = 0; w < W; ++w) v[w] = static_cast<double>(x[w]);
         if constexpr (sizeof(T) == 8) *reinterpret_cast<double2*>(at) = make_double2(x[0], x[1]);
         else *reinterpret_cast<float4*>(at) = make_float4(x[0], x[1], x[2], x[3]);
-        int top2;
-        const bool left = oz_emit_first_two<W>(v, inv, drow, P.plane, j0, top2);
-        top = max(top, top2);
+        int top_l;
+        const bool left = oz_emit_first<W, L>(v, inv, drow, P.plane, j0, top_l);
+        top = max(top, top_l);
         more |= (left ? 1u : 0u) << r;
       }
     }
-    // pass 2 (rare): rows with longer elements, or planes beyond the second that earlier launches have used and that must be zeroed
-    if (more != 0 || dirty > 2) {
+    // pass 2 (rare): rows with longer elements, or planes beyond the L-th that earlier launches have used and that must be zeroed
+    if (more != 0 || dirty > L) {
       for (int r = 0; r < kRowsPerThread; ++r) {
-        if (!(more >> r & 1u) && dirty <= 2) continue;
+        if (!(more >> r & 1u) && dirty <= L) continue;
         const int i = i0 + r;
         const double m = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, n - 1, nn, inv_n));
         bool tiny;
@@ -147,6 +153,10 @@ __global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst,
         }
       }
     }
+  };
+  if (c0 < n) {
+    if (dirty == 3) body(std::integral_constant<int, 3>{});
+    else body(std::integral_constant<int, 2>{});
   }
   oz_guard_commit(lossy, top, P.guard, P.lossy_slot, P.top_slot, P.dirty_slot);
 }

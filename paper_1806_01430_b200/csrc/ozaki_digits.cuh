@@ -85,44 +85,58 @@ __device__ __forceinline__ void oz_emit(const double (&v)[W], double inv, bool b
   }
 }
 
-// The first two digit levels of W consecutive elements, straight-line: no early exits, both planes stored unconditionally, so that a
+// The first two (oz_emit_first<W, L>: the first L) digit levels of W consecutive elements, straight-line: no early exits, both planes stored unconditionally, so that a
 // caller that encodes several rows per thread gives the compiler ONE basic block of independent FP64 chains (the walk of oz_emit is
 // a chain of dependent FP64 operations per element and level with a branch after each level; on B200 those are long-latency
 // operations, and the producers that used oz_emit row by row spent half their issue slots waiting on them -- ncu, r2r_producers).
 // (oz_first_two_words hands the two packed words back instead of storing them.)  Returns true when something is left below the second digit: the caller then runs oz_emit on the same elements (rare path; it
 // rewrites the two planes with the same digits and continues).  top2: 0 / 1 / 2 = highest non-zero digit among the two.
-template <int W>
-__device__ __forceinline__ bool oz_first_two_words(const double (&v)[W], double inv, int& word0, int& word1) {
+template <int W, int L>
+__device__ __forceinline__ bool oz_first_words(const double (&v)[W], double inv, int (&word)[L]) {
   static_assert(W == 2 || W == 4, "digits are packed two or four to a word");
-  word0 = 0;
-  word1 = 0;
+  static_assert(L >= 1 && L <= 7, "digit levels");
+#pragma unroll
+  for (int l = 0; l < L; ++l) word[l] = 0;
   bool left = false;
 #pragma unroll
   for (int q = 0; q < W; ++q) {
     double rem = v[q] * inv;
-    const double s0 = fma(rem, 64.0, 6755399441055744.0);                 // digit 1: unit 2^-6
-    rem = fma(-(s0 - 6755399441055744.0), 0.015625, rem);
-    const double s1 = fma(rem, 8192.0, 6755399441055744.0);               // digit 2: unit 2^-13
-    rem = fma(-(s1 - 6755399441055744.0), 0.0001220703125, rem);
-    word0 |= (__double2loint(s0) & 0xff) << (8 * q);
-    word1 |= (__double2loint(s1) & 0xff) << (8 * q);
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      // digit l + 1: unit 2^-(7 (l + 1) - 1); the constants fold (64, 1/64, 8192, 1/8192, 2^20, ...)
+      const double s = fma(rem, oz_pow2(7 * (l + 1) - 1), 6755399441055744.0);
+      rem = fma(-(s - 6755399441055744.0), oz_pow2(-(7 * (l + 1) - 1)), rem);
+      word[l] |= (__double2loint(s) & 0xff) << (8 * q);
+    }
     left = left || rem != 0.0;
   }
   return left;
 }
+// the same with the words stored: plane l of the row at drow + l * plane; top = highest non-zero level (1-based, 0: all zero)
+template <int W, int L>
+__device__ __forceinline__ bool oz_emit_first(const double (&v)[W], double inv, signed char* __restrict__ drow, size_t plane, int k0, int& top) {
+  int word[L];
+  const bool left = oz_first_words<W, L>(v, inv, word);
+  top = 0;
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    if constexpr (W == 4) *reinterpret_cast<int*>(drow + l * plane + k0) = word[l];
+    else *reinterpret_cast<unsigned short*>(drow + l * plane + k0) = static_cast<unsigned short>(word[l]);
+    if (word[l] != 0) top = l + 1;
+  }
+  return left;
+}
+template <int W>
+__device__ __forceinline__ bool oz_first_two_words(const double (&v)[W], double inv, int& word0, int& word1) {
+  int word[2];
+  const bool left = oz_first_words<W, 2>(v, inv, word);
+  word0 = word[0];
+  word1 = word[1];
+  return left;
+}
 template <int W>
 __device__ __forceinline__ bool oz_emit_first_two(const double (&v)[W], double inv, signed char* __restrict__ drow, size_t plane, int k0, int& top2) {
-  int word0, word1;
-  const bool left = oz_first_two_words<W>(v, inv, word0, word1);
-  if constexpr (W == 4) {
-    *reinterpret_cast<int*>(drow + k0) = word0;
-    *reinterpret_cast<int*>(drow + plane + k0) = word1;
-  } else {
-    *reinterpret_cast<unsigned short*>(drow + k0) = static_cast<unsigned short>(word0);
-    *reinterpret_cast<unsigned short*>(drow + plane + k0) = static_cast<unsigned short>(word1);
-  }
-  top2 = word1 != 0 ? 2 : (word0 != 0 ? 1 : 0);
-  return left;
+  return oz_emit_first<W, 2>(v, inv, drow, plane, k0, top2);
 }
 
 // End of a CTA's work on an operand: fold the threads' lossy / top into the guard words (every thread of a 256-thread CTA calls).

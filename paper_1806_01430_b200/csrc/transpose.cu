@@ -11,6 +11,8 @@
 //
 // gene 7 (one row of bt per launch): row i of bt is column i of b -- a strided gather; each
 // 8-byte element costs a 32-byte sector, which is the sector amplification the catalogue notes.
+#include <type_traits>
+
 #include "kernels.cuh"
 #include "ozaki_digits.cuh"
 
@@ -46,7 +48,7 @@ __device__ __forceinline__ float4 gather_piece(const float4* tile, int out_row, 
 // PLANES: the digit planes of bt for gene 8 (ozaki_digits.cuh) are written from the same registers as bt itself; P.exps[j] must
 // already hold the exponent of row j of bt (launch_fill_b_colexp).
 template <typename T, bool PUSH, bool PLANES = false>
-__global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt, const T* __restrict__ b, int n, int first_row,
+__global__ void __launch_bounds__(256, PLANES ? (sizeof(T) == 8 ? 5 : 6) : 1) transpose_tile_kernel(T* __restrict__ bt, const T* __restrict__ b, int n, int first_row,
                                                              BtPeers peers, OzOperand P = OzOperand{}) {
   using VT = typename VecOf<T>::type;
   constexpr int V = VecOf<T>::V;
@@ -90,73 +92,85 @@ __global__ void __launch_bounds__(256) transpose_tile_kernel(T* __restrict__ bt,
     // the exponents of this thread's rows of bt and the dirty mark were requested before the tile was loaded (below): nothing in
     // the store loop waits on global memory.  Pass 1 is straight-line: store the piece, walk its first two digit levels
     // (oz_emit_first_two: independent FP64 chains, no branches); pass 2 (rare) re-reads from the tile the pieces that have more.
-    unsigned more = 0;
     // FP64: the digits of the tile are collected in shared memory (64 rows x 64 bytes per plane) and leave as 16-byte stores --
     // 2-byte stores straight from the walk cost eight times the store instructions for the same sectors (N = 8192: 211 -> 199 us).
     // FP32 pieces hold four elements: their 4-byte digit stores go out directly (staging them costs occupancy and gains nothing)
     constexpr bool STAGED = V == 2;
     __shared__ __align__(16) unsigned char dig[STAGED ? 2 : 1][STAGED ? kTile : 1][STAGED ? kTile : 16];
+    // L = digit levels of the straight-line pass: two, or three once an earlier encoding of bt has needed a third (the application
+    // from N = 16384); a third level goes out directly (a third staging plane would cost a CTA per SM)
+    auto body = [&](auto levels) {
+      constexpr int L = decltype(levels)::value;
+      unsigned more = 0;
 #pragma unroll
-    for (int k = 0; k < STEPS; ++k) {
-      const int v = tid + 256 * k;
-      const int out_row = v / MB, chunk = v % MB;
-      const VT val = gather_piece(tile, out_row, chunk);
-      __stcs(reinterpret_cast<VT*>(bt + static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V), val);
-      bool tiny;
-      const double inv = oz_row_scale(row_exp[k], true, false, &tiny);
-      int top2;
-      bool left;
-      if constexpr (V == 2) {
-        const double e2[2] = {val.x, val.y};
-        // not finite, or beyond what the exponent covers (it cannot happen while the executor's flags are right): cut
-        left = tiny || !(fabs(val.x) * inv < 1.0) || !(fabs(val.y) * inv < 1.0);
-        int word0, word1;
-        left = oz_first_two_words<2>(e2, inv, word0, word1) || left;
-        *reinterpret_cast<unsigned short*>(&dig[0][out_row][chunk * V]) = static_cast<unsigned short>(word0);
-        *reinterpret_cast<unsigned short*>(&dig[1][out_row][chunk * V]) = static_cast<unsigned short>(word1);
-        top2 = word1 != 0 ? 2 : (word0 != 0 ? 1 : 0);
-      } else {
-        const double e4[4] = {static_cast<double>(val.x), static_cast<double>(val.y), static_cast<double>(val.z), static_cast<double>(val.w)};
-        left = tiny;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) left = left || !(fabs(e4[q]) * inv < 1.0);
-        signed char* drow = P.planes + static_cast<size_t>(in_col0 + out_row) * P.kq;
-        left = oz_emit_first_two<4>(e4, inv, drow, P.plane, in_row0 + chunk * V, top2) || left;
-      }
-      top = max(top, top2);
-      more |= (left ? 1u : 0u) << k;
-    }
-    if constexpr (STAGED) {
-      __syncthreads();
-#pragma unroll
-      for (int p = 0; p < 2; ++p) {
-        const int row = tid / 4, q = tid % 4;
-        *reinterpret_cast<int4*>(P.planes + p * P.plane + static_cast<size_t>(in_col0 + row) * P.kq + in_row0 + q * 16) =
-            *reinterpret_cast<const int4*>(&dig[p][row][q * 16]);
-      }
-    }
-    if (more != 0 || dirty > 2) {
       for (int k = 0; k < STEPS; ++k) {
-        if (!(more >> k & 1u) && dirty <= 2) continue;
         const int v = tid + 256 * k;
         const int out_row = v / MB, chunk = v % MB;
         const VT val = gather_piece(tile, out_row, chunk);
+        __stcs(reinterpret_cast<VT*>(bt + static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V), val);
         bool tiny;
         const double inv = oz_row_scale(row_exp[k], true, false, &tiny);
-        lossy |= tiny;
         signed char* drow = P.planes + static_cast<size_t>(in_col0 + out_row) * P.kq;
+        int top_l = 0;
+        bool left;
         if constexpr (V == 2) {
           const double e2[2] = {val.x, val.y};
-          lossy |= !(fabs(val.x) * inv < 1.0) | !(fabs(val.y) * inv < 1.0);
-          oz_emit<7, 2>(e2, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
+          // not finite, or beyond what the exponent covers (it cannot happen while the executor's flags are right): cut
+          left = tiny || !(fabs(val.x) * inv < 1.0) || !(fabs(val.y) * inv < 1.0);
+          int word[L];
+          left = oz_first_words<2, L>(e2, inv, word) || left;
+          *reinterpret_cast<unsigned short*>(&dig[0][out_row][chunk * V]) = static_cast<unsigned short>(word[0]);
+          *reinterpret_cast<unsigned short*>(&dig[1][out_row][chunk * V]) = static_cast<unsigned short>(word[1]);
+#pragma unroll
+          for (int l = 2; l < L; ++l)
+            *reinterpret_cast<unsigned short*>(drow + l * P.plane + in_row0 + chunk * V) = static_cast<unsigned short>(word[l]);
+#pragma unroll
+          for (int l = 0; l < L; ++l)
+            if (word[l] != 0) top_l = l + 1;
         } else {
           const double e4[4] = {static_cast<double>(val.x), static_cast<double>(val.y), static_cast<double>(val.z), static_cast<double>(val.w)};
+          left = tiny;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) lossy |= !(fabs(e4[q]) * inv < 1.0);
-          oz_emit<7, 4>(e4, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
+          for (int q = 0; q < 4; ++q) left = left || !(fabs(e4[q]) * inv < 1.0);
+          left = oz_emit_first<4, L>(e4, inv, drow, P.plane, in_row0 + chunk * V, top_l) || left;
+        }
+        top = max(top, top_l);
+        more |= (left ? 1u : 0u) << k;
+      }
+      if constexpr (STAGED) {
+        __syncthreads();
+#pragma unroll
+        for (int p = 0; p < 2; ++p) {
+          const int row = tid / 4, q = tid % 4;
+          *reinterpret_cast<int4*>(P.planes + p * P.plane + static_cast<size_t>(in_col0 + row) * P.kq + in_row0 + q * 16) =
+              *reinterpret_cast<const int4*>(&dig[p][row][q * 16]);
         }
       }
-    }
+      if (more != 0 || dirty > L) {
+        for (int k = 0; k < STEPS; ++k) {
+          if (!(more >> k & 1u) && dirty <= L) continue;
+          const int v = tid + 256 * k;
+          const int out_row = v / MB, chunk = v % MB;
+          const VT val = gather_piece(tile, out_row, chunk);
+          bool tiny;
+          const double inv = oz_row_scale(row_exp[k], true, false, &tiny);
+          lossy |= tiny;
+          signed char* drow = P.planes + static_cast<size_t>(in_col0 + out_row) * P.kq;
+          if constexpr (V == 2) {
+            const double e2[2] = {val.x, val.y};
+            lossy |= !(fabs(val.x) * inv < 1.0) | !(fabs(val.y) * inv < 1.0);
+            oz_emit<7, 2>(e2, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
+          } else {
+            const double e4[4] = {static_cast<double>(val.x), static_cast<double>(val.y), static_cast<double>(val.z), static_cast<double>(val.w)};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) lossy |= !(fabs(e4[q]) * inv < 1.0);
+            oz_emit<7, 4>(e4, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
+          }
+        }
+      }
+    };
+    if (dirty == 3) body(std::integral_constant<int, 3>{});
+    else body(std::integral_constant<int, 2>{});
     oz_guard_commit(lossy, top, P.guard, P.lossy_slot, P.top_slot, P.dirty_slot);
   } else {
 #pragma unroll

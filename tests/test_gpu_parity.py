@@ -1076,6 +1076,25 @@ def test_largest_configuration_matches_the_closed_form_on_sampled_row_blocks():
             assert bits_equal(ctx.fetch_rows(capi.ARRAY_BT, r0, rows), (j[None, :] - i) / n)
 
 
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("n,form", [(8192, 324), (16384, 335)])
+def test_three_digit_operands_from_the_producers_match_the_closed_form(n, form):
+    """From N = 8192 the elements of a need a third 7-bit digit, from N = 16384 those of bt too: once an encoding has used three
+    levels the producers walk three levels straight-line (fill.cu / transpose.cu, `dirty == 3`).  The first individual of a context
+    takes the two-level pass plus the general walk, the following ones the three-level pass: both must give the closed form."""
+    with capi.Context(n=n, dtype=capi.F64, timeout_s=600.0) as ctx:
+        j = np.arange(n, dtype=np.float64)
+        for _ in range(3):
+            out = ctx.measure("101010101001")
+            assert out.status == capi.MEASURED and ctx.stats().checksum == 0.0 and ctx.gene8_form() == form
+            for r0 in (0, 64, n // 2 - 64, n // 2, (2 * n // 3) // 64 * 64, n - 64):
+                got = ctx.fetch_rows(capi.ARRAY_C, r0, 64)
+                assert bits_equal(got, cpu.closed_form_c(n, r0, r0 + 64)), f"rows [{r0}, {r0 + 64}) of c"
+                i = np.arange(r0, r0 + 64, dtype=np.float64)[:, None]
+                assert bits_equal(ctx.fetch_rows(capi.ARRAY_A, r0, 64), (i + j[None, :]) / n)
+                assert bits_equal(ctx.fetch_rows(capi.ARRAY_BT, r0, 64), (j[None, :] - i) / n)
+
+
 # ---- host isolation of concurrent measurements (SURVEY H8) -----------------------------------------------------------------------------
 def _physical_cores():
     import os
