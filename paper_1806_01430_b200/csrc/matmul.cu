@@ -227,7 +227,7 @@ __global__ void __launch_bounds__(32 * WM * WN, (WM * WN <= 4 && MT * NT <= 16) 
 matmul_dmma_kernel(double* __restrict__ c, const double* __restrict__ a, const double* __restrict__ bt, int n,
                    int row0, int rows, int col0, int cols, int group, const int* __restrict__ run_if) {
   // guarded launch (FP64 auto mode): the tensor-core kernel took this contraction
-  if (run_if != nullptr && ozaki_pick_form(run_if[0] | run_if[3], run_if[1], run_if[2]) != 0) return;  // the tensor-core launch took it
+  if (run_if != nullptr && run_if[4] != 0) return;  // run_if[4]: the form the auto kernel before this launch recorded; non-zero = it took the product
   constexpr int THREADS = 32 * WM * WN;
   constexpr int TM = WM * MT * 8, TN = WN * NT * 8;
   constexpr int DLD = DK + 4;  // padded row: (DK+4)*8 B = 32 mod 128 for DK in {16, 32} => conflict-free fragments

@@ -2,14 +2,18 @@
 // (fixtures/matmul.c:25-28) as an error-free INT8 slice decomposition (Ozaki scheme) on tcgen05.mma.kind::i8.
 //
 // B200 has no FP64 tensor-core kind and its FP64 pipe peaks at 36 TFLOP/s, but INT8 MMAs with INT32 accumulation are
-// EXACT and ~120x faster per operation.  Each operand row is scaled by a power of two and cut into S signed 7-bit digits,
-//     x = 2^e * (d_1 2^-6 + d_2 2^-13 + ... + d_S 2^-(7S-1)) + r,   |d_t| <= 64,  |r| <= 2^(e - 7S)
-// (every step exact in FP64: power-of-two scaling, rint, subtraction of a prefix of x's own bits), so
-//     sum_k a_ik b_jk = 2^(ea_i + eb_j + 2) * sum_g 2^(-7g) L_g,        L_g = sum_{t+u=g} sum_k da_t[i][k] db_u[j][k]
-// where every L_g is an integer dot product the tensor core computes without rounding (|L_g| <= 7 * K * 2^12 < 2^31 for
-// K <= 74k).  Levels g > S + 1 are dropped: |error| <= (S + 3) K 2^(-7S) * max_k|a_ik| max_k|b_jk|, i.e. 2e-14 K max max for
-// S = 7 -- below what FP64 accumulation over K terms itself guarantees -- and ZERO whenever the operands carry <= 7S bits
-// below their row maximum: on the application's inputs ((i +- k) / N, 14 bits) the result is bit-identical to the CPU program.
+// EXACT and ~120x faster per operation.  Each operand row is scaled by a power of two and cut into S signed digits -- a first
+// one of 7 bits, 8-bit ones below it (ozaki_digits.cuh) --
+//     x = 2^e * (d_1 2^-6 + d_2 2^-14 + ... + d_S 2^-(8S-2)) + r,   |d_1| <= 64,  -128 <= d_t <= 127,  |r| <= 2^(e - 8S + 1)
+// (every step exact in FP64: power-of-two scaling, rounding to an integer, subtraction of a prefix of x's own bits), so
+//     sum_k a_ik b_jk = 2^(ea_i + eb_j + 4) * sum_g 2^(-8g) L_g,        L_g = sum_{t+u=g} sum_k da_t[i][k] db_u[j][k]
+// where every L_g is an integer dot product the tensor core computes without rounding: per term |d_1 d_u| <= 2^13 and
+// |d_t d_u| <= 2^14, so a level with p digit pairs stays below (p - 1) K 2^14 -- inside INT32 while K (p - 1) < 2^17 (p <= 4 at
+// K = 32768, any p up to K = 16384; oz_form_fits_int32 refuses the rest).  Levels g > S + 1 are dropped:
+// |error| <= (S + 3) K 2^(-7S) * max_k|a_ik| max_k|b_jk| (the bound of 7-bit digits; the 8-bit ones are inside it), i.e.
+// 2e-14 K max max for S = 7 -- below what FP64 accumulation over K terms itself guarantees -- and ZERO whenever the operands
+// carry <= 8S - 2 bits below their row maximum: on the application's inputs ((i +- k) / N: 14 bits at N = 4096, two digits up to
+// a = (i + k) / N at N = 8192 and bt at N = 16384) the result is bit-identical to the CPU program.
 //
 // Who runs it.  matmul_variant 40 .. 45: always, as the triangular form with S = 7 .. 2 slices (general kernels: ~2^-49 .. of
 // K max max).  Auto mode (variant 0, N >= 1024; launch_matmul<double> in matmul.cu): only where it is ERROR-FREE.  The slice pass
@@ -82,6 +86,7 @@ __device__ __forceinline__ void tc_mma_i8(unsigned d_tmem, unsigned long long ad
 }
 
 __device__ __forceinline__ double pow2(int e) { return oz_pow2(e); }
+constexpr double kOzLevelStep = 1.0 / (1 << kOzDigitBits);  // level g + 1 weighs 2^-kOzDigitBits of level g (ozaki_digits.cuh: 8-bit digits below the first)
 
 constexpr int kNonFinite = kOzNonFinite;  // row exponent of a row that holds an Inf or a NaN: its products are NaN
 // acc * 2^(ea + eb - 12): exact scaling (ldexp also covers results that leave the normal range)
@@ -244,7 +249,7 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
         for (int h = 0; h < 2; ++h) {
           double acc = static_cast<double>(static_cast<int>(lv[S - 1][e + h]));
 #pragma unroll
-          for (int g = S - 2; g >= 0; --g) acc = fma(acc, 0.0078125, static_cast<double>(static_cast<int>(lv[g][e + h])));
+          for (int g = S - 2; g >= 0; --g) acc = fma(acc, kOzLevelStep, static_cast<double>(static_cast<int>(lv[g][e + h])));
           v[h] = cpre[cb * 8 + e + h] + scaled(acc, ei, eb_sh[cb * 8 + e + h]);
         }
         if (!row_ok) continue;
@@ -560,12 +565,12 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
               if constexpr (LV <= 4) {
                 long long x = static_cast<int>(lv[0][e]);
 #pragma unroll
-                for (int l = 1; l < LV; ++l) x = (x << 7) + static_cast<int>(lv[l][e]);
+                for (int l = 1; l < LV; ++l) x = (x << kOzDigitBits) + static_cast<int>(lv[l][e]);
                 acc[jj][h * LD + e] = x;
               } else {
                 double x = static_cast<double>(static_cast<int>(lv[LV - 1][e]));
 #pragma unroll
-                for (int l = LV - 2; l >= 0; --l) x = fma(x, 0.0078125, static_cast<double>(static_cast<int>(lv[l][e])));
+                for (int l = LV - 2; l >= 0; --l) x = fma(x, kOzLevelStep, static_cast<double>(static_cast<int>(lv[l][e])));
                 hsum[jj][h * LD + e] = x;
               }
             }
@@ -593,7 +598,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
               cols_fast &= static_cast<unsigned>(ebv[e] + 399) < 799u;
             }
             if (cols_fast && row_fast) {
-              const int e_row = ei - 12 - 7 * (LV - 1);
+              const int e_row = ei - 12 - kOzDigitBits * (LV - 1);
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
                 const long long x = acc[jj][e];
@@ -603,7 +608,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
               }
             } else {
 #pragma unroll  // (a rolled loop would index acc and v dynamically and push them to local memory for both branches)
-              for (int e = 0; e < 16; ++e) v[e] = scaled(static_cast<double>(acc[jj][e]) * pow2(-7 * (LV - 1)), ei, ebv[e]);
+              for (int e = 0; e < 16; ++e) v[e] = scaled(static_cast<double>(acc[jj][e]) * pow2(-kOzDigitBits * (LV - 1)), ei, ebv[e]);
             }
           } else {
 #pragma unroll
@@ -749,7 +754,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
               for (int h = 0; h < 2; ++h) {
                 double sum = static_cast<double>(static_cast<int>(lv[LV - 1][e + h]));
 #pragma unroll
-                for (int l = LV - 2; l >= 0; --l) sum = fma(sum, 0.0078125, static_cast<double>(static_cast<int>(lv[l][e + h])));
+                for (int l = LV - 2; l >= 0; --l) sum = fma(sum, kOzLevelStep, static_cast<double>(static_cast<int>(lv[l][e + h])));
                 const int col = part * 32 + cb * 8 + e + h;
                 v[h] = cpre[cb * 8 + e + h] + scaled_fast(sum, ei, pa, row_fast, eb[col], pb[col]);
               }
@@ -1005,12 +1010,12 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
             if constexpr (LV <= 4) {
               long long x = static_cast<int>(lv[0][e]);
 #pragma unroll
-              for (int l = 1; l < LV; ++l) x = (x << 7) + static_cast<int>(lv[l][e]);
+              for (int l = 1; l < LV; ++l) x = (x << kOzDigitBits) + static_cast<int>(lv[l][e]);
               acc[jj][h * LD + e] = x;
             } else {
               double x = static_cast<double>(static_cast<int>(lv[LV - 1][e]));
 #pragma unroll
-              for (int l = LV - 2; l >= 0; --l) x = fma(x, 0.0078125, static_cast<double>(static_cast<int>(lv[l][e])));
+              for (int l = LV - 2; l >= 0; --l) x = fma(x, kOzLevelStep, static_cast<double>(static_cast<int>(lv[l][e])));
               hsum[jj][h * LD + e] = x;
             }
           }
@@ -1035,7 +1040,7 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
             cols_fast &= static_cast<unsigned>(ebv[e] + 399) < 799u;
           }
           if (cols_fast && row_fast) {
-            const int e_row = ei - 12 - 7 * (LV - 1);
+            const int e_row = ei - 12 - kOzDigitBits * (LV - 1);
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               const long long x = acc[jj][e];
@@ -1045,7 +1050,7 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
             }
           } else {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = scaled(static_cast<double>(acc[jj][e]) * pow2(-7 * (LV - 1)), ei, ebv[e]);
+            for (int e = 0; e < 16; ++e) v[e] = scaled(static_cast<double>(acc[jj][e]) * pow2(-kOzDigitBits * (LV - 1)), ei, ebv[e]);
           }
         } else {
 #pragma unroll
@@ -1111,7 +1116,8 @@ template <int CX, int CY, typename CT>
 __global__ void __launch_bounds__(OZP_THREADS, 1)
 matmul_ozaki_auto_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, const int* __restrict__ guard, int* __restrict__ ran) {
   extern __shared__ unsigned char smem_raw[];
-  const int form = sizeof(CT) == 8 ? ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]) : ozaki_pick_form_f32(guard[0] | guard[3], guard[1], guard[2]);
+  int form = sizeof(CT) == 8 ? ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]) : ozaki_pick_form_f32(guard[0] | guard[3], guard[1], guard[2]);
+  if (!oz_form_fits_int32(form, g.kq)) form = 0;  // the level sums could leave INT32: the fallback takes the product
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *ran = form;
     if (g.use_cond) cudaGraphSetConditional(g.cond, form == 0 ? 1u : 0u);
@@ -1140,7 +1146,8 @@ template <typename CT>
 __global__ void __launch_bounds__(OZP_THREADS, 1)
 matmul_ozaki_auto_pair_kernel(const OzPArgs g, const __grid_constant__ OzMaps maps, const int* __restrict__ guard, int* __restrict__ ran) {
   extern __shared__ unsigned char smem_raw[];
-  const int form = sizeof(CT) == 8 ? ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]) : ozaki_pick_form_f32(guard[0] | guard[3], guard[1], guard[2]);
+  int form = sizeof(CT) == 8 ? ozaki_pick_form(guard[0] | guard[3], guard[1], guard[2]) : ozaki_pick_form_f32(guard[0] | guard[3], guard[1], guard[2]);
+  if (!oz_form_fits_int32(form, g.kq)) form = 0;  // the level sums could leave INT32: the fallback takes the product
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     *ran = form;
     if (g.use_cond) cudaGraphSetConditional(g.cond, form == 0 ? 1u : 0u);
@@ -1707,6 +1714,7 @@ cudaError_t launch_matmul_ozaki(double* c, const double* a, const double* bt, vo
     return oz_go<7, 1, 64>(c, a, bt, scratch, n, row0, rows, col0, cols, stream);
   }
   // a fixed slice count: S planes are written and contracted (a general kernel with the truncation bound of the header)
+  if (!oz_form_fits_int32(slices * 111, oz_kq(n))) return cudaErrorNotSupported;  // the level sums could leave INT32 at this K
   cudaError_t e = cudaErrorInvalidValue;
   switch (slices) {
     case 2: e = oz_slices<2>(a, bt, scratch, n, row0, rows, col0, cols, stream, false, reuse_a); break;

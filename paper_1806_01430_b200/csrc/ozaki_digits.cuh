@@ -3,7 +3,14 @@
 // separate slice pass reading the operand back from HBM (the slice pass stays for operands that arrive any other way).
 //
 // Encoding (matmul_ozaki.cu header): row r of an operand is scaled by 2^-e_r, e_r = ilogb(max_k |x_rk|) + 1, and cut into signed
-// 7-bit digits d_1 .. d_S, x = 2^e (d_1 2^-6 + d_2 2^-13 + ...) + remainder, every step exact in FP64.  Plane t of row r lives
+// digits d_1 .. d_S, x = 2^e (d_1 2^-6 + d_2 2^-14 + d_3 2^-22 + ...) + remainder, every step exact in FP64: a first digit of 7 bits
+// (|d_1| <= 64, since |x| < 2^e) and digits of 8 bits below it (-128 <= d_t <= 127) -- what an int8 holds.  Digit t has the unit
+// 2^-oz_unit(t - 1).  Eight bits per digit need a lopsided rounding: the part left after a digit must lie in (-128.5 / 256, 127.5 / 256]
+// of the digit's unit RECURSIVELY, i.e. in (c - 1, c] with c = 127 / 255, or a later digit would have to be +128; so
+// d = ceil(R - c) = rint(R + 1 / 510) (R = what is left, in units of the digit; never a tie for finite binary R).  1 / 510 is not a
+// binary fraction and R + 1 / 510 is rounded: an R within 2^-46 of the boundary may get the other digit, which shows up as a digit
+// outside [-128, 127] one level down -- checked, and reported like bits below the last digit (the operand counts as cut and the
+// product goes to the FP64 pipe).  Plane t of row r lives
 // at planes + t * plane + r * kq.  The guard words record whether any element has bits below its 7th digit (or is not finite)
 // and the highest non-zero digit of each operand; the contraction kernel picks its form from them (ozaki_pick_form).
 #pragma once
@@ -19,6 +26,20 @@ constexpr int kOzNonFinite = 0x7fffffff;  // row exponent of a row that holds an
 #ifdef __CUDACC__
 
 __device__ __forceinline__ double oz_pow2(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
+
+constexpr int kOzDigitBits = 8;  // bits per digit below the first (the level step of the contraction's Horner sum)
+// digit t + 1 (t = 0, 1, ...) has the unit 2^-oz_unit(t): 6, 14, 22, ...
+__host__ __device__ constexpr int oz_unit(int t) { return 6 + kOzDigitBits * t; }
+constexpr double kOzRoundBias = 1.0 / 510.0;  // 1/2 - 127/255
+
+// one digit off `rem` (scaled so that the digit's unit is 1 / up): returns it, leaves the rest in rem (exact); out_of_range: not an int8
+__device__ __forceinline__ int oz_take_digit(double& rem, double up, double down, bool& out_of_range) {
+  const double s = fma(rem, up, kOzRoundBias) + 6755399441055744.0;  // rint without the conversion units: + 1.5 * 2^52
+  const int d = __double2loint(s);
+  rem = fma(-(s - 6755399441055744.0), down, rem);  // exact: removes a prefix of rem's bits
+  out_of_range = out_of_range || static_cast<unsigned>(d + 128) > 255u;
+  return d;
+}
 
 // exponent of a row whose largest magnitude is m (bad: the row holds a non-finite value): |x| < 2^e for every element
 __device__ __forceinline__ int oz_row_exponent(double m, bool bad) { return (m > 0.0 && !bad) ? ilogb(m) + 1 : 0; }
@@ -57,17 +78,12 @@ __device__ __forceinline__ void oz_emit(const double (&v)[W], double inv, bool b
       levels = t;
       break;
     }
-    const double up = oz_pow2(7 * (t + 1) - 1), down = oz_pow2(-(7 * (t + 1) - 1));
+    const double up = oz_pow2(oz_unit(t)), down = oz_pow2(-oz_unit(t));
     int word = 0;
+    bool bad_digit = false;
 #pragma unroll
-    for (int q = 0; q < W; ++q) {
-      // rint without the conversion units (they would bound this pass): adding 1.5 * 2^52 rounds to the integer grid
-      // (ties to even) and leaves the integer in the low word of the sum
-      const double shifted = fma(rem[q], up, 6755399441055744.0);
-      const int d = __double2loint(shifted);
-      rem[q] = fma(-(shifted - 6755399441055744.0), down, rem[q]);  // exact: removes a prefix of rem's bits
-      word |= (d & 0xff) << (8 * q);
-    }
+    for (int q = 0; q < W; ++q) word |= (oz_take_digit(rem[q], up, down, bad_digit) & 0xff) << (8 * q);
+    lossy |= bad_digit;
     dig[t] = word;
   }
   // bits below the last digit: the slices do not reproduce this element exactly
@@ -102,12 +118,8 @@ __device__ __forceinline__ bool oz_first_words(const double (&v)[W], double inv,
   for (int q = 0; q < W; ++q) {
     double rem = v[q] * inv;
 #pragma unroll
-    for (int l = 0; l < L; ++l) {
-      // digit l + 1: unit 2^-(7 (l + 1) - 1); the constants fold (64, 1/64, 8192, 1/8192, 2^20, ...)
-      const double s = fma(rem, oz_pow2(7 * (l + 1) - 1), 6755399441055744.0);
-      rem = fma(-(s - 6755399441055744.0), oz_pow2(-(7 * (l + 1) - 1)), rem);
-      word[l] |= (__double2loint(s) & 0xff) << (8 * q);
-    }
+    for (int l = 0; l < L; ++l)  // digit l + 1; the constants fold (64, 1/64, 16384, 1/16384, ...)
+      word[l] |= (oz_take_digit(rem, oz_pow2(oz_unit(l)), oz_pow2(-oz_unit(l)), left) & 0xff) << (8 * q);
     left = left || rem != 0.0;
   }
   return left;

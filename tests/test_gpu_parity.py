@@ -1077,11 +1077,12 @@ def test_largest_configuration_matches_the_closed_form_on_sampled_row_blocks():
 
 
 @pytest.mark.timeout(600)
-@pytest.mark.parametrize("n,form", [(8192, 324), (16384, 335)])
+@pytest.mark.parametrize("n,form", [(8192, 223), (16384, 324)])
 def test_three_digit_operands_from_the_producers_match_the_closed_form(n, form):
-    """From N = 8192 the elements of a need a third 7-bit digit, from N = 16384 those of bt too: once an encoding has used three
-    levels the producers walk three levels straight-line (fill.cu / transpose.cu, `dirty == 3`).  The first individual of a context
-    takes the two-level pass plus the general walk, the following ones the three-level pass: both must give the closed form."""
+    """Two digits (7 + 8 bits) carry the application's operands up to N = 8192; at N = 16384 the elements of a need a third (bt from
+    32768, the test above): once an encoding has used three levels the producers walk three levels straight-line (fill.cu /
+    transpose.cu, `dirty == 3`).  The first individual of a context takes the two-level pass plus the general walk, the following
+    ones the three-level pass: both must give the closed form."""
     with capi.Context(n=n, dtype=capi.F64, timeout_s=600.0) as ctx:
         j = np.arange(n, dtype=np.float64)
         for _ in range(3):

@@ -8,17 +8,24 @@ import pytest
 S = 7
 
 
+def unit(t):
+    """digit t (1-based) has the unit 2^-unit(t): a first digit of 7 bits, 8-bit digits below it (csrc/ozaki_digits.cuh)"""
+    return 6 + 8 * (t - 1)
+
+
 def slices(x):
-    """rows of x -> (exponents e, digits d[t] as int64 arrays, remainder r) with x = 2^e (sum_t d_t 2^-(7t-1)) + 2^e r."""
+    """rows of x -> (exponents e, digits d[t] as int64 arrays, remainder r) with x = 2^e (sum_t d_t 2^-unit(t)) + 2^e r.
+    Every digit is what an int8 holds; the lopsided rounding d = ceil(R - 127/255) keeps what is left inside (c - 1, c] of the
+    digit's unit, c = 127/255, so that the next digit is never +128."""
     mx = np.abs(x).max(axis=1)
     e = np.where(mx > 0, np.floor(np.log2(np.maximum(mx, 1e-300))).astype(np.int64) + 1, 0)
     rem = x * np.exp2(-e.astype(np.float64))[:, None]
     assert (np.abs(rem) < 1).all()
     digits = []
     for t in range(1, S + 1):
-        d = np.rint(rem * 2.0 ** (7 * t - 1))
-        rem = rem - d * 2.0 ** -(7 * t - 1)          # exact in float64
-        assert (np.abs(d) <= 64).all()
+        d = np.rint(rem * 2.0 ** unit(t) + 1.0 / 510.0)
+        rem = rem - d * 2.0 ** -unit(t)          # exact in float64
+        assert (np.abs(d) <= 64).all() if t == 1 else ((d >= -128) & (d <= 127)).all()
         digits.append(d.astype(np.int64))
     return e, digits, rem
 
@@ -30,7 +37,7 @@ def contract(a, bt, c0, keep=S + 1):
     for g in range(keep, 1, -1):                     # Horner from the smallest level, as the epilogue does
         level = sum(da[t - 1] @ db[g - t - 1].T for t in range(1, S + 1) if 1 <= g - t <= S)
         assert np.abs(level).max() < 2 ** 31         # INT32 accumulators
-        acc = acc / 128.0 + level
+        acc = acc / 256.0 + level
     return c0 + np.ldexp(acc, (ea[:, None] + eb[None, :] - 12).astype(np.int64))
 
 
@@ -44,7 +51,7 @@ def test_application_operands_use_two_digits_and_the_product_is_exact(n):
     a, bt = app_operands(n)
     for x in (a, bt):
         _, d, rem = slices(x)
-        assert (rem == 0).all() and all((dt == 0).all() for dt in d[2:])     # 14 bits: digits 1 and 2 only, so even the
+        assert (rem == 0).all() and all((dt == 0).all() for dt in d[2:])     # log2(N) + 2 bits: digits 1 and 2 only, so even the
         # 6-slice form (digits <= 6, pairs t + u <= 7) keeps every non-zero pair: the cheapest error-free form of auto mode
     i = np.arange(n, dtype=np.float64)
     s1, s2 = n * (n - 1) / 2, (n - 1) * n * (2 * n - 1) / 6
@@ -88,8 +95,8 @@ def test_guard_condition_is_the_error_free_condition():
     assert not cut_a and not cut_b and ta + tb > S + 1
     exact = a.astype(np.int64).astype(object) @ bt.astype(np.int64).astype(object).T
     assert (contract(a, bt, c0).astype(object) != exact).any()
-    # full-mantissa doubles: elements are cut
-    assert top(rs.uniform(-1, 1, (n, n)))[0]
+    # full-mantissa doubles of mixed magnitude (seven digits reach 54 bits below the row maximum): elements are cut
+    assert top(rs.uniform(-1, 1, (n, n)) * np.exp2(-rs.randint(0, 20, (n, n)).astype(np.float64)))[0]
 
 
 # ---- the forms of the persistent kernel (matmul_ozaki.cu: <SA, SB, LV>) and the rule that picks one -------------------------
@@ -104,7 +111,7 @@ def pairs_of(form):
 
 def test_rectangular_form_reproduces_the_product_exactly():
     """Digits a_1..a_SA against b_1..b_SB, every pair: when no operand has a digit beyond (SA, SB) the level sums, weighted
-    2^(-7 (t + u)), are the exact product -- with integers only."""
+    2^-(unit(t) + unit(u)), are the exact product -- with integers only."""
     rs = np.random.RandomState(5)
     k = 96
     for sa, sb in ((2, 2), (3, 2), (2, 3), (4, 4)):
@@ -119,10 +126,10 @@ def test_rectangular_form_reproduces_the_product_exactly():
             for u in range(1, sb + 1):
                 level = da[t - 1].astype(np.int64) @ db[u - 1].astype(np.int64).T
                 assert np.abs(level).max() < 2 ** 31
-                total = total + level.astype(object) * 2 ** (7 * (7 + 7 - t - u))      # common denominator 2^(7 * 14)
+                total = total + level.astype(object) * 2 ** (2 * unit(S) - unit(t) - unit(u))      # common denominator 2^(2 unit(S))
         exact = a.astype(np.int64).astype(object) @ b.astype(np.int64).astype(object).T
-        scale = np.array([[2 ** (int(x) + int(y) + 2) for y in eb] for x in ea], dtype=object)
-        assert (total * scale == exact * 2 ** (7 * 14)).all()
+        scale = np.array([[2 ** (int(x) + int(y)) for y in eb] for x in ea], dtype=object)
+        assert (total * scale == exact * 2 ** (2 * unit(S))).all()
 
 
 def test_pick_form_takes_the_cheapest_error_free_form():
