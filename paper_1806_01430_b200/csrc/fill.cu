@@ -62,9 +62,12 @@ __global__ void __launch_bounds__(256) fill2d_kernel(T* __restrict__ dst, int n,
 #pragma unroll
     for (int q = 0; q < V; ++q) {
       if (j0 + q >= n) break;
-      const double top = fabs(static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(0, j0 + q, nn, inv)));
-      const double bot = fabs(static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(n - 1, j0 + q, nn, inv)));
-      colexp[j0 + q] = oz_row_exponent(fmax(top, bot), false);
+      // (i - j) / N grows with i: the column's smallest element is its first, the largest its last
+      const double top = static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(0, j0 + q, nn, inv));
+      const double bot = static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(n - 1, j0 + q, nn, inv));
+      double scale;
+      bool tiny;
+      colexp[j0 + q] = oz_row_code(bot, top, false, true, &scale, &tiny);
     }
   }
   const int row0 = first_row + (blockIdx.y * blockDim.y + threadIdx.y) * kRowsPerThread;
@@ -89,7 +92,7 @@ inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 // instruction of a warp is one contiguous run of whole sectors (a thread owning 32 consecutive bytes would write each sector in two
 // halves, from two instructions): it stores them and, from the same registers, their 7-bit digits (16 / 32 bits per plane and
 // piece).  The row exponent needs the row's largest magnitude: (i + j) / N is non-negative and grows with j, so it is the row's
-// last element -- every thread computes it for itself.
+// first and last element -- every thread computes it for itself.
 template <typename T, bool POW2>
 __global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst, int n, T nn, T inv_n, OzOperand P) {
   constexpr int W = 16 / sizeof(T);          // elements per piece: 2 doubles / 4 floats
@@ -109,12 +112,14 @@ __global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst,
 #pragma unroll
     for (int r = 0; r < kRowsPerThread; ++r) {
       const int i = i0 + r;  // (n is a multiple of 64 here: every row of the block exists -- no test, one basic block)
-      const double m = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, n - 1, nn, inv_n));
-      const int e = oz_row_exponent(m, false);
+      // (i + j) / N grows with j: the row's smallest element is its first, the largest its last
+      const double lo = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, 0, nn, inv_n));
+      const double hi = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, n - 1, nn, inv_n));
       bool tiny;
-      const double inv = oz_row_scale(e, true, false, &tiny);
+      double inv;
+      const int word_e = oz_row_code(hi, lo, false, true, &inv, &tiny);
       lossy |= tiny;
-      if (c0 == 0) P.exps[i] = e;
+      if (c0 == 0) P.exps[i] = word_e;
       signed char* drow = P.planes + static_cast<size_t>(i) * P.kq;
 #pragma unroll
       for (int q = 0; q < PIECES; ++q) {
@@ -140,9 +145,11 @@ __global__ void __launch_bounds__(256) fill_a_planes_kernel(T* __restrict__ dst,
       for (int r = 0; r < kRowsPerThread; ++r) {
         if (!(more >> r & 1u) && dirty <= L) continue;
         const int i = i0 + r;
-        const double m = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, n - 1, nn, inv_n));
+        const double lo = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, 0, nn, inv_n));
+        const double hi = static_cast<double>(fill_value<T, FILL_INIT_A, POW2>(i, n - 1, nn, inv_n));
         bool tiny;
-        const double inv = oz_row_scale(oz_row_exponent(m, false), true, false, &tiny);
+        double inv;
+        (void)oz_row_code(hi, lo, false, true, &inv, &tiny);
         for (int q = 0; q < PIECES; ++q) {
           const int j0 = c0 + q * 256 * W;
           if (j0 >= n) break;

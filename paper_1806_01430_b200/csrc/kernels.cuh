@@ -133,15 +133,15 @@ inline int ozaki_pick_form(int cut, int top_a, int top_b) {
   return 0;
 }
 
-// The INT32 level accumulators: a level with p digit pairs stays below (p - 1) K 2^14 (first digits |d| <= 64, the others 8 bits);
-// p = min(SA, SB) for every form.  False: the form must not run on K = kq terms (auto mode then takes the fallback).
+// The INT32 level accumulators: a level with p digit pairs stays within p K 2^14 (8-bit digits: |d d'| <= 2^14); p = min(SA, SB)
+// for every form.  False: the form must not run on K = kq terms (auto mode then takes the fallback).
 #ifdef __CUDACC__
 __host__ __device__
 #endif
 inline bool oz_form_fits_int32(int form, int kq) {
   const int sa = form / 100, sb = form / 10 % 10;
   const int p = sa < sb ? sa : sb;
-  return p <= 1 || static_cast<long long>(p - 1) * kq < (1ll << 17);
+  return static_cast<long long>(p) * kq < (1ll << 17);
 }
 
 // FP32 auto mode has the forms whose epilogue is the TMA reduction (all but the 6 / 7-slice ones); beyond them: split TF32

@@ -4,16 +4,17 @@
 // B200 has no FP64 tensor-core kind and its FP64 pipe peaks at 36 TFLOP/s, but INT8 MMAs with INT32 accumulation are
 // EXACT and ~120x faster per operation.  Each operand row is scaled by a power of two and cut into S signed digits -- a first
 // one of 7 bits, 8-bit ones below it (ozaki_digits.cuh) --
-//     x = 2^e * (d_1 2^-6 + d_2 2^-14 + ... + d_S 2^-(8S-2)) + r,   |d_1| <= 64,  -128 <= d_t <= 127,  |r| <= 2^(e - 8S + 1)
-// (every step exact in FP64: power-of-two scaling, rounding to an integer, subtraction of a prefix of x's own bits), so
-//     sum_k a_ik b_jk = 2^(ea_i + eb_j + 4) * sum_g 2^(-8g) L_g,        L_g = sum_{t+u=g} sum_k da_t[i][k] db_u[j][k]
-// where every L_g is an integer dot product the tensor core computes without rounding: per term |d_1 d_u| <= 2^13 and
-// |d_t d_u| <= 2^14, so a level with p digit pairs stays below (p - 1) K 2^14 -- inside INT32 while K (p - 1) < 2^17 (p <= 4 at
-// K = 32768, any p up to K = 16384; oz_form_fits_int32 refuses the rest).  Levels g > S + 1 are dropped:
+//     x = +-2^e * (d_1 2^-7 + d_2 2^-15 + ... + d_S 2^-(8S-1)) + r,   -128 <= d_t <= 127,  |r| <= 2^(e - 8S)
+// (every step exact in FP64: power-of-two scaling, rounding to an integer, subtraction of a prefix of x's own bits; the sign: a row
+// whose largest element would need d_1 = +128 is encoded negated), so
+//     sum_k a_ik b_jk = +-2^(ea_i + eb_j + 2) * sum_g 2^(-8g) L_g,        L_g = sum_{t+u=g} sum_k da_t[i][k] db_u[j][k]
+// where every L_g is an integer dot product the tensor core computes without rounding: per term |d_t d_u| <= 2^14, so a level with
+// p digit pairs stays within p K 2^14 -- inside INT32 while K p < 2^17 (p <= 3 at K = 32768, any p up to K = 16384;
+// oz_form_fits_int32 refuses the rest).  Levels g > S + 1 are dropped:
 // |error| <= (S + 3) K 2^(-7S) * max_k|a_ik| max_k|b_jk| (the bound of 7-bit digits; the 8-bit ones are inside it), i.e.
 // 2e-14 K max max for S = 7 -- below what FP64 accumulation over K terms itself guarantees -- and ZERO whenever the operands
-// carry <= 8S - 2 bits below their row maximum: on the application's inputs ((i +- k) / N: 14 bits at N = 4096, two digits up to
-// a = (i + k) / N at N = 8192 and bt at N = 16384) the result is bit-identical to the CPU program.
+// carry <= 8S - 1 bits below their row maximum: on the application's inputs ((i +- k) / N: 14 bits at N = 4096; two digits hold both
+// operands up to N = 16384 and bt at N = 32768) the result is bit-identical to the CPU program.
 //
 // Who runs it.  matmul_variant 40 .. 45: always, as the triangular form with S = 7 .. 2 slices (general kernels: ~2^-49 .. of
 // K max max).  Auto mode (variant 0, N >= 1024; launch_matmul<double> in matmul.cu): only where it is ERROR-FREE.  The slice pass
@@ -89,10 +90,19 @@ __device__ __forceinline__ double pow2(int e) { return oz_pow2(e); }
 constexpr double kOzLevelStep = 1.0 / (1 << kOzDigitBits);  // level g + 1 weighs 2^-kOzDigitBits of level g (ozaki_digits.cuh: 8-bit digits below the first)
 
 constexpr int kNonFinite = kOzNonFinite;  // row exponent of a row that holds an Inf or a NaN: its products are NaN
-// acc * 2^(ea + eb - 12): exact scaling (ldexp also covers results that leave the normal range)
+// acc * 2^(ea + eb - 14): exact scaling (ldexp also covers results that leave the normal range); ea, eb: unpacked exponents
 __device__ __forceinline__ double scaled(double acc, int ea, int eb) {
   if (ea == kNonFinite || eb == kNonFinite) return __longlong_as_double(0x7ff8000000000000ll);
-  return ldexp(acc, ea + eb - 12);
+  return ldexp(acc, ea + eb - kOzPairUnit);
+}
+// rows encoded negated (ozaki_digits.cuh): the product of a row of a and a row of bt changes sign when exactly one of them is;
+// a zero stays +0 (the level sums are integers: the kernels never produce -0, which the store path for a zeroed c relies on)
+__device__ __forceinline__ double oz_signed(double v, bool neg) { return (neg && v != 0.0) ? -v : v; }
+// the same for a column's packed exponent word
+__device__ __forceinline__ double scaled_w(double acc, int ea, bool na, int eb_word) {
+  int eb;
+  const bool nb = oz_exp_unpack(eb_word, eb);
+  return oz_signed(scaled(acc, ea, eb), na != nb);
 }
 
 // C = CTAs per cluster: C consecutive column tiles of one tile-row share their a slices -- every CTA fetches 1/C of the rows
@@ -210,7 +220,8 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
     const int m = m_base + q * 32 + lane;
     const int m_limit = row0 + rows;
     const bool row_ok = m < m_limit;
-    const int ei = row_ok ? exp_a[m] : 0;  // kNonFinite marks a row that holds an Inf or a NaN
+    int ei;  // kNonFinite marks a row that holds an Inf or a NaN
+    const bool na = oz_exp_unpack(row_ok ? exp_a[m] : 0, ei);
     double* crow = c + static_cast<size_t>(row_ok ? m : 0) * n;
     const bool vec_ok = (n % 2 == 0) && (col0 % 2 == 0);
     int* eb_sh = reinterpret_cast<int*>(smem_raw + (bars + 128 - raw));  // 64 column exponents of this tile
@@ -250,7 +261,7 @@ matmul_ozaki_kernel(double* __restrict__ c, const __grid_constant__ CUtensorMap 
           double acc = static_cast<double>(static_cast<int>(lv[S - 1][e + h]));
 #pragma unroll
           for (int g = S - 2; g >= 0; --g) acc = fma(acc, kOzLevelStep, static_cast<double>(static_cast<int>(lv[g][e + h])));
-          v[h] = cpre[cb * 8 + e + h] + scaled(acc, ei, eb_sh[cb * 8 + e + h]);
+          v[h] = cpre[cb * 8 + e + h] + scaled_w(acc, ei, na, eb_sh[cb * 8 + e + h]);
         }
         if (!row_ok) continue;
         const int j = col0 + jr;
@@ -328,11 +339,14 @@ struct OzPArgs {
   int debug;  // MMX_OZ_DEBUG (rate probes, results are WRONG): 1 the producer signals stages without loading them, 2 the epilogue drops phase B
 };
 
-// sum * 2^(ea + eb - 12).  Fast path (both exponents moderate): two multiplications by exact powers of two, pa = 2^(ea - 12)
-// and pb = 2^eb -- neither product leaves the normal range, so the result is the one ldexp gives.
-__device__ __forceinline__ double scaled_fast(double sum, int ea, double pa, bool row_fast, int eb, double pb) {
-  if (row_fast && eb > -400 && eb < 400) return (sum * pa) * pb;
-  return scaled(sum, ea, eb);
+// +-sum * 2^(ea + eb - 14).  Fast path (both exponents moderate): two multiplications by exact powers of two, pa = 2^(ea - 14)
+// and pb = 2^eb -- neither product leaves the normal range, so the result is the one ldexp gives.  eb_word: the column's packed
+// exponent word, na: the row is encoded negated.
+__device__ __forceinline__ double scaled_fast(double sum, int ea, double pa, bool row_fast, bool na, int eb_word, double pb) {
+  int eb;
+  const bool nb = oz_exp_unpack(eb_word, eb);
+  if (row_fast && eb > -400 && eb < 400) return oz_signed((sum * pa) * pb, na != nb);
+  return oz_signed(scaled(sum, ea, eb), na != nb);
 }
 
 // CX x CY = CTAs per cluster working on CX x CY adjacent tiles: the a slices of a tile-row are fetched once per cluster row
@@ -523,15 +537,20 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
         const int m_base = g.row0 + by * OZ_BM, n_tile = bx * BN;
         const int buf = tile % NBUF;
         const int m = m_base + r;
-        const int ei = m < m_limit ? g.exp_a[m] : 0;  // kNonFinite marks a row that holds an Inf or a NaN
+        int ei;  // kNonFinite marks a row that holds an Inf or a NaN
+        const bool na = oz_exp_unpack(m < m_limit ? g.exp_a[m] : 0, ei);
         const bool row_fast = ei > -400 && ei < 400;
-        const double pa = pow2(row_fast ? ei - 12 : 0);
+        const double pa = pow2(row_fast ? ei - kOzPairUnit : 0);
         int* eb = eb_sh + (tile & 1) * BN;
         double* pb = pb_sh + (tile & 1) * BN;
         if (grp == 0 && r < BN) {
-          const int e = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
-          eb[r] = e;
-          if constexpr (Sh::SCALE_TABLE) pb[r] = pow2(e > -400 && e < 400 ? e : 0);
+          const int word = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
+          eb[r] = word;  // packed: exponent and sign of the column (oz_exp_unpack)
+          if constexpr (Sh::SCALE_TABLE) {
+            int e;
+            (void)oz_exp_unpack(word, e);
+            pb[r] = pow2(e > -400 && e < 400 ? e : 0);
+          }
         }
         // the exponents of this tile are complete; nobody is still reading the other copy (that was two tiles ago, and
         // everyone has passed the barrier of the tile in between)
@@ -591,28 +610,29 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
             // Whether the 16 columns of the chunk all have moderate exponents is decided once (the same for every lane), so the
             // common case is a branch-free loop the scheduler can interleave across elements.
             int ebv[16];
+            unsigned flip = 0;  // bit e: the product of this row and column e changes sign (one of the two is encoded negated)
             bool cols_fast = true;
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
-              ebv[e] = eb[j * 16 + e];
+              flip |= (oz_exp_unpack(eb[j * 16 + e], ebv[e]) != na ? 1u : 0u) << e;
               cols_fast &= static_cast<unsigned>(ebv[e] + 399) < 799u;
             }
             if (cols_fast && row_fast) {
-              const int e_row = ei - 12 - kOzDigitBits * (LV - 1);
+              const int e_row = ei - kOzPairUnit - kOzDigitBits * (LV - 1);
 #pragma unroll
               for (int e = 0; e < 16; ++e) {
                 const long long x = acc[jj][e];
                 const double d = static_cast<double>(x);
-                const int hi = __double2hiint(d) + (x != 0 ? (e_row + ebv[e]) * (1 << 20) : 0);  // stays a normal number
+                const int hi = x != 0 ? (__double2hiint(d) + (e_row + ebv[e]) * (1 << 20)) ^ static_cast<int>((flip >> e & 1u) << 31) : 0;  // stays a normal number
                 v[e] = __hiloint2double(hi, __double2loint(d));
               }
             } else {
 #pragma unroll  // (a rolled loop would index acc and v dynamically and push them to local memory for both branches)
-              for (int e = 0; e < 16; ++e) v[e] = scaled(static_cast<double>(acc[jj][e]) * pow2(-kOzDigitBits * (LV - 1)), ei, ebv[e]);
+              for (int e = 0; e < 16; ++e) v[e] = oz_signed(scaled(static_cast<double>(acc[jj][e]) * pow2(-kOzDigitBits * (LV - 1)), ei, ebv[e]), (flip >> e & 1u) != 0);
             }
           } else {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = scaled_fast(hsum[jj][e], ei, pa, row_fast, eb[j * 16 + e], pb[j * 16 + e]);
+            for (int e = 0; e < 16; ++e) v[e] = scaled_fast(hsum[jj][e], ei, pa, row_fast, na, eb[j * 16 + e], pb[j * 16 + e]);
           }
           const unsigned slab = slab0 + (sent % CR) * (8 * Sh::C_SLAB);
           if (g.debug & 16) {  // rate probe: conversions only
@@ -702,15 +722,18 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
         const int buf = tile % NBUF;
         const int m = m_base + r;
         const bool row_ok = m < m_limit;
-        const int ei = row_ok ? g.exp_a[m] : 0;  // kNonFinite marks a row that holds an Inf or a NaN
+        int ei;  // kNonFinite marks a row that holds an Inf or a NaN
+        const bool na = oz_exp_unpack(row_ok ? g.exp_a[m] : 0, ei);
         const bool row_fast = ei > -400 && ei < 400;
-        const double pa = pow2(row_fast ? ei - 12 : 0);
+        const double pa = pow2(row_fast ? ei - kOzPairUnit : 0);
         double* crow = static_cast<double*>(g.c) + static_cast<size_t>(row_ok ? m : 0) * g.n;
         int* eb = eb_sh + (tile & 1) * BN;
         double* pb = pb_sh + (tile & 1) * BN;
         if (r < BN) {
-          const int e = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
-          eb[r] = e;
+          const int word = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
+          int e;
+          (void)oz_exp_unpack(word, e);
+          eb[r] = word;  // packed: exponent and sign of the column
           pb[r] = pow2(e > -400 && e < 400 ? e : 0);
         }
 #pragma unroll 1
@@ -756,7 +779,7 @@ __device__ __forceinline__ void oz_persist_body(const OzPArgs& g, const CUtensor
 #pragma unroll
                 for (int l = LV - 2; l >= 0; --l) sum = fma(sum, kOzLevelStep, static_cast<double>(static_cast<int>(lv[l][e + h])));
                 const int col = part * 32 + cb * 8 + e + h;
-                v[h] = cpre[cb * 8 + e + h] + scaled_fast(sum, ei, pa, row_fast, eb[col], pb[col]);
+                v[h] = cpre[cb * 8 + e + h] + scaled_fast(sum, ei, pa, row_fast, na, eb[col], pb[col]);
               }
               if (!row_ok) continue;
               const int j = g.col0 + jr;
@@ -969,15 +992,20 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
       tile_at(tile, bx, by);
       const int m_base = g.row0 + by * OZ_BM, n_tile = bx * BN;
       const int m = m_base + r;
-      const int ei = m < m_limit ? g.exp_a[m] : 0;
+      int ei;
+      const bool na = oz_exp_unpack(m < m_limit ? g.exp_a[m] : 0, ei);
       const bool row_fast = ei > -400 && ei < 400;
-      const double pa = pow2(row_fast ? ei - 12 : 0);
+      const double pa = pow2(row_fast ? ei - kOzPairUnit : 0);
       int* eb = eb_sh + (tile & 1) * BN;
       double* pb = pb_sh + (tile & 1) * BN;
       if (grp == 0 && r < BN) {
-        const int e = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
-        eb[r] = e;
-        if constexpr (Sh::SCALE_TABLE) pb[r] = pow2(e > -400 && e < 400 ? e : 0);
+        const int word = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
+        eb[r] = word;  // packed: exponent and sign of the column (oz_exp_unpack)
+        if constexpr (Sh::SCALE_TABLE) {
+          int e;
+          (void)oz_exp_unpack(word, e);
+          pb[r] = pow2(e > -400 && e < 400 ? e : 0);
+        }
       }
       asm volatile("bar.sync 1, 256;\n" ::: "memory");
       mbar_wait(acc_full, tile & 1);
@@ -1033,28 +1061,29 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
         double v[16];
         if constexpr (LV <= 4) {
           int ebv[16];
+          unsigned flip = 0;  // bit e: the product of this row and column e changes sign (one of the two is encoded negated)
           bool cols_fast = true;
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            ebv[e] = eb[j * 16 + e];
+            flip |= (oz_exp_unpack(eb[j * 16 + e], ebv[e]) != na ? 1u : 0u) << e;
             cols_fast &= static_cast<unsigned>(ebv[e] + 399) < 799u;
           }
           if (cols_fast && row_fast) {
-            const int e_row = ei - 12 - kOzDigitBits * (LV - 1);
+            const int e_row = ei - kOzPairUnit - kOzDigitBits * (LV - 1);
 #pragma unroll
             for (int e = 0; e < 16; ++e) {
               const long long x = acc[jj][e];
               const double d = static_cast<double>(x);
-              const int hi = __double2hiint(d) + (x != 0 ? (e_row + ebv[e]) * (1 << 20) : 0);
+              const int hi = x != 0 ? (__double2hiint(d) + (e_row + ebv[e]) * (1 << 20)) ^ static_cast<int>((flip >> e & 1u) << 31) : 0;
               v[e] = __hiloint2double(hi, __double2loint(d));
             }
           } else {
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = scaled(static_cast<double>(acc[jj][e]) * pow2(-kOzDigitBits * (LV - 1)), ei, ebv[e]);
+            for (int e = 0; e < 16; ++e) v[e] = oz_signed(scaled(static_cast<double>(acc[jj][e]) * pow2(-kOzDigitBits * (LV - 1)), ei, ebv[e]), (flip >> e & 1u) != 0);
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) v[e] = scaled_fast(hsum[jj][e], ei, pa, row_fast, eb[j * 16 + e], pb[j * 16 + e]);
+          for (int e = 0; e < 16; ++e) v[e] = scaled_fast(hsum[jj][e], ei, pa, row_fast, na, eb[j * 16 + e], pb[j * 16 + e]);
         }
         if (lane == 0) tma_store_wait_read<0>();
         __syncwarp();
@@ -1187,8 +1216,8 @@ template <int S, typename T>
 __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const T* __restrict__ src, signed char* __restrict__ dst, int* __restrict__ exps,
                                                           size_t plane, int n, int kq, int src_row0, int nrows, int dst_row0,
                                                           int* __restrict__ guard, int lossy_slot, int top_slot, int dirty_slot) {
-  __shared__ double red[8];
-  __shared__ int e_sh;
+  __shared__ double red[8], red_lo[8], inv_sh;
+  __shared__ int tiny_sh;
   const int r = blockIdx.x;  // relative row
   const int tid = threadIdx.x;
   const bool live = r < nrows;
@@ -1211,13 +1240,14 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const T* __restrict
       for (int q = 0; q < 4; ++q) v[q] = (live && k0 + q < n) ? x[k0 + q] : 0.0;
     }
   };
-  double mx = 0.0;
+  double hi = 0.0, lo = 0.0;  // the row's largest and smallest element (zero padding included: harmless)
   int bad = 0;
   auto scan4 = [&](const double (&v)[4]) {
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       bad |= !isfinite(v[q]);
-      mx = fmax(mx, fabs(v[q]));
+      hi = fmax(hi, v[q]);
+      lo = fmin(lo, v[q]);
     }
   };
   double keep[KEEP][4];
@@ -1236,23 +1266,35 @@ __global__ void __launch_bounds__(256, 4) ozaki_slice_kernel(const T* __restrict
   }
   bad = __syncthreads_or(bad);
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-  if (tid % 32 == 0) red[tid / 32] = mx;
-  __syncthreads();
-  if (tid == 0) {
-    double m = red[0];
-#pragma unroll
-    for (int w = 1; w < 8; ++w) m = fmax(m, red[w]);
-    const int e = oz_row_exponent(m, bad != 0);
-    e_sh = e;
-    exps[dst_row0 + r] = bad ? kNonFinite : e;
+  for (int o = 16; o > 0; o >>= 1) {
+    hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+    lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+  }
+  if (tid % 32 == 0) {
+    red[tid / 32] = hi;
+    red_lo[tid / 32] = lo;
   }
   __syncthreads();
-  // exact power of two; a non-finite row gets zero digits, and so does a row whose maximum is below 2^-970 (1 / 2^e would
-  // overflow): both are flagged as lossy.  (Digit extraction by 64-bit integer arithmetic was measured slower than
-  // the FP64 form of oz_emit: 85 us against 70 us per operand at N = 4096.)
-  bool tiny;
-  const double inv = oz_row_scale(e_sh, live, bad != 0, &tiny);
+  if (tid == 0) {
+    double h = red[0], l = red_lo[0];
+#pragma unroll
+    for (int w = 1; w < 8; ++w) {
+      h = fmax(h, red[w]);
+      l = fmin(l, red_lo[w]);
+    }
+    // exponent, sign and scale of the row (ozaki_digits.cuh); exact power of two; a non-finite row gets zero digits, and so does a
+    // row whose maximum is below 2^-970 (1 / 2^e would overflow): both are flagged as lossy.  (Digit extraction by 64-bit integer
+    // arithmetic was measured slower than the FP64 form of oz_emit: 85 us against 70 us per operand at N = 4096.)
+    bool tiny_row;
+    double inv_row;
+    const int word = oz_row_code(h, l, bad != 0, live, &inv_row, &tiny_row);
+    inv_sh = inv_row;
+    tiny_sh = tiny_row ? 1 : 0;
+    exps[dst_row0 + r] = bad ? kNonFinite : word;
+  }
+  __syncthreads();
+  const bool tiny = tiny_sh != 0;
+  const double inv = inv_sh;
   signed char* drow = dst + static_cast<size_t>(dst_row0 + r) * kq;
   int lossy = bad | tiny, top = 0;  // top = highest non-zero digit (1-based) this thread has seen
   // Auto mode keeps an invariant on its scratch (zero-filled when the context is created): planes beyond guard[dirty_slot] hold

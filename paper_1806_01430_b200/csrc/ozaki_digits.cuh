@@ -2,17 +2,22 @@
 // gene 8 (the init-a fill, the transpose) can write its int8 digit planes while the values are still in registers, instead of a
 // separate slice pass reading the operand back from HBM (the slice pass stays for operands that arrive any other way).
 //
-// Encoding (matmul_ozaki.cu header): row r of an operand is scaled by 2^-e_r, e_r = ilogb(max_k |x_rk|) + 1, and cut into signed
-// digits d_1 .. d_S, x = 2^e (d_1 2^-6 + d_2 2^-14 + d_3 2^-22 + ...) + remainder, every step exact in FP64: a first digit of 7 bits
-// (|d_1| <= 64, since |x| < 2^e) and digits of 8 bits below it (-128 <= d_t <= 127) -- what an int8 holds.  Digit t has the unit
-// 2^-oz_unit(t - 1).  Eight bits per digit need a lopsided rounding: the part left after a digit must lie in (-128.5 / 256, 127.5 / 256]
-// of the digit's unit RECURSIVELY, i.e. in (c - 1, c] with c = 127 / 255, or a later digit would have to be +128; so
-// d = ceil(R - c) = rint(R + 1 / 510) (R = what is left, in units of the digit; never a tie for finite binary R).  1 / 510 is not a
-// binary fraction and R + 1 / 510 is rounded: an R within 2^-46 of the boundary may get the other digit, which shows up as a digit
-// outside [-128, 127] one level down -- checked, and reported like bits below the last digit (the operand counts as cut and the
-// product goes to the FP64 pipe).  Plane t of row r lives
-// at planes + t * plane + r * kq.  The guard words record whether any element has bits below its 7th digit (or is not finite)
-// and the highest non-zero digit of each operand; the contraction kernel picks its form from them (ozaki_pick_form).
+// Encoding (matmul_ozaki.cu header): row r of an operand is scaled by +-2^-e_r, e_r = ilogb(max_k |x_rk|) + 1, and cut into signed
+// 8-bit digits d_1 .. d_S (-128 <= d_t <= 127: what an int8 holds), x = +-2^e (d_1 2^-7 + d_2 2^-15 + d_3 2^-23 + ...) + remainder,
+// every step exact in FP64.  Digit t has the unit 2^-oz_unit(t - 1).
+//  * Eight bits per digit need a lopsided rounding: the part left after a digit must lie in (-128.5 / 256, 127.5 / 256] of the digit's
+//    unit RECURSIVELY, i.e. in (c - 1, c] with c = 127 / 255, or a later digit would have to be +128; so d = ceil(R - c) =
+//    rint(R + 1 / 510) (R = what is left, in units of the digit; never a tie for finite binary R).  1 / 510 is not a binary fraction
+//    and R + 1 / 510 is rounded: an R within 2^-46 of the boundary may get the other digit, which shows up as a digit outside
+//    [-128, 127] one level down -- checked, and reported like bits below the last digit (the operand counts as cut and the product
+//    goes to the FP64 pipe).
+//  * The first digit reaches -128 but only +127.498: a row whose largest element is positive and above 127 / 128 of 2^e is encoded
+//    NEGATED (two's-complement bytes reach -2^15 but only 2^15 - 129 when every byte is signed); when both ends of the row are that
+//    large the exponent grows by one instead.  The row's exponent word carries the sign (oz_exp_pack); the contraction's epilogue
+//    multiplies it back in.
+// Plane t of row r lives at planes + t * plane + r * kq.  The guard words record whether any element has bits below its 7th digit
+// (or is not finite) and the highest non-zero digit of each operand; the contraction kernel picks its form from them
+// (ozaki_pick_form).
 #pragma once
 
 #include <cuda_runtime.h>
@@ -28,8 +33,9 @@ constexpr int kOzNonFinite = 0x7fffffff;  // row exponent of a row that holds an
 __device__ __forceinline__ double oz_pow2(int e) { return __longlong_as_double(static_cast<long long>(e + 1023) << 52); }
 
 constexpr int kOzDigitBits = 8;  // bits per digit below the first (the level step of the contraction's Horner sum)
-// digit t + 1 (t = 0, 1, ...) has the unit 2^-oz_unit(t): 6, 14, 22, ...
-__host__ __device__ constexpr int oz_unit(int t) { return 6 + kOzDigitBits * t; }
+// digit t + 1 (t = 0, 1, ...) has the unit 2^-oz_unit(t): 7, 15, 23, ...
+__host__ __device__ constexpr int oz_unit(int t) { return 7 + kOzDigitBits * t; }
+constexpr int kOzPairUnit = 2 * (kOzDigitBits - 1);  // a product of two first digits has the unit 2^-14
 constexpr double kOzRoundBias = 1.0 / 510.0;  // 1/2 - 127/255
 
 // one digit off `rem` (scaled so that the digit's unit is 1 / up): returns it, leaves the rest in rem (exact); out_of_range: not an int8
@@ -52,6 +58,40 @@ __device__ __forceinline__ double oz_row_scale(int e, bool live, bool bad, bool*
   // 2^-e is a normal number for e <= 1022: two integer operations instead of scalbn's general path (the fused producers compute
   // this once per row AND thread)
   return e <= 1022 ? oz_pow2(-e) : scalbn(1.0, -e);
+}
+
+// The exponent word of a row: the exponent, and bit 30 flipped when the row is encoded negated (kOzNonFinite stays what it is)
+__host__ __device__ __forceinline__ int oz_exp_pack(int e, bool neg) { return neg ? e ^ 0x40000000 : e; }
+__host__ __device__ __forceinline__ bool oz_exp_unpack(int word, int& e) {
+  const bool neg = word != kOzNonFinite && (((word >> 30) ^ (word >> 31)) & 1) != 0;
+  e = neg ? word ^ 0x40000000 : word;
+  return neg;
+}
+// Exponent and sign of a row from its largest and smallest element (signed; bad: the row holds a non-finite value).  *inv = the
+// signed scale factor (0 for rows that get zero digits, *tiny as oz_row_scale).
+__device__ __forceinline__ int oz_row_code(double hi, double lo, bool bad, bool live, double* inv, bool* tiny) {
+  const double m = fmax(fabs(hi), fabs(lo));
+  int e = oz_row_exponent(m, bad);
+  double s = oz_row_scale(e, live, bad, tiny);
+  bool neg = false;
+  if (s != 0.0) {
+    const bool hi_big = hi * s > 0.9921875, lo_big = -lo * s > 0.9921875;  // 127 / 128
+    if (hi_big && lo_big) {
+      e += 1;
+      s = oz_row_scale(e, live, bad, tiny);
+    } else if (hi_big) {
+      neg = true;
+    }
+  }
+  *inv = neg ? -s : s;
+  return oz_exp_pack(e, neg);
+}
+// the signed scale factor of a row from its exponent word
+__device__ __forceinline__ double oz_row_scale_of(int word, bool* tiny) {
+  int e;
+  const bool neg = oz_exp_unpack(word, e);
+  const double s = oz_row_scale(e, true, false, tiny);
+  return neg ? -s : s;
 }
 
 // The digits of W (2 or 4) consecutive elements v[0..W) of one row, starting at column k0 (a multiple of W), packed W to a store.
@@ -118,7 +158,7 @@ __device__ __forceinline__ bool oz_first_words(const double (&v)[W], double inv,
   for (int q = 0; q < W; ++q) {
     double rem = v[q] * inv;
 #pragma unroll
-    for (int l = 0; l < L; ++l)  // digit l + 1; the constants fold (64, 1/64, 16384, 1/16384, ...)
+    for (int l = 0; l < L; ++l)  // digit l + 1; the constants fold (128, 1/128, 32768, 1/32768, ...)
       word[l] |= (oz_take_digit(rem, oz_pow2(oz_unit(l)), oz_pow2(-oz_unit(l)), left) & 0xff) << (8 * q);
     left = left || rem != 0.0;
   }

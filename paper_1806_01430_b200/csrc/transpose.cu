@@ -109,14 +109,14 @@ __global__ void __launch_bounds__(256, PLANES ? (sizeof(T) == 8 ? 5 : 6) : 1) tr
         const VT val = gather_piece(tile, out_row, chunk);
         __stcs(reinterpret_cast<VT*>(bt + static_cast<size_t>(in_col0 + out_row) * n + in_row0 + chunk * V), val);
         bool tiny;
-        const double inv = oz_row_scale(row_exp[k], true, false, &tiny);
+        const double inv = oz_row_scale_of(row_exp[k], &tiny), ainv = fabs(inv);
         signed char* drow = P.planes + static_cast<size_t>(in_col0 + out_row) * P.kq;
         int top_l = 0;
         bool left;
         if constexpr (V == 2) {
           const double e2[2] = {val.x, val.y};
           // not finite, or beyond what the exponent covers (it cannot happen while the executor's flags are right): cut
-          left = tiny || !(fabs(val.x) * inv < 1.0) || !(fabs(val.y) * inv < 1.0);
+          left = tiny || !(fabs(val.x) * ainv < 1.0) || !(fabs(val.y) * ainv < 1.0);
           int word[L];
           left = oz_first_words<2, L>(e2, inv, word) || left;
           *reinterpret_cast<unsigned short*>(&dig[0][out_row][chunk * V]) = static_cast<unsigned short>(word[0]);
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(256, PLANES ? (sizeof(T) == 8 ? 5 : 6) : 1) tr
           const double e4[4] = {static_cast<double>(val.x), static_cast<double>(val.y), static_cast<double>(val.z), static_cast<double>(val.w)};
           left = tiny;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) left = left || !(fabs(e4[q]) * inv < 1.0);
+          for (int q = 0; q < 4; ++q) left = left || !(fabs(e4[q]) * ainv < 1.0);
           left = oz_emit_first<4, L>(e4, inv, drow, P.plane, in_row0 + chunk * V, top_l) || left;
         }
         top = max(top, top_l);
@@ -153,17 +153,17 @@ __global__ void __launch_bounds__(256, PLANES ? (sizeof(T) == 8 ? 5 : 6) : 1) tr
           const int out_row = v / MB, chunk = v % MB;
           const VT val = gather_piece(tile, out_row, chunk);
           bool tiny;
-          const double inv = oz_row_scale(row_exp[k], true, false, &tiny);
+          const double inv = oz_row_scale_of(row_exp[k], &tiny), ainv = fabs(inv);
           lossy |= tiny;
           signed char* drow = P.planes + static_cast<size_t>(in_col0 + out_row) * P.kq;
           if constexpr (V == 2) {
             const double e2[2] = {val.x, val.y};
-            lossy |= !(fabs(val.x) * inv < 1.0) | !(fabs(val.y) * inv < 1.0);
+            lossy |= !(fabs(val.x) * ainv < 1.0) | !(fabs(val.y) * ainv < 1.0);
             oz_emit<7, 2>(e2, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
           } else {
             const double e4[4] = {static_cast<double>(val.x), static_cast<double>(val.y), static_cast<double>(val.z), static_cast<double>(val.w)};
 #pragma unroll
-            for (int q = 0; q < 4; ++q) lossy |= !(fabs(e4[q]) * inv < 1.0);
+            for (int q = 0; q < 4; ++q) lossy |= !(fabs(e4[q]) * ainv < 1.0);
             oz_emit<7, 4>(e4, inv, false, dirty, drow, P.plane, in_row0 + chunk * V, lossy, top);
           }
         }

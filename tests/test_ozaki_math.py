@@ -9,36 +9,42 @@ S = 7
 
 
 def unit(t):
-    """digit t (1-based) has the unit 2^-unit(t): a first digit of 7 bits, 8-bit digits below it (csrc/ozaki_digits.cuh)"""
-    return 6 + 8 * (t - 1)
+    """digit t (1-based) has the unit 2^-unit(t): 8-bit digits (csrc/ozaki_digits.cuh)"""
+    return 7 + 8 * (t - 1)
 
 
 def slices(x):
-    """rows of x -> (exponents e, digits d[t] as int64 arrays, remainder r) with x = 2^e (sum_t d_t 2^-unit(t)) + 2^e r.
-    Every digit is what an int8 holds; the lopsided rounding d = ceil(R - 127/255) keeps what is left inside (c - 1, c] of the
-    digit's unit, c = 127/255, so that the next digit is never +128."""
-    mx = np.abs(x).max(axis=1)
+    """rows of x -> (exponents e, signs s, digits d[t] as int64 arrays, remainder r) with x = s 2^e (sum_t d_t 2^-unit(t)) + s 2^e r.
+    Every digit is what an int8 holds: the lopsided rounding d = ceil(R - 127/255) keeps what is left inside (c - 1, c] of the
+    digit's unit, c = 127/255, so that the next digit is never +128; a row whose largest element is above 127/128 of 2^e is encoded
+    negated (s = -1), and when both ends of the row are that large e grows by one."""
+    hi, lo = x.max(axis=1), x.min(axis=1)
+    mx = np.maximum(np.abs(hi), np.abs(lo))
     e = np.where(mx > 0, np.floor(np.log2(np.maximum(mx, 1e-300))).astype(np.int64) + 1, 0)
-    rem = x * np.exp2(-e.astype(np.float64))[:, None]
-    assert (np.abs(rem) < 1).all()
+    sc = np.exp2(-e.astype(np.float64))
+    hi_big, lo_big = hi * sc > 127 / 128, -lo * sc > 127 / 128
+    e = e + (hi_big & lo_big)
+    sign = np.where(hi_big & ~lo_big, -1.0, 1.0)
+    rem = x * (sign * np.exp2(-e.astype(np.float64)))[:, None]
+    assert (rem > -1.004).all() and (rem < 0.9961).all()
     digits = []
     for t in range(1, S + 1):
         d = np.rint(rem * 2.0 ** unit(t) + 1.0 / 510.0)
         rem = rem - d * 2.0 ** -unit(t)          # exact in float64
-        assert (np.abs(d) <= 64).all() if t == 1 else ((d >= -128) & (d <= 127)).all()
+        assert ((d >= -128) & (d <= 127)).all()
         digits.append(d.astype(np.int64))
-    return e, digits, rem
+    return e, sign, digits, rem
 
 
 def contract(a, bt, c0, keep=S + 1):
-    ea, da, _ = slices(a)
-    eb, db, _ = slices(bt)
+    ea, sa, da, _ = slices(a)
+    eb, sb, db, _ = slices(bt)
     acc = np.zeros(a.shape[0:1] + bt.shape[0:1])
     for g in range(keep, 1, -1):                     # Horner from the smallest level, as the epilogue does
         level = sum(da[t - 1] @ db[g - t - 1].T for t in range(1, S + 1) if 1 <= g - t <= S)
         assert np.abs(level).max() < 2 ** 31         # INT32 accumulators
         acc = acc / 256.0 + level
-    return c0 + np.ldexp(acc, (ea[:, None] + eb[None, :] - 12).astype(np.int64))
+    return c0 + sa[:, None] * sb[None, :] * np.ldexp(acc, (ea[:, None] + eb[None, :] - 14).astype(np.int64))
 
 
 def app_operands(n):
@@ -50,7 +56,7 @@ def app_operands(n):
 def test_application_operands_use_two_digits_and_the_product_is_exact(n):
     a, bt = app_operands(n)
     for x in (a, bt):
-        _, d, rem = slices(x)
+        _, _, d, rem = slices(x)
         assert (rem == 0).all() and all((dt == 0).all() for dt in d[2:])     # log2(N) + 2 bits: digits 1 and 2 only, so even the
         # 6-slice form (digits <= 6, pairs t + u <= 7) keeps every non-zero pair: the cheapest error-free form of auto mode
     i = np.arange(n, dtype=np.float64)
@@ -81,7 +87,7 @@ def test_guard_condition_is_the_error_free_condition():
     c0 = np.zeros((n, n))
 
     def top(x):
-        _, d, rem = slices(x)
+        _, _, d, rem = slices(x)
         return (rem != 0).any(), max((t + 1 for t in range(S) if (d[t] != 0).any()), default=0)
 
     # 21-bit integers: nothing cut, 3 + 3 digits -> every pair kept -> exact
@@ -117,8 +123,8 @@ def test_rectangular_form_reproduces_the_product_exactly():
     for sa, sb in ((2, 2), (3, 2), (2, 3), (4, 4)):
         a = rs.randint(-(2 ** (7 * sa - 1)) + 1, 2 ** (7 * sa - 1), (8, k)).astype(np.float64)
         b = rs.randint(-(2 ** (7 * sb - 1)) + 1, 2 ** (7 * sb - 1), (8, k)).astype(np.float64)
-        ea, da, ra = slices(a)
-        eb, db, rb = slices(b)
+        ea, sa_, da, ra = slices(a)
+        eb, sb_, db, rb = slices(b)
         assert not ra.any() and not rb.any()
         assert not any(d.any() for d in da[sa:]) and not any(d.any() for d in db[sb:])   # nothing beyond the form's digits
         total = np.zeros((8, 8), dtype=object)
@@ -128,7 +134,7 @@ def test_rectangular_form_reproduces_the_product_exactly():
                 assert np.abs(level).max() < 2 ** 31
                 total = total + level.astype(object) * 2 ** (2 * unit(S) - unit(t) - unit(u))      # common denominator 2^(2 unit(S))
         exact = a.astype(np.int64).astype(object) @ b.astype(np.int64).astype(object).T
-        scale = np.array([[2 ** (int(x) + int(y)) for y in eb] for x in ea], dtype=object)
+        scale = np.array([[int(p) * int(q) * 2 ** (int(x) + int(y)) for y, q in zip(eb, sb_)] for x, p in zip(ea, sa_)], dtype=object)
         assert (total * scale == exact * 2 ** (2 * unit(S))).all()
 
 
