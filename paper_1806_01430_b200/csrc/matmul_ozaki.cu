@@ -861,6 +861,7 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
   volatile unsigned* tmem_slot_ptr = reinterpret_cast<volatile unsigned*>(smem_raw + (tmem_slot - raw));
   int* eb_sh = reinterpret_cast<int*>(smem_raw + (bars + 256 - raw));               // [2][BN] column exponents, alternating per tile
   double* pb_sh = reinterpret_cast<double*>(smem_raw + (bars + 256 + 1024 - raw));  // [2][BN] 2^exponent (clamped) of the same
+  unsigned* sg_sh = reinterpret_cast<unsigned*>(smem_raw + (bars + 208 - raw));     // [2][4] the columns encoded negated, one bit each
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   // pair tiles of 256 rows x BN columns in raster order; CTA `rank` owns rows [256 sy + 128 rank, + 128)
@@ -999,13 +1000,13 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
       int* eb = eb_sh + (tile & 1) * BN;
       double* pb = pb_sh + (tile & 1) * BN;
       if (grp == 0 && r < BN) {
-        const int word = n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0;
-        eb[r] = word;  // packed: exponent and sign of the column (oz_exp_unpack)
-        if constexpr (Sh::SCALE_TABLE) {
-          int e;
-          (void)oz_exp_unpack(word, e);
-          pb[r] = pow2(e > -400 && e < 400 ? e : 0);
-        }
+        int e;
+        const bool nb = oz_exp_unpack(n_tile + r < g.cols ? g.exp_b[n_tile + r] : 0, e);
+        eb[r] = e;
+        if constexpr (Sh::SCALE_TABLE) pb[r] = pow2(e > -400 && e < 400 ? e : 0);
+        // the columns encoded negated, one bit per column (a whole warp is here: r < BN holds for all of its lanes or none)
+        const unsigned negs = __ballot_sync(0xffffffffu, nb);
+        if (lane == 0) sg_sh[(tile & 1) * 4 + q] = negs;
       }
       asm volatile("bar.sync 1, 256;\n" ::: "memory");
       mbar_wait(acc_full, tile & 1);
@@ -1059,13 +1060,14 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
       for (int jj = 0; jj < MY; ++jj) {
         const int j = grp + 2 * jj;
         double v[16];
+        // bit e: the product of this row and column e of the chunk changes sign (exactly one of the two is encoded negated)
+        const unsigned flip = ((sg_sh[(tile & 1) * 4 + (j * 16) / 32] >> ((j * 16) % 32)) & 0xffffu) ^ (na ? 0xffffu : 0u);
         if constexpr (LV <= 4) {
           int ebv[16];
-          unsigned flip = 0;  // bit e: the product of this row and column e changes sign (one of the two is encoded negated)
           bool cols_fast = true;
 #pragma unroll
           for (int e = 0; e < 16; ++e) {
-            flip |= (oz_exp_unpack(eb[j * 16 + e], ebv[e]) != na ? 1u : 0u) << e;
+            ebv[e] = eb[j * 16 + e];
             cols_fast &= static_cast<unsigned>(ebv[e] + 399) < 799u;
           }
           if (cols_fast && row_fast) {
@@ -1083,7 +1085,11 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
           }
         } else {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) v[e] = scaled_fast(hsum[jj][e], ei, pa, row_fast, na, eb[j * 16 + e], pb[j * 16 + e]);
+          for (int e = 0; e < 16; ++e) {
+            const int ebe = eb[j * 16 + e];
+            const double mag = (row_fast && ebe > -400 && ebe < 400) ? (hsum[jj][e] * pa) * pb[j * 16 + e] : scaled(hsum[jj][e], ei, ebe);
+            v[e] = oz_signed(mag, (flip >> e & 1u) != 0);
+          }
         }
         if (lane == 0) tma_store_wait_read<0>();
         __syncwarp();

@@ -150,17 +150,33 @@ __device__ __forceinline__ void oz_emit(const double (&v)[W], double inv, bool b
 template <int W, int L>
 __device__ __forceinline__ bool oz_first_words(const double (&v)[W], double inv, int (&word)[L]) {
   static_assert(W == 2 || W == 4, "digits are packed two or four to a word");
-  static_assert(L >= 1 && L <= 7, "digit levels");
-#pragma unroll
-  for (int l = 0; l < L; ++l) word[l] = 0;
+  static_assert(L >= 1 && L <= 3, "digit levels of the straight-line pass");
+  // All L digits at once: X = x * inv * 2^(8 L - 1) is an integer exactly when nothing is left below digit L, and the bytes of
+  // X + 0x80..80 (offset binary, 0 .. 255 each) are the digits + 128 -- the same digits as the level-by-level walk of oz_emit gives
+  // (digits in [-128, 127] to the base 256 are unique), for three FP64 operations per element instead of four per level.
+  constexpr int kOffset = L == 1 ? 0x80 : L == 2 ? 0x8080 : 0x808080;
+  const double scale = inv * oz_pow2(oz_unit(L - 1));
+  int y[W];
   bool left = false;
 #pragma unroll
   for (int q = 0; q < W; ++q) {
-    double rem = v[q] * inv;
+    const double r = v[q] * scale;                         // exact (a power of two)
+    const double t = r + 6755399441055744.0;               // + 1.5 * 2^52: rint(r) sits in the low word
+    left = left || (t - 6755399441055744.0) != r;          // not an integer: bits below digit L (or |r| beyond 2^51: not finite, huge)
+    y[q] = __double2loint(t) + kOffset;
+    left = left || static_cast<unsigned>(y[q]) >= (1u << (8 * L));  // beyond what L bytes hold (cannot happen for |x inv| in range)
+  }
 #pragma unroll
-    for (int l = 0; l < L; ++l)  // digit l + 1; the constants fold (128, 1/128, 32768, 1/32768, ...)
-      word[l] |= (oz_take_digit(rem, oz_pow2(oz_unit(l)), oz_pow2(-oz_unit(l)), left) & 0xff) << (8 * q);
-    left = left || rem != 0.0;
+  for (int l = 0; l < L; ++l) {
+    // byte L - 1 - l of every element, packed (PRMT: three instructions for four elements)
+    const unsigned pick = static_cast<unsigned>(L - 1 - l) | (static_cast<unsigned>(4 + L - 1 - l) << 4);
+    if constexpr (W == 4) {
+      const unsigned lo = __byte_perm(static_cast<unsigned>(y[0]), static_cast<unsigned>(y[1]), pick);
+      const unsigned hi = __byte_perm(static_cast<unsigned>(y[2]), static_cast<unsigned>(y[3]), pick);
+      word[l] = static_cast<int>(__byte_perm(lo, hi, 0x5410) ^ 0x80808080u);
+    } else {
+      word[l] = static_cast<int>((__byte_perm(static_cast<unsigned>(y[0]), static_cast<unsigned>(y[1]), pick) & 0xffffu) ^ 0x8080u);
+    }
   }
   return left;
 }
