@@ -436,12 +436,49 @@ def test_fp64_auto_uses_the_tensor_cores_exactly_when_they_are_error_free():
     assert bits_equal(run(0, a, bt, c0), run(4, a, bt, c0))
 
 
+@pytest.mark.parametrize("kind,form", [("negated", 223), ("mixed", 335)])
+def test_fp64_auto_rows_encoded_negated_and_rows_with_two_large_ends(kind, form):
+    """8-bit digits reach -128 but only +127: a row whose largest element is positive and within 1/128 of 2^e is encoded negated
+    (csrc/ozaki_digits.cuh, oz_row_code), so that two digits hold 15-bit non-negative integers -- the application's a = (i + j) / N at
+    N = 16384; a row with such elements at BOTH ends takes the next exponent (and, here, a third digit).  The product is the exact
+    integer product either way."""
+    n = 1024
+    rs = np.random.RandomState(7)
+
+    def rows(which):
+        x = np.empty((n, n))
+        for r in range(n):
+            t = which if which != "mixed" else ("negated", "plain", "both")[r % 3]
+            if t == "negated":
+                x[r] = rs.randint(0, 2 ** 15, n)
+                x[r, r % n] = 2 ** 15 - 1                      # 32767 / 32768: the first digit would be +128
+            elif t == "plain":
+                x[r] = -rs.randint(0, 2 ** 15, n)
+                x[r, r % n] = -(2 ** 15 - 1)
+            else:
+                x[r] = rs.randint(-2 ** 15 + 1, 2 ** 15, n)
+                x[r, 0], x[r, 1] = 2 ** 15 - 1, -(2 ** 15 - 1)
+        return x
+    a, bt = rows(kind), rows(kind)
+    c0 = rs.randint(-1000, 1000, (n, n)).astype(np.float64)
+    with capi.Context(n=n, dtype=capi.F64) as ctx:
+        ctx.upload(capi.ARRAY_A, a)
+        ctx.upload(capi.ARRAY_BT, bt)
+        ctx.upload(capi.ARRAY_C, c0)
+        ctx.run_loop(8)
+        got = ctx.fetch(capi.ARRAY_C)
+        assert ctx.gene8_form() == form
+    want = (c0.astype(np.int64) + a.astype(np.int64) @ bt.astype(np.int64).T).astype(np.float64)
+    assert bits_equal(got, want)
+
+
 @pytest.mark.parametrize("digits_a,digits_bt,form", [(1, 1, 223), (1, 2, 223), (2, 2, 223), (3, 2, 324), (2, 3, 234), (3, 3, 335), (4, 3, 436), (3, 4, 346), (4, 4, 447),
                                                    (5, 1, 555), (6, 1, 666), (5, 3, 777), (4, 5, 0), (8, 1, 0)])
 def test_fp64_auto_runs_the_cheapest_error_free_form(digits_a, digits_bt, form):
     """One persistent launch reads the guard the slice pass wrote and picks the cheapest error-free form: the rectangular
     SA x SB digit-pair forms up to four digits per operand, the triangular 5 / 6 / 7-slice forms beyond (every non-zero
-    pair t + u <= S + 1 kept); integers of 7t - 1 bits plus sign take t digits.  mmx_gene8_form reports the choice as
+    pair t + u <= S + 1 kept); integers of 7t - 1 bits plus sign take t digits (t 8-bit digits hold 8t - 1 bits plus sign: 7t - 1
+    bits need exactly t of them for t <= 7).  mmx_gene8_form reports the choice as
     100 SA + 10 SB + levels; the result is the exact integer product (rounded once per Horner step, or not at all below
     2^53); 0 = no form qualifies and the FP64 pipe produced the result."""
     n = 1024
