@@ -291,7 +291,7 @@ def run_ours(args):
         if form > 0:
             # auto mode picked an INT8 tensor-core form on the device (mmx_gene8_form: 100 SA + 10 SB + levels): digits a_1..a_SA
             # against b_1..b_SB, pairs kept up to level t + u <= levels + 1.  This workload's operands carry log2(N) + 2 bits =
-            # two 7-bit digits each up to N = 4096: the 2 x 2 form, 4 INT8 slice products per FP64 term.  ms8 covers the two
+            # two 8-bit digits each up to N = 16384: the 2 x 2 form, 4 INT8 slice products per FP64 term.  ms8 covers the two
             # slice passes, that contraction and the guarded FP64-pipe launch that exits at once.
             sa, sb, lv = form // 100, form // 10 % 10, form % 10
             products = sum(1 for t in range(1, sa + 1) for u in range(1, sb + 1) if t + u <= lv + 1)
@@ -303,7 +303,7 @@ def run_ours(args):
             ops = products * flops / (msk * 1e-3) / 1e12
             ops_nest = products * flops / (ms8 * 1e-3) / 1e12
             roof = {"bound": "tensor", "pipe": "int8 (tcgen05.mma.kind::i8, INT32 accumulators in TMEM)",
-                    "kernel": f"matmul_ozaki_auto form {form} (gene 8 contraction: exact 7-bit INT8 slices, {sa} x {sb} digit pairs = {products} "
+                    "kernel": f"matmul_ozaki_auto form {form} (gene 8 contraction: exact 8-bit INT8 digit slices, {sa} x {sb} digit pairs = {products} "
                               f"slice products per FP64 term)",
                     "form": form, "slice_products_per_term": products,
                     "achieved": ops, "peak": int8_peak, "unit": "TOP/s", "frac": ops / int8_peak,
@@ -452,7 +452,7 @@ def e2e_host_buffers(ctx, n, dtype, esz, reps):
 def fp64_random_arm(n, device):
     """Gene 8 on uniform(-1, 1) operands from MT19937(seed 1) -- NOT the reference's inputs (the program generates its own): full
     53-bit mantissas, so no INT8 digit form is error-free and auto mode takes the FP64 pipe (DMMA).  Beside it the opt-in general
-    tensor-core kernel (matmul_variant 40: 7 exact 7-bit slices per operand, 28 slice products per term, truncation bound
+    tensor-core kernel (matmul_variant 40: 7 exact 8-bit slices per operand, 28 slice products per term, truncation bound
     2e-14 K max|a| max|b|), with its measured norm-wise error on a sample of rows."""
     import numpy as np
 
@@ -574,7 +574,7 @@ def fp32_arm(n, device, steps, peaks):
         int8_inferred = 2.0 * peaks["bf16_tflops"]
         int8_peak = capi.peak_probe(capi.PEAK_UMMA_I8, device)
         ops = products * flops / ms8 / 1e9
-        out["kernel"] = (f"matmul_ozaki_auto<float> form {form} (gene 8: the float operands' exact 7-bit INT8 digits, {sa} x {sb} pairs = "
+        out["kernel"] = (f"matmul_ozaki_auto<float> form {form} (gene 8: the float operands' exact 8-bit INT8 digits, {sa} x {sb} pairs = "
                          f"{products} slice products per term, result = the exact product rounded once to float; slice passes and the "
                          f"three guarded split-TF32 launches included)")
         out["roofline"] = {"bound": "tensor", "pipe": "int8", "achieved": ops, "peak": int8_peak, "unit": "TOP/s", "frac": ops / int8_peak,

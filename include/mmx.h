@@ -107,13 +107,13 @@ typedef struct mmx_config {
   int32_t host_threads;     /* threads for CPU-mapped nests; 1 = the reference program         */
   int32_t launch_batching;  /* 1: inner-loop launch trains are submitted as CUDA graphs        */
   int32_t matmul_variant;   /* gene-8 kernel: 0 auto (below N = 1024: DMMA in FP64, FFMA in FP32; from there the INT8 tensor cores
-                             * whenever exact 7-bit digit products lose nothing of the product, in the cheapest digit-pair form
+                             * whenever exact 8-bit digit products lose nothing of the product, in the cheapest digit-pair form
                              * that does, chosen on the device from the operands -- the application's inputs at N = 2^p qualify
                              * with 2 x 2 .. 3 x 3 pairs; the result is the exact product rounded once for forms of up to four
                              * levels and faithfully rounded (<= 1 ulp, exact when it fits 53 bits) beyond -- and otherwise DMMA in
                              * FP64, tcgen05 split-TF32 with compensated accumulation in FP32); 1 first SIMT kernel; 2, 4-13 DMMA tile shapes (FP64);
                              * 20, 22 SIMT tile shapes; 30 FP32 tcgen05 split-TF32 at any N % 4 == 0; 31 its wide-tile
-                             * uncompensated form; 40 FP64 on the tcgen05 INT8 tensor cores with 7 exact 7-bit slices per operand
+                             * uncompensated form; 40 FP64 on the tcgen05 INT8 tensor cores with 7 exact 8-bit slices per operand
                              * whatever the operands (error <= 2e-14 K max|a| max|b|), 41 .. 45 the same with 6 .. 2 slices */
   int32_t warmup;           /* untimed runs per genome before the timed repetitions (default 0) */
   /* Host-side isolation of concurrent measurements (the reference bounds the contention with `jobs`,
@@ -282,7 +282,7 @@ MMX_API int mmx_gene8_form(mmx_ctx* ctx, int slot, int32_t* form_out);
 MMX_API int mmx_time_gene8_contraction(mmx_ctx* ctx, int slot, int iters, int flush_l2, double* ms_out);
 
 /* The rule behind mmx_gene8_form, evaluated on the host (no device needed): the form the auto launch takes for operands of which
- * `cut` != 0 says some element has bits below its 7th digit, and top_a / top_bt are the highest non-zero 7-bit digits (1-based)
+ * `cut` != 0 says some element has bits below its 7th digit, and top_a / top_bt are the highest non-zero 8-bit digits (1-based)
  * anywhere in a / bt.  Returns 100 SA + 10 SB + levels, or 0 for the FP64 pipe. */
 MMX_API int mmx_gene8_pick_form(int cut, int top_a, int top_bt);
 

@@ -90,7 +90,7 @@ inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
 // ---- init-a + the digit planes of a (gene 0 fused with the encoding gene 8 needs; ozaki_digits.cuh) -----------------------------
 // A CTA covers 8 rows x 1024 columns.  Per row a thread owns two 16-byte pieces, half a CTA-row apart, so that every store
 // instruction of a warp is one contiguous run of whole sectors (a thread owning 32 consecutive bytes would write each sector in two
-// halves, from two instructions): it stores them and, from the same registers, their 7-bit digits (16 / 32 bits per plane and
+// halves, from two instructions): it stores them and, from the same registers, their 8-bit digits (16 / 32 bits per plane and
 // piece).  The row exponent needs the row's largest magnitude: (i + j) / N is non-negative and grows with j, so it is the row's
 // first and last element -- every thread computes it for itself.
 template <typename T, bool POW2>

@@ -650,7 +650,7 @@ cudaError_t launch_matmul<double>(double* c, const double* a, const double* bt, 
   if (!strict && scratch != nullptr && variant >= 40 && variant <= 45)  // 40 .. 45: 7 .. 2 slices
     return launch_matmul_ozaki(c, a, bt, scratch, n, row0, rows, col0, cols, 47 - variant, stream, nullptr, reuse_a);
   const bool dmma_ok = n % 2 == 0 && col0 % 2 == 0 && cols % 2 == 0;  // 16-byte aligned double2 accesses of c
-  // auto: the INT8 tensor cores whenever their 7-bit slices reproduce every operand element exactly and every non-zero digit
+  // auto: the INT8 tensor cores whenever their 8-bit digit slices reproduce every operand element exactly and every non-zero digit
   // pair is kept -- nothing of the product is dropped -- in the cheapest digit-pair form that does (ozaki_pick_form), else the FP64
   // pipe.  Forms with at most four levels (up to 2 x 3 / 3 x 2 digits: the application up to N = 8192) combine the level sums in a
   // 64-bit integer and round ONCE: the error-free product, bit-identical to the CPU program on the application's inputs.  Forms with

@@ -2,8 +2,8 @@
 // (fixtures/matmul.c:25-28) as an error-free INT8 slice decomposition (Ozaki scheme) on tcgen05.mma.kind::i8.
 //
 // B200 has no FP64 tensor-core kind and its FP64 pipe peaks at 36 TFLOP/s, but INT8 MMAs with INT32 accumulation are
-// EXACT and ~120x faster per operation.  Each operand row is scaled by a power of two and cut into S signed digits -- a first
-// one of 7 bits, 8-bit ones below it (ozaki_digits.cuh) --
+// EXACT and ~120x faster per operation.  Each operand row is scaled by a power of two and cut into S signed 8-bit digits
+// (ozaki_digits.cuh):
 //     x = +-2^e * (d_1 2^-7 + d_2 2^-15 + ... + d_S 2^-(8S-1)) + r,   -128 <= d_t <= 127,  |r| <= 2^(e - 8S)
 // (every step exact in FP64: power-of-two scaling, rounding to an integer, subtraction of a prefix of x's own bits; the sign: a row
 // whose largest element would need d_1 = +128 is encoded negated), so

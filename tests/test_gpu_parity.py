@@ -381,7 +381,7 @@ def test_fp64_int8_slices_within_tolerance_on_random_inputs(n, variant):
 
 @pytest.mark.parametrize("n", [256, 512, 1024])
 def test_fp64_int8_slices_are_exact_when_the_operands_are_short(n):
-    """Operands with at most 40 significant bits below their row maximum are reproduced EXACTLY by 7 slices of 7 bits, so
+    """Operands with at most 40 significant bits below their row maximum are reproduced EXACTLY by 7 slices of 8 bits (55 bits), so
     the integer products are the true products: whole individuals equal the CPU program bit for bit, and a product of
     small integers equals numpy's exact result."""
     ref = cpu.App(n).run()
