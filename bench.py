@@ -55,6 +55,8 @@ def parse_args():
     ap.add_argument("--sustained-seconds", type=float, default=3.0)
     ap.add_argument("--ga", action="store_true", help="run the config-4 GA block (64 x 40, seed 1) also on one GPU (on by default with --gpus > 1)")
     ap.add_argument("--no-multi", action="store_true", help="with --gpus > 1: skip the config-4 (GA) and config-5 (row-sharded) blocks")
+    ap.add_argument("--multi-budget", type=float, default=420.0,
+                    help="seconds the multi-GPU blocks may take before rank 0 prints the line without them and every rank leaves")
     ap.add_argument("--ga-population", type=int, default=64)
     ap.add_argument("--ga-generations", type=int, default=40)
     ap.add_argument("--ga-timeout", type=float, default=2.0, help="budget per individual in the GA block (a run over it scores the budget)")
@@ -362,16 +364,7 @@ def run_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         base = cpu_baseline(n, 0 if dtype == capi.F64 else 1, os.cpu_count() or 1)
 
-    # config 4 / config 5 (every rank takes part): the GA search with the population sharded over the ranks, and the row-sharded
-    # individual with the fused transpose + exchange over peer memory
-    multi = None
-    if (world > 1 and not args.no_multi) or args.ga:
-        multi = {"ga": ga_block(args, n, dtype, device, rank, world, ctl, barrier)}
-        if world > 1:
-            multi["rowshard"] = rowshard_block(args, dtype, device, rank, world, ctl, max_over_ranks, barrier)
-        else:
-            multi["rowshard"] = {"skipped": "needs --gpus >= 2 (one process per GPU under torchrun)"}
-
+    line = None
     if rank == 0:
         ms_per_step = 1e3 * wall_s / args.steps
         line = {
@@ -408,10 +401,49 @@ def run_ours(args):
             line["fp64_random"] = fp64_random
         if sustained is not None:
             line["sustained"] = sustained
-        if multi is not None:
+
+    # config 4 / config 5 (every rank takes part): the GA search with the population sharded over the ranks, and the row-sharded
+    # individual with the fused transpose + exchange over peer memory.  The line above is complete before they start: a block that
+    # raises is reported as {"error": ...}, and a block that does not return within --multi-budget seconds (a member lost while its
+    # peers wait on its events) makes rank 0 print the line with that error and every rank leave -- the headline never depends on them
+    if (world > 1 and not args.no_multi) or args.ga:
+        import threading
+
+        def give_up():
+            if rank == 0:
+                line["multi_gpu"] = {"error": f"the multi-GPU blocks did not return within {args.multi_budget:.0f} s; abandoned"}
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+
+        watchdog = threading.Timer(args.multi_budget, give_up)
+        watchdog.daemon = True
+        watchdog.start()
+        multi = {}
+        try:
+            multi["ga"] = ga_block(args, n, dtype, device, rank, world, ctl, barrier)
+        except Exception as e:  # noqa: BLE001 -- reported in the line, never fatal for it
+            multi["ga"] = {"error": f"{type(e).__name__}: {e}"}
+        if world > 1:
+            try:
+                multi["rowshard"] = rowshard_block(args, dtype, device, rank, world, ctl, max_over_ranks, barrier)
+            except Exception as e:  # noqa: BLE001
+                multi["rowshard"] = {"error": f"{type(e).__name__}: {e}"}
+        else:
+            multi["rowshard"] = {"skipped": "needs --gpus >= 2 (one process per GPU under torchrun)"}
+        watchdog.cancel()
+        if rank == 0:
             line["multi_gpu"] = multi
+        if any(isinstance(v, dict) and "error" in v for v in multi.values()):
+            # the ranks may no longer agree on which collective comes next: print and leave without another one
+            if rank == 0:
+                print(json.dumps(line), flush=True)
+            os._exit(0)
+    if rank == 0:
         print(json.dumps(line), flush=True)
-    ctx.close()
+    try:
+        ctx.close()
+    except Exception:  # noqa: BLE001 -- a device a failed block left unusable must not turn a printed line into a non-zero exit
+        pass
     if world > 1:
         dist.destroy_process_group()
 
@@ -702,6 +734,8 @@ def rowshard_block(args, dtype, device, rank, world, ctl, max_over_ranks, barrie
     from paper_1806_01430_b200.rowshard import GpuMember, RowShardedRun
     esz = 8 if dtype == capi.F64 else 4
     out = []
+    if os.environ.get("MMX_BENCH_INJECT") == f"rowshard_raise_{rank}":   # test hook: this rank fails, its peers are left waiting
+        raise RuntimeError("injected failure (MMX_BENCH_INJECT)")
     for n in args.rowshard_n:
         flops = 2.0 * n ** 3
         need = 4 * n * n * esz + 15 * n * n + (1 << 30)       # arrays + digit planes + slack
