@@ -37,6 +37,7 @@
 // 406 / 473 / 314) with the forms 2x2 / 3x2 / 3x3 the operands allow (first version, 6-slice triangular form for all: 119 / 151 /
 // 172); DMMA 33-35.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 
 #include "kernels.cuh"
@@ -337,6 +338,10 @@ struct OzPArgs {
   unsigned long long cond;
   int use_cond;
   int debug;  // MMX_OZ_DEBUG (rate probes, results are WRONG): 1 the producer signals stages without loading them, 2 the epilogue drops phase B
+  // MMX_OZ_TRACE=1 (pair body): SM clocks of the leader CTA of pair 0 at the hand-over points of every tile, 8 words per tile --
+  // [0] the issuing thread saw the accumulators free, [1] it saw the tile's first stage full, [2] it committed the tile,
+  // [3] an epilogue warp saw the commit, [4] that warp had read its share and arrived (tools/handover_trace.py prints them)
+  long long* trace;
 };
 
 // +-sum * 2^(ea + eb - 14).  Fast path (both exponents moderate): two multiplications by exact powers of two, pa = 2^(ea - 14)
@@ -900,6 +905,7 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
   tc_fence_after();
   const unsigned tmem_base = *tmem_slot_ptr;
   const unsigned lead_acc_empty = mapa_cluster(acc_empty, 0);
+  long long* const tr = blockIdx.x == 0 ? g.trace : nullptr;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -937,12 +943,16 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
       constexpr unsigned idesc_3 = idesc_m | (static_cast<unsigned>(BN >> 3) << 17);         // a_t x b_3
       int it = 0;
       for (int tile = 0; tile < my_tiles; ++tile) {
-        mbar_wait(acc_empty, tile & 1);  // completion #tile: the epilogue warps' initial arrival, then one per drained tile
+        // completion #tile: the epilogue warps' initial arrival, then one per drained tile
+        if (g.debug & 4096) mbar_wait_spin(acc_empty, tile & 1);
+        else mbar_wait(acc_empty, tile & 1);
         tc_fence_after();
+        if (tr != nullptr) tr[tile * 8 + 0] = clock64();
         for (int kb = 0; kb < k_stages; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(full_bar(s), (it / STAGES) & 1);
           tc_fence_after();
+          if (tr != nullptr && kb == 0) tr[tile * 8 + 1] = clock64();
           const unsigned st = base + s * Sh::STAGE_BYTES;
           const unsigned long long b12 = umma_desc_sw<BK>(st + Sh::A_BYTES), b3 = umma_desc_sw<BK>(st + Sh::A_BYTES + Sh::B1_BYTES);
 #pragma unroll
@@ -963,6 +973,7 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
           tc_commit2_mc(empty_bar(s), 3);
         }
         tc_commit2_mc(acc_full, 3);
+        if (tr != nullptr) tr[tile * 8 + 2] = clock64();
       }
     }
   } else {
@@ -1009,8 +1020,10 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
         if (lane == 0) sg_sh[(tile & 1) * 4 + q] = negs;
       }
       asm volatile("bar.sync 1, 256;\n" ::: "memory");
-      mbar_wait(acc_full, tile & 1);
+      if (g.debug & 4096) mbar_wait_spin(acc_full, tile & 1);
+      else mbar_wait(acc_full, tile & 1);
       tc_fence_after();
+      if (tr != nullptr && warp == 2 && lane == 0) tr[tile * 8 + 3] = clock64();
       if (g.debug & 2048) {  // rate probe: the set is handed back unread (what the drain costs per tile)
         tc_fence_before();
         __syncwarp();
@@ -1054,6 +1067,7 @@ __device__ __forceinline__ void oz_pair_body(const OzPArgs& g, const CUtensorMap
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive_cluster(lead_acc_empty);
+      if (tr != nullptr && warp == 2 && lane == 0) tr[tile * 8 + 4] = clock64();
       // phase B: scale, stage, reduce into c (overlaps the next tile's MMAs); tiles beyond the edge are dropped by the tensor map
       if (g.debug & 2) continue;
 #pragma unroll
@@ -1593,6 +1607,16 @@ cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, in
   g.use_cond = (cond != nullptr && cond->active) ? 1 : 0;
   static const int debug = [] { const char* e = getenv("MMX_OZ_DEBUG"); return e ? atoi(e) : 0; }();
   g.debug = debug;
+  static const int trace_on = [] { const char* e = getenv("MMX_OZ_TRACE"); return e ? atoi(e) : 0; }();
+  static long long* trace_buf = nullptr;  // one device, one stream at a time: a measuring hook, not a product path
+  constexpr int kTraceWords = 8 * 4096;
+  if (trace_on && trace_buf == nullptr && cudaMalloc(&trace_buf, kTraceWords * sizeof(long long)) != cudaSuccess) trace_buf = nullptr;
+  g.trace = trace_on ? trace_buf : nullptr;
+  if (g.trace != nullptr) {  // never inside a capture (the dump below synchronises)
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(stream, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) g.trace = nullptr;
+  }
+  if (g.trace != nullptr) cudaMemsetAsync(g.trace, 0, kTraceWords * sizeof(long long), stream);
   // the grid covers the 64-wide tiling (the forms with 128-wide tiles leave the surplus CTAs without a tile)
   const int tiles_x = (cols + 63) / 64, tiles_y = (rows + OZ_BM - 1) / OZ_BM;
   const dim3 grid(static_cast<unsigned>(std::min(tiles_x * tiles_y, oz_sm_count())));
@@ -1614,7 +1638,15 @@ cudaError_t oz_persist_contract(CT* c, void* scratch, int planes, int slices, in
         cfg.numAttrs = 1;
         const int* guard_words = L.guard;
         int* ran_word = L.guard + 4;
-        return cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_pair_kernel<CT>, g, maps, guard_words, ran_word);
+        const cudaError_t le = cudaLaunchKernelEx(&cfg, matmul_ozaki_auto_pair_kernel<CT>, g, maps, guard_words, ran_word);
+        if (g.trace != nullptr && le == cudaSuccess) {  // MMX_OZ_TRACE: the leader pair's clocks, one line per tile on stderr
+          static long long host[kTraceWords];
+          if (cudaStreamSynchronize(stream) == cudaSuccess && cudaMemcpy(host, g.trace, sizeof(host), cudaMemcpyDeviceToHost) == cudaSuccess)
+            for (int t = 0; t < kTraceWords / 8 && host[t * 8] != 0; ++t)
+              fprintf(stderr, "oztrace n=%d tile=%d free=%lld first_full=%lld committed=%lld seen=%lld arrived=%lld\n", n, t, host[t * 8] - host[0],
+                      host[t * 8 + 1] - host[0], host[t * 8 + 2] - host[0], host[t * 8 + 3] - host[0], host[t * 8 + 4] - host[0]);
+        }
+        return le;
       }
       OzClusterChoice cc = oz_auto_cluster_choice();
       if (sizeof(CT) != 8 && cc.shape != 11) {  // the multicast forms are instantiated for FP64 only

@@ -35,6 +35,20 @@ __device__ __forceinline__ void mbar_wait(unsigned bar, unsigned parity) {
     if (!ok && spins > (1u << 28)) __trap();
   }
 }
+// the same wait as a plain poll (mbarrier.test_wait never suspends the thread): a probe for what the suspended wait's wake-up costs
+__device__ __forceinline__ void mbar_wait_spin(unsigned bar, unsigned parity) {
+  unsigned ok = 0;
+  for (unsigned spins = 0; !ok; ++spins) {
+    asm volatile(
+        "{\n.reg .pred p;\n"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (!ok && spins > (1u << 28)) __trap();
+  }
+}
 __device__ __forceinline__ void tma_load_2d(unsigned dst, const CUtensorMap* map, int c0, int c1, unsigned bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(dst),
