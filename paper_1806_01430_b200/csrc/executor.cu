@@ -68,6 +68,11 @@ struct Slot {
   bool fuse_planes = false;        // set per plan / per API call
   bool planes_a_valid = false, planes_bt_valid = false;
   bool b_colexp_valid = false;     // the exponents of bt's rows were written by the init-b kernel (closed form of its own output)
+  // init-b inside the transpose: a plan that runs both nests whole on the device, with nothing touching b in between, lets the
+  // transpose kernel COMPUTE its tiles of b (and store them) instead of reading them back (launch_fill_b_transpose_planes).
+  // defer_b: the sequence allows it (begin_sequence); b_pending: init-b has been asked for and b is not written yet
+  bool defer_b = false;
+  bool b_pending = false;
   bool c_zero = false;             // the zero-c kernel filled c on the device and nothing has written c since (kCIsZero)
   std::map<int, Train> trains;  // by gene
   struct PlanGraph {
@@ -200,13 +205,19 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
     case 1: s.planes_a_valid = false; return launch_fill_row<T>(FILL_INIT_A, a, n, iter, s.cur);
     case 2:
       s.b_colexp_valid = false;
+      s.b_pending = false;
+      if (fuse && s.defer_b) {
+        const cudaError_t e = launch_b_colexp<T>(n, matmul_ozaki_operand(s.oz_planes, n, 1).exps, s.cur);
+        s.b_colexp_valid = s.b_pending = e == cudaSuccess;
+        return e;
+      }
       if (fuse) {
         const cudaError_t e = launch_fill_b_colexp<T>(b, n, matmul_ozaki_operand(s.oz_planes, n, 1).exps, s.cur);
         s.b_colexp_valid = e == cudaSuccess;
         return e;
       }
       return launch_fill2d<T>(FILL_INIT_B, b, n, row0, rows, s.cur);
-    case 3: s.b_colexp_valid = false; return launch_fill_row<T>(FILL_INIT_B, b, n, iter, s.cur);
+    case 3: s.b_colexp_valid = s.b_pending = false; return launch_fill_row<T>(FILL_INIT_B, b, n, iter, s.cur);
     case 4: {
       const cudaError_t e = launch_fill2d<T>(FILL_ZERO, c, n, row0, rows, s.cur);
       s.c_zero = e == cudaSuccess && row0 == 0 && rows == n;
@@ -215,13 +226,30 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
     case 5: s.c_zero = false; return launch_fill_row<T>(FILL_ZERO, c, n, iter, s.cur);
     case 6:
       s.planes_bt_valid = false;
+      if (s.b_pending) {
+        s.b_pending = false;
+        if (fuse && s.b_colexp_valid) {
+          const cudaError_t e = launch_fill_b_transpose_planes<T>(b, bt, n, matmul_ozaki_operand(s.oz_planes, n, 1), s.cur);
+          s.planes_bt_valid = e == cudaSuccess;
+          return e;
+        }
+        // (not reached while defer_b and this launch agree on `fuse`; kept so that b is never left unwritten)
+        if (const cudaError_t e = launch_fill2d<T>(FILL_INIT_B, b, n, 0, n, s.cur); e != cudaSuccess) return e;
+        s.b_colexp_valid = false;
+      }
       if (fuse && s.b_colexp_valid) {
         const cudaError_t e = launch_transpose_planes<T>(bt, b, n, matmul_ozaki_operand(s.oz_planes, n, 1), s.cur);
         s.planes_bt_valid = e == cudaSuccess;
         return e;
       }
       return launch_transpose<T>(bt, b, n, row0, rows, s.cur);
-    case 7: s.planes_bt_valid = false; return launch_transpose_row<T>(bt, b, n, iter, s.cur);
+    case 7:
+      s.planes_bt_valid = false;
+      if (s.b_pending) {  // (defer_b is only set for plans whose transpose nest is gene 6; kept so that b is never left unwritten)
+        s.b_pending = false;
+        if (const cudaError_t e = launch_fill2d<T>(FILL_INIT_B, b, n, 0, n, s.cur); e != cudaSuccess) return e;
+      }
+      return launch_transpose_row<T>(bt, b, n, iter, s.cur);
     case 8: {
       int variant = ctx->cfg.matmul_variant;  // 0 = auto (matmul.cu)
       if (variant == 0 && row0 == 0 && rows == n && s.oz_planes != nullptr) {
@@ -256,9 +284,12 @@ cudaError_t launch_gene_any(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter)
 
 // Start of a sequence of launches (a plan run, a capture, a single-kernel API call): no planes are valid yet, and the producers
 // of a and bt write them iff the matmul nest will consume them as ONE launch (MMX_FUSE_PLANES=0 switches the fusion off: A/B runs)
-void begin_sequence(Slot& s, bool matmul_is_one_launch) {
+void begin_sequence(Slot& s, bool matmul_is_one_launch, bool plan_allows_defer_b = false) {
   static const bool enabled = [] { const char* e = getenv("MMX_FUSE_PLANES"); return e == nullptr || atoi(e) != 0; }();
+  static const bool defer_enabled = [] { const char* e = getenv("MMX_FUSE_INIT_B"); return e == nullptr || atoi(e) != 0; }();  // 0: A/B runs
   s.fuse_planes = enabled && matmul_is_one_launch && s.oz_planes != nullptr;
+  s.defer_b = s.fuse_planes && defer_enabled && plan_allows_defer_b;
+  s.b_pending = false;
   s.planes_a_valid = s.planes_bt_valid = s.b_colexp_valid = false;
   s.c_zero = false;
 }
@@ -401,6 +432,24 @@ unsigned step_arrays(const mmx_plan_step& st) {
   }
 }
 
+// init-b may be produced inside the transpose kernel: both nests run whole on the device, init-b first, and no step between them
+// touches b (no copy of b, no host nest on it)
+bool can_defer_b(const mmx_plan_info& plan) {
+  int si = -1;
+  for (int k = 0; k < plan.num_steps; ++k) {
+    const mmx_plan_step& st = plan.steps[k];
+    const bool whole_gpu = st.kind == MMX_STEP_GPU && st.mode == MMX_MODE_GPU_NEST;
+    if (si < 0) {
+      if (whole_gpu && st.nest == MMX_NEST_INIT_B) si = k;
+      else if (step_arrays(st) >> MMX_ARRAY_B & 1u) return false;
+      continue;
+    }
+    if (st.nest == MMX_NEST_TRANSPOSE && st.kind == MMX_STEP_GPU) return whole_gpu;
+    if (step_arrays(st) >> MMX_ARRAY_B & 1u) return false;
+  }
+  return false;
+}
+
 // A plan whose every step is a whole-nest kernel (plus the checksum copy) has no host work
 // between launches: the individual is captured once as a CUDA graph (its "compile step", outside
 // the timed region) and replayed with a single launch -- this is what makes the N=256 fixture size
@@ -419,13 +468,13 @@ cudaError_t prepare_plan_graph(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan,
   // first-use work (function attributes, module load) must not happen inside a capture
   cudaError_t e = cudaSuccess;
   const bool one_launch = plan.modes[MMX_NEST_MATMUL] == MMX_MODE_GPU_NEST;
-  begin_sequence(s, one_launch);
+  begin_sequence(s, one_launch, can_defer_b(plan));
   for (int si = 0; si < plan.num_steps && e == cudaSuccess; ++si)
     if (plan.steps[si].kind == MMX_STEP_GPU) e = launch_gene_any(ctx, s, gene_of(plan.steps[si].nest, plan.steps[si].mode), IterRef{nullptr, 0});
   if (e == cudaSuccess) e = cudaStreamSynchronize(s.stream);
   if (e != cudaSuccess) return e;
   cudaGraph_t graph = nullptr;
-  begin_sequence(s, one_launch);
+  begin_sequence(s, one_launch, can_defer_b(plan));
   if ((e = cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
   const std::size_t esz = elem_size(ctx->cfg.dtype);
   // The program's data flow leaves three independent chains in front of the matmul nest: init-a, init-b -> transpose, zero-c
@@ -504,7 +553,7 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const 
   bool any_gpu = false, timed_out = false, sum_on_device = false;
   cudaError_t e = cudaSuccess;
 
-  begin_sequence(s, plan.modes[MMX_NEST_MATMUL] == MMX_MODE_GPU_NEST);
+  begin_sequence(s, plan.modes[MMX_NEST_MATMUL] == MMX_MODE_GPU_NEST, can_defer_b(plan));
   const Clock::time_point t0 = Clock::now();
   const Deadline dl{t0 + std::chrono::duration_cast<Clock::duration>(Seconds(budget)), ctx->cfg.early_timeout != 0};
   e = cudaEventRecord(s.ev_begin, s.stream);
@@ -648,6 +697,13 @@ RunResult run_plan_once(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan, const 
     if (!timed_out && dl.expired()) timed_out = true;
   }
 
+  if (s.b_pending) {  // a run cut short between init-b and the transpose that would have produced it: b is written all the same
+    s.b_pending = false;
+    const int nn = ctx->cfg.n;
+    const cudaError_t eb = ctx->cfg.dtype == MMX_F64 ? launch_fill2d<double>(FILL_INIT_B, static_cast<double*>(s.d_arr[MMX_ARRAY_B]), nn, 0, nn, s.stream)
+                                                     : launch_fill2d<float>(FILL_INIT_B, static_cast<float*>(s.d_arr[MMX_ARRAY_B]), nn, 0, nn, s.stream);
+    if (e == cudaSuccess) e = eb;
+  }
   if (e == cudaSuccess) e = cudaEventRecord(s.ev_end, s.stream);
   cudaError_t esync = cudaStreamSynchronize(s.stream);  // always drain, also after a timeout
   if (e == cudaSuccess) e = esync;

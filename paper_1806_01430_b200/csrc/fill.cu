@@ -253,6 +253,30 @@ cudaError_t launch_fill_b_colexp(T* b, int n, int* colexp, cudaStream_t stream) 
   return fill2d_go<T, FILL_INIT_B, false, W>(b, n, 0, n, stream, colexp);
 }
 
+// the column exponents of init-b WITHOUT the fill (the closed form of fill2d_kernel's first row block): for plans whose init-b nest
+// is produced inside the transpose kernel (launch_fill_b_transpose_planes)
+template <typename T, bool POW2>
+__global__ void __launch_bounds__(256) b_colexp_kernel(int n, T nn, T inv, int* __restrict__ colexp) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double top = static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(0, j, nn, inv));
+  const double bot = static_cast<double>(fill_value<T, FILL_INIT_B, POW2>(n - 1, j, nn, inv));
+  double scale;
+  bool tiny;
+  colexp[j] = oz_row_code(bot, top, false, true, &scale, &tiny);
+}
+
+template <typename T>
+cudaError_t launch_b_colexp(int n, int* colexp, cudaStream_t stream) {
+  if (!ozaki_fusable(n)) return cudaErrorInvalidValue;
+  const T nn = static_cast<T>(n), inv = static_cast<T>(1.0) / static_cast<T>(n);
+  if (is_pow2(n)) b_colexp_kernel<T, true><<<(n + 255) / 256, 256, 0, stream>>>(n, nn, inv, colexp);
+  else b_colexp_kernel<T, false><<<(n + 255) / 256, 256, 0, stream>>>(n, nn, inv, colexp);
+  return cudaGetLastError();
+}
+template cudaError_t launch_b_colexp<double>(int, int*, cudaStream_t);
+template cudaError_t launch_b_colexp<float>(int, int*, cudaStream_t);
+
 template cudaError_t launch_fill_a_planes<double>(double*, int, const OzOperand&, cudaStream_t);
 template cudaError_t launch_fill_a_planes<float>(float*, int, const OzOperand&, cudaStream_t);
 template cudaError_t launch_fill_b_colexp<double>(double*, int, int*, cudaStream_t);

@@ -75,6 +75,10 @@ template <typename T> cudaError_t launch_fill_a_planes(T* a, int n, const OzOper
 template <typename T> cudaError_t launch_fill_b_colexp(T* b, int n, int* colexp, cudaStream_t stream);
 // gene 6 over the whole array + the digit planes and guard words of bt, given pb.exps[j] for every row j of bt
 template <typename T> cudaError_t launch_transpose_planes(T* bt, const T* b, int n, const OzOperand& pb, cudaStream_t stream);
+// init-b + transpose + planes as ONE kernel (a plan that maps both nests to the device whole): the transpose computes its tiles of b,
+// writes them to b and goes on as above -- b is never read back.  launch_b_colexp: the exponents of bt's rows it needs beforehand
+template <typename T> cudaError_t launch_b_colexp(int n, int* colexp, cudaStream_t stream);
+template <typename T> cudaError_t launch_fill_b_transpose_planes(T* b, T* bt, int n, const OzOperand& pb, cudaStream_t stream);
 
 // gene 8: c[i][j] += sum_k a[i][k] * bt[j][k] (matmul.c:25-28).  variant: 1 SIMT, 2 DMMA (FP64 only).
 // Rows [row0, row0+rows) of a and c, columns [col0, col0+cols) of c (= rows of bt) only: the whole nest is

@@ -47,7 +47,11 @@ __device__ __forceinline__ float4 gather_piece(const float4* tile, int out_row, 
 // run): the all-gather of bt happens inside the kernel that produces it, as NVLink stores.
 // PLANES: the digit planes of bt for gene 8 (ozaki_digits.cuh) are written from the same registers as bt itself; P.exps[j] must
 // already hold the exponent of row j of bt (launch_fill_b_colexp).
-template <typename T, bool PUSH, bool PLANES = false>
+// GEN (with PLANES; 0 = off, 1 = N a power of two, 2 = any N): the tile of b does not come from memory -- the CTA COMPUTES it
+// (b[i][j] = (T)(i - j) / N, fixtures/matmul.c:12-14, the arithmetic of fill.cu bit for bit), stores it to b and lays it into shared
+// memory where the copies would have put it: the init-b nest and the transpose nest of a plan that maps both to the device run as ONE
+// kernel, and the 8 N^2 bytes of b are written but never read back (N = 4096: init-b 22.5 us + transpose 51 us become one launch).
+template <typename T, bool PUSH, bool PLANES = false, int GEN = 0>
 __global__ void __launch_bounds__(256, PLANES ? (sizeof(T) == 8 ? 5 : 6) : 1) transpose_tile_kernel(T* __restrict__ bt, const T* __restrict__ b, int n, int first_row,
                                                              BtPeers peers, OzOperand P = OzOperand{}) {
   using VT = typename VecOf<T>::type;
@@ -74,6 +78,27 @@ __global__ void __launch_bounds__(256, PLANES ? (sizeof(T) == 8 ? 5 : 6) : 1) tr
   // row; chunk c of row r lands at chunk c ^ ((r / V) & 7).  The copies bypass the registers and L1: how many bytes a CTA has in
   // flight is then not bounded by what L1 can track (with loads into registers the kernel lost 10 % when the shared-memory
   // carve-out left L1 28 KB instead of 60 -- profiles/r2x_transpose_l1.txt)
+  if constexpr (GEN != 0) {
+    // the tile is produced here: the values of init-b, 16 bytes per thread and step, lanes along the row of b (whole 512-byte runs
+    // per warp), to b itself (streaming: nothing on the device reads it again) and into the staged tile
+    T* b_out = const_cast<T*>(b);
+    const T nn = static_cast<T>(n), inv_n = static_cast<T>(1.0) / static_cast<T>(n);
+#pragma unroll
+    for (int k = 0; k < kSteps; ++k) {
+      const int v = tid + 256 * k;
+      const int row = v / MB, chunk = v % MB;
+      const int i = in_row0 + row, j0 = in_col0 + chunk * V;
+      T x[V];
+#pragma unroll
+      for (int w = 0; w < V; ++w) x[w] = GEN == 1 ? static_cast<T>(i - (j0 + w)) * inv_n : static_cast<T>(i - (j0 + w)) / nn;
+      VT val;
+      if constexpr (V == 2) val = make_double2(x[0], x[1]);
+      else val = make_float4(x[0], x[1], x[2], x[3]);
+      __stcs(reinterpret_cast<VT*>(b_out + static_cast<size_t>(i) * n + j0), val);
+      tile[row * MB + (chunk ^ ((row / V) & 7))] = val;
+    }
+    __syncthreads();
+  } else {
   const unsigned tile_s = static_cast<unsigned>(__cvta_generic_to_shared(tile));
 #pragma unroll
   for (int k = 0; k < kSteps; ++k) {
@@ -84,6 +109,7 @@ __global__ void __launch_bounds__(256, PLANES ? (sizeof(T) == 8 ? 5 : 6) : 1) tr
   }
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
   __syncthreads();
+  }
 
   // phase 2: lanes along the output row (coalesced 128-bit stores)
   int lossy = 0, top = 0;
@@ -250,6 +276,16 @@ cudaError_t launch_transpose_planes(T* bt, const T* b, int n, const OzOperand& p
 }
 
 template <typename T>
+cudaError_t launch_fill_b_transpose_planes(T* b, T* bt, int n, const OzOperand& pb, cudaStream_t stream) {
+  if (!ozaki_fusable(n) || pb.kq != n) return cudaErrorInvalidValue;
+  if (cudaError_t e = cudaMemsetAsync(pb.guard + pb.top_slot, 0, 2 * sizeof(int), stream); e != cudaSuccess) return e;   // words 2, 3
+  dim3 grid(n / kTile, n / kTile);
+  if ((n & (n - 1)) == 0) transpose_tile_kernel<T, false, true, 1><<<grid, 256, 0, stream>>>(bt, b, n, 0, BtPeers{}, pb);
+  else transpose_tile_kernel<T, false, true, 2><<<grid, 256, 0, stream>>>(bt, b, n, 0, BtPeers{}, pb);
+  return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_transpose_push(const BtPeers& peers, const T* b, int n, int row0, int rows, cudaStream_t stream) {
   if (rows <= 0) return cudaSuccess;
   if (peers.count < 1 || peers.count > kMaxPeers) return cudaErrorInvalidValue;
@@ -274,6 +310,8 @@ template cudaError_t launch_transpose<double>(double*, const double*, int, int, 
 template cudaError_t launch_transpose<float>(float*, const float*, int, int, int, cudaStream_t);
 template cudaError_t launch_transpose_planes<double>(double*, const double*, int, const OzOperand&, cudaStream_t);
 template cudaError_t launch_transpose_planes<float>(float*, const float*, int, const OzOperand&, cudaStream_t);
+template cudaError_t launch_fill_b_transpose_planes<double>(double*, double*, int, const OzOperand&, cudaStream_t);
+template cudaError_t launch_fill_b_transpose_planes<float>(float*, float*, int, const OzOperand&, cudaStream_t);
 template cudaError_t launch_transpose_push<double>(const BtPeers&, const double*, int, int, int, cudaStream_t);
 template cudaError_t launch_transpose_push<float>(const BtPeers&, const float*, int, int, int, cudaStream_t);
 template cudaError_t launch_transpose_row<double>(double*, const double*, int, IterRef, cudaStream_t);

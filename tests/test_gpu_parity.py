@@ -1225,6 +1225,26 @@ def test_fused_producers_at_sizes_that_are_not_a_multiple_of_the_cta_width(n, dt
             assert (np.abs(got - exact) <= bound + 1e-300).all()
 
 
+@pytest.mark.parametrize("launch_batching", [1, 0])
+@pytest.mark.parametrize("dtype", [capi.F64, capi.F32])
+@pytest.mark.parametrize("n", [1024, 4096])
+def test_init_b_produced_inside_the_transpose_leaves_every_array_the_oracles(n, dtype, launch_batching):
+    """A plan that runs init-b and the transpose whole on the device lets the transpose kernel compute its tiles of b
+    (launch_fill_b_transpose_planes) instead of reading them back: a, b, bt are the CPU program's bit for bit, c is (FP64) or is the
+    exact product rounded once (FP32), on the first run and on the graph replay; a genome whose transpose runs on the host in between
+    (b must exist in memory before it) gives the same arrays."""
+    ref = cpu.App(n, dtype, threads=8).run()
+    want_c = ref.c if dtype == capi.F64 else cpu.closed_form_c(n).astype(np.float32)
+    with capi.Context(n=n, dtype=dtype, launch_batching=launch_batching, timeout_s=120.0) as ctx:
+        for genome in ("101010101001", "101010101001", "101010001001", "101010101001"):
+            assert ctx.measure(genome).status == capi.MEASURED, genome
+            assert bits_equal(ctx.fetch(capi.ARRAY_B), ref.b), genome
+            assert bits_equal(ctx.fetch(capi.ARRAY_BT), ref.bt), genome
+            assert bits_equal(ctx.fetch(capi.ARRAY_A), ref.a), genome
+            assert bits_equal(ctx.fetch(capi.ARRAY_C), want_c), genome
+            assert ctx.gene8_form() == 223, (genome, ctx.gene8_form())
+
+
 # ---- hopeless runs are given up early (mmx_config.early_timeout) -------------------------------------------------------------------------
 def test_hopeless_runs_end_early_with_the_outcome_of_the_full_wait():
     """With a 2 s budget, a genome whose matmul nest runs on one host core at N = 2048 (~9 s) or as N^2 = 4M launches (~10 s) is a
