@@ -73,6 +73,11 @@ struct Slot {
   // defer_b: the sequence allows it (begin_sequence); b_pending: init-b has been asked for and b is not written yet
   bool defer_b = false;
   bool b_pending = false;
+  // whole-individual graphs only: nothing on the device reads b, so its 8 N^2 bytes are written by a plain fill on a side lane
+  // BESIDE the contraction (HBM is nearly idle there, and a fill CTA fits next to a contraction CTA: 32 x 256 registers, no shared
+  // memory) instead of by the transpose.  b_beside: the capture asks for it; b_unwritten: the transpose left b to that fill
+  bool b_beside = false;
+  bool b_unwritten = false;
   bool c_zero = false;             // the zero-c kernel filled c on the device and nothing has written c since (kCIsZero)
   std::map<int, Train> trains;  // by gene
   struct PlanGraph {
@@ -229,8 +234,9 @@ cudaError_t launch_gene(const mmx_ctx* ctx, Slot& s, int gene, IterRef iter, int
       if (s.b_pending) {
         s.b_pending = false;
         if (fuse && s.b_colexp_valid) {
-          const cudaError_t e = launch_fill_b_transpose_planes<T>(b, bt, n, matmul_ozaki_operand(s.oz_planes, n, 1), s.cur);
+          const cudaError_t e = launch_fill_b_transpose_planes<T>(s.b_beside ? nullptr : b, bt, n, matmul_ozaki_operand(s.oz_planes, n, 1), s.cur);
           s.planes_bt_valid = e == cudaSuccess;
+          s.b_unwritten = s.b_beside && e == cudaSuccess;
           return e;
         }
         // (not reached while defer_b and this launch agree on `fuse`; kept so that b is never left unwritten)
@@ -290,6 +296,7 @@ void begin_sequence(Slot& s, bool matmul_is_one_launch, bool plan_allows_defer_b
   s.fuse_planes = enabled && matmul_is_one_launch && s.oz_planes != nullptr;
   s.defer_b = s.fuse_planes && defer_enabled && plan_allows_defer_b;
   s.b_pending = false;
+  s.b_beside = s.b_unwritten = false;
   s.planes_a_valid = s.planes_bt_valid = s.b_colexp_valid = false;
   s.c_zero = false;
 }
@@ -476,6 +483,8 @@ cudaError_t prepare_plan_graph(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan,
   cudaGraph_t graph = nullptr;
   begin_sequence(s, one_launch, can_defer_b(plan));
   if ((e = cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
+  static const bool beside_enabled = [] { const char* v = getenv("MMX_B_BESIDE"); return v == nullptr || atoi(v) != 0; }();  // 0: A/B runs
+  bool b_lane_open = false;
   const std::size_t esz = elem_size(ctx->cfg.dtype);
   // The program's data flow leaves three independent chains in front of the matmul nest: init-a, init-b -> transpose, zero-c
   // (derive_dataflow finds the same edges in the source).  In the graph they are three branches: init-a and zero-c
@@ -506,8 +515,34 @@ cudaError_t prepare_plan_graph(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan,
     }
     if (fork && !joined && st.nest == MMX_NEST_INIT_A) s.cur = s.lane[0];
     if (fork && !joined && st.nest == MMX_NEST_ZERO_C) s.cur = s.lane[1];
+    s.b_beside = fork && beside_enabled && s.defer_b && !joined;
+    if (fork && joined && s.b_unwritten) {
+      // the transpose left b to us: a plain init-b fill on lane 0, released together with this step (the contraction) and joined
+      // at the end of the graph
+      s.b_unwritten = false;
+      e = cudaEventRecord(s.ev_fork, s.stream);
+      if (e == cudaSuccess) e = cudaStreamWaitEvent(s.lane[0], s.ev_fork, 0);
+      const int nn = ctx->cfg.n;
+      if (e == cudaSuccess)
+        e = ctx->cfg.dtype == MMX_F64 ? launch_fill2d<double>(FILL_INIT_B, static_cast<double*>(s.d_arr[MMX_ARRAY_B]), nn, 0, nn, s.lane[0])
+                                      : launch_fill2d<float>(FILL_INIT_B, static_cast<float*>(s.d_arr[MMX_ARRAY_B]), nn, 0, nn, s.lane[0]);
+      b_lane_open = true;
+      if (e != cudaSuccess) break;
+    }
     e = launch_gene_any(ctx, s, gene_of(st.nest, st.mode), IterRef{nullptr, 0});
     s.cur = s.stream;
+  }
+  s.b_beside = false;
+  if (s.b_unwritten) {  // (no step followed the join: not a plan this path sees -- b is written all the same)
+    s.b_unwritten = false;
+    const int nn = ctx->cfg.n;
+    const cudaError_t eb = ctx->cfg.dtype == MMX_F64 ? launch_fill2d<double>(FILL_INIT_B, static_cast<double*>(s.d_arr[MMX_ARRAY_B]), nn, 0, nn, s.stream)
+                                                     : launch_fill2d<float>(FILL_INIT_B, static_cast<float*>(s.d_arr[MMX_ARRAY_B]), nn, 0, nn, s.stream);
+    if (e == cudaSuccess) e = eb;
+  }
+  if (b_lane_open) {  // the fill of b rejoins the origin stream
+    cudaEventRecord(s.ev_join[0], s.lane[0]);
+    cudaStreamWaitEvent(s.stream, s.ev_join[0], 0);
   }
   if (forked && !joined) {  // (a device-only plan always has the matmul nest; kept for safety: every lane must rejoin the origin stream)
     for (int q = 0; q < 2; ++q) {
@@ -939,10 +974,14 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
     sl.device = ctx->devices[s];
     cudaError_t e;
     if ((e = cudaSetDevice(sl.device)) != cudaSuccess) return fail(e, "cudaSetDevice");
-    if ((e = cudaStreamCreateWithFlags(&sl.stream, cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "cudaStreamCreate");
+    // the slot's own stream outranks its side lanes: when a lane's kernel and the main chain's become ready together (the fill of b
+    // beside the contraction), the main chain's CTAs are placed first
+    int prio_low = 0, prio_high = 0;
+    cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+    if ((e = cudaStreamCreateWithPriority(&sl.stream, cudaStreamNonBlocking, prio_high)) != cudaSuccess) return fail(e, "cudaStreamCreate");
     sl.cur = sl.stream;
     for (int q = 0; q < 2; ++q) {
-      if ((e = cudaStreamCreateWithFlags(&sl.lane[q], cudaStreamNonBlocking)) != cudaSuccess) return fail(e, "cudaStreamCreate");
+      if ((e = cudaStreamCreateWithPriority(&sl.lane[q], cudaStreamNonBlocking, prio_low)) != cudaSuccess) return fail(e, "cudaStreamCreate");
       if ((e = cudaEventCreateWithFlags(&sl.ev_join[q], cudaEventDisableTiming)) != cudaSuccess) return fail(e, "cudaEventCreate");
     }
     if ((e = cudaEventCreateWithFlags(&sl.ev_fork, cudaEventDisableTiming)) != cudaSuccess) return fail(e, "cudaEventCreate");

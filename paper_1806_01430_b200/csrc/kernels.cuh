@@ -78,6 +78,7 @@ template <typename T> cudaError_t launch_transpose_planes(T* bt, const T* b, int
 // init-b + transpose + planes as ONE kernel (a plan that maps both nests to the device whole): the transpose computes its tiles of b,
 // writes them to b and goes on as above -- b is never read back.  launch_b_colexp: the exponents of bt's rows it needs beforehand
 template <typename T> cudaError_t launch_b_colexp(int n, int* colexp, cudaStream_t stream);
+// (b == NULL: the tiles are computed but b itself is not stored -- the caller writes it with launch_fill2d beside the contraction)
 template <typename T> cudaError_t launch_fill_b_transpose_planes(T* b, T* bt, int n, const OzOperand& pb, cudaStream_t stream);
 
 // gene 8: c[i][j] += sum_k a[i][k] * bt[j][k] (matmul.c:25-28).  variant: 1 SIMT, 2 DMMA (FP64 only).

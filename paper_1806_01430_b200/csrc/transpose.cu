@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256, PLANES ? (sizeof(T) == 8 ? 5 : 6) : 1) tr
       VT val;
       if constexpr (V == 2) val = make_double2(x[0], x[1]);
       else val = make_float4(x[0], x[1], x[2], x[3]);
-      __stcs(reinterpret_cast<VT*>(b_out + static_cast<size_t>(i) * n + j0), val);
+      if (b_out != nullptr) __stcs(reinterpret_cast<VT*>(b_out + static_cast<size_t>(i) * n + j0), val);  // NULL: b is written elsewhere
       tile[row * MB + (chunk ^ ((row / V) & 7))] = val;
     }
     __syncthreads();
