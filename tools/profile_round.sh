@@ -17,7 +17,7 @@ capture() {   # capture <name> <kernel regex> <skip> <count> <command...>
 }
 # the kernels of one FP64 individual at N = 4096 (launch_batching off: plain stream launches): the fused producers (init-a and the
 # transpose, which also write the digit planes), the HBM-bound fills, the INT8 contraction as CTA pairs, the guarded FP64-pipe launch, the trace
-capture f64 'fill_a_planes|fill2d|transpose_tile|ozaki_auto|matmul_dmma|trace' 9 9 python tools/one_individual.py f64 4096
+capture f64 'fill_a_planes|fill2d|b_colexp|transpose_tile|ozaki_auto|matmul_dmma|trace' 9 9 python tools/one_individual.py f64 4096
 python tools/ncu_summary.py --traffic $rep/${tag}_f64.ncu-rep 4096 $out/${tag}_ncu_traffic.json >> $out/${tag}_ncu_f64.log 2>&1
 # the FP64-pipe contraction itself (variant 4), the FP32 individual, the FP32 split-TF32 path (variant 30)
 capture dmma 'matmul_dmma' 2 1 python tools/one_individual.py f64 4096 4
