@@ -411,15 +411,33 @@ def run_ours(args):
     if (world > 1 and not args.no_multi) or args.ga:
         import threading
 
-        def give_up():
+        import signal
+        gave_up = threading.Lock()
+
+        def give_up(why=None):
+            if not gave_up.acquire(blocking=False):
+                return
             if rank == 0:
-                line["multi_gpu"] = {"error": f"the multi-GPU blocks did not return within {args.multi_budget:.0f} s; abandoned"}
+                line["multi_gpu"] = {"error": why or f"the multi-GPU blocks did not return within {args.multi_budget:.0f} s; abandoned"}
                 print(json.dumps(line), flush=True)
             os._exit(0)
 
         watchdog = threading.Timer(args.multi_budget, give_up)
         watchdog.daemon = True
         watchdog.start()
+        # a rank that dies hard makes the launcher SIGTERM the others: rank 0 still prints its line.  The main thread may sit inside a
+        # C call (a CUDA synchronise, a gloo collective) where Python-level handlers do not run, so the signal is taken from the wakeup
+        # pipe by a watcher thread
+        wake_r, wake_w = os.pipe()
+        os.set_blocking(wake_w, False)
+        signal.signal(signal.SIGTERM, lambda *_: None)
+        signal.set_wakeup_fd(wake_w, warn_on_full_buffer=False)
+
+        def on_sigterm():
+            os.read(wake_r, 1)
+            give_up("terminated by the launcher while the multi-GPU blocks ran (another rank died)")
+
+        threading.Thread(target=on_sigterm, daemon=True).start()
         multi = {}
         try:
             multi["ga"] = ga_block(args, n, dtype, device, rank, world, ctl, barrier)
@@ -433,6 +451,8 @@ def run_ours(args):
         else:
             multi["rowshard"] = {"skipped": "needs --gpus >= 2 (one process per GPU under torchrun)"}
         watchdog.cancel()
+        signal.set_wakeup_fd(-1)
+        signal.signal(signal.SIGTERM, signal.SIG_DFL)
         if rank == 0:
             line["multi_gpu"] = multi
         if any(isinstance(v, dict) and "error" in v for v in multi.values()):
@@ -738,6 +758,8 @@ def rowshard_block(args, dtype, device, rank, world, ctl, max_over_ranks, barrie
     out = []
     if os.environ.get("MMX_BENCH_INJECT") == f"rowshard_raise_{rank}":   # test hook: this rank fails, its peers are left waiting
         raise RuntimeError("injected failure (MMX_BENCH_INJECT)")
+    if os.environ.get("MMX_BENCH_INJECT") == f"rowshard_die_{rank}":     # test hook: this rank dies hard, the launcher ends the others
+        os._exit(3)
     for n in args.rowshard_n:
         flops = 2.0 * n ** 3
         need = 4 * n * n * esz + 15 * n * n + (1 << 30)       # arrays + digit planes + slack
