@@ -385,12 +385,12 @@ def run_ours(args):
                     "h2d_bytes_per_step": int(plan.h2d_bytes), "d2h_bytes_per_step": int(plan.d2h_bytes),
                     "note": "host clock around mmx_measure (plan + 6 launches + checksum D2H + sync); this genome has no host-side inputs"},
             "e2e_mixed": mixed, "e2e_host_buffers": host_io,
-            # the plan counts one launch per offloaded nest.  In auto mode at N % 64 == 0 (N >= 1024) a captured individual is seven
+            # the plan counts one launch per offloaded nest.  In auto mode at N % 64 == 0 (N >= 1024) a captured individual is six
             # kernels: init-a (+ digit planes), the column exponents of b (what is left of the init-b step), zero-c, the transpose
-            # (computes its tiles of b, writes bt + digit planes), the fill of b beside the contraction, the tensor-core contraction,
-            # the trace -- the fallback of auto mode sits in a conditional graph node that does not run (profiles/*_launches.csv lists
-            # the un-captured form: there the transpose also stores b and a guarded FP64-pipe launch retires at once: seven as well)
-            "gpu_launches": (int(plan.kernel_launches) + (1 if (n >= 1024 and n % 64 == 0) else
+            # (computes its tiles of b, writes b, bt + digit planes), the tensor-core contraction, the trace -- the fallback of auto
+            # mode sits in a conditional graph node that does not run (profiles/*_launches.csv lists the un-captured form, where a
+            # guarded FP64-pipe launch retires at once: seven)
+            "gpu_launches": (int(plan.kernel_launches) + (0 if (n >= 1024 and n % 64 == 0) else
                                                           3 if (dtype == capi.F64 and n >= 1024) else 0)) * args.steps,
             "clocks": clocks, "roofline": roof, "roofline_hbm": hbm_roof, "cpu_baseline": base,
             "checksum": checksum,

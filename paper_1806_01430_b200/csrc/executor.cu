@@ -73,8 +73,8 @@ struct Slot {
   // defer_b: the sequence allows it (begin_sequence); b_pending: init-b has been asked for and b is not written yet
   bool defer_b = false;
   bool b_pending = false;
-  // whole-individual graphs only: nothing on the device reads b, so its 8 N^2 bytes are written by a plain fill on a side lane
-  // BESIDE the contraction (HBM is nearly idle there, and a fill CTA fits next to a contraction CTA: 32 x 256 registers, no shared
+  // whole-individual graphs only, opt-in (MMX_B_BESIDE=1; measured slower on average, see prepare_plan_graph): nothing on the device
+  // reads b, so its 8 N^2 bytes are written by a plain fill on a side lane BESIDE the contraction (HBM is nearly idle there, and a fill CTA fits next to a contraction CTA: 32 x 256 registers, no shared
   // memory) instead of by the transpose.  b_beside: the capture asks for it; b_unwritten: the transpose left b to that fill
   bool b_beside = false;
   bool b_unwritten = false;
@@ -483,7 +483,9 @@ cudaError_t prepare_plan_graph(mmx_ctx* ctx, Slot& s, const mmx_plan_info& plan,
   cudaGraph_t graph = nullptr;
   begin_sequence(s, one_launch, can_defer_b(plan));
   if ((e = cudaStreamBeginCapture(s.stream, cudaStreamCaptureModeThreadLocal)) != cudaSuccess) return e;
-  static const bool beside_enabled = [] { const char* v = getenv("MMX_B_BESIDE"); return v == nullptr || atoi(v) != 0; }();  // 0: A/B runs
+  // opt-in (MMX_B_BESIDE=1): the best of five individuals gains 1 %, but the mean over individuals back to back LOSES 3 % (293.1 against
+  // 284.5 us at N = 4096, tools/e2e_overhead.py) -- the fill's stores share the L2 crossbar the contraction is bound by
+  static const bool beside_enabled = [] { const char* v = getenv("MMX_B_BESIDE"); return v != nullptr && atoi(v) != 0; }();
   bool b_lane_open = false;
   const std::size_t esz = elem_size(ctx->cfg.dtype);
   // The program's data flow leaves three independent chains in front of the matmul nest: init-a, init-b -> transpose, zero-c
