@@ -980,6 +980,8 @@ MMX_API int mmx_create(const mmx_config* cfg, mmx_ctx** out) {
     // beside the contraction), the main chain's CTAs are placed first
     int prio_low = 0, prio_high = 0;
     cudaDeviceGetStreamPriorityRange(&prio_low, &prio_high);
+    static const bool prio_enabled = [] { const char* v = getenv("MMX_STREAM_PRIO"); return v == nullptr || atoi(v) != 0; }();  // 0: A/B runs
+    if (!prio_enabled) prio_low = prio_high = 0;
     if ((e = cudaStreamCreateWithPriority(&sl.stream, cudaStreamNonBlocking, prio_high)) != cudaSuccess) return fail(e, "cudaStreamCreate");
     sl.cur = sl.stream;
     for (int q = 0; q < 2; ++q) {
